@@ -1,0 +1,625 @@
+/* oracle.c — plain fp64 CPU oracle: FEM generator, CSR, Jacobi-PCG, partition.
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Every function follows the
+ * definition it cites, in the paper's / SURVEY §8(c)'s order, with plain
+ * loops: no blocking, no fusion, no reordering, single thread.
+ *
+ * Paper anchors (PAPER.md = P):
+ *   P:69-75   iterative solvers from an initial guess, preconditioner M^{-1}
+ *   P:78      Laplace problem, FEM/FD Laplacian, cot weights w(i,j)
+ *   P:88      sparse system A u = b
+ *   P:132-135 Eq. (relativeError): ||Ax-b||/||b|| <= eps as the exit test
+ *   P:321-331 Eq. (MRH-TERMS): multiple right-hand sides
+ * Readings where the paper is silent are SURVEY §8(c) steps 1-11 and
+ * Q1-Q20, restated in DESIGN.md §3.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ */
+/* §8(c).2 counter-based PRNG: SplitMix64 (Steele, Lea, Flood 2014).   */
+/* ------------------------------------------------------------------ */
+uint64_t orc_splitmix64(uint64_t seed, uint64_t idx) {
+  uint64_t z = seed + (idx + 1) * 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+double orc_uniform(uint64_t seed, uint64_t idx) {
+  return (double)(orc_splitmix64(seed, idx) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+/* ------------------------------------------------------------------ */
+/* §8(c).1 meshes                                                      */
+/* ------------------------------------------------------------------ */
+static double tri_area2(const double *a, const double *b, const double *c) {
+  return (b[0] - a[0]) * (c[1] - a[1]) - (c[0] - a[0]) * (b[1] - a[1]);
+}
+
+void orc_mesh_free(orc_mesh *m) {
+  free(m->coord);
+  free(m->elem);
+  free(m->boundary);
+  memset(m, 0, sizeof(*m));
+}
+
+int orc_mesh_build(int family, int c, int jitter, uint64_t seed, orc_mesh *m) {
+  memset(m, 0, sizeof(*m));
+  if (c < 1) return ORC_ERR_INVALID_ARG;
+  double h = 1.0 / c;
+  m->family = family;
+  m->c = c;
+  if (family == ORC_P1_TRI || family == ORC_P2_TRI) {
+    int s = (family == ORC_P1_TRI) ? 1 : 2; /* lattice points per cell edge */
+    int64_t np = (int64_t)s * c + 1;        /* points per axis */
+    double hs = h / s;
+    m->dim = 2;
+    m->n_nodes = np * np;
+    m->n_elem = 2LL * c * c;
+    m->npe = (family == ORC_P1_TRI) ? 3 : 6;
+    m->coord = malloc(sizeof(double) * 2 * m->n_nodes);
+    m->elem = malloc(sizeof(int32_t) * m->npe * m->n_elem);
+    m->boundary = malloc(m->n_nodes);
+    if (!m->coord || !m->elem || !m->boundary) return ORC_ERR_OOM;
+    /* node id = a + np*b, x fastest (S:210 / §8(c).1) */
+    for (int64_t b = 0; b < np; b++)
+      for (int64_t a = 0; a < np; a++) {
+        int64_t id = a + np * b;
+        m->coord[2 * id + 0] = a * hs;
+        m->coord[2 * id + 1] = b * hs;
+        m->boundary[id] = (a == 0 || b == 0 || a == np - 1 || b == np - 1);
+      }
+    /* cells lexicographic; "/" split: T0=(v00,v10,v11), T1=(v00,v11,v01) */
+    for (int64_t j = 0; j < c; j++)
+      for (int64_t i = 0; i < c; i++) {
+        int64_t e0 = 2 * (i + (int64_t)c * j), e1 = e0 + 1;
+#define ID(a, b) ((int32_t)((a) + np * (b)))
+        int64_t a0 = s * i, b0 = s * j, a1 = a0 + s, b1 = b0 + s;
+        int32_t *t0 = m->elem + m->npe * e0, *t1 = m->elem + m->npe * e1;
+        t0[0] = ID(a0, b0); t0[1] = ID(a1, b0); t0[2] = ID(a1, b1);
+        t1[0] = ID(a0, b0); t1[1] = ID(a1, b1); t1[2] = ID(a0, b1);
+        if (family == ORC_P2_TRI) {
+          /* local DOFs 3,4,5 = midpoints of edges (0,1), (1,2), (0,2) */
+          t0[3] = ID(a0 + 1, b0);     t0[4] = ID(a1, b0 + 1);     t0[5] = ID(a0 + 1, b0 + 1);
+          t1[3] = ID(a0 + 1, b0 + 1); t1[4] = ID(a0 + 1, b1);     t1[5] = ID(a0, b0 + 1);
+        }
+#undef ID
+      }
+    if (jitter) {
+      if (family != ORC_P1_TRI) return ORC_ERR_INVALID_ARG;
+      /* §8(c).2: d = (2u-1)*(0.3h) per coordinate of every interior node,
+       * u = uniform(seed, 2*node+axis); boundary nodes fixed. */
+      for (int64_t id = 0; id < m->n_nodes; id++) {
+        if (m->boundary[id]) continue;
+        for (int ax = 0; ax < 2; ax++) {
+          double u = orc_uniform(seed, (uint64_t)(2 * id + ax));
+          double d = ((2.0 * u) - 1.0) * (0.3 * h);
+          m->coord[2 * id + ax] = m->coord[2 * id + ax] + d;
+        }
+      }
+      /* repair, one pass: every interior vertex of a triangle with signed
+       * area <= 0 is reset to its lattice point. */
+      uint8_t *mark = calloc(m->n_nodes, 1);
+      if (!mark) return ORC_ERR_OOM;
+      for (int64_t e = 0; e < m->n_elem; e++) {
+        const int32_t *t = m->elem + 3 * e;
+        double a2 = tri_area2(m->coord + 2 * t[0], m->coord + 2 * t[1], m->coord + 2 * t[2]);
+        if (a2 <= 0.0)
+          for (int k = 0; k < 3; k++)
+            if (!m->boundary[t[k]]) mark[t[k]] = 1;
+      }
+      for (int64_t id = 0; id < m->n_nodes; id++)
+        if (mark[id]) {
+          m->coord[2 * id + 0] = (id % np) * hs;
+          m->coord[2 * id + 1] = (id / np) * hs;
+          m->n_reset++;
+        }
+      free(mark);
+    }
+    return ORC_OK;
+  }
+  if (family == ORC_P1_TET) {
+    if (jitter) return ORC_ERR_INVALID_ARG;
+    int64_t np = (int64_t)c + 1;
+    m->dim = 3;
+    m->n_nodes = np * np * np;
+    m->n_elem = 6LL * c * c * c;
+    m->npe = 4;
+    m->coord = malloc(sizeof(double) * 3 * m->n_nodes);
+    m->elem = malloc(sizeof(int32_t) * 4 * m->n_elem);
+    m->boundary = malloc(m->n_nodes);
+    if (!m->coord || !m->elem || !m->boundary) return ORC_ERR_OOM;
+    for (int64_t l = 0; l < np; l++)
+      for (int64_t j = 0; j < np; j++)
+        for (int64_t i = 0; i < np; i++) {
+          int64_t id = i + np * (j + np * l);
+          m->coord[3 * id + 0] = i * h;
+          m->coord[3 * id + 1] = j * h;
+          m->coord[3 * id + 2] = l * h;
+          m->boundary[id] = (i == 0 || j == 0 || l == 0 || i == c || j == c || l == c);
+        }
+    /* Kuhn split: for each permutation π, v0 = corner, v_{m+1} = v_m + e_{π(m)} */
+    static const int perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    for (int64_t l = 0; l < c; l++)
+      for (int64_t j = 0; j < c; j++)
+        for (int64_t i = 0; i < c; i++) {
+          int64_t cell = i + (int64_t)c * (j + (int64_t)c * l);
+          for (int p = 0; p < 6; p++) {
+            int64_t v[3] = {i, j, l};
+            int32_t *t = m->elem + 4 * (6 * cell + p);
+            t[0] = (int32_t)(v[0] + np * (v[1] + np * v[2]));
+            for (int k = 0; k < 3; k++) {
+              v[perm[p][k]] += 1;
+              t[k + 1] = (int32_t)(v[0] + np * (v[1] + np * v[2]));
+            }
+          }
+        }
+    return ORC_OK;
+  }
+  return ORC_ERR_INVALID_ARG;
+}
+
+/* ------------------------------------------------------------------ */
+/* §8(c).3 element matrices                                            */
+/* ------------------------------------------------------------------ */
+/* barycentric gradients: P1 triangle.  g[a][0..1] = ∇λ_a; returns 2*signed area */
+static double tri_grads(const double *x, double g[3][2]) {
+  double d = tri_area2(x, x + 2, x + 4);
+  g[0][0] = (x[3] - x[5]) / d; g[0][1] = (x[4] - x[2]) / d;
+  g[1][0] = (x[5] - x[1]) / d; g[1][1] = (x[0] - x[4]) / d;
+  g[2][0] = (x[1] - x[3]) / d; g[2][1] = (x[2] - x[0]) / d;
+  return d;
+}
+
+static void cross3(const double *a, const double *b, double *o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+/* barycentric gradients: P1 tet; returns det J = 6 * signed volume.
+ * J = [e1 e2 e3], e_k = v_k - v_0;  rows of J^{-1} = (e2×e3, e3×e1, e1×e2)/det */
+static double tet_grads(const double *x, double g[4][3]) {
+  double e[3][3], cr[3][3];
+  for (int k = 0; k < 3; k++)
+    for (int d = 0; d < 3; d++) e[k][d] = x[3 * (k + 1) + d] - x[d];
+  cross3(e[1], e[2], cr[0]);
+  cross3(e[2], e[0], cr[1]);
+  cross3(e[0], e[1], cr[2]);
+  double det = e[0][0] * cr[0][0] + e[0][1] * cr[0][1] + e[0][2] * cr[0][2];
+  for (int k = 0; k < 3; k++)
+    for (int d = 0; d < 3; d++) g[k + 1][d] = cr[k][d] / det;
+  for (int d = 0; d < 3; d++) g[0][d] = -(g[1][d] + g[2][d] + g[3][d]);
+  return det;
+}
+
+/* 2D quadrature: edge midpoints m01, m12, m02 (λ-coordinates), weight |T|/3 */
+static const double MID_LAMBDA[3][3] = {{0.5, 0.5, 0.0}, {0.0, 0.5, 0.5}, {0.5, 0.0, 0.5}};
+static const int MID_EDGE[3][2] = {{0, 1}, {1, 2}, {0, 2}};
+
+/* P2 basis: φ_a(λ) and ∇φ_a(λ) for a = 0..5 (vertices, then midpoints 01,12,02) */
+static void p2_basis(const double lam[3], const double g[3][2], double phi[6], double gphi[6][2]) {
+  for (int a = 0; a < 3; a++) {
+    phi[a] = lam[a] * (2.0 * lam[a] - 1.0);
+    for (int d = 0; d < 2; d++) gphi[a][d] = (4.0 * lam[a] - 1.0) * g[a][d];
+  }
+  for (int e = 0; e < 3; e++) {
+    int i = MID_EDGE[e][0], j = MID_EDGE[e][1];
+    phi[3 + e] = 4.0 * lam[i] * lam[j];
+    for (int d = 0; d < 2; d++) gphi[3 + e][d] = 4.0 * (lam[i] * g[j][d] + lam[j] * g[i][d]);
+  }
+}
+
+int orc_elem_stiffness(int family, const double *x, double *Ke) {
+  if (family == ORC_P1_TRI) {
+    /* K_e = |T| G G^T  (G = barycentric gradients) */
+    double g[3][2];
+    double area = fabs(tri_grads(x, g)) / 2.0;
+    for (int a = 0; a < 3; a++)
+      for (int b = 0; b < 3; b++) Ke[3 * a + b] = area * (g[a][0] * g[b][0] + g[a][1] * g[b][1]);
+    return ORC_OK;
+  }
+  if (family == ORC_P1_TET) {
+    double g[4][3];
+    double vol = fabs(tet_grads(x, g)) / 6.0;
+    for (int a = 0; a < 4; a++)
+      for (int b = 0; b < 4; b++)
+        Ke[4 * a + b] = vol * (g[a][0] * g[b][0] + g[a][1] * g[b][1] + g[a][2] * g[b][2]);
+    return ORC_OK;
+  }
+  if (family == ORC_P2_TRI) {
+    /* ∫_T ∇φ_a·∇φ_b by the 3-point edge-midpoint rule (exact for degree 2) */
+    double g[3][2];
+    double area = fabs(tri_grads(x, g)) / 2.0;
+    for (int k = 0; k < 36; k++) Ke[k] = 0.0;
+    for (int q = 0; q < 3; q++) {
+      double phi[6], gp[6][2];
+      p2_basis(MID_LAMBDA[q], g, phi, gp);
+      for (int a = 0; a < 6; a++)
+        for (int b = 0; b < 6; b++)
+          Ke[6 * a + b] += (area / 3.0) * (gp[a][0] * gp[b][0] + gp[a][1] * gp[b][1]);
+    }
+    return ORC_OK;
+  }
+  return ORC_ERR_INVALID_ARG;
+}
+
+static double eval_f(int fkind, const double *fp, const double *p, int dim) {
+  switch (fkind) {
+    case ORC_F_ZERO: return 0.0;
+    case ORC_F_CONST: return fp[0];
+    case ORC_F_SIN2D: return 2.0 * M_PI * M_PI * sin(M_PI * p[0]) * sin(M_PI * p[1]);
+    case ORC_F_SIN3D: return 3.0 * M_PI * M_PI * sin(M_PI * p[0]) * sin(M_PI * p[1]) * sin(M_PI * p[2]);
+    case ORC_F_BUMP3D: {
+      double dx = p[0] - fp[0], dy = p[1] - fp[1], dz = p[2] - fp[2];
+      return exp(-(dx * dx + dy * dy + dz * dz) / (2.0 * fp[3] * fp[3]));
+    }
+    case ORC_F_LINEAR: {
+      double v = fp[0] + fp[1] * p[0] + fp[2] * p[1];
+      if (dim == 3) v += fp[3] * p[2];
+      return v;
+    }
+  }
+  return NAN;
+}
+
+/* §8(c).4 degree-2 load rules:  fe[a] += Σ_q w_q f(x_q) φ_a(x_q)
+ *   2D: the 3 edge midpoints, w = |T|/3 (P1: φ_a = λ_a; P2: P2 basis)
+ *   3D: 4-point rule, x_q = a v_q + b Σ_{r≠q} v_r, w = |T|/4            */
+int orc_elem_load(int family, const double *x, int fkind, const double *fp, double *fe) {
+  if (family == ORC_P1_TRI || family == ORC_P2_TRI) {
+    double g[3][2];
+    double area = fabs(tri_grads(x, g)) / 2.0;
+    for (int q = 0; q < 3; q++) {
+      int i = MID_EDGE[q][0], j = MID_EDGE[q][1];
+      double pq[2] = {0.5 * (x[2 * i] + x[2 * j]), 0.5 * (x[2 * i + 1] + x[2 * j + 1])};
+      double fq = eval_f(fkind, fp, pq, 2);
+      if (family == ORC_P1_TRI) {
+        for (int a = 0; a < 3; a++) fe[a] += (area / 3.0) * fq * MID_LAMBDA[q][a];
+      } else {
+        double phi[6], gp[6][2];
+        p2_basis(MID_LAMBDA[q], g, phi, gp);
+        for (int a = 0; a < 6; a++) fe[a] += (area / 3.0) * fq * phi[a];
+      }
+    }
+    return ORC_OK;
+  }
+  if (family == ORC_P1_TET) {
+    const double A = 0.5854101966249685, B = 0.1381966011250105;
+    double g[4][3];
+    double vol = fabs(tet_grads(x, g)) / 6.0;
+    for (int q = 0; q < 4; q++) {
+      double pq[3];
+      for (int d = 0; d < 3; d++) {
+        double s = 0.0;
+        for (int r = 0; r < 4; r++)
+          if (r != q) s += x[3 * r + d];
+        pq[d] = A * x[3 * q + d] + B * s;
+      }
+      double fq = eval_f(fkind, fp, pq, 3);
+      for (int a = 0; a < 4; a++) fe[a] += (vol / 4.0) * fq * (a == q ? A : B);
+    }
+    return ORC_OK;
+  }
+  return ORC_ERR_INVALID_ARG;
+}
+
+/* ------------------------------------------------------------------ */
+/* assembly of the Neumann stiffness K (element-graph pattern) and F   */
+/* ------------------------------------------------------------------ */
+static int cmp_i64(const void *a, const void *b) {
+  int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+  return (x > y) - (x < y);
+}
+
+void orc_csr_free(orc_csr *A) {
+  free(A->row_ptr);
+  free(A->col);
+  free(A->val);
+  memset(A, 0, sizeof(*A));
+}
+
+/* index of column j in row i (binary search; -1 if absent) */
+static int64_t csr_find(const orc_csr *A, int64_t i, int64_t j) {
+  int64_t lo = A->row_ptr[i], hi = A->row_ptr[i + 1] - 1;
+  while (lo <= hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (A->col[mid] == j) return mid;
+    if (A->col[mid] < j) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+int orc_assemble(const orc_mesh *m, int fkind, const double *fparam, orc_csr *K, double *F) {
+  int64_t nn = m->n_nodes, ne = m->n_elem;
+  int npe = m->npe, dim = m->dim;
+  memset(K, 0, sizeof(*K));
+  /* node -> incident elements */
+  int64_t *inc_ptr = calloc(nn + 1, sizeof(int64_t));
+  if (!inc_ptr) return ORC_ERR_OOM;
+  for (int64_t e = 0; e < ne; e++)
+    for (int a = 0; a < npe; a++) inc_ptr[m->elem[npe * e + a] + 1]++;
+  for (int64_t i = 0; i < nn; i++) inc_ptr[i + 1] += inc_ptr[i];
+  int64_t *inc = malloc(sizeof(int64_t) * (inc_ptr[nn] > 0 ? inc_ptr[nn] : 1));
+  int64_t *fill = calloc(nn, sizeof(int64_t));
+  if (!inc || !fill) return ORC_ERR_OOM;
+  for (int64_t e = 0; e < ne; e++)
+    for (int a = 0; a < npe; a++) {
+      int64_t v = m->elem[npe * e + a];
+      inc[inc_ptr[v] + fill[v]++] = e;
+    }
+  free(fill);
+  /* pattern: row i = sorted unique nodes of the elements incident to i */
+  int64_t maxbuf = 0;
+  for (int64_t i = 0; i < nn; i++)
+    if ((inc_ptr[i + 1] - inc_ptr[i]) * npe > maxbuf) maxbuf = (inc_ptr[i + 1] - inc_ptr[i]) * npe;
+  int64_t *buf = malloc(sizeof(int64_t) * (maxbuf > 0 ? maxbuf : 1));
+  K->n = nn;
+  K->row_ptr = calloc(nn + 1, sizeof(int64_t));
+  if (!buf || !K->row_ptr) return ORC_ERR_OOM;
+  for (int pass = 0; pass < 2; pass++) {
+    for (int64_t i = 0; i < nn; i++) {
+      int64_t nb = 0;
+      for (int64_t t = inc_ptr[i]; t < inc_ptr[i + 1]; t++)
+        for (int a = 0; a < npe; a++) buf[nb++] = m->elem[npe * inc[t] + a];
+      qsort(buf, nb, sizeof(int64_t), cmp_i64);
+      int64_t u = 0;
+      for (int64_t k = 0; k < nb; k++)
+        if (k == 0 || buf[k] != buf[k - 1]) buf[u++] = buf[k];
+      if (pass == 0) K->row_ptr[i + 1] = K->row_ptr[i] + u;
+      else memcpy(K->col + K->row_ptr[i], buf, sizeof(int64_t) * u);
+    }
+    if (pass == 0) {
+      K->nnz = K->row_ptr[nn];
+      K->col = malloc(sizeof(int64_t) * (K->nnz > 0 ? K->nnz : 1));
+      K->val = calloc(K->nnz > 0 ? K->nnz : 1, sizeof(double));
+      if (!K->col || !K->val) return ORC_ERR_OOM;
+    }
+  }
+  free(buf);
+  free(inc);
+  free(inc_ptr);
+  /* values: element by element, local (a,b) order */
+  for (int64_t i = 0; i < nn; i++) F[i] = 0.0;
+  double xe[6 * 3], Ke[36], fe[6];
+  for (int64_t e = 0; e < ne; e++) {
+    const int32_t *t = m->elem + npe * e;
+    for (int a = 0; a < npe; a++)
+      for (int d = 0; d < dim; d++) xe[dim * a + d] = m->coord[dim * t[a] + d];
+    orc_elem_stiffness(m->family, xe, Ke);
+    for (int a = 0; a < npe; a++)
+      for (int b = 0; b < npe; b++) K->val[csr_find(K, t[a], t[b])] += Ke[npe * a + b];
+    for (int a = 0; a < npe; a++) fe[a] = 0.0;
+    orc_elem_load(m->family, xe, fkind, fparam, fe);
+    for (int a = 0; a < npe; a++) F[t[a]] += fe[a];
+  }
+  return ORC_OK;
+}
+
+/* load vector only (same element loop as orc_assemble) */
+int orc_assemble_load(const orc_mesh *m, int fkind, const double *fparam, double *F) {
+  int npe = m->npe, dim = m->dim;
+  double xe[6 * 3], fe[6];
+  for (int64_t i = 0; i < m->n_nodes; i++) F[i] = 0.0;
+  for (int64_t e = 0; e < m->n_elem; e++) {
+    const int32_t *t = m->elem + npe * e;
+    for (int a = 0; a < npe; a++)
+      for (int d = 0; d < dim; d++) xe[dim * a + d] = m->coord[dim * t[a] + d];
+    for (int a = 0; a < npe; a++) fe[a] = 0.0;
+    orc_elem_load(m->family, xe, fkind, fparam, fe);
+    for (int a = 0; a < npe; a++) F[t[a]] += fe[a];
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* §8(c).5-6 Dirichlet elimination + value-independent pattern policy  */
+/* ------------------------------------------------------------------ */
+static int axis_neighbour(const orc_mesh *m, int64_t u, int64_t v) {
+  int64_t np = (m->family == ORC_P2_TRI) ? 2LL * m->c + 1 : (int64_t)m->c + 1;
+  int64_t cu[3] = {0, 0, 0}, cv[3] = {0, 0, 0};
+  for (int d = 0; d < m->dim; d++) {
+    cu[d] = u % np; u /= np;
+    cv[d] = v % np; v /= np;
+  }
+  int64_t dist = 0;
+  for (int d = 0; d < 3; d++) dist += llabs(cu[d] - cv[d]);
+  return dist <= 1; /* self or one axis step */
+}
+
+int orc_dirichlet(const orc_mesh *m, const orc_csr *K, const double *F, const double *g,
+                  int policy, orc_csr *Kff, double *bF, int64_t *free_of_node) {
+  memset(Kff, 0, sizeof(*Kff));
+  int64_t nf = 0;
+  for (int64_t i = 0; i < K->n; i++) free_of_node[i] = m->boundary[i] ? -1 : nf++;
+  Kff->n = nf;
+  Kff->row_ptr = calloc(nf + 1, sizeof(int64_t));
+  if (!Kff->row_ptr) return ORC_ERR_OOM;
+  for (int pass = 0; pass < 2; pass++) {
+    for (int64_t i = 0; i < K->n; i++) {
+      int64_t fi = free_of_node[i];
+      if (fi < 0) continue;
+      int64_t cnt = 0;
+      double s = 0.0;
+      for (int64_t k = K->row_ptr[i]; k < K->row_ptr[i + 1]; k++) {
+        int64_t j = K->col[k];
+        if (free_of_node[j] < 0) {
+          s += K->val[k] * g[j];
+          continue;
+        }
+        if (policy == ORC_PAT_AXIS && !axis_neighbour(m, i, j)) {
+          if (K->val[k] != 0.0) return ORC_ERR_POLICY;
+          continue;
+        }
+        if (pass == 1) {
+          Kff->col[Kff->row_ptr[fi] + cnt] = free_of_node[j];
+          Kff->val[Kff->row_ptr[fi] + cnt] = K->val[k];
+        }
+        cnt++;
+      }
+      if (pass == 0) Kff->row_ptr[fi + 1] = cnt;
+      else bF[fi] = F[i] - s;
+    }
+    if (pass == 0) {
+      for (int64_t i = 0; i < nf; i++) Kff->row_ptr[i + 1] += Kff->row_ptr[i];
+      Kff->nnz = Kff->row_ptr[nf];
+      Kff->col = malloc(sizeof(int64_t) * (Kff->nnz > 0 ? Kff->nnz : 1));
+      Kff->val = malloc(sizeof(double) * (Kff->nnz > 0 ? Kff->nnz : 1));
+      if (!Kff->col || !Kff->val) return ORC_ERR_OOM;
+    }
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* kernels of the method, written as their definitions                 */
+/* ------------------------------------------------------------------ */
+void orc_spmv(const orc_csr *A, const double *x, double *y) {
+  for (int64_t i = 0; i < A->n; i++) {
+    double s = 0.0;
+    for (int64_t k = A->row_ptr[i]; k < A->row_ptr[i + 1]; k++) s += A->val[k] * x[A->col[k]];
+    y[i] = s;
+  }
+}
+
+static double dot(int64_t n, const double *a, const double *b) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; i++) s += a[i] * b[i];
+  return s;
+}
+
+/* true relative residual ||b - A x|| / ||b||  (Eq. relativeError) */
+static double true_relres(const orc_csr *A, const double *b, const double *x, double nb, double *w) {
+  orc_spmv(A, x, w);
+  for (int64_t i = 0; i < A->n; i++) w[i] = b[i] - w[i];
+  return sqrt(dot(A->n, w, w)) / nb;
+}
+
+/* Jacobi-preconditioned CG, §8(c).8 (M = diag(A); exit test P:132-135).
+ * "Iterations" = number of products A p. */
+int orc_pcg(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter,
+            int64_t *iters, double *relres_rec, double *relres_true,
+            double *alpha_hist, double *beta_hist, int64_t hist_len) {
+  int64_t n = A->n;
+  *iters = 0;
+  *relres_rec = 0.0;
+  *relres_true = 0.0;
+  if (n < 0 || !(tol > 0.0) || max_iter < 1) return ORC_ERR_INVALID_ARG;
+  double *dinv = malloc(sizeof(double) * (n > 0 ? n : 1));
+  double *r = malloc(sizeof(double) * (n > 0 ? n : 1));
+  double *z = malloc(sizeof(double) * (n > 0 ? n : 1));
+  double *p = malloc(sizeof(double) * (n > 0 ? n : 1));
+  double *q = malloc(sizeof(double) * (n > 0 ? n : 1));
+  if (!dinv || !r || !z || !p || !q) return ORC_ERR_OOM;
+  int st = ORC_OK;
+  /* setup: dinv = 1/diag */
+  for (int64_t i = 0; i < n; i++) {
+    int64_t kd = csr_find(A, i, i);
+    double d = kd >= 0 ? A->val[kd] : 0.0;
+    if (d == 0.0) { st = ORC_ERR_ZERO_DIAGONAL; goto out; }
+    if (d < 0.0) { st = ORC_ERR_NOT_SPD; goto out; }
+    dinv[i] = 1.0 / d;
+  }
+  double nb = sqrt(dot(n, b, b));
+  if (nb == 0.0) {
+    for (int64_t i = 0; i < n; i++) x[i] = 0.0;
+    goto out;
+  }
+  int64_t k = 0;
+  int restart = 1;
+  double rho = 0.0;
+  for (;;) {
+    if (restart) {
+      /* r = b - A x; z = dinv∘r; p = z; rho = r·z */
+      orc_spmv(A, x, q);
+      for (int64_t i = 0; i < n; i++) r[i] = b[i] - q[i];
+      double rr = sqrt(dot(n, r, r));
+      *relres_rec = rr / nb;
+      if (rr <= tol * nb) break; /* -> exit check */
+      for (int64_t i = 0; i < n; i++) z[i] = dinv[i] * r[i];
+      for (int64_t i = 0; i < n; i++) p[i] = z[i];
+      rho = dot(n, r, z);
+      restart = 0;
+    }
+    if (k >= max_iter) { st = ORC_NOT_CONVERGED; break; }
+    orc_spmv(A, p, q);
+    double sigma = dot(n, p, q);
+    if (!(sigma > 0.0)) { st = ORC_ERR_NOT_SPD; break; }
+    double alpha = rho / sigma;
+    if (alpha_hist && k < hist_len) alpha_hist[k] = alpha;
+    k++;
+    for (int64_t i = 0; i < n; i++) x[i] = x[i] + alpha * p[i];
+    for (int64_t i = 0; i < n; i++) r[i] = r[i] - alpha * q[i];
+    double gamma = dot(n, r, r);
+    *relres_rec = sqrt(gamma) / nb;
+    if (sqrt(gamma) <= tol * nb) {
+      /* exit check on the true residual; residual replacement otherwise */
+      double t = true_relres(A, b, x, nb, q);
+      if (t <= tol) break;
+      restart = 1;
+      continue;
+    }
+    for (int64_t i = 0; i < n; i++) z[i] = dinv[i] * r[i];
+    double rho_new = dot(n, r, z);
+    double beta = rho_new / rho;
+    if (beta_hist && k - 1 < hist_len) beta_hist[k - 1] = beta;
+    rho = rho_new;
+    for (int64_t i = 0; i < n; i++) p[i] = z[i] + beta * p[i];
+  }
+  *iters = k;
+  *relres_true = true_relres(A, b, x, nb, q);
+  if (st == ORC_OK && !(*relres_true <= tol)) st = ORC_NOT_CONVERGED;
+out:
+  free(dinv); free(r); free(z); free(p); free(q);
+  return st;
+}
+
+/* §8(c).10: r_0 = 0, r_G = n, r_g = lower_bound(row_ptr, floor(g*nnz/G)) */
+void orc_partition(int64_t n, const int64_t *row_ptr, int G, int64_t *bounds) {
+  int64_t nnz = row_ptr[n];
+  bounds[0] = 0;
+  bounds[G] = n;
+  for (int g = 1; g < G; g++) {
+    int64_t target = ((int64_t)g * nnz) / G;
+    int64_t i = 0;
+    while (i < n && row_ptr[i] < target) i++; /* first i with row_ptr[i] >= target */
+    bounds[g] = i;
+  }
+}
+
+int64_t orc_halo(const orc_csr *A, int64_t r0, int64_t r1, int64_t *out, int64_t cap) {
+  /* mark every remote column referenced by rows [r0, r1), then list in order */
+  uint8_t *seen = calloc(A->n > 0 ? A->n : 1, 1);
+  if (!seen) return -1;
+  for (int64_t i = r0; i < r1; i++)
+    for (int64_t k = A->row_ptr[i]; k < A->row_ptr[i + 1]; k++) {
+      int64_t j = A->col[k];
+      if (j < r0 || j >= r1) seen[j] = 1;
+    }
+  int64_t cnt = 0;
+  for (int64_t j = 0; j < A->n; j++)
+    if (seen[j]) {
+      if (out && cnt < cap) out[cnt] = j;
+      cnt++;
+    }
+  free(seen);
+  return cnt;
+}
+
+/* Table 1 convention, used only as a pin: FD 7-point Laplacian on
+ * N^3 nodes, boundary rows = identity, interior rows keep all 7 couplings.
+ * Returns nnz by building row lengths node by node. */
+int64_t orc_fd_identity_rows_nnz(int64_t N) {
+  int64_t nnz = 0;
+  for (int64_t l = 0; l < N; l++)
+    for (int64_t j = 0; j < N; j++)
+      for (int64_t i = 0; i < N; i++) {
+        int bnd = (i == 0 || j == 0 || l == 0 || i == N - 1 || j == N - 1 || l == N - 1);
+        nnz += bnd ? 1 : 7;
+      }
+  return nnz;
+}

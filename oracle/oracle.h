@@ -1,0 +1,102 @@
+/* oracle.h — plain, slow, obviously-correct fp64 CPU oracle for the
+ * Jacobi-PCG hot path (arxiv 2201.05413, north_star in BASELINE.json).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or helper with the CUDA product under
+ * paper_2201_05413_b200/ and include/; neither side includes the other.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n; "S:n" = SPEC.md line n;
+ * "§8(c).k" = SURVEY.md §8(c) step k (the readings listed in DESIGN.md §3).
+ */
+#ifndef ORACLE_H
+#define ORACLE_H
+#include <stdint.h>
+
+#define ORC_OK 0
+#define ORC_NOT_CONVERGED 1
+#define ORC_ERR_INVALID_ARG 2
+#define ORC_ERR_ZERO_DIAGONAL 3
+#define ORC_ERR_NOT_SPD 4
+#define ORC_ERR_POLICY 5 /* a policy-dropped entry was not exactly 0.0 */
+#define ORC_ERR_OOM 6
+
+/* element families (§8(c).1) */
+#define ORC_P1_TRI 1  /* 2D lattice, "/" split, 3 nodes per element      */
+#define ORC_P1_TET 2  /* 3D lattice, Kuhn split, 4 nodes per element     */
+#define ORC_P2_TRI 3  /* 2D P2 on the "/" split, 6 DOFs per element      */
+
+/* load functions f of -Δu = f (§8(c).4, BASELINE.json configs) */
+#define ORC_F_ZERO 0
+#define ORC_F_CONST 1   /* f = fparam[0]                                  */
+#define ORC_F_SIN2D 2   /* f = 2π² sin πx sin πy                          */
+#define ORC_F_SIN3D 3   /* f = 3π² sin πx sin πy sin πz                   */
+#define ORC_F_BUMP3D 4  /* f = exp(-|x-c|²/(2σ²)), fparam = {cx,cy,cz,σ}  */
+#define ORC_F_LINEAR 5  /* f = p0 + p1 x + p2 y + p3 z, fparam = {p0..p3} */
+
+/* pattern policies (§8(c).6) */
+#define ORC_PAT_ELEMENT 0 /* element graph, explicit zeros stored          */
+#define ORC_PAT_AXIS 1    /* lattice axis neighbours only; dropped == 0.0  */
+
+typedef struct {
+  int dim;           /* 2 or 3 */
+  int family;        /* ORC_P1_TRI / ORC_P1_TET / ORC_P2_TRI */
+  int c;             /* cells per axis */
+  int64_t n_nodes;   /* DOF count (all, incl. boundary) */
+  int64_t n_elem;
+  int npe;           /* DOFs per element */
+  double *coord;     /* n_nodes*dim */
+  int32_t *elem;     /* n_elem*npe */
+  uint8_t *boundary; /* n_nodes: 1 if on ∂Ω */
+  int64_t n_reset;   /* jitter repair: nodes reset to the lattice */
+} orc_mesh;
+
+typedef struct {
+  int64_t n, nnz;
+  int64_t *row_ptr; /* n+1 */
+  int64_t *col;     /* nnz */
+  double *val;      /* nnz */
+} orc_csr;
+
+/* SplitMix64 output number idx of stream `seed` (§8(c).2):
+ * mix(seed + (idx+1)*0x9E3779B97F4A7C15). */
+uint64_t orc_splitmix64(uint64_t seed, uint64_t idx);
+/* top 53 bits × 2^-53, in [0,1) */
+double orc_uniform(uint64_t seed, uint64_t idx);
+
+int orc_mesh_build(int family, int c, int jitter, uint64_t seed, orc_mesh *m);
+void orc_mesh_free(orc_mesh *m);
+
+/* element matrices: coords of the element's nodes (npe*dim), Ke npe*npe */
+int orc_elem_stiffness(int family, const double *xe, double *Ke);
+/* element load: fe[a] += Σ_q w_q f(x_q) φ_a(x_q) */
+int orc_elem_load(int family, const double *xe, int fkind, const double *fparam, double *fe);
+
+/* Neumann stiffness (element-graph pattern, before BCs) and load F */
+int orc_assemble(const orc_mesh *m, int fkind, const double *fparam, orc_csr *K, double *F);
+/* load vector F only */
+int orc_assemble_load(const orc_mesh *m, int fkind, const double *fparam, double *F);
+/* Dirichlet elimination + pattern policy:  K_FF, b_F = F_F - K_FB g_B.
+ * g: n_nodes values (only boundary entries are read). */
+int orc_dirichlet(const orc_mesh *m, const orc_csr *K, const double *F, const double *g,
+                  int policy, orc_csr *Kff, double *bF /* n_free */, int64_t *free_of_node);
+void orc_csr_free(orc_csr *A);
+
+/* y = A x  (left-to-right within a row) */
+void orc_spmv(const orc_csr *A, const double *x, double *y);
+
+/* Jacobi-PCG, §8(c).8.  x in/out.  alpha_hist/beta_hist may be NULL. */
+int orc_pcg(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter,
+            int64_t *iters, double *relres_rec, double *relres_true,
+            double *alpha_hist, double *beta_hist, int64_t hist_len);
+
+/* row partition, §8(c).10: bounds[0..G] */
+void orc_partition(int64_t n, const int64_t *row_ptr, int G, int64_t *bounds);
+/* halo list of rows [r0,r1): sorted unique remote columns; returns count,
+ * writes at most cap entries to out (out may be NULL to count) */
+int64_t orc_halo(const orc_csr *A, int64_t r0, int64_t r1, int64_t *out, int64_t cap);
+
+/* Table 1 FD identity-boundary-row convention: nnz for N^3 nodes */
+int64_t orc_fd_identity_rows_nnz(int64_t N);
+
+#endif

@@ -1,0 +1,474 @@
+"""Pins of the oracle against what the paper and mathematics fix (CPU only).
+
+Each test names the fact it pins.  None re-types an oracle formula: the
+references are printed values (tests/golden/, cited), closed forms, textbook
+matrices, exact library solves (DST-I, dense Cholesky), invariants and brute
+force on tiny inputs.  P:n = /root/reference/PAPER.md line n; S:n = SPEC.md.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden_rows(name):
+    rows = []
+    with open(os.path.join(GOLD, name)) as fh:
+        for line in fh:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line.split())
+    return rows
+
+
+# ---------------------------------------------------------------- PRNG
+def test_splitmix64_reference_sequence():
+    want = [int(r[0], 16) for r in _golden_rows("splitmix64_seed0.txt")]
+    got = [O.splitmix64(0, i) for i in range(len(want))]
+    assert got == want
+
+
+def test_uniform_range_and_mean():
+    u = np.array([O.uniform(7, i) for i in range(20000)])
+    assert u.min() >= 0.0 and u.max() < 1.0
+    assert abs(u.mean() - 0.5) < 0.01
+
+
+# ---------------------------------------------------------------- structure
+def test_table1_nonzeros_paper():
+    """PAPER Table 1 nnz under the identity-boundary-row FD convention."""
+    for N, rows, nnz in _golden_rows("table1_nnz.txt"):
+        assert int(N) ** 3 == int(rows)
+        assert O.fd_identity_rows_nnz(int(N)) == int(nnz)
+
+
+def test_kuhn_p1_is_h_times_fd_stencil():
+    """Kuhn P1 stiffness on the lattice == h * 7-point FD Laplacian (P:78 'w(i,j)=1')."""
+    c = 8
+    h = 1.0 / c
+    P = O.build_problem("C5", c=c)
+    A = P["A"].to_dense() / h
+    m = c - 1
+    n = m ** 3
+    L = np.zeros((n, n))
+    for l in range(m):
+        for j in range(m):
+            for i in range(m):
+                r = i + m * (j + m * l)
+                L[r, r] = 6.0
+                for di, dj, dl in [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)]:
+                    a, b, cc = i + di, j + dj, l + dl
+                    if 0 <= a < m and 0 <= b < m and 0 <= cc < m:
+                        L[r, a + m * (b + m * cc)] = -1.0
+    assert np.max(np.abs(A - L)) < 1e-13
+
+
+def test_p1_lattice_2d_is_5point_stencil():
+    c = 8
+    A = O.build_problem("C1", c=c)["A"].to_dense()
+    m = c - 1
+    L = 4 * np.eye(m * m)
+    for j in range(m):
+        for i in range(m):
+            r = i + m * j
+            if i + 1 < m:
+                L[r, r + 1] = L[r + 1, r] = -1
+            if j + 1 < m:
+                L[r, r + m] = L[r + m, r] = -1
+    assert np.max(np.abs(A - L)) < 1e-14
+
+
+@pytest.mark.parametrize("name,c", [("C1", 16), ("C1", 64), ("C2", 16), ("C2", 33), ("C3", 8),
+                                    ("C3", 32), ("C4", 8), ("C4", 13), ("C5", 16)])
+def test_config_sizes_closed_forms(name, c):
+    """n and nnz closed forms of §8(c).7 (C1: 5m²-4m, C2: 7m²-8m+2, C3: 46c²-96c+53,
+    C4/C5: 7m³-6m²)."""
+    P = O.build_problem(name, c=c, k=1)
+    A = P["A"]
+    m = c - 1
+    want = {"C1": (m * m, 5 * m * m - 4 * m), "C2": (m * m, 7 * m * m - 8 * m + 2),
+            "C3": ((2 * c - 1) ** 2, 46 * c * c - 96 * c + 53),
+            "C4": (m ** 3, 7 * m ** 3 - 6 * m * m), "C5": (m ** 3, 7 * m ** 3 - 6 * m * m)}[name]
+    assert (A.n, A.nnz) == want
+    # CSR invariants: monotone row_ptr, strictly increasing columns, diag present
+    assert A.row_ptr[0] == 0 and np.all(np.diff(A.row_ptr) >= 1)
+    for i in range(A.n):
+        cols = A.col[A.row_ptr[i]:A.row_ptr[i + 1]]
+        assert np.all(np.diff(cols) > 0) and i in cols
+
+
+# ---------------------------------------------------------------- element matrices
+def test_p1_right_triangle_textbook():
+    """Right angle at vertex 0: K_e = [[1,-1/2,-1/2],[-1/2,1/2,0],[-1/2,0,1/2]] (h-free)."""
+    h = 0.125
+    K = O.elem_stiffness(O.P1_TRI, [0, 0, h, 0, 0, h])
+    want = np.array([[1, -.5, -.5], [-.5, .5, 0], [-.5, 0, .5]])
+    assert np.max(np.abs(K - want)) < 1e-15
+
+
+def test_p1_cot_formula_2d():
+    """K_ij = -1/2 cot(θ_k), θ_k the angle opposite edge ij (the 2D form of P:78's w)."""
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        x = rng.random((3, 2))
+        K = O.elem_stiffness(O.P1_TRI, x.ravel())
+        for i, j, k in [(0, 1, 2), (1, 2, 0), (0, 2, 1)]:
+            u, v = x[i] - x[k], x[j] - x[k]
+            cosang = u @ v / (np.linalg.norm(u) * np.linalg.norm(v))
+            ang = math.acos(np.clip(cosang, -1, 1))
+            assert abs(K[i, j] - (-0.5 / math.tan(ang))) < 1e-10 * max(1, abs(K[i, j]))
+
+
+def test_p1_cot_formula_3d_paper():
+    """w(i,j) = 1/6 Σ_k l_k cot α_k: per tet, K_ij = -(1/6) l_kl cot α_kl with l_kl the
+    length of the edge opposite ij and α_kl the dihedral angle at that edge."""
+    rng = np.random.default_rng(2)
+    for _ in range(50):
+        x = rng.random((4, 3))
+        K = O.elem_stiffness(O.P1_TET, x.ravel())
+        for i in range(4):
+            for j in range(i + 1, 4):
+                k, l = [t for t in range(4) if t not in (i, j)]
+                e = x[l] - x[k]
+                # dihedral angle at edge kl between faces (k,l,i) and (k,l,j)
+                def perp(p):
+                    d = x[p] - x[k]
+                    return d - (d @ e) / (e @ e) * e
+                a, b = perp(i), perp(j)
+                cosang = a @ b / (np.linalg.norm(a) * np.linalg.norm(b))
+                ang = math.acos(np.clip(cosang, -1, 1))
+                w = np.linalg.norm(e) / 6.0 / math.tan(ang)
+                assert abs(K[i, j] + w) < 1e-9 * max(1, abs(w))
+
+
+def test_p2_reference_triangle_textbook():
+    want = np.array(_golden_rows("p2_reference_stiffness.txt"), dtype=float) / 6.0
+    K = O.elem_stiffness(O.P2_TRI, [0, 0, 1, 0, 0, 1, .5, 0, .5, .5, 0, .5])
+    assert np.max(np.abs(K - want)) < 1e-14
+
+
+@pytest.mark.parametrize("fam", [O.P1_TRI, O.P2_TRI, O.P1_TET])
+def test_element_rowsum_symmetry(fam):
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        if fam == O.P1_TET:
+            x = rng.random((4, 3))
+        else:
+            v = rng.random((3, 2))
+            x = v if fam == O.P1_TRI else np.vstack([v, (v[0] + v[1]) / 2, (v[1] + v[2]) / 2,
+                                                     (v[0] + v[2]) / 2])
+        K = O.elem_stiffness(fam, x.ravel())
+        assert np.array_equal(K, K.T)
+        assert np.max(np.abs(K.sum(1))) < 1e-12 * np.max(np.abs(K))
+
+
+@pytest.mark.parametrize("name,c", [("C1", 16), ("C2", 32), ("C3", 16), ("C5", 8)])
+def test_neumann_stiffness_symmetric_zero_rowsum(name, c):
+    """north_star: 'the stiffness matrix is symmetric with zero row sums before BCs'."""
+    cfg = O.configs()[name]
+    mesh = O.Mesh(O.FAMILY[cfg["family"]], c, cfg["jitter"], cfg["seed"])
+    K, _ = O.assemble(mesh, O.F_ZERO)
+    S = K.to_scipy()
+    assert (S - S.T).nnz == 0 or np.max(np.abs((S - S.T).data)) == 0.0
+    rs = np.asarray(S.sum(axis=1)).ravel()
+    assert np.max(np.abs(rs)) <= 1e-15 * 8 * np.max(np.abs(S.diagonal()))
+
+
+# ---------------------------------------------------------------- load vectors
+@pytest.mark.parametrize("name,c,vol", [("C1", 16, 2), ("C5", 8, 3)])
+def test_load_constant_and_linear_exact(name, c, vol):
+    """Degree-2 rules integrate f·φ_i exactly for linear f; the lattice patch of an interior
+    node is point-symmetric, so F_i = f(x_i)·h^d (∫φ_i = h^d)."""
+    cfg = O.configs()[name]
+    mesh = O.Mesh(O.FAMILY[cfg["family"]], c)
+    h = 1.0 / c
+    coef = (0.7, 1.3, -2.1, 0.4)
+    F = O.assemble_load(mesh, O.F_LINEAR, coef)
+    X = mesh.coord
+    f = coef[0] + coef[1] * X[:, 0] + coef[2] * X[:, 1] + (coef[3] * X[:, 2] if vol == 3 else 0)
+    inner = ~mesh.boundary
+    assert np.max(np.abs(F[inner] - f[inner] * h ** vol)) < 1e-14
+    F1 = O.assemble_load(mesh, O.F_CONST, (1.0,))
+    assert np.max(np.abs(F1[inner] - h ** vol)) < 1e-16
+
+
+def test_load_p2_constant_exact():
+    """P2, f = 1: ∫φ_vertex = 0, ∫φ_midpoint = |T|/3 per triangle (exact integrals)."""
+    c = 8
+    h = 1.0 / c
+    mesh = O.Mesh(O.P2_TRI, c)
+    F = O.assemble_load(mesh, O.F_CONST, (1.0,))
+    np_ = 2 * c + 1
+    for idx in np.nonzero(~mesh.boundary)[0]:
+        a, b = idx % np_, idx // np_
+        if a % 2 == 0 and b % 2 == 0:
+            assert abs(F[idx]) < 1e-17
+        else:
+            assert abs(F[idx] - 2 * (h * h / 2) / 3) < 1e-16
+
+
+# ---------------------------------------------------------------- exact discrete solves
+def _dst_solve(b, m, dim, h):
+    from scipy.fft import dstn, idstn
+    j = np.arange(1, m + 1)
+    lam1 = 2 - 2 * np.cos(j * np.pi / (m + 1))
+    if dim == 2:
+        lam = lam1[None, :] + lam1[:, None]
+        B = b.reshape(m, m)
+    else:
+        lam = h * (lam1[None, None, :] + lam1[None, :, None] + lam1[:, None, None])
+        B = b.reshape(m, m, m)
+    return idstn(dstn(B, type=1) / lam, type=1).ravel()
+
+
+@pytest.mark.parametrize("name,c", [("C1", 64), ("C5", 32), ("C4", 16)])
+def test_pcg_matches_dst_exact_solution(name, c):
+    """Lattice K_FF is diagonalised by DST-I (closed-form spectrum); PCG to 1e-13 must
+    match the exact discrete solution."""
+    P = O.build_problem(name, c=c, k=2)
+    dim = 2 if name == "C1" else 3
+    for col in range(P["B"].shape[1]):
+        b = P["B"][:, col]
+        r = O.pcg(P["A"], b, tol=1e-13)
+        assert r.status == O.OK
+        xe = _dst_solve(b, c - 1, dim, 1.0 / c)
+        assert np.linalg.norm(r.x - xe) / np.linalg.norm(xe) < 1e-11
+
+
+@pytest.mark.parametrize("name,c", [("C1", 32), ("C5", 16)])
+def test_sin_mode_is_eigenvector(name, c):
+    """K s = λ s, s = sampled sin mode: λ = 8 sin²(πh/2) (2D), 12 h sin²(πh/2) (3D)."""
+    P = O.build_problem(name, c=c)
+    X = P["mesh"].coord[P["free_nodes"]]
+    h = 1.0 / c
+    s = np.prod(np.sin(np.pi * X), axis=1)
+    lam = (8 if name == "C1" else 12 * h) * math.sin(math.pi * h / 2) ** 2
+    y = O.spmv(P["A"], s)
+    assert np.max(np.abs(y - lam * s)) < 1e-14 * max(1, lam)
+
+
+@pytest.mark.parametrize("name,c", [("C1", 6), ("C2", 8), ("C3", 4), ("C4", 4), ("C5", 5)])
+def test_pcg_vs_dense_cholesky(name, c):
+    P = O.build_problem(name, c=c, k=1)
+    A = P["A"].to_dense()
+    b = P["B"][:, 0]
+    Lc = np.linalg.cholesky(A)
+    xe = np.linalg.solve(Lc.T, np.linalg.solve(Lc, b))
+    r = O.pcg(P["A"], b, tol=1e-14)
+    assert r.status == O.OK
+    assert np.linalg.norm(r.x - xe) / np.linalg.norm(xe) < 1e-12
+
+
+# ---------------------------------------------------------------- patch tests
+def test_p1_jittered_patch_linear_exact():
+    """P1 reproduces linear harmonic fields exactly on any (jittered) mesh."""
+    c = 32
+    mesh = O.Mesh(O.P1_TRI, c, True, 99)
+    K, F = O.assemble(mesh, O.F_ZERO)
+    X = mesh.coord
+    g = 1 + 2 * X[:, 0] - 3 * X[:, 1]
+    A, b, fmap = O.dirichlet(mesh, K, F, g, O.PAT_ELEMENT)
+    r = O.pcg(A, b, tol=1e-14)
+    u = g[fmap >= 0]
+    assert np.linalg.norm(r.x - u) / np.linalg.norm(u) < 1e-11
+
+
+@pytest.mark.parametrize("kind", ["harmonic", "poisson"])
+def test_p2_patch_quadratic_exact(kind):
+    """P2 reproduces quadratics exactly: x²-y² (f=0) and x²+y² (f=-4)."""
+    c = 8
+    mesh = O.Mesh(O.P2_TRI, c)
+    X = mesh.coord
+    if kind == "harmonic":
+        K, F = O.assemble(mesh, O.F_ZERO)
+        g = X[:, 0] ** 2 - X[:, 1] ** 2
+    else:
+        K, F = O.assemble(mesh, O.F_CONST, (-4.0,))
+        g = X[:, 0] ** 2 + X[:, 1] ** 2
+    A, b, fmap = O.dirichlet(mesh, K, F, g, O.PAT_ELEMENT)
+    r = O.pcg(A, b, tol=1e-14)
+    u = g[fmap >= 0]
+    assert np.linalg.norm(r.x - u) / np.linalg.norm(u) < 1e-12
+
+
+def test_p2_unit_square_centre_value():
+    """C3 reading: -Δu = 1, u = 0 on ∂[0,1]²: u(½,½) from the exact series
+    u = x(1-x)/2 - (4/π³) Σ_{m odd} sin(mπx) cosh(mπ(y-½)) / (m³ cosh(mπ/2)); P2 error O(h⁴)."""
+    exact = 0.125 - 4 / math.pi ** 3 * sum(
+        math.sin(m * math.pi / 2) / (m ** 3 * math.cosh(m * math.pi / 2)) for m in range(1, 200, 2))
+    assert abs(exact - 0.0736713532815138) < 1e-15
+    errs = []
+    for c in (16, 32):
+        P = O.build_problem("C3", c=c)
+        r = O.pcg(P["A"], P["B"][:, 0], tol=1e-14)
+        X = P["mesh"].coord[P["free_nodes"]]
+        i = np.nonzero((np.abs(X[:, 0] - .5) < 1e-12) & (np.abs(X[:, 1] - .5) < 1e-12))[0][0]
+        errs.append(abs(r.x[i] - exact))
+    assert errs[1] < 2e-8
+    assert 10 < errs[0] / errs[1] < 25  # ~16 for O(h^4)
+
+
+def test_c1_discretisation_error_second_order():
+    """x_err (Eq. ERROR-METRIC) vs sampled sin(πx)sin(πy) shrinks as O(h²)."""
+    errs = []
+    for c in (32, 64):
+        P = O.build_problem("C1", c=c)
+        r = O.pcg(P["A"], P["B"][:, 0], tol=1e-12)
+        X = P["mesh"].coord[P["free_nodes"]]
+        u = np.sin(np.pi * X[:, 0]) * np.sin(np.pi * X[:, 1])
+        errs.append(np.linalg.norm(u - r.x) / np.linalg.norm(u))
+    assert 1e-4 < errs[1] < 4e-4
+    assert 3.5 < errs[0] / errs[1] < 4.5
+
+
+# ---------------------------------------------------------------- PCG recurrence
+def _csr_from_dense(A):
+    n = A.shape[0]
+    rp, cols, vals = [0], [], []
+    for i in range(n):
+        nz = np.nonzero(A[i])[0]
+        cols += list(nz)
+        vals += list(A[i, nz])
+        rp.append(len(cols))
+    return O.Csr(n, rp, cols, vals)
+
+
+def test_spec_spmv_vector():
+    """[2,-1;-1,2,-1;-1,2]·[1,1,1] = [1,0,1]."""
+    A = _csr_from_dense(np.array([[2., -1, 0], [-1, 2, -1], [0, -1, 2]]))
+    assert np.array_equal(O.spmv(A, np.ones(3)), [1., 0., 1.])
+
+
+def test_identity_and_diagonal_converge_in_one_iteration():
+    """Jacobi-PCG on a diagonal (or identity) matrix needs one iteration."""
+    rng = np.random.default_rng(4)
+    for D in (np.eye(7), np.diag(rng.random(7) + 0.5)):
+        r = O.pcg(_csr_from_dense(D), rng.random(7), tol=1e-12)
+        assert r.status == O.OK and r.iterations == 1
+        assert np.allclose(D @ r.x, D @ np.linalg.solve(D, D @ r.x))
+
+
+def test_1d_laplacian_vs_dense():
+    """1D n=10 Dirichlet Laplacian, PCG vs dense solve within 1e-9."""
+    n = 10
+    A = 2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
+    b = np.arange(1, n + 1, dtype=float)
+    r = O.pcg(_csr_from_dense(A), b, tol=1e-12)
+    assert np.linalg.norm(r.x - np.linalg.solve(A, b)) / np.linalg.norm(np.linalg.solve(A, b)) < 1e-9
+
+
+def test_finite_termination_three_distinct_eigenvalues():
+    """CG terminates in m iterations when the preconditioned operator has m distinct
+    eigenvalues.  S = Q Λ Qᵀ with Q a normalised Hadamard matrix has constant diagonal
+    mean(Λ); A = D^{1/2} S D^{1/2} then has diag(A)⁻¹A ~ S/mean(Λ): 3 distinct eigenvalues."""
+    from scipy.linalg import hadamard
+    rng = np.random.default_rng(5)
+    n = 16
+    Q = hadamard(n) / 4.0
+    lam = np.array([1.0] * 6 + [2.0] * 5 + [5.0] * 5)
+    S = Q @ np.diag(lam) @ Q.T
+    d = rng.random(n) + 0.5
+    A = np.sqrt(d)[:, None] * S * np.sqrt(d)[None, :]
+    A = (A + A.T) / 2
+    r = O.pcg(_csr_from_dense(A), rng.standard_normal(n), tol=1e-10)
+    assert r.status == O.OK and r.iterations == 3
+
+
+def test_lanczos_ritz_values_hit_jacobi_spectrum():
+    """α, β of PCG define the Lanczos tridiagonal of D⁻¹K; its extreme eigenvalues converge to
+    the closed-form extremes 1 ∓ cos(π/c) of the 2D lattice's D⁻¹K."""
+    c = 32
+    P = O.build_problem("C1", c=c)
+    b = np.random.default_rng(6).standard_normal(P["A"].n)  # excites every mode
+    r = O.pcg(P["A"], b, tol=1e-12, hist=1000)
+    k = r.iterations - 1
+    a, bt = r.alpha[:k], r.beta[:k]
+    T = np.zeros((k, k))
+    for j in range(k):
+        T[j, j] = 1 / a[j] + (bt[j - 1] / a[j - 1] if j else 0)
+        if j + 1 < k:
+            T[j, j + 1] = T[j + 1, j] = math.sqrt(bt[j]) / a[j]
+    ev = np.linalg.eigvalsh(T)
+    lo, hi = 1 - math.cos(math.pi / c), 1 + math.cos(math.pi / c)
+    assert abs(ev[0] - lo) < 1e-8 * hi and abs(ev[-1] - hi) < 1e-8 * hi
+
+
+def test_status_codes_and_edge_cases():
+    A = _csr_from_dense(np.array([[2., -1, 0], [-1, 2, -1], [0, -1, 2]]))
+    # b = 0 -> x = 0, 0 iterations
+    r = O.pcg(A, np.zeros(3), x0=np.ones(3))
+    assert r.status == O.OK and r.iterations == 0 and np.all(r.x == 0)
+    # exact initial guess -> 0 iterations
+    r = O.pcg(A, np.array([1., 0, 1]), x0=np.ones(3))
+    assert r.status == O.OK and r.iterations == 0
+    # zero / negative diagonal, indefinite, bad args
+    assert O.pcg(_csr_from_dense(np.array([[0., 1], [1, 2]])), np.ones(2)).status == O.ERR_ZERO_DIAGONAL
+    assert O.pcg(_csr_from_dense(np.diag([1., -1])), np.ones(2)).status == O.ERR_NOT_SPD
+    indef = np.array([[1., 3], [3, 1]])
+    assert O.pcg(_csr_from_dense(indef), np.array([1., 0])).status == O.ERR_NOT_SPD
+    assert O.pcg(A, np.ones(3), tol=0.0).status == O.ERR_INVALID_ARG
+    assert O.pcg(A, np.ones(3), max_iter=0).status == O.ERR_INVALID_ARG
+    # max_iter reached: NOT_CONVERGED, x holds the last iterate
+    P = O.build_problem("C1", c=16)
+    r = O.pcg(P["A"], P["B"][:, 0], tol=1e-12, max_iter=5)
+    assert r.status == O.NOT_CONVERGED and r.iterations == 5 and r.relres_true > 1e-12
+
+
+@pytest.mark.parametrize("name,c", [("C1", 32), ("C2", 32), ("C3", 16), ("C4", 12)])
+def test_exit_contract_true_residual(name, c):
+    """S:397 / Eq. relativeError: converged ⇔ ||b-Ax||/||b|| ≤ ε."""
+    P = O.build_problem(name, c=c, k=2)
+    for j in range(P["B"].shape[1]):
+        b = P["B"][:, j]
+        r = O.pcg(P["A"], b, tol=1e-10)
+        t = np.linalg.norm(b - P["A"].to_scipy() @ r.x) / np.linalg.norm(b)
+        assert r.status == O.OK and t <= 1e-10 and abs(t - r.relres_true) < 1e-13
+
+
+def test_multi_rhs_linearity():
+    """Eq. MRH-TERMS: independent columns; solutions are linear in B."""
+    P = O.build_problem("C4", c=10, k=3)
+    B = P["B"]
+    X, res = O.pcg_multi(P["A"], np.column_stack([B[:, 0], B[:, 1], B[:, 0] + B[:, 1]]), tol=1e-13)
+    assert all(r.status == O.OK for r in res)
+    assert np.linalg.norm(X[:, 2] - X[:, 0] - X[:, 1]) / np.linalg.norm(X[:, 2]) < 1e-11
+
+
+# ---------------------------------------------------------------- jitter + partition
+def test_jitter_repair_invariants():
+    c = 256
+    h = 1.0 / c
+    mesh = O.Mesh(O.P1_TRI, c, True, O.configs()["C2"]["seed"])
+    X = mesh.coord
+    T = mesh.elem
+    a2 = ((X[T[:, 1], 0] - X[T[:, 0], 0]) * (X[T[:, 2], 1] - X[T[:, 0], 1])
+          - (X[T[:, 2], 0] - X[T[:, 0], 0]) * (X[T[:, 1], 1] - X[T[:, 0], 1]))
+    assert a2.min() > 0
+    np_ = c + 1
+    lat = np.stack([np.arange(mesh.n_nodes) % np_, np.arange(mesh.n_nodes) // np_], 1) * h
+    d = X - lat
+    assert np.all(d[mesh.boundary] == 0)
+    assert np.max(np.abs(d)) <= 0.3 * h
+    on_lattice = np.all(d == 0, axis=1) & ~mesh.boundary
+    assert on_lattice.sum() == mesh.n_reset  # reset nodes are exactly the interior lattice ones
+    assert mesh.n_reset > 0
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+def test_partition_rule_and_halo_brute_force(G):
+    P = O.build_problem("C2", c=24)
+    A = P["A"]
+    b = O.partition(A, G)
+    assert b[0] == 0 and b[G] == A.n and np.all(np.diff(b) >= 0)
+    for g in range(1, G):
+        assert b[g] == np.searchsorted(A.row_ptr, (g * A.nnz) // G, side="left")
+    for g in range(G):
+        r0, r1 = b[g], b[g + 1]
+        cols = set(A.col[A.row_ptr[r0]:A.row_ptr[r1]].tolist())
+        want = sorted(j for j in cols if j < r0 or j >= r1)
+        assert O.halo(A, r0, r1).tolist() == want
