@@ -1,0 +1,80 @@
+/* fem_gen.h — on-device assembly of the benchmark systems K u = f (the step
+ * before the solver).
+ *
+ * Builds, row by row on the GPU, the SPD stiffness matrix K_FF and load
+ * vector(s) b_F of -Δu = f on the unit square/cube with Dirichlet data g
+ * ("Laplace equation ... Dirichlet condition u=f on the
+ * boundary"; FEM discretisation P:78), following the readings of
+ * SURVEY.md §8(c) steps 1-7 restated in DESIGN.md §3:
+ *   meshes: c cells per axis, node id lexicographic (x fastest); 2D "/" split;
+ *           3D Kuhn split (6 tets per cube sharing the main diagonal); P2 on
+ *           the half-lattice;  jitter (P1_TRI only): d = (2u-1)(0.3h),
+ *           u = SplitMix64(seed, 2*node+axis), one-pass lattice reset of the
+ *           interior vertices of non-positive-area triangles;
+ *   K_e = |T| G G^T (P1), 3-point edge-midpoint rule (P2); degree-2 load rules;
+ *   Dirichlet elimination, b_F = F_F - K_FB g_B; pattern policy AXIS (lattice
+ *   P1: axis neighbours only; dropped entries must be exactly 0) or ELEMENT
+ *   (element graph, explicit zeros stored); columns ascending.
+ * Rows are numbered by free DOF (lexicographic, boundary skipped), so a row
+ * range [row_begin, row_end) is exactly one rank's slab under csr_create_dist.
+ *
+ * All array arguments are DEVICE pointers owned by the caller.  Errors:
+ * PCG_ERR_INVALID_ARG (bad spec / range / a policy-dropped entry that is not
+ * exactly 0), PCG_ERR_CUDA.
+ */
+#ifndef FEM_GEN_B200_H
+#define FEM_GEN_B200_H
+#include <stdint.h>
+
+#include "pcg.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FEM_P1_TRI 1
+#define FEM_P1_TET 2
+#define FEM_P2_TRI 3
+
+#define FEM_F_ZERO 0
+#define FEM_F_ONE 1
+#define FEM_F_SIN2D 2  /* 2π² sin πx sin πy        (u = sin πx sin πy)       */
+#define FEM_F_SIN3D 3  /* 3π² sin πx sin πy sin πz (u = sin πx sin πy sin πz) */
+#define FEM_F_BUMP3D 4 /* column s: exp(-|x-c_s|²/(2σ²)), c_s,axis = U(seed, 3s+axis) */
+
+#define FEM_G_ZERO 0
+#define FEM_G_X2MY2 1 /* g = x² - y² on the boundary */
+
+#define FEM_PAT_ELEMENT 0
+#define FEM_PAT_AXIS 1
+
+typedef struct {
+  int32_t family; /* FEM_P1_TRI / FEM_P1_TET / FEM_P2_TRI */
+  int32_t c;      /* cells per axis, >= 2 */
+  int32_t jitter; /* 0/1, FEM_P1_TRI only */
+  int32_t fkind;  /* FEM_F_* */
+  int32_t gkind;  /* FEM_G_* */
+  int32_t policy; /* FEM_PAT_* */
+  int32_t k;      /* right-hand sides: 1, or the bump count for FEM_F_BUMP3D (<= 32) */
+  int32_t pad;
+  uint64_t seed;  /* jitter / bump-centre stream */
+  double sigma;   /* bump width */
+} fem_spec;
+
+/* n_free: rows of K_FF; nnz_total: its nonzeros (closed form); n_nodes: all DOFs */
+pcg_status fem_problem_size(const fem_spec *spec, int64_t *n_free, int64_t *nnz_total, int64_t *n_nodes);
+
+/* Two phases over rows [row_begin, row_end):
+ *   phase 1 (d_col == NULL): writes d_row_ptr (row_end-row_begin+1 entries, starting at 0)
+ *            and *nnz_out (host) — the caller then allocates col/val;
+ *   phase 2: fills d_col (GLOBAL free-DOF column ids, int64), d_val, and d_B
+ *            (k column-major columns, leading dimension ldb >= rows; may be NULL). */
+pcg_status fem_assemble(const fem_spec *spec, int64_t row_begin, int64_t row_end, int64_t *d_row_ptr,
+                        int64_t *d_col, double *d_val, double *d_B, int64_t ldb, void *stream);
+pcg_status fem_count(const fem_spec *spec, int64_t row_begin, int64_t row_end, int64_t *d_row_ptr,
+                     int64_t *nnz_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

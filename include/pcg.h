@@ -1,0 +1,150 @@
+/* pcg.h — C ABI of the B200-native Jacobi-preconditioned CG solver.
+ *
+ * What it computes (the paper's problem statement, arxiv 2201.05413):
+ *   A u = b with sparse A, solved iteratively "starting
+ *   from an initial guess" with a preconditioner M^{-1} (here
+ *   Jacobi, M = diag(A)) until the relative residual of Eq. (relativeError)
+ *   ||A x - b||_2 / ||b||_2 <= eps; several right-hand sides
+ *   B = [b_1 .. b_t] (Eq. MRH-TERMS).  The exact recurrence,
+ *   stopping rule and iteration count are SURVEY.md §8(c).8-9, restated in
+ *   the recurrence residual fires the loop exit, the true
+ *   residual decides convergence (with residual replacement if it fails).
+ *
+ * Conventions (all entry points):
+ *   - Plain C types only.  No exceptions cross the ABI.  Every call returns a
+ *     pcg_status; on error, pcg_last_error() returns a thread-local message.
+ *   - Matrices are square n x n, CSR, 0-based, int64 row_ptr[n+1] and
+ *     col_idx[nnz], fp64 values; columns strictly increasing within a row
+ *     (SPEC.md S:28-34).  Inputs are COPIED: the caller keeps ownership.
+ *   - Vectors are fp64.  Solve/SpMV pointers may be host or device memory
+ *     (detected per pointer); host arrays are staged through device buffers.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is
+ *     ordered after prior work on it; calls return when results are in place
+ *     (synchronous).
+ *   - Deterministic: same inputs and same GPU count give bitwise-identical x
+ *     and iteration counts (fixed grid, fixed-order block reductions).
+ *   - Thread-safe for distinct matrix handles.
+ */
+#ifndef PCG_B200_H
+#define PCG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PCG_OK = 0,
+  PCG_NOT_CONVERGED = 1,           /* max_iter reached; x holds the last iterate */
+  PCG_ERR_INVALID_ARG = 2,         /* null pointer, n < 0, tol <= 0, max_iter < 1, k < 1 */
+  PCG_ERR_INDEX_OUT_OF_RANGE = 3,  /* col_idx outside [0, n)                       */
+  PCG_ERR_UNSORTED_OR_DUPLICATE = 4, /* columns not strictly increasing in a row   */
+  PCG_ERR_DIMENSION_MISMATCH = 5,  /* row_ptr[0] != 0, row_ptr[n] != nnz, decreasing*/
+  PCG_ERR_ZERO_DIAGONAL = 6,       /* a_ii missing or 0: Jacobi undefined         */
+  PCG_ERR_NOT_SPD = 7,             /* a_ii < 0, or p^T A p <= 0 during CG (breakdown)     */
+  PCG_ERR_NONFINITE = 8,           /* NaN/Inf in values or right-hand side         */
+  PCG_ERR_OOM = 9,
+  PCG_ERR_CUDA = 10,
+  PCG_ERR_NCCL = 11
+} pcg_status;
+
+/* csr_create flags */
+#define PCG_PTR_HOST 0x0   /* row_ptr/col_idx/val are host pointers   */
+#define PCG_PTR_DEVICE 0x1 /* ... are device pointers                 */
+#define PCG_FMT_AUTO 0x00  /* pick the faster device format, measured */
+#define PCG_FMT_CSR 0x10   /* force CSR (sub-warp per row)            */
+#define PCG_FMT_SELL 0x20  /* force SELL-32 (slices of 32 rows)       */
+
+/* format codes reported by pcg_matrix_stats.format */
+#define PCG_FORMAT_CSR 1
+#define PCG_FORMAT_SELL 2
+
+typedef struct pcg_matrix *pcg_matrix_t;
+typedef struct pcg_comm *pcg_comm_t;
+
+typedef struct {
+  int64_t iterations;       /* number of products A p              */
+  double relres_recurrence; /* sqrt(r.r)/||b|| of the recurrence at exit             */
+  double relres_true;       /* ||b - A x|| / ||b|| at exit (Eq. relativeError)      */
+  int32_t converged;        /* 1 iff relres_true <= tol                              */
+  int32_t status;           /* pcg_status of this solve / column                     */
+  int64_t replacements;     /* residual replacements performed                       */
+  double t_solve_s;         /* device time of the solve (CUDA events), excl. staging */
+  double bytes_algorithmic; /* Σ over iterations of the §8(d) per-iteration bytes    */
+  double flops;             /* Σ k (2 nnz + 13 n)                     */
+} pcg_info;
+
+typedef struct {
+  int64_t n, nnz;            /* local rows / local nonzeros                   */
+  int32_t format;            /* PCG_FORMAT_*                                  */
+  int32_t max_row_len;
+  int64_t sell_entries;      /* padded SELL entries (0 if not built)          */
+  double t_setup_s;          /* csr_create wall time                          */
+  double device_bytes;       /* device memory held by the handle              */
+  double spmv_us_csr, spmv_us_sell; /* autotune timings (0 if not measured)   */
+  int64_t n_ghost;           /* distributed: halo size (0 on one GPU)         */
+  int64_t row_begin, row_end, n_global;
+} pcg_matrix_stats;
+
+/* ---------------------------------------------------------------- setup (§8(a) a1) */
+/* Validate the CSR, narrow indices to int32 (nnz must be < 2^31 per GPU),
+ * upload, precompute dinv = 1/a_ii, build SELL-32 and pick the format (flags).
+ * Errors: INVALID_ARG, DIMENSION_MISMATCH, INDEX_OUT_OF_RANGE,
+ * UNSORTED_OR_DUPLICATE, NONFINITE, ZERO_DIAGONAL, NOT_SPD (a_ii < 0), OOM, CUDA. */
+pcg_status csr_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int64_t *col_idx,
+                      const double *val, int flags, void *stream, pcg_matrix_t *out);
+pcg_status csr_destroy(pcg_matrix_t A);
+pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *out);
+
+/* y = A x (one SpMV, the paper's MatMult).  x, y: n doubles (host or device).
+ * On a distributed handle: local rows, x local (owned rows), halo exchanged inside. */
+pcg_status pcg_spmv(pcg_matrix_t A, const double *x, double *y, void *stream);
+
+/* ---------------------------------------------------------------- solve (§8(a) a2-a6) */
+/* Jacobi-PCG for A x = b.  x is in/out: x0 in, solution out (caller-owned).
+ * b, x: n doubles, host or device.  tol > 0 (relative, Eq. relativeError),
+ * max_iter >= 1.  Returns OK, NOT_CONVERGED (x = last iterate), NOT_SPD
+ * (breakdown p^T A p <= 0), NONFINITE (b has NaN/Inf), or an error.
+ * b = 0 gives x = 0 and 0 iterations.  info may be NULL. */
+pcg_status pcg_solve(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
+                     void *stream, pcg_info *info);
+
+/* k right-hand sides (§8(a) a7): column j runs the single-RHS recurrence
+ * independently and freezes at its own convergence.
+ * B, X column-major with leading dimensions ldb, ldx >= n; X in/out.
+ * k >= 1 (k = 0 -> INVALID_ARG); k > 32 is processed in chunks of 32.
+ * infos: k entries (may be NULL).  Returns the worst column status. */
+pcg_status pcg_solve_multi(pcg_matrix_t A, int32_t k, const double *B, int64_t ldb, double *X,
+                           int64_t ldx, double tol, int64_t max_iter, void *stream,
+                           pcg_info *infos);
+
+/* ---------------------------------------------------------------- multi-GPU (§8(a) a8, §8(e)) */
+/* Row partition rule: bounds[0] = 0, bounds[G] = n,
+ * bounds[g] = lower_bound(row_ptr, floor(g*nnz/G)).  Host pointers. */
+pcg_status pcg_partition_rows(int64_t n, const int64_t *row_ptr, int32_t G, int64_t *bounds);
+/* NCCL bootstrap: rank 0 calls pcg_comm_unique_id (128 bytes), the caller broadcasts it
+ * (e.g. torch.distributed), every rank calls pcg_comm_init. */
+pcg_status pcg_comm_unique_id(void *id128);
+pcg_status pcg_comm_init(int32_t rank, int32_t size, const void *id128, pcg_comm_t *out);
+pcg_status pcg_comm_destroy(pcg_comm_t comm);
+/* Distributed matrix: this rank owns rows [row_begin, row_end) of the global n_global x
+ * n_global matrix; row_ptr_local (row_end-row_begin+1, starting at 0), global col_idx.
+ * Collective over comm (halo lists are exchanged).  pcg_solve / pcg_spmv on the
+ * handle then take local vectors of row_end-row_begin entries. */
+pcg_status csr_create_dist(pcg_comm_t comm, int64_t n_global, int64_t row_begin, int64_t row_end,
+                           int64_t nnz_local, const int64_t *row_ptr_local,
+                           const int64_t *col_idx_global, const double *val, int flags,
+                           void *stream, pcg_matrix_t *out);
+
+/* ---------------------------------------------------------------- diagnostics */
+const char *pcg_last_error(void);
+const char *pcg_status_string(pcg_status s);
+/* number of kernels this library launched in the calling process (monotone counter,
+ * for launch accounting in benchmarks) */
+int64_t pcg_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCG_B200_H */

@@ -1,0 +1,192 @@
+"""B200-native Jacobi-preconditioned CG for FEM Laplace systems (arxiv 2201.05413 hot path).
+
+Thin Python binding over the C ABI of ``libpcg_b200.so`` (include/pcg.h,
+include/fem_gen.h): argument marshalling only.  torch supplies device memory,
+streams and the process group used to broadcast the NCCL id; every step of the
+solve runs in the library's sm_100a kernels.  There is no CPU fallback: if the
+library or a GPU is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import (PCG_FMT_AUTO, PCG_FMT_CSR, PCG_FMT_SELL, PCG_FORMAT_CSR, PCG_FORMAT_SELL,  # noqa: F401
+                   PCG_OK, PCG_NOT_CONVERGED, PcgError, check, lib)
+from .problems import FemSpec, fem_spec, fem_build  # noqa: F401
+
+__all__ = ["Matrix", "Comm", "partition_rows", "fem_spec", "fem_build", "PcgError", "kernel_launches"]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    if stream is None:
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _as_tensor(a, dtype):
+    """torch tensor (any device) or numpy array -> contiguous tensor of dtype (no copy if possible)."""
+    torch = _torch()
+    if isinstance(a, np.ndarray):
+        a = torch.from_numpy(np.ascontiguousarray(a))
+    if a.dtype != dtype:
+        a = a.to(dtype)
+    return a.contiguous()
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def kernel_launches() -> int:
+    """Kernels launched by the library in this process (host launches + graph-executed)."""
+    return int(lib().pcg_kernel_launches())
+
+
+class Matrix:
+    """Device-resident SPD matrix (CSR + SELL-32) with solver workspace."""
+
+    def __init__(self, handle, n: int, nnz: int, comm=None):
+        self._h = C.c_void_p(handle)
+        self.n, self.nnz, self.comm = n, nnz, comm
+
+    # -------------------------------------------------------------- creation
+    @classmethod
+    def from_csr(cls, row_ptr, col, val, fmt: str = "auto", stream=None) -> "Matrix":
+        torch = _torch()
+        rp, ci, va = _as_tensor(row_ptr, torch.int64), _as_tensor(col, torch.int64), _as_tensor(val, torch.float64)
+        n = rp.numel() - 1
+        nnz = ci.numel()
+        dev = rp.is_cuda
+        if dev != ci.is_cuda or dev != va.is_cuda:
+            raise ValueError("row_ptr, col and val must live on the same device")
+        flags = (_lib.PCG_PTR_DEVICE if dev else _lib.PCG_PTR_HOST) | {
+            "auto": PCG_FMT_AUTO, "csr": PCG_FMT_CSR, "sell": PCG_FMT_SELL}[fmt]
+        h = C.c_void_p()
+        check(lib().csr_create(n, nnz, _ptr(rp), _ptr(ci), _ptr(va), flags, _stream_ptr(stream), C.byref(h)),
+              "csr_create")
+        return cls(h.value, n, nnz)
+
+    @classmethod
+    def from_csr_dist(cls, comm: "Comm", n_global: int, row_begin: int, row_end: int, row_ptr_local, col_global,
+                      val, fmt: str = "auto", stream=None) -> "Matrix":
+        torch = _torch()
+        rp, ci, va = (_as_tensor(row_ptr_local, torch.int64), _as_tensor(col_global, torch.int64),
+                      _as_tensor(val, torch.float64))
+        flags = (_lib.PCG_PTR_DEVICE if rp.is_cuda else _lib.PCG_PTR_HOST) | {
+            "auto": PCG_FMT_AUTO, "csr": PCG_FMT_CSR, "sell": PCG_FMT_SELL}[fmt]
+        h = C.c_void_p()
+        check(lib().csr_create_dist(comm._h, n_global, row_begin, row_end, ci.numel(), _ptr(rp), _ptr(ci), _ptr(va),
+                                    flags, _stream_ptr(stream), C.byref(h)), "csr_create_dist")
+        return cls(h.value, row_end - row_begin, ci.numel(), comm=comm)
+
+    def close(self):
+        if self._h and self._h.value:
+            lib().csr_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stats(self) -> dict:
+        s = _lib.MatrixStats()
+        check(lib().pcg_matrix_get_stats(self._h, C.byref(s)), "pcg_matrix_get_stats")
+        return s.as_dict()
+
+    # -------------------------------------------------------------- operations
+    def spmv(self, x, y=None, stream=None):
+        torch = _torch()
+        x = _as_tensor(x, torch.float64)
+        if y is None:
+            y = torch.empty(self.n, dtype=torch.float64, device=x.device)
+        check(lib().pcg_spmv(self._h, _ptr(x), _ptr(y), _stream_ptr(stream)), "pcg_spmv")
+        return y
+
+    def solve(self, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None, raise_on=("error",)):
+        """Jacobi-PCG.  Returns (x, info).  b/x0 may be host or device tensors; x is a new
+        tensor on b's device (x0 is not modified)."""
+        torch = _torch()
+        b = _as_tensor(b, torch.float64)
+        x = torch.zeros_like(b) if x0 is None else _as_tensor(x0, torch.float64).clone()
+        if b.device.type == "cpu":
+            b, x = b.pin_memory(), x.pin_memory()
+        info = _lib.PcgInfo()
+        st = lib().pcg_solve(self._h, _ptr(b), _ptr(x), float(tol), int(max_iter), _stream_ptr(stream),
+                             C.byref(info))
+        if st not in (PCG_OK, PCG_NOT_CONVERGED) or ("not_converged" in raise_on and st == PCG_NOT_CONVERGED):
+            raise PcgError(st, "pcg_solve")
+        d = info.as_dict()
+        d["status_name"] = _lib.STATUS[st]
+        return x, d
+
+    def solve_multi(self, B, X0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None):
+        """k right-hand sides, B an (n, k) tensor (column-major storage is used at the ABI:
+        pass B as B.T.contiguous().T or let this wrapper arrange it)."""
+        torch = _torch()
+        B = _as_tensor(B, torch.float64)
+        n, k = B.shape
+        Bc = B.t().contiguous()  # (k, n) row-major == (n, k) column-major, ld = n
+        Xc = torch.zeros_like(Bc) if X0 is None else _as_tensor(X0, torch.float64).t().contiguous()
+        if Bc.device.type == "cpu":
+            Bc, Xc = Bc.pin_memory(), Xc.pin_memory()
+        infos = (_lib.PcgInfo * k)()
+        st = lib().pcg_solve_multi(self._h, k, _ptr(Bc), n, _ptr(Xc), n, float(tol), int(max_iter),
+                                   _stream_ptr(stream), infos)
+        if st not in (PCG_OK, PCG_NOT_CONVERGED):
+            raise PcgError(st, "pcg_solve_multi")
+        out = []
+        for i in range(k):
+            d = infos[i].as_dict()
+            d["status_name"] = _lib.STATUS[infos[i].status]
+            out.append(d)
+        return Xc.t(), out
+
+
+class Comm:
+    """NCCL communicator owned by the library (bootstrap via torch.distributed)."""
+
+    def __init__(self, rank: int, size: int, unique_id: bytes):
+        self._h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        check(lib().pcg_comm_init(rank, size, buf, C.byref(self._h)), "pcg_comm_init")
+        self.rank, self.size = rank, size
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().pcg_comm_unique_id(buf), "pcg_comm_unique_id")
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "Comm":
+        """Rank 0 draws the NCCL id; torch.distributed broadcasts it."""
+        import torch.distributed as dist
+        rank, size = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(rank, size, obj[0])
+
+    def close(self):
+        if self._h and self._h.value:
+            lib().pcg_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+def partition_rows(row_ptr, G: int) -> np.ndarray:
+    """SURVEY §8(c).10 rule, computed by the library (host arrays)."""
+    rp = np.ascontiguousarray(np.asarray(row_ptr, dtype=np.int64))
+    out = np.zeros(G + 1, dtype=np.int64)
+    check(lib().pcg_partition_rows(len(rp) - 1, rp.ctypes.data_as(C.c_void_p), G,
+                                   out.ctypes.data_as(C.c_void_p)), "pcg_partition_rows")
+    return out

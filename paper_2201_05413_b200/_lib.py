@@ -1,0 +1,105 @@
+"""ctypes declarations of the C ABI in include/pcg.h and include/fem_gen.h.
+
+Argument marshalling only: every step of the solve runs in libpcg_b200.so.
+Importing fails loudly when the library is missing (no CPU fallback exists).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpcg_b200.so")
+
+STATUS = ["PCG_OK", "PCG_NOT_CONVERGED", "PCG_ERR_INVALID_ARG", "PCG_ERR_INDEX_OUT_OF_RANGE",
+          "PCG_ERR_UNSORTED_OR_DUPLICATE", "PCG_ERR_DIMENSION_MISMATCH", "PCG_ERR_ZERO_DIAGONAL",
+          "PCG_ERR_NOT_SPD", "PCG_ERR_NONFINITE", "PCG_ERR_OOM", "PCG_ERR_CUDA", "PCG_ERR_NCCL"]
+(PCG_OK, PCG_NOT_CONVERGED, PCG_ERR_INVALID_ARG, PCG_ERR_INDEX_OUT_OF_RANGE,
+ PCG_ERR_UNSORTED_OR_DUPLICATE, PCG_ERR_DIMENSION_MISMATCH, PCG_ERR_ZERO_DIAGONAL, PCG_ERR_NOT_SPD,
+ PCG_ERR_NONFINITE, PCG_ERR_OOM, PCG_ERR_CUDA, PCG_ERR_NCCL) = range(12)
+PCG_PTR_HOST, PCG_PTR_DEVICE = 0x0, 0x1
+PCG_FMT_AUTO, PCG_FMT_CSR, PCG_FMT_SELL = 0x00, 0x10, 0x20
+PCG_FORMAT_CSR, PCG_FORMAT_SELL = 1, 2
+
+
+class PcgInfo(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("relres_recurrence", C.c_double),
+                ("relres_true", C.c_double), ("converged", C.c_int32), ("status", C.c_int32),
+                ("replacements", C.c_int64), ("t_solve_s", C.c_double),
+                ("bytes_algorithmic", C.c_double), ("flops", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class MatrixStats(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("format", C.c_int32),
+                ("max_row_len", C.c_int32), ("sell_entries", C.c_int64), ("t_setup_s", C.c_double),
+                ("device_bytes", C.c_double), ("spmv_us_csr", C.c_double),
+                ("spmv_us_sell", C.c_double), ("n_ghost", C.c_int64), ("row_begin", C.c_int64),
+                ("row_end", C.c_int64), ("n_global", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class FemSpec(C.Structure):
+    _fields_ = [("family", C.c_int32), ("c", C.c_int32), ("jitter", C.c_int32),
+                ("fkind", C.c_int32), ("gkind", C.c_int32), ("policy", C.c_int32),
+                ("k", C.c_int32), ("pad", C.c_int32), ("seed", C.c_uint64), ("sigma", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2201_05413_b200.build` "
+                          "(the product has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, i32, dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+    P = C.POINTER
+    sig = {
+        "csr_create": [i64, i64, vp, vp, vp, C.c_int, vp, P(vp)],
+        "csr_destroy": [vp],
+        "pcg_matrix_get_stats": [vp, P(MatrixStats)],
+        "pcg_spmv": [vp, vp, vp, vp],
+        "pcg_solve": [vp, vp, vp, dbl, i64, vp, P(PcgInfo)],
+        "pcg_solve_multi": [vp, i32, vp, i64, vp, i64, dbl, i64, vp, P(PcgInfo)],
+        "pcg_partition_rows": [i64, vp, i32, vp],
+        "pcg_comm_unique_id": [vp],
+        "pcg_comm_init": [i32, i32, vp, P(vp)],
+        "pcg_comm_destroy": [vp],
+        "csr_create_dist": [vp, i64, i64, i64, i64, vp, vp, vp, C.c_int, vp, P(vp)],
+        "fem_problem_size": [P(FemSpec), P(i64), P(i64), P(i64)],
+        "fem_count": [P(FemSpec), i64, i64, vp, P(i64), vp],
+        "fem_assemble": [P(FemSpec), i64, i64, vp, vp, vp, vp, i64, vp],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = C.c_int
+    L.pcg_last_error.restype = C.c_char_p
+    L.pcg_last_error.argtypes = []
+    L.pcg_status_string.restype = C.c_char_p
+    L.pcg_status_string.argtypes = [C.c_int]
+    L.pcg_kernel_launches.restype = C.c_int64
+    L.pcg_kernel_launches.argtypes = []
+    _lib = L
+    return L
+
+
+class PcgError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = lib().pcg_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS[status] if 0 <= status < len(STATUS) else status}: {msg}")
+
+
+def check(status: int, where: str, ok=(PCG_OK,)):
+    if status not in ok:
+        raise PcgError(status, where)
+    return status

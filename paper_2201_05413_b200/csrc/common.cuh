@@ -1,0 +1,177 @@
+// common.cuh — internals shared by the product's CUDA translation units.
+// (Product code only: nothing here is shared with oracle/.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+
+#include "pcg.h"
+
+namespace pcgb {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string &msg);
+pcg_status fail(pcg_status s, const std::string &msg);
+extern std::atomic<int64_t> g_host_launches;  // kernels launched directly from host
+inline void count_launch(int64_t k = 1) { g_host_launches += k; }
+
+#define PCG_CUDA(call)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return ::pcgb::fail(e_ == cudaErrorMemoryAllocation ? PCG_ERR_OOM : PCG_ERR_CUDA, \
+                          std::string(#call) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+#define PCG_TRY(expr)                \
+  do {                               \
+    pcg_status s_ = (expr);          \
+    if (s_ != PCG_OK) return s_;     \
+  } while (0)
+
+// ------------------------------------------------------------------ device scalars
+// One per solve context.  Written only by "last block" finishers of the fused
+// kernels (deterministic fixed-order grid reductions), read by every block at
+// kernel entry.  done codes:
+enum : int {
+  DONE_RUNNING = 0,
+  DONE_CONVERGED = 1,  // recurrence residual fired (exit check follows)
+  DONE_BREAKDOWN = 2,  // sigma = p^T A p <= 0
+  DONE_MAXIT = 3,
+  DONE_ZERO_RHS = 4,
+  DONE_NONFINITE = 5,
+};
+
+struct Scalars {
+  double rho, alpha, beta, sigma, gamma;
+  double nb, tol, relres_rec, relres_true;
+  double rho_part[2];  // (r.z, r.r) partial sums awaiting a cross-GPU allreduce
+  double res_part[3];  // (w.w, w.z, b.b) of the residual pass
+  long long k, max_iter, replacements;
+  int done, parity, stage;  // parity: p[parity] holds the latest direction p_k
+  int pad0;
+  unsigned int cnt_a, cnt_b, cnt_c, cnt_d;  // last-block arrival counters (self-resetting)
+  unsigned long long graph_launches;        // kernels executed from graphs (finishers count)
+};
+
+// multi-RHS scalars, one set per column (k <= 32)
+constexpr int KMAX = 32;
+struct MultiScalars {
+  double rho[KMAX], alpha[KMAX], beta[KMAX], sigma[KMAX], gamma[KMAX];
+  double nb[KMAX], relres_rec[KMAX], relres_true[KMAX];
+  double xpend[KMAX];        // alpha still owed to x (applied by the next K1 / tail)
+  double part[3][KMAX];      // allreduce staging (sigma | rho',gamma | ww,wz,bb)
+  long long k[KMAX];
+  int done[KMAX];            // per column, same codes as Scalars::done
+  int active[KMAX];          // 1 while the column iterates (frozen columns: 0)
+  int replace[KMAX];         // residual replacement requested by the exit check
+  int parity, n_active, kcols, pad;
+  double tol;
+  long long max_iter;
+  unsigned int cnt_a, cnt_b, cnt_c, cnt_d;
+  unsigned long long graph_launches;
+};
+
+// ------------------------------------------------------------------ matrix views
+struct CsrView {
+  int64_t n;            // rows (local)
+  int64_t n_cols;       // columns addressable (n + ghosts)
+  const int *row_ptr;   // n+1 (int32: nnz < 2^31 per GPU)
+  const int *col;       // local column ids
+  const double *val;
+};
+
+struct SellView {
+  int64_t n;
+  int64_t n_slices;        // ceil(n/32)
+  const int64_t *slice_ptr; // n_slices+1, entry offsets (multiple of 32)
+  const int *col;          // [slice][t][lane]
+  const double *val;
+};
+
+// ------------------------------------------------------------------ reductions
+constexpr int BLOCK = 256;
+constexpr int WARPS = BLOCK / 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-order block sum of NV values; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double (*sm)[WARPS]) {
+#pragma unroll
+  for (int i = 0; i < NV; i++) v[i] = warp_sum(v[i]);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NV; i++) sm[i][w] = v[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < WARPS; j++) s += sm[i][j];
+      v[i] = s;
+    }
+  }
+}
+
+// Writes this block's NV partials, then returns true in exactly one block:
+// the last to arrive, after all partials are visible.
+template <int NV>
+__device__ __forceinline__ bool publish_and_arrive(const double (&v)[NV], double *partials,
+                                                   unsigned int *counter) {
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; i++) partials[(size_t)i * gridDim.x + blockIdx.x] = v[i];
+    __threadfence();
+    unsigned int prev = atomicAdd(counter, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
+// In the last block: fixed-order sum over all blocks' partials (bypassing L1).
+template <int NV>
+__device__ __forceinline__ void reduce_partials(const double *partials, double (&out)[NV],
+                                                double (*sm)[WARPS]) {
+  double v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; i++) {
+    double s = 0.0;
+    for (unsigned int b = threadIdx.x; b < gridDim.x; b += BLOCK)
+      s += __ldcg(partials + (size_t)i * gridDim.x + b);
+    v[i] = s;
+  }
+  __syncthreads();
+  block_sum<NV>(v, sm);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int i = 0; i < NV; i++) out[i] = v[i];
+}
+
+// streaming loads for matrix data (read once per pass, keep out of L1)
+__device__ __forceinline__ double ld_stream(const double *p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_stream(const int *p) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+int num_sms(int device);
+
+}  // namespace pcgb

@@ -1,0 +1,325 @@
+// dist.cu — multi-GPU row partition, halo plan and NCCL exchange.
+//
+// One process per GPU.  Rank g owns the contiguous rows [r_g, r_{g+1}) given by
+// the nnz-balanced rule of SURVEY §8(c).10.  Per PCG iteration the only data
+// exchange is the halo of z (the ghost copies of p advance locally by the same
+// recurrence, see solver.cu) plus two scalar allreduces (sigma; rho', gamma) —
+// the analogue of the paper's MatMult halo scatter and VecDot reductions
+// (P:194).
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <vector>
+
+#include "matrix.cuh"
+
+#define PCG_NCCL(call)                                                                         \
+  do {                                                                                         \
+    ncclResult_t r_ = (call);                                                                  \
+    if (r_ != ncclSuccess)                                                                     \
+      return ::pcgb::fail(PCG_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+namespace pcgb {
+
+pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_rp, const int64_t *d_col_check,
+                        const int64_t *d_col_store, const double *d_val, int64_t n_cols_check,
+                        int64_t diag_offset, int flags, cudaStream_t st);
+
+__global__ void mark_remote_kernel(int64_t nnz, const int64_t *__restrict__ col, int64_t r0, int64_t r1,
+                                   int64_t n_global, uint8_t *__restrict__ flag) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = col[k];
+    if (j < 0 || j >= n_global) continue;  // reported by validation
+    if (j < r0 || j >= r1) flag[j] = 1;
+  }
+}
+
+// global column -> local id: owned j -> j - r0 ; ghost j -> n + index in sorted ghost list
+__global__ void map_cols_kernel(int64_t nnz, const int64_t *__restrict__ col, int64_t r0, int64_t r1, int64_t n,
+                                const int64_t *__restrict__ ghost, int64_t n_ghost, int64_t *__restrict__ out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = col[k];
+    if (j >= r0 && j < r1) {
+      out[k] = j - r0;
+    } else {
+      int64_t lo = 0, hi = n_ghost;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (ghost[mid] < j) lo = mid + 1;
+        else hi = mid;
+      }
+      out[k] = n + lo;
+    }
+  }
+}
+
+__global__ void pack_kernel(int64_t m, const int *__restrict__ idx, const double *__restrict__ v,
+                            double *__restrict__ buf) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < m; s += (int64_t)gridDim.x * blockDim.x)
+    buf[s] = v[idx[s]];
+}
+
+__global__ void to_local_rows_kernel(int64_t m, const int64_t *__restrict__ g, int64_t r0, int *__restrict__ out) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < m; s += (int64_t)gridDim.x * blockDim.x)
+    out[s] = (int)(g[s] - r0);
+}
+
+pcg_status halo_exchange(pcg_matrix *A, double *vec, int width, cudaStream_t st) {
+  (void)width;
+  if (!A->comm || A->halo.nbr.empty()) return PCG_OK;
+  HaloPlan &hp = A->halo;
+  if (hp.n_send > 0) {
+    pack_kernel<<<(unsigned)std::min<int64_t>((hp.n_send + 255) / 256, 1184), 256, 0, st>>>(hp.n_send, hp.d_send_idx,
+                                                                                          vec, hp.d_send_buf);
+    count_launch();
+  }
+  PCG_NCCL(ncclGroupStart());
+  for (size_t t = 0; t < hp.nbr.size(); t++) {
+    if (hp.send_cnt[t] > 0)
+      PCG_NCCL(ncclSend(hp.d_send_buf + hp.send_off[t], (size_t)hp.send_cnt[t], ncclDouble, hp.nbr[t],
+                        A->comm->nccl, st));
+    if (hp.recv_cnt[t] > 0)
+      PCG_NCCL(ncclRecv(vec + A->n + hp.recv_off[t], (size_t)hp.recv_cnt[t], ncclDouble, hp.nbr[t], A->comm->nccl,
+                        st));
+  }
+  PCG_NCCL(ncclGroupEnd());
+  return PCG_OK;
+}
+
+pcg_status allreduce_sum(pcg_matrix *A, double *buf, int count, cudaStream_t st) {
+  if (!A->comm || A->comm->size == 1) return PCG_OK;
+  PCG_NCCL(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, A->comm->nccl, st));
+  return PCG_OK;
+}
+
+static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, int64_t r1, int64_t nnz,
+                                   const int64_t *row_ptr, const int64_t *col, const double *val, int flags,
+                                   cudaStream_t st, pcg_matrix *A) {
+  const int64_t n = r1 - r0;
+  const bool dev = (flags & PCG_PTR_DEVICE) != 0;
+  // stage inputs on the device
+  int64_t *drp = (int64_t *)row_ptr, *dcol = (int64_t *)col;
+  double *dval = (double *)val;
+  std::vector<void *> owned;
+  if (!dev) {
+    PCG_CUDA(cudaMalloc(&drp, sizeof(int64_t) * (n + 1)));
+    PCG_CUDA(cudaMalloc(&dcol, sizeof(int64_t) * (nnz > 0 ? nnz : 1)));
+    PCG_CUDA(cudaMalloc(&dval, sizeof(double) * (nnz > 0 ? nnz : 1)));
+    owned = {drp, dcol, dval};
+    PCG_CUDA(cudaMemcpyAsync(drp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st));
+    if (nnz) PCG_CUDA(cudaMemcpyAsync(dcol, col, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, st));
+    if (nnz) PCG_CUDA(cudaMemcpyAsync(dval, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+  }
+  int64_t ends[2];
+  PCG_CUDA(cudaMemcpyAsync(&ends[0], drp, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaMemcpyAsync(&ends[1], drp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  if (ends[0] != 0 || ends[1] != nnz)
+    return fail(PCG_ERR_DIMENSION_MISMATCH, "csr_create_dist: row_ptr_local[0] must be 0 and [n] = nnz_local");
+  // ---- ghost list: sorted unique remote columns (device mark + compaction)
+  uint8_t *flag;
+  PCG_CUDA(cudaMalloc(&flag, n_global > 0 ? n_global : 1));
+  PCG_CUDA(cudaMemsetAsync(flag, 0, n_global, st));
+  // out-of-range columns are caught by validation below; clamp marking to valid ones
+  mark_remote_kernel<<<1184, 256, 0, st>>>(nnz, dcol, r0, r1, n_global, flag);
+  count_launch();
+  int64_t *ghost, *d_cnt;
+  PCG_CUDA(cudaMalloc(&ghost, sizeof(int64_t) * (n_global > 0 ? n_global : 1)));
+  PCG_CUDA(cudaMalloc(&d_cnt, sizeof(int64_t)));
+  {
+    thrust::counting_iterator<int64_t> it(0);
+    size_t tb = 0;
+    cub::DeviceSelect::Flagged(nullptr, tb, it, flag, ghost, d_cnt, n_global, st);
+    void *tbuf;
+    PCG_CUDA(cudaMalloc(&tbuf, tb));
+    cub::DeviceSelect::Flagged(tbuf, tb, it, flag, ghost, d_cnt, n_global, st);
+    PCG_CUDA(cudaMemcpyAsync(&A->n_ghost, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    PCG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(tbuf);
+  }
+  cudaFree(flag);
+  const int64_t ng = A->n_ghost;
+  std::vector<int64_t> h_ghost(ng);
+  if (ng) PCG_CUDA(cudaMemcpy(h_ghost.data(), ghost, sizeof(int64_t) * ng, cudaMemcpyDeviceToHost));
+  // ---- validate on global columns (diag at global row), then map to local ids
+  int64_t *dloc;
+  PCG_CUDA(cudaMalloc(&dloc, sizeof(int64_t) * (nnz > 0 ? nnz : 1)));
+  {
+    // validation of structure happens in create_local against n_cols on the mapped
+    // ids; out-of-range globals must be caught first
+    map_cols_kernel<<<1184, 256, 0, st>>>(nnz, dcol, r0, r1, n, ghost, ng, dloc);
+    count_launch();
+  }
+  cudaFree(ghost);
+  cudaFree(d_cnt);
+  // ---- all ranks' bounds
+  const int G = C->size, me = C->rank;
+  int64_t *d_bounds;
+  PCG_CUDA(cudaMalloc(&d_bounds, sizeof(int64_t) * 2 * G));
+  int64_t mine[2] = {r0, r1};
+  PCG_CUDA(cudaMemcpyAsync(d_bounds + 2 * me, mine, sizeof(mine), cudaMemcpyHostToDevice, st));
+  PCG_NCCL(ncclAllGather(d_bounds + 2 * me, d_bounds, 2, ncclInt64, C->nccl, st));
+  std::vector<int64_t> hb(2 * G);
+  PCG_CUDA(cudaMemcpyAsync(hb.data(), d_bounds, sizeof(int64_t) * 2 * G, cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_bounds);
+  for (int g = 0; g < G; g++)
+    if (g > 0 && hb[2 * g] != hb[2 * g - 1])
+      return fail(PCG_ERR_INVALID_ARG, "csr_create_dist: rank row ranges are not contiguous in rank order");
+  // ---- receive lists: ghosts owned by each rank (contiguous runs of the sorted list)
+  std::vector<int64_t> need(G, 0), need_off(G, 0);
+  for (int64_t t = 0, g = 0; t < ng; t++) {
+    while (g < G && h_ghost[t] >= hb[2 * g + 1]) g++;
+    if (g >= G || h_ghost[t] < hb[2 * g])
+      return fail(PCG_ERR_INDEX_OUT_OF_RANGE, "csr_create_dist: column outside every rank's rows");
+    need[g]++;
+  }
+  for (int g = 1; g < G; g++) need_off[g] = need_off[g - 1] + need[g - 1];
+  // counts matrix M[h][g] = #rows rank h needs from rank g
+  int64_t *d_M;
+  PCG_CUDA(cudaMalloc(&d_M, sizeof(int64_t) * G * G));
+  PCG_CUDA(cudaMemcpyAsync(d_M + (size_t)G * me, need.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, st));
+  PCG_NCCL(ncclAllGather(d_M + (size_t)G * me, d_M, G, ncclInt64, C->nccl, st));
+  std::vector<int64_t> M((size_t)G * G);
+  PCG_CUDA(cudaMemcpyAsync(M.data(), d_M, sizeof(int64_t) * G * G, cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_M);
+  HaloPlan &hp = A->halo;
+  int64_t send_total = 0;
+  for (int g = 0; g < G; g++) {
+    if (g == me) continue;
+    const int64_t sc = M[(size_t)G * g + me], rc = need[g];
+    if (sc == 0 && rc == 0) continue;
+    hp.nbr.push_back(g);
+    hp.recv_off.push_back(need_off[g]);
+    hp.recv_cnt.push_back(rc);
+    hp.send_off.push_back(send_total);
+    hp.send_cnt.push_back(sc);
+    send_total += sc;
+  }
+  hp.n_send = send_total;
+  // ---- exchange index lists (global row ids) -> local send rows
+  int64_t *d_recv_idx = nullptr, *d_send_g = nullptr;
+  PCG_CUDA(cudaMalloc(&d_recv_idx, sizeof(int64_t) * (ng > 0 ? ng : 1)));
+  PCG_CUDA(cudaMalloc(&d_send_g, sizeof(int64_t) * (send_total > 0 ? send_total : 1)));
+  if (ng) PCG_CUDA(cudaMemcpyAsync(d_recv_idx, h_ghost.data(), sizeof(int64_t) * ng, cudaMemcpyHostToDevice, st));
+  PCG_NCCL(ncclGroupStart());
+  for (size_t t = 0; t < hp.nbr.size(); t++) {
+    if (hp.recv_cnt[t]) PCG_NCCL(ncclSend(d_recv_idx + hp.recv_off[t], hp.recv_cnt[t], ncclInt64, hp.nbr[t], C->nccl, st));
+    if (hp.send_cnt[t]) PCG_NCCL(ncclRecv(d_send_g + hp.send_off[t], hp.send_cnt[t], ncclInt64, hp.nbr[t], C->nccl, st));
+  }
+  PCG_NCCL(ncclGroupEnd());
+  PCG_CUDA(cudaMalloc(&hp.d_send_idx, sizeof(int) * (send_total > 0 ? send_total : 1)));
+  PCG_CUDA(cudaMalloc(&hp.d_send_buf, sizeof(double) * KMAX * (send_total > 0 ? send_total : 1)));
+  if (send_total) {
+    to_local_rows_kernel<<<(unsigned)std::min<int64_t>((send_total + 255) / 256, 1184), 256, 0, st>>>(
+        send_total, d_send_g, r0, hp.d_send_idx);
+    count_launch();
+  }
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_recv_idx);
+  cudaFree(d_send_g);
+  // ---- local matrix: n rows, n + n_ghost columns, diagonal at local i
+  A->comm = C;
+  A->row_begin = r0;
+  A->row_end = r1;
+  A->n_global = n_global;
+  pcg_status s = create_local(A, n, nnz, drp, dcol, dloc, dval, n_global, r0, flags, st);
+  cudaStreamSynchronize(st);
+  // all ranks fail together (a local validation error must not leave peers waiting)
+  {
+    int *d_s;
+    int hs = (int)s;
+    if (cudaMalloc(&d_s, sizeof(int)) == cudaSuccess) {
+      cudaMemcpyAsync(d_s, &hs, sizeof(int), cudaMemcpyHostToDevice, st);
+      ncclAllReduce(d_s, d_s, 1, ncclInt32, ncclMax, C->nccl, st);
+      int all = 0;
+      cudaMemcpyAsync(&all, d_s, sizeof(int), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      cudaFree(d_s);
+      if (s == PCG_OK && all != PCG_OK) s = fail((pcg_status)all, "csr_create_dist: another rank failed validation");
+    }
+  }
+  cudaFree(dloc);
+  for (void *p : owned) cudaFree(p);
+  return s;
+}
+
+}  // namespace pcgb
+
+using namespace pcgb;
+
+extern "C" pcg_status pcg_partition_rows(int64_t n, const int64_t *row_ptr, int32_t G, int64_t *bounds) {
+  if (n < 0 || G < 1 || !row_ptr || !bounds) return fail(PCG_ERR_INVALID_ARG, "pcg_partition_rows: bad argument");
+  const int64_t nnz = row_ptr[n];
+  bounds[0] = 0;
+  bounds[G] = n;
+  for (int g = 1; g < G; g++) {
+    const int64_t target = ((int64_t)g * nnz) / G;
+    bounds[g] = std::lower_bound(row_ptr, row_ptr + n + 1, target) - row_ptr;
+    if (bounds[g] > n) bounds[g] = n;
+  }
+  return PCG_OK;
+}
+
+extern "C" pcg_status pcg_comm_unique_id(void *id128) {
+  if (!id128) return fail(PCG_ERR_INVALID_ARG, "pcg_comm_unique_id: null");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  PCG_NCCL(ncclGetUniqueId(&id));
+  memcpy(id128, &id, sizeof(id));
+  return PCG_OK;
+}
+
+extern "C" pcg_status pcg_comm_init(int32_t rank, int32_t size, const void *id128, pcg_comm_t *out) {
+  if (!id128 || !out || size < 1 || rank < 0 || rank >= size)
+    return fail(PCG_ERR_INVALID_ARG, "pcg_comm_init: bad argument");
+  pcg_comm *c = new pcg_comm();
+  c->rank = rank;
+  c->size = size;
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&c->nccl, size, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(PCG_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  *out = c;
+  return PCG_OK;
+}
+
+extern "C" pcg_status pcg_comm_destroy(pcg_comm_t c) {
+  if (!c) return PCG_OK;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+  return PCG_OK;
+}
+
+extern "C" pcg_status csr_create_dist(pcg_comm_t comm, int64_t n_global, int64_t row_begin, int64_t row_end,
+                                      int64_t nnz_local, const int64_t *row_ptr_local,
+                                      const int64_t *col_idx_global, const double *val, int flags, void *stream,
+                                      pcg_matrix_t *out) {
+  if (!comm || !out || !row_ptr_local || (nnz_local > 0 && (!col_idx_global || !val)))
+    return fail(PCG_ERR_INVALID_ARG, "csr_create_dist: null argument");
+  *out = nullptr;
+  if (n_global < 0 || row_begin < 0 || row_end < row_begin || row_end > n_global || nnz_local < 0)
+    return fail(PCG_ERR_INVALID_ARG, "csr_create_dist: bad row range");
+  if (nnz_local >= (int64_t(1) << 31)) return fail(PCG_ERR_INVALID_ARG, "csr_create_dist: nnz per GPU must be < 2^31");
+  auto t0 = std::chrono::steady_clock::now();
+  pcg_matrix *A = new pcg_matrix();
+  cudaGetDevice(&A->device);
+  pcg_status s = create_dist_impl(comm, n_global, row_begin, row_end, nnz_local, row_ptr_local, col_idx_global, val,
+                                  flags, (cudaStream_t)stream, A);
+  if (s != PCG_OK) {
+    A->comm = nullptr;
+    csr_destroy(A);
+    return s;
+  }
+  A->t_setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = A;
+  return PCG_OK;
+}

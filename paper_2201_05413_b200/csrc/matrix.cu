@@ -1,0 +1,435 @@
+// matrix.cu — csr_create: validation, int32 narrowing,
+// dinv = 1/a_ii, SELL-32 build and measured format choice; workspace alloc.
+//
+// Validation follows the CSR invariants of SPEC.md S:28-34 (row_ptr[0] = 0,
+// row_ptr[n] = nnz, non-decreasing; columns in range and strictly increasing
+// within a row) plus finiteness and the Jacobi preconditioner's need
+// for a positive diagonal.  All checks run on the device, one
+// thread per row; the first offending row is reported.
+#include <cub/cub.cuh>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "matrix.cuh"
+
+namespace pcgb {
+
+enum : int {
+  E_DIM = 1,
+  E_INDEX = 2,
+  E_UNSORTED = 4,
+  E_NONFINITE = 8,
+  E_ZERO_DIAG = 16,
+  E_NEG_DIAG = 32,
+};
+
+struct ErrInfo {
+  int flags;
+  int max_len;
+  unsigned long long first_row[6];
+};
+
+__device__ __forceinline__ void report(ErrInfo *e, int bit, int64_t row) {
+  atomicOr(&e->flags, bit);
+  atomicMin(&e->first_row[__ffs(bit) - 1], (unsigned long long)row);
+}
+
+// col_map: optional (distributed) global -> local column translation is done by a
+// later pass; here columns are checked against [0, n_cols).
+__global__ void validate_kernel(int64_t n, int64_t nnz, int64_t n_cols, int64_t diag_offset,
+                                const int64_t *__restrict__ rp, const int64_t *__restrict__ col,
+                                const double *__restrict__ val, int *__restrict__ rp32,
+                                double *__restrict__ dinv, ErrInfo *err) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const int64_t s = rp[i];
+  if (i == n) {
+    rp32[n] = (int)s;
+    return;
+  }
+  const int64_t e = rp[i + 1];
+  rp32[i] = (int)s;
+  if (s < 0 || e < s || e > nnz) {
+    report(err, E_DIM, i);
+    dinv[i] = 0.0;
+    return;
+  }
+  atomicMax(&err->max_len, (int)(e - s));
+  double d = 0.0;
+  bool has_d = false;
+  int64_t prev = -1;
+  for (int64_t k = s; k < e; k++) {
+    const int64_t j = col[k];
+    const double a = val[k];
+    if (j < 0 || j >= n_cols) {
+      report(err, E_INDEX, i);
+      continue;
+    }
+    if (j <= prev) report(err, E_UNSORTED, i);
+    prev = j;
+    if (!isfinite(a)) report(err, E_NONFINITE, i);
+    if (j == i + diag_offset) {
+      d = a;
+      has_d = true;
+    }
+  }
+  if (!has_d || d == 0.0) {
+    report(err, E_ZERO_DIAG, i);
+    dinv[i] = 0.0;
+  } else {
+    if (d < 0.0) report(err, E_NEG_DIAG, i);
+    dinv[i] = 1.0 / d;
+  }
+}
+
+__global__ void narrow_kernel(int64_t nnz, const int64_t *__restrict__ col, const double *__restrict__ val,
+                              int *__restrict__ col32, double *__restrict__ valo, int64_t col_shift) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    col32[k] = (int)(col[k] - col_shift);
+    valo[k] = val[k];
+  }
+}
+
+// SELL-32: per slice the max row length, times 32 entries
+__global__ void slice_len_kernel(int64_t n, int64_t n_slices, const int *__restrict__ rp, int64_t *__restrict__ out) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > n_slices) return;
+  if (s == n_slices) {
+    out[s] = 0;
+    return;
+  }
+  int m = 0;
+  for (int l = 0; l < 32; l++) {
+    int64_t r = s * 32 + l;
+    if (r < n) m = max(m, rp[r + 1] - rp[r]);
+  }
+  out[s] = (int64_t)m * 32;
+}
+
+__global__ void sell_fill_kernel(int64_t n, int64_t n_slices, const int *__restrict__ rp,
+                                 const int *__restrict__ col, const double *__restrict__ val,
+                                 const int64_t *__restrict__ slice_ptr, int *__restrict__ scol,
+                                 double *__restrict__ sval) {
+  int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t s = tid >> 5;
+  int lane = tid & 31;
+  if (s >= n_slices) return;
+  int64_t row = s * 32 + lane;
+  int64_t base = slice_ptr[s];
+  int len = (int)((slice_ptr[s + 1] - base) >> 5);
+  int rs = 0, rl = 0;
+  if (row < n) {
+    rs = rp[row];
+    rl = rp[row + 1] - rs;
+  }
+  for (int t = 0; t < len; t++) {
+    int64_t e = base + (int64_t)t * 32 + lane;
+    if (t < rl) {
+      scol[e] = col[rs + t];
+      sval[e] = val[rs + t];
+    } else {  // padding: a_ii-position dummy, contributes 0 * finite
+      scol[e] = row < n ? (int)row : 0;
+      sval[e] = 0.0;
+    }
+  }
+}
+
+int num_sms(int device) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  return v > 0 ? v : 148;
+}
+
+// declared in solver.cu
+pcg_status launch_spmv_fmt(pcg_matrix *A, int fmt, const double *x, double *y, cudaStream_t st);
+int k1_blocks_per_sm(int fmt, int lanes);
+
+static pcg_status error_from_flags(const ErrInfo &e, int64_t row_offset) {
+  static const struct {
+    int bit;
+    pcg_status st;
+    const char *what;
+  } order[] = {
+      {E_DIM, PCG_ERR_DIMENSION_MISMATCH, "row_ptr not monotone / out of [0, nnz]"},
+      {E_INDEX, PCG_ERR_INDEX_OUT_OF_RANGE, "column index out of range"},
+      {E_UNSORTED, PCG_ERR_UNSORTED_OR_DUPLICATE, "columns not strictly increasing"},
+      {E_NONFINITE, PCG_ERR_NONFINITE, "non-finite value"},
+      {E_ZERO_DIAG, PCG_ERR_ZERO_DIAGONAL, "zero or missing diagonal"},
+      {E_NEG_DIAG, PCG_ERR_NOT_SPD, "negative diagonal (not SPD)"},
+  };
+  for (auto &o : order)
+    if (e.flags & o.bit)
+      return fail(o.st, std::string("csr_create: ") + o.what + " in row " +
+                            std::to_string((long long)e.first_row[__builtin_ctz(o.bit)] + row_offset));
+  return PCG_OK;
+}
+
+// Core of csr_create / csr_create_dist: columns already translated so that the
+// local matrix is n x n_cols (n_cols = n + n_ghost) with diagonal at i + 0.
+// d_col_check: columns as given by the caller (global ids on a distributed handle),
+// validated against [0, n_cols_check) with the diagonal at i + diag_offset;
+// d_col_store: the local ids the kernels gather with (same array on one GPU).
+pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_rp, const int64_t *d_col_check,
+                        const int64_t *d_col_store, const double *d_val, int64_t n_cols_check,
+                        int64_t diag_offset, int flags, cudaStream_t st) {
+  A->n = n;
+  A->nnz = nnz;
+  ErrInfo *d_err;
+  PCG_CUDA(cudaMalloc(&d_err, sizeof(ErrInfo)));
+  ErrInfo h_err;
+  memset(&h_err, 0, sizeof(h_err));
+  for (auto &r : h_err.first_row) r = ~0ull;
+  PCG_CUDA(cudaMemcpyAsync(d_err, &h_err, sizeof(ErrInfo), cudaMemcpyHostToDevice, st));
+  PCG_CUDA(cudaMalloc(&A->d_row_ptr, sizeof(int) * (n + 1)));
+  PCG_CUDA(cudaMalloc(&A->d_col, sizeof(int) * (nnz > 0 ? nnz : 1)));
+  PCG_CUDA(cudaMalloc(&A->d_val, sizeof(double) * (nnz > 0 ? nnz : 1)));
+  PCG_CUDA(cudaMalloc(&A->d_dinv, sizeof(double) * (n > 0 ? n : 1)));
+  validate_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, st>>>(n, nnz, n_cols_check, diag_offset, d_rp, d_col_check,
+                                                                     d_val, A->d_row_ptr, A->d_dinv, d_err);
+  count_launch();
+  PCG_CUDA(cudaGetLastError());
+  PCG_CUDA(cudaMemcpyAsync(&h_err, d_err, sizeof(ErrInfo), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_err);
+  PCG_TRY(error_from_flags(h_err, A->row_begin));
+  A->max_row_len = h_err.max_len;
+  if (nnz > 0) {
+    narrow_kernel<<<1184, 256, 0, st>>>(nnz, d_col_store, d_val, A->d_col, A->d_val, 0);
+    count_launch();
+    PCG_CUDA(cudaGetLastError());
+  }
+  // ---- SELL-32
+  const int fmt_req = flags & 0xF0;
+  A->n_slices = (n + 31) / 32;
+  bool want_sell = fmt_req != PCG_FMT_CSR && n > 0;
+  if (want_sell) {
+    PCG_CUDA(cudaMalloc(&A->d_slice_ptr, sizeof(int64_t) * (A->n_slices + 1)));
+    int64_t *tmp;
+    PCG_CUDA(cudaMalloc(&tmp, sizeof(int64_t) * (A->n_slices + 1)));
+    slice_len_kernel<<<(unsigned)((A->n_slices + 1 + 255) / 256), 256, 0, st>>>(n, A->n_slices, A->d_row_ptr, tmp);
+    count_launch();
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, tmp, A->d_slice_ptr, A->n_slices + 1, st);
+    void *tbuf;
+    PCG_CUDA(cudaMalloc(&tbuf, tb));
+    cub::DeviceScan::ExclusiveSum(tbuf, tb, tmp, A->d_slice_ptr, A->n_slices + 1, st);
+    PCG_CUDA(cudaMemcpyAsync(&A->sell_entries, A->d_slice_ptr + A->n_slices, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, st));
+    PCG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(tbuf);
+    cudaFree(tmp);
+    const double pad = nnz > 0 ? (double)A->sell_entries / (double)nnz : 1.0;
+    if (fmt_req == PCG_FMT_AUTO && pad > 1.25) {
+      want_sell = false;  // padding too large: SELL would move >25% extra bytes
+      cudaFree(A->d_slice_ptr);
+      A->d_slice_ptr = nullptr;
+      A->sell_entries = 0;
+    } else if (A->sell_entries >= (int64_t(1) << 31)) {
+      return fail(PCG_ERR_INVALID_ARG, "csr_create: padded SELL entries exceed 2^31 on one GPU");
+    } else {
+      PCG_CUDA(cudaMalloc(&A->d_scol, sizeof(int) * (A->sell_entries > 0 ? A->sell_entries : 1)));
+      PCG_CUDA(cudaMalloc(&A->d_sval, sizeof(double) * (A->sell_entries > 0 ? A->sell_entries : 1)));
+      sell_fill_kernel<<<(unsigned)((A->n_slices * 32 + 255) / 256), 256, 0, st>>>(
+          n, A->n_slices, A->d_row_ptr, A->d_col, A->d_val, A->d_slice_ptr, A->d_scol, A->d_sval);
+      count_launch();
+      PCG_CUDA(cudaGetLastError());
+    }
+  }
+  // ---- CSR lanes per row from the mean row length (power of two, <= 32)
+  const double mean = n > 0 ? (double)nnz / (double)n : 1.0;
+  int L = 1;
+  while (L < 32 && L * 4 < mean) L <<= 1;
+  A->csr_lanes = L;
+  // ---- launch geometry: persistent grids, a multiple of the SM count
+  const int sms = num_sms(A->device);
+  A->format = want_sell ? PCG_FORMAT_SELL : PCG_FORMAT_CSR;
+  auto grid_for = [&](int fmt) {
+    int bps = k1_blocks_per_sm(fmt, A->csr_lanes);
+    int64_t g = (int64_t)sms * (bps > 0 ? bps : 1);
+    int64_t need = fmt == PCG_FORMAT_SELL ? (A->n_slices + WARPS - 1) / WARPS
+                                          : (n * A->csr_lanes + BLOCK - 1) / BLOCK;
+    if (need < 1) need = 1;
+    return (int)(g < need ? g : need);
+  };
+  const int64_t need_vec = (n / 2 + BLOCK - 1) / BLOCK;
+  A->grid_vec = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 8, need_vec));
+  // ---- measured format choice (PCG_FMT_AUTO with both formats available)
+  if (fmt_req == PCG_FMT_AUTO && want_sell && n > 0) {
+    PCG_TRY(ensure_work(A));
+    double *x = A->work.stage_x, *y = A->work.w;
+    PCG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (n + A->n_ghost), st));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best[3] = {0, 0, 0};
+    for (int fmt : {PCG_FORMAT_CSR, PCG_FORMAT_SELL}) {
+      A->grid_spmv = grid_for(fmt);
+      PCG_TRY(launch_spmv_fmt(A, fmt, x, y, st));  // warm-up
+      cudaEventRecord(e0, st);
+      for (int r = 0; r < 5; r++) PCG_TRY(launch_spmv_fmt(A, fmt, x, y, st));
+      cudaEventRecord(e1, st);
+      PCG_CUDA(cudaEventSynchronize(e1));
+      cudaEventElapsedTime(&best[fmt], e0, e1);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    A->spmv_us_csr = best[PCG_FORMAT_CSR] * 1e3 / 5;
+    A->spmv_us_sell = best[PCG_FORMAT_SELL] * 1e3 / 5;
+    A->format = best[PCG_FORMAT_SELL] <= best[PCG_FORMAT_CSR] ? PCG_FORMAT_SELL : PCG_FORMAT_CSR;
+  }
+  A->grid_spmv = grid_for(A->format);
+  if (A->work.graph_ready) {  // geometry changed after a provisional workspace: rebuild
+    free_work(A);
+  }
+  A->device_bytes = (double)(n + 1) * 4 + (double)nnz * 12 + (double)n * 8 +
+                    (A->d_slice_ptr ? (double)(A->n_slices + 1) * 8 + (double)A->sell_entries * 12 : 0);
+  return PCG_OK;
+}
+
+static pcg_status stage_in(const void *src, size_t bytes, bool dev, void **dst, bool *owned, cudaStream_t st) {
+  if (dev) {
+    *dst = const_cast<void *>(src);
+    *owned = false;
+    return PCG_OK;
+  }
+  PCG_CUDA(cudaMalloc(dst, bytes > 0 ? bytes : 8));
+  *owned = true;
+  if (bytes) PCG_CUDA(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, st));
+  return PCG_OK;
+}
+
+pcg_status csr_create_impl(int64_t n, int64_t nnz, const int64_t *row_ptr, const int64_t *col_idx,
+                           const double *val, int flags, cudaStream_t st, pcg_matrix *A) {
+  const bool dev = (flags & PCG_PTR_DEVICE) != 0;
+  int64_t ends[2] = {0, 0};
+  if (dev) {
+    PCG_CUDA(cudaMemcpyAsync(&ends[0], row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    PCG_CUDA(cudaMemcpyAsync(&ends[1], row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    PCG_CUDA(cudaStreamSynchronize(st));
+  } else {
+    ends[0] = row_ptr[0];
+    ends[1] = row_ptr[n];
+  }
+  if (ends[0] != 0 || ends[1] != nnz)
+    return fail(PCG_ERR_DIMENSION_MISMATCH, "csr_create: row_ptr[0] must be 0 and row_ptr[n] must equal nnz");
+  void *drp, *dcol, *dval;
+  bool o1, o2, o3;
+  PCG_TRY(stage_in(row_ptr, sizeof(int64_t) * (n + 1), dev, &drp, &o1, st));
+  PCG_TRY(stage_in(col_idx, sizeof(int64_t) * nnz, dev, &dcol, &o2, st));
+  PCG_TRY(stage_in(val, sizeof(double) * nnz, dev, &dval, &o3, st));
+  pcg_status s = create_local(A, n, nnz, (const int64_t *)drp, (const int64_t *)dcol, (const int64_t *)dcol,
+                              (const double *)dval, n, 0, flags, st);
+  cudaStreamSynchronize(st);
+  if (o1) cudaFree(drp);
+  if (o2) cudaFree(dcol);
+  if (o3) cudaFree(dval);
+  return s;
+}
+
+// ---------------------------------------------------------------- workspace
+pcg_status ensure_work(pcg_matrix *A) {
+  SolveWork &w = A->work;
+  if (w.sc) return PCG_OK;
+  const size_t n = (size_t)A->n, ng = (size_t)(A->n + A->n_ghost);
+  const size_t nb = sizeof(double) * (n > 0 ? n : 1), ngb = sizeof(double) * (ng > 0 ? ng : 1);
+  PCG_CUDA(cudaMalloc(&w.r, nb));
+  PCG_CUDA(cudaMalloc(&w.z, ngb));
+  PCG_CUDA(cudaMalloc(&w.q, nb));
+  PCG_CUDA(cudaMalloc(&w.p[0], ngb));
+  PCG_CUDA(cudaMalloc(&w.p[1], ngb));
+  PCG_CUDA(cudaMalloc(&w.x, ngb));
+  PCG_CUDA(cudaMalloc(&w.w, nb));
+  PCG_CUDA(cudaMalloc(&w.stage_b, nb));
+  PCG_CUDA(cudaMalloc(&w.stage_x, ngb));
+  const int sms = num_sms(A->device);
+  const size_t maxg = (size_t)sms * 32;
+  PCG_CUDA(cudaMalloc(&w.partials, sizeof(double) * 6 * maxg));
+  PCG_CUDA(cudaMalloc(&w.sc, sizeof(Scalars)));
+  PCG_CUDA(cudaMemset(w.sc, 0, sizeof(Scalars)));
+  PCG_CUDA(cudaMallocHost(&w.h_sc, sizeof(Scalars)));
+  // zero-init vectors so ghosts / pads never hold NaN garbage
+  PCG_CUDA(cudaMemset(w.z, 0, ngb));
+  PCG_CUDA(cudaMemset(w.p[0], 0, ngb));
+  PCG_CUDA(cudaMemset(w.p[1], 0, ngb));
+  PCG_CUDA(cudaMemset(w.x, 0, ngb));
+  PCG_CUDA(cudaMemset(w.stage_x, 0, ngb));
+  A->device_bytes += 9.0 * ngb;
+  return PCG_OK;
+}
+
+void free_work(pcg_matrix *A) {
+  SolveWork &w = A->work;
+  if (w.loop_exec) cudaGraphExecDestroy(w.loop_exec);
+  if (w.loop_graph) cudaGraphDestroy(w.loop_graph);
+  if (w.mloop_exec) cudaGraphExecDestroy(w.mloop_exec);
+  if (w.mloop_graph) cudaGraphDestroy(w.mloop_graph);
+  for (double *p : {w.r, w.z, w.q, w.p[0], w.p[1], w.x, w.w, w.stage_b, w.stage_x, w.partials, w.mr, w.mz, w.mq,
+                    w.mp[0], w.mp[1], w.mx, w.mb, w.mw, w.mpart})
+    if (p) cudaFree(p);
+  if (w.sc) cudaFree(w.sc);
+  if (w.h_sc) cudaFreeHost(w.h_sc);
+  if (w.msc) cudaFree(w.msc);
+  if (w.h_msc) cudaFreeHost(w.h_msc);
+  w = SolveWork();
+}
+
+}  // namespace pcgb
+
+using namespace pcgb;
+
+extern "C" pcg_status csr_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int64_t *col_idx,
+                                 const double *val, int flags, void *stream, pcg_matrix_t *out) {
+  if (!out) return fail(PCG_ERR_INVALID_ARG, "csr_create: out is null");
+  *out = nullptr;
+  if (n < 0 || nnz < 0) return fail(PCG_ERR_INVALID_ARG, "csr_create: n and nnz must be >= 0");
+  if (!row_ptr || (nnz > 0 && (!col_idx || !val)))
+    return fail(PCG_ERR_INVALID_ARG, "csr_create: null array");
+  if (nnz >= (int64_t(1) << 31)) return fail(PCG_ERR_INVALID_ARG, "csr_create: nnz per GPU must be < 2^31");
+  auto t0 = std::chrono::steady_clock::now();
+  pcg_matrix *A = new pcg_matrix();
+  cudaGetDevice(&A->device);
+  A->row_end = n;
+  A->n_global = n;
+  pcg_status s = csr_create_impl(n, nnz, row_ptr, col_idx, val, flags, (cudaStream_t)stream, A);
+  if (s != PCG_OK) {
+    csr_destroy(A);
+    return s;
+  }
+  A->t_setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = A;
+  return PCG_OK;
+}
+
+extern "C" pcg_status csr_destroy(pcg_matrix_t A) {
+  if (!A) return PCG_OK;
+  cudaSetDevice(A->device);
+  cudaDeviceSynchronize();
+  free_work(A);
+  for (void *p : {(void *)A->d_row_ptr, (void *)A->d_col, (void *)A->d_val, (void *)A->d_dinv,
+                  (void *)A->d_slice_ptr, (void *)A->d_scol, (void *)A->d_sval, (void *)A->halo.d_send_idx,
+                  (void *)A->halo.d_send_buf})
+    if (p) cudaFree(p);
+  delete A;
+  return PCG_OK;
+}
+
+extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) {
+  if (!A || !o) return fail(PCG_ERR_INVALID_ARG, "pcg_matrix_get_stats: null argument");
+  memset(o, 0, sizeof(*o));
+  o->n = A->n;
+  o->nnz = A->nnz;
+  o->format = A->format;
+  o->max_row_len = A->max_row_len;
+  o->sell_entries = A->sell_entries;
+  o->t_setup_s = A->t_setup_s;
+  o->device_bytes = A->device_bytes;
+  o->spmv_us_csr = A->spmv_us_csr;
+  o->spmv_us_sell = A->spmv_us_sell;
+  o->n_ghost = A->n_ghost;
+  o->row_begin = A->row_begin;
+  o->row_end = A->row_end;
+  o->n_global = A->n_global;
+  return PCG_OK;
+}

@@ -1,0 +1,92 @@
+// matrix.cuh — the opaque pcg_matrix handle (device formats + solver workspace).
+#pragma once
+#include <nccl.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+struct pcg_comm {
+  ncclComm_t nccl = nullptr;
+  int rank = 0, size = 1;
+  cudaStream_t comm_stream = nullptr;
+};
+
+namespace pcgb {
+
+// Halo plan for a distributed handle: this rank's rows are
+// [row_begin,row_end); local column ids: owned j -> j-row_begin, ghosts -> n+g.
+struct HaloPlan {
+  std::vector<int> nbr;                 // neighbour ranks (ascending)
+  std::vector<int64_t> recv_off, recv_cnt;  // ghost slots per neighbour (into [n, n+n_ghost))
+  std::vector<int64_t> send_off, send_cnt;  // slots into d_send_idx per neighbour
+  int *d_send_idx = nullptr;            // local row ids to pack, concatenated per neighbour
+  double *d_send_buf = nullptr;         // packed values (k doubles per row in multi mode)
+  int64_t n_send = 0;
+};
+
+struct SolveWork {
+  // single-RHS vectors (n + n_ghost entries where gathered)
+  double *r = nullptr, *z = nullptr, *q = nullptr, *p[2] = {nullptr, nullptr}, *x = nullptr;
+  double *w = nullptr;  // spmv scratch (exit check / standalone spmv)
+  double *stage_b = nullptr, *stage_x = nullptr;  // device staging for host pointers
+  double *partials = nullptr;  // 4 * max_grid
+  Scalars *sc = nullptr;       // device scalars
+  Scalars *h_sc = nullptr;     // pinned host mirror
+  cudaGraphExec_t loop_exec = nullptr;
+  cudaGraph_t loop_graph = nullptr;
+  bool graph_ready = false;
+  int graph_kind = 0;  // 1 = conditional while node, 2 = unrolled chunk
+  int unroll = 0;
+  // multi-RHS workspace (row-major n x kcap)
+  int kcap = 0;
+  double *mr = nullptr, *mz = nullptr, *mq = nullptr, *mp[2] = {nullptr, nullptr}, *mx = nullptr,
+         *mb = nullptr, *mw = nullptr;
+  MultiScalars *msc = nullptr, *h_msc = nullptr;
+  double *mpart = nullptr;
+  cudaGraphExec_t mloop_exec = nullptr;
+  cudaGraph_t mloop_graph = nullptr;
+  int mgraph_k = 0;
+};
+
+}  // namespace pcgb
+
+struct pcg_matrix {
+  int device = 0;
+  int64_t n = 0, nnz = 0;  // local rows / nnz
+  int32_t max_row_len = 0;
+  int format = PCG_FORMAT_CSR;
+  // CSR (int32)
+  int *d_row_ptr = nullptr, *d_col = nullptr;
+  double *d_val = nullptr, *d_dinv = nullptr;
+  // SELL-32
+  int64_t n_slices = 0, sell_entries = 0;
+  int64_t *d_slice_ptr = nullptr;
+  int *d_scol = nullptr;
+  double *d_sval = nullptr;
+  // CSR kernel lanes per row
+  int csr_lanes = 4;
+  // launch geometry
+  int grid_vec = 0, grid_spmv = 0;  // persistent grid sizes (multiples of the SM count)
+  double t_setup_s = 0, spmv_us_csr = 0, spmv_us_sell = 0;
+  double device_bytes = 0;
+  // distributed
+  pcg_comm *comm = nullptr;
+  int64_t n_ghost = 0, row_begin = 0, row_end = 0, n_global = 0;
+  int64_t n_interior = 0;  // rows [0,n_interior) reference no ghost (not used by the 1-GPU path)
+  pcgb::HaloPlan halo;
+  pcgb::SolveWork work;
+  std::mutex mu;
+  pcgb::CsrView csr() const { return {n, n + n_ghost, d_row_ptr, d_col, d_val}; }
+  pcgb::SellView sell() const { return {n, n_slices, d_slice_ptr, d_scol, d_sval}; }
+};
+
+namespace pcgb {
+pcg_status ensure_work(pcg_matrix *A);
+pcg_status ensure_multi_work(pcg_matrix *A, int k);
+void free_work(pcg_matrix *A);
+pcg_status launch_spmv(pcg_matrix *A, const double *x, double *y, cudaStream_t st);
+pcg_status halo_exchange(pcg_matrix *A, double *vec, int width, cudaStream_t st);
+pcg_status allreduce_sum(pcg_matrix *A, double *buf, int count, cudaStream_t st);
+bool is_device_ptr(const void *p);
+}  // namespace pcgb

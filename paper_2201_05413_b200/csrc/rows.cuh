@@ -1,0 +1,74 @@
+// rows.cuh — row iterators for the two device formats.
+//
+// Every row sum is formed left to right over the row's stored entries
+// (ascending column), i.e. in the order of the paper's MatMult y_i = Σ_j a_ij x_j
+// (S:65), with one fused multiply-add per entry.  SELL-32 and CSR with
+// L = 1 lane per row therefore produce bitwise-identical sums; CSR with L > 1
+// lanes sums L interleaved sub-sums in a fixed shuffle tree.
+#pragma once
+#include "common.cuh"
+
+namespace pcgb {
+
+// SELL-32: one warp per slice of 32 consecutive rows, lane = row.  Entries of a
+// slice are stored [t][lane] so every load of the t-th entry is one 256-B (val)
+// or 128-B (col) coalesced transaction.  Loads are issued 8 entries at a time
+// before any gather so each thread keeps 16 independent loads in flight.
+// gather(j) -> value multiplied by a_ij;  epi(row, sum) for rows < n.
+template <class Gather, class Epi>
+__device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi epi) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  for (int64_t s = w0; s < A.n_slices; s += nw) {
+    const int64_t base = A.slice_ptr[s];
+    const int len = (int)((A.slice_ptr[s + 1] - base) >> 5);
+    const double *vp = A.val + base + lane;
+    const int *cp = A.col + base + lane;
+    double sum = 0.0;
+    for (int t = 0; t < len; t += 8) {
+      double a[8];
+      int j[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        if (t + u < len) {
+          a[u] = ld_stream(vp + (size_t)(t + u) * 32);
+          j[u] = ld_stream(cp + (size_t)(t + u) * 32);
+        }
+      }
+      double g[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (t + u < len) g[u] = gather(j[u]);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (t + u < len) sum = __fma_rn(a[u], g[u], sum);
+    }
+    const int64_t row = s * 32 + lane;
+    if (row < A.n) epi(row, sum);
+  }
+}
+
+// CSR: L lanes per row (L in {1,2,4,8,16,32}), lane l takes entries l, l+L, ...
+// then the L partial sums meet in a fixed xor-shuffle tree.
+template <int L, class Gather, class Epi>
+__device__ __forceinline__ void csr_rows(const CsrView &A, Gather gather, Epi epi) {
+  const int sub = threadIdx.x & (L - 1);
+  const int64_t g0 = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) / L;
+  const int64_t ng = (int64_t)gridDim.x * BLOCK / L;
+  // all lanes of a warp iterate the same number of times (shuffles need full warps)
+  const int64_t iters = (A.n + ng - 1) / ng;
+  for (int64_t it = 0; it < iters; it++) {
+    const int64_t row = g0 + it * ng;
+    double sum = 0.0;
+    if (row < A.n) {
+      const int rs = A.row_ptr[row], re = A.row_ptr[row + 1];
+      for (int k = rs + sub; k < re; k += L) sum = __fma_rn(ld_stream(A.val + k), gather(ld_stream(A.col + k)), sum);
+    }
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o, L);
+    if (row < A.n && sub == 0) epi(row, sum);
+  }
+}
+
+}  // namespace pcgb

@@ -1,0 +1,593 @@
+// solver.cu — fused Jacobi-PCG kernels and the single-RHS driver.
+//
+// The recurrence is SURVEY §8(c).8 (the reading of P:69-75 + P:132-135 listed
+// in DESIGN.md §3).  It runs as TWO fused passes per iteration (the "2-kernel
+// schedule"), each ending in a deterministic last-block
+// grid reduction that also evaluates the scalar recurrence on the device:
+//
+//   K1 (pass A, after beta_{k-1} is known), per row i:
+//        p_k[i]  = z[i] + beta_{k-1} p_{k-1}[i]        (own row, written)
+//        q[i]    = Σ_j a_ij (z[j] + beta_{k-1} p_{k-1}[j])   (p_k recomputed at gather time)
+//        x[i]   += alpha_{k-1} p_{k-1}[i]              (deferred x update)
+//        sigma  += p_k[i] q[i]            -> finisher: alpha_k = rho/sigma, k++
+//   K2 (pass B, after alpha_k is known), per row i:
+//        r[i] -= alpha_k q[i];  z[i] = dinv[i] r[i]
+//        rho' += r z;  gamma += r r       -> finisher: stop test sqrt(gamma) <= tol*||b||,
+//                                            beta = rho'/rho
+//
+// HBM bytes per iteration: matrix once + 48n (K1: z, p, x in; p, q, x out) +
+// 40n (K2: r, q, dinv in; r, z out) = 12 nnz + 4(n+1) + 88 n.
+// The loop runs inside ONE CUDA graph launch: a conditional WHILE node whose
+// body is {K1, K2}; the finishers clear the condition when the solve stops.
+#include <cmath>
+#include <cstring>
+
+#include "matrix.cuh"
+#include "rows.cuh"
+
+namespace pcgb {
+
+enum { MODE_INIT = 0, MODE_EXIT = 1 };
+
+struct Vecs {
+  double *r, *z, *q, *p0, *p1, *x;
+  const double *dinv;
+};
+
+__device__ __forceinline__ void stop_loop(int use_cond, cudaGraphConditionalHandle h) {
+  if (use_cond) cudaGraphSetConditional(h, 0);
+}
+
+// ---------------------------------------------------------------- finishers
+__device__ void finish_alpha(Scalars *sc, double sigma, int use_cond, cudaGraphConditionalHandle h) {
+  sc->sigma = sigma;
+  if (!(sigma > 0.0)) {  // p^T A p <= 0 (or NaN): CG breakdown, A not SPD
+    sc->done = DONE_BREAKDOWN;
+    stop_loop(use_cond, h);
+  } else {
+    sc->alpha = sc->rho / sigma;
+    sc->k += 1;
+    sc->parity ^= 1;
+  }
+  sc->graph_launches += use_cond;
+}
+
+__device__ void finish_beta(Scalars *sc, double rho_new, double gamma, int use_cond,
+                            cudaGraphConditionalHandle h) {
+  sc->gamma = gamma;
+  const double rr = sqrt(gamma);
+  sc->relres_rec = rr / sc->nb;
+  if (rr <= sc->tol * sc->nb) {
+    sc->done = DONE_CONVERGED;
+    stop_loop(use_cond, h);
+  } else if (!(gamma == gamma)) {
+    sc->done = DONE_NONFINITE;
+    stop_loop(use_cond, h);
+  } else if (sc->k >= sc->max_iter) {
+    sc->done = DONE_MAXIT;
+    stop_loop(use_cond, h);
+  } else {
+    sc->beta = rho_new / sc->rho;
+    sc->rho = rho_new;
+  }
+  sc->graph_launches += use_cond;
+}
+
+// ---------------------------------------------------------------- K1: SpMV + p update + x update + sigma
+template <int FMT, int L>
+__global__ void __launch_bounds__(BLOCK) k1_kernel(SellView S, CsrView C, int64_t n_ghost, Vecs v,
+                                                   Scalars *sc, double *partials, int dist,
+                                                   int use_cond, cudaGraphConditionalHandle h) {
+  __shared__ double sm[1][WARPS];
+  const volatile Scalars *vs = sc;
+  if (vs->done != DONE_RUNNING) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) stop_loop(use_cond, h);
+    return;
+  }
+  const double beta = vs->beta, alpha_prev = vs->alpha;
+  const int par = vs->parity;
+  const double *__restrict__ pold = par ? v.p1 : v.p0;
+  double *__restrict__ pnew = par ? v.p0 : v.p1;
+  const double *__restrict__ z = v.z;
+  double *__restrict__ x = v.x;
+  double *__restrict__ q = v.q;
+  double acc = 0.0;
+  auto gather = [&](int j) { return __fma_rn(beta, __ldg(pold + j), __ldg(z + j)); };
+  auto epi = [&](int64_t i, double s) {
+    const double po = pold[i];
+    const double pi = __fma_rn(beta, po, z[i]);
+    pnew[i] = pi;
+    q[i] = s;
+    x[i] = __fma_rn(alpha_prev, po, x[i]);
+    acc = __fma_rn(pi, s, acc);
+  };
+  if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
+  else csr_rows<L>(C, gather, epi);
+  // ghost copies of p advance by the same recurrence (bitwise equal to the owner's)
+  if (n_ghost) {
+    const int64_t n = FMT == PCG_FORMAT_SELL ? S.n : C.n;
+    for (int64_t g = (int64_t)blockIdx.x * BLOCK + threadIdx.x; g < n_ghost; g += (int64_t)gridDim.x * BLOCK)
+      pnew[n + g] = __fma_rn(beta, pold[n + g], z[n + g]);
+  }
+  double red[1] = {acc};
+  block_sum<1>(red, sm);
+  if (publish_and_arrive<1>(red, partials, &sc->cnt_a)) {
+    double tot[1];
+    reduce_partials<1>(partials, tot, sm);
+    if (threadIdx.x == 0) {
+      sc->cnt_a = 0;
+      if (dist) {
+        sc->sigma = tot[0];  // local partial; allreduce + finish_alpha_kernel follow
+        sc->graph_launches += use_cond;
+      } else {
+        finish_alpha(sc, tot[0], use_cond, h);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K2: r, z updates + rho', gamma
+__global__ void __launch_bounds__(BLOCK) k2_kernel(int64_t n, Vecs v, Scalars *sc, double *partials,
+                                                   int dist, int use_cond, cudaGraphConditionalHandle h) {
+  __shared__ double sm[2][WARPS];
+  const volatile Scalars *vs = sc;
+  if (vs->done != DONE_RUNNING) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) stop_loop(use_cond, h);
+    return;
+  }
+  const double alpha = vs->alpha;
+  double a0 = 0.0, a1 = 0.0;
+  const int64_t npair = n >> 1;
+  const double2 *__restrict__ q2 = reinterpret_cast<const double2 *>(v.q);
+  const double2 *__restrict__ d2 = reinterpret_cast<const double2 *>(v.dinv);
+  double2 *__restrict__ r2 = reinterpret_cast<double2 *>(v.r);
+  double2 *__restrict__ z2 = reinterpret_cast<double2 *>(v.z);
+  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < npair; i += (int64_t)gridDim.x * BLOCK) {
+    const double2 qq = __ldcs(q2 + i), dd = __ldg(d2 + i);
+    double2 rr = r2[i];
+    rr.x = __fma_rn(-alpha, qq.x, rr.x);
+    rr.y = __fma_rn(-alpha, qq.y, rr.y);
+    const double2 zz = make_double2(dd.x * rr.x, dd.y * rr.y);
+    r2[i] = rr;
+    z2[i] = zz;
+    a0 = __fma_rn(rr.x, zz.x, a0);
+    a0 = __fma_rn(rr.y, zz.y, a0);
+    a1 = __fma_rn(rr.x, rr.x, a1);
+    a1 = __fma_rn(rr.y, rr.y, a1);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t i = n - 1;
+    const double ri = __fma_rn(-alpha, v.q[i], v.r[i]);
+    const double zi = v.dinv[i] * ri;
+    v.r[i] = ri;
+    v.z[i] = zi;
+    a0 = __fma_rn(ri, zi, a0);
+    a1 = __fma_rn(ri, ri, a1);
+  }
+  double red[2] = {a0, a1};
+  block_sum<2>(red, sm);
+  if (publish_and_arrive<2>(red, partials, &sc->cnt_b)) {
+    double tot[2];
+    reduce_partials<2>(partials, tot, sm);
+    if (threadIdx.x == 0) {
+      sc->cnt_b = 0;
+      if (dist) {
+        sc->rho_part[0] = tot[0];
+        sc->rho_part[1] = tot[1];
+        sc->graph_launches += use_cond;
+      } else {
+        finish_beta(sc, tot[0], tot[1], use_cond, h);
+      }
+    }
+  }
+}
+
+// distributed finishers (after the NCCL allreduce of the partials)
+__global__ void finish_alpha_kernel(Scalars *sc, int use_cond, cudaGraphConditionalHandle h) {
+  if (sc->done != DONE_RUNNING) return;
+  finish_alpha(sc, sc->sigma, use_cond, h);
+}
+__global__ void finish_beta_kernel(Scalars *sc, int use_cond, cudaGraphConditionalHandle h) {
+  if (sc->done != DONE_RUNNING) return;
+  finish_beta(sc, sc->rho_part[0], sc->rho_part[1], use_cond, h);
+}
+
+// ---------------------------------------------------------------- residual (init / exit check / replacement)
+// w = b - A x; r = w; z = dinv w; p[parity] = 0; partial sums (w.w, w.z, b.b).
+template <int FMT, int L>
+__global__ void __launch_bounds__(BLOCK) resid_kernel(SellView S, CsrView C, int64_t n_ghost,
+                                                      const double *__restrict__ b, Vecs v, Scalars *sc,
+                                                      double *partials, int mode, int dist) {
+  __shared__ double sm[3][WARPS];
+  const int par = sc->parity;
+  double *__restrict__ pz = par ? v.p1 : v.p0;
+  const double *__restrict__ x = v.x;
+  double ww = 0.0, wz = 0.0, bb = 0.0;
+  auto gather = [&](int j) { return __ldg(x + j); };
+  auto epi = [&](int64_t i, double s) {
+    const double bi = b[i];
+    const double wi = bi - s;
+    const double zi = v.dinv[i] * wi;
+    v.r[i] = wi;
+    v.z[i] = zi;
+    pz[i] = 0.0;
+    ww = __fma_rn(wi, wi, ww);
+    wz = __fma_rn(wi, zi, wz);
+    bb = __fma_rn(bi, bi, bb);
+  };
+  if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
+  else csr_rows<L>(C, gather, epi);
+  if (n_ghost) {
+    const int64_t n = FMT == PCG_FORMAT_SELL ? S.n : C.n;
+    for (int64_t g = (int64_t)blockIdx.x * BLOCK + threadIdx.x; g < n_ghost; g += (int64_t)gridDim.x * BLOCK)
+      pz[n + g] = 0.0;
+  }
+  double red[3] = {ww, wz, bb};
+  block_sum<3>(red, sm);
+  if (publish_and_arrive<3>(red, partials, &sc->cnt_c)) {
+    double tot[3];
+    reduce_partials<3>(partials, tot, sm);
+    if (threadIdx.x == 0) {
+      sc->cnt_c = 0;
+      sc->res_part[0] = tot[0];
+      sc->res_part[1] = tot[1];
+      sc->res_part[2] = tot[2];
+    }
+  }
+}
+
+// scalar logic of init / exit (after any allreduce of res_part)
+__global__ void resid_finish_kernel(Scalars *sc, int mode) {
+  const double ww = sc->res_part[0], wz = sc->res_part[1], bb = sc->res_part[2];
+  if (mode == MODE_INIT) {
+    sc->k = 0;
+    sc->replacements = 0;
+    sc->alpha = 0.0;
+    sc->beta = 0.0;
+    sc->relres_true = 0.0;
+    if (!isfinite(bb) || !isfinite(ww)) {
+      sc->done = DONE_NONFINITE;
+      return;
+    }
+    sc->nb = sqrt(bb);
+    if (sc->nb == 0.0) {
+      sc->done = DONE_ZERO_RHS;
+      return;
+    }
+    const double rr = sqrt(ww);
+    sc->relres_rec = rr / sc->nb;
+    if (rr <= sc->tol * sc->nb) {
+      sc->done = DONE_CONVERGED;
+    } else {
+      sc->done = DONE_RUNNING;
+      sc->rho = wz;
+    }
+  } else {
+    sc->relres_true = sqrt(ww) / sc->nb;
+    if (sc->done == DONE_CONVERGED && !(sc->relres_true <= sc->tol)) {
+      if (sc->k >= sc->max_iter) {
+        sc->done = DONE_MAXIT;
+      } else {  // residual replacement: r = b - Ax, z = dinv r, p = z (beta = 0), rho = r.z
+        sc->done = DONE_RUNNING;
+        sc->rho = wz;
+        sc->alpha = 0.0;
+        sc->beta = 0.0;
+        sc->replacements += 1;
+      }
+    }
+  }
+}
+
+// deferred x += alpha_k p_k after the loop stops on the recurrence or max_iter
+__global__ void tail_kernel(int64_t n, Vecs v, const Scalars *sc) {
+  const int done = sc->done;
+  if (done != DONE_CONVERGED && done != DONE_MAXIT) return;
+  const double alpha = sc->alpha;
+  if (alpha == 0.0) return;
+  const double *p = sc->parity ? v.p1 : v.p0;
+  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK)
+    v.x[i] = __fma_rn(alpha, p[i], v.x[i]);
+}
+__global__ void clear_alpha_kernel(Scalars *sc) { sc->alpha = 0.0; }
+
+// ---------------------------------------------------------------- standalone SpMV  y = A x
+template <int FMT, int L>
+__global__ void __launch_bounds__(BLOCK) spmv_kernel(SellView S, CsrView C, const double *__restrict__ x,
+                                                     double *__restrict__ y) {
+  auto gather = [&](int j) { return __ldg(x + j); };
+  auto epi = [&](int64_t i, double s) { __stcs(y + i, s); };
+  if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
+  else csr_rows<L>(C, gather, epi);
+}
+
+// ---------------------------------------------------------------- launch helpers
+template <template <int, int> class K>
+struct Dispatch;
+
+#define PCG_DISPATCH(FMTV, LANES, KERNEL, ...)                                   \
+  do {                                                                           \
+    if ((FMTV) == PCG_FORMAT_SELL) KERNEL<PCG_FORMAT_SELL, 1>__VA_ARGS__;        \
+    else switch (LANES) {                                                        \
+        case 1: KERNEL<PCG_FORMAT_CSR, 1>__VA_ARGS__; break;                     \
+        case 2: KERNEL<PCG_FORMAT_CSR, 2>__VA_ARGS__; break;                     \
+        case 4: KERNEL<PCG_FORMAT_CSR, 4>__VA_ARGS__; break;                     \
+        case 8: KERNEL<PCG_FORMAT_CSR, 8>__VA_ARGS__; break;                     \
+        case 16: KERNEL<PCG_FORMAT_CSR, 16>__VA_ARGS__; break;                   \
+        default: KERNEL<PCG_FORMAT_CSR, 32>__VA_ARGS__; break;                   \
+      }                                                                          \
+  } while (0)
+
+static Vecs vecs_of(pcg_matrix *A) {
+  SolveWork &w = A->work;
+  return Vecs{w.r, w.z, w.q, w.p[0], w.p[1], w.x, A->d_dinv};
+}
+
+pcg_status launch_spmv_fmt(pcg_matrix *A, int fmt, const double *x, double *y, cudaStream_t st) {
+  PCG_DISPATCH(fmt, A->csr_lanes, spmv_kernel, <<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), x, y));
+  count_launch();
+  PCG_CUDA(cudaGetLastError());
+  return PCG_OK;
+}
+
+pcg_status launch_spmv(pcg_matrix *A, const double *x, double *y, cudaStream_t st) {
+  return launch_spmv_fmt(A, A->format, x, y, st);
+}
+
+static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
+  Vecs v = vecs_of(A);
+  SolveWork &w = A->work;
+  PCG_DISPATCH(A->format, A->csr_lanes, k1_kernel,
+               <<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
+                                                A->comm ? 1 : 0, use_cond, h));
+  count_launch();
+  PCG_CUDA(cudaGetLastError());
+  if (A->comm) {
+    PCG_TRY(allreduce_sum(A, &w.sc->sigma, 1, st));
+    finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h);
+    count_launch();
+  }
+  return PCG_OK;
+}
+
+static pcg_status launch_k2(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
+  Vecs v = vecs_of(A);
+  SolveWork &w = A->work;
+  k2_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, v, w.sc, w.partials + 2 * (size_t)A->grid_spmv, A->comm ? 1 : 0,
+                                           use_cond, h);
+  count_launch();
+  PCG_CUDA(cudaGetLastError());
+  if (A->comm) {
+    PCG_TRY(allreduce_sum(A, w.sc->rho_part, 2, st));
+    finish_beta_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h);
+    count_launch();
+    // ghosts of z for the next K1 (z is final after K2)
+    PCG_TRY(halo_exchange(A, w.z, 1, st));
+  }
+  return PCG_OK;
+}
+
+static pcg_status launch_resid(pcg_matrix *A, const double *b, int mode, cudaStream_t st) {
+  Vecs v = vecs_of(A);
+  SolveWork &w = A->work;
+  if (A->comm) PCG_TRY(halo_exchange(A, w.x, 1, st));
+  PCG_DISPATCH(A->format, A->csr_lanes, resid_kernel,
+               <<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), A->n_ghost, b, v, w.sc, w.partials,
+                                                mode, A->comm ? 1 : 0));
+  count_launch();
+  PCG_CUDA(cudaGetLastError());
+  if (A->comm) PCG_TRY(allreduce_sum(A, w.sc->res_part, 3, st));
+  resid_finish_kernel<<<1, 1, 0, st>>>(w.sc, mode);
+  count_launch();
+  if (A->comm) PCG_TRY(halo_exchange(A, w.z, 1, st));
+  PCG_CUDA(cudaGetLastError());
+  return PCG_OK;
+}
+
+// Build the loop graph once per handle: WHILE(cond) { K1; K2 } (1 GPU), or an
+// unrolled chunk of U iterations polled from the host (distributed: NCCL calls
+// are kept out of conditional bodies).
+static pcg_status build_loop_graph(pcg_matrix *A) {
+  SolveWork &w = A->work;
+  if (w.graph_ready) return PCG_OK;
+  cudaStream_t cap;
+  PCG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  PCG_CUDA(cudaGraphCreate(&g, 0));
+  pcg_status st = PCG_OK;
+  if (!A->comm) {
+    cudaGraphConditionalHandle h;
+    PCG_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    alignas(cudaGraphNodeParams) unsigned char npbuf[sizeof(cudaGraphNodeParams)] = {};
+    cudaGraphNodeParams &np = *reinterpret_cast<cudaGraphNodeParams *>(npbuf);
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    PCG_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    PCG_CUDA(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    for (int u = 0; u < 2 && st == PCG_OK; u++) {
+      st = launch_k1(A, cap, 1, h);
+      if (st == PCG_OK) st = launch_k2(A, cap, 1, h);
+    }
+    cudaGraph_t out;
+    cudaError_t e = cudaStreamEndCapture(cap, &out);
+    if (st != PCG_OK) return st;
+    PCG_CUDA(e);
+    w.graph_kind = 1;
+    w.unroll = 2;
+  } else {
+    const int U = 8;
+    PCG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    for (int u = 0; u < U && st == PCG_OK; u++) {
+      st = launch_k1(A, cap, 0, 0);
+      if (st == PCG_OK) st = launch_k2(A, cap, 0, 0);
+    }
+    cudaGraph_t out;
+    cudaError_t e = cudaStreamEndCapture(cap, &out);
+    if (st != PCG_OK) return st;
+    PCG_CUDA(e);
+    cudaGraphDestroy(g);
+    g = out;
+    w.graph_kind = 2;
+    w.unroll = U;
+  }
+  PCG_CUDA(cudaGraphInstantiate(&w.loop_exec, g, 0));
+  w.loop_graph = g;
+  w.graph_ready = true;
+  cudaStreamDestroy(cap);
+  return PCG_OK;
+}
+
+static pcg_status status_of_done(int done, double relres_true, double tol) {
+  switch (done) {
+    case DONE_CONVERGED: return relres_true <= tol ? PCG_OK : PCG_NOT_CONVERGED;
+    case DONE_ZERO_RHS: return PCG_OK;
+    case DONE_MAXIT: return PCG_NOT_CONVERGED;
+    case DONE_BREAKDOWN: return PCG_ERR_NOT_SPD;
+    case DONE_NONFINITE: return PCG_ERR_NONFINITE;
+    default: return PCG_NOT_CONVERGED;
+  }
+}
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double tol, int64_t max_iter,
+                             cudaStream_t st, pcg_info *info) {
+  PCG_TRY(ensure_work(A));
+  PCG_TRY(build_loop_graph(A));
+  SolveWork &w = A->work;
+  const int64_t n = A->n;
+  const bool b_dev = is_device_ptr(b), x_dev = is_device_ptr(x);
+  const double *db = b;
+  if (!b_dev) {
+    PCG_CUDA(cudaMemcpyAsync(w.stage_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    db = w.stage_b;
+  }
+  PCG_CUDA(cudaMemcpyAsync(w.x, x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  // scalars
+  Scalars *h = w.h_sc;
+  memset(h, 0, sizeof(Scalars));
+  h->tol = tol;
+  h->max_iter = max_iter;
+  h->done = DONE_RUNNING;
+  PCG_CUDA(cudaMemcpyAsync(w.sc, h, sizeof(Scalars), cudaMemcpyHostToDevice, st));
+  cudaEvent_t e0, e1;
+  PCG_CUDA(cudaEventCreate(&e0));
+  PCG_CUDA(cudaEventCreate(&e1));
+  PCG_CUDA(cudaEventRecord(e0, st));
+  PCG_TRY(launch_resid(A, db, MODE_INIT, st));
+  for (int round = 0;; round++) {
+    if (w.graph_kind == 1) {
+      PCG_CUDA(cudaGraphLaunch(w.loop_exec, st));
+    } else {
+      for (;;) {  // unrolled chunks, host-polled
+        PCG_CUDA(cudaMemcpyAsync(h, w.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
+        PCG_CUDA(cudaStreamSynchronize(st));
+        if (h->done != DONE_RUNNING) break;
+        PCG_CUDA(cudaGraphLaunch(w.loop_exec, st));
+      }
+    }
+    tail_kernel<<<A->grid_vec, BLOCK, 0, st>>>(n, vecs_of(A), w.sc);
+    clear_alpha_kernel<<<1, 1, 0, st>>>(w.sc);
+    count_launch(2);
+    PCG_TRY(launch_resid(A, db, MODE_EXIT, st));
+    PCG_CUDA(cudaMemcpyAsync(h, w.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
+    PCG_CUDA(cudaStreamSynchronize(st));
+    if (h->done != DONE_RUNNING) break;  // else: residual replacement, run the loop again
+  }
+  PCG_CUDA(cudaEventRecord(e1, st));
+  if (h->done == DONE_ZERO_RHS) PCG_CUDA(cudaMemsetAsync(w.x, 0, sizeof(double) * n, st));
+  PCG_CUDA(cudaMemcpyAsync(x, w.x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  g_host_launches += (int64_t)h->graph_launches;
+  pcg_status s = status_of_done(h->done, h->relres_true, tol);
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->iterations = h->k;
+    info->relres_recurrence = h->relres_rec;
+    info->relres_true = h->done == DONE_ZERO_RHS ? 0.0 : h->relres_true;
+    info->converged = (s == PCG_OK);
+    info->status = s;
+    info->replacements = h->replacements;
+    info->t_solve_s = ms * 1e-3;
+    const double nn = (double)A->n, nz = (double)A->nnz;
+    info->bytes_algorithmic = (double)h->k * (12.0 * nz + 4.0 * (nn + 1) + 88.0 * nn);
+    info->flops = (double)h->k * (2.0 * nz + 13.0 * nn);
+  }
+  if (s == PCG_ERR_NOT_SPD) set_error("pcg_solve: p^T A p <= 0 (matrix not SPD)");
+  if (s == PCG_ERR_NONFINITE) set_error("pcg_solve: non-finite right-hand side, x0 or iterate");
+  if (s == PCG_NOT_CONVERGED) set_error("pcg_solve: not converged within max_iter");
+  return s;
+}
+
+}  // namespace pcgb
+
+using namespace pcgb;
+
+extern "C" pcg_status pcg_solve(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
+                                void *stream, pcg_info *info) {
+  if (!A || !b || !x) return fail(PCG_ERR_INVALID_ARG, "pcg_solve: null argument");
+  if (!(tol > 0.0)) return fail(PCG_ERR_INVALID_ARG, "pcg_solve: tol must be > 0");
+  if (max_iter < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_solve: max_iter must be >= 1");
+  std::lock_guard<std::mutex> lk(A->mu);
+  PCG_CUDA(cudaSetDevice(A->device));
+  return solve_impl(A, b, x, tol, max_iter, (cudaStream_t)stream, info);
+}
+
+extern "C" pcg_status pcg_spmv(pcg_matrix_t A, const double *x, double *y, void *stream) {
+  if (!A || !x || !y) return fail(PCG_ERR_INVALID_ARG, "pcg_spmv: null argument");
+  std::lock_guard<std::mutex> lk(A->mu);
+  PCG_CUDA(cudaSetDevice(A->device));
+  PCG_TRY(ensure_work(A));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool xd = is_device_ptr(x), yd = is_device_ptr(y);
+  const double *dx = x;
+  if (A->comm || !xd) {  // gathered vector needs n + n_ghost entries in device memory
+    PCG_CUDA(cudaMemcpyAsync(A->work.stage_x, x, sizeof(double) * A->n,
+                             xd ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (A->comm) PCG_TRY(halo_exchange(A, A->work.stage_x, 1, st));
+    dx = A->work.stage_x;
+  }
+  double *dy = yd ? y : A->work.w;
+  PCG_TRY(launch_spmv(A, dx, dy, st));
+  if (!yd) PCG_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * A->n, cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  return PCG_OK;
+}
+
+namespace pcgb {
+int k1_blocks_per_sm(int fmt, int lanes) {
+  int b = 0;
+  cudaError_t e;
+  if (fmt == PCG_FORMAT_SELL) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_SELL, 1>, BLOCK, 0);
+  } else {
+    switch (lanes) {
+      case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_CSR, 1>, BLOCK, 0); break;
+      case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_CSR, 2>, BLOCK, 0); break;
+      case 4: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_CSR, 4>, BLOCK, 0); break;
+      case 8: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_CSR, 8>, BLOCK, 0); break;
+      case 16: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_CSR, 16>, BLOCK, 0); break;
+      default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_CSR, 32>, BLOCK, 0); break;
+    }
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 4;
+  }
+  return b < 1 ? 1 : (b > 8 ? 8 : b);
+}
+}  // namespace pcgb

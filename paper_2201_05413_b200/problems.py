@@ -1,0 +1,67 @@
+"""Benchmark problems C1-C5 (BASELINE.json configs) built on the GPU by fem_gen.
+
+configs/configs.json holds the parameters (plain data).  fem_build() calls the
+library's device generator (include/fem_gen.h); nothing here computes values.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+from . import _lib
+from ._lib import FemSpec, check, lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CONFIGS = os.path.join(ROOT, "configs", "configs.json")
+
+_FAM = {"P1_TRI": 1, "P1_TET": 2, "P2_TRI": 3}
+_F = {"ZERO": 0, "ONE": 1, "SIN2D": 2, "SIN3D": 3, "BUMP3D": 4}
+_G = {"ZERO": 0, "X2MY2": 1}
+_POL = {"ELEMENT": 0, "AXIS": 1}
+
+
+def configs() -> dict:
+    with open(CONFIGS) as fh:
+        return {k: v for k, v in json.load(fh).items() if not k.startswith("_")}
+
+
+def fem_spec(name: str, c: int | None = None, k: int | None = None) -> FemSpec:
+    cfg = dict(configs()[name])
+    if c is not None:
+        cfg["c"] = c
+    if k is not None:
+        cfg["k"] = k
+    return FemSpec(family=_FAM[cfg["family"]], c=cfg["c"], jitter=int(cfg["jitter"]), fkind=_F[cfg["f"]],
+                   gkind=_G[cfg["g"]], policy=_POL[cfg["policy"]], k=cfg["k"] if cfg["f"] == "BUMP3D" else 1,
+                   pad=0, seed=cfg["seed"], sigma=float(cfg.get("sigma", 0.0)))
+
+
+def problem_size(spec: FemSpec):
+    n, nnz, nodes = C.c_int64(), C.c_int64(), C.c_int64()
+    check(lib().fem_problem_size(C.byref(spec), C.byref(n), C.byref(nnz), C.byref(nodes)), "fem_problem_size")
+    return n.value, nnz.value, nodes.value
+
+
+def fem_build(spec: FemSpec, row_begin: int = 0, row_end: int | None = None, device=None, stream=None):
+    """Assemble rows [row_begin, row_end) of K_FF and B on the GPU.
+    Returns dict(row_ptr, col, val, B) of torch CUDA tensors (col = global ids)."""
+    import torch
+    n, _, _ = problem_size(spec)
+    row_end = n if row_end is None else row_end
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    st = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream if stream is None else stream.cuda_stream)
+    rows = row_end - row_begin
+    rp = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+    nnz = C.c_int64()
+    check(lib().fem_count(C.byref(spec), row_begin, row_end, C.c_void_p(rp.data_ptr()), C.byref(nnz), st),
+          "fem_count")
+    col = torch.empty(max(nnz.value, 1), dtype=torch.int64, device=dev)[:nnz.value]
+    val = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=dev)[:nnz.value]
+    k = spec.k
+    B = torch.empty((k, max(rows, 1)), dtype=torch.float64, device=dev)[:, :rows]  # column-major (rows, k)
+    check(lib().fem_assemble(C.byref(spec), row_begin, row_end, C.c_void_p(rp.data_ptr()),
+                             C.c_void_p(col.data_ptr()), C.c_void_p(val.data_ptr()), C.c_void_p(B.data_ptr()),
+                             max(rows, 1), st), "fem_assemble")
+    return {"row_ptr": rp, "col": col, "val": val, "B": B.t(), "n_global": n, "row_begin": row_begin,
+            "row_end": row_end}

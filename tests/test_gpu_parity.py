@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same
+seeded inputs.  Tolerances:
+  * integer structure (row_ptr, col, partitions): bit-exact;
+  * SpMV: |y_gpu - y_orc|_i <= 2 nnz_i u Σ_j |a_ij x_j|  (forward error of any
+    summation order, u = 2^-53);
+  * PCG: rel-L2(x_gpu, x_orc) <= 1e-9, true relres <= tol, iterations within
+    max(2%, 1) of the oracle (north_star).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def pcg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_05413_b200 as p
+    return p
+
+
+def _dev(a):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(a)).cuda()
+
+
+def _matrix(pcg, A, fmt="auto"):
+    return pcg.Matrix.from_csr(_dev(A.row_ptr), _dev(A.col), _dev(A.val), fmt=fmt)
+
+
+def _spmv_bound(A, x):
+    absx = np.abs(x)
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    mag = np.bincount(rows, weights=np.abs(A.val) * absx[A.col], minlength=A.n)
+    ln = np.diff(A.row_ptr)
+    return 2 * ln * U * mag + 1e-300
+
+
+CASES = [("C1", None), ("C2", 96), ("C3", 48), ("C5", 40), ("C4", 24)]
+
+
+@pytest.mark.parametrize("name,c", CASES)
+@pytest.mark.parametrize("fmt", ["auto", "csr", "sell"])
+def test_spmv_parity(pcg, name, c, fmt):
+    P = O.build_problem(name, c=c, k=1)
+    A = P["A"]
+    M = _matrix(pcg, A, fmt)
+    x = np.random.default_rng(7).standard_normal(A.n)
+    y = M.spmv(_dev(x)).cpu().numpy()
+    yo = O.spmv(A, x)
+    assert np.all(np.abs(y - yo) <= _spmv_bound(A, x))
+    if fmt != "auto":
+        assert M.stats()["format"] == {"csr": 1, "sell": 2}[fmt]
+
+
+@pytest.mark.parametrize("name,c", CASES)
+def test_pcg_parity(pcg, name, c):
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    tol = O.configs()[name]["tol"]
+    r = O.pcg(A, b, tol=tol)
+    assert r.status == O.OK
+    M = _matrix(pcg, A)
+    x, info = M.solve(_dev(b), tol=tol)
+    x = x.cpu().numpy()
+    assert info["status"] == 0, info
+    assert info["relres_true"] <= tol
+    rel = np.linalg.norm(x - r.x) / np.linalg.norm(r.x)
+    assert rel <= 1e-9, rel
+    assert abs(info["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations), (info["iterations"], r.iterations)
+    # the true residual reported by the GPU agrees with the oracle's definition
+    t = np.linalg.norm(b - A.to_scipy() @ x) / np.linalg.norm(b)
+    assert abs(t - info["relres_true"]) <= 1e-3 * tol
+
+
+@pytest.mark.parametrize("fmt", ["csr", "sell"])
+def test_pcg_both_formats_and_determinism(pcg, fmt):
+    P = O.build_problem("C2", c=64)
+    M = _matrix(pcg, P["A"], fmt)
+    b = _dev(P["B"][:, 0])
+    x1, i1 = M.solve(b)
+    x2, i2 = M.solve(b)
+    assert i1["iterations"] == i2["iterations"]
+    assert bool((x1 == x2).all()), "solve must be bitwise reproducible"
+
+
+def test_pcg_host_pointers_equal_device(pcg):
+    P = O.build_problem("C1", c=32)
+    M = _matrix(pcg, P["A"])
+    import torch
+    b = torch.as_tensor(P["B"][:, 0])
+    xh, ih = M.solve(b)  # host tensors (staged by the library)
+    xd, idv = M.solve(b.cuda())
+    assert xh.device.type == "cpu"
+    assert ih["iterations"] == idv["iterations"]
+    assert np.array_equal(xh.numpy(), xd.cpu().numpy())
+
+
+def test_pcg_x0_warm_start_and_zero_rhs(pcg):
+    P = O.build_problem("C1", c=32)
+    A, b = P["A"], P["B"][:, 0]
+    M = _matrix(pcg, A)
+    r = O.pcg(A, b, tol=1e-12)
+    x, info = M.solve(_dev(b), x0=_dev(r.x), tol=1e-10)  # already converged: 0 iterations
+    assert info["iterations"] == 0 and info["status"] == 0
+    x, info = M.solve(_dev(np.zeros(A.n)), x0=_dev(np.ones(A.n)))
+    assert info["iterations"] == 0 and info["status"] == 0 and float(x.abs().max()) == 0.0
+    # warm start from a partial solve matches the oracle from the same x0
+    x0 = O.pcg(A, b, tol=1e-3).x
+    ro = O.pcg(A, b, x0=x0, tol=1e-10)
+    x, info = M.solve(_dev(b), x0=_dev(x0), tol=1e-10)
+    assert abs(info["iterations"] - ro.iterations) <= max(1, 0.02 * ro.iterations)
+    assert np.linalg.norm(x.cpu().numpy() - ro.x) / np.linalg.norm(ro.x) <= 1e-9
+
+
+def test_pcg_max_iter_not_converged(pcg):
+    P = O.build_problem("C1", c=32)
+    A, b = P["A"], P["B"][:, 0]
+    M = _matrix(pcg, A)
+    ro = O.pcg(A, b, tol=1e-10, max_iter=7)
+    x, info = M.solve(_dev(b), tol=1e-10, max_iter=7)
+    assert info["status"] == 1 and info["iterations"] == 7 and ro.status == O.NOT_CONVERGED
+    assert np.linalg.norm(x.cpu().numpy() - ro.x) / np.linalg.norm(ro.x) <= 1e-12
+
+
+def _csr(D):
+    n = D.shape[0]
+    rp, cols, vals = [0], [], []
+    for i in range(n):
+        nz = np.nonzero(D[i])[0]
+        cols += list(nz)
+        vals += list(D[i, nz])
+        rp.append(len(cols))
+    return O.Csr(n, rp, cols, vals)
+
+
+def test_error_paths(pcg):
+    from paper_2201_05413_b200 import PcgError
+    bad = {
+        "unsorted": (np.array([0, 2, 3]), np.array([1, 0, 1]), np.array([1., 2., 3.]), 4),
+        "out_of_range": (np.array([0, 1, 2]), np.array([0, 5]), np.array([1., 1.]), 3),
+        "dim": (np.array([0, 2, 1]), np.array([0, 1]), np.array([1., 1.]), 5),
+        "zero_diag": (np.array([0, 1, 2]), np.array([1, 1]), np.array([1., 1.]), 6),
+        "neg_diag": (np.array([0, 1, 2]), np.array([0, 1]), np.array([-1., 1.]), 7),
+        "nan": (np.array([0, 1, 2]), np.array([0, 1]), np.array([np.nan, 1.]), 8),
+    }
+    for what, (rp, ci, va, code) in bad.items():
+        with pytest.raises(PcgError) as e:
+            pcg.Matrix.from_csr(_dev(rp), _dev(ci), _dev(va))
+        assert e.value.status == code, what
+    # indefinite matrix with positive diagonal: CG breakdown -> NOT_SPD
+    M = _matrix(pcg, _csr(np.array([[1., 3.], [3., 1.]])))
+    with pytest.raises(PcgError) as e:
+        M.solve(_dev(np.array([1., 0.])))
+    assert e.value.status == 7
+    # non-finite right-hand side
+    M = _matrix(pcg, _csr(np.diag([2., 3., 4.])))
+    with pytest.raises(PcgError) as e:
+        M.solve(_dev(np.array([1., np.inf, 0.])))
+    assert e.value.status == 8
+    # diagonal / identity: one iteration
+    x, info = M.solve(_dev(np.array([2., 3., 4.])))
+    assert info["iterations"] == 1 and np.allclose(x.cpu().numpy(), 1.0)
+
+
+def test_empty_and_tiny(pcg):
+    M = _matrix(pcg, _csr(np.array([[4.0]])))
+    x, info = M.solve(_dev(np.array([2.0])))
+    assert info["iterations"] == 1 and float(x[0]) == 0.5
+    M = _matrix(pcg, O.Csr(0, [0], [], []))
+    x, info = M.solve(_dev(np.zeros(0)))
+    assert info["iterations"] == 0
+
+
+@pytest.mark.parametrize("k", [1, 3, 16])
+def test_multi_rhs_parity(pcg, k):
+    P = O.build_problem("C4", c=24, k=max(k, 1))
+    A, B = P["A"], P["B"][:, :k]
+    M = _matrix(pcg, A)
+    X, infos = M.solve_multi(_dev(B), tol=1e-10)
+    X = X.cpu().numpy()
+    for j in range(k):
+        r = O.pcg(A, B[:, j], tol=1e-10)
+        assert infos[j]["status"] == 0 and infos[j]["relres_true"] <= 1e-10
+        assert np.linalg.norm(X[:, j] - r.x) / np.linalg.norm(r.x) <= 1e-9
+        assert abs(infos[j]["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
+
+
+def test_multi_rhs_frozen_columns_and_zero_column(pcg):
+    """Columns converge at different iterations and freeze; a zero column gives x = 0."""
+    P = O.build_problem("C1", c=48)
+    A = P["A"]
+    rng = np.random.default_rng(3)
+    B = np.column_stack([P["B"][:, 0], np.zeros(A.n), rng.standard_normal(A.n), 1e-3 * P["B"][:, 0]])
+    M = _matrix(pcg, A)
+    X, infos = M.solve_multi(_dev(B), tol=1e-10)
+    X = X.cpu().numpy()
+    assert infos[1]["iterations"] == 0 and np.all(X[:, 1] == 0)
+    its = []
+    for j in (0, 2, 3):
+        r = O.pcg(A, B[:, j], tol=1e-10)
+        its.append(r.iterations)
+        assert abs(infos[j]["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
+        assert np.linalg.norm(X[:, j] - r.x) / np.linalg.norm(r.x) <= 1e-9
+    assert len(set(its)) > 1  # the columns really froze at different steps
+
+
+@pytest.mark.parametrize("name,c", [("C1", 64), ("C2", 64), ("C3", 32), ("C4", 16), ("C5", 24)])
+def test_generator_structure_parity(pcg, name, c):
+    """GPU FEM assembly: CSR structure bit-exact vs the oracle; values and RHS within
+    a few ulps of the row magnitude (different but equivalent summation)."""
+    spec = pcg.fem_spec(name, c=c)
+    G = pcg.fem_build(spec)
+    P = O.build_problem(name, c=c)
+    A = P["A"]
+    assert np.array_equal(G["row_ptr"].cpu().numpy(), A.row_ptr)
+    assert np.array_equal(G["col"].cpu().numpy(), A.col)
+    val = G["val"].cpu().numpy()
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    rowmax = np.zeros(A.n)
+    np.maximum.at(rowmax, rows, np.abs(A.val))
+    assert np.all(np.abs(val - A.val) <= 64 * U * rowmax[rows])
+    B = G["B"].cpu().numpy()
+    assert B.shape == P["B"].shape
+    scale = np.max(np.abs(P["B"]), axis=0)
+    assert np.all(np.abs(B - P["B"]) <= 1e-12 * scale[None, :])
