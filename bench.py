@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark: Jacobi-PCG time-to-solution at rel-res 1e-10 on the C5 workload
+(3D P1 Kuhn cube, 512^3 cells, 133,432,831 unknowns, 932,463,091 nnz), on N GPUs.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+One "step" = one full pcg_solve (init, all iterations, exit check) from x0 = 0 on
+the device-resident system.  `value` is the device-timed time-to-solution (CUDA
+events, max over ranks).  `e2e` repeats it through the same public API with
+pinned HOST b and x (H2D of b, x0 and D2H of x inside the timed region).
+The roofline object reports the dominant fused kernel (K1: SpMV + p/x updates +
+sigma) against the measured HBM copy bandwidth in MEASURED_PEAKS.json.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return HBM_FALLBACK_GBS, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                for b, name in REASON_BITS.items():
+                    if bits & b and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+    def bad(self):
+        if BAD_REASONS & self.reasons:
+            return True
+        if self.samples and self.max_mhz and statistics.median(self.samples) < 0.5 * self.max_mhz \
+                and "sw_power_cap" not in self.reasons:
+            return True
+        return False
+
+
+# ------------------------------------------------------------------------------ CPU oracle leg
+def oracle_sample(cfg_name: str, c_sample: int, reps: int = 1):
+    """Time the oracle (as it stands, 1 thread) on the same construction at c_sample."""
+    import oracle as O
+    P = O.build_problem(cfg_name, c=c_sample)
+    A, b = P["A"], P["B"][:, 0]
+    times, its = [], None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = O.pcg(A, b, tol=O.configs()[cfg_name]["tol"])
+        times.append(time.perf_counter() - t0)
+        its = r.iterations
+    return {"n": A.n, "nnz": A.nnz, "iterations": its, "t_solve": times}
+
+
+def iter_bytes(n, nnz, k=1):
+    return 12.0 * nnz + 4.0 * (n + 1) + 88.0 * k * n
+
+
+def scale_to_workload(sample, n, nnz, iters):
+    """time-to-solution of the workload implied by the sample's per-iteration cost
+    (per-iteration bytes ratio) and the workload's iteration count."""
+    per_iter = statistics.median(sample["t_solve"]) / sample["iterations"]
+    return per_iter * iter_bytes(n, nnz) / iter_bytes(sample["n"], sample["nnz"]) * iters
+
+
+def estimate_iterations(name, c_full, sample):
+    # Jacobi-PCG iterations on the lattice grow ~1.95x per doubling of c (SURVEY §8(c) probes)
+    import math
+    return sample["iterations"] * 1.95 ** math.log2(c_full / sample["c"])
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2201_05413_b200.problems import configs
+    cfg = configs()[args.config]
+    c_full = args.c or cfg["c"]
+    from paper_2201_05413_b200.problems import fem_spec, problem_size
+    n, nnz, _ = problem_size(fem_spec(args.config, c=c_full))
+    import oracle as O
+    P = O.build_problem(args.config, c=args.sample_c)
+    A, b = P["A"], P["B"][:, 0]
+    times, its = [], 0
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = O.pcg(A, b, tol=cfg["tol"])
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+        its = r.iterations
+    sample = {"n": A.n, "nnz": A.nnz, "iterations": its, "t_solve": times, "c": args.sample_c}
+    iters = args.ref_iters or estimate_iterations(args.config, c_full, sample)
+    value = scale_to_workload(sample, n, nnz, iters)
+    desc = (f"oracle Jacobi-PCG (oracle/oracle.c, 1 thread, as it stands) on the {args.config} construction at "
+            f"c={args.sample_c} ({A.n} unknowns, {A.nnz} nnz, {its} iterations, median {statistics.median(times):.2f}"
+            f" s/solve); scaled to the workload by per-iteration bytes x {iters:.0f} iterations")
+    line = {"impl": "reference", "metric": "pcg_time_to_solution", "value": value, "unit": "s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args.config, c_full, n, nnz, args.gpus),
+            "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(name, c, n, nnz, gpus):
+    desc = {"C5": f"C5: 3D Laplace, P1 Kuhn tets on a {c}^3-cell unit cube, f=3pi^2 sin sin sin, u=0 on the "
+                  f"boundary, Jacobi-PCG x0=0 to rel-res 1e-10",
+            "C4": f"C4: 3D P1 Kuhn {c}^3 cells, 16 Gaussian-bump RHS", "C3": f"C3: 2D P2 {c}^2 cells, f=1",
+            "C2": f"C2: 2D jittered P1 {c}^2 cells, harmonic x^2-y^2 boundary data",
+            "C1": f"C1: 2D P1 {c}^2 cells, sin RHS"}[name]
+    return {"workload": desc, "config": name, "n": n, "nnz": nnz, "global_batch": 1, "tol": 1e-10,
+            "parallelism": f"row-partition over {gpus} GPU(s): NCCL halo of z + 2 scalar allreduces per iteration"
+            if gpus > 1 else "1 GPU",
+            "l2": "no flush needed: every iteration streams > 23 GB, >> 126 MB L2" if name == "C5" else
+            "working set may be L2-resident"}
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--c", type=int, default=None, help="override cells per axis (testing)")
+    ap.add_argument("--sample-c", type=int, default=96, help="oracle sample size for the CPU legs")
+    ap.add_argument("--ref-iters", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fmt", default="auto", choices=["auto", "csr", "sell"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2201_05413_b200 as pcg
+    from paper_2201_05413_b200.problems import configs, fem_build, fem_spec, problem_size
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = configs()[args.config]
+    c = args.c or cfg["c"]
+    spec = fem_spec(args.config, c=c)
+    n, nnz, _ = problem_size(spec)
+    tol, max_iter = cfg["tol"], cfg["max_iter"]
+
+    # ---- build the system on the device (setup, untimed)
+    t_setup0 = time.perf_counter()
+    comm = None
+    if world == 1:
+        P = fem_build(spec)
+        A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"], fmt=args.fmt)
+        r0, r1 = 0, n
+    else:
+        rp_full = fem_build_rowptr(spec, n)
+        bounds = pcg.partition_rows(rp_full, world)
+        del rp_full
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        P = fem_build(spec, r0, r1)
+        comm = pcg.Comm.from_process_group()
+        A = pcg.Matrix.from_csr_dist(comm, n, r0, r1, P["row_ptr"], P["col"], P["val"], fmt=args.fmt)
+    b = P["B"][:, 0].contiguous()
+    del P
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    t_setup = time.perf_counter() - t_setup0
+    stats = A.stats()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up
+    info = None
+    for _ in range(args.warmup):
+        x, info = A.solve(b, tol=tol, max_iter=max_iter)
+
+    # ---- timed region (device-resident inputs); re-measured once if clocks were bad
+    def timed(device_inputs: bool):
+        st = torch.cuda.current_stream()
+        if device_inputs:
+            bb = b
+        else:
+            bb = b.cpu().pin_memory()
+        barrier()
+        l0 = pcg.kernel_launches()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as cs:
+            e0.record(st)
+            infos = []
+            for _ in range(args.steps):
+                x, inf = A.solve(bb, tol=tol, max_iter=max_iter)  # host bb: staged H2D + D2H inside
+                infos.append(inf)
+            e1.record(st)
+            barrier()
+        ms = e0.elapsed_time(e1) / args.steps
+        return max_over_ranks(ms), infos, pcg.kernel_launches() - l0, cs, x
+
+    ms, infos, launches, cs, x = timed(True)
+    remeasured = False
+    if cs.bad():
+        ms, infos, launches, cs, x = timed(True)
+        remeasured = True
+    iters = infos[-1]["iterations"]
+    ms_e2e, infos_e2e, _, _, _ = timed(False)
+
+    # ---- roofline of the dominant kernel (K1) + standalone SpMV bandwidth
+    hbm, peak_kind = peaks()
+    roof = None
+    spmv_gbs = None
+    k_us = None
+    if world == 1:
+        import ctypes as C
+        us1, us2, done = C.c_double(), C.c_double(), C.c_int32()
+        pcg.check(pcg.lib().pcg_profile_kernels(A._h, C.c_void_p(b.data_ptr()), 20,
+                                                 C.c_void_p(torch.cuda.current_stream().cuda_stream),
+                                                 C.byref(us1), C.byref(us2), C.byref(done)), "pcg_profile_kernels")
+        k1_bytes = 12.0 * nnz + 4.0 * (n + 1) + 48.0 * n
+        k2_bytes = 40.0 * n
+        achieved = k1_bytes / (us1.value * 1e-6) / 1e9
+        roof = {"bound": "hbm", "kernel": "k1_kernel (SpMV + p/x updates + sigma, fused)",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "peak_source": peak_kind, "traffic": None,
+                "bytes_per_launch": k1_bytes, "us_per_launch": us1.value,
+                "k2": {"bytes_per_launch": k2_bytes, "us_per_launch": us2.value,
+                       "achieved": k2_bytes / (us2.value * 1e-6) / 1e9},
+                "iteration": {"bytes": iter_bytes(n, nnz), "us": us1.value + us2.value,
+                              "frac": iter_bytes(n, nnz) / ((us1.value + us2.value) * 1e-6) / 1e9 / hbm}}
+        k_us = (us1.value, us2.value)
+        xs = torch.ones(n, dtype=torch.float64, device="cuda")
+        ys = torch.empty_like(xs)
+        for _ in range(3):
+            A.spmv(xs, ys)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        e0.record()
+        for _ in range(reps):
+            A.spmv(xs, ys)
+        e1.record()
+        torch.cuda.synchronize()
+        spmv_us = e0.elapsed_time(e1) * 1e3 / reps
+        spmv_gbs = (12.0 * nnz + 4.0 * (n + 1) + 16.0 * n) / (spmv_us * 1e-6) / 1e9
+    else:
+        per_iter_us = ms * 1e3 / max(iters, 1)
+        achieved = (12.0 * nnz + 4.0 * (n + 1) + 88.0 * n) / world / (per_iter_us * 1e-6) / 1e9
+        roof = {"bound": "hbm", "kernel": "whole iteration (per GPU)", "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_kind, "traffic": None}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        smp = oracle_sample(args.config, args.sample_c)
+        smp["c"] = args.sample_c
+        v = scale_to_workload(smp, n, nnz, iters)
+        cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
+               "sample": f"oracle/oracle.c Jacobi-PCG, 1 thread, {args.config} construction at c={args.sample_c} "
+                         f"({smp['n']} unknowns, {smp['nnz']} nnz, {smp['iterations']} iterations, "
+                         f"{smp['t_solve'][0]:.2f} s); scaled by per-iteration bytes x {iters} GPU iterations"}
+
+    if rank == 0:
+        h2d = 16 * (r1 - r0)  # b and x0
+        d2h = 8 * (r1 - r0)   # x
+        line = {
+            "metric": "pcg_time_to_solution", "value": ms / 1e3, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(workload_config(args.config, c, n, nnz, world), iterations=iters,
+                           format={1: "csr", 2: "sell"}[stats["format"]], setup_s=round(t_setup, 3),
+                           relres_true=infos[-1]["relres_true"]),
+            "throughput": {"cg_iterations_per_s": iters / (ms / 1e3),
+                           "effective_GBps": iter_bytes(n, nnz) * iters / (ms / 1e3) / 1e9,
+                           "spmv_GBps": spmv_gbs, "spmv_frac_of_hbm": spmv_gbs / hbm if spmv_gbs else None},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": ms_e2e / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": cs.summary(), "remeasured": remeasured,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        A.close()
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def fem_build_rowptr(spec, n):
+    """Row pointer of the full system (device count pass), for the partition rule."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2201_05413_b200._lib import check, lib
+    rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    nnz = C.c_int64()
+    check(lib().fem_count(C.byref(spec), 0, n, C.c_void_p(rp.data_ptr()), C.byref(nnz),
+                          C.c_void_p(torch.cuda.current_stream().cuda_stream)), "fem_count")
+    return rp.cpu().numpy()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -137,9 +137,29 @@ pcg_status csr_create_dist(pcg_comm_t comm, int64_t n_global, int64_t row_begin,
                            const int64_t *col_idx_global, const double *val, int flags,
                            void *stream, pcg_matrix_t *out);
 
+/* Host-side halo planning (used by csr_create_dist; host pointers, no GPU needed).
+ * pcg_halo_ghosts: sorted unique columns outside [row_begin, row_end) referenced by the
+ *   local rows (col: nnz_local global ids).  Writes min(count, cap) ids; *n_ghost = count.
+ * pcg_halo_recv_plan: for a sorted ghost list and all ranks' row bounds (G+1 entries,
+ *   bounds[g]..bounds[g+1] owned by rank g), the number of ghosts owned by each rank and
+ *   the offset of its run in the ghost list (ghost slots are [n_local + offset, +count)).
+ *   INDEX_OUT_OF_RANGE if a ghost lies outside every rank's rows. */
+pcg_status pcg_halo_ghosts(int64_t row_begin, int64_t row_end, int64_t nnz_local, const int64_t *col_idx_global,
+                           int64_t *ghosts, int64_t cap, int64_t *n_ghost);
+pcg_status pcg_halo_recv_plan(int64_t n_ghost, const int64_t *ghosts, int32_t G, const int64_t *bounds,
+                              int64_t *recv_count, int64_t *recv_offset);
+
 /* ---------------------------------------------------------------- diagnostics */
 const char *pcg_last_error(void);
 const char *pcg_status_string(pcg_status s);
+/* Per-kernel timing for the roofline (bench/profiling only): runs the init pass on b
+ * (device pointer, x0 = 0), then `reps` PCG iterations launched one kernel at a time
+ * with CUDA events around each fused pass on `stream`.  Writes the mean device time
+ * of K1 (SpMV + p/x updates + sigma) and K2 (r/z updates + dots) in microseconds.
+ * Single-GPU handles only; stops early (fewer reps) if the solve converges. */
+pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32_t reps, void *stream, double *us_k1,
+                               double *us_k2, int32_t *reps_done);
+
 /* number of kernels this library launched in the calling process (monotone counter,
  * for launch accounting in benchmarks) */
 int64_t pcg_kernel_launches(void);

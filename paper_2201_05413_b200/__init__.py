@@ -190,3 +190,27 @@ def partition_rows(row_ptr, G: int) -> np.ndarray:
     check(lib().pcg_partition_rows(len(rp) - 1, rp.ctypes.data_as(C.c_void_p), G,
                                    out.ctypes.data_as(C.c_void_p)), "pcg_partition_rows")
     return out
+
+
+def halo_ghosts(row_begin: int, row_end: int, col_global) -> np.ndarray:
+    """Sorted unique remote columns of a rank's rows (host logic of csr_create_dist)."""
+    col = np.ascontiguousarray(np.asarray(col_global, dtype=np.int64))
+    cnt = C.c_int64()
+    check(lib().pcg_halo_ghosts(row_begin, row_end, len(col), col.ctypes.data_as(C.c_void_p), None, 0,
+                                C.byref(cnt)), "pcg_halo_ghosts")
+    out = np.zeros(max(cnt.value, 1), dtype=np.int64)
+    check(lib().pcg_halo_ghosts(row_begin, row_end, len(col), col.ctypes.data_as(C.c_void_p),
+                                out.ctypes.data_as(C.c_void_p), cnt.value, C.byref(cnt)), "pcg_halo_ghosts")
+    return out[:cnt.value]
+
+
+def halo_recv_plan(ghosts, bounds):
+    """Per-rank ghost counts and offsets (host logic of csr_create_dist)."""
+    g = np.ascontiguousarray(np.asarray(ghosts, dtype=np.int64))
+    b = np.ascontiguousarray(np.asarray(bounds, dtype=np.int64))
+    G = len(b) - 1
+    need, off = np.zeros(G, dtype=np.int64), np.zeros(G, dtype=np.int64)
+    check(lib().pcg_halo_recv_plan(len(g), g.ctypes.data_as(C.c_void_p), G, b.ctypes.data_as(C.c_void_p),
+                                   need.ctypes.data_as(C.c_void_p), off.ctypes.data_as(C.c_void_p)),
+          "pcg_halo_recv_plan")
+    return need, off

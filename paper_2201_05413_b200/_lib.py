@@ -71,9 +71,12 @@ def lib():
         "pcg_solve_multi": [vp, i32, vp, i64, vp, i64, dbl, i64, vp, P(PcgInfo)],
         "pcg_partition_rows": [i64, vp, i32, vp],
         "pcg_comm_unique_id": [vp],
+        "pcg_halo_ghosts": [i64, i64, i64, vp, vp, i64, P(i64)],
+        "pcg_halo_recv_plan": [i64, vp, i32, vp, vp, vp],
         "pcg_comm_init": [i32, i32, vp, P(vp)],
         "pcg_comm_destroy": [vp],
         "csr_create_dist": [vp, i64, i64, i64, i64, vp, vp, vp, C.c_int, vp, P(vp)],
+        "pcg_profile_kernels": [vp, vp, i32, vp, P(dbl), P(dbl), P(i32)],
         "fem_problem_size": [P(FemSpec), P(i64), P(i64), P(i64)],
         "fem_count": [P(FemSpec), i64, i64, vp, P(i64), vp],
         "fem_assemble": [P(FemSpec), i64, i64, vp, vp, vp, vp, i64, vp],

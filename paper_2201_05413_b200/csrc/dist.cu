@@ -171,14 +171,10 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
     if (g > 0 && hb[2 * g] != hb[2 * g - 1])
       return fail(PCG_ERR_INVALID_ARG, "csr_create_dist: rank row ranges are not contiguous in rank order");
   // ---- receive lists: ghosts owned by each rank (contiguous runs of the sorted list)
-  std::vector<int64_t> need(G, 0), need_off(G, 0);
-  for (int64_t t = 0, g = 0; t < ng; t++) {
-    while (g < G && h_ghost[t] >= hb[2 * g + 1]) g++;
-    if (g >= G || h_ghost[t] < hb[2 * g])
-      return fail(PCG_ERR_INDEX_OUT_OF_RANGE, "csr_create_dist: column outside every rank's rows");
-    need[g]++;
-  }
-  for (int g = 1; g < G; g++) need_off[g] = need_off[g - 1] + need[g - 1];
+  std::vector<int64_t> bnd(G + 1), need(G, 0), need_off(G, 0);
+  for (int g = 0; g < G; g++) bnd[g] = hb[2 * g];
+  bnd[G] = hb[2 * G - 1];
+  PCG_TRY(pcg_halo_recv_plan(ng, h_ghost.data(), G, bnd.data(), need.data(), need_off.data()));
   // counts matrix M[h][g] = #rows rank h needs from rank g
   int64_t *d_M;
   PCG_CUDA(cudaMalloc(&d_M, sizeof(int64_t) * G * G));
@@ -263,6 +259,36 @@ extern "C" pcg_status pcg_partition_rows(int64_t n, const int64_t *row_ptr, int3
     bounds[g] = std::lower_bound(row_ptr, row_ptr + n + 1, target) - row_ptr;
     if (bounds[g] > n) bounds[g] = n;
   }
+  return PCG_OK;
+}
+
+extern "C" pcg_status pcg_halo_ghosts(int64_t r0, int64_t r1, int64_t nnz, const int64_t *col, int64_t *ghosts,
+                                      int64_t cap, int64_t *n_ghost) {
+  if (!n_ghost || (nnz > 0 && !col) || r1 < r0 || nnz < 0) return fail(PCG_ERR_INVALID_ARG, "pcg_halo_ghosts: bad argument");
+  std::vector<int64_t> g;
+  for (int64_t k = 0; k < nnz; k++)
+    if (col[k] < r0 || col[k] >= r1) g.push_back(col[k]);
+  std::sort(g.begin(), g.end());
+  g.erase(std::unique(g.begin(), g.end()), g.end());
+  *n_ghost = (int64_t)g.size();
+  if (ghosts)
+    for (int64_t i = 0; i < (int64_t)g.size() && i < cap; i++) ghosts[i] = g[i];
+  return PCG_OK;
+}
+
+extern "C" pcg_status pcg_halo_recv_plan(int64_t ng, const int64_t *ghosts, int32_t G, const int64_t *bounds,
+                                         int64_t *need, int64_t *need_off) {
+  if (G < 1 || !bounds || !need || !need_off || (ng > 0 && !ghosts))
+    return fail(PCG_ERR_INVALID_ARG, "pcg_halo_recv_plan: bad argument");
+  for (int g = 0; g < G; g++) need[g] = 0;
+  for (int64_t t = 0, g = 0; t < ng; t++) {
+    while (g < G && ghosts[t] >= bounds[g + 1]) g++;
+    if (g >= G || ghosts[t] < bounds[g])
+      return fail(PCG_ERR_INDEX_OUT_OF_RANGE, "pcg_halo_recv_plan: ghost column outside every rank's rows");
+    need[g]++;
+  }
+  need_off[0] = 0;
+  for (int g = 1; g < G; g++) need_off[g] = need_off[g - 1] + need[g - 1];
   return PCG_OK;
 }
 

@@ -19,8 +19,11 @@
 // 40n (K2: r, q, dinv in; r, z out) = 12 nnz + 4(n+1) + 88 n.
 // The loop runs inside ONE CUDA graph launch: a conditional WHILE node whose
 // body is {K1, K2}; the finishers clear the condition when the solve stops.
+#include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <vector>
 
 #include "matrix.cuh"
 #include "rows.cuh"
@@ -74,7 +77,76 @@ __device__ void finish_beta(Scalars *sc, double rho_new, double gamma, int use_c
 }
 
 // ---------------------------------------------------------------- K1: SpMV + p update + x update + sigma
-template <int FMT, int L>
+// SELL-32 specialisation: one warp per slice, lane = row.  The dependent-load
+// chain per slice is kept to two round trips: the own-row vectors (z_i, p_i, x_i)
+// are requested together with the slice's matrix entries, and the next slice's
+// offsets are fetched one slice ahead (software pipelining).
+template <int CH>
+__device__ __forceinline__ void k1_sell_rows(const SellView &A, double beta, double alpha_prev,
+                                             const double *__restrict__ pold, double *__restrict__ pnew,
+                                             const double *__restrict__ z, double *__restrict__ x,
+                                             double *__restrict__ q, double &acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  int64_t s = w0;
+  int64_t base = 0, next = 0;
+  if (s < A.n_slices) {
+    base = __ldg(A.slice_ptr + s);
+    next = __ldg(A.slice_ptr + s + 1);
+  }
+  for (; s < A.n_slices; s += nw) {
+    const int len = (int)((next - base) >> 5);
+    const int64_t row = s * 32 + lane;
+    const bool ok = row < A.n;
+    // prefetch the following slice's offsets
+    const int64_t s2 = s + nw;
+    int64_t base2 = 0, next2 = 0;
+    if (s2 < A.n_slices) {
+      base2 = __ldg(A.slice_ptr + s2);
+      next2 = __ldg(A.slice_ptr + s2 + 1);
+    }
+    // own-row vectors, issued with the matrix stream
+    double po = 0.0, zi = 0.0, xi = 0.0;
+    if (ok) {
+      po = __ldg(pold + row);
+      zi = __ldg(z + row);
+      xi = __ldcs(x + row);
+    }
+    const double *vp = A.val + base + lane;
+    const int *cp = A.col + base + lane;
+    double sum = 0.0;
+    for (int t = 0; t < len; t += CH) {
+      double a[CH];
+      int j[CH];
+#pragma unroll
+      for (int u = 0; u < CH; u++) {
+        if (t + u < len) {
+          a[u] = ld_stream(vp + (size_t)(t + u) * 32);
+          j[u] = ld_stream(cp + (size_t)(t + u) * 32);
+        }
+      }
+      double g[CH];
+#pragma unroll
+      for (int u = 0; u < CH; u++)
+        if (t + u < len) g[u] = __fma_rn(beta, __ldg(pold + j[u]), __ldg(z + j[u]));
+#pragma unroll
+      for (int u = 0; u < CH; u++)
+        if (t + u < len) sum = __fma_rn(a[u], g[u], sum);
+    }
+    if (ok) {
+      const double pi = __fma_rn(beta, po, zi);
+      __stcs(pnew + row, pi);
+      __stcs(q + row, sum);
+      __stcs(x + row, __fma_rn(alpha_prev, po, xi));
+      acc = __fma_rn(pi, sum, acc);
+    }
+    base = base2;
+    next = next2;
+  }
+}
+
+template <int FMT, int L, int CH = 8>
 __global__ void __launch_bounds__(BLOCK) k1_kernel(SellView S, CsrView C, int64_t n_ghost, Vecs v,
                                                    Scalars *sc, double *partials, int dist,
                                                    int use_cond, cudaGraphConditionalHandle h) {
@@ -92,17 +164,20 @@ __global__ void __launch_bounds__(BLOCK) k1_kernel(SellView S, CsrView C, int64_
   double *__restrict__ x = v.x;
   double *__restrict__ q = v.q;
   double acc = 0.0;
-  auto gather = [&](int j) { return __fma_rn(beta, __ldg(pold + j), __ldg(z + j)); };
-  auto epi = [&](int64_t i, double s) {
-    const double po = pold[i];
-    const double pi = __fma_rn(beta, po, z[i]);
-    pnew[i] = pi;
-    q[i] = s;
-    x[i] = __fma_rn(alpha_prev, po, x[i]);
-    acc = __fma_rn(pi, s, acc);
-  };
-  if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
-  else csr_rows<L>(C, gather, epi);
+  if (FMT == PCG_FORMAT_SELL) {
+    k1_sell_rows<CH>(S, beta, alpha_prev, pold, pnew, z, x, q, acc);
+  } else {
+    auto gather = [&](int j) { return __fma_rn(beta, __ldg(pold + j), __ldg(z + j)); };
+    auto epi = [&](int64_t i, double s) {
+      const double po = pold[i];
+      const double pi = __fma_rn(beta, po, z[i]);
+      pnew[i] = pi;
+      q[i] = s;
+      x[i] = __fma_rn(alpha_prev, po, x[i]);
+      acc = __fma_rn(pi, s, acc);
+    };
+    csr_rows<L>(C, gather, epi);
+  }
   // ghost copies of p advance by the same recurrence (bitwise equal to the owner's)
   if (n_ghost) {
     const int64_t n = FMT == PCG_FORMAT_SELL ? S.n : C.n;
@@ -333,12 +408,24 @@ pcg_status launch_spmv(pcg_matrix *A, const double *x, double *y, cudaStream_t s
   return launch_spmv_fmt(A, A->format, x, y, st);
 }
 
+static int k1_chunk() {  // tuning knob (PCG_K1_CHUNK=4|8), default 8
+  static int c = [] {
+    const char *e = getenv("PCG_K1_CHUNK");
+    return (e && atoi(e) == 4) ? 4 : 8;
+  }();
+  return c;
+}
+
 static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
   Vecs v = vecs_of(A);
   SolveWork &w = A->work;
-  PCG_DISPATCH(A->format, A->csr_lanes, k1_kernel,
-               <<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
-                                                A->comm ? 1 : 0, use_cond, h));
+  if (A->format == PCG_FORMAT_SELL && k1_chunk() == 4)
+    k1_kernel<PCG_FORMAT_SELL, 1, 4><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc,
+                                                                     w.partials, A->comm ? 1 : 0, use_cond, h);
+  else
+    PCG_DISPATCH(A->format, A->csr_lanes, k1_kernel,
+                 <<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
+                                                  A->comm ? 1 : 0, use_cond, h));
   count_launch();
   PCG_CUDA(cudaGetLastError());
   if (A->comm) {
@@ -539,9 +626,16 @@ using namespace pcgb;
 
 extern "C" pcg_status pcg_solve(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
                                 void *stream, pcg_info *info) {
-  if (!A || !b || !x) return fail(PCG_ERR_INVALID_ARG, "pcg_solve: null argument");
+  if (!A || ((!b || !x) && A->n > 0)) return fail(PCG_ERR_INVALID_ARG, "pcg_solve: null argument");
   if (!(tol > 0.0)) return fail(PCG_ERR_INVALID_ARG, "pcg_solve: tol must be > 0");
   if (max_iter < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_solve: max_iter must be >= 1");
+  if (A->n == 0 && !A->comm) {  // empty system: b = 0, nothing to do
+    if (info) {
+      memset(info, 0, sizeof(*info));
+      info->converged = 1;
+    }
+    return PCG_OK;
+  }
   std::lock_guard<std::mutex> lk(A->mu);
   PCG_CUDA(cudaSetDevice(A->device));
   return solve_impl(A, b, x, tol, max_iter, (cudaStream_t)stream, info);
@@ -573,7 +667,8 @@ int k1_blocks_per_sm(int fmt, int lanes) {
   int b = 0;
   cudaError_t e;
   if (fmt == PCG_FORMAT_SELL) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_SELL, 1>, BLOCK, 0);
+    e = k1_chunk() == 4 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_SELL, 1, 4>, BLOCK, 0)
+                        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_SELL, 1, 8>, BLOCK, 0);
   } else {
     switch (lanes) {
       case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_CSR, 1>, BLOCK, 0); break;
@@ -591,3 +686,47 @@ int k1_blocks_per_sm(int fmt, int lanes) {
   return b < 1 ? 1 : (b > 8 ? 8 : b);
 }
 }  // namespace pcgb
+
+extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32_t reps, void *stream, double *us_k1,
+                                          double *us_k2, int32_t *reps_done) {
+  if (!A || !b || !us_k1 || !us_k2 || reps < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_profile_kernels: bad argument");
+  if (A->comm) return fail(PCG_ERR_INVALID_ARG, "pcg_profile_kernels: single-GPU handles only");
+  if (!is_device_ptr(b)) return fail(PCG_ERR_INVALID_ARG, "pcg_profile_kernels: b must be a device pointer");
+  std::lock_guard<std::mutex> lk(A->mu);
+  PCG_CUDA(cudaSetDevice(A->device));
+  PCG_TRY(ensure_work(A));
+  cudaStream_t st = (cudaStream_t)stream;
+  SolveWork &w = A->work;
+  PCG_CUDA(cudaMemsetAsync(w.x, 0, sizeof(double) * A->n, st));
+  Scalars *h = w.h_sc;
+  memset(h, 0, sizeof(Scalars));
+  h->tol = 1e-300;  // never stops on the residual inside the profiled window
+  h->max_iter = (long long)reps + 1;
+  PCG_CUDA(cudaMemcpyAsync(w.sc, h, sizeof(Scalars), cudaMemcpyHostToDevice, st));
+  PCG_TRY(launch_resid(A, b, MODE_INIT, st));
+  std::vector<cudaEvent_t> ev(2 * (size_t)reps + 1);
+  for (auto &e : ev) PCG_CUDA(cudaEventCreate(&e));
+  PCG_CUDA(cudaEventRecord(ev[0], st));
+  for (int r = 0; r < reps; r++) {
+    PCG_TRY(launch_k1(A, st, 0, 0));
+    PCG_CUDA(cudaEventRecord(ev[2 * r + 1], st));
+    PCG_TRY(launch_k2(A, st, 0, 0));
+    PCG_CUDA(cudaEventRecord(ev[2 * r + 2], st));
+  }
+  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_CUDA(cudaMemcpy(h, w.sc, sizeof(Scalars), cudaMemcpyDeviceToHost));
+  const int done = (int)std::min<long long>(h->k, reps);
+  double t1 = 0, t2 = 0;
+  for (int r = 0; r < done; r++) {
+    float a = 0, b2 = 0;
+    cudaEventElapsedTime(&a, ev[2 * r], ev[2 * r + 1]);
+    cudaEventElapsedTime(&b2, ev[2 * r + 1], ev[2 * r + 2]);
+    t1 += a;
+    t2 += b2;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+  *us_k1 = done ? t1 * 1e3 / done : 0.0;
+  *us_k2 = done ? t2 * 1e3 / done : 0.0;
+  if (reps_done) *reps_done = done;
+  return PCG_OK;
+}
