@@ -285,22 +285,31 @@ def main():
     k_us = None
     if world == 1:
         import ctypes as C
-        us1, us2, done = C.c_double(), C.c_double(), C.c_int32()
+        us = (C.c_double * 3)()
+        done = C.c_int32()
         pcg.check(pcg.lib().pcg_profile_kernels(A._h, C.c_void_p(b.data_ptr()), 20,
-                                                 C.c_void_p(torch.cuda.current_stream().cuda_stream),
-                                                 C.byref(us1), C.byref(us2), C.byref(done)), "pcg_profile_kernels")
-        k1_bytes = 12.0 * nnz + 4.0 * (n + 1) + 48.0 * n
-        k2_bytes = 40.0 * n
-        achieved = k1_bytes / (us1.value * 1e-6) / 1e9
-        roof = {"bound": "hbm", "kernel": "k1_kernel (SpMV + p/x updates + sigma, fused)",
-                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "peak_source": peak_kind, "traffic": None,
-                "bytes_per_launch": k1_bytes, "us_per_launch": us1.value,
-                "k2": {"bytes_per_launch": k2_bytes, "us_per_launch": us2.value,
-                       "achieved": k2_bytes / (us2.value * 1e-6) / 1e9},
-                "iteration": {"bytes": iter_bytes(n, nnz), "us": us1.value + us2.value,
-                              "frac": iter_bytes(n, nnz) / ((us1.value + us2.value) * 1e-6) / 1e9 / hbm}}
-        k_us = (us1.value, us2.value)
+                                                 C.c_void_p(torch.cuda.current_stream().cuda_stream), us,
+                                                 C.byref(done)), "pcg_profile_kernels")
+        mat = 12.0 * nnz + 4.0 * (n + 1)
+        if stats["schedule"] == 3:
+            names = ["k1a_kernel (p = z + beta p, x += alpha p_old; streaming)",
+                     "k1b_kernel (SpMV q = A p + sigma = p.q, grid finish -> alpha)",
+                     "k2_kernel (r -= alpha q, z = dinv r, rho', gamma, grid finish -> beta)"]
+            byts = [40.0 * n, mat + 16.0 * n, 40.0 * n]
+        else:
+            names = ["-", "k1_kernel (fused SpMV + p/x updates + sigma)", "k2_kernel (r/z updates + dots)"]
+            byts = [0.0, mat + 48.0 * n, 40.0 * n]
+        kern = [{"kernel": nm, "bytes_per_launch": bt, "us_per_launch": u, "achieved_GBps": bt / u / 1e3 if u else None}
+                for nm, bt, u in zip(names, byts, us) if bt]
+        dom = max(kern, key=lambda d: d["us_per_launch"])
+        it_us = sum(us)
+        roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved_GBps"], "peak": hbm,
+                "unit": "GB/s", "frac": dom["achieved_GBps"] / hbm, "peak_source": peak_kind, "traffic": None,
+                "bytes_per_launch": dom["bytes_per_launch"], "us_per_launch": dom["us_per_launch"],
+                "kernels": kern, "schedule": stats["schedule"],
+                "iteration": {"bytes": sum(byts), "us": it_us, "frac": sum(byts) / it_us / 1e3 / hbm,
+                              "frac_vs_88n_ideal": (mat + 88.0 * n) / it_us / 1e3 / hbm}}
+        k_us = list(us)
         xs = torch.ones(n, dtype=torch.float64, device="cuda")
         ys = torch.empty_like(xs)
         for _ in range(3):
@@ -339,7 +348,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(workload_config(args.config, c, n, nnz, world), iterations=iters,
-                           format={1: "csr", 2: "sell"}[stats["format"]], setup_s=round(t_setup, 3),
+                           format={1: "csr", 2: "sell", 3: "sell_tma"}[stats["format"]], setup_s=round(t_setup, 3),
                            relres_true=infos[-1]["relres_true"]),
             "throughput": {"cg_iterations_per_s": iters / (ms / 1e3),
                            "effective_GBps": iter_bytes(n, nnz) * iters / (ms / 1e3) / 1e9,

@@ -55,10 +55,12 @@ typedef enum {
 #define PCG_FMT_AUTO 0x00  /* pick the faster device format, measured */
 #define PCG_FMT_CSR 0x10   /* force CSR (sub-warp per row)            */
 #define PCG_FMT_SELL 0x20  /* force SELL-32 (slices of 32 rows)       */
+#define PCG_FMT_SELL_TMA 0x30 /* force SELL-32 with TMA-staged tiles  */
 
 /* format codes reported by pcg_matrix_stats.format */
 #define PCG_FORMAT_CSR 1
 #define PCG_FORMAT_SELL 2
+#define PCG_FORMAT_SELL_TMA 3 /* SELL-32, matrix tiles staged in shared memory by TMA bulk copies */
 
 typedef struct pcg_matrix *pcg_matrix_t;
 typedef struct pcg_comm *pcg_comm_t;
@@ -85,6 +87,10 @@ typedef struct {
   double spmv_us_csr, spmv_us_sell; /* autotune timings (0 if not measured)   */
   int64_t n_ghost;           /* distributed: halo size (0 on one GPU)         */
   int64_t row_begin, row_end, n_global;
+  double spmv_us_tma;        /* autotune timing of the TMA-staged SELL kernels */
+  int64_t stage_entries;     /* TMA stage size in entries (0 = unavailable)   */
+  int32_t stages;            /* TMA ring depth                                */
+  int32_t schedule;          /* passes per iteration: 3 (K1a,K1b,K2) or 2 (fused K1,K2) */
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */
@@ -154,11 +160,12 @@ const char *pcg_last_error(void);
 const char *pcg_status_string(pcg_status s);
 /* Per-kernel timing for the roofline (bench/profiling only): runs the init pass on b
  * (device pointer, x0 = 0), then `reps` PCG iterations launched one kernel at a time
- * with CUDA events around each fused pass on `stream`.  Writes the mean device time
- * of K1 (SpMV + p/x updates + sigma) and K2 (r/z updates + dots) in microseconds.
+ * with CUDA events between the passes on `stream`.  us[0..2] = mean device time in
+ * microseconds of: K1a (streaming p/x update; 0 under the fused schedule), K1b (SpMV
+ * + sigma; the fused K1 under schedule 2), K2 (r/z updates + dots).
  * Single-GPU handles only; stops early (fewer reps) if the solve converges. */
-pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32_t reps, void *stream, double *us_k1,
-                               double *us_k2, int32_t *reps_done);
+pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32_t reps, void *stream, double *us,
+                               int32_t *reps_done);
 
 /* number of kernels this library launched in the calling process (monotone counter,
  * for launch accounting in benchmarks) */

@@ -90,7 +90,14 @@ struct SellView {
   const int64_t *slice_ptr; // n_slices+1, entry offsets (multiple of 32)
   const int *col;          // [slice][t][lane]
   const double *val;
+  int stages;              // TMA-staged variant: shared-memory ring depth
+  int64_t stage_entries;   // ... and the largest tile (8 slices) in entries
+  const int *lead;         // per tile: max column referenced by tiles 0..t (prefix max)
+  int zero;                // always 0 at run time; opaque to the compiler (see cols_ready)
 };
+
+// internal format code of the TMA-staged SELL kernels (reported as PCG_FORMAT_SELL_TMA)
+constexpr int FMT_SELL_TMA = 3;
 
 // ------------------------------------------------------------------ reductions
 constexpr int BLOCK = 256;

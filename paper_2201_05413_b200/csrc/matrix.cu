@@ -8,11 +8,15 @@
 // thread per row; the first offending row is reported.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
+#include <vector>
 #include <cmath>
 #include <cstring>
 
 #include "matrix.cuh"
+#include "staged.cuh"
 
 namespace pcgb {
 
@@ -136,6 +140,25 @@ __global__ void sell_fill_kernel(int64_t n, int64_t n_slices, const int *__restr
   }
 }
 
+// per tile (WARPS slices): the largest column any entry references
+__global__ void tile_lead_kernel(int64_t n_slices, const int64_t *__restrict__ slice_ptr, const int *__restrict__ scol,
+                                 int *__restrict__ lead) {
+  const int64_t t = blockIdx.x;
+  int64_t s1 = (t + 1) * WARPS;
+  if (s1 > n_slices) s1 = n_slices;
+  const int64_t lo = slice_ptr[t * WARPS], hi = slice_ptr[s1];
+  int m = 0;
+  for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) m = max(m, scol[e]);
+  __shared__ int sm[256];
+  sm[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sm[threadIdx.x] = max(sm[threadIdx.x], sm[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) lead[t] = sm[0];
+}
+
 int num_sms(int device) {
   int v = 0;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
@@ -144,7 +167,8 @@ int num_sms(int device) {
 
 // declared in solver.cu
 pcg_status launch_spmv_fmt(pcg_matrix *A, int fmt, const double *x, double *y, cudaStream_t st);
-int k1_blocks_per_sm(int fmt, int lanes);
+int k1_blocks_per_sm(int fmt, int lanes, size_t smem);
+pcg_status prepare_staged(size_t smem);
 
 static pcg_status error_from_flags(const ErrInfo &e, int64_t row_offset) {
   static const struct {
@@ -242,47 +266,101 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
   int L = 1;
   while (L < 32 && L * 4 < mean) L <<= 1;
   A->csr_lanes = L;
+  // ---- TMA-staged SELL: largest tile (WARPS slices) sets the shared-memory stage size
+  A->stage_entries = 0;
+  if (want_sell && A->n_slices > 0) {
+    std::vector<int64_t> sp(A->n_slices + 1);
+    PCG_CUDA(cudaMemcpy(sp.data(), A->d_slice_ptr, sizeof(int64_t) * sp.size(), cudaMemcpyDeviceToHost));
+    int64_t mx = 0;
+    for (int64_t t = 0; t * WARPS < A->n_slices; t++)
+      mx = std::max(mx, sp[std::min<int64_t>((t + 1) * WARPS, A->n_slices)] - sp[t * WARPS]);
+    const char *e = getenv("PCG_STAGES");
+    A->stages = e ? std::max(1, std::min(4, atoi(e))) : 2;
+    A->stage_entries = mx;
+    const size_t smem = staged_smem_bytes(SellStage(A->stages, mx));
+    if (smem > 200 * 1024 || mx == 0) {
+      A->stage_entries = 0;
+    } else {
+      PCG_TRY(prepare_staged(smem));
+      // prefix-max lead column per tile -> L2 prefetch windows
+      const int64_t nt = (A->n_slices + WARPS - 1) / WARPS;
+      PCG_CUDA(cudaMalloc(&A->d_lead, sizeof(int) * nt));
+      tile_lead_kernel<<<(unsigned)nt, 256, 0, st>>>(A->n_slices, A->d_slice_ptr, A->d_scol, A->d_lead);
+      count_launch();
+      std::vector<int> ld(nt);
+      PCG_CUDA(cudaMemcpyAsync(ld.data(), A->d_lead, sizeof(int) * nt, cudaMemcpyDeviceToHost, st));
+      PCG_CUDA(cudaStreamSynchronize(st));
+      for (int64_t t = 1; t < nt; t++) ld[t] = std::max(ld[t], ld[t - 1]);
+      PCG_CUDA(cudaMemcpy(A->d_lead, ld.data(), sizeof(int) * nt, cudaMemcpyHostToDevice));
+      if (getenv("PCG_NO_L2PF")) {  // tuning knob: disable the L2 prefetch windows
+        cudaFree(A->d_lead);
+        A->d_lead = nullptr;
+      }
+    }
+  }
   // ---- launch geometry: persistent grids, a multiple of the SM count
   const int sms = num_sms(A->device);
-  A->format = want_sell ? PCG_FORMAT_SELL : PCG_FORMAT_CSR;
-  auto grid_for = [&](int fmt) {
-    int bps = k1_blocks_per_sm(fmt, A->csr_lanes);
+  auto configure = [&](int fmt) {
+    A->format = fmt;
+    A->dyn_smem = fmt == FMT_SELL_TMA ? staged_smem_bytes(SellStage(A->stages, A->stage_entries)) : 0;
+    int bps = k1_blocks_per_sm(fmt, A->csr_lanes, A->dyn_smem);
     int64_t g = (int64_t)sms * (bps > 0 ? bps : 1);
-    int64_t need = fmt == PCG_FORMAT_SELL ? (A->n_slices + WARPS - 1) / WARPS
-                                          : (n * A->csr_lanes + BLOCK - 1) / BLOCK;
+    int64_t need = fmt == FMT_SELL_TMA   ? (A->n_slices + WARPS - 1) / WARPS
+                   : fmt == PCG_FORMAT_SELL ? (A->n_slices + WARPS - 1) / WARPS
+                                            : (n * A->csr_lanes + BLOCK - 1) / BLOCK;
     if (need < 1) need = 1;
-    return (int)(g < need ? g : need);
+    A->grid_spmv = (int)(g < need ? g : need);
   };
   const int64_t need_vec = (n / 2 + BLOCK - 1) / BLOCK;
   A->grid_vec = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 8, need_vec));
-  // ---- measured format choice (PCG_FMT_AUTO with both formats available)
-  if (fmt_req == PCG_FMT_AUTO && want_sell && n > 0) {
+  std::vector<int> cands;
+  if (fmt_req == PCG_FMT_CSR || !want_sell) cands = {PCG_FORMAT_CSR};
+  else if (fmt_req == PCG_FMT_SELL) cands = {PCG_FORMAT_SELL};
+  else if (fmt_req == PCG_FMT_SELL_TMA) {
+    if (!A->stage_entries) return fail(PCG_ERR_INVALID_ARG, "csr_create: TMA-staged SELL unavailable for this matrix");
+    cands = {FMT_SELL_TMA};
+  } else {
+    cands = {PCG_FORMAT_CSR, PCG_FORMAT_SELL};
+    if (A->stage_entries) cands.push_back(FMT_SELL_TMA);
+  }
+  // ---- measured format choice (time 5 SpMVs of each candidate)
+  if (cands.size() > 1 && n > 0) {
     PCG_TRY(ensure_work(A));
     double *x = A->work.stage_x, *y = A->work.w;
     PCG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (n + A->n_ghost), st));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    float best[3] = {0, 0, 0};
-    for (int fmt : {PCG_FORMAT_CSR, PCG_FORMAT_SELL}) {
-      A->grid_spmv = grid_for(fmt);
+    float best = 1e30f;
+    int best_fmt = cands[0];
+    for (int fmt : cands) {
+      configure(fmt);
       PCG_TRY(launch_spmv_fmt(A, fmt, x, y, st));  // warm-up
       cudaEventRecord(e0, st);
       for (int r = 0; r < 5; r++) PCG_TRY(launch_spmv_fmt(A, fmt, x, y, st));
       cudaEventRecord(e1, st);
       PCG_CUDA(cudaEventSynchronize(e1));
-      cudaEventElapsedTime(&best[fmt], e0, e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (fmt == PCG_FORMAT_CSR) A->spmv_us_csr = ms * 1e3 / 5;
+      else if (fmt == PCG_FORMAT_SELL) A->spmv_us_sell = ms * 1e3 / 5;
+      else A->spmv_us_tma = ms * 1e3 / 5;
+      if (ms < best) {
+        best = ms;
+        best_fmt = fmt;
+      }
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    A->spmv_us_csr = best[PCG_FORMAT_CSR] * 1e3 / 5;
-    A->spmv_us_sell = best[PCG_FORMAT_SELL] * 1e3 / 5;
-    A->format = best[PCG_FORMAT_SELL] <= best[PCG_FORMAT_CSR] ? PCG_FORMAT_SELL : PCG_FORMAT_CSR;
+    configure(best_fmt);
+  } else {
+    configure(cands[0]);
   }
-  A->grid_spmv = grid_for(A->format);
-  if (A->work.graph_ready) {  // geometry changed after a provisional workspace: rebuild
-    free_work(A);
+  {
+    const char *sch = getenv("PCG_SCHEDULE");
+    A->schedule = (sch && atoi(sch) == 2) ? 2 : 3;
   }
+  if (A->work.graph_ready) free_work(A);  // geometry changed after a provisional workspace
   A->device_bytes = (double)(n + 1) * 4 + (double)nnz * 12 + (double)n * 8 +
                     (A->d_slice_ptr ? (double)(A->n_slices + 1) * 8 + (double)A->sell_entries * 12 : 0);
   return PCG_OK;
@@ -332,8 +410,9 @@ pcg_status csr_create_impl(int64_t n, int64_t nnz, const int64_t *row_ptr, const
 pcg_status ensure_work(pcg_matrix *A) {
   SolveWork &w = A->work;
   if (w.sc) return PCG_OK;
+  // +64 entries of padding: TMA tile copies round row counts up to 16-B multiples
   const size_t n = (size_t)A->n, ng = (size_t)(A->n + A->n_ghost);
-  const size_t nb = sizeof(double) * (n > 0 ? n : 1), ngb = sizeof(double) * (ng > 0 ? ng : 1);
+  const size_t nb = sizeof(double) * (n + 64), ngb = sizeof(double) * (ng + 64);
   PCG_CUDA(cudaMalloc(&w.r, nb));
   PCG_CUDA(cudaMalloc(&w.z, ngb));
   PCG_CUDA(cudaMalloc(&w.q, nb));
@@ -408,7 +487,7 @@ extern "C" pcg_status csr_destroy(pcg_matrix_t A) {
   cudaDeviceSynchronize();
   free_work(A);
   for (void *p : {(void *)A->d_row_ptr, (void *)A->d_col, (void *)A->d_val, (void *)A->d_dinv,
-                  (void *)A->d_slice_ptr, (void *)A->d_scol, (void *)A->d_sval, (void *)A->halo.d_send_idx,
+                  (void *)A->d_slice_ptr, (void *)A->d_scol, (void *)A->d_sval, (void *)A->d_lead, (void *)A->halo.d_send_idx,
                   (void *)A->halo.d_send_buf})
     if (p) cudaFree(p);
   delete A;
@@ -427,6 +506,10 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->device_bytes = A->device_bytes;
   o->spmv_us_csr = A->spmv_us_csr;
   o->spmv_us_sell = A->spmv_us_sell;
+  o->spmv_us_tma = A->spmv_us_tma;
+  o->stage_entries = A->stage_entries;
+  o->stages = A->stages;
+  o->schedule = A->schedule;
   o->n_ghost = A->n_ghost;
   o->row_begin = A->row_begin;
   o->row_end = A->row_end;

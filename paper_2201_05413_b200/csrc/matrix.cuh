@@ -66,9 +66,10 @@ struct pcg_matrix {
   double *d_sval = nullptr;
   // CSR kernel lanes per row
   int csr_lanes = 4;
+  int schedule = 3;  // 3: K1a + K1b + K2 (96n B), 2: fused K1 + K2 (88n B)
   // launch geometry
   int grid_vec = 0, grid_spmv = 0;  // persistent grid sizes (multiples of the SM count)
-  double t_setup_s = 0, spmv_us_csr = 0, spmv_us_sell = 0;
+  double t_setup_s = 0, spmv_us_csr = 0, spmv_us_sell = 0, spmv_us_tma = 0;
   double device_bytes = 0;
   // distributed
   pcg_comm *comm = nullptr;
@@ -78,7 +79,11 @@ struct pcg_matrix {
   pcgb::SolveWork work;
   std::mutex mu;
   pcgb::CsrView csr() const { return {n, n + n_ghost, d_row_ptr, d_col, d_val}; }
-  pcgb::SellView sell() const { return {n, n_slices, d_slice_ptr, d_scol, d_sval}; }
+  int stages = 2;
+  int64_t stage_entries = 0;  // 0: TMA-staged SELL unavailable
+  size_t dyn_smem = 0;        // dynamic shared memory of the chosen format's kernels
+  int *d_lead = nullptr;      // per-tile prefix-max column (TMA L2 prefetch windows)
+  pcgb::SellView sell() const { return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0}; }
 };
 
 namespace pcgb {

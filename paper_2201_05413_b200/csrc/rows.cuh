@@ -10,6 +10,17 @@
 
 namespace pcgb {
 
+// Ordering fence for the SELL loops.  Left alone, the SASS scheduler may emit
+// col[u] -> gather[u] -> col[u+1] -> ..., serialising one DRAM round trip per
+// entry.  Making every gather index depend on ALL column ids of the chunk
+// (j |= xor(j) & zero, with `zero` a run-time 0 the compiler cannot fold) forces
+// all column loads to be issued before the first gather address exists.
+__device__ __forceinline__ void cols_ready(int (&j)[8], int zero) {
+  const int x = (j[0] ^ j[1] ^ j[2] ^ j[3] ^ j[4] ^ j[5] ^ j[6] ^ j[7]) & zero;
+#pragma unroll
+  for (int u = 0; u < 8; u++) j[u] |= x;
+}
+
 // SELL-32: one warp per slice of 32 consecutive rows, lane = row.  Entries of a
 // slice are stored [t][lane] so every load of the t-th entry is one 256-B (val)
 // or 128-B (col) coalesced transaction.  Loads are issued 8 entries at a time
@@ -28,7 +39,7 @@ __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi 
     double sum = 0.0;
     for (int t = 0; t < len; t += 8) {
       double a[8];
-      int j[8];
+      int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
       for (int u = 0; u < 8; u++) {
         if (t + u < len) {
@@ -36,6 +47,7 @@ __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi 
           j[u] = ld_stream(cp + (size_t)(t + u) * 32);
         }
       }
+      cols_ready(j, A.zero);
       double g[8];
 #pragma unroll
       for (int u = 0; u < 8; u++)

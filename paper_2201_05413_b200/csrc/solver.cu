@@ -27,6 +27,7 @@
 
 #include "matrix.cuh"
 #include "rows.cuh"
+#include "staged.cuh"
 
 namespace pcgb {
 
@@ -42,7 +43,7 @@ __device__ __forceinline__ void stop_loop(int use_cond, cudaGraphConditionalHand
 }
 
 // ---------------------------------------------------------------- finishers
-__device__ void finish_alpha(Scalars *sc, double sigma, int use_cond, cudaGraphConditionalHandle h) {
+__device__ void finish_alpha(Scalars *sc, double sigma, int use_cond, cudaGraphConditionalHandle h, int flip = 1) {
   sc->sigma = sigma;
   if (!(sigma > 0.0)) {  // p^T A p <= 0 (or NaN): CG breakdown, A not SPD
     sc->done = DONE_BREAKDOWN;
@@ -50,7 +51,7 @@ __device__ void finish_alpha(Scalars *sc, double sigma, int use_cond, cudaGraphC
   } else {
     sc->alpha = sc->rho / sigma;
     sc->k += 1;
-    sc->parity ^= 1;
+    sc->parity ^= flip;
   }
   sc->graph_launches += use_cond;
 }
@@ -118,7 +119,7 @@ __device__ __forceinline__ void k1_sell_rows(const SellView &A, double beta, dou
     double sum = 0.0;
     for (int t = 0; t < len; t += CH) {
       double a[CH];
-      int j[CH];
+      int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
       for (int u = 0; u < CH; u++) {
         if (t + u < len) {
@@ -126,6 +127,7 @@ __device__ __forceinline__ void k1_sell_rows(const SellView &A, double beta, dou
           j[u] = ld_stream(cp + (size_t)(t + u) * 32);
         }
       }
+      cols_ready(j, A.zero);
       double g[CH];
 #pragma unroll
       for (int u = 0; u < CH; u++)
@@ -164,7 +166,26 @@ __global__ void __launch_bounds__(BLOCK) k1_kernel(SellView S, CsrView C, int64_
   double *__restrict__ x = v.x;
   double *__restrict__ q = v.q;
   double acc = 0.0;
-  if (FMT == PCG_FORMAT_SELL) {
+  if (FMT == FMT_SELL_TMA) {
+    struct Own {
+      double po, zi;
+    };
+    StageIO<1, 2> io;
+    io.own[0] = x;
+    io.pf[0] = pold;
+    io.pf[1] = z;
+    io.pf_len = S.n + n_ghost;
+    auto pre = [&](int64_t i) { return Own{__ldg(pold + i), __ldg(z + i)}; };
+    auto gather = [&](int j) { return __fma_rn(beta, __ldg(pold + j), __ldg(z + j)); };
+    auto epi = [&](int64_t i, double s, const Own &o, const double *own) {
+      const double pi = __fma_rn(beta, o.po, o.zi);
+      __stcs(pnew + i, pi);
+      __stcs(q + i, s);
+      __stcs(x + i, __fma_rn(alpha_prev, o.po, own[0]));
+      acc = __fma_rn(pi, s, acc);
+    };
+    sell_staged_rows<CH>(S, io, pre, gather, epi);
+  } else if (FMT == PCG_FORMAT_SELL) {
     k1_sell_rows<CH>(S, beta, alpha_prev, pold, pnew, z, x, q, acc);
   } else {
     auto gather = [&](int j) { return __fma_rn(beta, __ldg(pold + j), __ldg(z + j)); };
@@ -180,7 +201,7 @@ __global__ void __launch_bounds__(BLOCK) k1_kernel(SellView S, CsrView C, int64_
   }
   // ghost copies of p advance by the same recurrence (bitwise equal to the owner's)
   if (n_ghost) {
-    const int64_t n = FMT == PCG_FORMAT_SELL ? S.n : C.n;
+    const int64_t n = FMT != PCG_FORMAT_CSR ? S.n : C.n;
     for (int64_t g = (int64_t)blockIdx.x * BLOCK + threadIdx.x; g < n_ghost; g += (int64_t)gridDim.x * BLOCK)
       pnew[n + g] = __fma_rn(beta, pold[n + g], z[n + g]);
   }
@@ -257,10 +278,92 @@ __global__ void __launch_bounds__(BLOCK) k2_kernel(int64_t n, Vecs v, Scalars *s
   }
 }
 
+// ---------------------------------------------------------------- 3-pass schedule
+// K1a (streaming): p = z + beta p ; x += alpha_prev p_old   (reads z, p, x; writes p, x: 40n B)
+// K1b (SpMV):      q = A p ; sigma = p.q -> alpha           (matrix + 16n B)
+// K2  (as above):  r, z updates + rho', gamma -> beta       (40n B)
+// 96n + matrix bytes per iteration, every pass a plain streaming or SpMV pass.
+__global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, Vecs v, Scalars *sc, int use_cond,
+                                                    cudaGraphConditionalHandle h) {
+  const volatile Scalars *vs = sc;
+  if (vs->done != DONE_RUNNING) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) stop_loop(use_cond, h);
+    return;
+  }
+  const double beta = vs->beta, alpha_prev = vs->alpha;
+  double *__restrict__ p = v.p0;
+  const int64_t npair = n >> 1;
+  const double2 *__restrict__ z2 = reinterpret_cast<const double2 *>(v.z);
+  double2 *__restrict__ p2 = reinterpret_cast<double2 *>(p);
+  double2 *__restrict__ x2 = reinterpret_cast<double2 *>(v.x);
+  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < npair; i += (int64_t)gridDim.x * BLOCK) {
+    const double2 zz = __ldcs(z2 + i), po = p2[i];
+    double2 xx = __ldcs(x2 + i);
+    xx.x = __fma_rn(alpha_prev, po.x, xx.x);
+    xx.y = __fma_rn(alpha_prev, po.y, xx.y);
+    p2[i] = make_double2(__fma_rn(beta, po.x, zz.x), __fma_rn(beta, po.y, zz.y));
+    __stcs(x2 + i, xx);
+  }
+  const int64_t t = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+  if ((n & 1) && t == 0) {
+    const double po = p[n - 1];
+    v.x[n - 1] = __fma_rn(alpha_prev, po, v.x[n - 1]);
+    p[n - 1] = __fma_rn(beta, po, v.z[n - 1]);
+  }
+  for (int64_t g = t; g < n_ghost; g += (int64_t)gridDim.x * BLOCK) p[n + g] = __fma_rn(beta, p[n + g], v.z[n + g]);
+}
+
+template <int FMT, int L>
+__global__ void __launch_bounds__(BLOCK) k1b_kernel(SellView S, CsrView C, int64_t n_ghost, Vecs v, Scalars *sc,
+                                                    double *partials, int dist, int use_cond,
+                                                    cudaGraphConditionalHandle h) {
+  __shared__ double sm[1][WARPS];
+  const volatile Scalars *vs = sc;
+  if (vs->done != DONE_RUNNING) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) stop_loop(use_cond, h);
+    return;
+  }
+  const double *__restrict__ p = v.p0;
+  double *__restrict__ q = v.q;
+  double acc = 0.0;
+  auto gather = [&](int j) { return __ldg(p + j); };
+  auto epi = [&](int64_t i, double s) {
+    __stcs(q + i, s);
+    acc = __fma_rn(__ldg(p + i), s, acc);
+  };
+  if (FMT == FMT_SELL_TMA) {
+    StageIO<0, 1> io;
+    io.pf[0] = p;
+    io.pf_len = S.n + n_ghost;
+    auto pre = [&](int64_t) { return 0; };
+    auto epi2 = [&](int64_t i, double s, int, const double *) { epi(i, s); };
+    sell_staged_rows<8>(S, io, pre, gather, epi2);
+  } else if (FMT == PCG_FORMAT_SELL) {
+    sell_rows(S, gather, epi);
+  } else {
+    csr_rows<L>(C, gather, epi);
+  }
+  double red[1] = {acc};
+  block_sum<1>(red, sm);
+  if (publish_and_arrive<1>(red, partials, &sc->cnt_a)) {
+    double tot[1];
+    reduce_partials<1>(partials, tot, sm);
+    if (threadIdx.x == 0) {
+      sc->cnt_a = 0;
+      if (dist) {
+        sc->sigma = tot[0];
+        sc->graph_launches += use_cond;
+      } else {
+        finish_alpha(sc, tot[0], use_cond, h, 0);
+      }
+    }
+  }
+}
+
 // distributed finishers (after the NCCL allreduce of the partials)
-__global__ void finish_alpha_kernel(Scalars *sc, int use_cond, cudaGraphConditionalHandle h) {
+__global__ void finish_alpha_kernel(Scalars *sc, int use_cond, cudaGraphConditionalHandle h, int flip) {
   if (sc->done != DONE_RUNNING) return;
-  finish_alpha(sc, sc->sigma, use_cond, h);
+  finish_alpha(sc, sc->sigma, use_cond, h, flip);
 }
 __global__ void finish_beta_kernel(Scalars *sc, int use_cond, cudaGraphConditionalHandle h) {
   if (sc->done != DONE_RUNNING) return;
@@ -290,10 +393,20 @@ __global__ void __launch_bounds__(BLOCK) resid_kernel(SellView S, CsrView C, int
     wz = __fma_rn(wi, zi, wz);
     bb = __fma_rn(bi, bi, bb);
   };
-  if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
-  else csr_rows<L>(C, gather, epi);
+  if (FMT == FMT_SELL_TMA) {
+    StageIO<0, 1> io;
+    io.pf[0] = x;
+    io.pf_len = S.n + n_ghost;
+    auto pre = [&](int64_t i) { return b[i]; };
+    auto epi2 = [&](int64_t i, double s, double, const double *) { epi(i, s); };
+    sell_staged_rows<8>(S, io, pre, gather, epi2);
+  } else if (FMT == PCG_FORMAT_SELL) {
+    sell_rows(S, gather, epi);
+  } else {
+    csr_rows<L>(C, gather, epi);
+  }
   if (n_ghost) {
-    const int64_t n = FMT == PCG_FORMAT_SELL ? S.n : C.n;
+    const int64_t n = FMT != PCG_FORMAT_CSR ? S.n : C.n;
     for (int64_t g = (int64_t)blockIdx.x * BLOCK + threadIdx.x; g < n_ghost; g += (int64_t)gridDim.x * BLOCK)
       pz[n + g] = 0.0;
   }
@@ -368,11 +481,21 @@ __global__ void clear_alpha_kernel(Scalars *sc) { sc->alpha = 0.0; }
 // ---------------------------------------------------------------- standalone SpMV  y = A x
 template <int FMT, int L>
 __global__ void __launch_bounds__(BLOCK) spmv_kernel(SellView S, CsrView C, const double *__restrict__ x,
-                                                     double *__restrict__ y) {
+                                                     double *__restrict__ y, int64_t x_len) {
   auto gather = [&](int j) { return __ldg(x + j); };
   auto epi = [&](int64_t i, double s) { __stcs(y + i, s); };
-  if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
-  else csr_rows<L>(C, gather, epi);
+  if (FMT == FMT_SELL_TMA) {
+    StageIO<0, 1> io;
+    io.pf[0] = x;
+    io.pf_len = x_len;
+    auto pre = [&](int64_t) { return 0; };
+    auto epi2 = [&](int64_t i, double s, int, const double *) { __stcs(y + i, s); };
+    sell_staged_rows<8>(S, io, pre, gather, epi2);
+  } else if (FMT == PCG_FORMAT_SELL) {
+    sell_rows(S, gather, epi);
+  } else {
+    csr_rows<L>(C, gather, epi);
+  }
 }
 
 // ---------------------------------------------------------------- launch helpers
@@ -382,6 +505,7 @@ struct Dispatch;
 #define PCG_DISPATCH(FMTV, LANES, KERNEL, ...)                                   \
   do {                                                                           \
     if ((FMTV) == PCG_FORMAT_SELL) KERNEL<PCG_FORMAT_SELL, 1>__VA_ARGS__;        \
+    else if ((FMTV) == FMT_SELL_TMA) KERNEL<FMT_SELL_TMA, 1>__VA_ARGS__;         \
     else switch (LANES) {                                                        \
         case 1: KERNEL<PCG_FORMAT_CSR, 1>__VA_ARGS__; break;                     \
         case 2: KERNEL<PCG_FORMAT_CSR, 2>__VA_ARGS__; break;                     \
@@ -398,7 +522,7 @@ static Vecs vecs_of(pcg_matrix *A) {
 }
 
 pcg_status launch_spmv_fmt(pcg_matrix *A, int fmt, const double *x, double *y, cudaStream_t st) {
-  PCG_DISPATCH(fmt, A->csr_lanes, spmv_kernel, <<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), x, y));
+  PCG_DISPATCH(fmt, A->csr_lanes, spmv_kernel, <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), x, y, A->n + A->n_ghost));
   count_launch();
   PCG_CUDA(cudaGetLastError());
   return PCG_OK;
@@ -419,18 +543,33 @@ static int k1_chunk() {  // tuning knob (PCG_K1_CHUNK=4|8), default 8
 static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
   Vecs v = vecs_of(A);
   SolveWork &w = A->work;
+  if (A->schedule == 3) {  // K1a (streaming p/x update) + K1b (SpMV + sigma)
+    k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, use_cond, h);
+    count_launch();
+    PCG_DISPATCH(A->format, A->csr_lanes, k1b_kernel,
+                 <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
+                                                            A->comm ? 1 : 0, use_cond, h));
+    count_launch();
+    PCG_CUDA(cudaGetLastError());
+    if (A->comm) {
+      PCG_TRY(allreduce_sum(A, &w.sc->sigma, 1, st));
+      finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h, 0);
+      count_launch();
+    }
+    return PCG_OK;
+  }
   if (A->format == PCG_FORMAT_SELL && k1_chunk() == 4)
-    k1_kernel<PCG_FORMAT_SELL, 1, 4><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc,
+    k1_kernel<PCG_FORMAT_SELL, 1, 4><<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc,
                                                                      w.partials, A->comm ? 1 : 0, use_cond, h);
   else
     PCG_DISPATCH(A->format, A->csr_lanes, k1_kernel,
-                 <<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
+                 <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
                                                   A->comm ? 1 : 0, use_cond, h));
   count_launch();
   PCG_CUDA(cudaGetLastError());
   if (A->comm) {
     PCG_TRY(allreduce_sum(A, &w.sc->sigma, 1, st));
-    finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h);
+    finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h, 1);
     count_launch();
   }
   return PCG_OK;
@@ -458,7 +597,7 @@ static pcg_status launch_resid(pcg_matrix *A, const double *b, int mode, cudaStr
   SolveWork &w = A->work;
   if (A->comm) PCG_TRY(halo_exchange(A, w.x, 1, st));
   PCG_DISPATCH(A->format, A->csr_lanes, resid_kernel,
-               <<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), A->n_ghost, b, v, w.sc, w.partials,
+               <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, b, v, w.sc, w.partials,
                                                 mode, A->comm ? 1 : 0));
   count_launch();
   PCG_CUDA(cudaGetLastError());
@@ -611,7 +750,7 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
     info->replacements = h->replacements;
     info->t_solve_s = ms * 1e-3;
     const double nn = (double)A->n, nz = (double)A->nnz;
-    info->bytes_algorithmic = (double)h->k * (12.0 * nz + 4.0 * (nn + 1) + 88.0 * nn);
+    info->bytes_algorithmic = (double)h->k * (12.0 * nz + 4.0 * (nn + 1) + (A->schedule == 3 ? 96.0 : 88.0) * nn);
     info->flops = (double)h->k * (2.0 * nz + 13.0 * nn);
   }
   if (s == PCG_ERR_NOT_SPD) set_error("pcg_solve: p^T A p <= 0 (matrix not SPD)");
@@ -663,10 +802,24 @@ extern "C" pcg_status pcg_spmv(pcg_matrix_t A, const double *x, double *y, void 
 }
 
 namespace pcgb {
-int k1_blocks_per_sm(int fmt, int lanes) {
+// TMA-staged kernels need their dynamic shared memory opted in (> 48 KB)
+pcg_status prepare_staged(size_t smem) {
+  const int v = (int)smem;
+  PCG_CUDA(cudaFuncSetAttribute(k1_kernel<FMT_SELL_TMA, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
+  PCG_CUDA(cudaFuncSetAttribute(k1_kernel<FMT_SELL_TMA, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
+  PCG_CUDA(cudaFuncSetAttribute(resid_kernel<FMT_SELL_TMA, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
+  PCG_CUDA(cudaFuncSetAttribute(spmv_kernel<FMT_SELL_TMA, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
+  PCG_CUDA(cudaFuncSetAttribute(k1b_kernel<FMT_SELL_TMA, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
+  return PCG_OK;
+}
+
+int k1_blocks_per_sm(int fmt, int lanes, size_t smem) {
   int b = 0;
   cudaError_t e;
-  if (fmt == PCG_FORMAT_SELL) {
+  if (fmt == FMT_SELL_TMA) {
+    e = k1_chunk() == 4 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<FMT_SELL_TMA, 1, 4>, BLOCK, smem)
+                        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<FMT_SELL_TMA, 1, 8>, BLOCK, smem);
+  } else if (fmt == PCG_FORMAT_SELL) {
     e = k1_chunk() == 4 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_SELL, 1, 4>, BLOCK, 0)
                         : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<PCG_FORMAT_SELL, 1, 8>, BLOCK, 0);
   } else {
@@ -687,9 +840,9 @@ int k1_blocks_per_sm(int fmt, int lanes) {
 }
 }  // namespace pcgb
 
-extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32_t reps, void *stream, double *us_k1,
-                                          double *us_k2, int32_t *reps_done) {
-  if (!A || !b || !us_k1 || !us_k2 || reps < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_profile_kernels: bad argument");
+extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32_t reps, void *stream, double *us,
+                                          int32_t *reps_done) {
+  if (!A || !b || !us || reps < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_profile_kernels: bad argument");
   if (A->comm) return fail(PCG_ERR_INVALID_ARG, "pcg_profile_kernels: single-GPU handles only");
   if (!is_device_ptr(b)) return fail(PCG_ERR_INVALID_ARG, "pcg_profile_kernels: b must be a device pointer");
   std::lock_guard<std::mutex> lk(A->mu);
@@ -704,29 +857,38 @@ extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32
   h->max_iter = (long long)reps + 1;
   PCG_CUDA(cudaMemcpyAsync(w.sc, h, sizeof(Scalars), cudaMemcpyHostToDevice, st));
   PCG_TRY(launch_resid(A, b, MODE_INIT, st));
-  std::vector<cudaEvent_t> ev(2 * (size_t)reps + 1);
+  Vecs v = vecs_of(A);
+  std::vector<cudaEvent_t> ev(3 * (size_t)reps + 1);
   for (auto &e : ev) PCG_CUDA(cudaEventCreate(&e));
   PCG_CUDA(cudaEventRecord(ev[0], st));
   for (int r = 0; r < reps; r++) {
-    PCG_TRY(launch_k1(A, st, 0, 0));
-    PCG_CUDA(cudaEventRecord(ev[2 * r + 1], st));
+    if (A->schedule == 3) {
+      k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, 0, 0);
+      PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
+      PCG_DISPATCH(A->format, A->csr_lanes, k1b_kernel,
+                   <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
+                                                              0, 0, 0));
+      count_launch(2);
+    } else {
+      PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
+      PCG_TRY(launch_k1(A, st, 0, 0));
+    }
+    PCG_CUDA(cudaEventRecord(ev[3 * r + 2], st));
     PCG_TRY(launch_k2(A, st, 0, 0));
-    PCG_CUDA(cudaEventRecord(ev[2 * r + 2], st));
+    PCG_CUDA(cudaEventRecord(ev[3 * r + 3], st));
   }
   PCG_CUDA(cudaStreamSynchronize(st));
   PCG_CUDA(cudaMemcpy(h, w.sc, sizeof(Scalars), cudaMemcpyDeviceToHost));
   const int done = (int)std::min<long long>(h->k, reps);
-  double t1 = 0, t2 = 0;
-  for (int r = 0; r < done; r++) {
-    float a = 0, b2 = 0;
-    cudaEventElapsedTime(&a, ev[2 * r], ev[2 * r + 1]);
-    cudaEventElapsedTime(&b2, ev[2 * r + 1], ev[2 * r + 2]);
-    t1 += a;
-    t2 += b2;
-  }
+  double t[3] = {0, 0, 0};
+  for (int r = 0; r < done; r++)
+    for (int k = 0; k < 3; k++) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[3 * r + k], ev[3 * r + k + 1]);
+      t[k] += ms;
+    }
   for (auto &e : ev) cudaEventDestroy(e);
-  *us_k1 = done ? t1 * 1e3 / done : 0.0;
-  *us_k2 = done ? t2 * 1e3 / done : 0.0;
+  for (int k = 0; k < 3; k++) us[k] = done ? t[k] * 1e3 / done : 0.0;
   if (reps_done) *reps_done = done;
   return PCG_OK;
 }

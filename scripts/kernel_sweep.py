@@ -29,16 +29,23 @@ A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"], fmt=a.fmt)
 b = P["B"][:, 0].contiguous()
 del P
 torch.cuda.synchronize()
-us1, us2, done = C.c_double(), C.c_double(), C.c_int32()
+us = (C.c_double * 3)()
+done = C.c_int32()
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 for _ in range(2):
-    pcg.check(pcg.lib().pcg_profile_kernels(A._h, C.c_void_p(b.data_ptr()), a.reps, st, C.byref(us1), C.byref(us2),
-                                             C.byref(done)), "profile")
-k1 = 12.0 * nnz + 4.0 * (n + 1) + 48.0 * n
-k2 = 40.0 * n
-out = {"config": a.config, "c": spec.c, "n": n, "nnz": nnz, "env_chunk": os.environ.get("PCG_K1_CHUNK"),
-       "stats": A.stats(), "k1_us": us1.value, "k1_GBps": k1 / us1.value / 1e3, "k2_us": us2.value,
-       "k2_GBps": k2 / us2.value / 1e3, "iter_frac": (k1 + k2) / (us1.value + us2.value) / 1e3 / 6556.2}
+    pcg.check(pcg.lib().pcg_profile_kernels(A._h, C.c_void_p(b.data_ptr()), a.reps, st, us, C.byref(done)), "profile")
+stats = A.stats()
+mat = 12.0 * nnz + 4.0 * (n + 1)
+if stats["schedule"] == 3:
+    byts = [40.0 * n, mat + 16.0 * n, 40.0 * n]
+else:
+    byts = [0.0, mat + 48.0 * n, 40.0 * n]
+out = {"config": a.config, "c": spec.c, "n": n, "nnz": nnz, "env": {k: v for k, v in os.environ.items() if k.startswith("PCG_")},
+       "format": stats["format"], "schedule": stats["schedule"], "stages": stats["stages"],
+       "us": list(us), "GBps": [b_ / u / 1e3 if u else 0 for b_, u in zip(byts, us)],
+       "iter_us": sum(us), "iter_frac": sum(byts) / sum(us) / 1e3 / 6556.2,
+       "iter_frac_vs_88n": (mat + 88.0 * n) / sum(us) / 1e3 / 6556.2,
+       "spmv_us": {"csr": stats["spmv_us_csr"], "sell": stats["spmv_us_sell"], "tma": stats["spmv_us_tma"]}}
 if a.solve:
     x, info = A.solve(b)
     x, info = A.solve(b)

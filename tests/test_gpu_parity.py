@@ -46,7 +46,7 @@ CASES = [("C1", None), ("C2", 96), ("C3", 48), ("C5", 32), ("C4", 16)]
 
 
 @pytest.mark.parametrize("name,c", CASES)
-@pytest.mark.parametrize("fmt", ["auto", "csr", "sell"])
+@pytest.mark.parametrize("fmt", ["auto", "csr", "sell", "tma"])
 def test_spmv_parity(pcg, name, c, fmt):
     P = O.build_problem(name, c=c, k=1)
     A = P["A"]
@@ -56,7 +56,7 @@ def test_spmv_parity(pcg, name, c, fmt):
     yo = O.spmv(A, x)
     assert np.all(np.abs(y - yo) <= _spmv_bound(A, x))
     if fmt != "auto":
-        assert M.stats()["format"] == {"csr": 1, "sell": 2}[fmt]
+        assert M.stats()["format"] == {"csr": 1, "sell": 2, "tma": 3}[fmt]
 
 
 @pytest.mark.parametrize("name,c", CASES)
@@ -79,7 +79,7 @@ def test_pcg_parity(pcg, name, c):
     assert abs(t - info["relres_true"]) <= 1e-3 * tol
 
 
-@pytest.mark.parametrize("fmt", ["csr", "sell"])
+@pytest.mark.parametrize("fmt", ["csr", "sell", "tma"])
 def test_pcg_both_formats_and_determinism(pcg, fmt):
     P = O.build_problem("C2", c=64)
     M = _matrix(pcg, P["A"], fmt)
