@@ -113,14 +113,22 @@ class Matrix:
         check(lib().pcg_spmv(self._h, _ptr(x), _ptr(y), _stream_ptr(stream)), "pcg_spmv")
         return y
 
-    def solve(self, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None, raise_on=("error",)):
-        """Jacobi-PCG.  Returns (x, info).  b/x0 may be host or device tensors; x is a new
-        tensor on b's device (x0 is not modified)."""
+    def solve(self, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None, raise_on=("error",),
+              out=None):
+        """Jacobi-PCG.  Returns (x, info).  b/x0 may be host or device tensors.  x is a new
+        tensor on b's device (x0 is not modified) unless `out` is given: then `out` (same
+        device as b, float64, contiguous) holds x0 on entry and the solution on return."""
         torch = _torch()
         b = _as_tensor(b, torch.float64)
-        x = torch.zeros_like(b) if x0 is None else _as_tensor(x0, torch.float64).clone()
+        if out is not None:
+            x = out
+        else:
+            x = torch.zeros_like(b) if x0 is None else _as_tensor(x0, torch.float64).clone()
         if b.device.type == "cpu":
-            b, x = b.pin_memory(), x.pin_memory()
+            if not b.is_pinned():
+                b = b.pin_memory()
+            if not x.is_pinned():
+                x = x.pin_memory()
         info = _lib.PcgInfo()
         st = lib().pcg_solve(self._h, _ptr(b), _ptr(x), float(tol), int(max_iter), _stream_ptr(stream),
                              C.byref(info))

@@ -82,6 +82,7 @@ struct CsrView {
   const int *row_ptr;   // n+1 (int32: nnz < 2^31 per GPU)
   const int *col;       // local column ids
   const double *val;
+  int zero;             // run-time 0, opaque to the compiler (rows.cuh cols_ready)
 };
 
 struct SellView {

@@ -78,7 +78,7 @@ struct pcg_matrix {
   pcgb::HaloPlan halo;
   pcgb::SolveWork work;
   std::mutex mu;
-  pcgb::CsrView csr() const { return {n, n + n_ghost, d_row_ptr, d_col, d_val}; }
+  pcgb::CsrView csr() const { return {n, n + n_ghost, d_row_ptr, d_col, d_val, 0}; }
   int stages = 2;
   int64_t stage_entries = 0;  // 0: TMA-staged SELL unavailable
   size_t dyn_smem = 0;        // dynamic shared memory of the chosen format's kernels

@@ -17,6 +17,7 @@
 #include <cstring>
 
 #include "matrix.cuh"
+#include "rows.cuh"
 
 namespace pcgb {
 
@@ -121,10 +122,25 @@ __global__ void __launch_bounds__(BLOCK) mk1_kernel(CsrView A, MVecs v, MultiSca
     if (xp != 0.0) v.X[e] = __fma_rn(xp, po, v.X[e]);
     const int rs = A.row_ptr[row], re = A.row_ptr[row + 1];
     double sum = 0.0;
-    for (int k = rs; k < re; k++) {
-      const double a = __ldg(A.val + k);
-      const int64_t j = (int64_t)__ldg(A.col + k) * K + c;
-      sum = __fma_rn(a, __fma_rn(beta, __ldg(Po + j), __ldg(Z + j)), sum);
+    for (int k0 = rs; k0 < re; k0 += 8) {  // all 8 (val, col) loads before the first gather
+      double a[8], g[8];
+      int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (k0 + u < re) {
+          a[u] = __ldg(A.val + k0 + u);
+          j[u] = __ldg(A.col + k0 + u);
+        }
+      cols_ready(j, A.zero);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (k0 + u < re) {
+          const int64_t jj = (int64_t)j[u] * K + c;
+          g[u] = __fma_rn(beta, __ldg(Po + jj), __ldg(Z + jj));
+        }
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (k0 + u < re) sum = __fma_rn(a[u], g[u], sum);
     }
     const double pi = __fma_rn(beta, po, Z[e]);
     Pn[e] = pi;
@@ -237,7 +253,23 @@ __global__ void __launch_bounds__(BLOCK) mresid_kernel(CsrView A, MVecs v, Multi
   for (int64_t row = g0; row < A.n; row += ng) {
     const int rs = A.row_ptr[row], re = A.row_ptr[row + 1];
     double sum = 0.0;
-    for (int k = rs; k < re; k++) sum = __fma_rn(__ldg(A.val + k), __ldg(v.X + (int64_t)__ldg(A.col + k) * K + c), sum);
+    for (int k0 = rs; k0 < re; k0 += 8) {
+      double a[8], g[8];
+      int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (k0 + u < re) {
+          a[u] = __ldg(A.val + k0 + u);
+          j[u] = __ldg(A.col + k0 + u);
+        }
+      cols_ready(j, A.zero);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (k0 + u < re) g[u] = __ldg(v.X + (int64_t)j[u] * K + c);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (k0 + u < re) sum = __fma_rn(a[u], g[u], sum);
+    }
     const int64_t e = row * K + c;
     const double bi = v.Bm[e];
     const double w = bi - sum;

@@ -65,6 +65,7 @@ __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi 
 // then the L partial sums meet in a fixed xor-shuffle tree.
 template <int L, class Gather, class Epi>
 __device__ __forceinline__ void csr_rows(const CsrView &A, Gather gather, Epi epi) {
+  const int zero = A.zero;
   const int sub = threadIdx.x & (L - 1);
   const int64_t g0 = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) / L;
   const int64_t ng = (int64_t)gridDim.x * BLOCK / L;
@@ -75,7 +76,24 @@ __device__ __forceinline__ void csr_rows(const CsrView &A, Gather gather, Epi ep
     double sum = 0.0;
     if (row < A.n) {
       const int rs = A.row_ptr[row], re = A.row_ptr[row + 1];
-      for (int k = rs + sub; k < re; k += L) sum = __fma_rn(ld_stream(A.val + k), gather(ld_stream(A.col + k)), sum);
+      for (int k0 = rs + sub; k0 < re; k0 += 8 * L) {  // 8 entries per lane per chunk
+        double a[8];
+        int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (k0 + u * L < re) {
+            a[u] = ld_stream(A.val + k0 + u * L);
+            j[u] = ld_stream(A.col + k0 + u * L);
+          }
+        cols_ready(j, zero);
+        double g[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (k0 + u * L < re) g[u] = gather(j[u]);
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (k0 + u * L < re) sum = __fma_rn(a[u], g[u], sum);
+      }
     }
 #pragma unroll
     for (int o = L / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o, L);
