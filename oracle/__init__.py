@@ -71,6 +71,8 @@ def lib():
                                     P(_Csr), C.c_void_p, C.c_void_p]
         L.orc_csr_free.argtypes = [P(_Csr)]
         L.orc_spmv.argtypes = [P(_Csr), C.c_void_p, C.c_void_p]
+        L.orc_dot.argtypes = [C.c_int64, C.c_void_p, C.c_void_p]
+        L.orc_dot.restype = C.c_double
         L.orc_pcg.argtypes = [P(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64,
                               P(C.c_int64), P(C.c_double), P(C.c_double),
                               C.c_void_p, C.c_void_p, C.c_int64]
@@ -209,6 +211,14 @@ def spmv(A: Csr, x) -> np.ndarray:
     Ac = A._c()
     lib().orc_spmv(C.byref(Ac), _ptr(x), _ptr(y))
     return y
+
+
+def dot(a, b) -> float:
+    """a.b as the oracle's PCG evaluates it (Dot2: as if in twice fp64 precision)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    assert a.shape == b.shape
+    return float(lib().orc_dot(a.size, _ptr(a), _ptr(b)))
 
 
 class PcgResult(dict):

@@ -84,6 +84,8 @@ void orc_csr_free(orc_csr *A);
 
 /* y = A x  (left-to-right within a row) */
 void orc_spmv(const orc_csr *A, const double *x, double *y);
+/* a.b to (almost) exact rounding (Dot2, Ogita-Rump-Oishi 2005); reading R1 */
+double orc_dot(int64_t n, const double *a, const double *b);
 
 /* Jacobi-PCG, §8(c).8.  x in/out.  alpha_hist/beta_hist may be NULL. */
 int orc_pcg(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter,

@@ -472,3 +472,37 @@ def test_partition_rule_and_halo_brute_force(G):
         cols = set(A.col[A.row_ptr[r0]:A.row_ptr[r1]].tolist())
         want = sorted(j for j in cols if j < r0 or j >= r1)
         assert O.halo(A, r0, r1).tolist() == want
+
+
+# ---------------------------------------------------------------- inner products (reading R1)
+def _exact_dot(a, b):
+    """Σ a_i b_i in exact rational arithmetic, then rounded once to fp64."""
+    from fractions import Fraction
+    return float(sum(Fraction(float(x)) * Fraction(float(y)) for x, y in zip(a, b)))
+
+
+def test_dot_is_exactly_rounded_on_random_vectors():
+    rng = np.random.default_rng(11)
+    for n in (1, 7, 100, 2000):
+        a = rng.standard_normal(n) * np.exp(rng.uniform(-20, 20, n))
+        b = rng.standard_normal(n)
+        e = _exact_dot(a, b)
+        got = O.dot(a, b)
+        # Dot2 error bound: |got - e| <= u|e| + gamma_n^2 Σ|a_i b_i|  (Ogita-Rump-Oishi, Prop. 5.5)
+        u = 2.0 ** -53
+        g = n * u / (1 - n * u)
+        assert abs(got - e) <= u * abs(e) + g * g * float(np.sum(np.abs(a * b))) + 1e-300
+
+
+def test_dot_survives_cancellation_that_breaks_a_plain_sum():
+    # Σ = 1 exactly; a left-to-right fp64 sum returns 0
+    a = np.array([1e16, 1.0, -1e16])
+    b = np.ones(3)
+    assert float(a[0] * b[0] + a[1] * b[1] + a[2] * b[2]) == 0.0
+    assert O.dot(a, b) == 1.0
+    # ill-conditioned (cond ~ 1e20): still the exactly rounded value
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(50) * 1e10
+    a = np.concatenate([x[:25], x[:25], [3.0]])
+    b = np.concatenate([np.ones(25), -np.ones(25), [0.5]])
+    assert O.dot(a, b) == _exact_dot(a, b) == 1.5
