@@ -56,11 +56,15 @@ typedef enum {
 #define PCG_FMT_CSR 0x10   /* force CSR (sub-warp per row)            */
 #define PCG_FMT_SELL 0x20  /* force SELL-32 (slices of 32 rows)       */
 #define PCG_FMT_SELL_TMA 0x30 /* force SELL-32 with TMA-staged tiles  */
+#define PCG_FMT_SELL_SIGMA 0x40 /* force SELL-C-sigma: rows sorted by length inside windows of
+                                   sigma rows, applied as a symmetric permutation P A P^T
+                                   (vectors are permuted at the ABI boundary; one GPU only) */
 
 /* format codes reported by pcg_matrix_stats.format */
 #define PCG_FORMAT_CSR 1
 #define PCG_FORMAT_SELL 2
 #define PCG_FORMAT_SELL_TMA 3 /* SELL-32, matrix tiles staged in shared memory by TMA bulk copies */
+#define PCG_FORMAT_SELL_SIGMA 4 /* SELL-32 of the sigma-sorted system P A P^T */
 
 typedef struct pcg_matrix *pcg_matrix_t;
 typedef struct pcg_comm *pcg_comm_t;
@@ -91,6 +95,9 @@ typedef struct {
   int64_t stage_entries;     /* TMA stage size in entries (0 = unavailable)   */
   int32_t stages;            /* TMA ring depth                                */
   int32_t schedule;          /* passes per iteration: 3 (K1a,K1b,K2) or 2 (fused K1,K2) */
+  double spmv_us_sigma;      /* autotune timing of SELL-C-sigma (0 if not tried) */
+  int32_t sigma;             /* sorting window of SELL-C-sigma (0: natural row order) */
+  int32_t pad0;
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */
@@ -166,6 +173,15 @@ const char *pcg_status_string(pcg_status s);
  * Single-GPU handles only; stops early (fewer reps) if the solve converges. */
 pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32_t reps, void *stream, double *us,
                                int32_t *reps_done);
+
+/* Multi-RHS per-kernel timing (bench/profiling only): k columns of B (device,
+ * column-major, ld >= n, 1 <= k <= 32) run the init pass (X0 = 0) and then `reps`
+ * block iterations one kernel at a time.  us[0..2] = mean device time (microseconds)
+ * of: K1a (streaming X += alpha P, P = Z + beta P), K1b (SpMM Q = A P with
+ * per-column sigma), K2 (R/Z updates with per-column rho', gamma).
+ * Single-GPU handles only. */
+pcg_status pcg_profile_multi(pcg_matrix_t A, int32_t k, const double *B, int64_t ldb, int32_t reps, void *stream,
+                             double *us, int32_t *reps_done);
 
 /* number of kernels this library launched in the calling process (monotone counter,
  * for launch accounting in benchmarks) */

@@ -69,7 +69,8 @@ class Matrix:
         if dev != ci.is_cuda or dev != va.is_cuda:
             raise ValueError("row_ptr, col and val must live on the same device")
         flags = (_lib.PCG_PTR_DEVICE if dev else _lib.PCG_PTR_HOST) | {
-            "auto": PCG_FMT_AUTO, "csr": PCG_FMT_CSR, "sell": PCG_FMT_SELL, "tma": _lib.PCG_FMT_SELL_TMA}[fmt]
+            "auto": PCG_FMT_AUTO, "csr": PCG_FMT_CSR, "sell": PCG_FMT_SELL, "tma": _lib.PCG_FMT_SELL_TMA,
+            "sigma": _lib.PCG_FMT_SELL_SIGMA}[fmt]
         h = C.c_void_p()
         check(lib().csr_create(n, nnz, _ptr(rp), _ptr(ci), _ptr(va), flags, _stream_ptr(stream), C.byref(h)),
               "csr_create")
@@ -82,7 +83,8 @@ class Matrix:
         rp, ci, va = (_as_tensor(row_ptr_local, torch.int64), _as_tensor(col_global, torch.int64),
                       _as_tensor(val, torch.float64))
         flags = (_lib.PCG_PTR_DEVICE if rp.is_cuda else _lib.PCG_PTR_HOST) | {
-            "auto": PCG_FMT_AUTO, "csr": PCG_FMT_CSR, "sell": PCG_FMT_SELL, "tma": _lib.PCG_FMT_SELL_TMA}[fmt]
+            "auto": PCG_FMT_AUTO, "csr": PCG_FMT_CSR, "sell": PCG_FMT_SELL, "tma": _lib.PCG_FMT_SELL_TMA,
+            "sigma": _lib.PCG_FMT_SELL_SIGMA}[fmt]
         h = C.c_void_p()
         check(lib().csr_create_dist(comm._h, n_global, row_begin, row_end, ci.numel(), _ptr(rp), _ptr(ci), _ptr(va),
                                     flags, _stream_ptr(stream), C.byref(h)), "csr_create_dist")

@@ -18,7 +18,7 @@ STATUS = ["PCG_OK", "PCG_NOT_CONVERGED", "PCG_ERR_INVALID_ARG", "PCG_ERR_INDEX_O
  PCG_ERR_UNSORTED_OR_DUPLICATE, PCG_ERR_DIMENSION_MISMATCH, PCG_ERR_ZERO_DIAGONAL, PCG_ERR_NOT_SPD,
  PCG_ERR_NONFINITE, PCG_ERR_OOM, PCG_ERR_CUDA, PCG_ERR_NCCL) = range(12)
 PCG_PTR_HOST, PCG_PTR_DEVICE = 0x0, 0x1
-PCG_FMT_AUTO, PCG_FMT_CSR, PCG_FMT_SELL, PCG_FMT_SELL_TMA = 0x00, 0x10, 0x20, 0x30
+PCG_FMT_AUTO, PCG_FMT_CSR, PCG_FMT_SELL, PCG_FMT_SELL_TMA, PCG_FMT_SELL_SIGMA = 0x00, 0x10, 0x20, 0x30, 0x40
 PCG_FORMAT_CSR, PCG_FORMAT_SELL, PCG_FORMAT_SELL_TMA = 1, 2, 3
 
 
@@ -38,7 +38,8 @@ class MatrixStats(C.Structure):
                 ("device_bytes", C.c_double), ("spmv_us_csr", C.c_double),
                 ("spmv_us_sell", C.c_double), ("n_ghost", C.c_int64), ("row_begin", C.c_int64),
                 ("row_end", C.c_int64), ("n_global", C.c_int64), ("spmv_us_tma", C.c_double),
-                ("stage_entries", C.c_int64), ("stages", C.c_int32), ("schedule", C.c_int32)]
+                ("stage_entries", C.c_int64), ("stages", C.c_int32), ("schedule", C.c_int32),
+                ("spmv_us_sigma", C.c_double), ("sigma", C.c_int32), ("pad0", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -78,6 +79,7 @@ def lib():
         "pcg_comm_destroy": [vp],
         "csr_create_dist": [vp, i64, i64, i64, i64, vp, vp, vp, C.c_int, vp, P(vp)],
         "pcg_profile_kernels": [vp, vp, i32, vp, vp, P(i32)],
+        "pcg_profile_multi": [vp, i32, vp, i64, i32, vp, vp, P(i32)],
         "fem_problem_size": [P(FemSpec), P(i64), P(i64), P(i64)],
         "fem_count": [P(FemSpec), i64, i64, vp, P(i64), vp],
         "fem_assemble": [P(FemSpec), i64, i64, vp, vp, vp, vp, i64, vp],

@@ -190,6 +190,53 @@ static pcg_status error_from_flags(const ErrInfo &e, int64_t row_offset) {
   return PCG_OK;
 }
 
+// SELL-32 arrays from the device CSR (slice_ptr by a scan of per-slice max row
+// lengths; entries [slice][t][lane], padding col = row, val = 0).
+pcg_status build_sell(pcg_matrix *A, cudaStream_t st) {
+  if (A->d_slice_ptr) return PCG_OK;
+  const int64_t n = A->n;
+  A->n_slices = (n + 31) / 32;
+  PCG_CUDA(cudaMalloc(&A->d_slice_ptr, sizeof(int64_t) * (A->n_slices + 1)));
+  int64_t *tmp;
+  PCG_CUDA(cudaMalloc(&tmp, sizeof(int64_t) * (A->n_slices + 1)));
+  slice_len_kernel<<<(unsigned)((A->n_slices + 1 + 255) / 256), 256, 0, st>>>(n, A->n_slices, A->d_row_ptr, tmp);
+  count_launch();
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, tmp, A->d_slice_ptr, A->n_slices + 1, st);
+  void *tbuf;
+  PCG_CUDA(cudaMalloc(&tbuf, tb));
+  cub::DeviceScan::ExclusiveSum(tbuf, tb, tmp, A->d_slice_ptr, A->n_slices + 1, st);
+  PCG_CUDA(cudaMemcpyAsync(&A->sell_entries, A->d_slice_ptr + A->n_slices, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                           st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(tbuf);
+  cudaFree(tmp);
+  if (A->sell_entries >= (int64_t(1) << 31)) {
+    free_sell(A);
+    return fail(PCG_ERR_INVALID_ARG, "csr_create: padded SELL entries exceed 2^31 on one GPU");
+  }
+  PCG_CUDA(cudaMalloc(&A->d_scol, sizeof(int) * (A->sell_entries > 0 ? A->sell_entries : 1)));
+  PCG_CUDA(cudaMalloc(&A->d_sval, sizeof(double) * (A->sell_entries > 0 ? A->sell_entries : 1)));
+  if (A->n_slices > 0) {
+    sell_fill_kernel<<<(unsigned)((A->n_slices * 32 + 255) / 256), 256, 0, st>>>(
+        n, A->n_slices, A->d_row_ptr, A->d_col, A->d_val, A->d_slice_ptr, A->d_scol, A->d_sval);
+    count_launch();
+    PCG_CUDA(cudaGetLastError());
+  }
+  A->device_bytes += (double)(A->n_slices + 1) * 8 + (double)A->sell_entries * 12;
+  return PCG_OK;
+}
+
+void free_sell(pcg_matrix *A) {
+  for (void *p : {(void *)A->d_slice_ptr, (void *)A->d_scol, (void *)A->d_sval})
+    if (p) cudaFree(p);
+  if (A->d_slice_ptr) A->device_bytes -= (double)(A->n_slices + 1) * 8 + (double)A->sell_entries * 12;
+  A->d_slice_ptr = nullptr;
+  A->d_scol = nullptr;
+  A->d_sval = nullptr;
+  A->sell_entries = 0;
+}
+
 // Core of csr_create / csr_create_dist: columns already translated so that the
 // local matrix is n x n_cols (n_cols = n + n_ghost) with diagonal at i + 0.
 // d_col_check: columns as given by the caller (global ids on a distributed handle),
@@ -228,39 +275,19 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
   const int fmt_req = flags & 0xF0;
   A->n_slices = (n + 31) / 32;
   bool want_sell = fmt_req != PCG_FMT_CSR && n > 0;
+  double pad_nat = 1.0;
   if (want_sell) {
-    PCG_CUDA(cudaMalloc(&A->d_slice_ptr, sizeof(int64_t) * (A->n_slices + 1)));
-    int64_t *tmp;
-    PCG_CUDA(cudaMalloc(&tmp, sizeof(int64_t) * (A->n_slices + 1)));
-    slice_len_kernel<<<(unsigned)((A->n_slices + 1 + 255) / 256), 256, 0, st>>>(n, A->n_slices, A->d_row_ptr, tmp);
-    count_launch();
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, tmp, A->d_slice_ptr, A->n_slices + 1, st);
-    void *tbuf;
-    PCG_CUDA(cudaMalloc(&tbuf, tb));
-    cub::DeviceScan::ExclusiveSum(tbuf, tb, tmp, A->d_slice_ptr, A->n_slices + 1, st);
-    PCG_CUDA(cudaMemcpyAsync(&A->sell_entries, A->d_slice_ptr + A->n_slices, sizeof(int64_t),
-                             cudaMemcpyDeviceToHost, st));
-    PCG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(tbuf);
-    cudaFree(tmp);
-    const double pad = nnz > 0 ? (double)A->sell_entries / (double)nnz : 1.0;
-    if (fmt_req == PCG_FMT_AUTO && pad > 1.25) {
-      want_sell = false;  // padding too large: SELL would move >25% extra bytes
-      cudaFree(A->d_slice_ptr);
-      A->d_slice_ptr = nullptr;
-      A->sell_entries = 0;
-    } else if (A->sell_entries >= (int64_t(1) << 31)) {
-      return fail(PCG_ERR_INVALID_ARG, "csr_create: padded SELL entries exceed 2^31 on one GPU");
-    } else {
-      PCG_CUDA(cudaMalloc(&A->d_scol, sizeof(int) * (A->sell_entries > 0 ? A->sell_entries : 1)));
-      PCG_CUDA(cudaMalloc(&A->d_sval, sizeof(double) * (A->sell_entries > 0 ? A->sell_entries : 1)));
-      sell_fill_kernel<<<(unsigned)((A->n_slices * 32 + 255) / 256), 256, 0, st>>>(
-          n, A->n_slices, A->d_row_ptr, A->d_col, A->d_val, A->d_slice_ptr, A->d_scol, A->d_sval);
-      count_launch();
-      PCG_CUDA(cudaGetLastError());
+    PCG_TRY(build_sell(A, st));
+    pad_nat = nnz > 0 ? (double)A->sell_entries / (double)nnz : 1.0;
+    if (fmt_req == PCG_FMT_AUTO && pad_nat > 1.25) {
+      want_sell = false;  // padding too large: natural-order SELL would move >25% extra bytes
+      free_sell(A);
     }
+    if (fmt_req == PCG_FMT_SELL_SIGMA) want_sell = false;  // only the permuted SELL is a candidate
   }
+  // SELL-C-sigma candidate (sigma.cu): one GPU, and only where natural slices pad
+  const bool try_sigma = !A->comm && n > 0 &&
+                         (fmt_req == PCG_FMT_SELL_SIGMA || (fmt_req == PCG_FMT_AUTO && pad_nat > 1.02));
   // ---- CSR lanes per row from the mean row length (power of two, <= 32)
   const double mean = n > 0 ? (double)nnz / (double)n : 1.0;
   int L = 1;
@@ -314,8 +341,9 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
   const int64_t need_vec = (n / 2 + BLOCK - 1) / BLOCK;
   A->grid_vec = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 8, need_vec));
   std::vector<int> cands;
-  if (fmt_req == PCG_FMT_CSR || !want_sell) cands = {PCG_FORMAT_CSR};
+  if (fmt_req == PCG_FMT_CSR || (!want_sell && fmt_req != PCG_FMT_SELL_SIGMA)) cands = {PCG_FORMAT_CSR};
   else if (fmt_req == PCG_FMT_SELL) cands = {PCG_FORMAT_SELL};
+  else if (fmt_req == PCG_FMT_SELL_SIGMA) cands = {};
   else if (fmt_req == PCG_FMT_SELL_TMA) {
     if (!A->stage_entries) return fail(PCG_ERR_INVALID_ARG, "csr_create: TMA-staged SELL unavailable for this matrix");
     cands = {FMT_SELL_TMA};
@@ -324,24 +352,31 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
     if (A->stage_entries) cands.push_back(FMT_SELL_TMA);
   }
   // ---- measured format choice (time 5 SpMVs of each candidate)
-  if (cands.size() > 1 && n > 0) {
-    PCG_TRY(ensure_work(A));
+  const bool timed = n > 0 && (cands.size() > 1 || (try_sigma && fmt_req == PCG_FMT_AUTO));
+  float best = 1e30f;
+  int best_fmt = cands.empty() ? PCG_FORMAT_SELL : cands[0];
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  auto time_fmt = [&](int fmt, float *ms) -> pcg_status {
     double *x = A->work.stage_x, *y = A->work.w;
-    PCG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (n + A->n_ghost), st));
-    cudaEvent_t e0, e1;
+    configure(fmt);
+    PCG_TRY(launch_spmv_fmt(A, fmt, x, y, st));  // warm-up
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < 5; r++) PCG_TRY(launch_spmv_fmt(A, fmt, x, y, st));
+    cudaEventRecord(e1, st);
+    PCG_CUDA(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(ms, e0, e1);
+    return PCG_OK;
+  };
+  if (timed || try_sigma) {
+    PCG_TRY(ensure_work(A));
+    PCG_CUDA(cudaMemsetAsync(A->work.stage_x, 0, sizeof(double) * (n + A->n_ghost), st));
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    float best = 1e30f;
-    int best_fmt = cands[0];
+  }
+  if (timed) {
     for (int fmt : cands) {
-      configure(fmt);
-      PCG_TRY(launch_spmv_fmt(A, fmt, x, y, st));  // warm-up
-      cudaEventRecord(e0, st);
-      for (int r = 0; r < 5; r++) PCG_TRY(launch_spmv_fmt(A, fmt, x, y, st));
-      cudaEventRecord(e1, st);
-      PCG_CUDA(cudaEventSynchronize(e1));
       float ms = 0;
-      cudaEventElapsedTime(&ms, e0, e1);
+      PCG_TRY(time_fmt(fmt, &ms));
       if (fmt == PCG_FORMAT_CSR) A->spmv_us_csr = ms * 1e3 / 5;
       else if (fmt == PCG_FORMAT_SELL) A->spmv_us_sell = ms * 1e3 / 5;
       else A->spmv_us_tma = ms * 1e3 / 5;
@@ -350,19 +385,44 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
         best_fmt = fmt;
       }
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    configure(best_fmt);
-  } else {
-    configure(cands[0]);
   }
+  if (try_sigma) {
+    // build P A P^T, swap it in (the natural CSR/SELL move to S), build its SELL, time it
+    SigmaSys S;
+    PCG_TRY(sigma_build(A, st, &S));
+    sigma_swap(A, &S);
+    pcg_status bs = build_sell(A, st);
+    if (bs != PCG_OK) {
+      free_sell(A);
+      sigma_swap(A, &S);
+      sigma_free(&S);
+      if (fmt_req == PCG_FMT_SELL_SIGMA) return bs;
+    } else {
+      float ms = 0;
+      PCG_TRY(time_fmt(PCG_FORMAT_SELL, &ms));
+      A->spmv_us_sigma = ms * 1e3 / 5;
+      if (fmt_req == PCG_FMT_SELL_SIGMA || ms < best) {  // keep the permuted system
+        sigma_free(&S);
+        if (A->d_lead) cudaFree(A->d_lead);
+        A->d_lead = nullptr;
+        A->stage_entries = 0;
+        best_fmt = PCG_FORMAT_SELL;
+      } else {  // back to the natural system
+        free_sell(A);
+        sigma_swap(A, &S);
+        sigma_free(&S);
+      }
+    }
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  configure(best_fmt);
   {
     const char *sch = getenv("PCG_SCHEDULE");
     A->schedule = (sch && atoi(sch) == 2) ? 2 : 3;
   }
   if (A->work.graph_ready) free_work(A);  // geometry changed after a provisional workspace
-  A->device_bytes = (double)(n + 1) * 4 + (double)nnz * 12 + (double)n * 8 +
-                    (A->d_slice_ptr ? (double)(A->n_slices + 1) * 8 + (double)A->sell_entries * 12 : 0);
+  A->device_bytes += (double)(n + 1) * 4 + (double)nnz * 12 + (double)n * 8;
   return PCG_OK;
 }
 
@@ -488,6 +548,7 @@ extern "C" pcg_status csr_destroy(pcg_matrix_t A) {
   free_work(A);
   for (void *p : {(void *)A->d_row_ptr, (void *)A->d_col, (void *)A->d_val, (void *)A->d_dinv,
                   (void *)A->d_slice_ptr, (void *)A->d_scol, (void *)A->d_sval, (void *)A->d_lead, (void *)A->halo.d_send_idx,
+                  (void *)A->d_perm, (void *)A->d_iperm,
                   (void *)A->halo.d_send_buf})
     if (p) cudaFree(p);
   delete A;
@@ -499,7 +560,7 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   memset(o, 0, sizeof(*o));
   o->n = A->n;
   o->nnz = A->nnz;
-  o->format = A->format;
+  o->format = A->d_perm ? PCG_FORMAT_SELL_SIGMA : A->format;
   o->max_row_len = A->max_row_len;
   o->sell_entries = A->sell_entries;
   o->t_setup_s = A->t_setup_s;
@@ -514,5 +575,7 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->row_begin = A->row_begin;
   o->row_end = A->row_end;
   o->n_global = A->n_global;
+  o->spmv_us_sigma = A->spmv_us_sigma;
+  o->sigma = A->sigma;
   return PCG_OK;
 }

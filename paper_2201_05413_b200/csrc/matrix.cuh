@@ -49,6 +49,18 @@ struct SolveWork {
   int mgraph_k = 0;
 };
 
+// a symmetrically permuted copy of the system (SELL-C-sigma, sigma.cu)
+struct SigmaSys {
+  int *perm = nullptr, *iperm = nullptr;  // perm[i'] = original row of permuted row i'
+  int *row_ptr = nullptr, *col = nullptr;
+  double *val = nullptr, *dinv = nullptr;
+  int64_t *slice_ptr = nullptr;
+  int *scol = nullptr;
+  double *sval = nullptr;
+  int64_t sell_entries = 0;
+  int sigma = 0;
+};
+
 }  // namespace pcgb
 
 struct pcg_matrix {
@@ -69,7 +81,7 @@ struct pcg_matrix {
   int schedule = 3;  // 3: K1a + K1b + K2 (96n B), 2: fused K1 + K2 (88n B)
   // launch geometry
   int grid_vec = 0, grid_spmv = 0;  // persistent grid sizes (multiples of the SM count)
-  double t_setup_s = 0, spmv_us_csr = 0, spmv_us_sell = 0, spmv_us_tma = 0;
+  double t_setup_s = 0, spmv_us_csr = 0, spmv_us_sell = 0, spmv_us_tma = 0, spmv_us_sigma = 0;
   double device_bytes = 0;
   // distributed
   pcg_comm *comm = nullptr;
@@ -83,12 +95,25 @@ struct pcg_matrix {
   int64_t stage_entries = 0;  // 0: TMA-staged SELL unavailable
   size_t dyn_smem = 0;        // dynamic shared memory of the chosen format's kernels
   int *d_lead = nullptr;      // per-tile prefix-max column (TMA L2 prefetch windows)
+  // SELL-C-sigma: the device system is P A P^T (vectors in permuted order) when d_perm != null
+  int *d_perm = nullptr, *d_iperm = nullptr;
+  int sigma = 0;
   pcgb::SellView sell() const { return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0}; }
 };
 
 namespace pcgb {
 pcg_status ensure_work(pcg_matrix *A);
 pcg_status ensure_multi_work(pcg_matrix *A, int k);
+pcg_status build_sell(pcg_matrix *A, cudaStream_t st);
+int sigma_window();
+pcg_status sigma_build(pcg_matrix *A, cudaStream_t st, SigmaSys *S);
+void sigma_swap(pcg_matrix *A, SigmaSys *S);
+void sigma_free(SigmaSys *S);
+pcg_status perm_in(pcg_matrix *A, const double *src_dev, double *dst, cudaStream_t st);
+pcg_status perm_out(pcg_matrix *A, const double *src, double *dst_dev, cudaStream_t st);
+pcg_status perm_in_cols(pcg_matrix *A, int k, const double *src, int64_t lds, double *dst, int64_t ldd, cudaStream_t st);
+pcg_status perm_out_cols(pcg_matrix *A, int k, const double *src, int64_t lds, double *dst, int64_t ldd, cudaStream_t st);
+void free_sell(pcg_matrix *A);
 void free_work(pcg_matrix *A);
 pcg_status launch_spmv(pcg_matrix *A, const double *x, double *y, cudaStream_t st);
 pcg_status halo_exchange(pcg_matrix *A, double *vec, int width, cudaStream_t st);

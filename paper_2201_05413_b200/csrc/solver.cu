@@ -694,11 +694,26 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
   const int64_t n = A->n;
   const bool b_dev = is_device_ptr(b), x_dev = is_device_ptr(x);
   const double *db = b;
-  if (!b_dev) {
-    PCG_CUDA(cudaMemcpyAsync(w.stage_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  if (A->d_perm) {  // SELL-C-sigma: the device system is P A P^T; b' = P b, x0' = P x0
+    const double *bs = b, *xs = x;
+    if (!b_dev) {
+      PCG_CUDA(cudaMemcpyAsync(w.w, b, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      bs = w.w;
+    }
+    PCG_TRY(perm_in(A, bs, w.stage_b, st));
     db = w.stage_b;
+    if (!x_dev) {
+      PCG_CUDA(cudaMemcpyAsync(w.q, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      xs = w.q;
+    }
+    PCG_TRY(perm_in(A, xs, w.x, st));
+  } else {
+    if (!b_dev) {
+      PCG_CUDA(cudaMemcpyAsync(w.stage_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      db = w.stage_b;
+    }
+    PCG_CUDA(cudaMemcpyAsync(w.x, x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   }
-  PCG_CUDA(cudaMemcpyAsync(w.x, x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   // scalars
   Scalars *h = w.h_sc;
   memset(h, 0, sizeof(Scalars));
@@ -732,7 +747,16 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
   }
   PCG_CUDA(cudaEventRecord(e1, st));
   if (h->done == DONE_ZERO_RHS) PCG_CUDA(cudaMemsetAsync(w.x, 0, sizeof(double) * n, st));
-  PCG_CUDA(cudaMemcpyAsync(x, w.x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  if (A->d_perm) {  // x = P^T x'
+    if (x_dev) {
+      PCG_TRY(perm_out(A, w.x, x, st));
+    } else {
+      PCG_TRY(perm_out(A, w.x, w.w, st));
+      PCG_CUDA(cudaMemcpyAsync(x, w.w, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    }
+  } else {
+    PCG_CUDA(cudaMemcpyAsync(x, w.x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  }
   PCG_CUDA(cudaStreamSynchronize(st));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
@@ -787,6 +811,23 @@ extern "C" pcg_status pcg_spmv(pcg_matrix_t A, const double *x, double *y, void 
   PCG_TRY(ensure_work(A));
   cudaStream_t st = (cudaStream_t)stream;
   const bool xd = is_device_ptr(x), yd = is_device_ptr(y);
+  if (A->d_perm) {  // y = P^T (P A P^T)(P x)
+    const double *xs = x;
+    if (!xd) {
+      PCG_CUDA(cudaMemcpyAsync(A->work.stage_b, x, sizeof(double) * A->n, cudaMemcpyHostToDevice, st));
+      xs = A->work.stage_b;
+    }
+    PCG_TRY(perm_in(A, xs, A->work.stage_x, st));
+    PCG_TRY(launch_spmv(A, A->work.stage_x, A->work.w, st));
+    if (yd) {
+      PCG_TRY(perm_out(A, A->work.w, y, st));
+    } else {
+      PCG_TRY(perm_out(A, A->work.w, A->work.stage_b, st));
+      PCG_CUDA(cudaMemcpyAsync(y, A->work.stage_b, sizeof(double) * A->n, cudaMemcpyDeviceToHost, st));
+    }
+    PCG_CUDA(cudaStreamSynchronize(st));
+    return PCG_OK;
+  }
   const double *dx = x;
   if (A->comm || !xd) {  // gathered vector needs n + n_ghost entries in device memory
     PCG_CUDA(cudaMemcpyAsync(A->work.stage_x, x, sizeof(double) * A->n,
@@ -856,6 +897,10 @@ extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32
   h->tol = 1e-300;  // never stops on the residual inside the profiled window
   h->max_iter = (long long)reps + 1;
   PCG_CUDA(cudaMemcpyAsync(w.sc, h, sizeof(Scalars), cudaMemcpyHostToDevice, st));
+  if (A->d_perm) {
+    PCG_TRY(perm_in(A, b, w.stage_b, st));
+    b = w.stage_b;
+  }
   PCG_TRY(launch_resid(A, b, MODE_INIT, st));
   Vecs v = vecs_of(A);
   std::vector<cudaEvent_t> ev(3 * (size_t)reps + 1);

@@ -30,6 +30,11 @@ def _dev(a):
     return torch.as_tensor(np.ascontiguousarray(a)).cuda()
 
 
+def torch_cpu(a):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(a))
+
+
 def _matrix(pcg, A, fmt="auto"):
     return pcg.Matrix.from_csr(_dev(A.row_ptr), _dev(A.col), _dev(A.val), fmt=fmt)
 
@@ -46,7 +51,7 @@ CASES = [("C1", None), ("C2", 96), ("C3", 48), ("C5", 32), ("C4", 16)]
 
 
 @pytest.mark.parametrize("name,c", CASES)
-@pytest.mark.parametrize("fmt", ["auto", "csr", "sell", "tma"])
+@pytest.mark.parametrize("fmt", ["auto", "csr", "sell", "tma", "sigma"])
 def test_spmv_parity(pcg, name, c, fmt):
     P = O.build_problem(name, c=c, k=1)
     A = P["A"]
@@ -56,7 +61,12 @@ def test_spmv_parity(pcg, name, c, fmt):
     yo = O.spmv(A, x)
     assert np.all(np.abs(y - yo) <= _spmv_bound(A, x))
     if fmt != "auto":
-        assert M.stats()["format"] == {"csr": 1, "sell": 2, "tma": 3}[fmt]
+        assert M.stats()["format"] == {"csr": 1, "sell": 2, "tma": 3, "sigma": 4}[fmt]
+    if fmt == "sigma":  # rows keep their entry order: bitwise the natural SELL SpMV
+        ys = _matrix(pcg, A, "sell").spmv(_dev(x)).cpu().numpy()
+        assert np.array_equal(y, ys)
+        yh = M.spmv(torch_cpu(x)).numpy()  # host pointers through the permutation
+        assert np.array_equal(yh, y)
 
 
 @pytest.mark.parametrize("name,c", CASES)
@@ -230,3 +240,31 @@ def test_generator_structure_parity(pcg, name, c):
     assert B.shape == P["B"].shape
     scale = np.max(np.abs(P["B"]), axis=0)
     assert np.all(np.abs(B - P["B"]) <= 1e-12 * scale[None, :])
+
+
+@pytest.mark.parametrize("name,c", [("C3", 48), ("C2", 64), ("C1", None)])
+def test_sigma_pcg_parity(pcg, name, c):
+    """SELL-C-sigma (symmetric permutation P A P^T inside the library) against the oracle;
+    host and device pointers; multi-RHS through the same permuted handle."""
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    tol = O.configs()[name]["tol"]
+    r = O.pcg(A, b, tol=tol)
+    M = _matrix(pcg, A, "sigma")
+    st = M.stats()
+    assert st["format"] == 4 and st["sigma"] >= 64
+    for bb in (_dev(b), torch_cpu(b)):
+        x, info = M.solve(bb, tol=tol)
+        x = x.cpu().numpy()
+        assert info["status"] == 0 and info["relres_true"] <= tol
+        assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) <= 1e-9
+        assert abs(info["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
+    rng = np.random.default_rng(1)
+    B = np.column_stack([b, rng.standard_normal(A.n), np.zeros(A.n)])
+    X, infos = M.solve_multi(_dev(B), tol=tol)
+    X = X.cpu().numpy()
+    assert infos[2]["iterations"] == 0 and np.all(X[:, 2] == 0)
+    for j in range(2):
+        rj = O.pcg(A, B[:, j], tol=tol)
+        assert np.linalg.norm(X[:, j] - rj.x) / np.linalg.norm(rj.x) <= 1e-9
+        assert abs(infos[j]["iterations"] - rj.iterations) <= max(1, 0.02 * rj.iterations)
