@@ -141,6 +141,29 @@ pcg_status pcg_partition_rows(int64_t n, const int64_t *row_ptr, int32_t G, int6
 pcg_status pcg_comm_unique_id(void *id128);
 pcg_status pcg_comm_init(int32_t rank, int32_t size, const void *id128, pcg_comm_t *out);
 pcg_status pcg_comm_destroy(pcg_comm_t comm);
+
+/* Host-callback communicator: the same distributed path (csr_create_dist, pcg_solve,
+ * pcg_spmv) with every exchange step done by caller-supplied host functions instead of
+ * NCCL; device data is staged through host memory around each call and the
+ * iteration loop runs without CUDA graphs.  Meant for validating the multi-GPU code
+ * path where ranks cannot each have their own GPU (e.g. several processes sharing
+ * one GPU, exchanging over torch.distributed gloo) — never a performance path.
+ * All buffers are HOST memory; every callback returns 0 on success.
+ *   allreduce_sum_f64: in-place elementwise sum over ranks of buf[0..count)
+ *   allreduce_max_i32: in-place elementwise max over ranks
+ *   allgather_i64:     all[r*count + i] = rank r's mine[i]
+ *   exchange:          for each listed peer p: send send_bytes[p] bytes from send[p] to
+ *                      peers[p] and receive recv_bytes[p] bytes from peers[p] into recv[p]
+ *                      (all pairs posted together; counts match the peer's). */
+typedef struct {
+  void *ctx;
+  int (*allreduce_sum_f64)(void *ctx, double *buf, int64_t count);
+  int (*allreduce_max_i32)(void *ctx, int32_t *buf, int64_t count);
+  int (*allgather_i64)(void *ctx, const int64_t *mine, int64_t count, int64_t *all);
+  int (*exchange)(void *ctx, int32_t n_peers, const int32_t *peers, const void *const *send,
+                  const int64_t *send_bytes, void *const *recv, const int64_t *recv_bytes);
+} pcg_comm_ops;
+pcg_status pcg_comm_init_ops(int32_t rank, int32_t size, const pcg_comm_ops *ops, pcg_comm_t *out);
 /* Distributed matrix: this rank owns rows [row_begin, row_end) of the global n_global x
  * n_global matrix; row_ptr_local (row_end-row_begin+1, starting at 0), global col_idx.
  * Collective over comm (halo lists are exchanged).  pcg_solve / pcg_spmv on the

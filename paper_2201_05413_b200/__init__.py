@@ -187,6 +187,79 @@ class Comm:
         dist.broadcast_object_list(obj, src=0, group=group)
         return cls(rank, size, obj[0])
 
+    @classmethod
+    def host_callbacks(cls, group=None) -> "Comm":
+        """Communicator whose exchange steps run as host callbacks over a torch.distributed
+        process group (e.g. gloo): the library's distributed path with device data staged
+        through host memory.  For validating that path where ranks share one GPU; the
+        product path is NCCL (from_process_group)."""
+        import torch
+        import torch.distributed as dist
+        rank, size = dist.get_rank(group), dist.get_world_size(group)
+
+        def _arr(ptr, count, dtype):
+            return np.ctypeslib.as_array(ptr, shape=(count,)) if count > 0 else np.zeros(0, dtype)
+
+        def allreduce_f64(ctx, buf, count):
+            try:
+                a = _arr(buf, count, np.float64)
+                t = torch.from_numpy(a.copy())
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+                a[:] = t.numpy()
+                return 0
+            except Exception:
+                return 1
+
+        def allreduce_max(ctx, buf, count):
+            try:
+                a = _arr(buf, count, np.int32)
+                t = torch.from_numpy(a.copy())
+                dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+                a[:] = t.numpy()
+                return 0
+            except Exception:
+                return 1
+
+        def allgather(ctx, mine, count, out):
+            try:
+                m = torch.from_numpy(_arr(mine, count, np.int64).copy())
+                parts = [torch.empty_like(m) for _ in range(size)]
+                dist.all_gather(parts, m, group=group)
+                _arr(out, count * size, np.int64)[:] = torch.cat(parts).numpy()
+                return 0
+            except Exception:
+                return 1
+
+        def exchange(ctx, n_peers, peers, send, send_bytes, recv, recv_bytes):
+            try:
+                reqs, outs = [], []
+                for t in range(n_peers):
+                    p = int(peers[t])
+                    sb, rb = int(send_bytes[t]), int(recv_bytes[t])
+                    if sb > 0:
+                        buf = (C.c_uint8 * sb).from_address(send[t])
+                        reqs.append(dist.isend(torch.frombuffer(bytearray(buf), dtype=torch.uint8), p, group=group))
+                    if rb > 0:
+                        r = torch.empty(rb, dtype=torch.uint8)
+                        reqs.append(dist.irecv(r, p, group=group))
+                        outs.append((recv[t], r))
+                for q in reqs:
+                    q.wait()
+                for addr, r in outs:
+                    C.memmove(addr, r.numpy().ctypes.data, r.numel())
+                return 0
+            except Exception:
+                return 1
+
+        ops = _lib.CommOps(None, _lib.ALLREDUCE_F64(allreduce_f64), _lib.ALLREDUCE_MAX_I32(allreduce_max),
+                           _lib.ALLGATHER_I64(allgather), _lib.EXCHANGE(exchange))
+        self = cls.__new__(cls)
+        self._h = C.c_void_p()
+        self._ops = ops  # keep the callbacks alive as long as the communicator
+        check(lib().pcg_comm_init_ops(rank, size, C.byref(ops), C.byref(self._h)), "pcg_comm_init_ops")
+        self.rank, self.size = rank, size
+        return self
+
     def close(self):
         if self._h and self._h.value:
             lib().pcg_comm_destroy(self._h)

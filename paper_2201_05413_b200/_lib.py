@@ -45,6 +45,19 @@ class MatrixStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+# host-callback communicator (include/pcg.h pcg_comm_ops)
+ALLREDUCE_F64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+ALLREDUCE_MAX_I32 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int32), C.c_int64)
+ALLGATHER_I64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int64), C.c_int64, C.POINTER(C.c_int64))
+EXCHANGE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                       C.POINTER(C.c_int64), C.POINTER(C.c_void_p), C.POINTER(C.c_int64))
+
+
+class CommOps(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allreduce_sum_f64", ALLREDUCE_F64), ("allreduce_max_i32", ALLREDUCE_MAX_I32),
+                ("allgather_i64", ALLGATHER_I64), ("exchange", EXCHANGE)]
+
+
 class FemSpec(C.Structure):
     _fields_ = [("family", C.c_int32), ("c", C.c_int32), ("jitter", C.c_int32),
                 ("fkind", C.c_int32), ("gkind", C.c_int32), ("policy", C.c_int32),
@@ -76,6 +89,7 @@ def lib():
         "pcg_halo_ghosts": [i64, i64, i64, vp, vp, i64, P(i64)],
         "pcg_halo_recv_plan": [i64, vp, i32, vp, vp, vp],
         "pcg_comm_init": [i32, i32, vp, P(vp)],
+        "pcg_comm_init_ops": [i32, i32, P(CommOps), P(vp)],
         "pcg_comm_destroy": [vp],
         "csr_create_dist": [vp, i64, i64, i64, i64, vp, vp, vp, C.c_int, vp, P(vp)],
         "pcg_profile_kernels": [vp, vp, i32, vp, vp, P(i32)],

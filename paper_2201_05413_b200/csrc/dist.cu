@@ -68,6 +68,109 @@ __global__ void to_local_rows_kernel(int64_t m, const int64_t *__restrict__ g, i
     out[s] = (int)(g[s] - r0);
 }
 
+// ---------------------------------------------------------------- communicator backends
+// NCCL (the product path, stream-ordered and graph-capturable) or caller-supplied
+// host callbacks (pcg_comm_init_ops: device data staged through host memory).
+bool comm_uses_graphs(const pcg_comm *c) { return c && !c->use_ops; }
+
+#define PCG_OPS(call, what)                                                             \
+  do {                                                                                  \
+    if ((call) != 0) return ::pcgb::fail(PCG_ERR_NCCL, std::string(what) + ": host communicator callback failed"); \
+  } while (0)
+
+static pcg_status comm_allreduce_f64(pcg_comm *C, double *dbuf, int count, cudaStream_t st) {
+  if (C->size == 1 || count == 0) return PCG_OK;
+  if (!C->use_ops) {
+    PCG_NCCL(ncclAllReduce(dbuf, dbuf, (size_t)count, ncclDouble, ncclSum, C->nccl, st));
+    return PCG_OK;
+  }
+  std::vector<double> h(count);
+  PCG_CUDA(cudaMemcpyAsync(h.data(), dbuf, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_OPS(C->ops.allreduce_sum_f64(C->ops.ctx, h.data(), count), "allreduce_sum_f64");
+  PCG_CUDA(cudaMemcpyAsync(dbuf, h.data(), sizeof(double) * count, cudaMemcpyHostToDevice, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  return PCG_OK;
+}
+
+static pcg_status comm_allreduce_max_i32(pcg_comm *C, int *dbuf, int count, cudaStream_t st) {
+  if (C->size == 1 || count == 0) return PCG_OK;
+  if (!C->use_ops) {
+    PCG_NCCL(ncclAllReduce(dbuf, dbuf, (size_t)count, ncclInt32, ncclMax, C->nccl, st));
+    return PCG_OK;
+  }
+  std::vector<int32_t> h(count);
+  PCG_CUDA(cudaMemcpyAsync(h.data(), dbuf, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_OPS(C->ops.allreduce_max_i32(C->ops.ctx, h.data(), count), "allreduce_max_i32");
+  PCG_CUDA(cudaMemcpyAsync(dbuf, h.data(), sizeof(int32_t) * count, cudaMemcpyHostToDevice, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  return PCG_OK;
+}
+
+// all[r*count + i] = rank r's mine[i]; mine is C->rank's slot of all (device)
+static pcg_status comm_allgather_i64(pcg_comm *C, int64_t *dall, int count, cudaStream_t st) {
+  if (C->size == 1) return PCG_OK;
+  if (!C->use_ops) {
+    PCG_NCCL(ncclAllGather(dall + (size_t)count * C->rank, dall, (size_t)count, ncclInt64, C->nccl, st));
+    return PCG_OK;
+  }
+  std::vector<int64_t> mine(count), all((size_t)count * C->size);
+  PCG_CUDA(cudaMemcpyAsync(mine.data(), dall + (size_t)count * C->rank, sizeof(int64_t) * count,
+                           cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_OPS(C->ops.allgather_i64(C->ops.ctx, mine.data(), count, all.data()), "allgather_i64");
+  PCG_CUDA(cudaMemcpyAsync(dall, all.data(), sizeof(int64_t) * all.size(), cudaMemcpyHostToDevice, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  return PCG_OK;
+}
+
+struct Xfer {
+  int peer;
+  const void *send;  // device
+  int64_t scount;    // elements
+  void *recv;        // device
+  int64_t rcount;
+};
+
+// grouped point-to-point exchange of `esize`-byte elements (NCCL type `ty`)
+static pcg_status comm_exchange(pcg_comm *C, const std::vector<Xfer> &xs, ncclDataType_t ty, size_t esize,
+                                cudaStream_t st) {
+  if (xs.empty()) return PCG_OK;
+  if (!C->use_ops) {
+    PCG_NCCL(ncclGroupStart());
+    for (const Xfer &x : xs) {
+      if (x.scount > 0) PCG_NCCL(ncclSend(x.send, (size_t)x.scount, ty, x.peer, C->nccl, st));
+      if (x.rcount > 0) PCG_NCCL(ncclRecv(x.recv, (size_t)x.rcount, ty, x.peer, C->nccl, st));
+    }
+    PCG_NCCL(ncclGroupEnd());
+    return PCG_OK;
+  }
+  const size_t np = xs.size();
+  std::vector<std::vector<char>> hs(np), hr(np);
+  std::vector<const void *> sp(np);
+  std::vector<void *> rp(np);
+  std::vector<int64_t> sb(np), rb(np);
+  std::vector<int32_t> peers(np);
+  for (size_t t = 0; t < np; t++) {
+    peers[t] = xs[t].peer;
+    sb[t] = xs[t].scount * (int64_t)esize;
+    rb[t] = xs[t].rcount * (int64_t)esize;
+    hs[t].resize(sb[t] > 0 ? sb[t] : 1);
+    hr[t].resize(rb[t] > 0 ? rb[t] : 1);
+    sp[t] = hs[t].data();
+    rp[t] = hr[t].data();
+    if (sb[t] > 0) PCG_CUDA(cudaMemcpyAsync(hs[t].data(), xs[t].send, sb[t], cudaMemcpyDeviceToHost, st));
+  }
+  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_OPS(C->ops.exchange(C->ops.ctx, (int32_t)np, peers.data(), sp.data(), sb.data(), rp.data(), rb.data()),
+          "exchange");
+  for (size_t t = 0; t < np; t++)
+    if (rb[t] > 0) PCG_CUDA(cudaMemcpyAsync(xs[t].recv, hr[t].data(), rb[t], cudaMemcpyHostToDevice, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  return PCG_OK;
+}
+
 pcg_status halo_exchange(pcg_matrix *A, double *vec, int width, cudaStream_t st) {
   (void)width;
   if (!A->comm || A->halo.nbr.empty()) return PCG_OK;
@@ -77,23 +180,16 @@ pcg_status halo_exchange(pcg_matrix *A, double *vec, int width, cudaStream_t st)
                                                                                           vec, hp.d_send_buf);
     count_launch();
   }
-  PCG_NCCL(ncclGroupStart());
-  for (size_t t = 0; t < hp.nbr.size(); t++) {
-    if (hp.send_cnt[t] > 0)
-      PCG_NCCL(ncclSend(hp.d_send_buf + hp.send_off[t], (size_t)hp.send_cnt[t], ncclDouble, hp.nbr[t],
-                        A->comm->nccl, st));
-    if (hp.recv_cnt[t] > 0)
-      PCG_NCCL(ncclRecv(vec + A->n + hp.recv_off[t], (size_t)hp.recv_cnt[t], ncclDouble, hp.nbr[t], A->comm->nccl,
-                        st));
-  }
-  PCG_NCCL(ncclGroupEnd());
-  return PCG_OK;
+  std::vector<Xfer> xs;
+  for (size_t t = 0; t < hp.nbr.size(); t++)
+    xs.push_back({hp.nbr[t], hp.d_send_buf + hp.send_off[t], hp.send_cnt[t], vec + A->n + hp.recv_off[t],
+                  hp.recv_cnt[t]});
+  return comm_exchange(A->comm, xs, ncclDouble, sizeof(double), st);
 }
 
 pcg_status allreduce_sum(pcg_matrix *A, double *buf, int count, cudaStream_t st) {
   if (!A->comm || A->comm->size == 1) return PCG_OK;
-  PCG_NCCL(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, A->comm->nccl, st));
-  return PCG_OK;
+  return comm_allreduce_f64(A->comm, buf, count, st);
 }
 
 static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, int64_t r1, int64_t nnz,
@@ -162,7 +258,7 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
   PCG_CUDA(cudaMalloc(&d_bounds, sizeof(int64_t) * 2 * G));
   int64_t mine[2] = {r0, r1};
   PCG_CUDA(cudaMemcpyAsync(d_bounds + 2 * me, mine, sizeof(mine), cudaMemcpyHostToDevice, st));
-  PCG_NCCL(ncclAllGather(d_bounds + 2 * me, d_bounds, 2, ncclInt64, C->nccl, st));
+  PCG_TRY(comm_allgather_i64(C, d_bounds, 2, st));
   std::vector<int64_t> hb(2 * G);
   PCG_CUDA(cudaMemcpyAsync(hb.data(), d_bounds, sizeof(int64_t) * 2 * G, cudaMemcpyDeviceToHost, st));
   PCG_CUDA(cudaStreamSynchronize(st));
@@ -179,7 +275,7 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
   int64_t *d_M;
   PCG_CUDA(cudaMalloc(&d_M, sizeof(int64_t) * G * G));
   PCG_CUDA(cudaMemcpyAsync(d_M + (size_t)G * me, need.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, st));
-  PCG_NCCL(ncclAllGather(d_M + (size_t)G * me, d_M, G, ncclInt64, C->nccl, st));
+  PCG_TRY(comm_allgather_i64(C, d_M, G, st));
   std::vector<int64_t> M((size_t)G * G);
   PCG_CUDA(cudaMemcpyAsync(M.data(), d_M, sizeof(int64_t) * G * G, cudaMemcpyDeviceToHost, st));
   PCG_CUDA(cudaStreamSynchronize(st));
@@ -203,12 +299,12 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
   PCG_CUDA(cudaMalloc(&d_recv_idx, sizeof(int64_t) * (ng > 0 ? ng : 1)));
   PCG_CUDA(cudaMalloc(&d_send_g, sizeof(int64_t) * (send_total > 0 ? send_total : 1)));
   if (ng) PCG_CUDA(cudaMemcpyAsync(d_recv_idx, h_ghost.data(), sizeof(int64_t) * ng, cudaMemcpyHostToDevice, st));
-  PCG_NCCL(ncclGroupStart());
-  for (size_t t = 0; t < hp.nbr.size(); t++) {
-    if (hp.recv_cnt[t]) PCG_NCCL(ncclSend(d_recv_idx + hp.recv_off[t], hp.recv_cnt[t], ncclInt64, hp.nbr[t], C->nccl, st));
-    if (hp.send_cnt[t]) PCG_NCCL(ncclRecv(d_send_g + hp.send_off[t], hp.send_cnt[t], ncclInt64, hp.nbr[t], C->nccl, st));
+  {  // every rank sends the global ids it needs from a peer; what arrives is the peer's send list
+    std::vector<Xfer> xs;
+    for (size_t t = 0; t < hp.nbr.size(); t++)
+      xs.push_back({hp.nbr[t], d_recv_idx + hp.recv_off[t], hp.recv_cnt[t], d_send_g + hp.send_off[t], hp.send_cnt[t]});
+    PCG_TRY(comm_exchange(C, xs, ncclInt64, sizeof(int64_t), st));
   }
-  PCG_NCCL(ncclGroupEnd());
   PCG_CUDA(cudaMalloc(&hp.d_send_idx, sizeof(int) * (send_total > 0 ? send_total : 1)));
   PCG_CUDA(cudaMalloc(&hp.d_send_buf, sizeof(double) * KMAX * (send_total > 0 ? send_total : 1)));
   if (send_total) {
@@ -232,7 +328,7 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
     int hs = (int)s;
     if (cudaMalloc(&d_s, sizeof(int)) == cudaSuccess) {
       cudaMemcpyAsync(d_s, &hs, sizeof(int), cudaMemcpyHostToDevice, st);
-      ncclAllReduce(d_s, d_s, 1, ncclInt32, ncclMax, C->nccl, st);
+      (void)comm_allreduce_max_i32(C, d_s, 1, st);
       int all = 0;
       cudaMemcpyAsync(&all, d_s, sizeof(int), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
@@ -314,6 +410,19 @@ extern "C" pcg_status pcg_comm_init(int32_t rank, int32_t size, const void *id12
     delete c;
     return fail(PCG_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   }
+  *out = c;
+  return PCG_OK;
+}
+
+extern "C" pcg_status pcg_comm_init_ops(int32_t rank, int32_t size, const pcg_comm_ops *ops, pcg_comm_t *out) {
+  if (!ops || !out || size < 1 || rank < 0 || rank >= size || !ops->allreduce_sum_f64 || !ops->allreduce_max_i32 ||
+      !ops->allgather_i64 || !ops->exchange)
+    return fail(PCG_ERR_INVALID_ARG, "pcg_comm_init_ops: bad argument");
+  pcg_comm *c = new pcg_comm();
+  c->rank = rank;
+  c->size = size;
+  c->use_ops = true;
+  c->ops = *ops;
   *out = c;
   return PCG_OK;
 }

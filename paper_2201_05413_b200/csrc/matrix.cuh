@@ -7,9 +7,11 @@
 #include "common.cuh"
 
 struct pcg_comm {
-  ncclComm_t nccl = nullptr;
+  ncclComm_t nccl = nullptr;   // NCCL backend (null when ops are used)
   int rank = 0, size = 1;
   cudaStream_t comm_stream = nullptr;
+  bool use_ops = false;        // host-callback backend (pcg_comm_init_ops)
+  pcg_comm_ops ops{};
 };
 
 namespace pcgb {
@@ -118,5 +120,6 @@ void free_work(pcg_matrix *A);
 pcg_status launch_spmv(pcg_matrix *A, const double *x, double *y, cudaStream_t st);
 pcg_status halo_exchange(pcg_matrix *A, double *vec, int width, cudaStream_t st);
 pcg_status allreduce_sum(pcg_matrix *A, double *buf, int count, cudaStream_t st);
+bool comm_uses_graphs(const pcg_comm *c);
 bool is_device_ptr(const void *p);
 }  // namespace pcgb

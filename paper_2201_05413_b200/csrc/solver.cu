@@ -615,6 +615,12 @@ static pcg_status launch_resid(pcg_matrix *A, const double *b, int mode, cudaStr
 static pcg_status build_loop_graph(pcg_matrix *A) {
   SolveWork &w = A->work;
   if (w.graph_ready) return PCG_OK;
+  if (A->comm && !comm_uses_graphs(A->comm)) {  // host-callback communicator: direct launches
+    w.graph_kind = 3;
+    w.unroll = 8;
+    w.graph_ready = true;
+    return PCG_OK;
+  }
   cudaStream_t cap;
   PCG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
   cudaGraph_t g;
@@ -734,7 +740,14 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
         PCG_CUDA(cudaMemcpyAsync(h, w.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
         PCG_CUDA(cudaStreamSynchronize(st));
         if (h->done != DONE_RUNNING) break;
-        PCG_CUDA(cudaGraphLaunch(w.loop_exec, st));
+        if (w.graph_kind == 2) {
+          PCG_CUDA(cudaGraphLaunch(w.loop_exec, st));
+        } else {  // 3: the same iterations launched directly (collectives through host callbacks)
+          for (int u = 0; u < w.unroll; u++) {
+            PCG_TRY(launch_k1(A, st, 0, 0));
+            PCG_TRY(launch_k2(A, st, 0, 0));
+          }
+        }
       }
     }
     tail_kernel<<<A->grid_vec, BLOCK, 0, st>>>(n, vecs_of(A), w.sc);

@@ -16,7 +16,7 @@ def _declared_functions():
     for h in ("pcg.h", "fem_gen.h"):
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-        names += re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*([a-z_0-9]+)\s*\(", src, flags=re.M)
+        names += re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+(?:\s+|\s*\*\s*)([a-z_0-9]+)\s*\(", src, flags=re.M)
     return sorted(set(names))
 
 

@@ -1,0 +1,120 @@
+"""The library's DISTRIBUTED path (csr_create_dist, halo plan, pack kernel, ghost
+advance of p, distributed finishers, pcg_solve / pcg_spmv on local rows) run for
+real on the GPU by 2-3 processes that share cuda:0.  This run has one GPU, and
+NCCL refuses two ranks on one device, so the exchange steps go through the
+library's host-callback communicator (pcg_comm_init_ops) over torch.distributed
+gloo; every kernel and every line of host planning is the NCCL path's own.  The
+per-rank results are gathered and compared with the oracle on the undivided
+system (parity bars of DESIGN.md §5), and the plan with the oracle's halo lists.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, c, use_generator, out_q):
+    import torch
+    import torch.distributed as dist
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_2201_05413_b200 as pcg
+        P = O.build_problem(name, c=c, k=1)
+        A, b = P["A"], P["B"][:, 0]
+        bounds = pcg.partition_rows(A.row_ptr, world)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        comm = pcg.Comm.host_callbacks()
+        if use_generator:  # bench.py's path: rows generated on the device
+            spec = pcg.fem_spec(name, c=c)
+            G = pcg.fem_build(spec, r0, r1)
+            rp, col, val, bl = G["row_ptr"], G["col"], G["val"], G["B"][:, 0].contiguous()
+        else:
+            rp = torch.as_tensor(A.row_ptr[r0:r1 + 1] - A.row_ptr[r0]).cuda()
+            col = torch.as_tensor(A.col[A.row_ptr[r0]:A.row_ptr[r1]]).cuda()
+            val = torch.as_tensor(A.val[A.row_ptr[r0]:A.row_ptr[r1]]).cuda()
+            bl = torch.as_tensor(b[r0:r1]).cuda()
+        M = pcg.Matrix.from_csr_dist(comm, A.n, r0, r1, rp, col, val)
+        st = M.stats()
+        x, info = M.solve(bl, tol=1e-10)
+        xr = np.random.default_rng(100 + rank).standard_normal(r1 - r0)
+        y = M.spmv(torch.as_tensor(xr).cuda()).cpu().numpy()
+        out_q.put((rank, dict(r0=r0, r1=r1, n_ghost=st["n_ghost"], x=x.cpu().numpy(), info=info, xr=xr, y=y,
+                              b=bl.cpu().numpy())))
+        M.close()
+        comm.close()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        out_q.put((rank, {"error": f"{e!r}\n{traceback.format_exc()}"}))
+
+
+def _run(world, name, c, use_generator=False):
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, c, use_generator, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, d = q.get(timeout=600)
+        res[r] = d
+    for p in procs:
+        p.join(timeout=120)
+    for r, d in res.items():
+        assert "error" not in d, d.get("error")
+    return [res[r] for r in range(world)]
+
+
+@pytest.mark.parametrize("world,name,c,gen", [(2, "C2", 48, False), (3, "C3", 24, False), (2, "C5", 32, True),
+                                              (3, "C1", None, False)])
+def test_distributed_path_on_one_gpu(world, name, c, gen):
+    parts = _run(world, name, c, gen)
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    tol = O.configs()[name]["tol"]
+    # plan: contiguous row blocks of the partition rule, ghost counts == oracle halo lists
+    bounds = O.partition(A, world)
+    for g, d in enumerate(parts):
+        assert (d["r0"], d["r1"]) == (bounds[g], bounds[g + 1])
+        assert d["n_ghost"] == len(O.halo(A, d["r0"], d["r1"]))
+    bg = np.concatenate([d["b"] for d in parts])
+    scale = np.max(np.abs(b))
+    assert np.all(np.abs(bg - b) <= 1e-12 * scale)  # generator RHS (exact copy otherwise)
+    # distributed SpMV == oracle SpMV rows, within the forward-error bound of any summation order
+    xr = np.concatenate([d["xr"] for d in parts])
+    y = np.concatenate([d["y"] for d in parts])
+    yo = O.spmv(A, xr)
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    mag = np.bincount(rows, weights=np.abs(A.val) * np.abs(xr)[A.col], minlength=A.n)
+    assert np.all(np.abs(y - yo) <= 2 * np.diff(A.row_ptr) * U * mag * (1 + 1e-9) + (1e-13 * mag if gen else 0))
+    # distributed PCG == oracle PCG (same recurrence, reduction order differs)
+    r = O.pcg(A, bg, tol=tol)
+    x = np.concatenate([d["x"] for d in parts])
+    its = {d["info"]["iterations"] for d in parts}
+    assert len(its) == 1  # every rank ran the same number of iterations
+    it = its.pop()
+    assert all(d["info"]["status"] == 0 and d["info"]["relres_true"] <= tol for d in parts)
+    assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) <= 1e-9
+    assert abs(it - r.iterations) <= max(1, 0.02 * r.iterations), (it, r.iterations)
