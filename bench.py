@@ -9,8 +9,12 @@ One "step" = one full pcg_solve (init, all iterations, exit check) from x0 = 0 o
 the device-resident system.  `value` is the device-timed time-to-solution (CUDA
 events, max over ranks).  `e2e` repeats it through the same public API with
 pinned HOST b and x (H2D of b, x0 and D2H of x inside the timed region).
-The roofline object reports the dominant fused kernel (K1: SpMV + p/x updates +
-sigma) against the measured HBM copy bandwidth in MEASURED_PEAKS.json.
+The roofline object reports the dominant kernel (K1b: SpMV + sigma) against the
+measured HBM copy bandwidth in MEASURED_PEAKS.json.
+
+--config C4 (k = 16 right-hand sides) times pcg_solve_multi instead (a step = one
+multi-RHS solve of all 16 columns; roofline = the SpMM pass).  The driver's
+default line is C5.
 """
 from __future__ import annotations
 
@@ -225,7 +229,10 @@ def main():
         P = fem_build(spec, r0, r1)
         comm = pcg.Comm.from_process_group()
         A = pcg.Matrix.from_csr_dist(comm, n, r0, r1, P["row_ptr"], P["col"], P["val"], fmt=args.fmt)
-    b = P["B"][:, 0].contiguous()
+    kcols = P["B"].shape[1]
+    multi = kcols > 1
+    b = P["B"][:, 0].contiguous() if not multi else None
+    Bm = P["B"].t().contiguous().t() if multi else None  # (n, k) view of a column-major block
     del P
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -244,20 +251,28 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def step(bb, out):
+        if multi:
+            X, infos = A.solve_multi(bb, tol=tol, max_iter=max_iter, out=out)
+            return X, infos
+        x, inf = A.solve(bb, tol=tol, max_iter=max_iter, out=out)
+        return x, [inf]
+
     # ---- warm-up
-    info = None
     for _ in range(args.warmup):
-        x, info = A.solve(b, tol=tol, max_iter=max_iter)
+        step(Bm if multi else b, None)
 
     # ---- timed region (device-resident inputs); re-measured once if clocks were bad
     def timed(device_inputs: bool):
         st = torch.cuda.current_stream()
+        src = Bm if multi else b
         if device_inputs:
-            bb = b
-            xx = torch.empty_like(b)
+            bb = src
+            xx = torch.empty_like(src.t().contiguous()).t() if multi else torch.empty_like(src)
         else:  # pinned host buffers, allocated outside the timed region
-            bb = b.cpu().pin_memory()
-            xx = torch.empty(bb.shape, dtype=torch.float64).pin_memory()
+            bb = (src.t().cpu().pin_memory().t()) if multi else src.cpu().pin_memory()
+            xx = (torch.empty(src.shape[::-1], dtype=torch.float64).pin_memory().t() if multi
+                  else torch.empty(src.shape, dtype=torch.float64).pin_memory())
         barrier()
         l0 = pcg.kernel_launches()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -266,7 +281,7 @@ def main():
             infos = []
             for _ in range(args.steps):
                 xx.zero_()  # x0 = 0 every step (host memset for the e2e leg)
-                x, inf = A.solve(bb, tol=tol, max_iter=max_iter, out=xx)  # host: H2D b, x0 + D2H x inside
+                x, inf = step(bb, xx)  # host buffers: H2D b, x0 + D2H x inside the library call
                 infos.append(inf)
             e1.record(st)
             barrier()
@@ -278,7 +293,7 @@ def main():
     if cs.bad():
         ms, infos, launches, cs, x = timed(True)
         remeasured = True
-    iters = infos[-1]["iterations"]
+    iters = max(i["iterations"] for i in infos[-1])  # block iterations (max over columns)
     ms_e2e, infos_e2e, _, _, _ = timed(False)
 
     # ---- roofline of the dominant kernel (K1) + standalone SpMV bandwidth
@@ -286,7 +301,31 @@ def main():
     roof = None
     spmv_gbs = None
     k_us = None
-    if world == 1:
+    if world == 1 and multi:
+        import ctypes as C
+        us = (C.c_double * 3)()
+        done = C.c_int32()
+        Bc = Bm.t().contiguous()
+        pcg.check(pcg.lib().pcg_profile_multi(A._h, kcols, C.c_void_p(Bc.data_ptr()), n, 20,
+                                               C.c_void_p(torch.cuda.current_stream().cuda_stream), us,
+                                               C.byref(done)), "pcg_profile_multi")
+        mat = 12.0 * nnz + 4.0 * (n + 1)
+        names = ["mk1a_kernel (X += alpha P, P = Z + beta P; streaming, per column)",
+                 "mspmm_kernel (SpMM Q = A P over SELL-32, per-column sigma, grid finish -> alpha)",
+                 "mk2_kernel (R -= alpha Q, Z = dinv R, rho', gamma per column, finish -> beta)"]
+        byts = [40.0 * kcols * n, mat + 16.0 * kcols * n, 40.0 * kcols * n]
+        kern = [{"kernel": nm, "bytes_per_launch": bt, "us_per_launch": u, "achieved_GBps": bt / u / 1e3 if u else None}
+                for nm, bt, u in zip(names, byts, us)]
+        dom = max(kern, key=lambda d: d["us_per_launch"])
+        it_us = sum(us)
+        roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved_GBps"], "peak": hbm,
+                "unit": "GB/s", "frac": dom["achieved_GBps"] / hbm, "peak_source": peak_kind, "traffic": None,
+                "bytes_per_launch": dom["bytes_per_launch"], "us_per_launch": dom["us_per_launch"],
+                "kernels": kern, "schedule": 3,
+                "iteration": {"bytes": sum(byts), "us": it_us, "frac": sum(byts) / it_us / 1e3 / hbm,
+                              "frac_vs_88n_ideal": (mat + 88.0 * kcols * n) / it_us / 1e3 / hbm}}
+        k_us = list(us)
+    elif world == 1:
         import ctypes as C
         us = (C.c_double * 3)()
         done = C.c_int32()
@@ -346,24 +385,24 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = oracle_sample(args.config, args.sample_c)
         smp["c"] = args.sample_c
-        v = scale_to_workload(smp, n, nnz, iters)
+        v = scale_to_workload(smp, n, nnz, iters) * kcols  # the oracle solves the k columns one by one
         cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
                "sample": f"oracle/oracle.c Jacobi-PCG, 1 thread, {args.config} construction at c={args.sample_c} "
                          f"({smp['n']} unknowns, {smp['nnz']} nnz, {smp['iterations']} iterations, "
                          f"{smp['t_solve'][0]:.2f} s); scaled by per-iteration bytes x {iters} GPU iterations"}
 
     if rank == 0:
-        h2d = 16 * (r1 - r0)  # b and x0
-        d2h = 8 * (r1 - r0)   # x
+        h2d = 16 * (r1 - r0) * kcols  # b and x0 per column
+        d2h = 8 * (r1 - r0) * kcols   # x per column
         line = {
             "metric": "pcg_time_to_solution", "value": ms / 1e3, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(workload_config(args.config, c, n, nnz, world), iterations=iters,
-                           format={1: "csr", 2: "sell", 3: "sell_tma"}[stats["format"]], setup_s=round(t_setup, 3),
-                           relres_true=infos[-1]["relres_true"]),
+                           format={1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[stats["format"]], setup_s=round(t_setup, 3),
+                           relres_true=max(i["relres_true"] for i in infos[-1]), k_rhs=kcols),
             "throughput": {"cg_iterations_per_s": iters / (ms / 1e3),
-                           "effective_GBps": iter_bytes(n, nnz) * iters / (ms / 1e3) / 1e9,
+                           "effective_GBps": iter_bytes(n, nnz, kcols) * iters / (ms / 1e3) / 1e9,
                            "spmv_GBps": spmv_gbs, "spmv_frac_of_hbm": spmv_gbs / hbm if spmv_gbs else None},
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -140,16 +140,27 @@ class Matrix:
         d["status_name"] = _lib.STATUS[st]
         return x, d
 
-    def solve_multi(self, B, X0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None):
+    def solve_multi(self, B, X0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None, out=None):
         """k right-hand sides, B an (n, k) tensor (column-major storage is used at the ABI:
-        pass B as B.T.contiguous().T or let this wrapper arrange it)."""
+        pass B as B.T.contiguous().T or let this wrapper arrange it).  With `out` (an (n, k)
+        float64 column-major tensor on B's device, i.e. out.t() contiguous), out holds X0 on
+        entry and the solutions on return, and no copies are made around the library call."""
         torch = _torch()
-        B = _as_tensor(B, torch.float64)
+        if not isinstance(B, torch.Tensor):
+            B = _as_tensor(B, torch.float64)
         n, k = B.shape
         Bc = B.t().contiguous()  # (k, n) row-major == (n, k) column-major, ld = n
-        Xc = torch.zeros_like(Bc) if X0 is None else _as_tensor(X0, torch.float64).t().contiguous()
+        if out is not None:
+            if not out.t().is_contiguous() or out.shape != (n, k) or out.dtype != torch.float64:
+                raise ValueError("out must be an (n, k) float64 column-major tensor")
+            Xc = out.t()
+        else:
+            Xc = torch.zeros_like(Bc) if X0 is None else _as_tensor(X0, torch.float64).t().contiguous()
         if Bc.device.type == "cpu":
-            Bc, Xc = Bc.pin_memory(), Xc.pin_memory()
+            if not Bc.is_pinned():
+                Bc = Bc.pin_memory()
+            if not Xc.is_pinned():
+                Xc = Xc.pin_memory()
         infos = (_lib.PcgInfo * k)()
         st = lib().pcg_solve_multi(self._h, k, _ptr(Bc), n, _ptr(Xc), n, float(tol), int(max_iter),
                                    _stream_ptr(stream), infos)

@@ -168,15 +168,17 @@ __device__ __forceinline__ void reduce_partials(const double *partials, double (
     for (int i = 0; i < NV; i++) out[i] = v[i];
 }
 
-// streaming loads for matrix data (read once per pass, keep out of L1)
+// streaming loads for matrix data (read once per pass, keep out of L1).  volatile:
+// a non-volatile asm with no memory operand counts as side-effect free, and the
+// compiler may then hoist it out of the branch that guards its address.
 __device__ __forceinline__ double ld_stream(const double *p) {
   double v;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ int ld_stream(const int *p) {
   int v;
-  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 

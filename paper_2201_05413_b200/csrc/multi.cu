@@ -228,7 +228,7 @@ __device__ __forceinline__ double long_row_sum(const double *vp, const int *cp, 
 // Per (slice, column) the row values meet in a fixed xor tree and lane 0 adds
 // them to the warp's accumulator in slice order; warps are combined in order.
 template <int MODE, bool LONG>
-__global__ void __launch_bounds__(BLOCK) mspmm_kernel(SellView S, MVecs v, MultiScalars *sc, double *partials, int k,
+__global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, MVecs v, MultiScalars *sc, double *partials, int k,
                                                       int pf, int use_cond, cudaGraphConditionalHandle h) {
   constexpr int NV = MODE == MS_SPMM ? 1 : 3;
   __shared__ int s_act[KMAX];
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(BLOCK) mspmm_kernel(SellView S, MVecs v, Multi
         }
       cols_ready(j, S.zero);
       if (pf) {  // first touch of a gathered line is (mostly) its largest column: start every
-                 // column's fetch now so only the first gather round waits on HBM
+                      // column's fetch now so only the first gather round waits on HBM
         const int jl = j[len > 0 ? len - 1 : 0];
 #pragma unroll 1
         for (int c = 0; c < k; c++)
@@ -572,10 +572,12 @@ template <int MODE>
 static void launch_mspmm(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
   SolveWork &w = A->work;
   const int g = mgrid_spmm(A);
+  const SellView S = A->sell();
+  const MVecs v = mvecs_of(A);
   if (A->max_row_len > 8)
-    mspmm_kernel<MODE, true><<<g, BLOCK, 0, st>>>(A->sell(), mvecs_of(A), w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
+    mspmm_kernel<MODE, true><<<g, BLOCK, 0, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
   else
-    mspmm_kernel<MODE, false><<<g, BLOCK, 0, st>>>(A->sell(), mvecs_of(A), w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
+    mspmm_kernel<MODE, false><<<g, BLOCK, 0, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
 }
 
 static double *mpart_rz(pcg_matrix *A) { return A->work.mpart + (size_t)3 * KMAX * num_sms(A->device) * 8; }
