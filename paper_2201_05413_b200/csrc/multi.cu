@@ -243,6 +243,12 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
   if (threadIdx.x < KMAX) s_act[threadIdx.x] = threadIdx.x < k && (MODE == MS_RESID || vs->active[threadIdx.x]);
 
   for (int t = threadIdx.x; t < NV * WARPS * KMAX; t += BLOCK) (&s_red[0][0][0])[t] = 0.0;
+  extern __shared__ double s_acc[];  // MS_SPMM: [k][BLOCK] per-thread sigma partials
+  // MS_SPMM with k <= 16: per-thread sigma partials in shared memory (no per-slice warp
+  // reduction); larger k would cost occupancy, so those reduce per slice instead
+  const bool acc_smem = MODE == MS_SPMM && k <= 16;
+  if (acc_smem)
+    for (int t = threadIdx.x; t < k * BLOCK; t += BLOCK) s_acc[t] = 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t w0 = (int64_t)blockIdx.x * WARPS + wid, nw = (int64_t)gridDim.x * WARPS;
@@ -274,42 +280,53 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
           r[NV - 1] = bi * bi;
         }
       }
+      if (MODE == MS_SPMM && acc_smem) {  // per-thread running sum; lanes meet once, at the end
+        s_acc[c * BLOCK + threadIdx.x] += r[0];
+      } else {
 #pragma unroll
-      for (int i = 0; i < NV; i++) {
-        r[i] = warp_sum(r[i]);
-        if (lane == 0) s_red[i][wid][c] += r[i];
+        for (int i = 0; i < NV; i++) {
+          r[i] = warp_sum(r[i]);
+          if (lane == 0) s_red[i][wid][c] += r[i];
+        }
       }
     };
     if (!LONG || len <= 8) {  // fast path: the slice's entries stay in registers for all columns
       double a[8];
       int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-      for (int u = 0; u < 8; u++)
+      for (int u = 0; u < 8; u++) {
+        a[u] = 0.0;
         if (u < len) {
           a[u] = ld_stream(vp + (size_t)u * 32);
           j[u] = ld_stream(cp + (size_t)u * 32);
         }
+      }
       cols_ready(j, S.zero);
       if (pf) {  // first touch of a gathered line is (mostly) its largest column: start every
-                      // column's fetch now so only the first gather round waits on HBM
-        const int jl = j[len > 0 ? len - 1 : 0];
+                 // column's fetch now so only the first gather round waits on HBM
+        int jl = j[0];  // j[len - 1] without dynamic register indexing
+#pragma unroll
+        for (int u = 1; u < 8; u++) jl = u == len - 1 ? j[u] : jl;
 #pragma unroll 1
         for (int c = 0; c < k; c++)
           if (s_act[c]) prefetch_l2(G + (size_t)c * v.ld + jl);
       }
+      unsigned int off[8];  // byte offsets of the gathered entries (columns < 2^29)
+#pragma unroll
+      for (int u = 0; u < 8; u++) off[u] = (unsigned int)j[u] << 3;
       const int64_t ld = v.ld;
-      const double *Gc = G;
+      const char *Gb = reinterpret_cast<const char *>(G);
 #pragma unroll 1
-      for (int c = 0; c < k; c++, Gc += ld) {
+      for (int c = 0; c < k; c++, Gb += ld * 8) {
         if (!s_act[c]) continue;
         double g[8];
 #pragma unroll
-        for (int u = 0; u < 8; u++)
-          if (u < len) g[u] = __ldg(Gc + j[u]);
+        for (int u = 0; u < 8; u++) g[u] = u < len ? __ldg(reinterpret_cast<const double *>(Gb + off[u])) : 0.0;
+        // entries past the row's length are a = g = 0: fma(0, 0, s) == s exactly (s is never -0),
+        // so the unpredicated chain is bitwise the left-to-right sum over the row
         double sum = 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; u++)
-          if (u < len) sum = __fma_rn(a[u], g[u], sum);
+        for (int u = 0; u < 8; u++) sum = __fma_rn(a[u], g[u], sum);
         finish_col(c, sum);
       }
     } else {
@@ -318,6 +335,12 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
         if (!s_act[c]) continue;
         finish_col(c, long_row_sum(vp, cp, len, G + (size_t)c * v.ld, S.zero));
       }
+    }
+  }
+  if (acc_smem) {  // each warp folds its lanes' running sums (fixed xor tree)
+    for (int c = 0; c < k; c++) {
+      const double t = warp_sum(s_acc[c * BLOCK + threadIdx.x]);
+      if (lane == 0) s_red[0][wid][c] = t;
     }
   }
   __syncthreads();
@@ -545,11 +568,18 @@ static dim3 mgrid_vec(pcg_matrix *A, int k) {
 }
 
 // SpMM pass: persistent grid of SMs x resident blocks (<= 8 per SM: the partials capacity)
-static int mgrid_spmm(pcg_matrix *A) {
+static int mgrid_spmm(pcg_matrix *A, int k) {
+  static bool attr = false;  // up to 32 KB of per-thread sigma partials (k <= 16)
+  if (!attr) {
+    cudaFuncSetAttribute(mspmm_kernel<MS_SPMM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * BLOCK * 16);
+    cudaFuncSetAttribute(mspmm_kernel<MS_SPMM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * BLOCK * 16);
+    attr = true;
+  }
   int b = 0;
+  const size_t smem = k <= 16 ? sizeof(double) * BLOCK * k : 0;
   cudaError_t e = A->max_row_len > 8
-                      ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, mspmm_kernel<MS_SPMM, true>, BLOCK, 0)
-                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, mspmm_kernel<MS_SPMM, false>, BLOCK, 0);
+                      ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, mspmm_kernel<MS_SPMM, true>, BLOCK, smem)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, mspmm_kernel<MS_SPMM, false>, BLOCK, smem);
   if (e != cudaSuccess) {
     cudaGetLastError();
     b = 4;
@@ -571,13 +601,14 @@ static int spmm_prefetch() {
 template <int MODE>
 static void launch_mspmm(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
   SolveWork &w = A->work;
-  const int g = mgrid_spmm(A);
+  const int g = mgrid_spmm(A, k);
   const SellView S = A->sell();
   const MVecs v = mvecs_of(A);
+  const size_t smem = MODE == MS_SPMM && k <= 16 ? sizeof(double) * BLOCK * k : 0;
   if (A->max_row_len > 8)
-    mspmm_kernel<MODE, true><<<g, BLOCK, 0, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
+    mspmm_kernel<MODE, true><<<g, BLOCK, smem, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
   else
-    mspmm_kernel<MODE, false><<<g, BLOCK, 0, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
+    mspmm_kernel<MODE, false><<<g, BLOCK, smem, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
 }
 
 static double *mpart_rz(pcg_matrix *A) { return A->work.mpart + (size_t)3 * KMAX * num_sms(A->device) * 8; }
