@@ -510,6 +510,7 @@ void free_work(pcg_matrix *A) {
   if (w.sc) cudaFree(w.sc);
   if (w.h_sc) cudaFreeHost(w.h_sc);
   if (w.msc) cudaFree(w.msc);
+  if (w.pbar) cudaFree(w.pbar);
   if (w.h_msc) cudaFreeHost(w.h_msc);
   w = SolveWork();
 }

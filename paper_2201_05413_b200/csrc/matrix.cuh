@@ -49,6 +49,15 @@ struct SolveWork {
   cudaGraphExec_t mloop_exec = nullptr;
   cudaGraph_t mloop_graph = nullptr;
   int mgraph_k = 0;
+  // persistent cooperative solve (persist.cu)
+  void *pbar = nullptr;  // grid barrier state
+  int pgrid = 0;
+};
+
+// single-RHS solver vectors (p0/p1: direction double buffer of the 2-pass schedule)
+struct Vecs {
+  double *r, *z, *q, *p0, *p1, *x;
+  const double *dinv;
 };
 
 // a symmetrically permuted copy of the system (SELL-C-sigma, sigma.cu)
@@ -107,6 +116,8 @@ namespace pcgb {
 pcg_status ensure_work(pcg_matrix *A);
 pcg_status ensure_multi_work(pcg_matrix *A, int k);
 pcg_status build_sell(pcg_matrix *A, cudaStream_t st);
+bool persist_wanted(const pcg_matrix *A);
+pcg_status persist_launch(pcg_matrix *A, Vecs v, cudaStream_t st);
 int sigma_window();
 pcg_status sigma_build(pcg_matrix *A, cudaStream_t st, SigmaSys *S);
 void sigma_swap(pcg_matrix *A, SigmaSys *S);

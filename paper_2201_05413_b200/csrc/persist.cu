@@ -1,0 +1,247 @@
+// persist.cu — the whole Jacobi-PCG loop of a single-GPU solve as ONE
+// cooperative (co-resident, persistent) kernel.
+//
+// Same dataflow and bytes as the 3-pass schedule of solver.cu (K1a p/x update,
+// K1b SpMV + sigma, K2 r/z update + rho', gamma; 12 nnz + 4(n+1) + 96 n bytes per
+// iteration), but the three passes are separated by grid-wide barriers instead
+// of kernel boundaries, and the scalar recurrence (alpha, beta, the stop test of
+// SURVEY §8(c).8) is evaluated redundantly and identically by every block from
+// the fixed-order block partials — so there is no finisher, no launch and no
+// graph node per pass.  For systems whose passes take tens of microseconds
+// (C1-C4) the kernel boundaries, not HBM, set the iteration time; for C5 the
+// 3-pass graph is kept (the host picks by size, PCG_PERSIST overrides).
+//
+// Co-residency of all blocks is guaranteed by cudaLaunchCooperativeKernel with a
+// grid of at most (resident blocks per SM) x SMs; the barrier is a sense counter
+// in global memory.  One launch per solve (per residual replacement).
+#include <cstdlib>
+
+#include "matrix.cuh"
+#include "rows.cuh"
+
+namespace pcgb {
+
+struct GridBar {
+  unsigned int count;
+  unsigned int gen;
+};
+
+__device__ __forceinline__ void grid_sync(GridBar *b) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int *vgen = &b->gen;
+    const unsigned int g = *vgen;
+    __threadfence();
+    if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
+      b->count = 0;
+      __threadfence();
+      atomicAdd(&b->gen, 1u);
+    } else {
+      while (*vgen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// fixed-order sum of NV x gridDim.x partials, identical in every block; result in all threads
+template <int NV>
+__device__ __forceinline__ void all_blocks_sum(const double *part, double (&out)[NV], double (*sm)[WARPS],
+                                               double *s_tot) {
+  double v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; i++) {
+    double s = 0.0;
+    for (unsigned int b = threadIdx.x; b < gridDim.x; b += BLOCK) s += __ldcg(part + (size_t)i * gridDim.x + b);
+    v[i] = s;
+  }
+  block_sum<NV>(v, sm);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int i = 0; i < NV; i++) s_tot[i] = v[i];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; i++) out[i] = s_tot[i];
+  __syncthreads();
+}
+
+template <int FMT, int L>
+__global__ void __launch_bounds__(BLOCK, 3) pcg_persist_kernel(SellView S, CsrView C, Vecs v, Scalars *sc, double *part,
+                                                            GridBar *bar) {
+  __shared__ double sm[2][WARPS];
+  __shared__ double s_tot[2];
+  const int64_t n = FMT == PCG_FORMAT_SELL ? S.n : C.n;
+  // recurrence state: read once, then evolved identically by every block
+  double rho = sc->rho, beta = sc->beta, alpha = sc->alpha;
+  const double tol = sc->tol, nb = sc->nb;
+  long long k = sc->k;
+  const long long max_iter = sc->max_iter;
+  int done = sc->done;
+  double sigma = sc->sigma, gamma = sc->gamma, relres_rec = sc->relres_rec;
+  double *__restrict__ p = v.p0;
+  double *__restrict__ q = v.q;
+  const int64_t npair = n >> 1;
+  const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
+  double *part_s = part, *part_rz = part + gridDim.x;  // sigma | (rho', gamma)
+  while (done == DONE_RUNNING) {
+    // ---- K1a: p = z + beta p ; x += alpha_prev p_old
+    {
+      double2 *__restrict__ p2 = reinterpret_cast<double2 *>(p);
+      double2 *__restrict__ x2 = reinterpret_cast<double2 *>(v.x);
+      const double2 *__restrict__ z2 = reinterpret_cast<const double2 *>(v.z);
+      for (int64_t i = tid; i < npair; i += nth) {
+        const double2 zz = __ldcs(z2 + i), po = p2[i];
+        double2 xx = __ldcs(x2 + i);
+        xx.x = __fma_rn(alpha, po.x, xx.x);
+        xx.y = __fma_rn(alpha, po.y, xx.y);
+        p2[i] = make_double2(__fma_rn(beta, po.x, zz.x), __fma_rn(beta, po.y, zz.y));
+        __stcs(x2 + i, xx);
+      }
+      if ((n & 1) && tid == 0) {
+        const double po = p[n - 1];
+        v.x[n - 1] = __fma_rn(alpha, po, v.x[n - 1]);
+        p[n - 1] = __fma_rn(beta, po, v.z[n - 1]);
+      }
+    }
+    grid_sync(bar);
+    // ---- K1b: q = A p ; sigma = p.q
+    {
+      double acc = 0.0;
+      auto gather = [&](int j) { return __ldg(p + j); };
+      auto epi = [&](int64_t i, double s) {
+        __stcs(q + i, s);
+        acc = __fma_rn(__ldg(p + i), s, acc);
+      };
+      if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
+      else csr_rows<L>(C, gather, epi);
+      double red[1] = {acc};
+      block_sum<1>(red, sm);
+      if (threadIdx.x == 0) part_s[blockIdx.x] = red[0];
+    }
+    grid_sync(bar);
+    {
+      double t[1];
+      all_blocks_sum<1>(part_s, t, sm, s_tot);
+      sigma = t[0];
+    }
+    if (!(sigma > 0.0)) {  // p^T A p <= 0: breakdown (x already holds every applied update)
+      done = DONE_BREAKDOWN;
+      break;
+    }
+    alpha = rho / sigma;
+    k += 1;
+    // ---- K2: r -= alpha q ; z = dinv r ; rho' = r.z ; gamma = r.r
+    {
+      double a0 = 0.0, a1 = 0.0;
+      const double2 *__restrict__ q2 = reinterpret_cast<const double2 *>(q);
+      const double2 *__restrict__ d2 = reinterpret_cast<const double2 *>(v.dinv);
+      double2 *__restrict__ r2 = reinterpret_cast<double2 *>(v.r);
+      double2 *__restrict__ z2 = reinterpret_cast<double2 *>(v.z);
+      for (int64_t i = tid; i < npair; i += nth) {
+        const double2 qq = __ldcs(q2 + i), dd = __ldg(d2 + i);
+        double2 rr = r2[i];
+        rr.x = __fma_rn(-alpha, qq.x, rr.x);
+        rr.y = __fma_rn(-alpha, qq.y, rr.y);
+        const double2 zz = make_double2(dd.x * rr.x, dd.y * rr.y);
+        r2[i] = rr;
+        z2[i] = zz;
+        a0 = __fma_rn(rr.x, zz.x, a0);
+        a0 = __fma_rn(rr.y, zz.y, a0);
+        a1 = __fma_rn(rr.x, rr.x, a1);
+        a1 = __fma_rn(rr.y, rr.y, a1);
+      }
+      if ((n & 1) && tid == 0) {
+        const int64_t i = n - 1;
+        const double ri = __fma_rn(-alpha, q[i], v.r[i]);
+        const double zi = v.dinv[i] * ri;
+        v.r[i] = ri;
+        v.z[i] = zi;
+        a0 = __fma_rn(ri, zi, a0);
+        a1 = __fma_rn(ri, ri, a1);
+      }
+      double red[2] = {a0, a1};
+      block_sum<2>(red, sm);
+      if (threadIdx.x == 0) {
+        part_rz[blockIdx.x] = red[0];
+        part_rz[gridDim.x + blockIdx.x] = red[1];
+      }
+    }
+    grid_sync(bar);
+    double t[2];
+    all_blocks_sum<2>(part_rz, t, sm, s_tot);
+    gamma = t[1];
+    const double rr = sqrt(gamma);
+    relres_rec = rr / nb;
+    if (rr <= tol * nb) {
+      done = DONE_CONVERGED;  // alpha_k still owed to x (tail_kernel)
+    } else if (!(gamma == gamma)) {
+      done = DONE_NONFINITE;
+    } else if (k >= max_iter) {
+      done = DONE_MAXIT;
+    } else {
+      beta = t[0] / rho;
+      rho = t[0];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->rho = rho;
+    sc->beta = beta;
+    sc->alpha = alpha;
+    sc->sigma = sigma;
+    sc->gamma = gamma;
+    sc->relres_rec = relres_rec;
+    sc->k = k;
+    sc->done = done;
+    sc->parity = 0;
+    sc->graph_launches += 1;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static void *persist_fn(int fmt, int lanes) {
+  if (fmt == PCG_FORMAT_SELL) return (void *)pcg_persist_kernel<PCG_FORMAT_SELL, 1>;
+  switch (lanes) {
+    case 1: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 1>;
+    case 2: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 2>;
+    case 4: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 4>;
+    case 8: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 8>;
+    case 16: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 16>;
+    default: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 32>;
+  }
+}
+
+// Whether the handle solves with the persistent kernel: one GPU, SELL or CSR, and a
+// system small enough that kernel boundaries matter (PCG_PERSIST=0/1 forces it).
+bool persist_wanted(const pcg_matrix *A) {
+  if (A->comm || (A->format != PCG_FORMAT_SELL && A->format != PCG_FORMAT_CSR)) return false;
+  const char *e = getenv("PCG_PERSIST");
+  if (e) return atoi(e) != 0;
+  return A->n <= (int64_t(32) << 20);
+}
+
+pcg_status persist_launch(pcg_matrix *A, Vecs v, cudaStream_t st) {
+  SolveWork &w = A->work;
+  void *fn = persist_fn(A->format, A->csr_lanes);
+  if (!w.pbar) {
+    PCG_CUDA(cudaMalloc(&w.pbar, sizeof(GridBar)));
+    PCG_CUDA(cudaMemset(w.pbar, 0, sizeof(GridBar)));
+    int b = 0;
+    PCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, BLOCK, 0));
+    const int64_t need = A->format == PCG_FORMAT_SELL ? (A->n_slices + WARPS - 1) / WARPS
+                                                     : (A->n * A->csr_lanes + BLOCK - 1) / BLOCK;
+    w.pgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(A->device) * std::min(b, 8),
+                                                        std::max<int64_t>(need, 1)));
+  }
+  SellView S = A->sell();
+  CsrView C = A->csr();
+  Scalars *sc = w.sc;
+  double *part = w.partials;  // 3 x grid (<= 8 x SMs; partials hold 6 x 32 x SMs)
+  GridBar *bar = (GridBar *)w.pbar;
+  void *args[] = {&S, &C, &v, &sc, &part, &bar};
+  PCG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(w.pgrid), dim3(BLOCK), args, 0, st));
+  count_launch();
+  return PCG_OK;
+}
+
+}  // namespace pcgb

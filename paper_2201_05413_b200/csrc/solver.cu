@@ -33,10 +33,6 @@ namespace pcgb {
 
 enum { MODE_INIT = 0, MODE_EXIT = 1 };
 
-struct Vecs {
-  double *r, *z, *q, *p0, *p1, *x;
-  const double *dinv;
-};
 
 __device__ __forceinline__ void stop_loop(int use_cond, cudaGraphConditionalHandle h) {
   if (use_cond) cudaGraphSetConditional(h, 0);
@@ -695,7 +691,8 @@ bool is_device_ptr(const void *p) {
 static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double tol, int64_t max_iter,
                              cudaStream_t st, pcg_info *info) {
   PCG_TRY(ensure_work(A));
-  PCG_TRY(build_loop_graph(A));
+  const bool persist = persist_wanted(A);
+  if (!persist) PCG_TRY(build_loop_graph(A));
   SolveWork &w = A->work;
   const int64_t n = A->n;
   const bool b_dev = is_device_ptr(b), x_dev = is_device_ptr(x);
@@ -733,7 +730,9 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
   PCG_CUDA(cudaEventRecord(e0, st));
   PCG_TRY(launch_resid(A, db, MODE_INIT, st));
   for (int round = 0;; round++) {
-    if (w.graph_kind == 1) {
+    if (persist) {
+      PCG_TRY(persist_launch(A, vecs_of(A), st));
+    } else if (w.graph_kind == 1) {
       PCG_CUDA(cudaGraphLaunch(w.loop_exec, st));
     } else {
       for (;;) {  // unrolled chunks, host-polled
