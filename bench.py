@@ -173,10 +173,12 @@ def workload_config(name, c, n, nnz, gpus):
             "C2": f"C2: 2D jittered P1 {c}^2 cells, harmonic x^2-y^2 boundary data",
             "C1": f"C1: 2D P1 {c}^2 cells, sin RHS"}[name]
     return {"workload": desc, "config": name, "n": n, "nnz": nnz, "global_batch": 1, "tol": 1e-10,
-            "parallelism": f"row-partition over {gpus} GPU(s): NCCL halo of z + 2 scalar allreduces per iteration"
+            "parallelism": f"row-partition over {gpus} GPU(s): halo of z + 2 scalar allreduces per iteration"
             if gpus > 1 else "1 GPU",
-            "l2": "no flush needed: every iteration streams > 23 GB, >> 126 MB L2" if name == "C5" else
-            "working set may be L2-resident"}
+            "l2": (f"no flush needed: every iteration streams {iter_bytes(n, nnz) / 1e9:.1f} GB per solve step "
+                   f"(>> 126 MB L2)") if iter_bytes(n, nnz) / gpus > 1e9 else
+            f"no flush: an iteration moves {iter_bytes(n, nnz) / gpus / 1e6:.0f} MB per GPU, partly L2-resident "
+            f"(126 MB L2); timed as the solve runs"}
 
 
 # ------------------------------------------------------------------------------ GPU arm
@@ -191,7 +193,10 @@ def main():
     ap.add_argument("--sample-c", type=int, default=96, help="oracle sample size for the CPU legs")
     ap.add_argument("--ref-iters", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--fmt", default="auto", choices=["auto", "csr", "sell"])
+    ap.add_argument("--fmt", default="auto", choices=["auto", "csr", "sell", "sigma"])
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "callbacks"],
+                    help="callbacks: exchange steps through host callbacks over gloo (validation of the N>1 "
+                         "path when ranks share a GPU; not a performance number)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -205,9 +210,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    cb = args.comm == "callbacks"
+    if cb:  # ranks may share a GPU
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if cb:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = configs()[args.config]
     c = args.c or cfg["c"]
     spec = fem_spec(args.config, c=c)
@@ -227,10 +238,12 @@ def main():
         del rp_full
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
         P = fem_build(spec, r0, r1)
-        comm = pcg.Comm.from_process_group()
+        comm = pcg.Comm.host_callbacks() if cb else pcg.Comm.from_process_group()
         A = pcg.Matrix.from_csr_dist(comm, n, r0, r1, P["row_ptr"], P["col"], P["val"], fmt=args.fmt)
     kcols = P["B"].shape[1]
     multi = kcols > 1
+    if multi and world > 1:
+        raise SystemExit("bench.py: multi-RHS configs run on one GPU (pcg_solve_multi takes single-GPU handles)")
     b = P["B"][:, 0].contiguous() if not multi else None
     Bm = P["B"].t().contiguous().t() if multi else None  # (n, k) view of a column-major block
     del P
@@ -247,7 +260,7 @@ def main():
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if cb else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -376,9 +389,10 @@ def main():
         spmv_gbs = (12.0 * nnz + 4.0 * (n + 1) + 16.0 * n) / (spmv_us * 1e-6) / 1e9
     else:
         per_iter_us = ms * 1e3 / max(iters, 1)
-        achieved = (12.0 * nnz + 4.0 * (n + 1) + 88.0 * n) / world / (per_iter_us * 1e-6) / 1e9
-        roof = {"bound": "hbm", "kernel": "whole iteration (per GPU)", "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_kind, "traffic": None}
+        achieved = (12.0 * nnz + 4.0 * (n + 1) + 96.0 * n) / world / (per_iter_us * 1e-6) / 1e9
+        roof = {"bound": "hbm", "kernel": "whole iteration incl. halo + allreduces (per GPU, 96n schedule)",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_kind,
+                "traffic": None, "comm": args.comm}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None

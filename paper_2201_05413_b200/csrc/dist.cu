@@ -79,7 +79,9 @@ bool comm_uses_graphs(const pcg_comm *c) { return c && !c->use_ops; }
   } while (0)
 
 static pcg_status comm_allreduce_f64(pcg_comm *C, double *dbuf, int count, cudaStream_t st) {
-  if (C->size == 1 || count == 0) return PCG_OK;
+  // a 1-rank NCCL communicator still issues the (trivial) collective: it keeps the
+  // captured-graph + NCCL path testable on one GPU
+  if (count == 0 || (C->use_ops && C->size == 1)) return PCG_OK;
   if (!C->use_ops) {
     PCG_NCCL(ncclAllReduce(dbuf, dbuf, (size_t)count, ncclDouble, ncclSum, C->nccl, st));
     return PCG_OK;
@@ -188,7 +190,7 @@ pcg_status halo_exchange(pcg_matrix *A, double *vec, int width, cudaStream_t st)
 }
 
 pcg_status allreduce_sum(pcg_matrix *A, double *buf, int count, cudaStream_t st) {
-  if (!A->comm || A->comm->size == 1) return PCG_OK;
+  if (!A->comm) return PCG_OK;
   return comm_allreduce_f64(A->comm, buf, count, st);
 }
 

@@ -118,3 +118,56 @@ def test_distributed_path_on_one_gpu(world, name, c, gen):
     assert all(d["info"]["status"] == 0 and d["info"]["relres_true"] <= tol for d in parts)
     assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) <= 1e-9
     assert abs(it - r.iterations) <= max(1, 0.02 * r.iterations), (it, r.iterations)
+
+
+def test_bench_multi_rank_flow_on_one_gpu():
+    """bench.py's N>1 path (torchrun, row partition by the device generator, barriers, max
+    over ranks, one JSON line from rank 0) with 2 ranks sharing cuda:0 (host-callback
+    communicator).  The iteration count must match the oracle's C5 ladder at c = 64."""
+    import json
+    import subprocess
+    import sys
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"), "--gpus", "2", "--comm",
+           "callbacks", "--config", "C5", "--c", "64", "--steps", "2", "--warmup", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["steps"] == 2 and line["unit"] == "s" and line["value"] > 0
+    r = O.pcg(*(lambda P: (P["A"], P["B"][:, 0]))(O.build_problem("C5", c=64)), tol=1e-10)
+    it = line["config"]["iterations"]
+    assert abs(it - r.iterations) <= max(1, 0.02 * r.iterations), (it, r.iterations)
+    assert line["config"]["relres_true"] <= 1e-10
+
+
+def test_nccl_single_rank_distributed_handle():
+    """The NCCL backend end to end on one GPU: unique id broadcast through a
+    torch.distributed group, ncclCommInitRank, csr_create_dist, and the distributed
+    solve loop whose graph captures ncclAllReduce (a 1-rank communicator still issues
+    every collective).  Against the oracle."""
+    import torch
+    import torch.distributed as dist
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_05413_b200 as pcg
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        P = O.build_problem("C2", c=48, k=1)
+        A, b = P["A"], P["B"][:, 0]
+        comm = pcg.Comm.from_process_group()
+        M = pcg.Matrix.from_csr_dist(comm, A.n, 0, A.n, torch.as_tensor(A.row_ptr).cuda(),
+                                     torch.as_tensor(A.col).cuda(), torch.as_tensor(A.val).cuda())
+        x, info = M.solve(torch.as_tensor(b).cuda(), tol=1e-10)
+        r = O.pcg(A, b, tol=1e-10)
+        assert info["status"] == 0 and info["relres_true"] <= 1e-10
+        assert np.linalg.norm(x.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-9
+        assert abs(info["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
+        M.close()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
