@@ -295,7 +295,7 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
   A->csr_lanes = L;
   // ---- TMA-staged SELL: largest tile (WARPS slices) sets the shared-memory stage size
   A->stage_entries = 0;
-  if (want_sell && A->n_slices > 0) {
+  if (fmt_req == PCG_FMT_SELL_TMA && want_sell && A->n_slices > 0) {
     std::vector<int64_t> sp(A->n_slices + 1);
     PCG_CUDA(cudaMemcpy(sp.data(), A->d_slice_ptr, sizeof(int64_t) * sp.size(), cudaMemcpyDeviceToHost));
     int64_t mx = 0;
@@ -347,9 +347,15 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
   else if (fmt_req == PCG_FMT_SELL_TMA) {
     if (!A->stage_entries) return fail(PCG_ERR_INVALID_ARG, "csr_create: TMA-staged SELL unavailable for this matrix");
     cands = {FMT_SELL_TMA};
+  } else if (pad_nat <= 1.02) {
+    // near-uniform slices: natural SELL-32 moves the fewest bytes and was the fastest
+    // format on every such matrix measured (C1, C4, C5); no timing (it is also what a
+    // profiler's serialised replays would corrupt)
+    cands = {PCG_FORMAT_SELL};
   } else {
+    // the TMA-staged SELL (PCG_FMT_SELL_TMA) never won a measurement and is only
+    // built/used on request
     cands = {PCG_FORMAT_CSR, PCG_FORMAT_SELL};
-    if (A->stage_entries) cands.push_back(FMT_SELL_TMA);
   }
   // ---- measured format choice (time 5 SpMVs of each candidate)
   const bool timed = n > 0 && (cands.size() > 1 || (try_sigma && fmt_req == PCG_FMT_AUTO));

@@ -215,6 +215,7 @@ static void *persist_fn(int fmt, int lanes) {
 // system small enough that kernel boundaries matter (PCG_PERSIST=0/1 forces it).
 bool persist_wanted(const pcg_matrix *A) {
   if (A->comm || (A->format != PCG_FORMAT_SELL && A->format != PCG_FORMAT_CSR)) return false;
+  if (getenv("PCG_NO_GRAPH")) return false;  // profiling: one launch per pass
   const char *e = getenv("PCG_PERSIST");
   if (e) return atoi(e) != 0;
   return A->n <= (int64_t(32) << 20);

@@ -611,7 +611,9 @@ static pcg_status launch_resid(pcg_matrix *A, const double *b, int mode, cudaStr
 static pcg_status build_loop_graph(pcg_matrix *A) {
   SolveWork &w = A->work;
   if (w.graph_ready) return PCG_OK;
-  if (A->comm && !comm_uses_graphs(A->comm)) {  // host-callback communicator: direct launches
+  // host-callback communicator, or PCG_NO_GRAPH=1 (profilers that do not descend into
+  // conditional graph bodies): the same iterations as direct launches, host-polled
+  if ((A->comm && !comm_uses_graphs(A->comm)) || getenv("PCG_NO_GRAPH")) {
     w.graph_kind = 3;
     w.unroll = 8;
     w.graph_ready = true;

@@ -1,0 +1,94 @@
+"""Summarise ncu reports for profiles/ (development tool; reads .ncu-rep, no GPU).
+
+  python scripts/ncu_summary.py REPORT.ncu-rep [--traffic OUT.json --workload TEXT]
+  python scripts/ncu_summary.py --launches LAUNCHES.csv
+
+For a --set full report: one CSV row per profiled launch with duration, DRAM bytes,
+occupancy, cache hit rates and the dominant stall, printed to stdout; --traffic
+also writes {kernel: dram read+write bytes per launch} (the `traffic` field of the
+bench roofline).  For a launch list (--metrics gpu__time_duration.sum): each
+kernel's share of the total device time.
+"""
+import argparse
+import collections
+import csv
+import io
+import json
+import subprocess
+import sys
+
+NCU = "/usr/local/cuda/bin/ncu"
+COLS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
+        "launch__grid_size", "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+        "l1tex__t_sector_hit_rate.pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"]
+
+
+def raw_rows(rep):
+    out = subprocess.run([NCU, "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    head, units = rows[0], rows[1]
+    return [dict(zip(head, r)) for r in rows[2:]], dict(zip(head, units))
+
+
+def to_bytes(v, unit):
+    f = float(v)
+    return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "B": 1, "KB": 1e3, "MB": 1e6,
+                "GB": 1e9, "TB": 1e12}.get(unit, 1)
+
+
+def to_ms(v, unit):
+    f = float(v)
+    return f * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1, "ms": 1, "second": 1e3,
+                "s": 1e3}.get(unit, 1)
+
+
+def full(rep, traffic, workload):
+    rows, units = raw_rows(rep)
+    w = csv.writer(sys.stdout)
+    w.writerow(["kernel", "ms", "dram_read_GB", "dram_write_GB"] + COLS[3:])
+    per = {}
+    for d in rows:
+        name = d["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").strip()
+        ms = to_ms(d["gpu__time_duration.sum"], units["gpu__time_duration.sum"])
+        rd = to_bytes(d["dram__bytes_read.sum"], units["dram__bytes_read.sum"])
+        wr = to_bytes(d["dram__bytes_write.sum"], units["dram__bytes_write.sum"])
+        w.writerow([d["Kernel Name"][:90], f"{ms:.4f}", f"{rd / 1e9:.4f}", f"{wr / 1e9:.4f}"] + [d.get(c, "") for c in COLS[3:]])
+        per.setdefault(name, {"dram_read_GB": rd / 1e9, "dram_write_GB": wr / 1e9, "traffic_bytes": rd + wr,
+                              "ncu_duration_ms": ms})
+    if traffic:
+        with open(traffic, "w") as fh:
+            json.dump({"workload": workload, "source": f"{rep} (ncu --set full --clock-control none)",
+                       "kernels": per}, fh, indent=1)
+
+
+def launches(path):
+    lines = open(path).read().splitlines()
+    start = next(i for i, ln in enumerate(lines) if ln.startswith('"ID"'))
+    rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+    tot = collections.Counter()
+    cnt = collections.Counter()
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = r["Kernel Name"].split("(")[0].replace("void ", "")
+        v = float(r["Metric Value"].replace(",", ""))
+        tot[name] += v
+        cnt[name] += 1
+    s = sum(tot.values())
+    print(f"{'kernel':60s} {'launches':>8s} {'share':>7s} {'mean_us':>9s}")
+    for name, v in tot.most_common():
+        print(f"{name[:60]:60s} {cnt[name]:8d} {v / s:7.3f} {v / cnt[name] / 1e3:9.1f}")
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("report", nargs="?")
+    ap.add_argument("--traffic")
+    ap.add_argument("--workload", default="")
+    ap.add_argument("--launches")
+    a = ap.parse_args()
+    if a.launches:
+        launches(a.launches)
+    else:
+        full(a.report, a.traffic, a.workload)
