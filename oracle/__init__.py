@@ -77,6 +77,9 @@ def lib():
                               P(C.c_int64), P(C.c_double), P(C.c_double),
                               C.c_void_p, C.c_void_p, C.c_int64]
         L.orc_partition.argtypes = [C.c_int64, C.c_void_p, C.c_int, C.c_void_p]
+        L.orc_fd_cube.argtypes = [C.c_int64, C.c_int, P(_Csr), C.c_void_p]
+        L.orc_bicgstab.argtypes = [P(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_int64,
+                                   P(C.c_int64), P(C.c_double), P(C.c_double)]
         L.orc_halo.restype = C.c_int64
         L.orc_halo.argtypes = [P(_Csr), C.c_int64, C.c_int64, C.c_void_p, C.c_int64]
         L.orc_fd_identity_rows_nnz.restype = C.c_int64
@@ -237,6 +240,31 @@ def pcg(A: Csr, b, x0=None, tol=1e-10, max_iter=50000, hist: int = 0) -> PcgResu
                        C.byref(rt), _ptr(ah), _ptr(bh), hist)
     return PcgResult(x=x, iterations=it.value, relres_rec=rr.value, relres_true=rt.value,
                      status=st, alpha=ah, beta=bh)
+
+
+FD_X2MY2, FD_EXPSIN = 1, 2
+
+
+def fd_cube(N: int, fkind: int = FD_X2MY2):
+    """Table 1 system: FD Laplace on N^3 nodes, identity boundary rows
+    with b = f (Dirichlet), b = 0 inside.  Returns (Csr, b)."""
+    b = np.zeros(N ** 3)
+    s = _Csr()
+    st = lib().orc_fd_cube(N, fkind, C.byref(s), _ptr(b))
+    if st != OK:
+        raise RuntimeError(f"orc_fd_cube: {st}")
+    return Csr._from_c(s), b
+
+
+def bicgstab(A: Csr, b, x0=None, tol=1e-10, max_iter=50000, block=1) -> PcgResult:
+    """Right-preconditioned BiCGSTAB with (block-)Jacobi (R2)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(A.n) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+    it, rr, rt = C.c_int64(0), C.c_double(0), C.c_double(0)
+    Ac = A._c()
+    st = lib().orc_bicgstab(C.byref(Ac), _ptr(b), _ptr(x), tol, max_iter, block, C.byref(it), C.byref(rr),
+                            C.byref(rt))
+    return PcgResult(x=x, iterations=it.value, relres_rec=rr.value, relres_true=rt.value, status=st)
 
 
 def pcg_multi(A: Csr, B, X0=None, tol=1e-10, max_iter=50000):

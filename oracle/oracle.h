@@ -101,4 +101,14 @@ int64_t orc_halo(const orc_csr *A, int64_t r0, int64_t r1, int64_t *out, int64_t
 /* Table 1 FD identity-boundary-row convention: nnz for N^3 nodes */
 int64_t orc_fd_identity_rows_nnz(int64_t N);
 
+/* the Table 1 system as a problem (Laplace, Dirichlet u = f on the
+ * boundary, identity boundary rows; nonsymmetric) and preconditioned BiCGSTAB */
+#define ORC_FD_X2MY2 1  /* f = x^2 - y^2 (discrete solution == f exactly) */
+#define ORC_FD_EXPSIN 2 /* f = exp(pi x) sin(pi y)                        */
+/* BiCGSTAB shadow residual r^_i = 2 u(seed, i) - 1, u = orc_uniform (reading R2) */
+#define ORC_BICG_SEED 5413ULL
+int orc_fd_cube(int64_t N, int fkind, orc_csr *A, double *b /* N^3 */);
+int orc_bicgstab(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter, int64_t bs,
+                 int64_t *iters, double *relres_rec, double *relres_true);
+
 #endif

@@ -506,3 +506,87 @@ def test_dot_survives_cancellation_that_breaks_a_plain_sum():
     a = np.concatenate([x[:25], x[:25], [3.0]])
     b = np.concatenate([np.ones(25), -np.ones(25), [0.5]])
     assert O.dot(a, b) == _exact_dot(a, b) == 1.5
+
+
+# ---------------------------------------------------------------- N2: Table 1 systems + BiCGSTAB (reading R2)
+@pytest.mark.parametrize("N,want", [(16, 20560), (128, 14099408)])
+def test_fd_cube_is_table1(N, want):
+    """The identity-boundary-row FD system has exactly the non-zero count the paper
+    prints for Cube 1 (128^3 nodes: 14,099,408) and SPEC's 16^3 = 20,560."""
+    A, b = O.fd_cube(N)
+    assert A.n == N ** 3 and A.nnz == want
+    rl = np.diff(A.row_ptr)
+    assert set(np.unique(rl)) == {1, 7}
+    assert np.all(np.diff(A.col[A.row_ptr[N * N + N + 1]:A.row_ptr[N * N + N + 2]]) > 0)
+
+
+def _grid(N):
+    h = 1.0 / (N - 1)
+    i = np.arange(N)
+    return np.tile(i, N * N) * h, np.tile(np.repeat(i, N), N) * h
+
+
+@pytest.mark.parametrize("bs", [1, 2, 5])
+def test_bicgstab_reproduces_the_harmonic_quadratic(bs):
+    """Second differences are exact for quadratics: the discrete solution of the
+    Table 1 system with boundary data x^2 - y^2 is x^2 - y^2 at every node."""
+    N = 14
+    A, b = O.fd_cube(N)
+    X, Y = _grid(N)
+    r = O.bicgstab(A, b, tol=1e-13, block=bs)
+    assert r.status == O.OK and r.relres_true <= 1e-13
+    assert np.max(np.abs(r.x - (X * X - Y * Y))) <= 1e-11
+
+
+def test_bicgstab_block_equal_to_matrix_is_one_step():
+    """M = A (one Block-Jacobi block covering the matrix): the first step is exact."""
+    A, b = O.fd_cube(6, O.FD_EXPSIN)
+    r = O.bicgstab(A, b, tol=1e-12, block=A.n)
+    assert r.status == O.OK and r.iterations == 1
+    assert np.allclose(r.x, np.linalg.solve(A.to_dense(), b), rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("bs", [1, 3, 7])
+def test_bicgstab_matches_dense_solve_on_nonsymmetric(bs):
+    rng = np.random.default_rng(21)
+    n = 60
+    D = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.15)
+    D += np.diag(np.abs(D).sum(1) + 1.0)  # strictly diagonally dominant, nonsymmetric
+    rp, cols, vals = [0], [], []
+    for i in range(n):
+        nz = np.nonzero(D[i])[0]
+        cols += list(nz)
+        vals += list(D[i, nz])
+        rp.append(len(cols))
+    A = O.Csr(n, rp, cols, vals)
+    bb = rng.standard_normal(n)
+    r = O.bicgstab(A, bb, tol=1e-13, block=bs)
+    assert r.status == O.OK
+    xe = np.linalg.solve(D, bb)
+    assert np.linalg.norm(r.x - xe) / np.linalg.norm(xe) <= 1e-11
+
+
+def test_bicgstab_on_spd_lattice_matches_dst():
+    """On the SPD C1 lattice system BiCGSTAB reaches the DST-I exact solution too."""
+    from scipy.fft import dstn, idstn
+    c = 32
+    P = O.build_problem("C1", c=c)
+    A, b = P["A"], P["B"][:, 0]
+    m = c - 1
+    jj = np.arange(1, m + 1)
+    l1 = 2 - 2 * np.cos(jj * np.pi / c)
+    xe = idstn(dstn(b.reshape(m, m), type=1) / (l1[None, :] + l1[:, None]), type=1).ravel()
+    r = O.bicgstab(A, b, tol=1e-13)
+    assert r.status == O.OK
+    assert np.linalg.norm(r.x - xe) / np.linalg.norm(xe) <= 1e-11
+
+
+def test_bicgstab_status_codes():
+    A, b = O.fd_cube(10, O.FD_EXPSIN)
+    r = O.bicgstab(A, b, tol=1e-12, max_iter=3)
+    assert r.status == O.NOT_CONVERGED and r.iterations == 3
+    r = O.bicgstab(A, np.zeros(A.n))
+    assert r.status == O.OK and r.iterations == 0 and np.all(r.x == 0)
+    I = O.Csr(5, list(range(6)), list(range(5)), [2.0] * 5)
+    r = O.bicgstab(I, np.arange(1.0, 6.0), tol=1e-14)
+    assert r.status == O.OK and r.iterations == 1 and np.allclose(r.x, np.arange(1.0, 6.0) / 2)
