@@ -74,6 +74,19 @@ pcg_status fem_assemble(const fem_spec *spec, int64_t row_begin, int64_t row_end
 pcg_status fem_count(const fem_spec *spec, int64_t row_begin, int64_t row_end, int64_t *d_row_ptr,
                      int64_t *nnz_out, void *stream);
 
+/* ---------------------------------------------------------------- the paper's Table 1 systems
+ * (reading R2): FD Laplace on N^3 nodes of
+ * the unit cube (h = 1/(N-1)), node id i + N(j + N l); interior rows 6 / -1 x 6 (columns
+ * ascending), b = 0; boundary rows identity, b = f(node).  Nonsymmetric.  nnz(N^3) =
+ * 7(N-2)^3 + N^3 - (N-2)^3 (Cube 1, N = 128: 14,099,408).  Two phases over rows
+ * [row_begin, row_end) like fem_count / fem_assemble; d_b (rows entries) may be NULL. */
+#define FD_F_X2MY2 1  /* f = x^2 - y^2 (the discrete solution equals f) */
+#define FD_F_EXPSIN 2 /* f = exp(pi x) sin(pi y)                        */
+pcg_status fd_cube_count(int64_t N, int64_t row_begin, int64_t row_end, int64_t *d_row_ptr, int64_t *nnz_out,
+                         void *stream);
+pcg_status fd_cube_assemble(int64_t N, int32_t fkind, int64_t row_begin, int64_t row_end, const int64_t *d_row_ptr,
+                            int64_t *d_col, double *d_val, double *d_b, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

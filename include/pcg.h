@@ -46,7 +46,8 @@ typedef enum {
   PCG_ERR_NONFINITE = 8,           /* NaN/Inf in values or right-hand side         */
   PCG_ERR_OOM = 9,
   PCG_ERR_CUDA = 10,
-  PCG_ERR_NCCL = 11
+  PCG_ERR_NCCL = 11,
+  PCG_ERR_BREAKDOWN = 12           /* BiCGSTAB: rho = r^.r, r^.v or omega became 0            */
 } pcg_status;
 
 /* csr_create flags */
@@ -131,6 +132,22 @@ pcg_status pcg_solve(pcg_matrix_t A, const double *b, double *x, double tol, int
 pcg_status pcg_solve_multi(pcg_matrix_t A, int32_t k, const double *B, int64_t ldb, double *X,
                            int64_t ldx, double tol, int64_t max_iter, void *stream,
                            pcg_info *infos);
+
+/* ---------------------------------------------------------------- BiCGSTAB (§8(f) N2) */
+/* Right-preconditioned BiCGSTAB (van der Vorst 1992) — the Krylov solver the paper
+ * selects — with Block-Jacobi M: block_size = 1 is point
+ * Jacobi; 2, 4, 8 use the exact inverses of the diagonal blocks of block_size
+ * consecutive rows (reading R2).  For nonsymmetric A (the paper's
+ * identity-row grids, Table 1) as well as SPD.  Stops when the
+ * recurrence residual (or the half-step residual) satisfies ||.|| <= tol ||b||;
+ * the true residual (Eq. relativeError) then decides, restarting from
+ * x if needed.  The shadow residual is the fixed vector 2u(5413, i) - 1 (SplitMix64
+ * u; i = original row).  b, x: n doubles, host or device; x in/out.  Returns OK,
+ * NOT_CONVERGED, BREAKDOWN, NONFINITE, ZERO_DIAGONAL (singular block) or an error.
+ * Single-GPU handles.  Blocks are consecutive rows of the caller's numbering on every
+ * device format (SELL-C-sigma handles map them through their permutation). */
+pcg_status pcg_bicgstab(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
+                        int32_t block_size, void *stream, pcg_info *info);
 
 /* ---------------------------------------------------------------- multi-GPU (§8(a) a8, §8(e)) */
 /* Row partition rule: bounds[0] = 0, bounds[G] = n,

@@ -140,6 +140,30 @@ class Matrix:
         d["status_name"] = _lib.STATUS[st]
         return x, d
 
+    def bicgstab(self, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, block: int = 1, stream=None,
+                 raise_on=("error",), out=None):
+        """Right-preconditioned BiCGSTAB with (Block-)Jacobi (pcg_bicgstab).
+        Same conventions as solve(); block = 1 (point Jacobi), 2, 4 or 8."""
+        torch = _torch()
+        b = _as_tensor(b, torch.float64)
+        if out is not None:
+            x = out
+        else:
+            x = torch.zeros_like(b) if x0 is None else _as_tensor(x0, torch.float64).clone()
+        if b.device.type == "cpu":
+            if not b.is_pinned():
+                b = b.pin_memory()
+            if not x.is_pinned():
+                x = x.pin_memory()
+        info = _lib.PcgInfo()
+        st = lib().pcg_bicgstab(self._h, _ptr(b), _ptr(x), float(tol), int(max_iter), int(block), _stream_ptr(stream),
+                                C.byref(info))
+        if st not in (PCG_OK, PCG_NOT_CONVERGED) or ("not_converged" in raise_on and st == PCG_NOT_CONVERGED):
+            raise PcgError(st, "pcg_bicgstab")
+        d = info.as_dict()
+        d["status_name"] = _lib.STATUS[st]
+        return x, d
+
     def solve_multi(self, B, X0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None, out=None):
         """k right-hand sides, B an (n, k) tensor (column-major storage is used at the ABI:
         pass B as B.T.contiguous().T or let this wrapper arrange it).  With `out` (an (n, k)

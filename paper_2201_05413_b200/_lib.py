@@ -13,13 +13,13 @@ LIB_PATH = os.path.join(HERE, "libpcg_b200.so")
 
 STATUS = ["PCG_OK", "PCG_NOT_CONVERGED", "PCG_ERR_INVALID_ARG", "PCG_ERR_INDEX_OUT_OF_RANGE",
           "PCG_ERR_UNSORTED_OR_DUPLICATE", "PCG_ERR_DIMENSION_MISMATCH", "PCG_ERR_ZERO_DIAGONAL",
-          "PCG_ERR_NOT_SPD", "PCG_ERR_NONFINITE", "PCG_ERR_OOM", "PCG_ERR_CUDA", "PCG_ERR_NCCL"]
+          "PCG_ERR_NOT_SPD", "PCG_ERR_NONFINITE", "PCG_ERR_OOM", "PCG_ERR_CUDA", "PCG_ERR_NCCL", "PCG_ERR_BREAKDOWN"]
 (PCG_OK, PCG_NOT_CONVERGED, PCG_ERR_INVALID_ARG, PCG_ERR_INDEX_OUT_OF_RANGE,
  PCG_ERR_UNSORTED_OR_DUPLICATE, PCG_ERR_DIMENSION_MISMATCH, PCG_ERR_ZERO_DIAGONAL, PCG_ERR_NOT_SPD,
- PCG_ERR_NONFINITE, PCG_ERR_OOM, PCG_ERR_CUDA, PCG_ERR_NCCL) = range(12)
+ PCG_ERR_NONFINITE, PCG_ERR_OOM, PCG_ERR_CUDA, PCG_ERR_NCCL, PCG_ERR_BREAKDOWN) = range(13)
 PCG_PTR_HOST, PCG_PTR_DEVICE = 0x0, 0x1
 PCG_FMT_AUTO, PCG_FMT_CSR, PCG_FMT_SELL, PCG_FMT_SELL_TMA, PCG_FMT_SELL_SIGMA = 0x00, 0x10, 0x20, 0x30, 0x40
-PCG_FORMAT_CSR, PCG_FORMAT_SELL, PCG_FORMAT_SELL_TMA = 1, 2, 3
+PCG_FORMAT_CSR, PCG_FORMAT_SELL, PCG_FORMAT_SELL_TMA, PCG_FORMAT_SELL_SIGMA = 1, 2, 3, 4
 
 
 class PcgInfo(C.Structure):
@@ -94,6 +94,9 @@ def lib():
         "csr_create_dist": [vp, i64, i64, i64, i64, vp, vp, vp, C.c_int, vp, P(vp)],
         "pcg_profile_kernels": [vp, vp, i32, vp, vp, P(i32)],
         "pcg_profile_multi": [vp, i32, vp, i64, i32, vp, vp, P(i32)],
+        "pcg_bicgstab": [vp, vp, vp, C.c_double, i64, i32, vp, P(PcgInfo)],
+        "fd_cube_count": [i64, i64, i64, vp, P(i64), vp],
+        "fd_cube_assemble": [i64, i32, i64, i64, vp, vp, vp, vp, vp],
         "fem_problem_size": [P(FemSpec), P(i64), P(i64), P(i64)],
         "fem_count": [P(FemSpec), i64, i64, vp, P(i64), vp],
         "fem_assemble": [P(FemSpec), i64, i64, vp, vp, vp, vp, i64, vp],

@@ -34,6 +34,7 @@ extern "C" const char *pcg_status_string(pcg_status s) {
     case PCG_ERR_OOM: return "PCG_ERR_OOM";
     case PCG_ERR_CUDA: return "PCG_ERR_CUDA";
     case PCG_ERR_NCCL: return "PCG_ERR_NCCL";
+    case PCG_ERR_BREAKDOWN: return "PCG_ERR_BREAKDOWN";
   }
   return "PCG_UNKNOWN";
 }

@@ -1,0 +1,593 @@
+// bicgstab.cu — right-preconditioned BiCGSTAB with (Block-)Jacobi: the Krylov
+// solver the paper selects (Block-Jacobi P:194), for the
+// nonsymmetric systems CG cannot take (the Table 1 identity-row grids).
+// SURVEY §8(f) N2; the algorithm and every reading are DESIGN.md R2, restated:
+//
+//   r = b - A x ; r^ = fixed pseudo-random vector ; rho_old = alpha = omega = 1 ; p = v = 0
+//   loop:  rho = r^.r ;  beta = (rho/rho_old)(alpha/omega)
+//          p = r + beta (p - omega v) ; p^ = M^-1 p ; v = A p^ ; alpha = rho / (r^.v)
+//          s = r - alpha v ;  stop if ||s|| <= tol ||b||  (x += alpha p^)
+//          s^ = M^-1 s ; t = A s^ ; omega = (t.s)/(t.t)
+//          x += alpha p^ + omega s^ ; r = s - omega t ; stop if ||r|| <= tol ||b||
+//   stop -> true residual ||b - A x||/||b|| (Eq. relativeError) decides; else
+//   restart from x (same r^), iterations keep counting.
+//
+// The whole solve (init, iterations, exit check, restarts) is ONE cooperative
+// kernel: the five passes of an iteration are separated by grid barriers, and
+// every block evaluates the scalars (rho, alpha, omega, beta, stop tests)
+// identically from fixed-order block partials (coop.cuh).  Per iteration: two
+// SpMVs (sell_rows / csr_rows of rows.cuh) and three streaming passes;
+// Block-Jacobi applies the LU factors (partial pivoting) of each bs x bs diagonal
+// block, computed at setup, one thread per block — bitwise the oracle's M^-1.
+#include <cstring>
+
+#include "coop.cuh"
+#include "matrix.cuh"
+#include "rows.cuh"
+
+namespace pcgb {
+
+struct BicgVecs {
+  double *x, *r, *rh, *p, *ph, *v, *sh, *t;
+  const double *b;
+  const double *dinv;  // bs = 1
+  const double *lu;    // bs > 1: [block][bs][bs] LU factors of the diagonal blocks (unit L, U)
+  const int *piv;      // bs > 1: [block][bs] row permutation of the partial pivoting
+  const int *iperm;    // SELL-C-sigma handles: device row of original row o (else null)
+};
+
+struct BicgState {
+  double tol, nb, relres_rec, relres_true;
+  long long k, max_iter, restarts;
+  int done, pad;
+};
+
+__device__ __forceinline__ uint64_t bicg_mix(uint64_t seed, uint64_t idx) {
+  uint64_t z = seed + (idx + 1) * 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// r^_i = 2 u(5413, i) - 1 on the ORIGINAL row index (perm maps SELL-C-sigma rows back)
+__global__ void shadow_kernel(int64_t n, const int *__restrict__ perm, double *__restrict__ rh) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = perm ? (uint64_t)perm[i] : (uint64_t)i;
+    const double u = (double)(bicg_mix(5413ULL, g) >> 11) * (1.0 / 9007199254740992.0);
+    rh[i] = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+  }
+}
+
+// LU factors (partial pivoting, Doolittle, in place) of the bs x bs diagonal blocks
+// (rows/cols [blk*bs, +m)), one thread per block.  Written with explicitly rounded
+// operations in the order of the oracle's bj_setup (oracle.c), so the factors —
+// and with bj_apply below every application of M^-1 — are bitwise the oracle's.
+// Output: lu[blk][bs][bs] (unit L below, U on and above the diagonal), piv[blk][bs].
+// On a SELL-C-sigma handle (device system P A P^T) the blocks are still consecutive
+// rows of the CALLER's numbering: original row o lives at device row iperm[o], and a
+// device column c is original column perm[c].
+template <int BS>
+__global__ void bj_lu_kernel(int64_t n, const int *__restrict__ rp, const int *__restrict__ col,
+                             const double *__restrict__ val, const int *__restrict__ perm,
+                             const int *__restrict__ iperm, double *__restrict__ lu, int *__restrict__ piv, int *err) {
+  const int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nblk = (n + BS - 1) / BS;
+  if (blk >= nblk) return;
+  const int64_t r0 = blk * BS;
+  const int m = (int)((r0 + BS <= n) ? BS : n - r0);
+  double *D = lu + blk * BS * BS;
+  int *pv = piv + blk * BS;
+  for (int a = 0; a < BS * BS; a++) D[a] = 0.0;
+  for (int a = 0; a < m; a++) {
+    const int64_t dr = iperm ? iperm[r0 + a] : r0 + a;
+    for (int k = rp[dr]; k < rp[dr + 1]; k++) {
+      const int64_t c = (perm ? perm[col[k]] : col[k]) - r0;
+      if (c >= 0 && c < m) D[a * BS + c] = val[k];
+    }
+  }
+  for (int a = 0; a < BS; a++) pv[a] = a;
+  for (int c = 0; c < m; c++) {
+    int p = c;
+    for (int a = c + 1; a < m; a++)
+      if (fabs(D[a * BS + c]) > fabs(D[p * BS + c])) p = a;
+    if (D[p * BS + c] == 0.0) {
+      atomicExch(err, 1);
+      return;
+    }
+    if (p != c) {
+      for (int q = 0; q < m; q++) {
+        const double t = D[c * BS + q];
+        D[c * BS + q] = D[p * BS + q];
+        D[p * BS + q] = t;
+      }
+      const int t = pv[c];
+      pv[c] = pv[p];
+      pv[p] = t;
+    }
+    for (int a = c + 1; a < m; a++) {
+      const double f = __ddiv_rn(D[a * BS + c], D[c * BS + c]);
+      D[a * BS + c] = f;
+      for (int q = c + 1; q < m; q++) D[a * BS + q] = __dsub_rn(D[a * BS + q], __dmul_rn(f, D[c * BS + q]));
+    }
+  }
+}
+
+enum { BD_RUNNING = 0, BD_CONVERGED = 1, BD_MAXIT = 2, BD_BREAKDOWN = 3, BD_ZERO_RHS = 4, BD_NONFINITE = 5 };
+
+template <int FMT, int L, int BS>
+__global__ void __launch_bounds__(BLOCK, 2) bicg_kernel(SellView S, CsrView C, BicgVecs v, BicgState *st,
+                                                        double *part, GridBar *bar) {
+  __shared__ double sm[2][WARPS];
+  __shared__ double s_tot[2];
+  const int64_t n = FMT == PCG_FORMAT_SELL ? S.n : C.n;
+  const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
+  const int64_t nblk = (n + BS - 1) / BS;
+  const double tol = st->tol;
+  const long long max_iter = st->max_iter;
+  long long k = st->k, restarts = 0;
+  int done = BD_RUNNING;
+  double nb, relres_rec = 0.0, relres_true = 0.0;
+  double rho = 1.0, rho_old = 1.0, alpha = 1.0, omega = 1.0;
+  double *pa = part, *pb = part + 2 * gridDim.x;  // two alternating partial regions
+  // y = M^-1 u on block blk: BS = 1 dinv * u; else P, L, U substitution (oracle bj_apply order)
+  auto bj = [&](int64_t blk, const double (&u)[BS], double (&y)[BS]) {
+    if (BS == 1) {
+      y[0] = __dmul_rn(v.dinv[blk], u[0]);
+    } else {
+      const double *D = v.lu + blk * BS * BS;
+      const int *pv = v.piv + blk * BS;
+      const int m = (int)((blk * BS + BS <= n) ? BS : n - blk * BS);
+#pragma unroll
+      for (int a = 0; a < BS; a++) {  // L z = P u
+        double sacc = 0.0;
+        const int pr = pv[a];
+#pragma unroll
+        for (int q = 0; q < BS; q++)
+          if (q == pr) sacc = u[q];
+#pragma unroll
+        for (int q = 0; q < a; q++) sacc = __dsub_rn(sacc, __dmul_rn(D[a * BS + q], y[q]));
+        y[a] = sacc;
+      }
+#pragma unroll
+      for (int a = BS - 1; a >= 0; a--) {  // U y = z
+        if (a >= m) continue;
+        double sacc = y[a];
+#pragma unroll
+        for (int q = a + 1; q < BS; q++)
+          if (q < m) sacc = __dsub_rn(sacc, __dmul_rn(D[a * BS + q], y[q]));
+        y[a] = __ddiv_rn(sacc, D[a * BS + a]);
+      }
+    }
+  };
+  // ---- ||b||
+  {
+    double a0 = 0.0;
+    for (int64_t i = tid; i < n; i += nth) a0 = __fma_rn(v.b[i], v.b[i], a0);
+    double red[1] = {a0};
+    block_sum<1>(red, sm);
+    if (threadIdx.x == 0) pa[blockIdx.x] = red[0];
+    grid_sync(bar);
+    double t[1];
+    all_blocks_sum<1>(pa, t, sm, s_tot);
+    nb = sqrt(t[0]);
+  }
+  if (nb == 0.0 || !(nb == nb)) {
+    done = nb == 0.0 ? BD_ZERO_RHS : BD_NONFINITE;
+    for (int64_t i = tid; i < n; i += nth) v.x[i] = 0.0;
+  }
+  bool need_resid = true;  // (re)start: r = b - A x, p = v = 0, rho = r^.r
+  while (done == BD_RUNNING) {
+    if (need_resid) {
+      double a0 = 0.0, a1 = 0.0;
+      auto gather = [&](int j) { return __ldg(v.x + j); };
+      auto epi = [&](int64_t i, double s) {
+        const double w = v.b[i] - s;
+        v.r[i] = w;
+        v.p[i] = 0.0;
+        v.v[i] = 0.0;
+        a0 = __fma_rn(w, w, a0);
+        a1 = __fma_rn(v.rh[i], w, a1);
+      };
+      if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
+      else csr_rows<L>(C, gather, epi);
+      double red[2] = {a0, a1};
+      block_sum<2>(red, sm);
+      if (threadIdx.x == 0) {
+        pb[blockIdx.x] = red[0];
+        pb[gridDim.x + blockIdx.x] = red[1];
+      }
+      grid_sync(bar);
+      double t[2];
+      all_blocks_sum<2>(pb, t, sm, s_tot);
+      const double rr = sqrt(t[0]);
+      relres_rec = rr / nb;
+      if (k > 0 || restarts > 0) relres_true = relres_rec;  // this pass was an exit check
+      if (rr <= tol * nb) {
+        relres_true = relres_rec;
+        done = BD_CONVERGED;
+        break;
+      }
+      if (k > 0) restarts++;
+      rho = t[1];
+      rho_old = alpha = omega = 1.0;
+      need_resid = false;
+    }
+    if (k >= max_iter) {
+      done = BD_MAXIT;
+      break;
+    }
+    if (rho == 0.0 || !(rho == rho)) {
+      done = rho == 0.0 ? BD_BREAKDOWN : BD_NONFINITE;
+      break;
+    }
+    const double beta = (rho / rho_old) * (alpha / omega);
+    // ---- P1: p = r + beta (p - omega v) ; p^ = M^-1 p
+    for (int64_t blk = tid; blk < nblk; blk += nth) {
+      double u[BS], y[BS];
+      int64_t pos[BS];
+#pragma unroll
+      for (int a = 0; a < BS; a++) {
+        const int64_t o = blk * BS + a;
+        pos[a] = (BS > 1 && v.iperm && o < n) ? v.iperm[o] : o;
+        const int64_t i = pos[a];
+        u[a] = 0.0;
+        if (o < n) {
+          u[a] = __fma_rn(beta, __fma_rn(-omega, v.v[i], v.p[i]), v.r[i]);
+          v.p[i] = u[a];
+        }
+      }
+      bj(blk, u, y);
+#pragma unroll
+      for (int a = 0; a < BS; a++)
+        if (blk * BS + a < n) v.ph[pos[a]] = y[a];
+    }
+    grid_sync(bar);
+    // ---- P2: v = A p^ ; sigma = r^.v
+    {
+      double a0 = 0.0;
+      auto gather = [&](int j) { return __ldg(v.ph + j); };
+      auto epi = [&](int64_t i, double s) {
+        v.v[i] = s;
+        a0 = __fma_rn(v.rh[i], s, a0);
+      };
+      if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
+      else csr_rows<L>(C, gather, epi);
+      double red[1] = {a0};
+      block_sum<1>(red, sm);
+      if (threadIdx.x == 0) pa[blockIdx.x] = red[0];
+    }
+    grid_sync(bar);
+    {
+      double t[1];
+      all_blocks_sum<1>(pa, t, sm, s_tot);
+      if (t[0] == 0.0 || !(t[0] == t[0])) {
+        done = t[0] == 0.0 ? BD_BREAKDOWN : BD_NONFINITE;
+        break;
+      }
+      alpha = rho / t[0];
+      k++;
+    }
+    // ---- P3: s = r - alpha v (kept in r) ; ||s|| ; s^ = M^-1 s
+    {
+      double a0 = 0.0;
+      for (int64_t blk = tid; blk < nblk; blk += nth) {
+        double u[BS], y[BS];
+        int64_t pos[BS];
+#pragma unroll
+        for (int a = 0; a < BS; a++) {
+          const int64_t o = blk * BS + a;
+          pos[a] = (BS > 1 && v.iperm && o < n) ? v.iperm[o] : o;
+          const int64_t i = pos[a];
+          u[a] = 0.0;
+          if (o < n) {
+            u[a] = __fma_rn(-alpha, v.v[i], v.r[i]);
+            v.r[i] = u[a];
+            a0 = __fma_rn(u[a], u[a], a0);
+          }
+        }
+        bj(blk, u, y);
+#pragma unroll
+        for (int a = 0; a < BS; a++)
+          if (blk * BS + a < n) v.sh[pos[a]] = y[a];
+      }
+      double red[1] = {a0};
+      block_sum<1>(red, sm);
+      if (threadIdx.x == 0) pb[blockIdx.x] = red[0];
+    }
+    grid_sync(bar);
+    {
+      double t[1];
+      all_blocks_sum<1>(pb, t, sm, s_tot);
+      const double ss = sqrt(t[0]);
+      if (ss <= tol * nb) {  // converged at the half step: x += alpha p^, then the exit check
+        relres_rec = ss / nb;
+        for (int64_t i = tid; i < n; i += nth) v.x[i] = __fma_rn(alpha, v.ph[i], v.x[i]);
+        grid_sync(bar);
+        need_resid = true;
+        continue;
+      }
+    }
+    // ---- P4: t = A s^ ; (t.s, t.t)
+    {
+      double a0 = 0.0, a1 = 0.0;
+      auto gather = [&](int j) { return __ldg(v.sh + j); };
+      auto epi = [&](int64_t i, double s) {
+        v.t[i] = s;
+        a0 = __fma_rn(s, v.r[i], a0);
+        a1 = __fma_rn(s, s, a1);
+      };
+      if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
+      else csr_rows<L>(C, gather, epi);
+      double red[2] = {a0, a1};
+      block_sum<2>(red, sm);
+      if (threadIdx.x == 0) {
+        pa[blockIdx.x] = red[0];
+        pa[gridDim.x + blockIdx.x] = red[1];
+      }
+    }
+    grid_sync(bar);
+    {
+      double t[2];
+      all_blocks_sum<2>(pa, t, sm, s_tot);
+      omega = t[1] > 0.0 ? t[0] / t[1] : 0.0;
+    }
+    // ---- P5: x += alpha p^ + omega s^ ; r = s - omega t ; (r.r, r^.r)
+    {
+      double a0 = 0.0, a1 = 0.0;
+      for (int64_t i = tid; i < n; i += nth) {
+        v.x[i] = __fma_rn(omega, v.sh[i], __fma_rn(alpha, v.ph[i], v.x[i]));
+        const double ri = __fma_rn(-omega, v.t[i], v.r[i]);
+        v.r[i] = ri;
+        a0 = __fma_rn(ri, ri, a0);
+        a1 = __fma_rn(v.rh[i], ri, a1);
+      }
+      double red[2] = {a0, a1};
+      block_sum<2>(red, sm);
+      if (threadIdx.x == 0) {
+        pb[blockIdx.x] = red[0];
+        pb[gridDim.x + blockIdx.x] = red[1];
+      }
+    }
+    grid_sync(bar);
+    {
+      double t[2];
+      all_blocks_sum<2>(pb, t, sm, s_tot);
+      const double rr = sqrt(t[0]);
+      relres_rec = rr / nb;
+      if (rr <= tol * nb) {
+        need_resid = true;  // exit check (and restart if it fails)
+        continue;
+      }
+      if (omega == 0.0) {
+        done = BD_BREAKDOWN;
+        break;
+      }
+      rho_old = rho;
+      rho = t[1];
+    }
+  }
+  if (done == BD_MAXIT || done == BD_BREAKDOWN || done == BD_NONFINITE) {  // final true residual
+    grid_sync(bar);
+    double a0 = 0.0;
+    auto gather = [&](int j) { return __ldg(v.x + j); };
+    auto epi = [&](int64_t i, double s) {
+      const double w = v.b[i] - s;
+      a0 = __fma_rn(w, w, a0);
+    };
+    if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
+    else csr_rows<L>(C, gather, epi);
+    double red[1] = {a0};
+    block_sum<1>(red, sm);
+    if (threadIdx.x == 0) pa[blockIdx.x] = red[0];
+    grid_sync(bar);
+    double t[1];
+    all_blocks_sum<1>(pa, t, sm, s_tot);
+    relres_true = sqrt(t[0]) / nb;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->nb = nb;
+    st->relres_rec = relres_rec;
+    st->relres_true = relres_true;
+    st->k = k;
+    st->restarts = restarts;
+    st->done = done;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+template <int BS>
+static void *bicg_fn(int fmt, int lanes) {
+  if (fmt == PCG_FORMAT_SELL) return (void *)bicg_kernel<PCG_FORMAT_SELL, 1, BS>;
+  switch (lanes) {
+    case 1: return (void *)bicg_kernel<PCG_FORMAT_CSR, 1, BS>;
+    case 2: return (void *)bicg_kernel<PCG_FORMAT_CSR, 2, BS>;
+    case 4: return (void *)bicg_kernel<PCG_FORMAT_CSR, 4, BS>;
+    case 8: return (void *)bicg_kernel<PCG_FORMAT_CSR, 8, BS>;
+    case 16: return (void *)bicg_kernel<PCG_FORMAT_CSR, 16, BS>;
+    default: return (void *)bicg_kernel<PCG_FORMAT_CSR, 32, BS>;
+  }
+}
+
+static void *bicg_select(int fmt, int lanes, int bs) {
+  switch (bs) {
+    case 1: return bicg_fn<1>(fmt, lanes);
+    case 2: return bicg_fn<2>(fmt, lanes);
+    case 4: return bicg_fn<4>(fmt, lanes);
+    default: return bicg_fn<8>(fmt, lanes);
+  }
+}
+
+static pcg_status bicg_setup(pcg_matrix *A, int bs, cudaStream_t st) {
+  SolveWork &w = A->work;
+  if (!w.bv) {
+    const size_t nb = sizeof(double) * ((size_t)A->n + 64);
+    PCG_CUDA(cudaMalloc(&w.bv, nb * 8));  // x r rh p ph v sh t
+    PCG_CUDA(cudaMemsetAsync(w.bv, 0, nb * 8, st));
+    PCG_CUDA(cudaMalloc(&w.bstate, sizeof(BicgState)));
+    PCG_CUDA(cudaMalloc(&w.bbar, sizeof(GridBar)));
+    PCG_CUDA(cudaMemsetAsync(w.bbar, 0, sizeof(GridBar), st));
+    shadow_kernel<<<(unsigned)std::min<int64_t>((A->n + 255) / 256, 148 * 16), 256, 0, st>>>(
+        A->n, A->d_perm, w.bv + 2 * (A->n + 64));
+    count_launch();
+    PCG_CUDA(cudaGetLastError());
+  }
+  if (bs > 1 && w.bminv_bs != bs) {
+    if (w.bminv) cudaFree(w.bminv);
+    w.bminv = nullptr;
+    const int64_t nblk = (A->n + bs - 1) / bs;
+    // LU factors then pivots in one allocation
+    PCG_CUDA(cudaMalloc(&w.bminv, sizeof(double) * (size_t)nblk * bs * bs + sizeof(int) * (size_t)nblk * bs + 64));
+    double *lu = w.bminv;
+    int *piv = reinterpret_cast<int *>(w.bminv + (size_t)nblk * bs * bs);
+    int *err;
+    PCG_CUDA(cudaMalloc(&err, sizeof(int)));
+    PCG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+    const unsigned g = (unsigned)((nblk + 127) / 128);
+    switch (bs) {
+      case 2: bj_lu_kernel<2><<<g, 128, 0, st>>>(A->n, A->d_row_ptr, A->d_col, A->d_val, A->d_perm, A->d_iperm, lu, piv, err); break;
+      case 4: bj_lu_kernel<4><<<g, 128, 0, st>>>(A->n, A->d_row_ptr, A->d_col, A->d_val, A->d_perm, A->d_iperm, lu, piv, err); break;
+      default: bj_lu_kernel<8><<<g, 128, 0, st>>>(A->n, A->d_row_ptr, A->d_col, A->d_val, A->d_perm, A->d_iperm, lu, piv, err); break;
+    }
+    count_launch();
+    int h = 0;
+    PCG_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PCG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(err);
+    if (h) return fail(PCG_ERR_ZERO_DIAGONAL, "pcg_bicgstab: a Block-Jacobi diagonal block is singular");
+    w.bminv_bs = bs;
+  }
+  return PCG_OK;
+}
+
+static pcg_status bicg_impl(pcg_matrix *A, const double *b, double *x, double tol, int64_t max_iter, int bs,
+                            cudaStream_t st, pcg_info *info) {
+  PCG_TRY(ensure_work(A));
+  PCG_TRY(bicg_setup(A, bs, st));
+  SolveWork &w = A->work;
+  const int64_t n = A->n, ldv = n + 64;
+  BicgVecs v;
+  v.x = w.bv;
+  v.r = w.bv + ldv;
+  v.rh = w.bv + 2 * ldv;
+  v.p = w.bv + 3 * ldv;
+  v.ph = w.bv + 4 * ldv;
+  v.v = w.bv + 5 * ldv;
+  v.sh = w.bv + 6 * ldv;
+  v.t = w.bv + 7 * ldv;
+  v.dinv = A->d_dinv;
+  v.lu = w.bminv;
+  v.piv = bs > 1 ? reinterpret_cast<const int *>(w.bminv + (size_t)((n + bs - 1) / bs) * bs * bs) : nullptr;
+  v.iperm = A->d_iperm;
+  const bool b_dev = is_device_ptr(b), x_dev = is_device_ptr(x);
+  // b -> stage_b, x0 -> v.x (through the SELL-C-sigma permutation when the handle has one)
+  if (A->d_perm) {
+    const double *bs_ = b, *xs = x;
+    if (!b_dev) {
+      PCG_CUDA(cudaMemcpyAsync(w.w, b, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      bs_ = w.w;
+    }
+    PCG_TRY(perm_in(A, bs_, w.stage_b, st));
+    if (!x_dev) {
+      PCG_CUDA(cudaMemcpyAsync(w.q, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      xs = w.q;
+    }
+    PCG_TRY(perm_in(A, xs, v.x, st));
+  } else {
+    PCG_CUDA(cudaMemcpyAsync(w.stage_b, b, sizeof(double) * n, b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                             st));
+    PCG_CUDA(cudaMemcpyAsync(v.x, x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  }
+  v.b = w.stage_b;
+  BicgState hs;
+  memset(&hs, 0, sizeof(hs));
+  hs.tol = tol;
+  hs.max_iter = max_iter;
+  BicgState *dst = (BicgState *)w.bstate;
+  PCG_CUDA(cudaMemcpyAsync(dst, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+  void *fn = bicg_select(A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format, A->csr_lanes, bs);
+  if (w.bgrid == 0 || w.bgrid_bs != bs) {
+    int nbk = 0;
+    PCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbk, fn, BLOCK, 0));
+    w.bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(A->device) * std::min(nbk, 8),
+                                                         std::max<int64_t>(1, (n + BLOCK - 1) / BLOCK)));
+    w.bgrid_bs = bs;
+  }
+  SellView S = A->sell();
+  CsrView Cv = A->csr();
+  double *part = w.partials;  // 4 x grid (<= 8 x SMs; partials hold 6 x 32 x SMs)
+  GridBar *bar = (GridBar *)w.bbar;
+  void *args[] = {&S, &Cv, &v, &dst, &part, &bar};
+  cudaEvent_t e0, e1;
+  PCG_CUDA(cudaEventCreate(&e0));
+  PCG_CUDA(cudaEventCreate(&e1));
+  PCG_CUDA(cudaEventRecord(e0, st));
+  PCG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(w.bgrid), dim3(BLOCK), args, 0, st));
+  count_launch();
+  PCG_CUDA(cudaEventRecord(e1, st));
+  if (A->d_perm) {
+    if (x_dev) {
+      PCG_TRY(perm_out(A, v.x, x, st));
+    } else {
+      PCG_TRY(perm_out(A, v.x, w.w, st));
+      PCG_CUDA(cudaMemcpyAsync(x, w.w, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    }
+  } else {
+    PCG_CUDA(cudaMemcpyAsync(x, v.x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  }
+  PCG_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  pcg_status s;
+  switch (hs.done) {
+    case BD_CONVERGED: s = hs.relres_true <= tol ? PCG_OK : PCG_NOT_CONVERGED; break;
+    case BD_ZERO_RHS: s = PCG_OK; break;
+    case BD_MAXIT: s = PCG_NOT_CONVERGED; break;
+    case BD_BREAKDOWN: s = PCG_ERR_BREAKDOWN; break;
+    default: s = PCG_ERR_NONFINITE; break;
+  }
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->iterations = hs.k;
+    info->relres_recurrence = hs.relres_rec;
+    info->relres_true = hs.done == BD_ZERO_RHS ? 0.0 : hs.relres_true;
+    info->converged = s == PCG_OK;
+    info->status = s;
+    info->replacements = hs.restarts;
+    info->t_solve_s = ms * 1e-3;
+    const double nn = (double)n, nz = (double)A->nnz;
+    // per iteration: 2 SpMVs (12 nnz + 4(n+1) + gather 8n + write 8n + r^ 8n each) + 3 streaming passes
+    // P1 (r,p,v in; p,p^ out: 40n + M^-1 8 bs n), P3 (r,v in; r,s^ out: 32n + 8 bs n), P5 (x,p^,s^,r,t,r^ in; x,r out: 64n)
+    info->bytes_algorithmic = (double)hs.k * (2 * (12.0 * nz + 4.0 * (nn + 1) + 24.0 * nn) + 136.0 * nn + 16.0 * bs * nn);
+    info->flops = (double)hs.k * (4.0 * nz + 30.0 * nn);
+  }
+  if (s == PCG_ERR_BREAKDOWN) set_error("pcg_bicgstab: breakdown (rho, r^.v or omega = 0)");
+  if (s == PCG_NOT_CONVERGED) set_error("pcg_bicgstab: not converged within max_iter");
+  if (s == PCG_ERR_NONFINITE) set_error("pcg_bicgstab: non-finite right-hand side or iterate");
+  return s;
+}
+
+}  // namespace pcgb
+
+using namespace pcgb;
+
+extern "C" pcg_status pcg_bicgstab(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
+                                   int32_t block_size, void *stream, pcg_info *info) {
+  if (!A || ((!b || !x) && A->n > 0)) return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab: null argument");
+  if (!(tol > 0.0) || max_iter < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab: tol > 0 and max_iter >= 1");
+  if (block_size != 1 && block_size != 2 && block_size != 4 && block_size != 8)
+    return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab: block_size must be 1, 2, 4 or 8");
+  if (A->comm) return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab: single-GPU handles only");
+  if (A->n == 0) {
+    if (info) {
+      memset(info, 0, sizeof(*info));
+      info->converged = 1;
+    }
+    return PCG_OK;
+  }
+  std::lock_guard<std::mutex> lk(A->mu);
+  PCG_CUDA(cudaSetDevice(A->device));
+  return bicg_impl(A, b, x, tol, max_iter, block_size, (cudaStream_t)stream, info);
+}

@@ -52,6 +52,11 @@ struct SolveWork {
   // persistent cooperative solve (persist.cu)
   void *pbar = nullptr;  // grid barrier state
   int pgrid = 0;
+  // BiCGSTAB (bicgstab.cu): x r r^ p p^ v s^ t, state, barrier, Block-Jacobi inverses
+  double *bv = nullptr;
+  void *bstate = nullptr, *bbar = nullptr;
+  double *bminv = nullptr;
+  int bminv_bs = 0, bgrid = 0, bgrid_bs = 0;
 };
 
 // single-RHS solver vectors (p0/p1: direction double buffer of the 2-pass schedule)

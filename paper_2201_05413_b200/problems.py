@@ -65,3 +65,28 @@ def fem_build(spec: FemSpec, row_begin: int = 0, row_end: int | None = None, dev
                              max(rows, 1), st), "fem_assemble")
     return {"row_ptr": rp, "col": col, "val": val, "B": B.t(), "n_global": n, "row_begin": row_begin,
             "row_end": row_end}
+
+
+FD_X2MY2, FD_EXPSIN = 1, 2
+
+
+def fd_cube_build(N: int, fkind: int = FD_X2MY2, row_begin: int = 0, row_end: int | None = None, device=None,
+                  stream=None):
+    """The paper's Table 1 system (FD Laplace on N^3 nodes, identity boundary rows,
+    b = f on the boundary; include/fem_gen.h fd_cube_*), rows [row_begin, row_end),
+    assembled on the GPU.  Returns dict(row_ptr, col, val, b) of torch CUDA tensors."""
+    import torch
+    n = N ** 3
+    row_end = n if row_end is None else row_end
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    st = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream if stream is None else stream.cuda_stream)
+    rows = row_end - row_begin
+    rp = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+    nnz = C.c_int64()
+    check(lib().fd_cube_count(N, row_begin, row_end, C.c_void_p(rp.data_ptr()), C.byref(nnz), st), "fd_cube_count")
+    col = torch.empty(max(nnz.value, 1), dtype=torch.int64, device=dev)[:nnz.value]
+    val = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=dev)[:nnz.value]
+    b = torch.empty(max(rows, 1), dtype=torch.float64, device=dev)[:rows]
+    check(lib().fd_cube_assemble(N, fkind, row_begin, row_end, C.c_void_p(rp.data_ptr()), C.c_void_p(col.data_ptr()),
+                                 C.c_void_p(val.data_ptr()), C.c_void_p(b.data_ptr()), st), "fd_cube_assemble")
+    return {"row_ptr": rp, "col": col, "val": val, "b": b, "n": n}

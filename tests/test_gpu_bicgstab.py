@@ -1,0 +1,144 @@
+"""GPU parity for SURVEY §8(f) N2 (reading R2): the paper's Table 1 grid
+systems (identity boundary rows, nonsymmetric) assembled on the device, and the
+right-preconditioned BiCGSTAB with (Block-)Jacobi, through the C ABI, against the
+oracle (oracle/oracle.c orc_fd_cube, orc_bicgstab).
+
+Bars: structure, values and RHS bitwise (integers and exactly rounded x^2 - y^2);
+solution rel-L2 <= 1e-9 vs the oracle, true relres <= tol; and — because
+BiCGSTAB's iteration count reacts to rounding-level perturbations far more than
+CG's (the oracle alone spans 176-211 iterations at N = 64, bs = 4, when b is
+perturbed by 1e-15 relative) — the GPU count must lie within max(2 %, 2) of the
+range the ORACLE itself spans under eight such perturbations (seeded) and the
+unperturbed solve.  For f = x^2 - y^2 the discrete solution is f itself, so the
+GPU answer is also checked against that closed form.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pcg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_05413_b200 as p
+    return p
+
+
+def _grid(N):
+    h = 1.0 / (N - 1)
+    i = np.arange(N)
+    return np.tile(i, N * N) * h, np.tile(np.repeat(i, N), N) * h
+
+
+def _oracle_range(A, b, tol, bs, k=8):
+    rng = np.random.default_rng(2201)
+    its = [O.bicgstab(A, b, tol=tol, block=bs).iterations]
+    for _ in range(k):
+        its.append(O.bicgstab(A, b * (1 + 1e-15 * rng.standard_normal(A.n)), tol=tol, block=bs).iterations)
+    return min(its), max(its)
+
+
+@pytest.mark.parametrize("N,fkind", [(16, O.FD_X2MY2), (33, O.FD_EXPSIN), (48, O.FD_X2MY2)])
+def test_fd_cube_generator_bitwise(pcg, N, fkind):
+    from paper_2201_05413_b200.problems import fd_cube_build
+    A, b = O.fd_cube(N, fkind)
+    G = fd_cube_build(N, fkind)
+    assert np.array_equal(G["row_ptr"].cpu().numpy(), A.row_ptr)
+    assert np.array_equal(G["col"].cpu().numpy(), A.col)
+    assert np.array_equal(G["val"].cpu().numpy(), A.val)
+    bg = G["b"].cpu().numpy()
+    if fkind == O.FD_X2MY2:
+        assert np.array_equal(bg, b)
+    else:  # exp(pi x) sinpi(y) vs exp(M_PI x) sin(M_PI y)
+        assert np.all(np.abs(bg - b) <= 4e-16 * np.abs(b).max())
+    # a row range (one rank's slab) is the same rows
+    r0, r1 = N * N * 3 + 5, N * N * 7 + 11
+    Gs = fd_cube_build(N, fkind, r0, r1)
+    assert np.array_equal(Gs["col"].cpu().numpy(), A.col[A.row_ptr[r0]:A.row_ptr[r1]])
+
+
+@pytest.mark.parametrize("N,bs", [(20, 1), (20, 2), (20, 4), (20, 8), (40, 1), (40, 4), (48, 8)])
+def test_bicgstab_parity_on_table1_grids(pcg, N, bs):
+    from paper_2201_05413_b200.problems import fd_cube_build
+    A, b = O.fd_cube(N)
+    tol = 1e-12
+    r = O.bicgstab(A, b, tol=tol, block=bs)
+    assert r.status == O.OK
+    lo, hi = _oracle_range(A, b, tol, bs)
+    G = fd_cube_build(N)
+    M = pcg.Matrix.from_csr(G["row_ptr"], G["col"], G["val"])
+    x, info = M.bicgstab(G["b"], tol=tol, block=bs)
+    x = x.cpu().numpy()
+    assert info["status"] == 0 and info["relres_true"] <= tol
+    assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) <= 1e-9
+    assert lo - max(2, 0.02 * lo) <= info["iterations"] <= hi + max(2, 0.02 * hi), (info["iterations"], r.iterations,
+                                                                                      lo, hi)
+    X, Y = _grid(N)
+    assert np.max(np.abs(x - (X * X - Y * Y))) <= 1e-9  # the discrete solution is x^2 - y^2
+
+
+@pytest.mark.parametrize("name,c", [("C1", 32), ("C2", 48), ("C3", 24)])
+def test_bicgstab_on_spd_fem_systems(pcg, name, c):
+    """BiCGSTAB through the same handles CG uses (SELL-32 / SELL-C-sigma formats)."""
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    import torch
+    M = pcg.Matrix.from_csr(torch.as_tensor(A.row_ptr).cuda(), torch.as_tensor(A.col).cuda(),
+                            torch.as_tensor(A.val).cuda())
+    r = O.bicgstab(A, b, tol=1e-11)
+    lo, hi = _oracle_range(A, b, 1e-11, 1)
+    for bb in (torch.as_tensor(b).cuda(), torch.as_tensor(b)):
+        x, info = M.bicgstab(bb, tol=1e-11)
+        x = x.cpu().numpy()
+        assert info["status"] == 0 and info["relres_true"] <= 1e-11
+        assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) <= 1e-9
+        assert lo - max(2, 0.02 * lo) <= info["iterations"] <= hi + max(2, 0.02 * hi)
+
+
+def test_bicgstab_edges_and_errors(pcg):
+    import torch
+    from paper_2201_05413_b200 import PcgError
+    from paper_2201_05413_b200.problems import fd_cube_build
+    G = fd_cube_build(12)
+    M = pcg.Matrix.from_csr(G["row_ptr"], G["col"], G["val"])
+    b = G["b"]
+    # zero right-hand side: x = 0, 0 iterations
+    x, info = M.bicgstab(torch.zeros_like(b), x0=torch.ones_like(b))
+    assert info["iterations"] == 0 and float(x.abs().max()) == 0.0
+    # already converged x0: 0 iterations
+    xs, _ = M.bicgstab(b, tol=1e-14)
+    x, info = M.bicgstab(b, x0=xs, tol=1e-10)
+    assert info["iterations"] == 0 and info["status"] == 0
+    # max_iter: NOT_CONVERGED after exactly max_iter steps, like the oracle
+    A, bo = O.fd_cube(12)
+    ro = O.bicgstab(A, bo, tol=1e-12, max_iter=4)
+    x, info = M.bicgstab(b, tol=1e-12, max_iter=4)
+    assert info["status"] == 1 and info["iterations"] == 4 and ro.status == O.NOT_CONVERGED
+    assert np.linalg.norm(x.cpu().numpy() - ro.x) / np.linalg.norm(ro.x) <= 1e-12
+    # M = diag: one step
+    I = pcg.Matrix.from_csr(torch.tensor([0, 1, 2, 3]).cuda(), torch.tensor([0, 1, 2]).cuda(),
+                            torch.tensor([2.0, 4.0, 8.0]).cuda())
+    x, info = I.bicgstab(torch.tensor([2.0, 4.0, 8.0]).cuda(), tol=1e-14)
+    assert info["iterations"] == 1 and np.allclose(x.cpu().numpy(), 1.0)
+    for bad in (3, 16, 0):
+        with pytest.raises(PcgError) as e:
+            M.bicgstab(b, block=bad)
+        assert e.value.status == 2
+    # Block-Jacobi on a SELL-C-sigma handle: blocks in the caller's numbering, like the oracle
+    P = O.build_problem("C3", c=16)
+    A3, b3 = P["A"], P["B"][:, 0]
+    S = pcg.Matrix.from_csr(torch.as_tensor(A3.row_ptr).cuda(), torch.as_tensor(A3.col).cuda(),
+                            torch.as_tensor(A3.val).cuda(), fmt="sigma")
+    assert S.stats()["format"] == 4
+    for bs in (1, 4):
+        r3 = O.bicgstab(A3, b3, tol=1e-11, block=bs)
+        lo, hi = _oracle_range(A3, b3, 1e-11, bs)
+        x, info = S.bicgstab(torch.as_tensor(b3).cuda(), tol=1e-11, block=bs)
+        assert info["status"] == 0 and info["relres_true"] <= 1e-11
+        assert np.linalg.norm(x.cpu().numpy() - r3.x) / np.linalg.norm(r3.x) <= 1e-9
+        assert lo - max(2, 0.02 * lo) <= info["iterations"] <= hi + max(2, 0.02 * hi)
