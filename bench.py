@@ -197,7 +197,10 @@ def main():
     ap.add_argument("--comm", default="nccl", choices=["nccl", "callbacks"],
                     help="callbacks: exchange steps through host callbacks over gloo (validation of the N>1 "
                          "path when ranks share a GPU; not a performance number)")
+    ap.add_argument("--block", type=int, default=1, help="Block-Jacobi block size for the CUBE* BiCGSTAB configs")
     args = ap.parse_args()
+    if args.config.startswith("CUBE"):
+        return run_bicgstab(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -437,6 +440,119 @@ def main():
         comm.close()
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+# ------------------------------------------------------------------------------ SURVEY §8(f) N2
+CUBES = {"CUBE1": 128, "CUBE2": 256, "CUBE3": 512}  # the paper's Table 1 grids, nodes per axis
+
+
+def run_bicgstab(args):
+    """The paper's own iterative experiment on its own regular grids: BiCGSTAB + (Block-)
+    Jacobi on the Table 1 identity-row FD systems, eps = 1e-12,
+    boundary data x^2 - y^2 (reading R2).  A step = one pcg_bicgstab solve
+    from x0 = 0 on one GPU; the iteration is one cooperative kernel, so the roofline is
+    the whole iteration's algorithmic bytes over its time."""
+    N = args.c or CUBES[args.config]
+    tol, bs = 1e-12, args.block
+    n = N ** 3
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return 0
+        import oracle as O
+        Ns = 48
+        A, b = O.fd_cube(Ns)
+        times, its = [], 0
+        for s_ in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            r = O.bicgstab(A, b, tol=tol, block=bs)
+            if s_ >= args.warmup:
+                times.append(time.perf_counter() - t0)
+            its = r.iterations
+        iters = its * (N - 1) / (Ns - 1)  # BiCGSTAB+Jacobi steps grow ~linearly in N here (37/81/169 at 16/32/64)
+        nnz = 7 * (N - 2) ** 3 + n - (N - 2) ** 3
+        per_iter_bytes = lambda nn, zz: 2 * (12.0 * zz + 28.0 * nn) + 136.0 * nn  # noqa: E731
+        v = statistics.median(times) / its * per_iter_bytes(n, nnz) / per_iter_bytes(A.n, A.nnz) * iters
+        line = {"impl": "reference", "metric": "bicgstab_time_to_solution", "value": v, "unit": "s", "n_gpus": 1,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{args.config}: Table 1 grid {N}^3 nodes, BiCGSTAB block={bs}", "n": n},
+                "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
+                                 "sample": f"oracle BiCGSTAB on the {Ns}^3 grid ({its} iterations), scaled by "
+                                           f"per-iteration bytes x {iters:.0f} estimated iterations"},
+                "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+    import torch
+
+    import paper_2201_05413_b200 as pcg
+    from paper_2201_05413_b200.problems import fd_cube_build
+    torch.cuda.set_device(0)
+    t0 = time.perf_counter()
+    G = fd_cube_build(N)
+    A = pcg.Matrix.from_csr(G["row_ptr"], G["col"], G["val"], fmt=args.fmt)
+    b = G["b"].contiguous()
+    nnz = G["col"].numel()
+    del G
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        A.bicgstab(b, tol=tol, block=bs)
+
+    def timed(device_inputs):
+        bb = b if device_inputs else b.cpu().pin_memory()
+        xx = torch.empty_like(bb) if device_inputs else torch.empty(bb.shape, dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        l0 = pcg.kernel_launches()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st = torch.cuda.current_stream()
+        infos = []
+        with ClockSampler(0) as cs:
+            e0.record(st)
+            for _ in range(args.steps):
+                xx.zero_()
+                x, inf = A.bicgstab(bb, tol=tol, block=bs, out=xx)
+                infos.append(inf)
+            e1.record(st)
+            torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.steps, infos, pcg.kernel_launches() - l0, cs, x
+
+    ms, infos, launches, cs, x = timed(True)
+    remeasured = False
+    if cs.bad():
+        ms, infos, launches, cs, x = timed(True)
+        remeasured = True
+    ms_e2e = timed(False)[0]
+    inf = infos[-1]
+    iters = inf["iterations"]
+    hbm, peak_kind = peaks()
+    per_iter_bytes = inf["bytes_algorithmic"] / max(iters, 1)
+    achieved = per_iter_bytes * iters / (inf["t_solve_s"]) / 1e9
+    # x_err of Eq. ERROR-METRIC (P:127-131): the discrete solution is x^2 - y^2 exactly
+    h = 1.0 / (N - 1)
+    idx = torch.arange(n, device=x.device, dtype=torch.float64)
+    X = torch.remainder(idx, N) * h
+    Y = torch.remainder(torch.div(idx, N, rounding_mode="floor"), N) * h
+    xg = X * X - Y * Y
+    x_err = float(torch.linalg.norm(x.to(xg.device) - xg) / torch.linalg.norm(xg))
+    line = {"metric": "bicgstab_time_to_solution", "value": ms / 1e3, "unit": "s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: paper Table 1 grid, {N}^3 nodes, identity boundary rows, "
+                                   f"b = x^2 - y^2 on the boundary; BiCGSTAB + "
+                                   f"{'Jacobi' if bs == 1 else f'Block-Jacobi({bs})'}, eps = 1e-12, x0 = 0",
+                       "n": n, "nnz": nnz, "tol": tol, "block": bs, "iterations": iters, "relres_true": inf["relres_true"],
+                       "x_err": x_err, "format": {1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[A.stats()["format"]],
+                       "setup_s": round(setup, 3), "parallelism": "1 GPU",
+                       "paper_context": "Cube 1 (128^3): BiCGSTAB+BJacobi 17.4 s, 128 it. on 1 Broadwell core; "
+                                        "0.34 s on 576 cores (P:211, P:220, eps 1e-12)"},
+            "roofline": {"bound": "hbm", "kernel": "bicg_kernel (whole BiCGSTAB iteration, one cooperative kernel)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "peak_source": peak_kind, "traffic": None, "bytes_per_iteration": per_iter_bytes},
+            "cpu_baseline": None,
+            "e2e": {"value": ms_e2e / 1e3, "unit": "s", "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": launches, "clocks": cs.summary(), "remeasured": remeasured}
+    print(json.dumps(line), flush=True)
     return 0
 
 

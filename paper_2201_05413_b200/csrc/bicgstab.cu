@@ -114,51 +114,167 @@ __global__ void bj_lu_kernel(int64_t n, const int *__restrict__ rp, const int *_
 
 enum { BD_RUNNING = 0, BD_CONVERGED = 1, BD_MAXIT = 2, BD_BREAKDOWN = 3, BD_ZERO_RHS = 4, BD_NONFINITE = 5 };
 
+// Block-uniform scalar state lives in shared memory (thread 0 writes after the
+// fixed-order reductions, a barrier publishes), not in registers across the
+// passes; each pass is its own non-inlined function, so the SpMV passes get a
+// register allocation of their own (no spills in the gather loops).
+struct BicgShared {
+  double rho, rho_old, alpha, omega, beta, nb, relres_rec, relres_true;
+  long long k, restarts;
+  int done, need_resid, half;
+};
+
+enum { SP_RESID = 0, SP_AV = 1, SP_AT = 2, SP_FINAL = 3 };
+
+// the SpMV passes: RESID w = b - A x (r = w, p = v = 0; partials w.w, r^.w),
+// AV v = A p^ (r^.v), AT t = A s^ (t.s, t.t), FINAL w = b - A x (w.w)
+template <int FMT, int L, int MODE>
+__device__ __noinline__ void bicg_spmv_pass(const SellView &S, const CsrView &C, const BicgVecs &v, double *out,
+                                            double (*sm)[WARPS]) {
+  double a0 = 0.0, a1 = 0.0;
+  const double *__restrict__ G = MODE == SP_AV ? v.ph : (MODE == SP_AT ? v.sh : v.x);
+  auto gather = [&](int j) { return __ldg(G + j); };
+  auto epi = [&](int64_t i, double sv) {
+    if (MODE == SP_RESID || MODE == SP_FINAL) {
+      const double w = v.b[i] - sv;
+      a0 = __fma_rn(w, w, a0);
+      if (MODE == SP_RESID) {
+        v.r[i] = w;
+        v.p[i] = 0.0;
+        v.v[i] = 0.0;
+        a1 = __fma_rn(v.rh[i], w, a1);
+      }
+    } else if (MODE == SP_AV) {
+      v.v[i] = sv;
+      a0 = __fma_rn(v.rh[i], sv, a0);
+    } else {
+      v.t[i] = sv;
+      a0 = __fma_rn(sv, v.r[i], a0);
+      a1 = __fma_rn(sv, sv, a1);
+    }
+  };
+  if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
+  else csr_rows<L>(C, gather, epi);
+  double red[2] = {a0, a1};
+  block_sum<2>(red, sm);
+  if (threadIdx.x == 0) {
+    out[blockIdx.x] = red[0];
+    out[gridDim.x + blockIdx.x] = red[1];
+  }
+}
+
+// y = M^-1 u on block blk: BS = 1 dinv * u; else P, L, U substitution (oracle bj_apply order)
+template <int BS>
+__device__ __forceinline__ void bj_apply(const BicgVecs &v, int64_t n, int64_t blk, const double (&u)[BS],
+                                         double (&y)[BS]) {
+  if (BS == 1) {
+    y[0] = __dmul_rn(v.dinv[blk], u[0]);
+  } else {
+    const double *D = v.lu + blk * BS * BS;
+    const int *pv = v.piv + blk * BS;
+    const int m = (int)((blk * BS + BS <= n) ? BS : n - blk * BS);
+#pragma unroll
+    for (int a = 0; a < BS; a++) {  // L z = P u
+      double sacc = 0.0;
+      const int pr = pv[a];
+#pragma unroll
+      for (int c = 0; c < BS; c++)
+        if (c == pr) sacc = u[c];
+#pragma unroll
+      for (int c = 0; c < a; c++) sacc = __dsub_rn(sacc, __dmul_rn(D[a * BS + c], y[c]));
+      y[a] = sacc;
+    }
+#pragma unroll
+    for (int a = BS - 1; a >= 0; a--) {  // U y = z
+      if (a >= m) continue;
+      double sacc = y[a];
+#pragma unroll
+      for (int c = a + 1; c < BS; c++)
+        if (c < m) sacc = __dsub_rn(sacc, __dmul_rn(D[a * BS + c], y[c]));
+      y[a] = __ddiv_rn(sacc, D[a * BS + a]);
+    }
+  }
+}
+
+// P1 (STAGE 0): p = r + beta (p - omega v) ; p^ = M^-1 p
+// P3 (STAGE 1): s = r - alpha v (kept in r) ; s^ = M^-1 s ; partial s.s
+template <int BS, int STAGE>
+__device__ __noinline__ void bicg_precond_pass(const BicgVecs &v, int64_t n, double c1, double c2, double *out,
+                                               double (*sm)[WARPS]) {
+  const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
+  const int64_t nblk = (n + BS - 1) / BS;
+  double a0 = 0.0;
+  for (int64_t blk = tid; blk < nblk; blk += nth) {
+    double u[BS], y[BS];
+    int64_t pos[BS];
+#pragma unroll
+    for (int a = 0; a < BS; a++) {
+      const int64_t o = blk * BS + a;
+      pos[a] = (BS > 1 && v.iperm && o < n) ? v.iperm[o] : o;
+      const int64_t i = pos[a];
+      u[a] = 0.0;
+      if (o < n) {
+        if (STAGE == 0) {  // c1 = beta, c2 = omega
+          u[a] = __fma_rn(c1, __fma_rn(-c2, v.v[i], v.p[i]), v.r[i]);
+          v.p[i] = u[a];
+        } else {  // c1 = alpha
+          u[a] = __fma_rn(-c1, v.v[i], v.r[i]);
+          v.r[i] = u[a];
+          a0 = __fma_rn(u[a], u[a], a0);
+        }
+      }
+    }
+    bj_apply<BS>(v, n, blk, u, y);
+    double *dst = STAGE == 0 ? v.ph : v.sh;
+#pragma unroll
+    for (int a = 0; a < BS; a++)
+      if (blk * BS + a < n) dst[pos[a]] = y[a];
+  }
+  if (STAGE == 1) {
+    double red[1] = {a0};
+    block_sum<1>(red, sm);
+    if (threadIdx.x == 0) out[blockIdx.x] = red[0];
+  }
+}
+
+// P5: x += alpha p^ + omega s^ ; r = s - omega t ; partials r.r, r^.r
+__device__ __noinline__ void bicg_update_pass(const BicgVecs &v, int64_t n, double alpha, double omega, double *out,
+                                              double (*sm)[WARPS]) {
+  const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
+  double a0 = 0.0, a1 = 0.0;
+  for (int64_t i = tid; i < n; i += nth) {
+    v.x[i] = __fma_rn(omega, v.sh[i], __fma_rn(alpha, v.ph[i], v.x[i]));
+    const double ri = __fma_rn(-omega, v.t[i], v.r[i]);
+    v.r[i] = ri;
+    a0 = __fma_rn(ri, ri, a0);
+    a1 = __fma_rn(v.rh[i], ri, a1);
+  }
+  double red[2] = {a0, a1};
+  block_sum<2>(red, sm);
+  if (threadIdx.x == 0) {
+    out[blockIdx.x] = red[0];
+    out[gridDim.x + blockIdx.x] = red[1];
+  }
+}
+
 template <int FMT, int L, int BS>
-__global__ void __launch_bounds__(BLOCK, 2) bicg_kernel(SellView S, CsrView C, BicgVecs v, BicgState *st,
+__global__ void __launch_bounds__(BLOCK, 3) bicg_kernel(SellView S_, CsrView C_, BicgVecs v_, BicgState *st,
                                                         double *part, GridBar *bar) {
   __shared__ double sm[2][WARPS];
   __shared__ double s_tot[2];
+  __shared__ BicgShared q;
+  __shared__ SellView S;
+  __shared__ CsrView C;
+  __shared__ BicgVecs v;
+  if (threadIdx.x == 0) {
+    S = S_;
+    C = C_;
+    v = v_;
+  }
+  __syncthreads();
   const int64_t n = FMT == PCG_FORMAT_SELL ? S.n : C.n;
   const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
-  const int64_t nblk = (n + BS - 1) / BS;
-  const double tol = st->tol;
-  const long long max_iter = st->max_iter;
-  long long k = st->k, restarts = 0;
-  int done = BD_RUNNING;
-  double nb, relres_rec = 0.0, relres_true = 0.0;
-  double rho = 1.0, rho_old = 1.0, alpha = 1.0, omega = 1.0;
   double *pa = part, *pb = part + 2 * gridDim.x;  // two alternating partial regions
-  // y = M^-1 u on block blk: BS = 1 dinv * u; else P, L, U substitution (oracle bj_apply order)
-  auto bj = [&](int64_t blk, const double (&u)[BS], double (&y)[BS]) {
-    if (BS == 1) {
-      y[0] = __dmul_rn(v.dinv[blk], u[0]);
-    } else {
-      const double *D = v.lu + blk * BS * BS;
-      const int *pv = v.piv + blk * BS;
-      const int m = (int)((blk * BS + BS <= n) ? BS : n - blk * BS);
-#pragma unroll
-      for (int a = 0; a < BS; a++) {  // L z = P u
-        double sacc = 0.0;
-        const int pr = pv[a];
-#pragma unroll
-        for (int q = 0; q < BS; q++)
-          if (q == pr) sacc = u[q];
-#pragma unroll
-        for (int q = 0; q < a; q++) sacc = __dsub_rn(sacc, __dmul_rn(D[a * BS + q], y[q]));
-        y[a] = sacc;
-      }
-#pragma unroll
-      for (int a = BS - 1; a >= 0; a--) {  // U y = z
-        if (a >= m) continue;
-        double sacc = y[a];
-#pragma unroll
-        for (int q = a + 1; q < BS; q++)
-          if (q < m) sacc = __dsub_rn(sacc, __dmul_rn(D[a * BS + q], y[q]));
-        y[a] = __ddiv_rn(sacc, D[a * BS + a]);
-      }
-    }
-  };
   // ---- ||b||
   {
     double a0 = 0.0;
@@ -169,228 +285,133 @@ __global__ void __launch_bounds__(BLOCK, 2) bicg_kernel(SellView S, CsrView C, B
     grid_sync(bar);
     double t[1];
     all_blocks_sum<1>(pa, t, sm, s_tot);
-    nb = sqrt(t[0]);
+    if (threadIdx.x == 0) {
+      q.nb = sqrt(t[0]);
+      q.k = st->k;
+      q.restarts = 0;
+      q.relres_rec = q.relres_true = 0.0;
+      q.rho = q.rho_old = q.alpha = q.omega = 1.0;
+      q.done = q.nb == 0.0 ? BD_ZERO_RHS : (!(q.nb == q.nb) ? BD_NONFINITE : BD_RUNNING);
+      q.need_resid = 1;
+    }
+    __syncthreads();
   }
-  if (nb == 0.0 || !(nb == nb)) {
-    done = nb == 0.0 ? BD_ZERO_RHS : BD_NONFINITE;
+  if (q.done != BD_RUNNING)
     for (int64_t i = tid; i < n; i += nth) v.x[i] = 0.0;
-  }
-  bool need_resid = true;  // (re)start: r = b - A x, p = v = 0, rho = r^.r
-  while (done == BD_RUNNING) {
-    if (need_resid) {
-      double a0 = 0.0, a1 = 0.0;
-      auto gather = [&](int j) { return __ldg(v.x + j); };
-      auto epi = [&](int64_t i, double s) {
-        const double w = v.b[i] - s;
-        v.r[i] = w;
-        v.p[i] = 0.0;
-        v.v[i] = 0.0;
-        a0 = __fma_rn(w, w, a0);
-        a1 = __fma_rn(v.rh[i], w, a1);
-      };
-      if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
-      else csr_rows<L>(C, gather, epi);
-      double red[2] = {a0, a1};
-      block_sum<2>(red, sm);
-      if (threadIdx.x == 0) {
-        pb[blockIdx.x] = red[0];
-        pb[gridDim.x + blockIdx.x] = red[1];
-      }
+  const double tol = st->tol;
+  const long long max_iter = st->max_iter;
+  while (q.done == BD_RUNNING) {
+    if (q.need_resid) {  // (re)start / exit check
+      bicg_spmv_pass<FMT, L, SP_RESID>(S, C, v, pb, sm);
       grid_sync(bar);
       double t[2];
       all_blocks_sum<2>(pb, t, sm, s_tot);
-      const double rr = sqrt(t[0]);
-      relres_rec = rr / nb;
-      if (k > 0 || restarts > 0) relres_true = relres_rec;  // this pass was an exit check
-      if (rr <= tol * nb) {
-        relres_true = relres_rec;
-        done = BD_CONVERGED;
-        break;
-      }
-      if (k > 0) restarts++;
-      rho = t[1];
-      rho_old = alpha = omega = 1.0;
-      need_resid = false;
-    }
-    if (k >= max_iter) {
-      done = BD_MAXIT;
-      break;
-    }
-    if (rho == 0.0 || !(rho == rho)) {
-      done = rho == 0.0 ? BD_BREAKDOWN : BD_NONFINITE;
-      break;
-    }
-    const double beta = (rho / rho_old) * (alpha / omega);
-    // ---- P1: p = r + beta (p - omega v) ; p^ = M^-1 p
-    for (int64_t blk = tid; blk < nblk; blk += nth) {
-      double u[BS], y[BS];
-      int64_t pos[BS];
-#pragma unroll
-      for (int a = 0; a < BS; a++) {
-        const int64_t o = blk * BS + a;
-        pos[a] = (BS > 1 && v.iperm && o < n) ? v.iperm[o] : o;
-        const int64_t i = pos[a];
-        u[a] = 0.0;
-        if (o < n) {
-          u[a] = __fma_rn(beta, __fma_rn(-omega, v.v[i], v.p[i]), v.r[i]);
-          v.p[i] = u[a];
-        }
-      }
-      bj(blk, u, y);
-#pragma unroll
-      for (int a = 0; a < BS; a++)
-        if (blk * BS + a < n) v.ph[pos[a]] = y[a];
-    }
-    grid_sync(bar);
-    // ---- P2: v = A p^ ; sigma = r^.v
-    {
-      double a0 = 0.0;
-      auto gather = [&](int j) { return __ldg(v.ph + j); };
-      auto epi = [&](int64_t i, double s) {
-        v.v[i] = s;
-        a0 = __fma_rn(v.rh[i], s, a0);
-      };
-      if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
-      else csr_rows<L>(C, gather, epi);
-      double red[1] = {a0};
-      block_sum<1>(red, sm);
-      if (threadIdx.x == 0) pa[blockIdx.x] = red[0];
-    }
-    grid_sync(bar);
-    {
-      double t[1];
-      all_blocks_sum<1>(pa, t, sm, s_tot);
-      if (t[0] == 0.0 || !(t[0] == t[0])) {
-        done = t[0] == 0.0 ? BD_BREAKDOWN : BD_NONFINITE;
-        break;
-      }
-      alpha = rho / t[0];
-      k++;
-    }
-    // ---- P3: s = r - alpha v (kept in r) ; ||s|| ; s^ = M^-1 s
-    {
-      double a0 = 0.0;
-      for (int64_t blk = tid; blk < nblk; blk += nth) {
-        double u[BS], y[BS];
-        int64_t pos[BS];
-#pragma unroll
-        for (int a = 0; a < BS; a++) {
-          const int64_t o = blk * BS + a;
-          pos[a] = (BS > 1 && v.iperm && o < n) ? v.iperm[o] : o;
-          const int64_t i = pos[a];
-          u[a] = 0.0;
-          if (o < n) {
-            u[a] = __fma_rn(-alpha, v.v[i], v.r[i]);
-            v.r[i] = u[a];
-            a0 = __fma_rn(u[a], u[a], a0);
-          }
-        }
-        bj(blk, u, y);
-#pragma unroll
-        for (int a = 0; a < BS; a++)
-          if (blk * BS + a < n) v.sh[pos[a]] = y[a];
-      }
-      double red[1] = {a0};
-      block_sum<1>(red, sm);
-      if (threadIdx.x == 0) pb[blockIdx.x] = red[0];
-    }
-    grid_sync(bar);
-    {
-      double t[1];
-      all_blocks_sum<1>(pb, t, sm, s_tot);
-      const double ss = sqrt(t[0]);
-      if (ss <= tol * nb) {  // converged at the half step: x += alpha p^, then the exit check
-        relres_rec = ss / nb;
-        for (int64_t i = tid; i < n; i += nth) v.x[i] = __fma_rn(alpha, v.ph[i], v.x[i]);
-        grid_sync(bar);
-        need_resid = true;
-        continue;
-      }
-    }
-    // ---- P4: t = A s^ ; (t.s, t.t)
-    {
-      double a0 = 0.0, a1 = 0.0;
-      auto gather = [&](int j) { return __ldg(v.sh + j); };
-      auto epi = [&](int64_t i, double s) {
-        v.t[i] = s;
-        a0 = __fma_rn(s, v.r[i], a0);
-        a1 = __fma_rn(s, s, a1);
-      };
-      if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
-      else csr_rows<L>(C, gather, epi);
-      double red[2] = {a0, a1};
-      block_sum<2>(red, sm);
       if (threadIdx.x == 0) {
-        pa[blockIdx.x] = red[0];
-        pa[gridDim.x + blockIdx.x] = red[1];
+        const double rr = sqrt(t[0]);
+        q.relres_rec = rr / q.nb;
+        if (q.k > 0 || q.restarts > 0) q.relres_true = q.relres_rec;  // this pass was an exit check
+        if (rr <= tol * q.nb) {
+          q.relres_true = q.relres_rec;
+          q.done = BD_CONVERGED;
+        } else {
+          if (q.k > 0) q.restarts++;
+          q.rho = t[1];
+          q.rho_old = q.alpha = q.omega = 1.0;
+          q.need_resid = 0;
+        }
       }
+      __syncthreads();
+      if (q.done != BD_RUNNING) break;
     }
+    if (threadIdx.x == 0) {
+      if (q.k >= max_iter) q.done = BD_MAXIT;
+      else if (q.rho == 0.0 || !(q.rho == q.rho)) q.done = q.rho == 0.0 ? BD_BREAKDOWN : BD_NONFINITE;
+      else q.beta = (q.rho / q.rho_old) * (q.alpha / q.omega);
+    }
+    __syncthreads();
+    if (q.done != BD_RUNNING) break;
+    bicg_precond_pass<BS, 0>(v, n, q.beta, q.omega, nullptr, sm);  // P1
+    grid_sync(bar);
+    bicg_spmv_pass<FMT, L, SP_AV>(S, C, v, pa, sm);  // P2
     grid_sync(bar);
     {
       double t[2];
       all_blocks_sum<2>(pa, t, sm, s_tot);
-      omega = t[1] > 0.0 ? t[0] / t[1] : 0.0;
-    }
-    // ---- P5: x += alpha p^ + omega s^ ; r = s - omega t ; (r.r, r^.r)
-    {
-      double a0 = 0.0, a1 = 0.0;
-      for (int64_t i = tid; i < n; i += nth) {
-        v.x[i] = __fma_rn(omega, v.sh[i], __fma_rn(alpha, v.ph[i], v.x[i]));
-        const double ri = __fma_rn(-omega, v.t[i], v.r[i]);
-        v.r[i] = ri;
-        a0 = __fma_rn(ri, ri, a0);
-        a1 = __fma_rn(v.rh[i], ri, a1);
-      }
-      double red[2] = {a0, a1};
-      block_sum<2>(red, sm);
       if (threadIdx.x == 0) {
-        pb[blockIdx.x] = red[0];
-        pb[gridDim.x + blockIdx.x] = red[1];
+        if (t[0] == 0.0 || !(t[0] == t[0])) {
+          q.done = t[0] == 0.0 ? BD_BREAKDOWN : BD_NONFINITE;
+        } else {
+          q.alpha = q.rho / t[0];
+          q.k++;
+        }
+      }
+      __syncthreads();
+      if (q.done != BD_RUNNING) break;
+    }
+    bicg_precond_pass<BS, 1>(v, n, q.alpha, 0.0, pb, sm);  // P3
+    grid_sync(bar);
+    {
+      double t[1];
+      all_blocks_sum<1>(pb, t, sm, s_tot);
+      if (threadIdx.x == 0) {
+        const double ss = sqrt(t[0]);
+        q.half = ss <= tol * q.nb;
+        if (q.half) q.relres_rec = ss / q.nb;
+      }
+      __syncthreads();
+      if (q.half) {  // converged at the half step: x += alpha p^, then the exit check
+        const double alpha = q.alpha;
+        for (int64_t i = tid; i < n; i += nth) v.x[i] = __fma_rn(alpha, v.ph[i], v.x[i]);
+        grid_sync(bar);
+        if (threadIdx.x == 0) q.need_resid = 1;
+        __syncthreads();
+        continue;
       }
     }
+    bicg_spmv_pass<FMT, L, SP_AT>(S, C, v, pa, sm);  // P4
+    grid_sync(bar);
+    {
+      double t[2];
+      all_blocks_sum<2>(pa, t, sm, s_tot);
+      if (threadIdx.x == 0) q.omega = t[1] > 0.0 ? t[0] / t[1] : 0.0;
+      __syncthreads();
+    }
+    bicg_update_pass(v, n, q.alpha, q.omega, pb, sm);  // P5
     grid_sync(bar);
     {
       double t[2];
       all_blocks_sum<2>(pb, t, sm, s_tot);
-      const double rr = sqrt(t[0]);
-      relres_rec = rr / nb;
-      if (rr <= tol * nb) {
-        need_resid = true;  // exit check (and restart if it fails)
-        continue;
+      if (threadIdx.x == 0) {
+        const double rr = sqrt(t[0]);
+        q.relres_rec = rr / q.nb;
+        if (rr <= tol * q.nb) {
+          q.need_resid = 1;  // exit check (and restart if it fails)
+        } else if (q.omega == 0.0) {
+          q.done = BD_BREAKDOWN;
+        } else {
+          q.rho_old = q.rho;
+          q.rho = t[1];
+        }
       }
-      if (omega == 0.0) {
-        done = BD_BREAKDOWN;
-        break;
-      }
-      rho_old = rho;
-      rho = t[1];
+      __syncthreads();
     }
   }
-  if (done == BD_MAXIT || done == BD_BREAKDOWN || done == BD_NONFINITE) {  // final true residual
+  if (q.done == BD_MAXIT || q.done == BD_BREAKDOWN || q.done == BD_NONFINITE) {  // final true residual
     grid_sync(bar);
-    double a0 = 0.0;
-    auto gather = [&](int j) { return __ldg(v.x + j); };
-    auto epi = [&](int64_t i, double s) {
-      const double w = v.b[i] - s;
-      a0 = __fma_rn(w, w, a0);
-    };
-    if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
-    else csr_rows<L>(C, gather, epi);
-    double red[1] = {a0};
-    block_sum<1>(red, sm);
-    if (threadIdx.x == 0) pa[blockIdx.x] = red[0];
+    bicg_spmv_pass<FMT, L, SP_FINAL>(S, C, v, pa, sm);
     grid_sync(bar);
     double t[1];
     all_blocks_sum<1>(pa, t, sm, s_tot);
-    relres_true = sqrt(t[0]) / nb;
+    if (threadIdx.x == 0) q.relres_true = sqrt(t[0]) / q.nb;
+    __syncthreads();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    st->nb = nb;
-    st->relres_rec = relres_rec;
-    st->relres_true = relres_true;
-    st->k = k;
-    st->restarts = restarts;
-    st->done = done;
+    st->nb = q.nb;
+    st->relres_rec = q.relres_rec;
+    st->relres_true = q.relres_true;
+    st->k = q.k;
+    st->restarts = q.restarts;
+    st->done = q.done;
   }
 }
 
