@@ -325,6 +325,8 @@ def build_problem(name: str, c: int | None = None, k: int | None = None) -> dict
     g = np.zeros(mesh.n_nodes)
     if cfg["g"] == "X2MY2":
         g = X[:, 0] * X[:, 0] - X[:, 1] * X[:, 1]
+    elif cfg["g"] == "LINEAR3D":  # reading R3: harmonic and reproduced exactly by P1 (patch test)
+        g = ((1.0 + 2.0 * X[:, 0]) - 3.0 * X[:, 1]) + 0.5 * X[:, 2]
     loads = []
     if cfg["f"] == "BUMP3D":
         for cs in bump_centres(cfg["seed"], cfg["k"]):

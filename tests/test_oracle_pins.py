@@ -590,3 +590,72 @@ def test_bicgstab_status_codes():
     I = O.Csr(5, list(range(6)), list(range(5)), [2.0] * 5)
     r = O.bicgstab(I, np.arange(1.0, 6.0), tol=1e-14)
     assert r.status == O.OK and r.iterations == 1 and np.allclose(r.x, np.arange(1.0, 6.0) / 2)
+
+
+# ---------------------------------------------------------------- N4: C6 jittered Kuhn tets (reading R3)
+def test_kuhn_tet_volume_bound_at_015h():
+    """Multilinear corner bound: with every vertex of a Kuhn tet moved by at most 0.15h per
+    coordinate, the signed volume keeps its sign and stays >= 0.1 of the lattice volume
+    (so the C6 mesh needs no repair); at 0.2h a fixed-vertex tet already degenerates."""
+    import itertools
+
+    def kuhn(p):
+        v = [np.zeros(3)]
+        for k in range(3):
+            w = v[-1].copy()
+            w[p[k]] += 1
+            v.append(w)
+        return v
+
+    def vol(V):
+        return np.linalg.det(np.array([V[1] - V[0], V[2] - V[0], V[3] - V[0]])) / 6
+
+    corners = list(itertools.product([-1, 1], repeat=3))
+    for d, lo in ((0.15, 0.1 / 6 - 1e-12), (0.2, None)):
+        worst = 1e9
+        for p in itertools.permutations(range(3)):
+            V = kuhn(p)
+            s0 = np.sign(vol(V))
+            for cs in itertools.product(corners, repeat=4):
+                worst = min(worst, s0 * vol([v + d * np.array(c) for v, c in zip(V, cs)]))
+        if lo is not None:
+            assert worst >= lo
+        else:
+            assert worst < 0
+
+
+def test_c6_mesh_jitter_is_bounded_and_deterministic():
+    c = 8
+    m1 = O.Mesh(O.P1_TET, c, True, O.configs()["C6"]["seed"])
+    m2 = O.Mesh(O.P1_TET, c, True, O.configs()["C6"]["seed"])
+    assert np.array_equal(m1.coord, m2.coord)
+    h = 1.0 / c
+    np_ = c + 1
+    idx = np.arange(m1.n_nodes)
+    lat = np.stack([idx % np_, (idx // np_) % np_, idx // (np_ * np_)], 1) * h
+    d = m1.coord - lat
+    assert np.all(d[m1.boundary] == 0)
+    assert np.max(np.abs(d)) <= 0.15 * h and np.max(np.abs(d)) > 0.1 * h
+
+
+def test_c6_patch_test_reproduces_the_linear_field():
+    """P1 reproduces linear fields exactly: with g = 1 + 2x - 3y + z/2 and f = 0 the discrete
+    solution on the jittered mesh equals g at every free node."""
+    P = O.build_problem("C6", c=10)
+    r = O.pcg(P["A"], P["B"][:, 0], tol=1e-13)
+    X = P["mesh"].coord[P["free_nodes"]]
+    ex = ((1.0 + 2.0 * X[:, 0]) - 3.0 * X[:, 1]) + 0.5 * X[:, 2]
+    assert r.status == O.OK and np.max(np.abs(r.x - ex)) <= 1e-11
+
+
+def test_c6_neumann_stiffness_symmetric_zero_rowsums_and_dense_solve():
+    m = O.Mesh(O.P1_TET, 5, True, O.configs()["C6"]["seed"])
+    K, F = O.assemble(m, O.F_ZERO)
+    D = K.to_dense()
+    assert np.max(np.abs(D - D.T)) <= 1e-15 * np.abs(D).max()
+    assert np.max(np.abs(D.sum(1))) <= 1e-14 * np.abs(D).max()
+    P = O.build_problem("C6", c=5)
+    A, b = P["A"], P["B"][:, 0]
+    xe = np.linalg.solve(A.to_dense(), b)
+    r = O.pcg(A, b, tol=1e-14)
+    assert np.linalg.norm(r.x - xe) / np.linalg.norm(xe) <= 1e-12
