@@ -142,6 +142,8 @@ def run_reference(args):
     import oracle as O
     P = O.build_problem(args.config, c=args.sample_c)
     A, b = P["A"], P["B"][:, 0]
+    if nnz < 0:  # 3D element pattern: no closed form; the sample's nnz per row
+        nnz = int(round(A.nnz / A.n * n))
     times, its = [], 0
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -171,7 +173,9 @@ def workload_config(name, c, n, nnz, gpus):
                   f"boundary, Jacobi-PCG x0=0 to rel-res 1e-10",
             "C4": f"C4: 3D P1 Kuhn {c}^3 cells, 16 Gaussian-bump RHS", "C3": f"C3: 2D P2 {c}^2 cells, f=1",
             "C2": f"C2: 2D jittered P1 {c}^2 cells, harmonic x^2-y^2 boundary data",
-            "C1": f"C1: 2D P1 {c}^2 cells, sin RHS"}[name]
+            "C1": f"C1: 2D P1 {c}^2 cells, sin RHS",
+            "C6": f"C6: 3D P1 Kuhn tets on a {c}^3-cell cube, interior nodes jittered by +-0.15h (irregular "
+                  f"stand-in for the paper's Sphere meshes), f = 0, linear Dirichlet data"}[name]
     return {"workload": desc, "config": name, "n": n, "nnz": nnz, "global_batch": 1, "tol": 1e-10,
             "parallelism": f"row-partition over {gpus} GPU(s): halo of z + 2 scalar allreduces per iteration"
             if gpus > 1 else "1 GPU",
@@ -233,14 +237,18 @@ def main():
     comm = None
     if world == 1:
         P = fem_build(spec)
+        nnz = P["col"].numel()  # (the 3D element pattern has no closed form: problem_size gives -1)
         A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"], fmt=args.fmt)
         r0, r1 = 0, n
     else:
         rp_full = fem_build_rowptr(spec, n)
+        rp_full_nnz = rp_full[-1]
         bounds = pcg.partition_rows(rp_full, world)
         del rp_full
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
         P = fem_build(spec, r0, r1)
+        if nnz < 0:
+            nnz = int(rp_full_nnz)
         comm = pcg.Comm.host_callbacks() if cb else pcg.Comm.from_process_group()
         A = pcg.Matrix.from_csr_dist(comm, n, r0, r1, P["row_ptr"], P["col"], P["val"], fmt=args.fmt)
     kcols = P["B"].shape[1]

@@ -25,6 +25,7 @@ a = ap.parse_args()
 spec = fem_spec(a.config, c=a.c)
 n, nnz, _ = problem_size(spec)
 P = fem_build(spec)
+nnz = P["col"].numel()  # the 3D element pattern has no closed form (problem_size: -1)
 A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"], fmt=a.fmt)
 b = P["B"][:, 0].contiguous()
 del P
