@@ -43,7 +43,8 @@ extern "C" {
 #define FEM_F_BUMP3D 4 /* column s: exp(-|x-c_s|²/(2σ²)), c_s,axis = U(seed, 3s+axis) */
 
 #define FEM_G_ZERO 0
-#define FEM_G_X2MY2 1 /* g = x² - y² on the boundary */
+#define FEM_G_X2MY2 1    /* g = x² - y² on the boundary                                   */
+#define FEM_G_LINEAR3D 2 /* g = 1 + 2x - 3y + z/2 (3D; P1 reproduces it exactly: reading R3) */
 
 #define FEM_PAT_ELEMENT 0
 #define FEM_PAT_AXIS 1

@@ -65,6 +65,21 @@ __device__ __forceinline__ void jittered(const Geo &g, int a, int b, double &x, 
   y = __dadd_rn(y, dy);
 }
 
+// 3D (reading R3): interior nodes move by (2u-1)(0.15h)
+// per coordinate, u = SplitMix64(seed, 3*node+axis); for this amplitude every Kuhn
+// tet keeps its orientation (volume >= 0.1 of the lattice tet's), so no repair.
+__device__ __forceinline__ void node_xyz(const Geo &g, int i, int j, int l, double (&X)[3]) {
+  X[0] = (double)i * g.h;
+  X[1] = (double)j * g.h;
+  X[2] = (double)l * g.h;
+  if (!g.jitter || i == 0 || j == 0 || l == 0 || i == g.c || j == g.c || l == g.c) return;
+  const uint64_t id = (uint64_t)i + (uint64_t)g.np * ((uint64_t)j + (uint64_t)g.np * (uint64_t)l);
+  const double amp = __dmul_rn(0.15, g.h);
+#pragma unroll
+  for (int ax = 0; ax < 3; ax++)
+    X[ax] = __dadd_rn(X[ax], __dmul_rn(__dsub_rn(__dmul_rn(2.0, u01(g.seed, 3 * id + ax)), 1.0), amp));
+}
+
 __device__ __forceinline__ double area2_rn(double x0, double y0, double x1, double y1, double x2, double y2) {
   return __dsub_rn(__dmul_rn(__dsub_rn(x1, x0), __dsub_rn(y2, y0)), __dmul_rn(__dsub_rn(x2, x0), __dsub_rn(y1, y0)));
 }
@@ -251,8 +266,7 @@ __device__ void row_p1tet(const fem_spec &s, const Geo &g, int i, int j, int l, 
           for (int k = 0; k < 4; k++) acc.touched[(v[k][2] - l + 1) * 9 + (v[k][1] - j + 1) * 3 + (v[k][0] - i + 1)] = true;
           if (!values) continue;
           double X[4][3];
-          for (int k = 0; k < 4; k++)
-            for (int d = 0; d < 3; d++) X[k][d] = v[k][d] * g.h;
+          for (int k = 0; k < 4; k++) node_xyz(g, v[k][0], v[k][1], v[k][2], X[k]);
           double e[3][3];
           for (int k = 0; k < 3; k++)
             for (int d = 0; d < 3; d++) e[k][d] = X[k + 1][d] - X[0][d];
@@ -291,8 +305,11 @@ __device__ void row_p1tet(const fem_spec &s, const Geo &g, int i, int j, int l, 
       }
 }
 
-__device__ __forceinline__ double g_eval(const fem_spec &s, double x, double y) {
-  return s.gkind == FEM_G_X2MY2 ? x * x - y * y : 0.0;
+__device__ __forceinline__ double g_eval(const fem_spec &s, double x, double y, double z = 0.0) {
+  if (s.gkind == FEM_G_X2MY2) return x * x - y * y;
+  if (s.gkind == FEM_G_LINEAR3D) return __dadd_rn(__dsub_rn(__dadd_rn(1.0, __dmul_rn(2.0, x)), __dmul_rn(3.0, y)),
+                                                  __dmul_rn(0.5, z));
+  return 0.0;
 }
 
 // Assemble row r (global free index) into acc, then visit slots in ascending
@@ -343,7 +360,14 @@ __device__ int build_row(const fem_spec &s, const Geo &g, int64_t r, bool values
           const int t = (dl + 1) * 9 + (dj + 1) * 3 + (di + 1);
           if (!acc.touched[t]) continue;
           const int ni = i + di, nj = j + dj, nl = l + dl;
-          if (ni == 0 || nj == 0 || nl == 0 || ni == g.c || nj == g.c || nl == g.c) continue;  // g = 0 in 3D
+          if (ni == 0 || nj == 0 || nl == 0 || ni == g.c || nj == g.c || nl == g.c) {  // Dirichlet lift
+            if (values && s.gkind != FEM_G_ZERO) {
+              double Xb[3];
+              node_xyz(g, ni, nj, nl, Xb);
+              acc.b[0] -= acc.val[t] * g_eval(s, Xb[0], Xb[1], Xb[2]);
+            }
+            continue;
+          }
           if (s.policy == FEM_PAT_AXIS && abs(di) + abs(dj) + abs(dl) > 1) {
             if (values && acc.val[t] != 0.0) atomicOr(bad, 1);
             continue;
@@ -392,8 +416,12 @@ pcg_status check_spec(const fem_spec *s) {
   if (!s) return fail(PCG_ERR_INVALID_ARG, "fem: null spec");
   if (s->family < FEM_P1_TRI || s->family > FEM_P2_TRI) return fail(PCG_ERR_INVALID_ARG, "fem: bad family");
   if (s->c < 2) return fail(PCG_ERR_INVALID_ARG, "fem: c must be >= 2");
-  if (s->jitter && s->family != FEM_P1_TRI) return fail(PCG_ERR_INVALID_ARG, "fem: jitter needs P1_TRI");
-  if (s->family == FEM_P1_TET && s->gkind != FEM_G_ZERO) return fail(PCG_ERR_INVALID_ARG, "fem: 3D supports g = 0");
+  if (s->jitter && s->family == FEM_P2_TRI) return fail(PCG_ERR_INVALID_ARG, "fem: jitter needs P1 elements");
+  if (s->family == FEM_P1_TET && s->gkind != FEM_G_ZERO && s->gkind != FEM_G_LINEAR3D)
+    return fail(PCG_ERR_INVALID_ARG, "fem: 3D supports g = 0 or LINEAR3D");
+  if (s->family != FEM_P1_TET && s->gkind == FEM_G_LINEAR3D) return fail(PCG_ERR_INVALID_ARG, "fem: LINEAR3D is 3D");
+  if (s->family == FEM_P1_TET && s->jitter && s->policy == FEM_PAT_AXIS)
+    return fail(PCG_ERR_INVALID_ARG, "fem: jittered tets need the ELEMENT pattern");
   if (s->fkind == FEM_F_BUMP3D && (s->k < 1 || s->k > MAXK || s->family != FEM_P1_TET))
     return fail(PCG_ERR_INVALID_ARG, "fem: BUMP3D needs P1_TET and 1 <= k <= 32");
   if (s->policy == FEM_PAT_AXIS && (s->family == FEM_P2_TRI))

@@ -17,7 +17,7 @@ CONFIGS = os.path.join(ROOT, "configs", "configs.json")
 
 _FAM = {"P1_TRI": 1, "P1_TET": 2, "P2_TRI": 3}
 _F = {"ZERO": 0, "ONE": 1, "SIN2D": 2, "SIN3D": 3, "BUMP3D": 4}
-_G = {"ZERO": 0, "X2MY2": 1}
+_G = {"ZERO": 0, "X2MY2": 1, "LINEAR3D": 2}
 _POL = {"ELEMENT": 0, "AXIS": 1}
 
 
