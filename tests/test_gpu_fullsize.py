@@ -39,7 +39,7 @@ def pcg():
     return p
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C4", "C3"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C4", "C3", "C6"])
 def test_fullsize_vs_oracle_golden(pcg, name):
     g = _gold()
     if name not in g:
