@@ -9,7 +9,10 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpcg_b200.so")
+# PCG_LIB_VARIANT=<name> loads _variants/libpcg_<name>.so (scripts/build_variant.py: A/B builds
+# of the same sources with -D knobs; development only, never the default)
+LIB_PATH = (os.path.join(HERE, "_variants", f"libpcg_{os.environ['PCG_LIB_VARIANT']}.so")
+            if os.environ.get("PCG_LIB_VARIANT") else os.path.join(HERE, "libpcg_b200.so"))
 
 STATUS = ["PCG_OK", "PCG_NOT_CONVERGED", "PCG_ERR_INVALID_ARG", "PCG_ERR_INDEX_OUT_OF_RANGE",
           "PCG_ERR_UNSORTED_OR_DUPLICATE", "PCG_ERR_DIMENSION_MISMATCH", "PCG_ERR_ZERO_DIAGONAL",

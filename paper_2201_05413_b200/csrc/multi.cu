@@ -250,7 +250,12 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
   if (acc_smem)
     for (int t = threadIdx.x; t < k * BLOCK; t += BLOCK) s_acc[t] = 0.0;
   __syncthreads();
+  unsigned int act = 0;  // active columns as a register mask (s_act costs a shared load per use)
+  for (int c = 0; c < k; c++) act |= (unsigned int)s_act[c] << c;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // grid-stride slice map: at any time the whole grid works on one window of rows, so
+  // gathered lines shared with other SMs (the far stencil neighbours) meet in L2.  (A
+  // contiguous chunk per block, for L1 reuse, measured 316 vs 229 us on C4.)
   const int64_t w0 = (int64_t)blockIdx.x * WARPS + wid, nw = (int64_t)gridDim.x * WARPS;
   const double *__restrict__ G = MODE == MS_SPMM ? v.P : v.X;  // gathered block vector
   for (int64_t s = w0; s < S.n_slices; s += nw) {
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
         const size_t e = (size_t)c * v.ld + row;
         if (MODE == MS_SPMM) {
           __stcs(v.Q + e, sum);
-          r[0] = __ldg(v.P + e) * sum;
+          r[0] = __ldg(v.P + e) * sum;  // (reusing the diagonal's gather measured slower)
         } else {
           const double bi = v.Bm[e];
           const double w = bi - sum;
@@ -303,13 +308,14 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
       }
       cols_ready(j, S.zero);
       if (pf) {  // first touch of a gathered line is (mostly) its largest column: start every
-                 // column's fetch now so only the first gather round waits on HBM
-        int jl = j[0];  // j[len - 1] without dynamic register indexing
+                 // column's fetch now so only the first gather round waits on HBM (padding
+                 // entries are column 0; a select of j[len - 1] went to local memory)
+        int jl = j[0];
 #pragma unroll
-        for (int u = 1; u < 8; u++) jl = u == len - 1 ? j[u] : jl;
+        for (int u = 1; u < 8; u++) jl = max(jl, j[u]);
 #pragma unroll 1
         for (int c = 0; c < k; c++)
-          if (s_act[c]) prefetch_l2(G + (size_t)c * v.ld + jl);
+          if (act >> c & 1) prefetch_l2(G + (size_t)c * v.ld + jl);
       }
       unsigned int off[8];  // byte offsets of the gathered entries (columns < 2^29)
 #pragma unroll
@@ -318,7 +324,7 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
       const char *Gb = reinterpret_cast<const char *>(G);
 #pragma unroll 1
       for (int c = 0; c < k; c++, Gb += ld * 8) {
-        if (!s_act[c]) continue;
+        if (!(act >> c & 1)) continue;
         double g[8];
 #pragma unroll
         for (int u = 0; u < 8; u++) g[u] = u < len ? __ldg(reinterpret_cast<const double *>(Gb + off[u])) : 0.0;
@@ -332,7 +338,7 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
     } else {
 #pragma unroll 1
       for (int c = 0; c < k; c++) {
-        if (!s_act[c]) continue;
+        if (!(act >> c & 1)) continue;
         finish_col(c, long_row_sum(vp, cp, len, G + (size_t)c * v.ld, S.zero));
       }
     }
