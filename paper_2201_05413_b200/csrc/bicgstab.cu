@@ -12,11 +12,13 @@
 //   stop -> true residual ||b - A x||/||b|| (Eq. relativeError) decides; else
 //   restart from x (same r^), iterations keep counting.
 //
-// The whole solve (init, iterations, exit check, restarts) is ONE cooperative
-// kernel: the five passes of an iteration are separated by grid barriers, and
-// every block evaluates the scalars (rho, alpha, omega, beta, stop tests)
-// identically from fixed-order block partials (coop.cuh).  Per iteration: two
-// SpMVs (sell_rows / csr_rows of rows.cuh) and three streaming passes;
+// Two device schedules of the same five passes per iteration — two SpMVs
+// (sell_rows / csr_rows of rows.cuh) and three streaming passes:
+//  * graph (default): five kernels per iteration in a CUDA-graph conditional WHILE
+//    loop; last-block finishers evaluate the scalars on the device;
+//  * persist (PCG_BICG=persist): the whole solve (init, iterations, exit check,
+//    restarts) as ONE cooperative kernel, passes separated by grid barriers, every
+//    block evaluating the scalars identically from fixed-order block partials.
 // Block-Jacobi applies the LU factors (partial pivoting) of each bs x bs diagonal
 // block, computed at setup, one thread per block — bitwise the oracle's M^-1.
 #include <cstring>
@@ -126,23 +128,24 @@ struct BicgShared {
 
 enum { SP_RESID = 0, SP_AV = 1, SP_AT = 2, SP_FINAL = 3 };
 
-// the SpMV passes: RESID w = b - A x (r = w, p = v = 0; partials w.w, r^.w),
+// the SpMV passes: RESID w = b - A x (r = w, p = v = 0; sums w.w, r^.w, b.b),
 // AV v = A p^ (r^.v), AT t = A s^ (t.s, t.t), FINAL w = b - A x (w.w)
 template <int FMT, int L, int MODE>
-__device__ __noinline__ void bicg_spmv_pass(const SellView &S, const CsrView &C, const BicgVecs &v, double *out,
-                                            double (*sm)[WARPS]) {
-  double a0 = 0.0, a1 = 0.0;
+__device__ __forceinline__ void spmv_body(const SellView &S, const CsrView &C, const BicgVecs &v, double &a0,
+                                          double &a1, double &a2) {
   const double *__restrict__ G = MODE == SP_AV ? v.ph : (MODE == SP_AT ? v.sh : v.x);
   auto gather = [&](int j) { return __ldg(G + j); };
   auto epi = [&](int64_t i, double sv) {
     if (MODE == SP_RESID || MODE == SP_FINAL) {
-      const double w = v.b[i] - sv;
+      const double bi = v.b[i];
+      const double w = bi - sv;
       a0 = __fma_rn(w, w, a0);
       if (MODE == SP_RESID) {
         v.r[i] = w;
         v.p[i] = 0.0;
         v.v[i] = 0.0;
         a1 = __fma_rn(v.rh[i], w, a1);
+        a2 = __fma_rn(bi, bi, a2);
       }
     } else if (MODE == SP_AV) {
       v.v[i] = sv;
@@ -155,6 +158,13 @@ __device__ __noinline__ void bicg_spmv_pass(const SellView &S, const CsrView &C,
   };
   if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
   else csr_rows<L>(C, gather, epi);
+}
+
+template <int FMT, int L, int MODE>
+__device__ __noinline__ void bicg_spmv_pass(const SellView &S, const CsrView &C, const BicgVecs &v, double *out,
+                                            double (*sm)[WARPS]) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  spmv_body<FMT, L, MODE>(S, C, v, a0, a1, a2);
   double red[2] = {a0, a1};
   block_sum<2>(red, sm);
   if (threadIdx.x == 0) {
@@ -199,11 +209,9 @@ __device__ __forceinline__ void bj_apply(const BicgVecs &v, int64_t n, int64_t b
 // P1 (STAGE 0): p = r + beta (p - omega v) ; p^ = M^-1 p
 // P3 (STAGE 1): s = r - alpha v (kept in r) ; s^ = M^-1 s ; partial s.s
 template <int BS, int STAGE>
-__device__ __noinline__ void bicg_precond_pass(const BicgVecs &v, int64_t n, double c1, double c2, double *out,
-                                               double (*sm)[WARPS]) {
+__device__ __forceinline__ void precond_body(const BicgVecs &v, int64_t n, double c1, double c2, double &a0) {
   const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
   const int64_t nblk = (n + BS - 1) / BS;
-  double a0 = 0.0;
   for (int64_t blk = tid; blk < nblk; blk += nth) {
     double u[BS], y[BS];
     int64_t pos[BS];
@@ -230,6 +238,13 @@ __device__ __noinline__ void bicg_precond_pass(const BicgVecs &v, int64_t n, dou
     for (int a = 0; a < BS; a++)
       if (blk * BS + a < n) dst[pos[a]] = y[a];
   }
+}
+
+template <int BS, int STAGE>
+__device__ __noinline__ void bicg_precond_pass(const BicgVecs &v, int64_t n, double c1, double c2, double *out,
+                                               double (*sm)[WARPS]) {
+  double a0 = 0.0;
+  precond_body<BS, STAGE>(v, n, c1, c2, a0);
   if (STAGE == 1) {
     double red[1] = {a0};
     block_sum<1>(red, sm);
@@ -238,10 +253,9 @@ __device__ __noinline__ void bicg_precond_pass(const BicgVecs &v, int64_t n, dou
 }
 
 // P5: x += alpha p^ + omega s^ ; r = s - omega t ; partials r.r, r^.r
-__device__ __noinline__ void bicg_update_pass(const BicgVecs &v, int64_t n, double alpha, double omega, double *out,
-                                              double (*sm)[WARPS]) {
+__device__ __forceinline__ void update_body(const BicgVecs &v, int64_t n, double alpha, double omega, double &a0,
+                                            double &a1) {
   const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
-  double a0 = 0.0, a1 = 0.0;
   for (int64_t i = tid; i < n; i += nth) {
     v.x[i] = __fma_rn(omega, v.sh[i], __fma_rn(alpha, v.ph[i], v.x[i]));
     const double ri = __fma_rn(-omega, v.t[i], v.r[i]);
@@ -249,6 +263,12 @@ __device__ __noinline__ void bicg_update_pass(const BicgVecs &v, int64_t n, doub
     a0 = __fma_rn(ri, ri, a0);
     a1 = __fma_rn(v.rh[i], ri, a1);
   }
+}
+
+__device__ __noinline__ void bicg_update_pass(const BicgVecs &v, int64_t n, double alpha, double omega, double *out,
+                                              double (*sm)[WARPS]) {
+  double a0 = 0.0, a1 = 0.0;
+  update_body(v, n, alpha, omega, a0, a1);
   double red[2] = {a0, a1};
   block_sum<2>(red, sm);
   if (threadIdx.x == 0) {
@@ -415,6 +435,178 @@ __global__ void __launch_bounds__(BLOCK, 3) bicg_kernel(SellView S_, CsrView C_,
   }
 }
 
+// ---------------------------------------------------------------- graph schedule
+// The same iteration as five kernels per iteration inside a CUDA-graph conditional
+// WHILE loop (body = two iterations), for systems whose passes are long enough
+// that kernel boundaries cost less than one kernel holding every pass (register
+// pressure, spills).  Scalars live in BgScalars on the device; each reducing
+// kernel's last block (publish_and_arrive: fixed-order partials) evaluates the
+// recurrence exactly as the persistent kernel's thread 0 does.  Any finisher that
+// ends the loop sets `stop` (and the graph condition); later kernels of the body
+// see `stop` and return.  The exit check / restart (resid pass) runs between
+// graph launches, host-driven, as in the CG solver.
+struct BgScalars {
+  double tol, nb, rho, rho_old, alpha, omega, beta, relres_rec, relres_true;
+  long long k, max_iter, restarts;
+  int done, half, need_resid, stop;
+  unsigned int cnt[4];
+};
+
+enum { BR_INIT = 0, BR_CHECK = 1, BR_FINAL = 2 };
+
+__device__ __forceinline__ void bg_stop(BgScalars *sc, int use_cond, cudaGraphConditionalHandle h) {
+  sc->stop = 1;
+  if (use_cond) cudaGraphSetConditional(h, 0);
+}
+
+// loop-top tests of the persistent kernel (max_iter, rho breakdown) and beta
+__device__ __forceinline__ void bg_loop_top(BgScalars *sc, int use_cond, cudaGraphConditionalHandle h) {
+  if (sc->k >= sc->max_iter) {
+    sc->done = BD_MAXIT;
+    bg_stop(sc, use_cond, h);
+  } else if (sc->rho == 0.0 || !(sc->rho == sc->rho)) {
+    sc->done = sc->rho == 0.0 ? BD_BREAKDOWN : BD_NONFINITE;
+    bg_stop(sc, use_cond, h);
+  } else {
+    sc->beta = (sc->rho / sc->rho_old) * (sc->alpha / sc->omega);
+  }
+}
+
+#define BG_ENTRY()                                                        \
+  const volatile BgScalars *vs = sc;                                      \
+  if (vs->stop) {                                                         \
+    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0); \
+    return;                                                               \
+  }
+
+// SpMV kernels: RESID (rmode BR_INIT / BR_CHECK), AV, AT, FINAL (rmode BR_FINAL)
+template <int FMT, int L, int MODE>
+__global__ void __launch_bounds__(BLOCK) bg_spmv_kernel(SellView S, CsrView C, BicgVecs v, BgScalars *sc,
+                                                        double *part, int rmode, int use_cond,
+                                                        cudaGraphConditionalHandle h) {
+  __shared__ double sm[3][WARPS];
+  if (MODE == SP_AV || MODE == SP_AT) {
+    BG_ENTRY();
+    if (MODE == SP_AT && vs->half) return;  // converged at the half step: no t this iteration
+  }
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  spmv_body<FMT, L, MODE>(S, C, v, a0, a1, a2);
+  double red[3] = {a0, a1, a2};
+  block_sum<3>(red, sm);
+  if (!publish_and_arrive<3>(red, part, &sc->cnt[0])) return;
+  double t[3];
+  reduce_partials<3>(part, t, sm);
+  if (threadIdx.x != 0) return;
+  sc->cnt[0] = 0;
+  if (MODE == SP_RESID) {
+    if (rmode == BR_INIT) {
+      sc->nb = sqrt(t[2]);
+      sc->k = 0;
+      sc->restarts = 0;
+      sc->relres_rec = sc->relres_true = 0.0;
+      sc->stop = sc->half = sc->need_resid = 0;
+      if (sc->nb == 0.0 || !(sc->nb == sc->nb)) {
+        sc->done = sc->nb == 0.0 ? BD_ZERO_RHS : BD_NONFINITE;
+        return;
+      }
+      sc->done = BD_RUNNING;
+    }
+    const double rr = sqrt(t[0]);
+    sc->relres_rec = rr / sc->nb;
+    if (rmode == BR_CHECK) sc->relres_true = sc->relres_rec;
+    if (rr <= sc->tol * sc->nb) {
+      sc->relres_true = sc->relres_rec;
+      sc->done = BD_CONVERGED;
+    } else {
+      if (rmode == BR_CHECK) sc->restarts++;
+      sc->rho = t[1];
+      sc->rho_old = sc->alpha = sc->omega = 1.0;
+      sc->stop = sc->half = sc->need_resid = 0;
+      bg_loop_top(sc, 0, h);
+    }
+  } else if (MODE == SP_FINAL) {
+    sc->relres_true = sqrt(t[0]) / sc->nb;
+  } else if (MODE == SP_AV) {
+    if (t[0] == 0.0 || !(t[0] == t[0])) {
+      sc->done = t[0] == 0.0 ? BD_BREAKDOWN : BD_NONFINITE;
+      bg_stop(sc, use_cond, h);
+    } else {
+      sc->alpha = sc->rho / t[0];
+      sc->k++;
+    }
+  } else {  // SP_AT
+    sc->omega = t[1] > 0.0 ? t[0] / t[1] : 0.0;
+  }
+}
+
+// P1 / P3 (precond_body); P3's last block takes the half-step test
+template <int BS, int STAGE>
+__global__ void __launch_bounds__(BLOCK) bg_precond_kernel(int64_t n, BicgVecs v, BgScalars *sc, double *part,
+                                                           int use_cond, cudaGraphConditionalHandle h) {
+  __shared__ double sm[1][WARPS];
+  BG_ENTRY();
+  double a0 = 0.0;
+  if (STAGE == 0) {
+    precond_body<BS, 0>(v, n, vs->beta, vs->omega, a0);
+    return;
+  }
+  precond_body<BS, 1>(v, n, vs->alpha, 0.0, a0);
+  double red[1] = {a0};
+  block_sum<1>(red, sm);
+  if (!publish_and_arrive<1>(red, part, &sc->cnt[1])) return;
+  double t[1];
+  reduce_partials<1>(part, t, sm);
+  if (threadIdx.x != 0) return;
+  sc->cnt[1] = 0;
+  const double ss = sqrt(t[0]);
+  if (ss <= sc->tol * sc->nb) {
+    sc->half = 1;
+    sc->relres_rec = ss / sc->nb;
+  }
+}
+
+// P5; at a half-step convergence only x += alpha p^, then the loop ends for the exit check
+__global__ void __launch_bounds__(BLOCK) bg_update_kernel(int64_t n, BicgVecs v, BgScalars *sc, double *part,
+                                                          int use_cond, cudaGraphConditionalHandle h) {
+  __shared__ double sm[2][WARPS];
+  BG_ENTRY();
+  const int half = vs->half;
+  const double alpha = vs->alpha, omega = vs->omega;
+  double a0 = 0.0, a1 = 0.0;
+  if (half) {
+    const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
+    for (int64_t i = tid; i < n; i += nth) v.x[i] = __fma_rn(alpha, v.ph[i], v.x[i]);
+  } else {
+    update_body(v, n, alpha, omega, a0, a1);
+  }
+  double red[2] = {a0, a1};
+  block_sum<2>(red, sm);
+  if (!publish_and_arrive<2>(red, part, &sc->cnt[2])) return;
+  double t[2];
+  reduce_partials<2>(part, t, sm);
+  if (threadIdx.x != 0) return;
+  sc->cnt[2] = 0;
+  if (half) {
+    sc->half = 0;
+    sc->need_resid = 1;
+    bg_stop(sc, use_cond, h);
+    return;
+  }
+  const double rr = sqrt(t[0]);
+  sc->relres_rec = rr / sc->nb;
+  if (rr <= sc->tol * sc->nb) {
+    sc->need_resid = 1;
+    bg_stop(sc, use_cond, h);
+  } else if (sc->omega == 0.0) {
+    sc->done = BD_BREAKDOWN;
+    bg_stop(sc, use_cond, h);
+  } else {
+    sc->rho_old = sc->rho;
+    sc->rho = t[1];
+    bg_loop_top(sc, use_cond, h);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 template <int BS>
 static void *bicg_fn(int fmt, int lanes) {
@@ -436,6 +628,146 @@ static void *bicg_select(int fmt, int lanes, int bs) {
     case 4: return bicg_fn<4>(fmt, lanes);
     default: return bicg_fn<8>(fmt, lanes);
   }
+}
+
+// graph schedule: launchers per (format, CSR lanes, block size)
+struct BgOps {
+  void (*iter)(pcg_matrix *, const BicgVecs &, BgScalars *, double *, cudaStream_t, int, cudaGraphConditionalHandle);
+  void (*resid)(pcg_matrix *, const BicgVecs &, BgScalars *, double *, int, cudaStream_t);
+};
+
+template <int FMT, int L, int BS>
+static void bg_iteration(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double *part, cudaStream_t st, int use_cond,
+                         cudaGraphConditionalHandle h) {
+  const SellView S = A->sell();
+  const CsrView C = A->csr();
+  const int gs = A->grid_spmv, gv = A->grid_vec;
+  bg_precond_kernel<BS, 0><<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, use_cond, h);
+  bg_spmv_kernel<FMT, L, SP_AV><<<gs, BLOCK, 0, st>>>(S, C, v, sc, part, 0, use_cond, h);
+  bg_precond_kernel<BS, 1><<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, use_cond, h);
+  bg_spmv_kernel<FMT, L, SP_AT><<<gs, BLOCK, 0, st>>>(S, C, v, sc, part, 0, use_cond, h);
+  bg_update_kernel<<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, use_cond, h);
+  count_launch(5);
+}
+
+template <int FMT, int L, int BS>
+static void bg_resid(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double *part, int rmode, cudaStream_t st) {
+  if (rmode == BR_FINAL)
+    bg_spmv_kernel<FMT, L, SP_FINAL><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), v, sc, part, rmode, 0, 0);
+  else
+    bg_spmv_kernel<FMT, L, SP_RESID><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), v, sc, part, rmode, 0, 0);
+  count_launch();
+}
+
+template <int FMT, int L, int BS>
+static BgOps bg_ops_t() {
+  return {bg_iteration<FMT, L, BS>, bg_resid<FMT, L, BS>};
+}
+
+template <int BS>
+static BgOps bg_ops_bs(int fmt, int lanes) {
+  if (fmt == PCG_FORMAT_SELL) return bg_ops_t<PCG_FORMAT_SELL, 1, BS>();
+  switch (lanes) {
+    case 1: return bg_ops_t<PCG_FORMAT_CSR, 1, BS>();
+    case 2: return bg_ops_t<PCG_FORMAT_CSR, 2, BS>();
+    case 4: return bg_ops_t<PCG_FORMAT_CSR, 4, BS>();
+    case 8: return bg_ops_t<PCG_FORMAT_CSR, 8, BS>();
+    case 16: return bg_ops_t<PCG_FORMAT_CSR, 16, BS>();
+    default: return bg_ops_t<PCG_FORMAT_CSR, 32, BS>();
+  }
+}
+
+static BgOps bg_ops(int fmt, int lanes, int bs) {
+  switch (bs) {
+    case 1: return bg_ops_bs<1>(fmt, lanes);
+    case 2: return bg_ops_bs<2>(fmt, lanes);
+    case 4: return bg_ops_bs<4>(fmt, lanes);
+    default: return bg_ops_bs<8>(fmt, lanes);
+  }
+}
+
+// default: the graph schedule (measured faster on both Table 1 grids);
+// PCG_BICG=persist selects the single cooperative kernel
+static int bicg_use_graph(const pcg_matrix *) {
+  const char *e = getenv("PCG_BICG");
+  return !(e && !strcmp(e, "persist"));
+}
+
+static pcg_status bg_build(pcg_matrix *A, const BgOps &ops, const BicgVecs &v, int bs) {
+  SolveWork &w = A->work;
+  if (w.bg_exec && w.bg_bs == bs) return PCG_OK;
+  if (w.bg_exec) cudaGraphExecDestroy(w.bg_exec);
+  if (w.bg_graph) cudaGraphDestroy(w.bg_graph);
+  w.bg_exec = nullptr;
+  w.bg_graph = nullptr;
+  cudaStream_t cap;
+  PCG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  PCG_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  PCG_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  alignas(cudaGraphNodeParams) unsigned char npbuf[sizeof(cudaGraphNodeParams)] = {};
+  cudaGraphNodeParams &np = *reinterpret_cast<cudaGraphNodeParams *>(npbuf);
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  PCG_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+  PCG_CUDA(cudaStreamBeginCaptureToGraph(cap, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal));
+  BgScalars *sc = (BgScalars *)w.bgsc;
+  for (int u = 0; u < 2; u++) ops.iter(A, v, sc, w.partials, cap, 1, h);  // body = two iterations
+  cudaGraph_t out;
+  cudaError_t e = cudaStreamEndCapture(cap, &out);
+  cudaStreamDestroy(cap);
+  PCG_CUDA(e);
+  PCG_CUDA(cudaGraphInstantiate(&w.bg_exec, g, 0));
+  w.bg_graph = g;
+  w.bg_bs = bs;
+  return PCG_OK;
+}
+
+// graph-scheduled solve; fills the persistent kernel's BicgState fields
+static pcg_status bg_solve(pcg_matrix *A, const BicgVecs &v, int bs, double tol, int64_t max_iter, cudaStream_t st,
+                           BicgState *hs) {
+  SolveWork &w = A->work;
+  if (!w.bgsc) PCG_CUDA(cudaMalloc(&w.bgsc, sizeof(BgScalars)));
+  const BgOps ops = bg_ops(A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format, A->csr_lanes, bs);
+  PCG_TRY(bg_build(A, ops, v, bs));
+  BgScalars *sc = (BgScalars *)w.bgsc, h;
+  memset(&h, 0, sizeof(h));
+  h.tol = tol;
+  h.max_iter = max_iter;
+  PCG_CUDA(cudaMemcpyAsync(sc, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  auto read = [&]() -> pcg_status {
+    PCG_CUDA(cudaGetLastError());
+    PCG_CUDA(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    PCG_CUDA(cudaStreamSynchronize(st));
+    return PCG_OK;
+  };
+  ops.resid(A, v, sc, w.partials, BR_INIT, st);
+  PCG_TRY(read());
+  if (h.done == BD_ZERO_RHS || h.done == BD_NONFINITE) PCG_CUDA(cudaMemsetAsync(v.x, 0, sizeof(double) * A->n, st));
+  while (h.done == BD_RUNNING) {
+    PCG_CUDA(cudaGraphLaunch(w.bg_exec, st));
+    count_launch();
+    PCG_TRY(read());
+    if (h.done != BD_RUNNING) break;
+    ops.resid(A, v, sc, w.partials, BR_CHECK, st);  // exit check (need_resid), restart if it fails
+    PCG_TRY(read());
+  }
+  if (h.done == BD_MAXIT || h.done == BD_BREAKDOWN || h.done == BD_NONFINITE) {
+    ops.resid(A, v, sc, w.partials, BR_FINAL, st);
+    PCG_TRY(read());
+  }
+  hs->nb = h.nb;
+  hs->relres_rec = h.relres_rec;
+  hs->relres_true = h.relres_true;
+  hs->k = h.k;
+  hs->restarts = h.restarts;
+  hs->done = h.done;
+  return PCG_OK;
 }
 
 static pcg_status bicg_setup(pcg_matrix *A, int bs, cudaStream_t st) {
@@ -523,28 +855,36 @@ static pcg_status bicg_impl(pcg_matrix *A, const double *b, double *x, double to
   memset(&hs, 0, sizeof(hs));
   hs.tol = tol;
   hs.max_iter = max_iter;
-  BicgState *dst = (BicgState *)w.bstate;
-  PCG_CUDA(cudaMemcpyAsync(dst, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
-  void *fn = bicg_select(A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format, A->csr_lanes, bs);
-  if (w.bgrid == 0 || w.bgrid_bs != bs) {
-    int nbk = 0;
-    PCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbk, fn, BLOCK, 0));
-    w.bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(A->device) * std::min(nbk, 8),
-                                                         std::max<int64_t>(1, (n + BLOCK - 1) / BLOCK)));
-    w.bgrid_bs = bs;
-  }
-  SellView S = A->sell();
-  CsrView Cv = A->csr();
-  double *part = w.partials;  // 4 x grid (<= 8 x SMs; partials hold 6 x 32 x SMs)
-  GridBar *bar = (GridBar *)w.bbar;
-  void *args[] = {&S, &Cv, &v, &dst, &part, &bar};
   cudaEvent_t e0, e1;
   PCG_CUDA(cudaEventCreate(&e0));
   PCG_CUDA(cudaEventCreate(&e1));
-  PCG_CUDA(cudaEventRecord(e0, st));
-  PCG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(w.bgrid), dim3(BLOCK), args, 0, st));
-  count_launch();
-  PCG_CUDA(cudaEventRecord(e1, st));
+  if (bicg_use_graph(A)) {
+    PCG_CUDA(cudaEventRecord(e0, st));
+    const pcg_status gs = bg_solve(A, v, bs, tol, max_iter, st, &hs);
+    PCG_CUDA(cudaEventRecord(e1, st));
+    if (gs != PCG_OK) return gs;
+  } else {
+    BicgState *dst = (BicgState *)w.bstate;
+    PCG_CUDA(cudaMemcpyAsync(dst, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+    void *fn = bicg_select(A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format, A->csr_lanes, bs);
+    if (w.bgrid == 0 || w.bgrid_bs != bs) {
+      int nbk = 0;
+      PCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbk, fn, BLOCK, 0));
+      w.bgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(A->device) * std::min(nbk, 8),
+                                                           std::max<int64_t>(1, (n + BLOCK - 1) / BLOCK)));
+      w.bgrid_bs = bs;
+    }
+    SellView S = A->sell();
+    CsrView Cv = A->csr();
+    double *part = w.partials;  // 4 x grid (<= 8 x SMs; partials hold 6 x 32 x SMs)
+    GridBar *bar = (GridBar *)w.bbar;
+    void *args[] = {&S, &Cv, &v, &dst, &part, &bar};
+    PCG_CUDA(cudaEventRecord(e0, st));
+    PCG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(w.bgrid), dim3(BLOCK), args, 0, st));
+    count_launch();
+    PCG_CUDA(cudaEventRecord(e1, st));
+    PCG_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  }
   if (A->d_perm) {
     if (x_dev) {
       PCG_TRY(perm_out(A, v.x, x, st));
@@ -555,7 +895,6 @@ static pcg_status bicg_impl(pcg_matrix *A, const double *b, double *x, double to
   } else {
     PCG_CUDA(cudaMemcpyAsync(x, v.x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   }
-  PCG_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(hs), cudaMemcpyDeviceToHost, st));
   PCG_CUDA(cudaStreamSynchronize(st));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);

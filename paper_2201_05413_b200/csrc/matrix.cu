@@ -510,6 +510,8 @@ void free_work(pcg_matrix *A) {
   if (w.loop_graph) cudaGraphDestroy(w.loop_graph);
   if (w.mloop_exec) cudaGraphExecDestroy(w.mloop_exec);
   if (w.mloop_graph) cudaGraphDestroy(w.mloop_graph);
+  if (w.bg_exec) cudaGraphExecDestroy(w.bg_exec);
+  if (w.bg_graph) cudaGraphDestroy(w.bg_graph);
   for (double *p : {w.r, w.z, w.q, w.p[0], w.p[1], w.x, w.w, w.stage_b, w.stage_x, w.partials, w.mr, w.mz, w.mq,
                     w.mp[0], w.mp[1], w.mx, w.mb, w.mw, w.mpart})
     if (p) cudaFree(p);
@@ -517,7 +519,7 @@ void free_work(pcg_matrix *A) {
   if (w.h_sc) cudaFreeHost(w.h_sc);
   if (w.msc) cudaFree(w.msc);
   if (w.pbar) cudaFree(w.pbar);
-  for (void *q : {(void *)w.bv, w.bstate, w.bbar, (void *)w.bminv})
+  for (void *q : {(void *)w.bv, w.bstate, w.bbar, (void *)w.bminv, w.bgsc})
     if (q) cudaFree(q);
   if (w.h_msc) cudaFreeHost(w.h_msc);
   w = SolveWork();

@@ -57,6 +57,11 @@ struct SolveWork {
   void *bstate = nullptr, *bbar = nullptr;
   double *bminv = nullptr;
   int bminv_bs = 0, bgrid = 0, bgrid_bs = 0;
+  // BiCGSTAB graph schedule: device scalars, loop graph (per block size)
+  void *bgsc = nullptr;
+  cudaGraphExec_t bg_exec = nullptr;
+  cudaGraph_t bg_graph = nullptr;
+  int bg_bs = 0;
 };
 
 // single-RHS solver vectors (p0/p1: direction double buffer of the 2-pass schedule)

@@ -62,8 +62,15 @@ def test_fd_cube_generator_bitwise(pcg, N, fkind):
     assert np.array_equal(Gs["col"].cpu().numpy(), A.col[A.row_ptr[r0]:A.row_ptr[r1]])
 
 
+@pytest.fixture(params=["graph", "persist"])
+def schedule(request, monkeypatch):
+    """Both device schedules: the graph of five kernels per iteration and the persistent kernel."""
+    monkeypatch.setenv("PCG_BICG", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("N,bs", [(20, 1), (20, 2), (20, 4), (20, 8), (40, 1), (40, 4), (48, 8)])
-def test_bicgstab_parity_on_table1_grids(pcg, N, bs):
+def test_bicgstab_parity_on_table1_grids(pcg, schedule, N, bs):
     from paper_2201_05413_b200.problems import fd_cube_build
     A, b = O.fd_cube(N)
     tol = 1e-12
@@ -83,7 +90,7 @@ def test_bicgstab_parity_on_table1_grids(pcg, N, bs):
 
 
 @pytest.mark.parametrize("name,c", [("C1", 32), ("C2", 48), ("C3", 24)])
-def test_bicgstab_on_spd_fem_systems(pcg, name, c):
+def test_bicgstab_on_spd_fem_systems(pcg, schedule, name, c):
     """BiCGSTAB through the same handles CG uses (SELL-32 / SELL-C-sigma formats)."""
     P = O.build_problem(name, c=c, k=1)
     A, b = P["A"], P["B"][:, 0]
@@ -100,7 +107,7 @@ def test_bicgstab_on_spd_fem_systems(pcg, name, c):
         assert lo - max(2, 0.02 * lo) <= info["iterations"] <= hi + max(2, 0.02 * hi)
 
 
-def test_bicgstab_edges_and_errors(pcg):
+def test_bicgstab_edges_and_errors(pcg, schedule):
     import torch
     from paper_2201_05413_b200 import PcgError
     from paper_2201_05413_b200.problems import fd_cube_build
