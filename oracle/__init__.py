@@ -26,7 +26,7 @@ P1_TRI, P1_TET, P2_TRI = 1, 2, 3
 FAMILY = {"P1_TRI": P1_TRI, "P1_TET": P1_TET, "P2_TRI": P2_TRI}
 F_ZERO, F_CONST, F_SIN2D, F_SIN3D, F_BUMP3D, F_LINEAR = 0, 1, 2, 3, 4, 5
 PAT_ELEMENT, PAT_AXIS = 0, 1
-OK, NOT_CONVERGED, ERR_INVALID_ARG, ERR_ZERO_DIAGONAL, ERR_NOT_SPD, ERR_POLICY, ERR_OOM = range(7)
+OK, NOT_CONVERGED, ERR_INVALID_ARG, ERR_ZERO_DIAGONAL, ERR_NOT_SPD, ERR_POLICY, ERR_OOM, ERR_INDEX = range(8)
 
 
 def build(force: bool = False) -> str:
@@ -81,6 +81,8 @@ def lib():
         L.orc_bicgstab.argtypes = [P(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_int64,
                                    P(C.c_int64), P(C.c_double), P(C.c_double)]
         L.orc_halo.restype = C.c_int64
+        L.orc_coo_to_csr.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_halo.argtypes = [P(_Csr), C.c_int64, C.c_int64, C.c_void_p, C.c_int64]
         L.orc_fd_identity_rows_nnz.restype = C.c_int64
         L.orc_fd_identity_rows_nnz.argtypes = [C.c_int64]
@@ -265,6 +267,26 @@ def bicgstab(A: Csr, b, x0=None, tol=1e-10, max_iter=50000, block=1) -> PcgResul
     st = lib().orc_bicgstab(C.byref(Ac), _ptr(b), _ptr(x), tol, max_iter, block, C.byref(it), C.byref(rr),
                             C.byref(rt))
     return PcgResult(x=x, iterations=it.value, relres_rec=rr.value, relres_true=rt.value, status=st)
+
+
+def coo_to_csr(n_rows: int, n_cols: int, row, col, val):
+    """SPEC coo_to_csr: (row_ptr, col, val) numpy arrays; duplicates summed in
+    input order.  Raises IndexError for an out-of-range index (SPEC IndexOutOfRange)."""
+    row = np.ascontiguousarray(row, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int64)
+    val = np.ascontiguousarray(val, dtype=np.float64)
+    nnz = row.size
+    rp = np.zeros(n_rows + 1, dtype=np.int64)
+    co = np.zeros(max(nnz, 1), dtype=np.int64)
+    vo = np.zeros(max(nnz, 1))
+    u = C.c_int64(0)
+    st = lib().orc_coo_to_csr(n_rows, n_cols, nnz, _ptr(row), _ptr(col), _ptr(val), _ptr(rp), _ptr(co), _ptr(vo),
+                              C.byref(u))
+    if st == ERR_INDEX:
+        raise IndexError("orc_coo_to_csr: index out of range")
+    if st != OK:
+        raise RuntimeError(f"orc_coo_to_csr: {st}")
+    return rp, co[:u.value].copy(), vo[:u.value].copy()
 
 
 def pcg_multi(A: Csr, B, X0=None, tol=1e-10, max_iter=50000):

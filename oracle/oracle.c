@@ -939,3 +939,44 @@ out:
   bj_free(&M);
   return st;
 }
+
+/* ---------------------------------------------------------------- COO -> CSR
+ * SPEC coo_to_csr: "duplicates summed; CSR invariants hold";
+ * IndexOutOfRange for an index outside its dimension.  The order of the sum of a
+ * duplicate group is the input order (qsort on (row, col, input position), then a
+ * left-to-right sum from 0.0): the dense accumulation A[r][c] += v in input order. */
+static const int64_t *coo_r, *coo_c;
+static int cmp_coo(const void *pa, const void *pb) {
+  const int64_t a = *(const int64_t *)pa, b = *(const int64_t *)pb;
+  if (coo_r[a] != coo_r[b]) return coo_r[a] < coo_r[b] ? -1 : 1;
+  if (coo_c[a] != coo_c[b]) return coo_c[a] < coo_c[b] ? -1 : 1;
+  return a < b ? -1 : (a > b);
+}
+
+int orc_coo_to_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t *row, const int64_t *col,
+                   const double *val, int64_t *row_ptr, int64_t *col_out, double *val_out, int64_t *nnz_out) {
+  if (n_rows < 0 || n_cols < 0 || nnz < 0) return ORC_ERR_INVALID_ARG;
+  for (int64_t k = 0; k < nnz; k++)
+    if (row[k] < 0 || row[k] >= n_rows || col[k] < 0 || col[k] >= n_cols) return ORC_ERR_INDEX;
+  int64_t *ord = malloc(sizeof(int64_t) * (nnz > 0 ? nnz : 1));
+  if (!ord) return ORC_ERR_OOM;
+  for (int64_t k = 0; k < nnz; k++) ord[k] = k;
+  coo_r = row;
+  coo_c = col;
+  qsort(ord, nnz, sizeof(int64_t), cmp_coo);
+  for (int64_t r = 0; r <= n_rows; r++) row_ptr[r] = 0;
+  int64_t u = 0;
+  for (int64_t k = 0; k < nnz;) {
+    const int64_t r = row[ord[k]], c = col[ord[k]];
+    double s = 0.0;
+    while (k < nnz && row[ord[k]] == r && col[ord[k]] == c) s += val[ord[k++]];
+    col_out[u] = c;
+    val_out[u] = s;
+    row_ptr[r + 1]++;
+    u++;
+  }
+  for (int64_t r = 0; r < n_rows; r++) row_ptr[r + 1] += row_ptr[r];
+  *nnz_out = u;
+  free(ord);
+  return ORC_OK;
+}

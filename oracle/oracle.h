@@ -20,6 +20,7 @@
 #define ORC_ERR_NOT_SPD 4
 #define ORC_ERR_POLICY 5 /* a policy-dropped entry was not exactly 0.0 */
 #define ORC_ERR_OOM 6
+#define ORC_ERR_INDEX 7  /* an index outside its dimension (coo_to_csr)     */
 
 /* element families (§8(c).1) */
 #define ORC_P1_TRI 1  /* 2D lattice, "/" split, 3 nodes per element      */
@@ -110,5 +111,13 @@ int64_t orc_fd_identity_rows_nnz(int64_t N);
 int orc_fd_cube(int64_t N, int fkind, orc_csr *A, double *b /* N^3 */);
 int orc_bicgstab(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter, int64_t bs,
                  int64_t *iters, double *relres_rec, double *relres_true);
+
+/* SURVEY §8(f) N1 / SPEC coo_to_csr: COO triplets -> CSR.  Entries ordered
+ * by (row, col); the values of equal (row, col) entries are summed left to right in
+ * INPUT order starting from 0.0, i.e. A[r][c] = sum over the entries (r, c, v) in order
+ * (SPEC: "duplicates summed").  Caller-owned outputs: row_ptr[n_rows+1], col_out[nnz],
+ * val_out[nnz]; *nnz_out = unique entries.  ORC_ERR_INDEX if an index is out of range. */
+int orc_coo_to_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t *row, const int64_t *col,
+                   const double *val, int64_t *row_ptr, int64_t *col_out, double *val_out, int64_t *nnz_out);
 
 #endif

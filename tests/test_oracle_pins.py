@@ -659,3 +659,60 @@ def test_c6_neumann_stiffness_symmetric_zero_rowsums_and_dense_solve():
     xe = np.linalg.solve(A.to_dense(), b)
     r = O.pcg(A, b, tol=1e-14)
     assert np.linalg.norm(r.x - xe) / np.linalg.norm(xe) <= 1e-12
+
+
+# ---------------------------------------------------------------- COO -> CSR
+def test_coo_to_csr_spec_examples():
+    rp, c, v = O.coo_to_csr(2, 2, [0, 0, 1], [0, 0, 1], [1.0, 3.0, 2.0])  # S:55 duplicate summation
+    assert rp.tolist() == [0, 1, 2] and c.tolist() == [0, 1] and v.tolist() == [4.0, 2.0]
+    rp, c, v = O.coo_to_csr(3, 3, [], [], [])  # S:56 empty
+    assert rp.tolist() == [0, 0, 0, 0] and c.size == 0
+    rp, c, v = O.coo_to_csr(3, 3, [2, 0, 1], [2, 0, 1], [1.0, 1.0, 1.0])  # S:57 identity (any order)
+    assert rp.tolist() == [0, 1, 2, 3] and c.tolist() == [0, 1, 2] and v.tolist() == [1.0, 1.0, 1.0]
+    with pytest.raises(IndexError):  # S:53 IndexOutOfRange
+        O.coo_to_csr(2, 3, [0, 2], [0, 0], [1.0, 1.0])
+    with pytest.raises(IndexError):
+        O.coo_to_csr(2, 3, [0], [-1], [1.0])
+
+
+@pytest.mark.parametrize("seed,nr,nc,nnz", [(1, 7, 5, 60), (2, 40, 40, 900), (3, 1, 9, 30), (4, 13, 1, 25)])
+def test_coo_to_csr_brute_force_dense(seed, nr, nc, nnz):
+    """Dense accumulation in input order (A[r][c] += v) is the definition: bitwise equal
+    values, pattern = the set of positions present (explicit zero sums kept)."""
+    from coo_inputs import triplets
+    r, c, v = triplets(seed, nr, nc, nnz)
+    rp, co, vo = O.coo_to_csr(nr, nc, r, c, v)
+    D = np.zeros((nr, nc))
+    present = np.zeros((nr, nc), dtype=bool)
+    for k in range(nnz):
+        D[r[k], c[k]] += v[k]
+        present[r[k], c[k]] = True
+    assert rp[0] == 0 and rp[-1] == co.size == present.sum()
+    for i in range(nr):
+        cols = co[rp[i]:rp[i + 1]]
+        assert np.all(np.diff(cols) > 0)  # strictly increasing within a row (S:32)
+        assert cols.tolist() == np.nonzero(present[i])[0].tolist()
+        assert np.array_equal(vo[rp[i]:rp[i + 1]], D[i, cols])  # bitwise
+    assert np.any(vo == 0.0) or nr * nc < 40  # the cancelling pair stays an explicit entry
+
+
+@pytest.mark.parametrize("fam,c,jit", [(O.P1_TRI, 6, False), (O.P1_TRI, 8, True), (O.P2_TRI, 4, False),
+                                       (O.P1_TET, 3, False)])
+def test_coo_to_csr_of_element_triplets_is_the_assembly(fam, c, jit):
+    """Element-by-element assembly through COO (triplets (t_a, t_b, Ke[a][b]) emitted in
+    element order, local (a, b) order) is orc_assemble's stiffness, bitwise: the two
+    oracle paths (incidence-list pattern + csr_find, versus sort + ordered sum) agree."""
+    m = O.Mesh(fam, c, jitter=jit, seed=77)
+    K, _ = O.assemble(m, O.F_ZERO)
+    rows, cols, vals = [], [], []
+    for e in range(m.n_elem):
+        t = m.elem[e]
+        Ke = O.elem_stiffness(fam, m.coord[t].ravel())
+        for a in range(m.npe):
+            for b in range(m.npe):
+                rows.append(t[a])
+                cols.append(t[b])
+                vals.append(Ke[a, b])
+    rp, co, vo = O.coo_to_csr(m.n_nodes, m.n_nodes, rows, cols, vals)
+    assert np.array_equal(rp, K.row_ptr) and np.array_equal(co, K.col)
+    assert np.array_equal(vo, K.val)
