@@ -88,6 +88,27 @@ pcg_status fd_cube_count(int64_t N, int64_t row_begin, int64_t row_end, int64_t 
 pcg_status fd_cube_assemble(int64_t N, int32_t fkind, int64_t row_begin, int64_t row_end, const int64_t *d_row_ptr,
                             int64_t *d_col, double *d_val, double *d_b, void *stream);
 
+/* Generic COO -> CSR on the device (SURVEY §8(f) N1 "generic COO -> CSR (sort +
+ * segmented reduce)"; SPEC coo_to_csr: "duplicates summed; CSR invariants
+ * hold", IndexOutOfRange), the staging step of element-by-element assembly.
+ * Output entries are ordered by (row, col), columns strictly increasing within a
+ * row.  The values of the entries that share a (row, col) are summed left to right
+ * in INPUT order starting from 0.0 (a stable radix sort keeps that order), so the
+ * result is bitwise the dense accumulation A[row][col] += val over the entries in
+ * order; a group that sums to 0.0 stays an explicit entry.
+ *   row[nnz], col[nnz] (int64), val[nnz] (f64): DEVICE pointers, read only, caller-owned.
+ *   row_ptr[n_rows + 1] (int64), col_out[nnz] (int64), val_out[nnz] (f64): DEVICE buffers,
+ *   caller-owned (nnz entries always suffice); *nnz_out (HOST) = number of unique entries.
+ * Sizes: 0 <= n_rows, n_cols < 2^31, 0 <= nnz < 2^31.  Scratch (~44 B per entry) is
+ * allocated and freed inside; returns when the result is complete (synchronous on
+ * `stream`).  Errors: PCG_ERR_INVALID_ARG (null pointer, sizes out of range; outputs
+ * untouched), PCG_ERR_INDEX_OUT_OF_RANGE (an index outside [0, n_rows) x [0, n_cols);
+ * outputs unspecified), PCG_ERR_OOM, PCG_ERR_CUDA.
+ * Example: (0,0,1), (0,0,3), (1,1,2) in 2 x 2 -> row_ptr {0,1,2}, col {0,1}, val {4,2}. */
+pcg_status coo_to_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t *row, const int64_t *col,
+                      const double *val, int64_t *row_ptr, int64_t *col_out, double *val_out, int64_t *nnz_out,
+                      void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,9 +15,9 @@ import numpy as np
 from . import _lib
 from ._lib import (PCG_FMT_AUTO, PCG_FMT_CSR, PCG_FMT_SELL, PCG_FORMAT_CSR, PCG_FORMAT_SELL,  # noqa: F401
                    PCG_OK, PCG_NOT_CONVERGED, PcgError, check, lib)
-from .problems import FemSpec, fem_spec, fem_build  # noqa: F401
+from .problems import FemSpec, coo_to_csr, fem_spec, fem_build  # noqa: F401
 
-__all__ = ["Matrix", "Comm", "partition_rows", "fem_spec", "fem_build", "PcgError", "kernel_launches"]
+__all__ = ["Matrix", "Comm", "partition_rows", "fem_spec", "fem_build", "coo_to_csr", "PcgError", "kernel_launches"]
 
 
 def _torch():

@@ -100,6 +100,7 @@ def lib():
         "pcg_bicgstab": [vp, vp, vp, C.c_double, i64, i32, vp, P(PcgInfo)],
         "fd_cube_count": [i64, i64, i64, vp, P(i64), vp],
         "fd_cube_assemble": [i64, i32, i64, i64, vp, vp, vp, vp, vp],
+        "coo_to_csr": [i64, i64, i64, vp, vp, vp, vp, vp, vp, P(i64), vp],
         "fem_problem_size": [P(FemSpec), P(i64), P(i64), P(i64)],
         "fem_count": [P(FemSpec), i64, i64, vp, P(i64), vp],
         "fem_assemble": [P(FemSpec), i64, i64, vp, vp, vp, vp, i64, vp],

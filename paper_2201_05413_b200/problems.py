@@ -90,3 +90,27 @@ def fd_cube_build(N: int, fkind: int = FD_X2MY2, row_begin: int = 0, row_end: in
     check(lib().fd_cube_assemble(N, fkind, row_begin, row_end, C.c_void_p(rp.data_ptr()), C.c_void_p(col.data_ptr()),
                                  C.c_void_p(val.data_ptr()), C.c_void_p(b.data_ptr()), st), "fd_cube_assemble")
     return {"row_ptr": rp, "col": col, "val": val, "b": b, "n": n}
+
+
+def coo_to_csr(row, col, val, n_rows: int, n_cols: int | None = None, stream=None):
+    """Generic COO -> CSR on the GPU (include/fem_gen.h coo_to_csr; SPEC coo_to_csr):
+    (row, col) sorted, duplicates summed in input order.  row/col int64, val float64
+    CUDA tensors.  Returns dict(row_ptr, col, val) of CUDA tensors (int64, int64, f64)."""
+    import torch
+    n_cols = n_rows if n_cols is None else n_cols
+    dev = row.device
+    row = row.to(torch.int64).contiguous()
+    col = col.to(torch.int64).contiguous()
+    val = val.to(torch.float64).contiguous()
+    nnz = row.numel()
+    if col.numel() != nnz or val.numel() != nnz:
+        raise ValueError("coo_to_csr: row, col and val must have the same length")
+    st = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream if stream is None else stream.cuda_stream)
+    rp = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
+    co = torch.empty(max(nnz, 1), dtype=torch.int64, device=dev)
+    vo = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+    u = C.c_int64()
+    check(lib().coo_to_csr(n_rows, n_cols, nnz, C.c_void_p(row.data_ptr()), C.c_void_p(col.data_ptr()),
+                           C.c_void_p(val.data_ptr()), C.c_void_p(rp.data_ptr()), C.c_void_p(co.data_ptr()),
+                           C.c_void_p(vo.data_ptr()), C.byref(u), st), "coo_to_csr")
+    return {"row_ptr": rp, "col": co[:u.value], "val": vo[:u.value]}
