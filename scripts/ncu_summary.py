@@ -54,8 +54,9 @@ def full(rep, traffic, workload):
         rd = to_bytes(d["dram__bytes_read.sum"], units["dram__bytes_read.sum"])
         wr = to_bytes(d["dram__bytes_write.sum"], units["dram__bytes_write.sum"])
         w.writerow([d["Kernel Name"][:90], f"{ms:.4f}", f"{rd / 1e9:.4f}", f"{wr / 1e9:.4f}"] + [d.get(c, "") for c in COLS[3:]])
-        per.setdefault(name, {"dram_read_GB": rd / 1e9, "dram_write_GB": wr / 1e9, "traffic_bytes": rd + wr,
-                              "ncu_duration_ms": ms})
+        # the LAST launch of each kernel is kept: steady state (earlier ones are setup or warm-up)
+        per[name] = {"dram_read_GB": rd / 1e9, "dram_write_GB": wr / 1e9, "traffic_bytes": rd + wr,
+                     "ncu_duration_ms": ms}
     if traffic:
         with open(traffic, "w") as fh:
             json.dump({"workload": workload, "source": f"{rep} (ncu --set full --clock-control none)",
