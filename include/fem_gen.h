@@ -88,6 +88,23 @@ pcg_status fd_cube_count(int64_t N, int64_t row_begin, int64_t row_end, int64_t 
 pcg_status fd_cube_assemble(int64_t N, int32_t fkind, int64_t row_begin, int64_t row_end, const int64_t *d_row_ptr,
                             int64_t *d_col, double *d_val, double *d_b, void *stream);
 
+/* Element-by-element assembly, step 1 (generic path): the
+ * elements' stiffness matrices K_e as COO triplets over ALL lattice nodes (Neumann,
+ * before Dirichlet elimination; node id lexicographic, x fastest, boundary included).
+ * Elements are enumerated as the row-wise generator visits them (cells
+ * lexicographic, then the split's element order); element e's triplets sit at
+ * [(e - e0) * npe^2, (e - e0 + 1) * npe^2), local (a, b) row-major.  coo_to_csr of all
+ * elements' triplets is the assembled Neumann stiffness (explicit zeros kept).
+ *   P1: K_e = |T| G G^T (barycentric gradients G; §8(c).3);
+ *   P2: K_e[a][b] = sum over the 3 edge midpoints of |T|/3 grad phi_a . grad phi_b.
+ * fem_element_count: n_elem (2c^2 triangles, 6c^3 tets), npe (3 / 6 / 4), n_nodes.
+ * d_row, d_col (int64) and d_val (f64): DEVICE buffers of (e1 - e0) * npe^2 entries,
+ * caller-owned.  Synchronous on `stream`.  Errors: PCG_ERR_INVALID_ARG (bad spec or
+ * range, null buffer), PCG_ERR_CUDA. */
+pcg_status fem_element_count(const fem_spec *spec, int64_t *n_elem, int32_t *npe, int64_t *n_nodes);
+pcg_status fem_element_coo(const fem_spec *spec, int64_t e0, int64_t e1, int64_t *d_row, int64_t *d_col,
+                           double *d_val, void *stream);
+
 /* Generic COO -> CSR on the device (SURVEY §8(f) N1 "generic COO -> CSR (sort +
  * segmented reduce)"; SPEC coo_to_csr: "duplicates summed; CSR invariants
  * hold", IndexOutOfRange), the staging step of element-by-element assembly.

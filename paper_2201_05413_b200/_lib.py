@@ -101,6 +101,8 @@ def lib():
         "fd_cube_count": [i64, i64, i64, vp, P(i64), vp],
         "fd_cube_assemble": [i64, i32, i64, i64, vp, vp, vp, vp, vp],
         "coo_to_csr": [i64, i64, i64, vp, vp, vp, vp, vp, vp, P(i64), vp],
+        "fem_element_count": [P(FemSpec), P(i64), P(i32), P(i64)],
+        "fem_element_coo": [P(FemSpec), i64, i64, vp, vp, vp, vp],
         "fem_problem_size": [P(FemSpec), P(i64), P(i64), P(i64)],
         "fem_count": [P(FemSpec), i64, i64, vp, P(i64), vp],
         "fem_assemble": [P(FemSpec), i64, i64, vp, vp, vp, vp, i64, vp],

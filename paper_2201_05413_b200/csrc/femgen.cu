@@ -412,6 +412,131 @@ __global__ void centres_kernel(uint64_t seed, int k, double *ctr) {
   if (t < 3 * k) ctr[t] = u01(seed, (uint64_t)t);  // c_s,axis = U(seed, 3s + axis)
 }
 
+// ------------------------------------------------------------ element-by-element triplets
+// One thread per element e (cells lexicographic, then the split's element order —
+// the row-wise generator's enumeration): its npe x npe stiffness matrix K_e over ALL
+// lattice nodes (Neumann, before Dirichlet elimination), emitted as triplets
+// (node_a, node_b, K_e[a][b]) at position e * npe^2 + a * npe + b.  coo_to_csr of
+// the triplets of every element sums each entry over the elements in element order:
+// the assembled stiffness (generic path).
+//   P1: K_e = |T| G G^T with G the barycentric gradients (P:78 cot formula, §8(c).3)
+//   P2: K_e[a][b] = sum over the 3 edge midpoints q of |T|/3 grad phi_a . grad phi_b
+__global__ void __launch_bounds__(128) elem_coo_kernel(fem_spec s, int64_t e0, int64_t e1, int64_t *__restrict__ ro,
+                                                       int64_t *__restrict__ co, double *__restrict__ vo) {
+  const int64_t e = e0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= e1) return;
+  const Geo g = make_geo(s);
+  const int64_t np = g.np;
+  const size_t o = (size_t)(e - e0);
+  if (s.family == FEM_P1_TRI || s.family == FEM_P2_TRI) {
+    const int64_t cell = e >> 1;
+    const int t = (int)(e & 1);
+    const int ci = (int)(cell % g.c), cj = (int)(cell / g.c);
+    if (s.family == FEM_P1_TRI) {
+      int va[3], vb[3];
+      tri_verts(ci, cj, t, va, vb);
+      double x[3], y[3];
+      for (int k = 0; k < 3; k++) node_xy(g, va[k], vb[k], x[k], y[k]);
+      const double d = (x[1] - x[0]) * (y[2] - y[0]) - (x[2] - x[0]) * (y[1] - y[0]);
+      double gx[3], gy[3];
+      gx[0] = (y[1] - y[2]) / d; gy[0] = (x[2] - x[1]) / d;
+      gx[1] = (y[2] - y[0]) / d; gy[1] = (x[0] - x[2]) / d;
+      gx[2] = (y[0] - y[1]) / d; gy[2] = (x[1] - x[0]) / d;
+      const double area = fabs(d) * 0.5;
+      for (int a = 0; a < 3; a++)
+        for (int b = 0; b < 3; b++) {
+          const size_t q = o * 9 + a * 3 + b;
+          ro[q] = va[a] + np * vb[a];
+          co[q] = va[b] + np * vb[b];
+          vo[q] = area * (gx[a] * gx[b] + gy[a] * gy[b]);
+        }
+    } else {
+      const int a0 = 2 * ci, b0 = 2 * cj, a1 = a0 + 2, b1 = b0 + 2;
+      int da[6], db[6];
+      if (t == 0) {
+        const int A[6] = {a0, a1, a1, a0 + 1, a1, a0 + 1}, B[6] = {b0, b0, b1, b0, b0 + 1, b0 + 1};
+        for (int k = 0; k < 6; k++) { da[k] = A[k]; db[k] = B[k]; }
+      } else {
+        const int A[6] = {a0, a1, a0, a0 + 1, a0 + 1, a0}, B[6] = {b0, b1, b1, b0 + 1, b1, b0 + 1};
+        for (int k = 0; k < 6; k++) { da[k] = A[k]; db[k] = B[k]; }
+      }
+      double x[3], y[3];
+      for (int k = 0; k < 3; k++) { x[k] = da[k] * g.hs; y[k] = db[k] * g.hs; }
+      const double d = (x[1] - x[0]) * (y[2] - y[0]) - (x[2] - x[0]) * (y[1] - y[0]);
+      double gx[3], gy[3];
+      gx[0] = (y[1] - y[2]) / d; gy[0] = (x[2] - x[1]) / d;
+      gx[1] = (y[2] - y[0]) / d; gy[1] = (x[0] - x[2]) / d;
+      gx[2] = (y[0] - y[1]) / d; gy[2] = (x[1] - x[0]) / d;
+      const double w = (fabs(d) * 0.5) / 3.0;
+      const int E[3][2] = {{0, 1}, {1, 2}, {0, 2}};
+      double K[6][6];
+      for (int a = 0; a < 6; a++)
+        for (int b = 0; b < 6; b++) K[a][b] = 0.0;
+      for (int q = 0; q < 3; q++) {
+        double L[3] = {0, 0, 0};
+        L[E[q][0]] = 0.5;
+        L[E[q][1]] = 0.5;
+        double phx[6], phy[6];
+        for (int v = 0; v < 3; v++) {
+          phx[v] = (4.0 * L[v] - 1.0) * gx[v];
+          phy[v] = (4.0 * L[v] - 1.0) * gy[v];
+        }
+        for (int m = 0; m < 3; m++) {
+          const int i0 = E[m][0], i1 = E[m][1];
+          phx[3 + m] = 4.0 * (L[i0] * gx[i1] + L[i1] * gx[i0]);
+          phy[3 + m] = 4.0 * (L[i0] * gy[i1] + L[i1] * gy[i0]);
+        }
+        for (int a = 0; a < 6; a++)
+          for (int b = 0; b < 6; b++) K[a][b] += w * (phx[a] * phx[b] + phy[a] * phy[b]);
+      }
+      for (int a = 0; a < 6; a++)
+        for (int b = 0; b < 6; b++) {
+          const size_t q = o * 36 + a * 6 + b;
+          ro[q] = da[a] + np * db[a];
+          co[q] = da[b] + np * db[b];
+          vo[q] = K[a][b];
+        }
+    }
+    return;
+  }
+  // P1_TET: Kuhn tet p of cell (ci, cj, cl)
+  const int PERM[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  const int64_t cell = e / 6;
+  const int p = (int)(e % 6);
+  const int ci = (int)(cell % g.c), cj = (int)((cell / g.c) % g.c), cl = (int)(cell / ((int64_t)g.c * g.c));
+  int v[4][3];
+  v[0][0] = ci; v[0][1] = cj; v[0][2] = cl;
+  for (int k = 0; k < 3; k++) {
+    v[k + 1][0] = v[k][0]; v[k + 1][1] = v[k][1]; v[k + 1][2] = v[k][2];
+    v[k + 1][PERM[p][k]] += 1;
+  }
+  double X[4][3];
+  for (int k = 0; k < 4; k++) node_xyz(g, v[k][0], v[k][1], v[k][2], X[k]);
+  double ed[3][3];
+  for (int k = 0; k < 3; k++)
+    for (int d = 0; d < 3; d++) ed[k][d] = X[k + 1][d] - X[0][d];
+  double G[4][3];
+  const int CA[3] = {1, 2, 0}, CB[3] = {2, 0, 1};
+  for (int k = 0; k < 3; k++) {
+    const double *u = ed[CA[k]], *w = ed[CB[k]];
+    G[k + 1][0] = u[1] * w[2] - u[2] * w[1];
+    G[k + 1][1] = u[2] * w[0] - u[0] * w[2];
+    G[k + 1][2] = u[0] * w[1] - u[1] * w[0];
+  }
+  const double det = ed[0][0] * G[1][0] + ed[0][1] * G[1][1] + ed[0][2] * G[1][2];
+  for (int k = 1; k < 4; k++)
+    for (int d = 0; d < 3; d++) G[k][d] /= det;
+  for (int d = 0; d < 3; d++) G[0][d] = -(G[1][d] + G[2][d] + G[3][d]);
+  const double vol = fabs(det) / 6.0;
+  for (int a = 0; a < 4; a++)
+    for (int b = 0; b < 4; b++) {
+      const size_t q = o * 16 + a * 4 + b;
+      ro[q] = v[a][0] + np * (v[a][1] + np * (int64_t)v[a][2]);
+      co[q] = v[b][0] + np * (v[b][1] + np * (int64_t)v[b][2]);
+      vo[q] = vol * (G[a][0] * G[b][0] + G[a][1] * G[b][1] + G[a][2] * G[b][2]);
+    }
+}
+
 pcg_status check_spec(const fem_spec *s) {
   if (!s) return fail(PCG_ERR_INVALID_ARG, "fem: null spec");
   if (s->family < FEM_P1_TRI || s->family > FEM_P2_TRI) return fail(PCG_ERR_INVALID_ARG, "fem: bad family");
@@ -505,5 +630,32 @@ extern "C" pcg_status fem_assemble(const fem_spec *s, int64_t r0, int64_t r1, in
   PCG_CUDA(cudaFreeAsync(bad, st));
   PCG_CUDA(cudaStreamSynchronize(st));
   if (h_bad) return fail(PCG_ERR_INVALID_ARG, "fem_assemble: AXIS policy dropped a nonzero entry");
+  return PCG_OK;
+}
+
+extern "C" pcg_status fem_element_count(const fem_spec *s, int64_t *n_elem, int32_t *npe, int64_t *n_nodes) {
+  PCG_TRY(check_spec(s));
+  const Geo g = make_geo(*s);
+  const int64_t c = s->c;
+  if (n_elem) *n_elem = s->family == FEM_P1_TET ? 6 * c * c * c : 2 * c * c;
+  if (npe) *npe = s->family == FEM_P1_TET ? 4 : (s->family == FEM_P2_TRI ? 6 : 3);
+  if (n_nodes) *n_nodes = s->family == FEM_P1_TET ? (int64_t)g.np * g.np * g.np : (int64_t)g.np * g.np;
+  return PCG_OK;
+}
+
+extern "C" pcg_status fem_element_coo(const fem_spec *s, int64_t e0, int64_t e1, int64_t *d_row, int64_t *d_col,
+                                      double *d_val, void *stream) {
+  PCG_TRY(check_spec(s));
+  int64_t ne = 0;
+  fem_element_count(s, &ne, nullptr, nullptr);
+  if (e0 < 0 || e1 < e0 || e1 > ne || ((!d_row || !d_col || !d_val) && e1 > e0))
+    return fail(PCG_ERR_INVALID_ARG, "fem_element_coo: bad element range or null output");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (e1 > e0) {
+    elem_coo_kernel<<<(unsigned)((e1 - e0 + 127) / 128), 128, 0, st>>>(*s, e0, e1, d_row, d_col, d_val);
+    count_launch();
+    PCG_CUDA(cudaGetLastError());
+  }
+  PCG_CUDA(cudaStreamSynchronize(st));
   return PCG_OK;
 }

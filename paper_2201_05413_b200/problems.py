@@ -114,3 +114,28 @@ def coo_to_csr(row, col, val, n_rows: int, n_cols: int | None = None, stream=Non
                            C.c_void_p(val.data_ptr()), C.c_void_p(rp.data_ptr()), C.c_void_p(co.data_ptr()),
                            C.c_void_p(vo.data_ptr()), C.byref(u), st), "coo_to_csr")
     return {"row_ptr": rp, "col": co[:u.value], "val": vo[:u.value]}
+
+
+def fem_element_triplets(spec, stream=None):
+    """Element-by-element assembly, step 1 (include/fem_gen.h fem_element_coo): every
+    element's stiffness K_e as (row, col, val) CUDA tensors over all lattice nodes,
+    element-major.  Returns dict(row, col, val, n_nodes, npe)."""
+    import torch
+    ne, npe, nn = C.c_int64(), C.c_int32(), C.c_int64()
+    check(lib().fem_element_count(C.byref(spec), C.byref(ne), C.byref(npe), C.byref(nn)), "fem_element_count")
+    m = ne.value * npe.value * npe.value
+    dev = torch.device("cuda", torch.cuda.current_device())
+    st = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream if stream is None else stream.cuda_stream)
+    r = torch.empty(max(m, 1), dtype=torch.int64, device=dev)[:m]
+    c = torch.empty(max(m, 1), dtype=torch.int64, device=dev)[:m]
+    v = torch.empty(max(m, 1), dtype=torch.float64, device=dev)[:m]
+    check(lib().fem_element_coo(C.byref(spec), 0, ne.value, C.c_void_p(r.data_ptr()), C.c_void_p(c.data_ptr()),
+                                C.c_void_p(v.data_ptr()), st), "fem_element_coo")
+    return {"row": r, "col": c, "val": v, "n_nodes": nn.value, "npe": npe.value}
+
+
+def fem_assemble_elements(spec, stream=None):
+    """Element-by-element assembly on the GPU: fem_element_coo then coo_to_csr — the
+    Neumann stiffness over all lattice nodes as dict(row_ptr, col, val)."""
+    T = fem_element_triplets(spec, stream)
+    return coo_to_csr(T["row"], T["col"], T["val"], T["n_nodes"], T["n_nodes"], stream)
