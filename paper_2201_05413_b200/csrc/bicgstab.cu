@@ -240,6 +240,73 @@ __device__ __forceinline__ void precond_body(const BicgVecs &v, int64_t n, doubl
   }
 }
 
+// Block-Jacobi (BS > 1) on natural row order, one lane per ROW: the BS lanes of a
+// block hold its BS rows (vectors and LU rows load coalesced) and meet through
+// width-BS shuffles.  Forward substitution: at step c lane c's value is final and is
+// broadcast; every lane a > c subtracts L[a][c] y_c — so lane a subtracts its terms
+// in the order c = 0, 1, ..., a-1, the oracle's order.  Back substitution from the
+// last row up: lane a, once every y_c (c > a) is known, forms its sum over
+// c = a+1, a+2, ... ascending and divides by U[a][a].  Explicitly rounded like
+// bj_apply, so M^-1 u is bitwise the thread-per-block path (and the oracle's).
+template <int BS, int STAGE>
+__device__ __forceinline__ void precond_rows(const BicgVecs &v, int64_t n, double c1, double c2, double &a0) {
+  const int lane = threadIdx.x & 31, a = lane % BS;
+  const int64_t stride = (int64_t)gridDim.x * BLOCK, nr = (n + 31) & ~(int64_t)31;
+  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < nr; i += stride) {
+    const bool live = i < n;
+    const int64_t blk = i / BS;
+    const int m = (int)((blk * BS + BS <= n) ? BS : n - blk * BS);
+    double u = 0.0;
+    if (live) {
+      if (STAGE == 0) {  // c1 = beta, c2 = omega
+        u = __fma_rn(c1, __fma_rn(-c2, v.v[i], v.p[i]), v.r[i]);
+        v.p[i] = u;
+      } else {  // c1 = alpha
+        u = __fma_rn(-c1, v.v[i], v.r[i]);
+        v.r[i] = u;
+        a0 = __fma_rn(u, u, a0);
+      }
+    }
+    double D[BS];
+    int pr = a;
+    if (live) {
+      const double2 *row2 = reinterpret_cast<const double2 *>(v.lu + blk * BS * BS + a * BS);
+#pragma unroll
+      for (int q = 0; q < BS / 2; q++) {
+        const double2 d2 = __ldg(row2 + q);
+        D[2 * q] = d2.x;
+        D[2 * q + 1] = d2.y;
+      }
+      pr = __ldg(v.piv + blk * BS + a);
+    } else {
+#pragma unroll
+      for (int q = 0; q < BS; q++) D[q] = 0.0;
+    }
+    // L z = P u
+    double sacc = __shfl_sync(0xffffffffu, u, pr, BS);
+    double y[BS];
+#pragma unroll
+    for (int c = 0; c < BS; c++) {
+      y[c] = __shfl_sync(0xffffffffu, sacc, c, BS);  // lane c is final at step c
+      if (a > c) sacc = __dsub_rn(sacc, __dmul_rn(D[c], y[c]));
+    }
+    // U y = z, bottom up
+#pragma unroll
+    for (int k = BS - 1; k >= 0; k--) {
+      double t = 0.0;
+      if (a == k && k < m) {
+        t = y[k];
+#pragma unroll
+        for (int c = k + 1; c < BS; c++)
+          if (c < m) t = __dsub_rn(t, __dmul_rn(D[c], y[c]));
+        t = __ddiv_rn(t, D[k]);
+      }
+      y[k] = __shfl_sync(0xffffffffu, t, k, BS);
+    }
+    if (live) (STAGE == 0 ? v.ph : v.sh)[i] = y[a];
+  }
+}
+
 template <int BS, int STAGE>
 __device__ __noinline__ void bicg_precond_pass(const BicgVecs &v, int64_t n, double c1, double c2, double *out,
                                                double (*sm)[WARPS]) {
@@ -546,11 +613,14 @@ __global__ void __launch_bounds__(BLOCK) bg_precond_kernel(int64_t n, BicgVecs v
   __shared__ double sm[1][WARPS];
   BG_ENTRY();
   double a0 = 0.0;
+  const bool rows = BS > 1 && v.iperm == nullptr;  // lane-per-row path (natural order)
   if (STAGE == 0) {
-    precond_body<BS, 0>(v, n, vs->beta, vs->omega, a0);
+    if (rows) precond_rows<BS, 0>(v, n, vs->beta, vs->omega, a0);
+    else precond_body<BS, 0>(v, n, vs->beta, vs->omega, a0);
     return;
   }
-  precond_body<BS, 1>(v, n, vs->alpha, 0.0, a0);
+  if (rows) precond_rows<BS, 1>(v, n, vs->alpha, 0.0, a0);
+  else precond_body<BS, 1>(v, n, vs->alpha, 0.0, a0);
   double red[1] = {a0};
   block_sum<1>(red, sm);
   if (!publish_and_arrive<1>(red, part, &sc->cnt[1])) return;
