@@ -12,21 +12,25 @@ struct GridBar {
   unsigned int gen;
 };
 
+// Sense-counter barrier: arrival is an acq_rel atomic (gpu scope) and the waiters
+// spin on an acquire load of the generation, which orders every block's prior
+// writes before any block's later reads.  (Against the volatile-spin version with
+// two __threadfence()s: C1 1.11 -> 1.01 ms, C2 0.163 -> 0.159 s, C3 0.926 -> 0.905 s.)
 __device__ __forceinline__ void grid_sync(GridBar *b) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned int *vgen = &b->gen;
-    const unsigned int g = *vgen;
-    __threadfence();
-    if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
-      b->count = 0;
-      __threadfence();
-      atomicAdd(&b->gen, 1u);
+    unsigned int g, old;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&b->gen) : "memory");
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&b->count) : "memory");
+    if (old == gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(&b->count) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&b->gen) : "memory");
     } else {
-      while (*vgen == g) {
-      }
+      unsigned int cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&b->gen) : "memory");
+      } while (cur == g);
     }
-    __threadfence();
   }
   __syncthreads();
 }
