@@ -332,3 +332,50 @@ def halo_recv_plan(ghosts, bounds):
                                    need.ctypes.data_as(C.c_void_p), off.ctypes.data_as(C.c_void_p)),
           "pcg_halo_recv_plan")
     return need, off
+
+
+# ---------------------------------------------------------------- the C ABI's names
+# (include/pcg.h, include/fem_gen.h): thin aliases of the methods above, so a caller
+# can follow the header entry point by entry point.  Argument marshalling only.
+def csr_create(row_ptr, col, val, fmt: str = "auto", stream=None) -> Matrix:
+    """include/pcg.h csr_create: validate, narrow and upload a CSR matrix (host or device tensors)."""
+    return Matrix.from_csr(row_ptr, col, val, fmt=fmt, stream=stream)
+
+
+def csr_create_dist(comm: Comm, n_global: int, row_begin: int, row_end: int, row_ptr_local, col_global, val,
+                    fmt: str = "auto", stream=None) -> Matrix:
+    """include/pcg.h csr_create_dist: this rank's rows [row_begin, row_end) with global column ids."""
+    return Matrix.from_csr_dist(comm, n_global, row_begin, row_end, row_ptr_local, col_global, val, fmt=fmt,
+                                stream=stream)
+
+
+def csr_destroy(A: Matrix) -> None:
+    """include/pcg.h csr_destroy."""
+    A.close()
+
+
+def pcg_spmv(A: Matrix, x, y=None, stream=None):
+    """include/pcg.h pcg_spmv: y = A x."""
+    return A.spmv(x, y, stream=stream)
+
+
+def pcg_solve(A: Matrix, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None):
+    """include/pcg.h pcg_solve: Jacobi-PCG from x0; returns (x, info)."""
+    return A.solve(b, x0=x0, tol=tol, max_iter=max_iter, stream=stream)
+
+
+def pcg_solve_multi(A: Matrix, B, X0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None):
+    """include/pcg.h pcg_solve_multi: k independent Jacobi-PCG solves; returns (X, infos)."""
+    return A.solve_multi(B, X0=X0, tol=tol, max_iter=max_iter, stream=stream)
+
+
+def pcg_bicgstab(A: Matrix, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, block_size: int = 1,
+                 stream=None):
+    """include/pcg.h pcg_bicgstab: right-preconditioned BiCGSTAB with (Block-)Jacobi."""
+    return A.bicgstab(b, x0=x0, tol=tol, max_iter=max_iter, block=block_size, stream=stream)
+
+
+pcg_partition_rows = partition_rows
+
+__all__ += ["csr_create", "csr_create_dist", "csr_destroy", "pcg_spmv", "pcg_solve", "pcg_solve_multi",
+            "pcg_bicgstab", "pcg_partition_rows"]

@@ -76,3 +76,11 @@ def test_fem_problem_size_closed_forms(pcg, name, c):
             "C4": (2048383, 14241907), "C5": (133432831, 932463091)}
     if c == O.configs()[name]["c"]:
         assert (n, nnz) == want[name]
+
+
+def test_python_binding_has_the_abi_names():
+    """The binding exposes the C ABI's entry points under their header names (no GPU needed)."""
+    import paper_2201_05413_b200 as pcg
+    for name in ("csr_create", "csr_create_dist", "csr_destroy", "pcg_spmv", "pcg_solve", "pcg_solve_multi",
+                 "pcg_bicgstab", "pcg_partition_rows", "coo_to_csr"):
+        assert callable(getattr(pcg, name)), name
