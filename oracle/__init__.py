@@ -83,6 +83,8 @@ def lib():
         L.orc_halo.restype = C.c_int64
         L.orc_coo_to_csr.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_pcg_pipelined.argtypes = [P(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]
         L.orc_halo.argtypes = [P(_Csr), C.c_int64, C.c_int64, C.c_void_p, C.c_int64]
         L.orc_fd_identity_rows_nnz.restype = C.c_int64
         L.orc_fd_identity_rows_nnz.argtypes = [C.c_int64]
@@ -287,6 +289,16 @@ def coo_to_csr(n_rows: int, n_cols: int, row, col, val):
     if st != OK:
         raise RuntimeError(f"orc_coo_to_csr: {st}")
     return rp, co[:u.value].copy(), vo[:u.value].copy()
+
+
+def pcg_pipelined(A: Csr, b, x0=None, tol=1e-10, max_iter=50000) -> PcgResult:
+    """SURVEY §8(f) N3 (reading R4): preconditioned pipelined CG, one reduction per iteration."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(A.n) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+    it, rr, rt = C.c_int64(0), C.c_double(0), C.c_double(0)
+    Ac = A._c()
+    st = lib().orc_pcg_pipelined(C.byref(Ac), _ptr(b), _ptr(x), tol, max_iter, C.byref(it), C.byref(rr), C.byref(rt))
+    return PcgResult(x=x, iterations=it.value, relres_rec=rr.value, relres_true=rt.value, status=st)
 
 
 def pcg_multi(A: Csr, B, X0=None, tol=1e-10, max_iter=50000):

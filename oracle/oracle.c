@@ -980,3 +980,98 @@ int orc_coo_to_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t *r
   free(ord);
   return ORC_OK;
 }
+
+/* ---------------------------------------------------------------- pipelined PCG
+ * SURVEY §8(f) N3, reading R4: Ghysels & Vanroose (2014) Alg. 3, restated
+ * with M^-1 = diag(A)^-1:
+ *   (re)start: r = b - A x;  stop test on ||r||;  u = M^-1 r;  w = A u
+ *   loop:  gamma = r.u;  delta = w.u;  rr = r.r           (the one reduction)
+ *          stop test: sqrt(rr) <= tol ||b||  -> exit check (true residual, §8(c).8)
+ *          m = M^-1 w;  n = A m
+ *          first step after a (re)start: beta = 0, alpha = gamma / delta
+ *          else beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old)
+ *          z = n + beta z;  q = m + beta q;  s = w + beta s;  p = u + beta p
+ *          x += alpha p;  r -= alpha s;  u -= alpha q;  w -= alpha z
+ * In exact arithmetic the iterates are standard PCG's; iterations = SpMVs on m. */
+int orc_pcg_pipelined(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter, int64_t *iters,
+                      double *relres_rec, double *relres_true) {
+  int64_t n = A->n;
+  *iters = 0;
+  *relres_rec = 0.0;
+  *relres_true = 0.0;
+  if (n < 0 || !(tol > 0.0) || max_iter < 1) return ORC_ERR_INVALID_ARG;
+  const size_t sz = sizeof(double) * (n > 0 ? n : 1);
+  double *dinv = malloc(sz), *r = malloc(sz), *u = malloc(sz), *w = malloc(sz), *m = malloc(sz), *nv = malloc(sz);
+  double *z = calloc(n > 0 ? n : 1, sizeof(double)), *q = calloc(n > 0 ? n : 1, sizeof(double));
+  double *s = calloc(n > 0 ? n : 1, sizeof(double)), *p = calloc(n > 0 ? n : 1, sizeof(double));
+  int st = ORC_OK;
+  if (!dinv || !r || !u || !w || !m || !nv || !z || !q || !s || !p) { st = ORC_ERR_OOM; goto out; }
+  for (int64_t i = 0; i < n; i++) {
+    int64_t kd = csr_find(A, i, i);
+    double d = kd >= 0 ? A->val[kd] : 0.0;
+    if (d == 0.0) { st = ORC_ERR_ZERO_DIAGONAL; goto out; }
+    if (d < 0.0) { st = ORC_ERR_NOT_SPD; goto out; }
+    dinv[i] = 1.0 / d;
+  }
+  double nb = sqrt(dot(n, b, b));
+  if (nb == 0.0) {
+    for (int64_t i = 0; i < n; i++) x[i] = 0.0;
+    goto out;
+  }
+  int64_t k = 0;
+  int restart = 1, first = 1;
+  double gamma_old = 0.0, alpha_old = 0.0;
+  for (;;) {
+    if (restart) {
+      orc_spmv(A, x, nv);
+      for (int64_t i = 0; i < n; i++) r[i] = b[i] - nv[i];
+      double rr0 = sqrt(dot(n, r, r));
+      *relres_rec = rr0 / nb;
+      if (rr0 <= tol * nb) break; /* -> exit check */
+      for (int64_t i = 0; i < n; i++) u[i] = dinv[i] * r[i];
+      orc_spmv(A, u, w);
+      restart = 0;
+      first = 1;
+    }
+    const double gamma = dot(n, r, u), delta = dot(n, w, u), rr = sqrt(dot(n, r, r));
+    *relres_rec = rr / nb;
+    if (!first && rr <= tol * nb) {
+      const double t = true_relres(A, b, x, nb, nv);
+      if (t <= tol) break;
+      restart = 1;
+      continue;
+    }
+    if (k >= max_iter) { st = ORC_NOT_CONVERGED; break; }
+    for (int64_t i = 0; i < n; i++) m[i] = dinv[i] * w[i];
+    orc_spmv(A, m, nv);
+    double alpha, beta;
+    if (first) {
+      beta = 0.0;
+      alpha = gamma / delta;
+    } else {
+      beta = gamma / gamma_old;
+      alpha = gamma / (delta - beta * gamma / alpha_old);
+    }
+    if (!(alpha > 0.0)) { st = ORC_ERR_NOT_SPD; break; }
+    for (int64_t i = 0; i < n; i++) {
+      z[i] = nv[i] + beta * z[i];
+      q[i] = m[i] + beta * q[i];
+      s[i] = w[i] + beta * s[i];
+      p[i] = u[i] + beta * p[i];
+      x[i] = x[i] + alpha * p[i];
+      r[i] = r[i] - alpha * s[i];
+      u[i] = u[i] - alpha * q[i];
+      w[i] = w[i] - alpha * z[i];
+    }
+    gamma_old = gamma;
+    alpha_old = alpha;
+    first = 0;
+    k++;
+  }
+  *iters = k;
+  *relres_true = true_relres(A, b, x, nb, nv);
+  if (st == ORC_OK && !(*relres_true <= tol)) st = ORC_NOT_CONVERGED;
+out:
+  free(dinv); free(r); free(u); free(w); free(m); free(nv); free(z); free(q); free(s); free(p);
+  return st;
+}

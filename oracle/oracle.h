@@ -112,6 +112,14 @@ int orc_fd_cube(int64_t N, int fkind, orc_csr *A, double *b /* N^3 */);
 int orc_bicgstab(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter, int64_t bs,
                  int64_t *iters, double *relres_rec, double *relres_true);
 
+/* SURVEY §8(f) N3 (reading R4): preconditioned pipelined CG (Ghysels &
+ * Vanroose 2014, "Hiding global synchronization latency in the preconditioned
+ * Conjugate Gradient algorithm", Alg. 3) with the Jacobi preconditioner: one
+ * reduction phase (r.u, w.u, r.r) per iteration, the SpMV on m = M^-1 w overlapping
+ * it.  Same stopping rule, exit check and replacement as orc_pcg (§8(c).8). */
+int orc_pcg_pipelined(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter, int64_t *iters,
+                      double *relres_rec, double *relres_true);
+
 /* SURVEY §8(f) N1 / SPEC coo_to_csr: COO triplets -> CSR.  Entries ordered
  * by (row, col); the values of equal (row, col) entries are summed left to right in
  * INPUT order starting from 0.0, i.e. A[r][c] = sum over the entries (r, c, v) in order

@@ -716,3 +716,55 @@ def test_coo_to_csr_of_element_triplets_is_the_assembly(fam, c, jit):
     rp, co, vo = O.coo_to_csr(m.n_nodes, m.n_nodes, rows, cols, vals)
     assert np.array_equal(rp, K.row_ptr) and np.array_equal(co, K.col)
     assert np.array_equal(vo, K.val)
+
+
+# ---------------------------------------------------------------- pipelined PCG (reading R4)
+def _csr_from_dense(D):
+    n = D.shape[0]
+    rp, col, val = [0], [], []
+    for i in range(n):
+        for j in range(n):
+            if D[i, j] != 0.0 or i == j:
+                col.append(j)
+                val.append(D[i, j])
+        rp.append(len(col))
+    return O.Csr(n, rp, col, val)
+
+
+def test_pipelined_identity_and_diagonal_one_step():
+    b = np.random.default_rng(5).uniform(-1, 1, 40)
+    r = O.pcg_pipelined(_csr_from_dense(np.eye(40)), b, tol=1e-14)
+    assert r.status == O.OK and r.iterations == 1 and np.array_equal(r.x, b)
+    d = np.random.default_rng(6).uniform(0.5, 3.0, 40)
+    r = O.pcg_pipelined(_csr_from_dense(np.diag(d)), b, tol=1e-12)
+    assert r.status == O.OK and r.iterations == 1 and np.allclose(r.x, b / d, rtol=4e-16, atol=0)
+
+
+@pytest.mark.parametrize("name,c", [("C1", 8), ("C3", 4), ("C5", 4)])
+def test_pipelined_equals_pcg_in_exact_arithmetic(name, c):
+    """Ghysels-Vanroose's recurrences are PCG's rewritten: after k steps the iterate is
+    PCG's k-th iterate, up to rounding (checked for k = 1..8)."""
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    for k in range(1, 9):
+        xc = O.pcg(A, b, tol=1e-15, max_iter=k).x
+        xp = O.pcg_pipelined(A, b, tol=1e-15, max_iter=k).x
+        assert np.linalg.norm(xp - xc) <= 1e-12 * np.linalg.norm(xc), k
+
+
+@pytest.mark.parametrize("name,c", [("C1", 32), ("C2", 32), ("C4", 16), ("C6", 8)])
+def test_pipelined_converges_like_pcg(name, c):
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    tol = O.configs()[name]["tol"]
+    rc = O.pcg(A, b, tol=tol)
+    rp = O.pcg_pipelined(A, b, tol=tol)
+    assert rp.status == O.OK and rp.relres_true <= tol
+    assert abs(rp.iterations - rc.iterations) <= max(2, 0.03 * rc.iterations), (rp.iterations, rc.iterations)
+    assert np.linalg.norm(rp.x - rc.x) <= 1e-8 * np.linalg.norm(rc.x)
+
+
+def test_pipelined_max_iter():
+    P = O.build_problem("C1", c=16, k=1)
+    r = O.pcg_pipelined(P["A"], P["B"][:, 0], tol=1e-12, max_iter=5)
+    assert r.status == O.NOT_CONVERGED and r.iterations == 5
