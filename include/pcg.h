@@ -149,6 +149,22 @@ pcg_status pcg_solve_multi(pcg_matrix_t A, int32_t k, const double *B, int64_t l
 pcg_status pcg_bicgstab(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
                         int32_t block_size, void *stream, pcg_info *info);
 
+/* Preconditioned pipelined CG (reading R4: Ghysels &
+ * Vanroose 2014, Alg. 3) with the Jacobi preconditioner: the same problem, inputs,
+ * stopping rule (recurrence residual, then the true residual of Eq. relativeError,
+ * P:132-135), exit check and residual replacement as pcg_solve, but ONE reduction
+ * phase per iteration (r.u, w.u, r.r) with the SpMV on m = M^-1 w independent of it —
+ * the latency-reduced variant: one grid barrier per iteration on one GPU, one
+ * allreduce per iteration across GPUs.  Iterates equal PCG's in exact arithmetic;
+ * in floating point the iteration count may differ slightly.
+ * Arguments as pcg_solve (b, x host or device; x in/out; info: iterations = SpMVs
+ * on m, residuals, device time, algorithmic bytes = k (12 nnz + 4(n+1) + 160 n)).
+ * Single-GPU handles only (PCG_ERR_INVALID_ARG for distributed ones).
+ * Errors: PCG_ERR_INVALID_ARG, PCG_NOT_CONVERGED (x holds the last iterate),
+ * PCG_ERR_NOT_SPD (alpha <= 0), PCG_ERR_NONFINITE, PCG_ERR_OOM, PCG_ERR_CUDA. */
+pcg_status pcg_solve_pipelined(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
+                               void *stream, pcg_info *info);
+
 /* ---------------------------------------------------------------- multi-GPU (§8(a) a8, §8(e)) */
 /* Row partition rule: bounds[0] = 0, bounds[G] = n,
  * bounds[g] = lower_bound(row_ptr, floor(g*nnz/G)).  Host pointers. */

@@ -992,7 +992,9 @@ int orc_coo_to_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t *r
  *          else beta = gamma / gamma_old, alpha = gamma / (delta - beta gamma / alpha_old)
  *          z = n + beta z;  q = m + beta q;  s = w + beta s;  p = u + beta p
  *          x += alpha p;  r -= alpha s;  u -= alpha q;  w -= alpha z
- * In exact arithmetic the iterates are standard PCG's; iterations = SpMVs on m. */
+ * In exact arithmetic the iterates are standard PCG's; iterations = SpMVs on m.
+ * alpha <= 0 on the first step after a (re)start: not SPD; on a later step the
+ * recurrences have drifted (pipelined CG's known instability): restart from x. */
 int orc_pcg_pipelined(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter, int64_t *iters,
                       double *relres_rec, double *relres_true) {
   int64_t n = A->n;
@@ -1052,7 +1054,14 @@ int orc_pcg_pipelined(const orc_csr *A, const double *b, double *x, double tol, 
       beta = gamma / gamma_old;
       alpha = gamma / (delta - beta * gamma / alpha_old);
     }
-    if (!(alpha > 0.0)) { st = ORC_ERR_NOT_SPD; break; }
+    if (!(alpha > 0.0)) {
+      /* reading R4: on the first step after a (re)start alpha = r.M^-1 r / (u.A u) <= 0
+       * means A is not SPD; later, the recurrences (w = A u, z = A q, s = A p kept by
+       * updates) have drifted — restart from the current x (residual replacement) */
+      if (first) { st = ORC_ERR_NOT_SPD; break; }
+      restart = 1;
+      continue;
+    }
     for (int64_t i = 0; i < n; i++) {
       z[i] = nv[i] + beta * z[i];
       q[i] = m[i] + beta * q[i];

@@ -140,6 +140,30 @@ class Matrix:
         d["status_name"] = _lib.STATUS[st]
         return x, d
 
+    def solve_pipelined(self, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None,
+                        raise_on=("error",), out=None):
+        """Pipelined Jacobi-PCG (pcg_solve_pipelined): one reduction per
+        iteration.  Same conventions as solve()."""
+        torch = _torch()
+        b = _as_tensor(b, torch.float64)
+        if out is not None:
+            x = out
+        else:
+            x = torch.zeros_like(b) if x0 is None else _as_tensor(x0, torch.float64).clone()
+        if b.device.type == "cpu":
+            if not b.is_pinned():
+                b = b.pin_memory()
+            if not x.is_pinned():
+                x = x.pin_memory()
+        info = _lib.PcgInfo()
+        st = lib().pcg_solve_pipelined(self._h, _ptr(b), _ptr(x), float(tol), int(max_iter), _stream_ptr(stream),
+                                       C.byref(info))
+        if st not in (PCG_OK, PCG_NOT_CONVERGED) or ("not_converged" in raise_on and st == PCG_NOT_CONVERGED):
+            raise PcgError(st, "pcg_solve_pipelined")
+        d = info.as_dict()
+        d["status_name"] = _lib.STATUS[st]
+        return x, d
+
     def bicgstab(self, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, block: int = 1, stream=None,
                  raise_on=("error",), out=None):
         """Right-preconditioned BiCGSTAB with (Block-)Jacobi (pcg_bicgstab).
@@ -369,6 +393,11 @@ def pcg_solve_multi(A: Matrix, B, X0=None, tol: float = 1e-10, max_iter: int = 5
     return A.solve_multi(B, X0=X0, tol=tol, max_iter=max_iter, stream=stream)
 
 
+def pcg_solve_pipelined(A: Matrix, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None):
+    """include/pcg.h pcg_solve_pipelined: pipelined Jacobi-PCG (one reduction per iteration)."""
+    return A.solve_pipelined(b, x0=x0, tol=tol, max_iter=max_iter, stream=stream)
+
+
 def pcg_bicgstab(A: Matrix, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, block_size: int = 1,
                  stream=None):
     """include/pcg.h pcg_bicgstab: right-preconditioned BiCGSTAB with (Block-)Jacobi."""
@@ -378,4 +407,4 @@ def pcg_bicgstab(A: Matrix, b, x0=None, tol: float = 1e-10, max_iter: int = 5000
 pcg_partition_rows = partition_rows
 
 __all__ += ["csr_create", "csr_create_dist", "csr_destroy", "pcg_spmv", "pcg_solve", "pcg_solve_multi",
-            "pcg_bicgstab", "pcg_partition_rows"]
+            "pcg_solve_pipelined", "pcg_bicgstab", "pcg_partition_rows"]

@@ -98,6 +98,7 @@ def lib():
         "pcg_profile_kernels": [vp, vp, i32, vp, vp, P(i32)],
         "pcg_profile_multi": [vp, i32, vp, i64, i32, vp, vp, P(i32)],
         "pcg_bicgstab": [vp, vp, vp, C.c_double, i64, i32, vp, P(PcgInfo)],
+        "pcg_solve_pipelined": [vp, vp, vp, C.c_double, i64, vp, P(PcgInfo)],
         "fd_cube_count": [i64, i64, i64, vp, P(i64), vp],
         "fd_cube_assemble": [i64, i32, i64, i64, vp, vp, vp, vp, vp],
         "coo_to_csr": [i64, i64, i64, vp, vp, vp, vp, vp, vp, P(i64), vp],

@@ -57,6 +57,10 @@ struct SolveWork {
   void *bstate = nullptr, *bbar = nullptr;
   double *bminv = nullptr;
   int bminv_bs = 0, bgrid = 0, bgrid_bs = 0;
+  // pipelined PCG (pipelined.cu): x r u w m0 m1 z q s p, state, barrier, grid
+  double *pv = nullptr;
+  void *pstate = nullptr, *ppbar = nullptr;
+  int ppgrid = 0;
   // BiCGSTAB graph schedule: device scalars, loop graph (per block size)
   void *bgsc = nullptr;
   cudaGraphExec_t bg_exec = nullptr;
