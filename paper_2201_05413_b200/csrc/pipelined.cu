@@ -86,8 +86,10 @@ __device__ __forceinline__ void pipe_publish(const double (&a)[3], double *part,
     for (int i = 0; i < NV; i++) part[(size_t)i * gridDim.x + blockIdx.x] = red[i];
 }
 
-template <int FMT, int L>
-__global__ void __launch_bounds__(BLOCK, 2) pipe_kernel(SellView S_, CsrView C_, PipeVecs v_, PipeState *st,
+// MINB: resident blocks per SM the kernel is compiled for — 1 (no spills: the
+// latency-bound small systems) or 3 (more warps in flight: the larger ones)
+template <int FMT, int L, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB) pipe_kernel(SellView S_, CsrView C_, PipeVecs v_, PipeState *st,
                                                         double *part, GridBar *bar) {
   __shared__ double sm[3][WARPS];
   __shared__ double s_tot[3];
@@ -263,16 +265,23 @@ __global__ void __launch_bounds__(BLOCK, 2) pipe_kernel(SellView S_, CsrView C_,
 }
 
 // ---------------------------------------------------------------- host side
-static void *pipe_fn(int fmt, int lanes) {
-  if (fmt == PCG_FORMAT_SELL) return (void *)pipe_kernel<PCG_FORMAT_SELL, 1>;
+template <int MINB>
+static void *pipe_fn_b(int fmt, int lanes) {
+  if (fmt == PCG_FORMAT_SELL) return (void *)pipe_kernel<PCG_FORMAT_SELL, 1, MINB>;
   switch (lanes) {
-    case 1: return (void *)pipe_kernel<PCG_FORMAT_CSR, 1>;
-    case 2: return (void *)pipe_kernel<PCG_FORMAT_CSR, 2>;
-    case 4: return (void *)pipe_kernel<PCG_FORMAT_CSR, 4>;
-    case 8: return (void *)pipe_kernel<PCG_FORMAT_CSR, 8>;
-    case 16: return (void *)pipe_kernel<PCG_FORMAT_CSR, 16>;
-    default: return (void *)pipe_kernel<PCG_FORMAT_CSR, 32>;
+    case 1: return (void *)pipe_kernel<PCG_FORMAT_CSR, 1, MINB>;
+    case 2: return (void *)pipe_kernel<PCG_FORMAT_CSR, 2, MINB>;
+    case 4: return (void *)pipe_kernel<PCG_FORMAT_CSR, 4, MINB>;
+    case 8: return (void *)pipe_kernel<PCG_FORMAT_CSR, 8, MINB>;
+    case 16: return (void *)pipe_kernel<PCG_FORMAT_CSR, 16, MINB>;
+    default: return (void *)pipe_kernel<PCG_FORMAT_CSR, 32, MINB>;
   }
+}
+
+// measured (C1 / C4 / C6 solve seconds): 1 block/SM 0.54 ms / 0.105 / 0.142, 2 blocks
+// 0.70 ms / 0.083 / 0.127, 3 blocks 0.72 ms / 0.080 / 0.124
+static void *pipe_fn(int fmt, int lanes, int64_t n) {
+  return n < (int64_t(1) << 18) ? pipe_fn_b<1>(fmt, lanes) : pipe_fn_b<3>(fmt, lanes);
 }
 
 static pcg_status pipe_impl(pcg_matrix *A, const double *b, double *x, double tol, int64_t max_iter, cudaStream_t st,
@@ -325,7 +334,7 @@ static pcg_status pipe_impl(pcg_matrix *A, const double *b, double *x, double to
   hs.max_iter = max_iter;
   PipeState *dst = (PipeState *)w.pstate;
   PCG_CUDA(cudaMemcpyAsync(dst, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
-  void *fn = pipe_fn(A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format, A->csr_lanes);
+  void *fn = pipe_fn(A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format, A->csr_lanes, n);
   if (w.ppgrid == 0) {
     int nbk = 0;
     PCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbk, fn, BLOCK, 0));
