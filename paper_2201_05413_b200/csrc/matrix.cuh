@@ -130,6 +130,7 @@ namespace pcgb {
 pcg_status ensure_work(pcg_matrix *A);
 pcg_status ensure_multi_work(pcg_matrix *A, int k);
 pcg_status build_sell(pcg_matrix *A, cudaStream_t st);
+int persist_schedule(const pcg_matrix *A);
 bool persist_wanted(const pcg_matrix *A);
 pcg_status persist_launch(pcg_matrix *A, Vecs v, cudaStream_t st);
 int sigma_window();

@@ -22,7 +22,10 @@
 
 namespace pcgb {
 
-template <int FMT, int L>
+// SCHED 3: K1a | K1b | K2, three barriers per iteration (96 n bytes); SCHED 2: K1 (SpMV
+// with p = z + beta p recomputed at gather time, x += alpha_prev p_old) | K2, two
+// barriers (88 n bytes, twice the gathers).
+template <int FMT, int L, int SCHED>
 __global__ void __launch_bounds__(BLOCK, 3) pcg_persist_kernel(SellView S, CsrView C, Vecs v, Scalars *sc, double *part,
                                                             GridBar *bar) {
   __shared__ double sm[2][WARPS];
@@ -35,12 +38,38 @@ __global__ void __launch_bounds__(BLOCK, 3) pcg_persist_kernel(SellView S, CsrVi
   const long long max_iter = sc->max_iter;
   int done = sc->done;
   double sigma = sc->sigma, gamma = sc->gamma, relres_rec = sc->relres_rec;
-  double *__restrict__ p = v.p0;
+  double *__restrict__ p = v.p0;  // SCHED 3 (SCHED 2 tracks p[par])
   double *__restrict__ q = v.q;
   const int64_t npair = n >> 1;
   const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
   double *part_s = part, *part_rz = part + gridDim.x;  // sigma | (rho', gamma)
+  int par = sc->parity;  // SCHED 2: p[par] is the current direction
   while (done == DONE_RUNNING) {
+    if (SCHED == 2) {
+      // ---- K1: p_new = z + beta p_old ; q = A p_new ; sigma ; x += alpha_prev p_old
+      double acc = 0.0;
+      const double *__restrict__ pold = par ? v.p1 : v.p0;
+      double *__restrict__ pnew = par ? v.p0 : v.p1;
+      if (FMT == PCG_FORMAT_SELL) {
+        k1_sell_rows<8>(S, beta, alpha, pold, pnew, v.z, v.x, q, acc);
+      } else {
+        auto gather = [&](int j) { return __fma_rn(beta, __ldg(pold + j), __ldg(v.z + j)); };
+        auto epi = [&](int64_t i, double s) {
+          const double po = pold[i];
+          const double pi = __fma_rn(beta, po, v.z[i]);
+          pnew[i] = pi;
+          q[i] = s;
+          v.x[i] = __fma_rn(alpha, po, v.x[i]);
+          acc = __fma_rn(pi, s, acc);
+        };
+        csr_rows<L>(C, gather, epi);
+      }
+      double red[1] = {acc};
+      block_sum<1>(red, sm);
+      if (threadIdx.x == 0) part_s[blockIdx.x] = red[0];
+      par ^= 1;
+      p = pnew;
+    } else {
     // ---- K1a: p = z + beta p ; x += alpha_prev p_old
     {
       double2 *__restrict__ p2 = reinterpret_cast<double2 *>(p);
@@ -74,6 +103,7 @@ __global__ void __launch_bounds__(BLOCK, 3) pcg_persist_kernel(SellView S, CsrVi
       double red[1] = {acc};
       block_sum<1>(red, sm);
       if (threadIdx.x == 0) part_s[blockIdx.x] = red[0];
+    }
     }
     grid_sync(bar);
     {
@@ -149,22 +179,34 @@ __global__ void __launch_bounds__(BLOCK, 3) pcg_persist_kernel(SellView S, CsrVi
     sc->relres_rec = relres_rec;
     sc->k = k;
     sc->done = done;
-    sc->parity = 0;
+    sc->parity = SCHED == 2 ? par : 0;
     sc->graph_launches += 1;
   }
 }
 
 // ---------------------------------------------------------------- host side
-static void *persist_fn(int fmt, int lanes) {
-  if (fmt == PCG_FORMAT_SELL) return (void *)pcg_persist_kernel<PCG_FORMAT_SELL, 1>;
+template <int SCHED>
+static void *persist_fn_s(int fmt, int lanes) {
+  if (fmt == PCG_FORMAT_SELL) return (void *)pcg_persist_kernel<PCG_FORMAT_SELL, 1, SCHED>;
   switch (lanes) {
-    case 1: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 1>;
-    case 2: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 2>;
-    case 4: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 4>;
-    case 8: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 8>;
-    case 16: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 16>;
-    default: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 32>;
+    case 1: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 1, SCHED>;
+    case 2: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 2, SCHED>;
+    case 4: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 4, SCHED>;
+    case 8: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 8, SCHED>;
+    case 16: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 16, SCHED>;
+    default: return (void *)pcg_persist_kernel<PCG_FORMAT_CSR, 32, SCHED>;
   }
+}
+
+static void *persist_fn(int fmt, int lanes, int sched) {
+  return sched == 2 ? persist_fn_s<2>(fmt, lanes) : persist_fn_s<3>(fmt, lanes);
+}
+
+// Schedule inside the persistent kernel: 2 passes (two barriers, twice the gathers) for
+// the smallest, barrier-bound systems, else 3 (measured: C1 0.85 vs 1.00 ms; C2 0.182 vs
+// 0.160 s, C4 0.044 vs 0.036 s, C3 1.20 vs 0.90 s); PCG_SCHEDULE forces either.
+int persist_schedule(const pcg_matrix *A) {
+  return getenv("PCG_SCHEDULE") ? A->schedule : (A->n < (int64_t(1) << 16) ? 2 : 3);
 }
 
 // Whether the handle solves with the persistent kernel: one GPU, SELL or CSR, and a
@@ -179,7 +221,7 @@ bool persist_wanted(const pcg_matrix *A) {
 
 pcg_status persist_launch(pcg_matrix *A, Vecs v, cudaStream_t st) {
   SolveWork &w = A->work;
-  void *fn = persist_fn(A->format, A->csr_lanes);
+  void *fn = persist_fn(A->format, A->csr_lanes, persist_schedule(A));
   if (!w.pbar) {
     PCG_CUDA(cudaMalloc(&w.pbar, sizeof(GridBar)));
     PCG_CUDA(cudaMemset(w.pbar, 0, sizeof(GridBar)));

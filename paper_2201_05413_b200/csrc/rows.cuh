@@ -101,4 +101,75 @@ __device__ __forceinline__ void csr_rows(const CsrView &A, Gather gather, Epi ep
   }
 }
 
+// Schedule-2 K1 row engine (solver.cu k1_kernel, persist.cu): SpMV + p update + x update + sigma.
+// SELL-32 specialisation: one warp per slice, lane = row.  The dependent-load
+// chain per slice is kept to two round trips: the own-row vectors (z_i, p_i, x_i)
+// are requested together with the slice's matrix entries, and the next slice's
+// offsets are fetched one slice ahead (software pipelining).
+template <int CH>
+__device__ __forceinline__ void k1_sell_rows(const SellView &A, double beta, double alpha_prev,
+                                             const double *__restrict__ pold, double *__restrict__ pnew,
+                                             const double *__restrict__ z, double *__restrict__ x,
+                                             double *__restrict__ q, double &acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  int64_t s = w0;
+  int64_t base = 0, next = 0;
+  if (s < A.n_slices) {
+    base = __ldg(A.slice_ptr + s);
+    next = __ldg(A.slice_ptr + s + 1);
+  }
+  for (; s < A.n_slices; s += nw) {
+    const int len = (int)((next - base) >> 5);
+    const int64_t row = s * 32 + lane;
+    const bool ok = row < A.n;
+    // prefetch the following slice's offsets
+    const int64_t s2 = s + nw;
+    int64_t base2 = 0, next2 = 0;
+    if (s2 < A.n_slices) {
+      base2 = __ldg(A.slice_ptr + s2);
+      next2 = __ldg(A.slice_ptr + s2 + 1);
+    }
+    // own-row vectors, issued with the matrix stream
+    double po = 0.0, zi = 0.0, xi = 0.0;
+    if (ok) {
+      po = __ldg(pold + row);
+      zi = __ldg(z + row);
+      xi = __ldcs(x + row);
+    }
+    const double *vp = A.val + base + lane;
+    const int *cp = A.col + base + lane;
+    double sum = 0.0;
+    for (int t = 0; t < len; t += CH) {
+      double a[CH];
+      int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < CH; u++) {
+        if (t + u < len) {
+          a[u] = ld_stream(vp + (size_t)(t + u) * 32);
+          j[u] = ld_stream(cp + (size_t)(t + u) * 32);
+        }
+      }
+      cols_ready(j, A.zero);
+      double g[CH];
+#pragma unroll
+      for (int u = 0; u < CH; u++)
+        if (t + u < len) g[u] = __fma_rn(beta, __ldg(pold + j[u]), __ldg(z + j[u]));
+#pragma unroll
+      for (int u = 0; u < CH; u++)
+        if (t + u < len) sum = __fma_rn(a[u], g[u], sum);
+    }
+    if (ok) {
+      const double pi = __fma_rn(beta, po, zi);
+      __stcs(pnew + row, pi);
+      __stcs(q + row, sum);
+      __stcs(x + row, __fma_rn(alpha_prev, po, xi));
+      acc = __fma_rn(pi, sum, acc);
+    }
+    base = base2;
+    next = next2;
+  }
+}
+
 }  // namespace pcgb
