@@ -159,7 +159,10 @@ pcg_status pcg_bicgstab(pcg_matrix_t A, const double *b, double *x, double tol, 
  * in floating point the iteration count may differ slightly.
  * Arguments as pcg_solve (b, x host or device; x in/out; info: iterations = SpMVs
  * on m, residuals, device time, algorithmic bytes = k (12 nnz + 4(n+1) + 160 n)).
- * Single-GPU handles only (PCG_ERR_INVALID_ARG for distributed ones).
+ * Single-GPU handles: the whole solve as one cooperative kernel (one grid barrier per
+ * iteration).  Distributed handles (csr_create_dist): per iteration one fused kernel,
+ * ONE allreduce of three sums, one halo exchange of m, one finisher; collective call
+ * from every rank, b and x are the rank's rows.
  * Errors: PCG_ERR_INVALID_ARG, PCG_NOT_CONVERGED (x holds the last iterate),
  * PCG_ERR_NOT_SPD (alpha <= 0), PCG_ERR_NONFINITE, PCG_ERR_OOM, PCG_ERR_CUDA. */
 pcg_status pcg_solve_pipelined(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,

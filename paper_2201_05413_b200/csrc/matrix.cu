@@ -519,7 +519,7 @@ void free_work(pcg_matrix *A) {
   if (w.h_sc) cudaFreeHost(w.h_sc);
   if (w.msc) cudaFree(w.msc);
   if (w.pbar) cudaFree(w.pbar);
-  for (void *q : {(void *)w.bv, w.bstate, w.bbar, (void *)w.bminv, w.bgsc, (void *)w.pv, w.pstate, w.ppbar})
+  for (void *q : {(void *)w.bv, w.bstate, w.bbar, (void *)w.bminv, w.bgsc, (void *)w.pv, w.pstate, w.ppbar, w.pdsc})
     if (q) cudaFree(q);
   if (w.h_msc) cudaFreeHost(w.h_msc);
   w = SolveWork();

@@ -59,7 +59,7 @@ struct SolveWork {
   int bminv_bs = 0, bgrid = 0, bgrid_bs = 0;
   // pipelined PCG (pipelined.cu): x r u w m0 m1 z q s p, state, barrier, grid
   double *pv = nullptr;
-  void *pstate = nullptr, *ppbar = nullptr;
+  void *pstate = nullptr, *ppbar = nullptr, *pdsc = nullptr;
   int ppgrid = 0;
   // BiCGSTAB graph schedule: device scalars, loop graph (per block size)
   void *bgsc = nullptr;

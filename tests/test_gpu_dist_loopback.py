@@ -53,10 +53,11 @@ def _worker(rank, world, port, name, c, use_generator, out_q):
         M = pcg.Matrix.from_csr_dist(comm, A.n, r0, r1, rp, col, val)
         st = M.stats()
         x, info = M.solve(bl, tol=1e-10)
+        xp, infop = M.solve_pipelined(bl, tol=1e-10)  # N3: one allreduce per iteration
         xr = np.random.default_rng(100 + rank).standard_normal(r1 - r0)
         y = M.spmv(torch.as_tensor(xr).cuda()).cpu().numpy()
         out_q.put((rank, dict(r0=r0, r1=r1, n_ghost=st["n_ghost"], x=x.cpu().numpy(), info=info, xr=xr, y=y,
-                              b=bl.cpu().numpy())))
+                              b=bl.cpu().numpy(), xp=xp.cpu().numpy(), infop=infop)))
         M.close()
         comm.close()
         dist.destroy_process_group()
@@ -120,6 +121,28 @@ def test_distributed_path_on_one_gpu(world, name, c, gen):
     assert abs(it - r.iterations) <= max(1, 0.02 * r.iterations), (it, r.iterations)
 
 
+@pytest.mark.parametrize("world,name,c", [(2, "C1", None), (3, "C4", 24), (2, "C2", 48)])
+def test_distributed_pipelined_on_one_gpu(world, name, c):
+    """pcg_solve_pipelined on distributed handles (reading R4; one allreduce per
+    iteration): every rank runs the same number of steps; the gathered solution
+    matches the oracle's pipelined and standard PCG solutions; the count stays within
+    max(2, 3 %) of the oracle's pipelined count (no restarts on these systems)."""
+    parts = _run(world, name, c)
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    tol = O.configs()[name]["tol"]
+    ro = O.pcg_pipelined(A, b, tol=tol)
+    rc = O.pcg(A, b, tol=tol)
+    x = np.concatenate([d["xp"] for d in parts])
+    its = {d["infop"]["iterations"] for d in parts}
+    assert len(its) == 1
+    it = its.pop()
+    assert all(d["infop"]["status"] == 0 and d["infop"]["relres_true"] <= tol for d in parts)
+    assert np.linalg.norm(x - ro.x) <= 1e-8 * np.linalg.norm(ro.x)
+    assert np.linalg.norm(x - rc.x) <= 1e-8 * np.linalg.norm(rc.x)
+    assert abs(it - ro.iterations) <= max(2, 0.03 * ro.iterations), (it, ro.iterations)
+
+
 def test_bench_multi_rank_flow_on_one_gpu():
     """bench.py's N>1 path (torchrun, row partition by the device generator, barriers, max
     over ranks, one JSON line from rank 0) with 2 ranks sharing cuda:0 (host-callback
@@ -167,6 +190,12 @@ def test_nccl_single_rank_distributed_handle():
         assert info["status"] == 0 and info["relres_true"] <= 1e-10
         assert np.linalg.norm(x.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-9
         assert abs(info["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
+        # the pipelined solver's distributed schedule through NCCL (one allreduce per step)
+        xp, ip = M.solve_pipelined(torch.as_tensor(b).cuda(), tol=1e-10)
+        rp = O.pcg_pipelined(A, b, tol=1e-10)
+        assert ip["status"] == 0 and ip["relres_true"] <= 1e-10
+        assert np.linalg.norm(xp.cpu().numpy() - rp.x) / np.linalg.norm(rp.x) <= 1e-8
+        assert abs(ip["iterations"] - rp.iterations) <= max(2, 0.03 * rp.iterations)
         M.close()
         comm.close()
     finally:
