@@ -202,6 +202,8 @@ def main():
                     help="callbacks: exchange steps through host callbacks over gloo (validation of the N>1 "
                          "path when ranks share a GPU; not a performance number)")
     ap.add_argument("--block", type=int, default=1, help="Block-Jacobi block size for the CUBE* BiCGSTAB configs")
+    ap.add_argument("--solver", default="pcg", choices=["pcg", "pipelined"],
+                    help="single-RHS solver: Jacobi-PCG (the benchmark) or the pipelined variant (SURVEY N3)")
     args = ap.parse_args()
     if args.config.startswith("CUBE"):
         return run_bicgstab(args)
@@ -279,7 +281,8 @@ def main():
         if multi:
             X, infos = A.solve_multi(bb, tol=tol, max_iter=max_iter, out=out)
             return X, infos
-        x, inf = A.solve(bb, tol=tol, max_iter=max_iter, out=out)
+        solve = A.solve_pipelined if args.solver == "pipelined" else A.solve
+        x, inf = solve(bb, tol=tol, max_iter=max_iter, out=out)
         return x, [inf]
 
     # ---- warm-up
@@ -412,6 +415,16 @@ def main():
                 "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_kind,
                 "traffic": None, "comm": args.comm}
 
+    if args.solver == "pipelined" and not multi:  # the whole pipelined solve is one kernel
+        inf = infos[-1][0]
+        ach = inf["bytes_algorithmic"] / world / max(inf["t_solve_s"], 1e-12) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "peak_source": peak_kind, "traffic": None,
+                "kernel": ("pipe_kernel (whole pipelined solve: per iteration one fused SpMV + 8 vector updates, "
+                           "12 nnz + 4(n+1) + 160 n bytes, one grid barrier)" if world == 1 else
+                           "pd_fused_kernel + one allreduce + halo per iteration (per GPU, 160n schedule)"),
+                "pcg_kernels_for_comparison": roof}
+
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -432,7 +445,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(workload_config(args.config, c, n, nnz, world), iterations=iters,
                            format={1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[stats["format"]], setup_s=round(t_setup, 3),
-                           relres_true=max(i["relres_true"] for i in infos[-1]), k_rhs=kcols),
+                           relres_true=max(i["relres_true"] for i in infos[-1]), k_rhs=kcols,
+                           solver="jacobi-pcg" if args.solver == "pcg" else "pipelined jacobi-pcg (N3)"),
             "throughput": {"cg_iterations_per_s": iters / (ms / 1e3),
                            "effective_GBps": iter_bytes(n, nnz, kcols) * iters / (ms / 1e3) / 1e9,
                            "spmv_GBps": spmv_gbs, "spmv_frac_of_hbm": spmv_gbs / hbm if spmv_gbs else None},
