@@ -505,39 +505,84 @@ def run_bicgstab(args):
                 "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
+    import ctypes as C
+
     import torch
+    import torch.distributed as dist
 
     import paper_2201_05413_b200 as pcg
+    from paper_2201_05413_b200._lib import check, lib
     from paper_2201_05413_b200.problems import fd_cube_build
-    torch.cuda.set_device(0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cb = args.comm == "callbacks"
+    if cb:  # ranks may share a GPU
+        local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    if world > 1:
+        if bs != 1:
+            raise SystemExit("bench.py: distributed BiCGSTAB takes point Jacobi (--block 1)")
+        if cb:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t0 = time.perf_counter()
-    G = fd_cube_build(N)
-    A = pcg.Matrix.from_csr(G["row_ptr"], G["col"], G["val"], fmt=args.fmt)
+    comm = None
+    if world == 1:
+        r0, r1 = 0, n
+        G = fd_cube_build(N)
+        A = pcg.Matrix.from_csr(G["row_ptr"], G["col"], G["val"], fmt=args.fmt)
+        nnz = G["col"].numel()
+    else:  # the partition rule on the full row pointer, then this rank's rows on its GPU
+        rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        tot = C.c_int64()
+        check(lib().fd_cube_count(N, 0, n, C.c_void_p(rp.data_ptr()), C.byref(tot),
+                                  C.c_void_p(torch.cuda.current_stream().cuda_stream)), "fd_cube_count")
+        bounds = pcg.partition_rows(rp.cpu().numpy(), world)
+        del rp
+        nnz = tot.value
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        G = fd_cube_build(N, row_begin=r0, row_end=r1)
+        comm = pcg.Comm.host_callbacks() if cb else pcg.Comm.from_process_group()
+        A = pcg.Matrix.from_csr_dist(comm, n, r0, r1, G["row_ptr"], G["col"], G["val"], fmt=args.fmt)
     b = G["b"].contiguous()
-    nnz = G["col"].numel()
     del G
     torch.cuda.synchronize()
     setup = time.perf_counter() - t0
     for _ in range(args.warmup):
         A.bicgstab(b, tol=tol, block=bs)
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allreduce(v, op):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if cb else "cuda")
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
     def timed(device_inputs):
         bb = b if device_inputs else b.cpu().pin_memory()
         xx = torch.empty_like(bb) if device_inputs else torch.empty(bb.shape, dtype=torch.float64).pin_memory()
-        torch.cuda.synchronize()
+        barrier()
         l0 = pcg.kernel_launches()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         st = torch.cuda.current_stream()
         infos = []
-        with ClockSampler(0) as cs:
+        with ClockSampler(local) as cs:
             e0.record(st)
             for _ in range(args.steps):
                 xx.zero_()
                 x, inf = A.bicgstab(bb, tol=tol, block=bs, out=xx)
                 infos.append(inf)
             e1.record(st)
-            torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / args.steps, infos, pcg.kernel_launches() - l0, cs, x
+            barrier()
+        ms = e0.elapsed_time(e1) / args.steps
+        return allreduce(ms, dist.ReduceOp.MAX if world > 1 else None), infos, pcg.kernel_launches() - l0, cs, x
 
     ms, infos, launches, cs, x = timed(True)
     remeasured = False
@@ -546,33 +591,48 @@ def run_bicgstab(args):
         remeasured = True
     ms_e2e = timed(False)[0]
     inf = infos[-1]
+    A_fmt = A.stats()["format"]
     iters = inf["iterations"]
     hbm, peak_kind = peaks()
-    per_iter_bytes = inf["bytes_algorithmic"] / max(iters, 1)
-    achieved = per_iter_bytes * iters / (inf["t_solve_s"]) / 1e9
+    per_iter_bytes = inf["bytes_algorithmic"] / max(iters, 1)  # this rank's rows
+    achieved = per_iter_bytes * iters / allreduce(inf["t_solve_s"], dist.ReduceOp.MAX if world > 1 else None) / 1e9
     # x_err of Eq. ERROR-METRIC: the discrete solution is x^2 - y^2 exactly
     h = 1.0 / (N - 1)
-    idx = torch.arange(n, device=x.device, dtype=torch.float64)
+    idx = torch.arange(r0, r1, device=x.device, dtype=torch.float64)
     X = torch.remainder(idx, N) * h
     Y = torch.remainder(torch.div(idx, N, rounding_mode="floor"), N) * h
     xg = X * X - Y * Y
-    x_err = float(torch.linalg.norm(x.to(xg.device) - xg) / torch.linalg.norm(xg))
-    line = {"metric": "bicgstab_time_to_solution", "value": ms / 1e3, "unit": "s", "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+    e2 = allreduce(float(torch.sum((x.to(xg.device) - xg) ** 2)), dist.ReduceOp.SUM if world > 1 else None)
+    g2 = allreduce(float(torch.sum(xg ** 2)), dist.ReduceOp.SUM if world > 1 else None)
+    x_err = (e2 / g2) ** 0.5
+    if comm is not None:
+        A.close()
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    line = {"metric": "bicgstab_time_to_solution", "value": ms / 1e3, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: paper Table 1 grid, {N}^3 nodes, identity boundary rows, "
                                    f"b = x^2 - y^2 on the boundary; BiCGSTAB + "
                                    f"{'Jacobi' if bs == 1 else f'Block-Jacobi({bs})'}, eps = 1e-12, x0 = 0",
                        "n": n, "nnz": nnz, "tol": tol, "block": bs, "iterations": iters, "relres_true": inf["relres_true"],
-                       "x_err": x_err, "format": {1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[A.stats()["format"]],
-                       "setup_s": round(setup, 3), "parallelism": "1 GPU",
+                       "x_err": x_err, "format": {1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[A_fmt],
+                       "setup_s": round(setup, 3),
+                       "parallelism": "1 GPU" if world == 1 else f"{world} GPUs, rows partitioned ({args.comm})",
                        "paper_context": "Cube 1 (128^3): BiCGSTAB+BJacobi 17.4 s, 128 it. on 1 Broadwell core; "
                                         "0.34 s on 576 cores (P:211, P:220, eps 1e-12)"},
-            "roofline": {"bound": "hbm", "kernel": "bicg_kernel (whole BiCGSTAB iteration, one cooperative kernel)",
+            "roofline": {"bound": "hbm",
+                         "kernel": ("five kernels per BiCGSTAB iteration (graph schedule; bytes per iteration "
+                                    "over its time)" if world == 1 else
+                                    "five kernels + four allreduces + two halos per iteration (rank 0's rows)"),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "peak_source": peak_kind, "traffic": None, "bytes_per_iteration": per_iter_bytes},
             "cpu_baseline": None,
-            "e2e": {"value": ms_e2e / 1e3, "unit": "s", "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n},
+            "e2e": {"value": ms_e2e / 1e3, "unit": "s", "h2d_bytes_per_step": 16 * (r1 - r0),
+                    "d2h_bytes_per_step": 8 * (r1 - r0)},
             "gpu_launches": launches, "clocks": cs.summary(), "remeasured": remeasured}
     print(json.dumps(line), flush=True)
     return 0

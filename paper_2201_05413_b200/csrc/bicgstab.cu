@@ -52,9 +52,10 @@ __device__ __forceinline__ uint64_t bicg_mix(uint64_t seed, uint64_t idx) {
 }
 
 // r^_i = 2 u(5413, i) - 1 on the ORIGINAL row index (perm maps SELL-C-sigma rows back)
-__global__ void shadow_kernel(int64_t n, const int *__restrict__ perm, double *__restrict__ rh) {
+// (distributed handles: row0 = the rank's first global row)
+__global__ void shadow_kernel(int64_t n, const int *__restrict__ perm, int64_t row0, double *__restrict__ rh) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t g = perm ? (uint64_t)perm[i] : (uint64_t)i;
+    const uint64_t g = perm ? (uint64_t)perm[i] : (uint64_t)(row0 + i);
     const double u = (double)(bicg_mix(5413ULL, g) >> 11) * (1.0 / 9007199254740992.0);
     rh[i] = __dsub_rn(__dmul_rn(2.0, u), 1.0);
   }
@@ -514,6 +515,7 @@ __global__ void __launch_bounds__(BLOCK, 3) bicg_kernel(SellView S_, CsrView C_,
 // graph launches, host-driven, as in the CG solver.
 struct BgScalars {
   double tol, nb, rho, rho_old, alpha, omega, beta, relres_rec, relres_true;
+  double part[3];  // distributed handles: this rank's sums awaiting the allreduce
   long long k, max_iter, restarts;
   int done, half, need_resid, stop;
   unsigned int cnt[4];
@@ -546,25 +548,10 @@ __device__ __forceinline__ void bg_loop_top(BgScalars *sc, int use_cond, cudaGra
     return;                                                               \
   }
 
-// SpMV kernels: RESID (rmode BR_INIT / BR_CHECK), AV, AT, FINAL (rmode BR_FINAL)
-template <int FMT, int L, int MODE>
-__global__ void __launch_bounds__(BLOCK) bg_spmv_kernel(SellView S, CsrView C, BicgVecs v, BgScalars *sc,
-                                                        double *part, int rmode, int use_cond,
-                                                        cudaGraphConditionalHandle h) {
-  __shared__ double sm[3][WARPS];
-  if (MODE == SP_AV || MODE == SP_AT) {
-    BG_ENTRY();
-    if (MODE == SP_AT && vs->half) return;  // converged at the half step: no t this iteration
-  }
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  spmv_body<FMT, L, MODE>(S, C, v, a0, a1, a2);
-  double red[3] = {a0, a1, a2};
-  block_sum<3>(red, sm);
-  if (!publish_and_arrive<3>(red, part, &sc->cnt[0])) return;
-  double t[3];
-  reduce_partials<3>(part, t, sm);
-  if (threadIdx.x != 0) return;
-  sc->cnt[0] = 0;
+// finishers (thread 0 of the last block, or a 1-thread kernel after the allreduce on
+// distributed handles) — the persistent kernel's scalar logic
+template <int MODE>
+__device__ void bg_fin_spmv(BgScalars *sc, const double *t, int rmode, int use_cond, cudaGraphConditionalHandle h) {
   if (MODE == SP_RESID) {
     if (rmode == BR_INIT) {
       sc->nb = sqrt(t[2]);
@@ -606,28 +593,7 @@ __global__ void __launch_bounds__(BLOCK) bg_spmv_kernel(SellView S, CsrView C, B
   }
 }
 
-// P1 / P3 (precond_body); P3's last block takes the half-step test
-template <int BS, int STAGE>
-__global__ void __launch_bounds__(BLOCK) bg_precond_kernel(int64_t n, BicgVecs v, BgScalars *sc, double *part,
-                                                           int use_cond, cudaGraphConditionalHandle h) {
-  __shared__ double sm[1][WARPS];
-  BG_ENTRY();
-  double a0 = 0.0;
-  const bool rows = BS > 1 && v.iperm == nullptr;  // lane-per-row path (natural order)
-  if (STAGE == 0) {
-    if (rows) precond_rows<BS, 0>(v, n, vs->beta, vs->omega, a0);
-    else precond_body<BS, 0>(v, n, vs->beta, vs->omega, a0);
-    return;
-  }
-  if (rows) precond_rows<BS, 1>(v, n, vs->alpha, 0.0, a0);
-  else precond_body<BS, 1>(v, n, vs->alpha, 0.0, a0);
-  double red[1] = {a0};
-  block_sum<1>(red, sm);
-  if (!publish_and_arrive<1>(red, part, &sc->cnt[1])) return;
-  double t[1];
-  reduce_partials<1>(part, t, sm);
-  if (threadIdx.x != 0) return;
-  sc->cnt[1] = 0;
+__device__ void bg_fin_p3(BgScalars *sc, const double *t) {
   const double ss = sqrt(t[0]);
   if (ss <= sc->tol * sc->nb) {
     sc->half = 1;
@@ -635,27 +601,7 @@ __global__ void __launch_bounds__(BLOCK) bg_precond_kernel(int64_t n, BicgVecs v
   }
 }
 
-// P5; at a half-step convergence only x += alpha p^, then the loop ends for the exit check
-__global__ void __launch_bounds__(BLOCK) bg_update_kernel(int64_t n, BicgVecs v, BgScalars *sc, double *part,
-                                                          int use_cond, cudaGraphConditionalHandle h) {
-  __shared__ double sm[2][WARPS];
-  BG_ENTRY();
-  const int half = vs->half;
-  const double alpha = vs->alpha, omega = vs->omega;
-  double a0 = 0.0, a1 = 0.0;
-  if (half) {
-    const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
-    for (int64_t i = tid; i < n; i += nth) v.x[i] = __fma_rn(alpha, v.ph[i], v.x[i]);
-  } else {
-    update_body(v, n, alpha, omega, a0, a1);
-  }
-  double red[2] = {a0, a1};
-  block_sum<2>(red, sm);
-  if (!publish_and_arrive<2>(red, part, &sc->cnt[2])) return;
-  double t[2];
-  reduce_partials<2>(part, t, sm);
-  if (threadIdx.x != 0) return;
-  sc->cnt[2] = 0;
+__device__ void bg_fin_update(BgScalars *sc, const double *t, int half, int use_cond, cudaGraphConditionalHandle h) {
   if (half) {
     sc->half = 0;
     sc->need_resid = 1;
@@ -675,6 +621,92 @@ __global__ void __launch_bounds__(BLOCK) bg_update_kernel(int64_t n, BicgVecs v,
     sc->rho = t[1];
     bg_loop_top(sc, use_cond, h);
   }
+}
+
+// last block: the finisher (one GPU) or this rank's sums into sc->part (distributed)
+template <int NV>
+__device__ __forceinline__ bool bg_last(double (&red)[NV], double *part, unsigned int *cnt, BgScalars *sc, int dist,
+                                        double (*sm)[WARPS], double (&t)[NV]) {
+  block_sum<NV>(red, sm);
+  if (!publish_and_arrive<NV>(red, part, cnt)) return false;
+  reduce_partials<NV>(part, t, sm);
+  if (threadIdx.x != 0) return false;
+  *cnt = 0;
+  if (dist) {
+#pragma unroll
+    for (int i = 0; i < NV; i++) sc->part[i] = t[i];
+    return false;
+  }
+  return true;
+}
+
+// SpMV kernels: RESID (rmode BR_INIT / BR_CHECK), AV, AT, FINAL (rmode BR_FINAL)
+template <int FMT, int L, int MODE>
+__global__ void __launch_bounds__(BLOCK) bg_spmv_kernel(SellView S, CsrView C, BicgVecs v, BgScalars *sc,
+                                                        double *part, int rmode, int dist, int use_cond,
+                                                        cudaGraphConditionalHandle h) {
+  __shared__ double sm[3][WARPS];
+  if (MODE == SP_AV || MODE == SP_AT) {
+    BG_ENTRY();
+    if (MODE == SP_AT && vs->half) return;  // converged at the half step: no t this iteration
+  }
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  spmv_body<FMT, L, MODE>(S, C, v, a0, a1, a2);
+  double red[3] = {a0, a1, a2}, t[3];
+  if (bg_last<3>(red, part, &sc->cnt[0], sc, dist, sm, t)) bg_fin_spmv<MODE>(sc, t, rmode, use_cond, h);
+}
+
+// P1 / P3 (precond_body); P3's last block takes the half-step test
+template <int BS, int STAGE>
+__global__ void __launch_bounds__(BLOCK) bg_precond_kernel(int64_t n, BicgVecs v, BgScalars *sc, double *part,
+                                                           int dist, int use_cond, cudaGraphConditionalHandle h) {
+  __shared__ double sm[1][WARPS];
+  BG_ENTRY();
+  double a0 = 0.0;
+  const bool rows = BS > 1 && v.iperm == nullptr;  // lane-per-row path (natural order)
+  if (STAGE == 0) {
+    if (rows) precond_rows<BS, 0>(v, n, vs->beta, vs->omega, a0);
+    else precond_body<BS, 0>(v, n, vs->beta, vs->omega, a0);
+    return;
+  }
+  if (rows) precond_rows<BS, 1>(v, n, vs->alpha, 0.0, a0);
+  else precond_body<BS, 1>(v, n, vs->alpha, 0.0, a0);
+  double red[1] = {a0}, t[1];
+  if (bg_last<1>(red, part, &sc->cnt[1], sc, dist, sm, t)) bg_fin_p3(sc, t);
+}
+
+// P5; at a half-step convergence only x += alpha p^, then the loop ends for the exit check
+__global__ void __launch_bounds__(BLOCK) bg_update_kernel(int64_t n, BicgVecs v, BgScalars *sc, double *part,
+                                                          int dist, int use_cond, cudaGraphConditionalHandle h) {
+  __shared__ double sm[2][WARPS];
+  BG_ENTRY();
+  const int half = vs->half;
+  const double alpha = vs->alpha, omega = vs->omega;
+  double a0 = 0.0, a1 = 0.0;
+  if (half) {
+    const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
+    for (int64_t i = tid; i < n; i += nth) v.x[i] = __fma_rn(alpha, v.ph[i], v.x[i]);
+  } else {
+    update_body(v, n, alpha, omega, a0, a1);
+  }
+  double red[2] = {a0, a1}, t[2];
+  if (bg_last<2>(red, part, &sc->cnt[2], sc, dist, sm, t)) bg_fin_update(sc, t, half, use_cond, h);
+}
+
+// distributed handles: the finisher after the allreduce of sc->part
+enum { BF_RESID = 0, BF_AV = 1, BF_P3 = 2, BF_AT = 3, BF_UPDATE = 4, BF_FINAL = 5 };
+__global__ void bg_finish_kernel(BgScalars *sc, int which, int rmode) {
+  const double t[3] = {sc->part[0], sc->part[1], sc->part[2]};
+  if (which == BF_RESID) return bg_fin_spmv<SP_RESID>(sc, t, rmode, 0, 0);
+  if (which == BF_FINAL) return bg_fin_spmv<SP_FINAL>(sc, t, rmode, 0, 0);
+  if (sc->stop) return;  // a finisher earlier in this chunk ended the loop
+  if (which == BF_AV) return bg_fin_spmv<SP_AV>(sc, t, 0, 0, 0);
+  if (which == BF_P3) return bg_fin_p3(sc, t);
+  if (which == BF_AT) {
+    if (!sc->half) bg_fin_spmv<SP_AT>(sc, t, 0, 0, 0);
+    return;
+  }
+  bg_fin_update(sc, t, sc->half, 0, 0);
 }
 
 // ---------------------------------------------------------------- host side
@@ -712,20 +744,20 @@ static void bg_iteration(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double
   const SellView S = A->sell();
   const CsrView C = A->csr();
   const int gs = A->grid_spmv, gv = A->grid_vec;
-  bg_precond_kernel<BS, 0><<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, use_cond, h);
-  bg_spmv_kernel<FMT, L, SP_AV><<<gs, BLOCK, 0, st>>>(S, C, v, sc, part, 0, use_cond, h);
-  bg_precond_kernel<BS, 1><<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, use_cond, h);
-  bg_spmv_kernel<FMT, L, SP_AT><<<gs, BLOCK, 0, st>>>(S, C, v, sc, part, 0, use_cond, h);
-  bg_update_kernel<<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, use_cond, h);
+  bg_precond_kernel<BS, 0><<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, 0, use_cond, h);
+  bg_spmv_kernel<FMT, L, SP_AV><<<gs, BLOCK, 0, st>>>(S, C, v, sc, part, 0, 0, use_cond, h);
+  bg_precond_kernel<BS, 1><<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, 0, use_cond, h);
+  bg_spmv_kernel<FMT, L, SP_AT><<<gs, BLOCK, 0, st>>>(S, C, v, sc, part, 0, 0, use_cond, h);
+  bg_update_kernel<<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, 0, use_cond, h);
   count_launch(5);
 }
 
 template <int FMT, int L, int BS>
 static void bg_resid(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double *part, int rmode, cudaStream_t st) {
   if (rmode == BR_FINAL)
-    bg_spmv_kernel<FMT, L, SP_FINAL><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), v, sc, part, rmode, 0, 0);
+    bg_spmv_kernel<FMT, L, SP_FINAL><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), v, sc, part, rmode, 0, 0, 0);
   else
-    bg_spmv_kernel<FMT, L, SP_RESID><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), v, sc, part, rmode, 0, 0);
+    bg_spmv_kernel<FMT, L, SP_RESID><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), v, sc, part, rmode, 0, 0, 0);
   count_launch();
 }
 
@@ -840,17 +872,113 @@ static pcg_status bg_solve(pcg_matrix *A, const BicgVecs &v, int bs, double tol,
   return PCG_OK;
 }
 
+// distributed handles (csr_create_dist; point Jacobi): the same five passes as
+// direct launches with the exchanges between them — halo of p^ before v = A p^ and
+// of s^ before t = A s^; an allreduce of this rank's sums before every finisher (four
+// per iteration: r^.v | s.s | t.s, t.t | r.r, r^.r).  U iterations per host poll;
+// the exit check / restart between polls, as on one GPU.
+template <int FMT, int L>
+struct BgdOps {
+  static void spmv(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, int mode, int rmode, cudaStream_t st) {
+    double *part = A->work.partials;
+    const SellView S = A->sell();
+    const CsrView C = A->csr();
+    switch (mode) {
+      case SP_RESID: bg_spmv_kernel<FMT, L, SP_RESID><<<A->grid_spmv, BLOCK, 0, st>>>(S, C, v, sc, part, rmode, 1, 0, 0); break;
+      case SP_AV: bg_spmv_kernel<FMT, L, SP_AV><<<A->grid_spmv, BLOCK, 0, st>>>(S, C, v, sc, part, 0, 1, 0, 0); break;
+      case SP_AT: bg_spmv_kernel<FMT, L, SP_AT><<<A->grid_spmv, BLOCK, 0, st>>>(S, C, v, sc, part, 0, 1, 0, 0); break;
+      default: bg_spmv_kernel<FMT, L, SP_FINAL><<<A->grid_spmv, BLOCK, 0, st>>>(S, C, v, sc, part, rmode, 1, 0, 0); break;
+    }
+    count_launch();
+  }
+};
+using BgdSpmv = void (*)(pcg_matrix *, const BicgVecs &, BgScalars *, int, int, cudaStream_t);
+static BgdSpmv bgd_spmv_fn(int fmt, int lanes) {
+  if (fmt == PCG_FORMAT_SELL) return BgdOps<PCG_FORMAT_SELL, 1>::spmv;
+  switch (lanes) {
+    case 1: return BgdOps<PCG_FORMAT_CSR, 1>::spmv;
+    case 2: return BgdOps<PCG_FORMAT_CSR, 2>::spmv;
+    case 4: return BgdOps<PCG_FORMAT_CSR, 4>::spmv;
+    case 8: return BgdOps<PCG_FORMAT_CSR, 8>::spmv;
+    case 16: return BgdOps<PCG_FORMAT_CSR, 16>::spmv;
+    default: return BgdOps<PCG_FORMAT_CSR, 32>::spmv;
+  }
+}
+
+static pcg_status bgd_solve(pcg_matrix *A, const BicgVecs &v, double tol, int64_t max_iter, cudaStream_t st,
+                            BicgState *hs) {
+  SolveWork &w = A->work;
+  if (!w.bgsc) PCG_CUDA(cudaMalloc(&w.bgsc, sizeof(BgScalars)));
+  BgScalars *sc = (BgScalars *)w.bgsc, h;
+  memset(&h, 0, sizeof(h));
+  h.tol = tol;
+  h.max_iter = max_iter;
+  PCG_CUDA(cudaMemcpyAsync(sc, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  const BgdSpmv spmv = bgd_spmv_fn(A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format, A->csr_lanes);
+  double *part = w.partials;
+  auto read = [&]() -> pcg_status {
+    PCG_CUDA(cudaGetLastError());
+    PCG_CUDA(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    PCG_CUDA(cudaStreamSynchronize(st));
+    return PCG_OK;
+  };
+  auto finish = [&](int which, int rmode, int count) -> pcg_status {
+    PCG_TRY(allreduce_sum(A, sc->part, count, st));
+    bg_finish_kernel<<<1, 1, 0, st>>>(sc, which, rmode);
+    count_launch();
+    return PCG_OK;
+  };
+  auto resid = [&](int rmode) -> pcg_status {  // the (re)start / exit check / final residual
+    PCG_TRY(halo_exchange(A, v.x, 1, st));
+    spmv(A, v, sc, rmode == BR_FINAL ? SP_FINAL : SP_RESID, rmode, st);
+    PCG_TRY(finish(rmode == BR_FINAL ? BF_FINAL : BF_RESID, rmode, rmode == BR_FINAL ? 1 : 3));
+    return read();
+  };
+  const int U = 8;
+  PCG_TRY(resid(BR_INIT));
+  if (h.done == BD_ZERO_RHS || h.done == BD_NONFINITE) PCG_CUDA(cudaMemsetAsync(v.x, 0, sizeof(double) * A->n, st));
+  while (h.done == BD_RUNNING) {
+    for (int u = 0; u < U; u++) {
+      bg_precond_kernel<1, 0><<<A->grid_vec, BLOCK, 0, st>>>(A->n, v, sc, part, 1, 0, 0);  // p, p^
+      count_launch();
+      PCG_TRY(halo_exchange(A, v.ph, 1, st));
+      spmv(A, v, sc, SP_AV, 0, st);  // v = A p^
+      PCG_TRY(finish(BF_AV, 0, 1));
+      bg_precond_kernel<1, 1><<<A->grid_vec, BLOCK, 0, st>>>(A->n, v, sc, part, 1, 0, 0);  // s, s^
+      count_launch();
+      PCG_TRY(finish(BF_P3, 0, 1));
+      PCG_TRY(halo_exchange(A, v.sh, 1, st));
+      spmv(A, v, sc, SP_AT, 0, st);  // t = A s^
+      PCG_TRY(finish(BF_AT, 0, 2));
+      bg_update_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, v, sc, part, 1, 0, 0);
+      count_launch();
+      PCG_TRY(finish(BF_UPDATE, 0, 2));
+    }
+    PCG_TRY(read());
+    if (h.done != BD_RUNNING) break;
+    if (h.stop) PCG_TRY(resid(BR_CHECK));  // exit check (need_resid), restart if it fails
+  }
+  if (h.done == BD_MAXIT || h.done == BD_BREAKDOWN || h.done == BD_NONFINITE) PCG_TRY(resid(BR_FINAL));
+  hs->nb = h.nb;
+  hs->relres_rec = h.relres_rec;
+  hs->relres_true = h.relres_true;
+  hs->k = h.k;
+  hs->restarts = h.restarts;
+  hs->done = h.done;
+  return PCG_OK;
+}
+
 static pcg_status bicg_setup(pcg_matrix *A, int bs, cudaStream_t st) {
   SolveWork &w = A->work;
   if (!w.bv) {
-    const size_t nb = sizeof(double) * ((size_t)A->n + 64);
+    const size_t nb = sizeof(double) * ((size_t)(A->n + A->n_ghost) + 64);  // ghost slots for x, p^, s^
     PCG_CUDA(cudaMalloc(&w.bv, nb * 8));  // x r rh p ph v sh t
     PCG_CUDA(cudaMemsetAsync(w.bv, 0, nb * 8, st));
     PCG_CUDA(cudaMalloc(&w.bstate, sizeof(BicgState)));
     PCG_CUDA(cudaMalloc(&w.bbar, sizeof(GridBar)));
     PCG_CUDA(cudaMemsetAsync(w.bbar, 0, sizeof(GridBar), st));
     shadow_kernel<<<(unsigned)std::min<int64_t>((A->n + 255) / 256, 148 * 16), 256, 0, st>>>(
-        A->n, A->d_perm, w.bv + 2 * (A->n + 64));
+        A->n, A->d_perm, A->row_begin, w.bv + 2 * (A->n + A->n_ghost + 64));
     count_launch();
     PCG_CUDA(cudaGetLastError());
   }
@@ -887,7 +1015,7 @@ static pcg_status bicg_impl(pcg_matrix *A, const double *b, double *x, double to
   PCG_TRY(ensure_work(A));
   PCG_TRY(bicg_setup(A, bs, st));
   SolveWork &w = A->work;
-  const int64_t n = A->n, ldv = n + 64;
+  const int64_t n = A->n, ldv = n + A->n_ghost + 64;
   BicgVecs v;
   v.x = w.bv;
   v.r = w.bv + ldv;
@@ -928,7 +1056,12 @@ static pcg_status bicg_impl(pcg_matrix *A, const double *b, double *x, double to
   cudaEvent_t e0, e1;
   PCG_CUDA(cudaEventCreate(&e0));
   PCG_CUDA(cudaEventCreate(&e1));
-  if (bicg_use_graph(A)) {
+  if (A->comm) {
+    PCG_CUDA(cudaEventRecord(e0, st));
+    const pcg_status gs = bgd_solve(A, v, tol, max_iter, st, &hs);
+    PCG_CUDA(cudaEventRecord(e1, st));
+    if (gs != PCG_OK) return gs;
+  } else if (bicg_use_graph(A)) {
     PCG_CUDA(cudaEventRecord(e0, st));
     const pcg_status gs = bg_solve(A, v, bs, tol, max_iter, st, &hs);
     PCG_CUDA(cudaEventRecord(e1, st));
@@ -1009,7 +1142,8 @@ extern "C" pcg_status pcg_bicgstab(pcg_matrix_t A, const double *b, double *x, d
   if (!(tol > 0.0) || max_iter < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab: tol > 0 and max_iter >= 1");
   if (block_size != 1 && block_size != 2 && block_size != 4 && block_size != 8)
     return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab: block_size must be 1, 2, 4 or 8");
-  if (A->comm) return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab: single-GPU handles only");
+  if (A->comm && block_size != 1)
+    return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab: distributed handles take point Jacobi (block_size 1)");
   if (A->n == 0) {
     if (info) {
       memset(info, 0, sizeof(*info));

@@ -200,3 +200,73 @@ def test_nccl_single_rank_distributed_handle():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+def _bicg_worker(rank, world, port, N, out_q):
+    import torch
+    import torch.distributed as dist
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_2201_05413_b200 as pcg
+        from paper_2201_05413_b200.problems import fd_cube_build
+        A, b = O.fd_cube(N)
+        bounds = pcg.partition_rows(A.row_ptr, world)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        G = fd_cube_build(N, row_begin=r0, row_end=r1)  # this rank's rows, generated on the device
+        comm = pcg.Comm.host_callbacks()
+        M = pcg.Matrix.from_csr_dist(comm, A.n, r0, r1, G["row_ptr"], G["col"], G["val"])
+        x, info = M.bicgstab(G["b"], tol=1e-12)
+        out_q.put((rank, dict(x=x.cpu().numpy(), info=info)))
+        M.close()
+        comm.close()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        out_q.put((rank, {"error": f"{e!r}\n{traceback.format_exc()}"}))
+
+
+@pytest.mark.parametrize("world,N", [(2, 20), (3, 32)])
+def test_distributed_bicgstab_on_one_gpu(world, N):
+    """pcg_bicgstab on distributed handles (N2 on the paper's own setting: the Table 1
+    FD grid row-partitioned; point Jacobi; four allreduces and two halo exchanges per
+    iteration) with 2-3 ranks sharing the GPU through the host-callback communicator.
+    Same bars as the single-GPU BiCGSTAB test: x within 1e-9 of the oracle and of the
+    closed form x^2 - y^2, iterations within max(2 %, 2) of the range the oracle spans
+    under rounding-level perturbations of b."""
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bicg_worker, args=(r, world, port, N, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, d = q.get(timeout=600)
+        res[r] = d
+    for p in procs:
+        p.join(timeout=120)
+    for d in res.values():
+        assert "error" not in d, d.get("error")
+    parts = [res[r] for r in range(world)]
+    A, b = O.fd_cube(N)
+    ro = O.bicgstab(A, b, tol=1e-12)
+    rng = np.random.default_rng(2201)
+    its = [ro.iterations] + [O.bicgstab(A, b * (1 + 1e-15 * rng.standard_normal(A.n)), tol=1e-12).iterations
+                             for _ in range(8)]
+    lo, hi = min(its), max(its)
+    x = np.concatenate([d["x"] for d in parts])
+    gits = {d["info"]["iterations"] for d in parts}
+    assert len(gits) == 1
+    it = gits.pop()
+    assert all(d["info"]["status"] == 0 and d["info"]["relres_true"] <= 1e-12 for d in parts)
+    assert np.linalg.norm(x - ro.x) <= 1e-9 * np.linalg.norm(ro.x)
+    assert lo - max(2, 0.02 * lo) <= it <= hi + max(2, 0.02 * hi), (it, lo, hi)
+    i = np.arange(N)
+    X, Y = np.tile(i, N * N) / (N - 1), np.tile(np.repeat(i, N), N) / (N - 1)
+    assert np.max(np.abs(x - (X * X - Y * Y))) <= 1e-9
