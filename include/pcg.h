@@ -144,8 +144,11 @@ pcg_status pcg_solve_multi(pcg_matrix_t A, int32_t k, const double *B, int64_t l
  * x if needed.  The shadow residual is the fixed vector 2u(5413, i) - 1 (SplitMix64
  * u; i = original row).  b, x: n doubles, host or device; x in/out.  Returns OK,
  * NOT_CONVERGED, BREAKDOWN, NONFINITE, ZERO_DIAGONAL (singular block) or an error.
- * Single-GPU handles.  Blocks are consecutive rows of the caller's numbering on every
- * device format (SELL-C-sigma handles map them through their permutation). */
+ * Blocks are consecutive rows of the caller's numbering on every device format
+ * (SELL-C-sigma handles map them through their permutation).  Distributed handles
+ * (csr_create_dist): collective call from every rank with its rows of b and x,
+ * block_size 1 only (INVALID_ARG otherwise); the shadow residual uses global row ids,
+ * so the iterates are those of the undivided system up to reduction order. */
 pcg_status pcg_bicgstab(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
                         int32_t block_size, void *stream, pcg_info *info);
 
