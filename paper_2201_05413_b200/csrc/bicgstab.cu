@@ -851,10 +851,16 @@ static pcg_status bg_solve(pcg_matrix *A, const BicgVecs &v, int bs, double tol,
   ops.resid(A, v, sc, w.partials, BR_INIT, st);
   PCG_TRY(read());
   if (h.done == BD_ZERO_RHS || h.done == BD_NONFINITE) PCG_CUDA(cudaMemsetAsync(v.x, 0, sizeof(double) * A->n, st));
+  const bool direct = getenv("PCG_NO_GRAPH") != nullptr;  // profilers: the same kernels, launched directly
   while (h.done == BD_RUNNING) {
-    PCG_CUDA(cudaGraphLaunch(w.bg_exec, st));
-    count_launch();
+    if (direct) {
+      for (int u = 0; u < 8; u++) ops.iter(A, v, sc, w.partials, st, 0, 0);
+    } else {
+      PCG_CUDA(cudaGraphLaunch(w.bg_exec, st));
+      count_launch();
+    }
     PCG_TRY(read());
+    if (direct && h.stop == 0 && h.done == BD_RUNNING) continue;
     if (h.done != BD_RUNNING) break;
     ops.resid(A, v, sc, w.partials, BR_CHECK, st);  // exit check (need_resid), restart if it fails
     PCG_TRY(read());
