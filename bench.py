@@ -198,6 +198,8 @@ def main():
     ap.add_argument("--ref-iters", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fmt", default="auto", choices=["auto", "csr", "sell", "sigma"])
+    ap.add_argument("--drop-zeros", action="store_true",
+                    help="store no explicit zero entries (PCG_DROP_ZEROS; C3' of SURVEY Q7, same iterates)")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "callbacks"],
                     help="callbacks: exchange steps through host callbacks over gloo (validation of the N>1 "
                          "path when ranks share a GPU; not a performance number)")
@@ -240,7 +242,7 @@ def main():
     if world == 1:
         P = fem_build(spec)
         nnz = P["col"].numel()  # (the 3D element pattern has no closed form: problem_size gives -1)
-        A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"], fmt=args.fmt)
+        A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"], fmt=args.fmt, drop_zeros=args.drop_zeros)
         r0, r1 = 0, n
     else:
         rp_full = fem_build_rowptr(spec, n)
@@ -252,7 +254,14 @@ def main():
         if nnz < 0:
             nnz = int(rp_full_nnz)
         comm = pcg.Comm.host_callbacks() if cb else pcg.Comm.from_process_group()
-        A = pcg.Matrix.from_csr_dist(comm, n, r0, r1, P["row_ptr"], P["col"], P["val"], fmt=args.fmt)
+        A = pcg.Matrix.from_csr_dist(comm, n, r0, r1, P["row_ptr"], P["col"], P["val"], fmt=args.fmt,
+                                     drop_zeros=args.drop_zeros)
+    nnz_given = nnz
+    if args.drop_zeros:  # the bytes an iteration moves are those of the stored pattern
+        t = torch.tensor([float(A.stats()["nnz"])], dtype=torch.float64, device="cpu" if cb else "cuda")
+        if world > 1:
+            dist.all_reduce(t)
+        nnz = int(t.item())
     kcols = P["B"].shape[1]
     multi = kcols > 1
     if multi and world > 1:
@@ -430,7 +439,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = oracle_sample(args.config, args.sample_c)
         smp["c"] = args.sample_c
-        v = scale_to_workload(smp, n, nnz, iters) * kcols  # the oracle solves the k columns one by one
+        v = scale_to_workload(smp, n, nnz_given, iters) * kcols  # the oracle solves the k columns one by one
         cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
                "sample": f"oracle/oracle.c Jacobi-PCG, 1 thread, {args.config} construction at c={args.sample_c} "
                          f"({smp['n']} unknowns, {smp['nnz']} nnz, {smp['iterations']} iterations, "
@@ -446,7 +455,8 @@ def main():
             "config": dict(workload_config(args.config, c, n, nnz, world), iterations=iters,
                            format={1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[stats["format"]], setup_s=round(t_setup, 3),
                            relres_true=max(i["relres_true"] for i in infos[-1]), k_rhs=kcols,
-                           solver="jacobi-pcg" if args.solver == "pcg" else "pipelined jacobi-pcg (N3)"),
+                           solver="jacobi-pcg" if args.solver == "pcg" else "pipelined jacobi-pcg (N3)",
+                           **({"drop_zeros": True, "nnz_given": nnz_given} if args.drop_zeros else {})),
             "throughput": {"cg_iterations_per_s": iters / (ms / 1e3),
                            "effective_GBps": iter_bytes(n, nnz, kcols) * iters / (ms / 1e3) / 1e9,
                            "spmv_GBps": spmv_gbs, "spmv_frac_of_hbm": spmv_gbs / hbm if spmv_gbs else None},

@@ -53,6 +53,10 @@ typedef enum {
 /* csr_create flags */
 #define PCG_PTR_HOST 0x0   /* row_ptr/col_idx/val are host pointers   */
 #define PCG_PTR_DEVICE 0x1 /* ... are device pointers                 */
+#define PCG_DROP_ZEROS 0x100 /* do not store off-diagonal entries whose value is exactly 0.0 (SURVEY
+                              * §8(c) Q7's C3': the products are unchanged — 0 * x added to a partial
+                              * sum is exact for finite x — with fewer bytes; stats report the stored
+                              * nnz).  Default: every given entry is stored (the pattern policy).   */
 #define PCG_FMT_AUTO 0x00  /* pick the faster device format, measured */
 #define PCG_FMT_CSR 0x10   /* force CSR (sub-warp per row)            */
 #define PCG_FMT_SELL 0x20  /* force SELL-32 (slices of 32 rows)       */

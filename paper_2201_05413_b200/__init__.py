@@ -60,7 +60,7 @@ class Matrix:
 
     # -------------------------------------------------------------- creation
     @classmethod
-    def from_csr(cls, row_ptr, col, val, fmt: str = "auto", stream=None) -> "Matrix":
+    def from_csr(cls, row_ptr, col, val, fmt: str = "auto", stream=None, drop_zeros: bool = False) -> "Matrix":
         torch = _torch()
         rp, ci, va = _as_tensor(row_ptr, torch.int64), _as_tensor(col, torch.int64), _as_tensor(val, torch.float64)
         n = rp.numel() - 1
@@ -71,24 +71,34 @@ class Matrix:
         flags = (_lib.PCG_PTR_DEVICE if dev else _lib.PCG_PTR_HOST) | {
             "auto": PCG_FMT_AUTO, "csr": PCG_FMT_CSR, "sell": PCG_FMT_SELL, "tma": _lib.PCG_FMT_SELL_TMA,
             "sigma": _lib.PCG_FMT_SELL_SIGMA}[fmt]
+        if drop_zeros:
+            flags |= _lib.PCG_DROP_ZEROS
         h = C.c_void_p()
         check(lib().csr_create(n, nnz, _ptr(rp), _ptr(ci), _ptr(va), flags, _stream_ptr(stream), C.byref(h)),
               "csr_create")
-        return cls(h.value, n, nnz)
+        m = cls(h.value, n, nnz)
+        if drop_zeros:
+            m.nnz = m.stats()["nnz"]
+        return m
 
     @classmethod
     def from_csr_dist(cls, comm: "Comm", n_global: int, row_begin: int, row_end: int, row_ptr_local, col_global,
-                      val, fmt: str = "auto", stream=None) -> "Matrix":
+                      val, fmt: str = "auto", stream=None, drop_zeros: bool = False) -> "Matrix":
         torch = _torch()
         rp, ci, va = (_as_tensor(row_ptr_local, torch.int64), _as_tensor(col_global, torch.int64),
                       _as_tensor(val, torch.float64))
         flags = (_lib.PCG_PTR_DEVICE if rp.is_cuda else _lib.PCG_PTR_HOST) | {
             "auto": PCG_FMT_AUTO, "csr": PCG_FMT_CSR, "sell": PCG_FMT_SELL, "tma": _lib.PCG_FMT_SELL_TMA,
             "sigma": _lib.PCG_FMT_SELL_SIGMA}[fmt]
+        if drop_zeros:
+            flags |= _lib.PCG_DROP_ZEROS
         h = C.c_void_p()
         check(lib().csr_create_dist(comm._h, n_global, row_begin, row_end, ci.numel(), _ptr(rp), _ptr(ci), _ptr(va),
                                     flags, _stream_ptr(stream), C.byref(h)), "csr_create_dist")
-        return cls(h.value, row_end - row_begin, ci.numel(), comm=comm)
+        m = cls(h.value, row_end - row_begin, ci.numel(), comm=comm)
+        if drop_zeros:
+            m.nnz = m.stats()["nnz"]
+        return m
 
     def close(self):
         if self._h and self._h.value:

@@ -21,6 +21,7 @@ STATUS = ["PCG_OK", "PCG_NOT_CONVERGED", "PCG_ERR_INVALID_ARG", "PCG_ERR_INDEX_O
  PCG_ERR_UNSORTED_OR_DUPLICATE, PCG_ERR_DIMENSION_MISMATCH, PCG_ERR_ZERO_DIAGONAL, PCG_ERR_NOT_SPD,
  PCG_ERR_NONFINITE, PCG_ERR_OOM, PCG_ERR_CUDA, PCG_ERR_NCCL, PCG_ERR_BREAKDOWN) = range(13)
 PCG_PTR_HOST, PCG_PTR_DEVICE = 0x0, 0x1
+PCG_DROP_ZEROS = 0x100
 PCG_FMT_AUTO, PCG_FMT_CSR, PCG_FMT_SELL, PCG_FMT_SELL_TMA, PCG_FMT_SELL_SIGMA = 0x00, 0x10, 0x20, 0x30, 0x40
 PCG_FORMAT_CSR, PCG_FORMAT_SELL, PCG_FORMAT_SELL_TMA, PCG_FORMAT_SELL_SIGMA = 1, 2, 3, 4
 

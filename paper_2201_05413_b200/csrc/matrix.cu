@@ -237,6 +237,72 @@ void free_sell(pcg_matrix *A) {
   A->sell_entries = 0;
 }
 
+// PCG_DROP_ZEROS: off-diagonal entries whose value is exactly 0.0 are not stored.
+// Row by row, order kept; the diagonal (local column i) always stays.
+__global__ void dz_count_kernel(int64_t n, const int *__restrict__ rp, const int *__restrict__ col,
+                                const double *__restrict__ val, int *__restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int c = 0;
+    for (int k = rp[i]; k < rp[i + 1]; k++) c += (val[k] != 0.0 || col[k] == (int)i);
+    cnt[i] = c;
+  }
+}
+__global__ void dz_copy_kernel(int64_t n, const int *__restrict__ rp, const int *__restrict__ col,
+                               const double *__restrict__ val, const int *__restrict__ rp2, int *__restrict__ col2,
+                               double *__restrict__ val2) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int o = rp2[i];
+    for (int k = rp[i]; k < rp[i + 1]; k++)
+      if (val[k] != 0.0 || col[k] == (int)i) {
+        col2[o] = col[k];
+        val2[o] = val[k];
+        o++;
+      }
+  }
+}
+
+static pcg_status drop_zeros(pcg_matrix *A, cudaStream_t st) {
+  const int64_t n = A->n;
+  if (n == 0 || A->nnz == 0) return PCG_OK;
+  int *cnt = nullptr, *rp2 = nullptr, *col2 = nullptr, *mx = nullptr;
+  double *val2 = nullptr;
+  PCG_CUDA(cudaMalloc(&cnt, sizeof(int) * (n + 1)));
+  PCG_CUDA(cudaMalloc(&rp2, sizeof(int) * (n + 1)));
+  PCG_CUDA(cudaMalloc(&mx, sizeof(int)));
+  const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  dz_count_kernel<<<g, 256, 0, st>>>(n, A->d_row_ptr, A->d_col, A->d_val, cnt);
+  PCG_CUDA(cudaMemsetAsync(cnt + n, 0, sizeof(int), st));
+  size_t tb = 0, tm = 0;
+  PCG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, rp2, (int)(n + 1), st));
+  PCG_CUDA(cub::DeviceReduce::Max(nullptr, tm, cnt, mx, (int)n, st));
+  void *tmp = nullptr;
+  PCG_CUDA(cudaMalloc(&tmp, std::max(tb, tm)));
+  PCG_CUDA(cub::DeviceReduce::Max(tmp, tm, cnt, mx, (int)n, st));
+  PCG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, rp2, (int)(n + 1), st));
+  int nnz2 = 0, maxlen = 0;
+  PCG_CUDA(cudaMemcpyAsync(&nnz2, rp2 + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaMemcpyAsync(&maxlen, mx, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_CUDA(cudaMalloc(&col2, sizeof(int) * std::max(nnz2, 1)));
+  PCG_CUDA(cudaMalloc(&val2, sizeof(double) * std::max(nnz2, 1)));
+  dz_copy_kernel<<<g, 256, 0, st>>>(n, A->d_row_ptr, A->d_col, A->d_val, rp2, col2, val2);
+  count_launch(2);
+  PCG_CUDA(cudaGetLastError());
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(A->d_row_ptr);
+  cudaFree(A->d_col);
+  cudaFree(A->d_val);
+  cudaFree(cnt);
+  cudaFree(mx);
+  cudaFree(tmp);
+  A->d_row_ptr = rp2;
+  A->d_col = col2;
+  A->d_val = val2;
+  A->nnz = nnz2;
+  A->max_row_len = maxlen;
+  return PCG_OK;
+}
+
 // Core of csr_create / csr_create_dist: columns already translated so that the
 // local matrix is n x n_cols (n_cols = n + n_ghost) with diagonal at i + 0.
 // d_col_check: columns as given by the caller (global ids on a distributed handle),
@@ -271,6 +337,8 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
     count_launch();
     PCG_CUDA(cudaGetLastError());
   }
+  if (flags & PCG_DROP_ZEROS) PCG_TRY(drop_zeros(A, st));
+  nnz = A->nnz;
   // ---- SELL-32
   const int fmt_req = flags & 0xF0;
   A->n_slices = (n + 31) / 32;

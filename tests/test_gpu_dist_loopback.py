@@ -28,7 +28,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, c, use_generator, out_q):
+def _worker(rank, world, port, name, c, use_generator, out_q, drop=False):
     import torch
     import torch.distributed as dist
     try:
@@ -50,7 +50,7 @@ def _worker(rank, world, port, name, c, use_generator, out_q):
             col = torch.as_tensor(A.col[A.row_ptr[r0]:A.row_ptr[r1]]).cuda()
             val = torch.as_tensor(A.val[A.row_ptr[r0]:A.row_ptr[r1]]).cuda()
             bl = torch.as_tensor(b[r0:r1]).cuda()
-        M = pcg.Matrix.from_csr_dist(comm, A.n, r0, r1, rp, col, val)
+        M = pcg.Matrix.from_csr_dist(comm, A.n, r0, r1, rp, col, val, drop_zeros=drop)
         st = M.stats()
         x, info = M.solve(bl, tol=1e-10)
         xp, infop = M.solve_pipelined(bl, tol=1e-10)  # N3: one allreduce per iteration
@@ -66,7 +66,7 @@ def _worker(rank, world, port, name, c, use_generator, out_q):
         out_q.put((rank, {"error": f"{e!r}\n{traceback.format_exc()}"}))
 
 
-def _run(world, name, c, use_generator=False):
+def _run(world, name, c, use_generator=False, drop=False):
     import torch
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
@@ -74,7 +74,7 @@ def _run(world, name, c, use_generator=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, c, use_generator, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, c, use_generator, q, drop)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -88,10 +88,11 @@ def _run(world, name, c, use_generator=False):
     return [res[r] for r in range(world)]
 
 
-@pytest.mark.parametrize("world,name,c,gen", [(2, "C2", 48, False), (3, "C3", 24, False), (2, "C5", 32, True),
-                                              (3, "C1", None, False)])
-def test_distributed_path_on_one_gpu(world, name, c, gen):
-    parts = _run(world, name, c, gen)
+@pytest.mark.parametrize("world,name,c,gen,drop", [(2, "C2", 48, False, False), (3, "C3", 24, False, False),
+                                                   (2, "C5", 32, True, False), (3, "C1", None, False, False),
+                                                   (2, "C3", 24, False, True)])  # C3': explicit zeros dropped
+def test_distributed_path_on_one_gpu(world, name, c, gen, drop):
+    parts = _run(world, name, c, gen, drop)
     P = O.build_problem(name, c=c, k=1)
     A, b = P["A"], P["B"][:, 0]
     tol = O.configs()[name]["tol"]
