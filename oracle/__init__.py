@@ -86,6 +86,7 @@ def lib():
         L.orc_pcg_pipelined.argtypes = [P(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_void_p,
                                         C.c_void_p, C.c_void_p]
         L.orc_halo.argtypes = [P(_Csr), C.c_int64, C.c_int64, C.c_void_p, C.c_int64]
+        L.orc_rcm.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_fd_identity_rows_nnz.restype = C.c_int64
         L.orc_fd_identity_rows_nnz.argtypes = [C.c_int64]
         _lib = L
@@ -289,6 +290,18 @@ def coo_to_csr(n_rows: int, n_cols: int, row, col, val):
     if st != OK:
         raise RuntimeError(f"orc_coo_to_csr: {st}")
     return rp, co[:u.value].copy(), vo[:u.value].copy()
+
+
+def rcm(A: Csr):
+    """SURVEY §8(f) N4: reverse Cuthill-McKee order of A's pattern (oracle.h orc_rcm);
+    perm[k] = original index of the k-th node (new -> old)."""
+    rp = np.ascontiguousarray(A.row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(A.col, dtype=np.int64)
+    perm = np.zeros(max(A.n, 1), dtype=np.int64)
+    st = lib().orc_rcm(A.n, _ptr(rp), _ptr(col), _ptr(perm))
+    if st != OK:
+        raise RuntimeError(f"orc_rcm: {st}")
+    return perm[:A.n].copy()
 
 
 def pcg_pipelined(A: Csr, b, x0=None, tol=1e-10, max_iter=50000) -> PcgResult:

@@ -1084,3 +1084,96 @@ out:
   free(dinv); free(r); free(u); free(w); free(m); free(nv); free(z); free(q); free(s); free(p);
   return st;
 }
+
+/* ---------------------------------------------------------------------------
+ * reverse Cuthill-McKee (oracle.h orc_rcm)
+ * ------------------------------------------------------------------------- */
+static int rcm_less(const int64_t *deg, int64_t a, int64_t b) {
+  return deg[a] < deg[b] || (deg[a] == deg[b] && a < b);
+}
+
+/* BFS from s (lvl[] = -1 on entry for every node of s's component, left filled);
+ * *ecc = last level index; returns the least (degree, id) node of the last level */
+static int64_t rcm_bfs(const int64_t *rp, const int64_t *col, const int64_t *deg, int64_t s, int64_t *lvl,
+                       int64_t *queue, int64_t *ecc) {
+  int64_t head = 0, tail = 0;
+  queue[tail++] = s;
+  lvl[s] = 0;
+  while (head < tail) {
+    const int64_t u = queue[head++];
+    for (int64_t k = rp[u]; k < rp[u + 1]; k++) {
+      const int64_t v = col[k];
+      if (v != u && lvl[v] < 0) {
+        lvl[v] = lvl[u] + 1;
+        queue[tail++] = v;
+      }
+    }
+  }
+  *ecc = lvl[queue[tail - 1]];
+  int64_t best = -1;
+  for (int64_t t = 0; t < tail; t++)
+    if (lvl[queue[t]] == *ecc && (best < 0 || rcm_less(deg, queue[t], best))) best = queue[t];
+  for (int64_t t = 0; t < tail; t++) lvl[queue[t]] = -1; /* reset for the next search */
+  return best;
+}
+
+int orc_rcm(int64_t n, const int64_t *row_ptr, const int64_t *col, int64_t *perm) {
+  if (n < 0) return ORC_ERR_INVALID_ARG;
+  if (n == 0) return ORC_OK;
+  int64_t *deg = malloc(sizeof(int64_t) * n), *lvl = malloc(sizeof(int64_t) * n);
+  int64_t *queue = malloc(sizeof(int64_t) * n), *order = malloc(sizeof(int64_t) * n);
+  char *placed = calloc((size_t)n, 1);
+  if (!deg || !lvl || !queue || !order || !placed) {
+    free(deg); free(lvl); free(queue); free(order); free(placed);
+    return ORC_ERR_OOM;
+  }
+  for (int64_t i = 0; i < n; i++) {
+    deg[i] = 0;
+    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) deg[i] += col[k] != i;
+    lvl[i] = -1;
+  }
+  int64_t pos = 0;
+  while (pos < n) {
+    /* component start: least (degree, id) unnumbered node */
+    int64_t s = -1;
+    for (int64_t i = 0; i < n; i++)
+      if (!placed[i] && (s < 0 || rcm_less(deg, i, s))) s = i;
+    /* George-Liu pseudo-peripheral node */
+    int64_t r = s, ecc_r, ecc_x;
+    int64_t x = rcm_bfs(row_ptr, col, deg, r, lvl, queue, &ecc_r);
+    for (;;) {
+      const int64_t x2 = rcm_bfs(row_ptr, col, deg, x, lvl, queue, &ecc_x);
+      if (ecc_x > ecc_r) {
+        r = x;
+        ecc_r = ecc_x;
+        x = x2;
+      } else {
+        break;
+      }
+    }
+    /* Cuthill-McKee from r */
+    int64_t head = pos;
+    order[pos++] = r;
+    placed[r] = 1;
+    while (head < pos) {
+      const int64_t u = order[head++];
+      const int64_t first = pos;
+      for (int64_t k = row_ptr[u]; k < row_ptr[u + 1]; k++) {
+        const int64_t v = col[k];
+        if (v != u && !placed[v]) {
+          placed[v] = 1;
+          order[pos++] = v;
+        }
+      }
+      for (int64_t a = first + 1; a < pos; a++) /* insertion sort by (degree, id) */
+        for (int64_t b = a; b > first && rcm_less(deg, order[b], order[b - 1]); b--) {
+          const int64_t t = order[b];
+          order[b] = order[b - 1];
+          order[b - 1] = t;
+        }
+    }
+  }
+  for (int64_t k = 0; k < n; k++) perm[k] = order[n - 1 - k];
+  free(deg); free(lvl); free(queue); free(order); free(placed);
+  return ORC_OK;
+}

@@ -128,4 +128,18 @@ int orc_pcg_pipelined(const orc_csr *A, const double *b, double *x, double tol, 
 int orc_coo_to_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t *row, const int64_t *col,
                    const double *val, int64_t *row_ptr, int64_t *col_out, double *val_out, int64_t *nnz_out);
 
+/* reverse Cuthill-McKee ordering of the graph of a symmetric
+ * pattern (edges = off-diagonal entries; explicit zeros are edges).  Plain
+ * sequential algorithm (Cuthill & McKee 1969, reversed per George 1971), start
+ * nodes by the George-Liu pseudo-peripheral search (1979), ties by node id:
+ *   component start s = the unnumbered node of least (degree, id);
+ *   r = s; repeat { x = least (degree, id) node of the last BFS level of r;
+ *                   if ecc(x) > ecc(r) then r = x else stop };
+ *   from r, a FIFO queue: each dequeued node appends its unnumbered neighbours
+ *   in increasing (degree, id);
+ *   components in that order; finally the whole order is reversed.
+ * perm[k] = the original index of the node placed k-th (new -> old).  The
+ * pattern must be symmetric (not checked). */
+int orc_rcm(int64_t n, const int64_t *row_ptr, const int64_t *col, int64_t *perm);
+
 #endif
