@@ -57,6 +57,11 @@ typedef enum {
                               * §8(c) Q7's C3': the products are unchanged — 0 * x added to a partial
                               * sum is exact for finite x — with fewer bytes; stats report the stored
                               * nnz).  Default: every given entry is stored (the pattern policy).   */
+#define PCG_REORDER_RCM 0x200 /* one GPU: keep the system in reverse Cuthill-McKee order
+                               * (csr_rcm_order) as P A P^T; b, x0 gathered and x scattered
+                               * inside the calls, so the caller's numbering is unchanged.
+                               * restores gather locality for a mesh
+                               * numbered arbitrarily.  INVALID_ARG on a distributed handle. */
 #define PCG_FMT_AUTO 0x00  /* pick the faster device format, measured */
 #define PCG_FMT_CSR 0x10   /* force CSR (sub-warp per row)            */
 #define PCG_FMT_SELL 0x20  /* force SELL-32 (slices of 32 rows)       */
@@ -102,7 +107,7 @@ typedef struct {
   int32_t schedule;          /* passes per iteration: 3 (K1a,K1b,K2) or 2 (fused K1,K2) */
   double spmv_us_sigma;      /* autotune timing of SELL-C-sigma (0 if not tried) */
   int32_t sigma;             /* sorting window of SELL-C-sigma (0: natural row order) */
-  int32_t pad0;
+  int32_t reorder;           /* 1: the device system is RCM-reordered (PCG_REORDER_RCM) */
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */
@@ -113,6 +118,20 @@ typedef struct {
 pcg_status csr_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int64_t *col_idx,
                       const double *val, int flags, void *stream, pcg_matrix_t *out);
 pcg_status csr_destroy(pcg_matrix_t A);
+
+/* reverse Cuthill-McKee order of a symmetric CSR pattern (edges =
+ * off-diagonal entries, explicit zeros included), computed on the device.  The
+ * order is the sequential algorithm's exactly (start per component = least
+ * (degree, id) node, George-Liu pseudo-peripheral search, neighbours appended in
+ * increasing (degree, id), reversed), bit-identical to the oracle's orc_rcm.
+ * perm[k] = original index of the node placed k-th (n int64, caller-owned).
+ * row_ptr/col_idx/perm: host, or device with PCG_PTR_DEVICE in flags.  The pattern
+ * must be symmetric (not checked).  n, nnz < 2^31.  Errors: INVALID_ARG,
+ * DIMENSION_MISMATCH, INDEX_OUT_OF_RANGE, OOM, CUDA.  Use: order a global matrix
+ * before csr_create_dist partitions it (contiguous blocks of a banded order have
+ * small halos), or pass PCG_REORDER_RCM to csr_create on one GPU. */
+pcg_status csr_rcm_order(int64_t n, int64_t nnz, const int64_t *row_ptr, const int64_t *col_idx, int flags,
+                         void *stream, int64_t *perm);
 pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *out);
 
 /* y = A x (one SpMV, the paper's MatMult).  x, y: n doubles (host or device).

@@ -60,7 +60,8 @@ class Matrix:
 
     # -------------------------------------------------------------- creation
     @classmethod
-    def from_csr(cls, row_ptr, col, val, fmt: str = "auto", stream=None, drop_zeros: bool = False) -> "Matrix":
+    def from_csr(cls, row_ptr, col, val, fmt: str = "auto", stream=None, drop_zeros: bool = False,
+                 reorder: str | None = None) -> "Matrix":
         torch = _torch()
         rp, ci, va = _as_tensor(row_ptr, torch.int64), _as_tensor(col, torch.int64), _as_tensor(val, torch.float64)
         n = rp.numel() - 1
@@ -73,6 +74,10 @@ class Matrix:
             "sigma": _lib.PCG_FMT_SELL_SIGMA}[fmt]
         if drop_zeros:
             flags |= _lib.PCG_DROP_ZEROS
+        if reorder not in (None, "rcm"):
+            raise ValueError(f"reorder must be None or 'rcm', not {reorder!r}")
+        if reorder == "rcm":
+            flags |= _lib.PCG_REORDER_RCM
         h = C.c_void_p()
         check(lib().csr_create(n, nnz, _ptr(rp), _ptr(ci), _ptr(va), flags, _stream_ptr(stream), C.byref(h)),
               "csr_create")
@@ -342,6 +347,22 @@ def partition_rows(row_ptr, G: int) -> np.ndarray:
     check(lib().pcg_partition_rows(len(rp) - 1, rp.ctypes.data_as(C.c_void_p), G,
                                    out.ctypes.data_as(C.c_void_p)), "pcg_partition_rows")
     return out
+
+
+def csr_rcm_order(row_ptr, col, stream=None):
+    """include/pcg.h csr_rcm_order: reverse Cuthill-McKee order of a symmetric CSR pattern,
+    computed on the GPU (SURVEY §8(f) N4).  row_ptr/col: int64 host arrays or CUDA tensors;
+    returns perm (new -> old) on the same side (numpy int64 or CUDA int64 tensor)."""
+    torch = _torch()
+    rp, ci = _as_tensor(row_ptr, torch.int64), _as_tensor(col, torch.int64)
+    n = rp.numel() - 1
+    dev = rp.is_cuda
+    if dev != ci.is_cuda:
+        raise ValueError("row_ptr and col must live on the same device")
+    perm = torch.empty(max(n, 0), dtype=torch.int64, device=rp.device)
+    check(lib().csr_rcm_order(n, ci.numel(), _ptr(rp), _ptr(ci), _lib.PCG_PTR_DEVICE if dev else _lib.PCG_PTR_HOST,
+                              _stream_ptr(stream), _ptr(perm)), "csr_rcm_order")
+    return perm if dev else perm.numpy()
 
 
 def halo_ghosts(row_begin: int, row_end: int, col_global) -> np.ndarray:

@@ -22,6 +22,7 @@ STATUS = ["PCG_OK", "PCG_NOT_CONVERGED", "PCG_ERR_INVALID_ARG", "PCG_ERR_INDEX_O
  PCG_ERR_NONFINITE, PCG_ERR_OOM, PCG_ERR_CUDA, PCG_ERR_NCCL, PCG_ERR_BREAKDOWN) = range(13)
 PCG_PTR_HOST, PCG_PTR_DEVICE = 0x0, 0x1
 PCG_DROP_ZEROS = 0x100
+PCG_REORDER_RCM = 0x200
 PCG_FMT_AUTO, PCG_FMT_CSR, PCG_FMT_SELL, PCG_FMT_SELL_TMA, PCG_FMT_SELL_SIGMA = 0x00, 0x10, 0x20, 0x30, 0x40
 PCG_FORMAT_CSR, PCG_FORMAT_SELL, PCG_FORMAT_SELL_TMA, PCG_FORMAT_SELL_SIGMA = 1, 2, 3, 4
 
@@ -43,7 +44,7 @@ class MatrixStats(C.Structure):
                 ("spmv_us_sell", C.c_double), ("n_ghost", C.c_int64), ("row_begin", C.c_int64),
                 ("row_end", C.c_int64), ("n_global", C.c_int64), ("spmv_us_tma", C.c_double),
                 ("stage_entries", C.c_int64), ("stages", C.c_int32), ("schedule", C.c_int32),
-                ("spmv_us_sigma", C.c_double), ("sigma", C.c_int32), ("pad0", C.c_int32)]
+                ("spmv_us_sigma", C.c_double), ("sigma", C.c_int32), ("reorder", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -103,6 +104,7 @@ def lib():
         "fd_cube_count": [i64, i64, i64, vp, P(i64), vp],
         "fd_cube_assemble": [i64, i32, i64, i64, vp, vp, vp, vp, vp],
         "coo_to_csr": [i64, i64, i64, vp, vp, vp, vp, vp, vp, P(i64), vp],
+        "csr_rcm_order": [i64, i64, vp, vp, C.c_int, vp, vp],
         "fem_element_count": [P(FemSpec), P(i64), P(i32), P(i64)],
         "fem_element_coo": [P(FemSpec), i64, i64, vp, vp, vp, vp],
         "fem_problem_size": [P(FemSpec), P(i64), P(i64), P(i64)],

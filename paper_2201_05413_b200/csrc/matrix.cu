@@ -339,6 +339,21 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
   }
   if (flags & PCG_DROP_ZEROS) PCG_TRY(drop_zeros(A, st));
   nnz = A->nnz;
+  if ((flags & PCG_REORDER_RCM) && n > 0) {
+    if (A->comm)
+      return fail(PCG_ERR_INVALID_ARG,
+                  "csr_create_dist: PCG_REORDER_RCM is one-GPU only; order the global matrix with csr_rcm_order "
+                  "before partitioning");
+    int *perm = nullptr;
+    PCG_CUDA(cudaMalloc(&perm, sizeof(int) * n));
+    pcg_status s = rcm_order(n, A->d_row_ptr, A->d_col, perm, st);
+    if (s != PCG_OK) {
+      cudaFree(perm);
+      return s;
+    }
+    PCG_TRY(apply_perm(A, perm, st));
+    A->reorder = 1;
+  }
   // ---- SELL-32
   const int fmt_req = flags & 0xF0;
   A->n_slices = (n + 31) / 32;
@@ -639,7 +654,7 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   memset(o, 0, sizeof(*o));
   o->n = A->n;
   o->nnz = A->nnz;
-  o->format = A->d_perm ? PCG_FORMAT_SELL_SIGMA : A->format;
+  o->format = A->sigma ? PCG_FORMAT_SELL_SIGMA : A->format;
   o->max_row_len = A->max_row_len;
   o->sell_entries = A->sell_entries;
   o->t_setup_s = A->t_setup_s;
@@ -656,5 +671,6 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->n_global = A->n_global;
   o->spmv_us_sigma = A->spmv_us_sigma;
   o->sigma = A->sigma;
+  o->reorder = A->reorder;
   return PCG_OK;
 }

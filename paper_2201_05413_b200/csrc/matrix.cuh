@@ -121,8 +121,10 @@ struct pcg_matrix {
   size_t dyn_smem = 0;        // dynamic shared memory of the chosen format's kernels
   int *d_lead = nullptr;      // per-tile prefix-max column (TMA L2 prefetch windows)
   // SELL-C-sigma: the device system is P A P^T (vectors in permuted order) when d_perm != null
+  // (also PCG_REORDER_RCM: perm = the RCM order, composed with the sigma sort if both)
   int *d_perm = nullptr, *d_iperm = nullptr;
   int sigma = 0;
+  int reorder = 0;  // 1: PCG_REORDER_RCM applied
   pcgb::SellView sell() const { return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0}; }
 };
 
@@ -137,6 +139,8 @@ int sigma_window();
 pcg_status sigma_build(pcg_matrix *A, cudaStream_t st, SigmaSys *S);
 void sigma_swap(pcg_matrix *A, SigmaSys *S);
 void sigma_free(SigmaSys *S);
+pcg_status apply_perm(pcg_matrix *A, int *perm, cudaStream_t st);
+pcg_status rcm_order(int64_t n, const int *rp, const int *col, int *perm, cudaStream_t st);
 pcg_status perm_in(pcg_matrix *A, const double *src_dev, double *dst, cudaStream_t st);
 pcg_status perm_out(pcg_matrix *A, const double *src, double *dst_dev, cudaStream_t st);
 pcg_status perm_in_cols(pcg_matrix *A, int k, const double *src, int64_t lds, double *dst, int64_t ldd, cudaStream_t st);

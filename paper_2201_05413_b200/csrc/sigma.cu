@@ -65,6 +65,12 @@ __global__ void invert_perm_kernel(int64_t n, const int *__restrict__ perm, int 
     iperm[perm[i]] = (int)i;
 }
 
+// p[i] = outer[p[i]]: a permutation of an already permuted system, in the caller's order
+__global__ void compose_perm_kernel(int64_t n, const int *__restrict__ outer, int *__restrict__ p) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = outer[p[i]];
+}
+
 __global__ void perm_len_kernel(int64_t n, const int *__restrict__ perm, const int *__restrict__ rp,
                                 const double *__restrict__ dinv, int *__restrict__ len2, double *__restrict__ dinv2) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -164,10 +170,54 @@ pcg_status sigma_build(pcg_matrix *A, cudaStream_t st, SigmaSys *S) {
   perm_fill_kernel<<<grid_for(n * 32), 256, 0, st>>>(n, S->perm, S->iperm, A->d_row_ptr, A->d_col, A->d_val, S->row_ptr,
                                                       S->col, S->val);
   count_launch(5);
+  if (A->d_perm) {  // A is already a permuted system (PCG_REORDER_RCM): compose to the caller's order
+    compose_perm_kernel<<<grid_for(n), 256, 0, st>>>(n, A->d_perm, S->perm);
+    invert_perm_kernel<<<grid_for(n), 256, 0, st>>>(n, S->perm, S->iperm);
+    count_launch(2);
+  }
   PCG_CUDA(cudaGetLastError());
   PCG_CUDA(cudaStreamSynchronize(st));
   cudaFree(tbuf);
   cudaFree(len2);
+  return PCG_OK;
+}
+
+// A := P A P^T for a full permutation (perm[i'] = row of A placed at i', device, n
+// ints; ownership passes to A).  Rows keep their entries in order, columns renamed
+// (as above); A must not hold SELL arrays yet.  Used by PCG_REORDER_RCM (rcm.cu).
+pcg_status apply_perm(pcg_matrix *A, int *perm, cudaStream_t st) {
+  const int64_t n = A->n, nnz = A->nnz;
+  int *iperm = nullptr, *rp2 = nullptr, *col2 = nullptr, *len2 = nullptr;
+  double *val2 = nullptr, *dinv2 = nullptr;
+  PCG_CUDA(cudaMalloc(&iperm, sizeof(int) * std::max<int64_t>(n, 1)));
+  PCG_CUDA(cudaMalloc(&rp2, sizeof(int) * (n + 1)));
+  PCG_CUDA(cudaMalloc(&len2, sizeof(int) * (n + 1)));
+  PCG_CUDA(cudaMalloc(&col2, sizeof(int) * std::max<int64_t>(nnz, 1)));
+  PCG_CUDA(cudaMalloc(&val2, sizeof(double) * std::max<int64_t>(nnz, 1)));
+  PCG_CUDA(cudaMalloc(&dinv2, sizeof(double) * std::max<int64_t>(n, 1)));
+  invert_perm_kernel<<<grid_for(n), 256, 0, st>>>(n, perm, iperm);
+  perm_len_kernel<<<grid_for(n + 1), 256, 0, st>>>(n, perm, A->d_row_ptr, A->d_dinv, len2, dinv2);
+  size_t tb = 0;
+  PCG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, len2, rp2, n + 1, st));
+  void *tbuf;
+  PCG_CUDA(cudaMalloc(&tbuf, tb));
+  PCG_CUDA(cub::DeviceScan::ExclusiveSum(tbuf, tb, len2, rp2, n + 1, st));
+  perm_fill_kernel<<<grid_for(n * 32), 256, 0, st>>>(n, perm, iperm, A->d_row_ptr, A->d_col, A->d_val, rp2, col2, val2);
+  count_launch(4);
+  PCG_CUDA(cudaGetLastError());
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(tbuf);
+  cudaFree(len2);
+  cudaFree(A->d_row_ptr);
+  cudaFree(A->d_col);
+  cudaFree(A->d_val);
+  cudaFree(A->d_dinv);
+  A->d_row_ptr = rp2;
+  A->d_col = col2;
+  A->d_val = val2;
+  A->d_dinv = dinv2;
+  A->d_perm = perm;
+  A->d_iperm = iperm;
   return PCG_OK;
 }
 
