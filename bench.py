@@ -198,6 +198,10 @@ def main():
     ap.add_argument("--ref-iters", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fmt", default="auto", choices=["auto", "csr", "sell", "sigma"])
+    ap.add_argument("--relabel", type=int, default=None, metavar="SEED",
+                    help="N4: number the mesh nodes in a seeded random order (an unordered mesher's output)")
+    ap.add_argument("--reorder", default="none", choices=["none", "rcm"],
+                    help="N4: reverse Cuthill-McKee (PCG_REORDER_RCM on one GPU; csr_rcm_order before the partition)")
     ap.add_argument("--drop-zeros", action="store_true",
                     help="store no explicit zero entries (PCG_DROP_ZEROS; C3' of SURVEY Q7, same iterates)")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "callbacks"],
@@ -239,10 +243,41 @@ def main():
     # ---- build the system on the device (setup, untimed)
     t_setup0 = time.perf_counter()
     comm = None
-    if world == 1:
+    reorder = "rcm" if args.reorder == "rcm" else None
+    if args.relabel is not None or (reorder and world > 1):
+        # the global system, numbered in a seeded random order (inputs.py) and/or
+        # put in RCM order: inside csr_create on one GPU (PCG_REORDER_RCM), by csr_rcm_order on
+        # the global pattern before the contiguous row partition on N GPUs
+        from paper_2201_05413_b200.inputs import relabel_csr_torch, relabel_order
+        P = fem_build(spec)
+        nnz = P["col"].numel()
+        rp, col, val, B = P["row_ptr"], P["col"], P["val"], P["B"]
+        del P
+        if args.relabel is not None:
+            q = relabel_order(n, args.relabel)
+            rp, col, val = relabel_csr_torch(rp, col, val, q)
+            B = B[torch.as_tensor(q, device=B.device)]
+        if reorder and world > 1:
+            o = pcg.csr_rcm_order(rp, col)
+            rp, col, val = relabel_csr_torch(rp, col, val, o)
+            B = B[o]
+        if world == 1:
+            r0, r1 = 0, n
+            A = pcg.Matrix.from_csr(rp, col, val, fmt=args.fmt, drop_zeros=args.drop_zeros, reorder=reorder)
+        else:
+            bounds = pcg.partition_rows(rp.cpu().numpy(), world)
+            r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+            e0, e1 = int(rp[r0]), int(rp[r1])
+            comm = pcg.Comm.host_callbacks() if cb else pcg.Comm.from_process_group()
+            A = pcg.Matrix.from_csr_dist(comm, n, r0, r1, (rp[r0:r1 + 1] - e0).contiguous(), col[e0:e1].contiguous(),
+                                         val[e0:e1].contiguous(), fmt=args.fmt, drop_zeros=args.drop_zeros)
+        P = {"B": B[r0:r1]}
+        del rp, col, val, B
+    elif world == 1:
         P = fem_build(spec)
         nnz = P["col"].numel()  # (the 3D element pattern has no closed form: problem_size gives -1)
-        A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"], fmt=args.fmt, drop_zeros=args.drop_zeros)
+        A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"], fmt=args.fmt, drop_zeros=args.drop_zeros,
+                                reorder=reorder)
         r0, r1 = 0, n
     else:
         rp_full = fem_build_rowptr(spec, n)
@@ -456,7 +491,9 @@ def main():
                            format={1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[stats["format"]], setup_s=round(t_setup, 3),
                            relres_true=max(i["relres_true"] for i in infos[-1]), k_rhs=kcols,
                            solver="jacobi-pcg" if args.solver == "pcg" else "pipelined jacobi-pcg (N3)",
-                           **({"drop_zeros": True, "nnz_given": nnz_given} if args.drop_zeros else {})),
+                           **({"drop_zeros": True, "nnz_given": nnz_given} if args.drop_zeros else {}),
+                           **({"relabel_seed": args.relabel} if args.relabel is not None else {}),
+                           **({"reorder": args.reorder, "n_ghost": stats["n_ghost"]} if reorder else {})),
             "throughput": {"cg_iterations_per_s": iters / (ms / 1e3),
                            "effective_GBps": iter_bytes(n, nnz, kcols) * iters / (ms / 1e3) / 1e9,
                            "spmv_GBps": spmv_gbs, "spmv_frac_of_hbm": spmv_gbs / hbm if spmv_gbs else None},

@@ -168,6 +168,38 @@ def test_bench_multi_rank_flow_on_one_gpu():
     assert line["config"]["relres_true"] <= 1e-10
 
 
+def test_bench_multi_rank_rcm_partition_on_one_gpu():
+    """bench.py --relabel/--reorder rcm with 2 ranks (N4): the randomly numbered C6 is put in
+    RCM order by csr_rcm_order on the global pattern before the partition; the halo per rank
+    is then an interface (compare: the oracle's halo of the RCM-ordered matrix), and the
+    solve meets the oracle's iteration count."""
+    import json
+    import subprocess
+    import sys
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2201_05413_b200 import inputs as I
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"), "--gpus", "2", "--comm",
+           "callbacks", "--config", "C6", "--c", "12", "--steps", "2", "--warmup", "1", "--relabel", "7",
+           "--reorder", "rcm", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    P = O.build_problem("C6", c=12, k=1)
+    A = P["A"]
+    q = I.relabel_order(A.n, 7)
+    Ar = O.Csr(A.n, *I.relabel_csr_numpy(A.row_ptr, A.col, A.val, q))
+    Ao = O.Csr(A.n, *I.relabel_csr_numpy(Ar.row_ptr, Ar.col, Ar.val, O.rcm(Ar)))
+    b = O.partition(Ao, 2)
+    assert line["config"]["n_ghost"] == len(O.halo(Ao, int(b[0]), int(b[1])))  # rank 0's halo
+    r = O.pcg(A, P["B"][:, 0], tol=1e-10)
+    it = line["config"]["iterations"]
+    assert abs(it - r.iterations) <= max(1, 0.02 * r.iterations), (it, r.iterations)
+
+
 def test_nccl_single_rank_distributed_handle():
     """The NCCL backend end to end on one GPU: unique id broadcast through a
     torch.distributed group, ncclCommInitRank, csr_create_dist, and the distributed

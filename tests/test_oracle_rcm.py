@@ -118,3 +118,18 @@ def test_rcm_bfs_level_invariants(n, seed):
     assert lv[-1] >= ecc_s
     # bandwidth of the Delaunay graph drops well below the random numbering's
     assert _bandwidth(A, p) < 0.25 * _bandwidth(A, np.arange(n))
+
+
+def test_rcm_partition_halos_shrink():
+    # N4 multi-GPU: contiguous row blocks of a randomly numbered mesh need almost every
+    # remote node as a ghost; of the RCM-ordered mesh, only the block interfaces
+    P = O.build_problem("C6", c=12, k=1)
+    A = P["A"]
+    q = I.relabel_order(A.n, 7)
+    Ar = O.Csr(A.n, *I.relabel_csr_numpy(A.row_ptr, A.col, A.val, q))
+    p = O.rcm(Ar)
+    Ao = O.Csr(A.n, *I.relabel_csr_numpy(Ar.row_ptr, Ar.col, Ar.val, p))
+    for G in (2, 4):
+        hr = [len(O.halo(Ar, int(b0), int(b1))) for b0, b1 in zip(O.partition(Ar, G)[:-1], O.partition(Ar, G)[1:])]
+        ho = [len(O.halo(Ao, int(b0), int(b1))) for b0, b1 in zip(O.partition(Ao, G)[:-1], O.partition(Ao, G)[1:])]
+        assert max(ho) < 0.25 * max(hr), (G, ho, hr)
