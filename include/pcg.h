@@ -108,6 +108,7 @@ typedef struct {
   double spmv_us_sigma;      /* autotune timing of SELL-C-sigma (0 if not tried) */
   int32_t sigma;             /* sorting window of SELL-C-sigma (0: natural row order) */
   int32_t reorder;           /* 1: the device system is RCM-reordered (PCG_REORDER_RCM) */
+  int64_t overlap_rows;      /* distributed: rows whose SpMV overlaps the halo exchange (0: off) */
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */

@@ -50,6 +50,7 @@ struct Scalars {
   double nb, tol, relres_rec, relres_true;
   double rho_part[2];  // (r.z, r.r) partial sums awaiting a cross-GPU allreduce
   double res_part[3];  // (w.w, w.z, b.b) of the residual pass
+  double sigma_acc;    // distributed overlap: p.q of the row ranges already done this iteration
   long long k, max_iter, replacements;
   int done, parity, stage;  // parity: p[parity] holds the latest direction p_k
   int pad0;

@@ -194,6 +194,63 @@ pcg_status allreduce_sum(pcg_matrix *A, double *buf, int count, cudaStream_t st)
   return comm_allreduce_f64(A->comm, buf, count, st);
 }
 
+// rows that reference a ghost column (need the halo before their SpMV)
+__global__ void ghost_rows_kernel(int64_t n, const int *__restrict__ rp, const int *__restrict__ col,
+                                  uint8_t *__restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t f = 0;
+    for (int k = rp[i]; k < rp[i + 1]; k++) f |= col[k] >= (int)n;
+    flag[i] = f;
+  }
+}
+
+// The longest run of rows without ghost columns, aligned to SELL slices, becomes the
+// interior range whose SpMV runs while the z halo is in flight (north_star
+// (c): "halos ... overlapped with the interior SpMV").  Contiguous blocks of a banded
+// order (lattice, RCM) have their boundary rows at both ends.  Off if the range is
+// under a quarter of the rows, for the TMA-staged format, or with PCG_NO_OVERLAP=1.
+static pcg_status overlap_plan(pcg_matrix *A, cudaStream_t st) {
+  A->ov = false;
+  const int64_t n = A->n;
+  if (getenv("PCG_NO_OVERLAP") || A->halo.nbr.empty() || n < 64) return PCG_OK;
+  if (A->format != PCG_FORMAT_SELL && A->format != PCG_FORMAT_CSR) return PCG_OK;
+  uint8_t *d_flag;
+  PCG_CUDA(cudaMalloc(&d_flag, n));
+  ghost_rows_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(n, A->d_row_ptr, A->d_col,
+                                                                                           d_flag);
+  count_launch();
+  std::vector<uint8_t> f(n);
+  PCG_CUDA(cudaMemcpyAsync(f.data(), d_flag, n, cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_flag);
+  int64_t best_a = 0, best_b = 0;
+  for (int64_t i = 0; i < n;) {
+    if (f[i]) {
+      i++;
+      continue;
+    }
+    int64_t j = i;
+    while (j < n && !f[j]) j++;
+    if (j - i > best_b - best_a) {
+      best_a = i;
+      best_b = j;
+    }
+    i = j;
+  }
+  const int64_t ia = best_a == 0 ? 0 : (best_a + 31) & ~int64_t(31);
+  const int64_t ib = best_b == n ? n : best_b & ~int64_t(31);
+  if (ib - ia < n / 4 || (ia == 0 && ib == n)) return PCG_OK;
+  if (!A->ov_side) {
+    PCG_CUDA(cudaStreamCreateWithFlags(&A->ov_side, cudaStreamNonBlocking));
+    PCG_CUDA(cudaEventCreateWithFlags(&A->ov_fork, cudaEventDisableTiming));
+    PCG_CUDA(cudaEventCreateWithFlags(&A->ov_join, cudaEventDisableTiming));
+  }
+  A->ov_ia = ia;
+  A->ov_ib = ib;
+  A->ov = true;
+  return PCG_OK;
+}
+
 static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, int64_t r1, int64_t nnz,
                                    const int64_t *row_ptr, const int64_t *col, const double *val, int flags,
                                    cudaStream_t st, pcg_matrix *A) {
@@ -323,6 +380,7 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
   A->row_end = r1;
   A->n_global = n_global;
   pcg_status s = create_local(A, n, nnz, drp, dcol, dloc, dval, n_global, r0, flags, st);
+  if (s == PCG_OK) s = overlap_plan(A, st);
   cudaStreamSynchronize(st);
   // all ranks fail together (a local validation error must not leave peers waiting)
   {

@@ -640,6 +640,9 @@ extern "C" pcg_status csr_destroy(pcg_matrix_t A) {
   cudaSetDevice(A->device);
   cudaDeviceSynchronize();
   free_work(A);
+  if (A->ov_side) cudaStreamDestroy(A->ov_side);
+  if (A->ov_fork) cudaEventDestroy(A->ov_fork);
+  if (A->ov_join) cudaEventDestroy(A->ov_join);
   for (void *p : {(void *)A->d_row_ptr, (void *)A->d_col, (void *)A->d_val, (void *)A->d_dinv,
                   (void *)A->d_slice_ptr, (void *)A->d_scol, (void *)A->d_sval, (void *)A->d_lead, (void *)A->halo.d_send_idx,
                   (void *)A->d_perm, (void *)A->d_iperm,
@@ -672,5 +675,6 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->spmv_us_sigma = A->spmv_us_sigma;
   o->sigma = A->sigma;
   o->reorder = A->reorder;
+  o->overlap_rows = A->ov ? A->ov_ib - A->ov_ia : 0;
   return PCG_OK;
 }

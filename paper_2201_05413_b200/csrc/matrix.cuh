@@ -125,6 +125,12 @@ struct pcg_matrix {
   int *d_perm = nullptr, *d_iperm = nullptr;
   int sigma = 0;
   int reorder = 0;  // 1: PCG_REORDER_RCM applied
+  // distributed: halo exchange overlapped with the interior SpMV (dist.cu overlap_plan).
+  // Rows [ov_ia, ov_ib) reference no ghost; the z halo runs on ov_side meanwhile.
+  bool ov = false;
+  int64_t ov_ia = 0, ov_ib = 0;
+  cudaStream_t ov_side = nullptr;
+  cudaEvent_t ov_fork = nullptr, ov_join = nullptr;
   pcgb::SellView sell() const { return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0}; }
 };
 

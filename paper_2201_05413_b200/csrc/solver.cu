@@ -241,9 +241,11 @@ __global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, 
 }
 
 template <int FMT, int L>
+// row0/phase: the distributed overlap runs K1b over row ranges (views offset by row0);
+// phase 1 starts p.q (sigma_acc = local), 3 adds to it, 2 completes it (sigma = acc + local)
 __global__ void __launch_bounds__(BLOCK) k1b_kernel(SellView S, CsrView C, int64_t n_ghost, Vecs v, Scalars *sc,
                                                     double *partials, int dist, int use_cond,
-                                                    cudaGraphConditionalHandle h) {
+                                                    cudaGraphConditionalHandle h, int64_t row0, int phase) {
   __shared__ double sm[1][WARPS];
   const volatile Scalars *vs = sc;
   if (vs->done != DONE_RUNNING) {
@@ -251,12 +253,13 @@ __global__ void __launch_bounds__(BLOCK) k1b_kernel(SellView S, CsrView C, int64
     return;
   }
   const double *__restrict__ p = v.p0;
-  double *__restrict__ q = v.q;
+  double *__restrict__ q = v.q + row0;
+  const double *__restrict__ pr = v.p0 + row0;
   double acc = 0.0;
   auto gather = [&](int j) { return __ldg(p + j); };
   auto epi = [&](int64_t i, double s) {
     __stcs(q + i, s);
-    acc = __fma_rn(__ldg(p + i), s, acc);
+    acc = __fma_rn(__ldg(pr + i), s, acc);
   };
   if (FMT == FMT_SELL_TMA) {
     StageIO<0, 1> io;
@@ -277,7 +280,13 @@ __global__ void __launch_bounds__(BLOCK) k1b_kernel(SellView S, CsrView C, int64
     reduce_partials<1>(partials, tot, sm);
     if (threadIdx.x == 0) {
       sc->cnt_a = 0;
-      if (dist) {
+      if (phase == 1) {
+        sc->sigma_acc = tot[0];
+      } else if (phase == 3) {
+        sc->sigma_acc += tot[0];
+      } else if (phase == 2) {
+        sc->sigma = sc->sigma_acc + tot[0];
+      } else if (dist) {
         sc->sigma = tot[0];
         sc->graph_launches += use_cond;
       } else {
@@ -285,6 +294,15 @@ __global__ void __launch_bounds__(BLOCK) k1b_kernel(SellView S, CsrView C, int64
       }
     }
   }
+}
+
+// distributed overlap: ghost copies of p advance once the z halo has arrived
+__global__ void __launch_bounds__(BLOCK) ghost_p_kernel(int64_t n, int64_t n_ghost, Vecs v, const Scalars *sc) {
+  const volatile Scalars *vs = sc;
+  if (vs->done != DONE_RUNNING) return;
+  const double beta = vs->beta;
+  for (int64_t g = (int64_t)blockIdx.x * BLOCK + threadIdx.x; g < n_ghost; g += (int64_t)gridDim.x * BLOCK)
+    v.p0[n + g] = __fma_rn(beta, v.p0[n + g], v.z[n + g]);
 }
 
 // distributed finishers (after the NCCL allreduce of the partials)
@@ -470,12 +488,57 @@ static int k1_chunk() {  // tuning knob (PCG_K1_CHUNK=4|8), default 8
 static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
   Vecs v = vecs_of(A);
   SolveWork &w = A->work;
+  if (A->schedule == 3 && A->comm && A->ov) {
+    // halo of z on the side stream || K1a (owned rows) + K1b over the interior rows;
+    // then the ghost p update and K1b over the boundary rows (head, tail)
+    PCG_CUDA(cudaEventRecord(A->ov_fork, st));
+    PCG_CUDA(cudaStreamWaitEvent(A->ov_side, A->ov_fork, 0));
+    PCG_TRY(halo_exchange(A, w.z, 1, A->ov_side));
+    PCG_CUDA(cudaEventRecord(A->ov_join, A->ov_side));
+    k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, 0, v, w.sc, use_cond, h);
+    count_launch();
+    struct Range {
+      int64_t r0, r1;
+    } rs[3] = {{A->ov_ia, A->ov_ib}, {0, A->ov_ia}, {A->ov_ib, A->n}};
+    int last = rs[2].r1 > rs[2].r0 ? 2 : 1;
+    for (int t = 0; t <= last; t++) {
+      const Range R = rs[t];
+      if (t == 1) {  // boundary rows need the ghosts: join the halo, advance ghost p
+        PCG_CUDA(cudaStreamWaitEvent(st, A->ov_join, 0));
+        ghost_p_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((A->n_ghost + BLOCK - 1) / BLOCK, 1184)),
+                         BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc);
+        count_launch();
+      }
+      if (R.r1 <= R.r0) continue;
+      const int phase = t == 0 ? 1 : (t == last ? 2 : 3);
+      SellView S = A->sell();
+      CsrView Cv = A->csr();
+      const int64_t s0 = R.r0 / 32, s1 = R.r1 == A->n ? A->n_slices : R.r1 / 32;
+      S.slice_ptr += s0;
+      S.n_slices = s1 - s0;
+      S.n = R.r1 - R.r0;
+      Cv.row_ptr += R.r0;
+      Cv.n = R.r1 - R.r0;
+      const int64_t need = A->format == PCG_FORMAT_SELL ? (S.n_slices + WARPS - 1) / WARPS
+                                                       : (Cv.n * A->csr_lanes + BLOCK - 1) / BLOCK;
+      const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(A->grid_spmv, need));
+      PCG_DISPATCH(A->format, A->csr_lanes, k1b_kernel,
+                   <<<g, BLOCK, A->dyn_smem, st>>>(S, Cv, A->n_ghost, v, w.sc, w.partials, 1, use_cond, h, R.r0,
+                                                  phase));
+      count_launch();
+    }
+    PCG_CUDA(cudaGetLastError());
+    PCG_TRY(allreduce_sum(A, &w.sc->sigma, 1, st));
+    finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h, 0);
+    count_launch();
+    return PCG_OK;
+  }
   if (A->schedule == 3) {  // K1a (streaming p/x update) + K1b (SpMV + sigma)
     k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, use_cond, h);
     count_launch();
     PCG_DISPATCH(A->format, A->csr_lanes, k1b_kernel,
                  <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
-                                                            A->comm ? 1 : 0, use_cond, h));
+                                                            A->comm ? 1 : 0, use_cond, h, 0, 0));
     count_launch();
     PCG_CUDA(cudaGetLastError());
     if (A->comm) {
@@ -513,8 +576,8 @@ static pcg_status launch_k2(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     PCG_TRY(allreduce_sum(A, w.sc->rho_part, 2, st));
     finish_beta_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h);
     count_launch();
-    // ghosts of z for the next K1 (z is final after K2)
-    PCG_TRY(halo_exchange(A, w.z, 1, st));
+    // ghosts of z for the next K1 (z is final after K2); the overlapped K1 exchanges them itself
+    if (!(A->ov && A->schedule == 3)) PCG_TRY(halo_exchange(A, w.z, 1, st));
   }
   return PCG_OK;
 }
@@ -858,7 +921,7 @@ extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32
       PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
       PCG_DISPATCH(A->format, A->csr_lanes, k1b_kernel,
                    <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
-                                                              0, 0, 0));
+                                                              0, 0, 0, 0, 0));
       count_launch(2);
     } else {
       PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));

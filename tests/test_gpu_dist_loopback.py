@@ -56,7 +56,7 @@ def _worker(rank, world, port, name, c, use_generator, out_q, drop=False):
         xp, infop = M.solve_pipelined(bl, tol=1e-10)  # N3: one allreduce per iteration
         xr = np.random.default_rng(100 + rank).standard_normal(r1 - r0)
         y = M.spmv(torch.as_tensor(xr).cuda()).cpu().numpy()
-        out_q.put((rank, dict(r0=r0, r1=r1, n_ghost=st["n_ghost"], x=x.cpu().numpy(), info=info, xr=xr, y=y,
+        out_q.put((rank, dict(r0=r0, r1=r1, n_ghost=st["n_ghost"], overlap_rows=st["overlap_rows"], x=x.cpu().numpy(), info=info, xr=xr, y=y,
                               b=bl.cpu().numpy(), xp=xp.cpu().numpy(), infop=infop)))
         M.close()
         comm.close()
@@ -101,6 +101,8 @@ def test_distributed_path_on_one_gpu(world, name, c, gen, drop):
     for g, d in enumerate(parts):
         assert (d["r0"], d["r1"]) == (bounds[g], bounds[g + 1])
         assert d["n_ghost"] == len(O.halo(A, d["r0"], d["r1"]))
+    # the banded configs run the overlapped schedule (interior SpMV while the halo is in flight)
+    assert all(d["overlap_rows"] > 0 for d in parts)
     bg = np.concatenate([d["b"] for d in parts])
     scale = np.max(np.abs(b))
     assert np.all(np.abs(bg - b) <= 1e-12 * scale)  # generator RHS (exact copy otherwise)
