@@ -489,13 +489,12 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
   Vecs v = vecs_of(A);
   SolveWork &w = A->work;
   if (A->schedule == 3 && A->comm && A->ov) {
-    // halo of z on the side stream || K1a (owned rows) + K1b over the interior rows;
-    // then the ghost p update and K1b over the boundary rows (head, tail)
+    // K1a (owned rows) + K1b over the interior rows on the side stream || the z halo on
+    // the main stream (every NCCL call stays on one stream, in one order on all ranks);
+    // after the join the ghost p update and K1b over the boundary rows (head, tail)
     PCG_CUDA(cudaEventRecord(A->ov_fork, st));
     PCG_CUDA(cudaStreamWaitEvent(A->ov_side, A->ov_fork, 0));
-    PCG_TRY(halo_exchange(A, w.z, 1, A->ov_side));
-    PCG_CUDA(cudaEventRecord(A->ov_join, A->ov_side));
-    k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, 0, v, w.sc, use_cond, h);
+    k1a_kernel<<<A->grid_vec, BLOCK, 0, A->ov_side>>>(A->n, 0, v, w.sc, use_cond, h);
     count_launch();
     struct Range {
       int64_t r0, r1;
@@ -503,7 +502,9 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     int last = rs[2].r1 > rs[2].r0 ? 2 : 1;
     for (int t = 0; t <= last; t++) {
       const Range R = rs[t];
-      if (t == 1) {  // boundary rows need the ghosts: join the halo, advance ghost p
+      if (t == 1) {  // boundary rows need the ghosts: halo, join, advance ghost p
+        PCG_CUDA(cudaEventRecord(A->ov_join, A->ov_side));
+        PCG_TRY(halo_exchange(A, w.z, 1, st));
         PCG_CUDA(cudaStreamWaitEvent(st, A->ov_join, 0));
         ghost_p_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((A->n_ghost + BLOCK - 1) / BLOCK, 1184)),
                          BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc);
@@ -522,8 +523,9 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
       const int64_t need = A->format == PCG_FORMAT_SELL ? (S.n_slices + WARPS - 1) / WARPS
                                                        : (Cv.n * A->csr_lanes + BLOCK - 1) / BLOCK;
       const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(A->grid_spmv, need));
+      cudaStream_t ks = t == 0 ? A->ov_side : st;
       PCG_DISPATCH(A->format, A->csr_lanes, k1b_kernel,
-                   <<<g, BLOCK, A->dyn_smem, st>>>(S, Cv, A->n_ghost, v, w.sc, w.partials, 1, use_cond, h, R.r0,
+                   <<<g, BLOCK, A->dyn_smem, ks>>>(S, Cv, A->n_ghost, v, w.sc, w.partials, 1, use_cond, h, R.r0,
                                                   phase));
       count_launch();
     }
