@@ -392,16 +392,18 @@ def halo_recv_plan(ghosts, bounds):
 # ---------------------------------------------------------------- the C ABI's names
 # (include/pcg.h, include/fem_gen.h): thin aliases of the methods above, so a caller
 # can follow the header entry point by entry point.  Argument marshalling only.
-def csr_create(row_ptr, col, val, fmt: str = "auto", stream=None) -> Matrix:
-    """include/pcg.h csr_create: validate, narrow and upload a CSR matrix (host or device tensors)."""
-    return Matrix.from_csr(row_ptr, col, val, fmt=fmt, stream=stream)
+def csr_create(row_ptr, col, val, fmt: str = "auto", stream=None, drop_zeros: bool = False,
+               reorder: str | None = None) -> Matrix:
+    """include/pcg.h csr_create: validate, narrow and upload a CSR matrix (host or device tensors);
+    drop_zeros -> PCG_DROP_ZEROS, reorder="rcm" -> PCG_REORDER_RCM."""
+    return Matrix.from_csr(row_ptr, col, val, fmt=fmt, stream=stream, drop_zeros=drop_zeros, reorder=reorder)
 
 
 def csr_create_dist(comm: Comm, n_global: int, row_begin: int, row_end: int, row_ptr_local, col_global, val,
-                    fmt: str = "auto", stream=None) -> Matrix:
+                    fmt: str = "auto", stream=None, drop_zeros: bool = False) -> Matrix:
     """include/pcg.h csr_create_dist: this rank's rows [row_begin, row_end) with global column ids."""
     return Matrix.from_csr_dist(comm, n_global, row_begin, row_end, row_ptr_local, col_global, val, fmt=fmt,
-                                stream=stream)
+                                stream=stream, drop_zeros=drop_zeros)
 
 
 def csr_destroy(A: Matrix) -> None:
@@ -436,6 +438,7 @@ def pcg_bicgstab(A: Matrix, b, x0=None, tol: float = 1e-10, max_iter: int = 5000
 
 
 pcg_partition_rows = partition_rows
+solve = pcg_solve  # SURVEY §8(b) "Python: pcg.solve(A, b, x0, tol, max_iter)"
 
 __all__ += ["csr_create", "csr_create_dist", "csr_destroy", "pcg_spmv", "pcg_solve", "pcg_solve_multi",
-            "pcg_solve_pipelined", "pcg_bicgstab", "pcg_partition_rows"]
+            "pcg_solve_pipelined", "pcg_bicgstab", "pcg_partition_rows", "csr_rcm_order", "solve"]

@@ -82,5 +82,5 @@ def test_python_binding_has_the_abi_names():
     """The binding exposes the C ABI's entry points under their header names (no GPU needed)."""
     import paper_2201_05413_b200 as pcg
     for name in ("csr_create", "csr_create_dist", "csr_destroy", "pcg_spmv", "pcg_solve", "pcg_solve_multi",
-                 "pcg_bicgstab", "pcg_partition_rows", "coo_to_csr"):
+                 "pcg_bicgstab", "pcg_partition_rows", "coo_to_csr", "csr_rcm_order", "pcg_solve_pipelined", "solve"):
         assert callable(getattr(pcg, name)), name
