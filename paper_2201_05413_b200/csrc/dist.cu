@@ -212,8 +212,22 @@ __global__ void ghost_rows_kernel(int64_t n, const int *__restrict__ rp, const i
 static pcg_status overlap_plan(pcg_matrix *A, cudaStream_t st) {
   A->ov = false;
   const int64_t n = A->n;
-  if (getenv("PCG_NO_OVERLAP") || A->halo.nbr.empty() || n < 64) return PCG_OK;
+  // PCG_FORCE_OVERLAP=1 (tests): the split schedule even without a halo (1-rank NCCL handle),
+  // interior = the middle half, so the captured fork/join graph runs on one GPU
+  const bool force = getenv("PCG_FORCE_OVERLAP") && n >= 256;
+  if (getenv("PCG_NO_OVERLAP") || ((A->halo.nbr.empty() || n < 64) && !force)) return PCG_OK;
   if (A->format != PCG_FORMAT_SELL && A->format != PCG_FORMAT_CSR) return PCG_OK;
+  if (force) {
+    if (!A->ov_side) {
+      PCG_CUDA(cudaStreamCreateWithFlags(&A->ov_side, cudaStreamNonBlocking));
+      PCG_CUDA(cudaEventCreateWithFlags(&A->ov_fork, cudaEventDisableTiming));
+      PCG_CUDA(cudaEventCreateWithFlags(&A->ov_join, cudaEventDisableTiming));
+    }
+    A->ov_ia = (n / 4) & ~int64_t(31);
+    A->ov_ib = (3 * n / 4) & ~int64_t(31);
+    A->ov = true;
+    return PCG_OK;
+  }
   uint8_t *d_flag;
   PCG_CUDA(cudaMalloc(&d_flag, n));
   ghost_rows_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(n, A->d_row_ptr, A->d_col,

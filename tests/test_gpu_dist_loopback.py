@@ -202,11 +202,15 @@ def test_bench_multi_rank_rcm_partition_on_one_gpu():
     assert abs(it - r.iterations) <= max(1, 0.02 * r.iterations), (it, r.iterations)
 
 
-def test_nccl_single_rank_distributed_handle():
+@pytest.mark.parametrize("force_overlap", [False, True])
+def test_nccl_single_rank_distributed_handle(force_overlap, monkeypatch):
     """The NCCL backend end to end on one GPU: unique id broadcast through a
     torch.distributed group, ncclCommInitRank, csr_create_dist, and the distributed
     solve loop whose graph captures ncclAllReduce (a 1-rank communicator still issues
-    every collective).  Against the oracle."""
+    every collective).  Against the oracle.  force_overlap: the split K1 schedule
+    (side-stream fork/join captured in the NCCL loop graph, three row ranges)."""
+    if force_overlap:
+        monkeypatch.setenv("PCG_FORCE_OVERLAP", "1")
     import torch
     import torch.distributed as dist
     if not torch.cuda.is_available():
@@ -220,6 +224,7 @@ def test_nccl_single_rank_distributed_handle():
         comm = pcg.Comm.from_process_group()
         M = pcg.Matrix.from_csr_dist(comm, A.n, 0, A.n, torch.as_tensor(A.row_ptr).cuda(),
                                      torch.as_tensor(A.col).cuda(), torch.as_tensor(A.val).cuda())
+        assert (M.stats()["overlap_rows"] > 0) == force_overlap
         x, info = M.solve(torch.as_tensor(b).cuda(), tol=1e-10)
         r = O.pcg(A, b, tol=1e-10)
         assert info["status"] == 0 and info["relres_true"] <= 1e-10
