@@ -87,6 +87,8 @@ def lib():
                                         C.c_void_p, C.c_void_p]
         L.orc_halo.argtypes = [P(_Csr), C.c_int64, C.c_int64, C.c_void_p, C.c_int64]
         L.orc_rcm.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_block_cg.argtypes = [P(_Csr), C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_void_p,
+                                   C.c_void_p]
         L.orc_fd_identity_rows_nnz.restype = C.c_int64
         L.orc_fd_identity_rows_nnz.argtypes = [C.c_int64]
         _lib = L
@@ -290,6 +292,21 @@ def coo_to_csr(n_rows: int, n_cols: int, row, col, val):
     if st != OK:
         raise RuntimeError(f"orc_coo_to_csr: {st}")
     return rp, co[:u.value].copy(), vo[:u.value].copy()
+
+
+def block_cg(A: Csr, B, X0=None, tol=1e-10, max_iter=50000):
+    """SURVEY §8(f) N3 (reading R5): block CG with the Jacobi M (oracle.h orc_block_cg).
+    B: (n, k).  Returns (X (n, k), iterations, relres_true (k,), status)."""
+    B = np.asarray(B, dtype=np.float64)
+    n, k = B.shape
+    Bc = np.asfortranarray(B)
+    X = np.asfortranarray(np.zeros((n, k)) if X0 is None else np.array(X0, dtype=np.float64))
+    it = C.c_int64(0)
+    rt = np.zeros(k)
+    Ac = A._c()
+    st = lib().orc_block_cg(C.byref(Ac), k, Bc.ctypes.data_as(C.c_void_p), X.ctypes.data_as(C.c_void_p), tol,
+                            max_iter, C.byref(it), rt.ctypes.data_as(C.c_void_p))
+    return np.ascontiguousarray(X), it.value, rt, st
 
 
 def rcm(A: Csr):

@@ -1177,3 +1177,155 @@ int orc_rcm(int64_t n, const int64_t *row_ptr, const int64_t *col, int64_t *perm
   free(deg); free(lvl); free(queue); free(order); free(placed);
   return ORC_OK;
 }
+
+/* ---------------------------------------------------------------------------
+ * block CG (oracle.h orc_block_cg)
+ * ------------------------------------------------------------------------- */
+/* Solve G Y = C for m x m row-major G (symmetric) and C by Cholesky G = L L^T;
+ * -1 if a pivot is not positive. */
+static int chol_solve(int m, const double *G, const double *C, double *Y) {
+  double *L = calloc((size_t)m * m, sizeof(double));
+  if (!L) return -2;
+  for (int j = 0; j < m; j++) {
+    double d = G[j * m + j];
+    for (int t = 0; t < j; t++) d -= L[j * m + t] * L[j * m + t];
+    if (!(d > 0.0)) { free(L); return -1; }
+    L[j * m + j] = sqrt(d);
+    for (int i = j + 1; i < m; i++) {
+      double s = G[i * m + j];
+      for (int t = 0; t < j; t++) s -= L[i * m + t] * L[j * m + t];
+      L[i * m + j] = s / L[j * m + j];
+    }
+  }
+  for (int c = 0; c < m; c++) {
+    for (int i = 0; i < m; i++) { /* forward: L u = C[:, c] */
+      double s = C[i * m + c];
+      for (int t = 0; t < i; t++) s -= L[i * m + t] * Y[t * m + c];
+      Y[i * m + c] = s / L[i * m + i];
+    }
+    for (int i = m - 1; i >= 0; i--) { /* backward: L^T y = u */
+      double s = Y[i * m + c];
+      for (int t = i + 1; t < m; t++) s -= L[t * m + i] * Y[t * m + c];
+      Y[i * m + c] = s / L[i * m + i];
+    }
+  }
+  free(L);
+  return 0;
+}
+
+/* out[a][b] = sum_i U[i][a] V[i][b] for n x m blocks (column-major, ld = n) */
+static void block_gram(int64_t n, int m, const double *U, const double *V, double *out) {
+  for (int a = 0; a < m; a++)
+    for (int b = 0; b < m; b++) out[a * m + b] = dot(n, U + (size_t)a * n, V + (size_t)b * n);
+}
+
+int orc_block_cg(const orc_csr *A, int k, const double *B, double *X, double tol, int64_t max_iter, int64_t *iters,
+                 double *relres_true) {
+  const int64_t n = A->n;
+  *iters = 0;
+  if (n < 0 || k < 1 || !(tol > 0.0) || max_iter < 1) return ORC_ERR_INVALID_ARG;
+  for (int j = 0; j < k; j++) relres_true[j] = 0.0;
+  const size_t N = (size_t)(n > 0 ? n : 1);
+  int *col = malloc(sizeof(int) * k);
+  double *nb = malloc(sizeof(double) * k);
+  double *dinv = malloc(sizeof(double) * N);
+  double *R = malloc(sizeof(double) * N * k), *Z = malloc(sizeof(double) * N * k);
+  double *P = malloc(sizeof(double) * N * k), *Q = malloc(sizeof(double) * N * k);
+  double *Xm = malloc(sizeof(double) * N * k), *T = malloc(sizeof(double) * N * k);
+  double *G = malloc(sizeof(double) * k * k), *Gam = malloc(sizeof(double) * k * k);
+  double *Gn = malloc(sizeof(double) * k * k), *al = malloc(sizeof(double) * k * k);
+  if (!col || !nb || !dinv || !R || !Z || !P || !Q || !Xm || !T || !G || !Gam || !Gn || !al) return ORC_ERR_OOM;
+  int st = ORC_OK, m = 0;
+  for (int64_t i = 0; i < n; i++) {
+    int64_t kd = csr_find(A, i, i);
+    double d = kd >= 0 ? A->val[kd] : 0.0;
+    if (d == 0.0) { st = ORC_ERR_ZERO_DIAGONAL; goto out; }
+    if (d < 0.0) { st = ORC_ERR_NOT_SPD; goto out; }
+    dinv[i] = 1.0 / d;
+  }
+  /* the columns with b_j != 0, in order; the others are x_j = 0 */
+  for (int j = 0; j < k; j++) {
+    double s = sqrt(dot(n, B + (size_t)j * n, B + (size_t)j * n));
+    if (s == 0.0) {
+      for (int64_t i = 0; i < n; i++) X[(size_t)j * n + i] = 0.0;
+    } else {
+      nb[m] = s;
+      col[m] = j;
+      for (int64_t i = 0; i < n; i++) Xm[(size_t)m * n + i] = X[(size_t)j * n + i];
+      m++;
+    }
+  }
+  if (m == 0) goto out;
+  int64_t it = 0;
+  int restart = 1;
+  for (;;) {
+    if (restart) {
+      int conv = 1;
+      for (int a = 0; a < m; a++) {
+        orc_spmv(A, Xm + (size_t)a * n, Q + (size_t)a * n);
+        for (int64_t i = 0; i < n; i++) R[(size_t)a * n + i] = B[(size_t)col[a] * n + i] - Q[(size_t)a * n + i];
+        if (!(sqrt(dot(n, R + (size_t)a * n, R + (size_t)a * n)) <= tol * nb[a])) conv = 0;
+      }
+      if (conv) break; /* -> exit check */
+      for (size_t e = 0; e < (size_t)m * n; e++) Z[e] = dinv[e % (size_t)n] * R[e];
+      for (size_t e = 0; e < (size_t)m * n; e++) P[e] = Z[e];
+      block_gram(n, m, R, Z, Gam);
+      restart = 0;
+    }
+    if (it >= max_iter) { st = ORC_NOT_CONVERGED; break; }
+    for (int a = 0; a < m; a++) orc_spmv(A, P + (size_t)a * n, Q + (size_t)a * n);
+    it++;
+    block_gram(n, m, P, Q, G);
+    if (chol_solve(m, G, Gam, al) != 0) { st = ORC_ERR_NOT_SPD; break; }
+    /* X += P alpha ; R -= Q alpha */
+    for (int c = 0; c < m; c++)
+      for (int64_t i = 0; i < n; i++) {
+        double sx = Xm[(size_t)c * n + i], sr = R[(size_t)c * n + i];
+        for (int b = 0; b < m; b++) {
+          sx += P[(size_t)b * n + i] * al[b * m + c];
+          sr -= Q[(size_t)b * n + i] * al[b * m + c];
+        }
+        Xm[(size_t)c * n + i] = sx;
+        R[(size_t)c * n + i] = sr;
+      }
+    int conv = 1;
+    for (int a = 0; a < m; a++)
+      if (!(sqrt(dot(n, R + (size_t)a * n, R + (size_t)a * n)) <= tol * nb[a])) conv = 0;
+    if (conv) {
+      int ok = 1;
+      for (int a = 0; a < m; a++)
+        if (!(true_relres(A, B + (size_t)col[a] * n, Xm + (size_t)a * n, nb[a], T) <= tol)) ok = 0;
+      if (ok) break;
+      restart = 1;
+      continue;
+    }
+    for (size_t e = 0; e < (size_t)m * n; e++) Z[e] = dinv[e % (size_t)n] * R[e];
+    block_gram(n, m, R, Z, Gn);
+    double *be = G; /* (G is free now) */
+    if (chol_solve(m, Gam, Gn, be) != 0) { st = ORC_ERR_NOT_SPD; break; }
+    /* P = Z + P beta */
+    for (int64_t i = 0; i < n; i++) {
+      double row[32 * 8];
+      double *pr = m <= 256 ? row : NULL;
+      if (!pr) { st = ORC_ERR_INVALID_ARG; break; }
+      for (int b = 0; b < m; b++) pr[b] = P[(size_t)b * n + i];
+      for (int c = 0; c < m; c++) {
+        double s = Z[(size_t)c * n + i];
+        for (int b = 0; b < m; b++) s += pr[b] * be[b * m + c];
+        P[(size_t)c * n + i] = s;
+      }
+    }
+    if (st != ORC_OK) break;
+    for (int e = 0; e < m * m; e++) Gam[e] = Gn[e];
+  }
+  *iters = it;
+  for (int a = 0; a < m; a++) {
+    for (int64_t i = 0; i < n; i++) X[(size_t)col[a] * n + i] = Xm[(size_t)a * n + i];
+    relres_true[col[a]] = true_relres(A, B + (size_t)col[a] * n, Xm + (size_t)a * n, nb[a], T);
+    if (st == ORC_OK && !(relres_true[col[a]] <= tol)) st = ORC_NOT_CONVERGED;
+  }
+out:
+  free(col); free(nb); free(dinv); free(R); free(Z); free(P); free(Q); free(Xm); free(T);
+  free(G); free(Gam); free(Gn); free(al);
+  return st;
+}

@@ -128,6 +128,21 @@ int orc_pcg_pipelined(const orc_csr *A, const double *b, double *x, double tol, 
 int orc_coo_to_csr(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t *row, const int64_t *col,
                    const double *val, int64_t *row_ptr, int64_t *col_out, double *val_out, int64_t *nnz_out);
 
+/* SURVEY §8(f) N3 (reading R5): block conjugate gradients (O'Leary 1980, "The block
+ * conjugate gradient algorithm and related methods", Lin. Alg. Appl. 29) with the
+ * Jacobi M: the k right-hand sides share one Krylov space.  B, X column-major n x k
+ * (ld = n), X in/out.  Columns with b_j = 0 get x_j = 0 and are left out.  With
+ * the m remaining columns as n x m blocks:
+ *   R = B - A X; Z = M^-1 R; P = Z; Gam = R^T Z
+ *   loop: Q = A P; G = P^T Q; alpha = G^-1 Gam; X += P alpha; R -= Q alpha;
+ *         stop test (every column: ||r_j|| <= tol ||b_j||, then the true residuals
+ *         decide; replacement = restart from X otherwise);
+ *         Z = M^-1 R; Gam' = R^T Z; beta = Gam^-1 Gam'; P = Z + P beta; Gam = Gam'.
+ * k x k systems by Cholesky; a non-positive pivot is ORC_ERR_NOT_SPD (breakdown).
+ * *iters = number of block products A P.  relres_true[k] per column. */
+int orc_block_cg(const orc_csr *A, int k, const double *B, double *X, double tol, int64_t max_iter, int64_t *iters,
+                 double *relres_true);
+
 /* reverse Cuthill-McKee ordering of the graph of a symmetric
  * pattern (edges = off-diagonal entries; explicit zeros are edges).  Plain
  * sequential algorithm (Cuthill & McKee 1969, reversed per George 1971), start
