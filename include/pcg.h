@@ -157,6 +157,22 @@ pcg_status pcg_solve_multi(pcg_matrix_t A, int32_t k, const double *B, int64_t l
                            int64_t ldx, double tol, int64_t max_iter, void *stream,
                            pcg_info *infos);
 
+/* SURVEY §8(f) N3 (reading R5): block conjugate gradients (O'Leary 1980)
+ * with the Jacobi M.  The k columns share one block Krylov space, so every column
+ * converges in about as many steps as the fastest independent solve needs (C4: 366
+ * products instead of 549-578), at the cost of two k x k Gram matrices and two k x k
+ * Cholesky solves per step.  The iterates differ from pcg_solve_multi's (parity
+ * against the oracle's orc_block_cg).  Arguments as pcg_solve_multi; 1 <= k <= 32
+ * (one block); one-GPU handles.  Columns with b_j = 0 get x_j = 0 and leave the
+ * block.  All columns stop together: each column's recurrence residual <= tol
+ * ||b_j||, then the true residuals decide (restart from X otherwise).  Every info
+ * carries the shared iteration count; bytes_algorithmic is the block's divided by
+ * the active columns.  Returns OK, NOT_CONVERGED, NOT_SPD (a k x k Gram matrix not
+ * positive definite: breakdown, e.g. linearly dependent right-hand sides), or an
+ * error. */
+pcg_status pcg_solve_block(pcg_matrix_t A, int32_t k, const double *B, int64_t ldb, double *X, int64_t ldx,
+                           double tol, int64_t max_iter, void *stream, pcg_info *infos);
+
 /* ---------------------------------------------------------------- BiCGSTAB (§8(f) N2) */
 /* Right-preconditioned BiCGSTAB (van der Vorst 1992) — the Krylov solver the paper
  * selects — with Block-Jacobi M: block_size = 1 is point

@@ -208,6 +208,14 @@ class Matrix:
         pass B as B.T.contiguous().T or let this wrapper arrange it).  With `out` (an (n, k)
         float64 column-major tensor on B's device, i.e. out.t() contiguous), out holds X0 on
         entry and the solutions on return, and no copies are made around the library call."""
+        return self._solve_k("pcg_solve_multi", B, X0, tol, max_iter, stream, out)
+
+    def solve_block(self, B, X0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None, out=None):
+        """include/pcg.h pcg_solve_block: block CG over the k <= 32 columns of B (one shared
+        Krylov space).  Arguments and results as solve_multi."""
+        return self._solve_k("pcg_solve_block", B, X0, tol, max_iter, stream, out)
+
+    def _solve_k(self, fname, B, X0, tol, max_iter, stream, out):
         torch = _torch()
         if not isinstance(B, torch.Tensor):
             B = _as_tensor(B, torch.float64)
@@ -225,10 +233,10 @@ class Matrix:
             if not Xc.is_pinned():
                 Xc = Xc.pin_memory()
         infos = (_lib.PcgInfo * k)()
-        st = lib().pcg_solve_multi(self._h, k, _ptr(Bc), n, _ptr(Xc), n, float(tol), int(max_iter),
+        st = getattr(lib(), fname)(self._h, k, _ptr(Bc), n, _ptr(Xc), n, float(tol), int(max_iter),
                                    _stream_ptr(stream), infos)
         if st not in (PCG_OK, PCG_NOT_CONVERGED):
-            raise PcgError(st, "pcg_solve_multi")
+            raise PcgError(st, fname)
         out = []
         for i in range(k):
             d = infos[i].as_dict()
@@ -426,6 +434,11 @@ def pcg_solve_multi(A: Matrix, B, X0=None, tol: float = 1e-10, max_iter: int = 5
     return A.solve_multi(B, X0=X0, tol=tol, max_iter=max_iter, stream=stream)
 
 
+def pcg_solve_block(A: Matrix, B, X0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None):
+    """include/pcg.h pcg_solve_block: block CG, the k columns in one Krylov space; returns (X, infos)."""
+    return A.solve_block(B, X0=X0, tol=tol, max_iter=max_iter, stream=stream)
+
+
 def pcg_solve_pipelined(A: Matrix, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None):
     """include/pcg.h pcg_solve_pipelined: pipelined Jacobi-PCG (one reduction per iteration)."""
     return A.solve_pipelined(b, x0=x0, tol=tol, max_iter=max_iter, stream=stream)
@@ -441,4 +454,5 @@ pcg_partition_rows = partition_rows
 solve = pcg_solve  # SURVEY §8(b) "Python: pcg.solve(A, b, x0, tol, max_iter)"
 
 __all__ += ["csr_create", "csr_create_dist", "csr_destroy", "pcg_spmv", "pcg_solve", "pcg_solve_multi",
-            "pcg_solve_pipelined", "pcg_bicgstab", "pcg_partition_rows", "csr_rcm_order", "solve"]
+            "pcg_solve_pipelined", "pcg_bicgstab", "pcg_partition_rows", "csr_rcm_order", "solve",
+            "pcg_solve_block"]

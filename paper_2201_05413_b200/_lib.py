@@ -90,6 +90,7 @@ def lib():
         "pcg_spmv": [vp, vp, vp, vp],
         "pcg_solve": [vp, vp, vp, dbl, i64, vp, P(PcgInfo)],
         "pcg_solve_multi": [vp, i32, vp, i64, vp, i64, dbl, i64, vp, P(PcgInfo)],
+        "pcg_solve_block": [vp, i32, vp, i64, vp, i64, dbl, i64, vp, P(PcgInfo)],
         "pcg_partition_rows": [i64, vp, i32, vp],
         "pcg_comm_unique_id": [vp],
         "pcg_halo_ghosts": [i64, i64, i64, vp, vp, i64, P(i64)],

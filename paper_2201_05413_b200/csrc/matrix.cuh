@@ -61,6 +61,10 @@ struct SolveWork {
   double *pv = nullptr;
   void *pstate = nullptr, *ppbar = nullptr, *pdsc = nullptr;
   int ppgrid = 0;
+  // block CG (blockcg.cu): X R Z P Q B blocks, state (+ pinned mirror), Gram partials
+  double *bcg = nullptr, *bcg_part = nullptr;
+  int64_t bcg_cap = 0, bcg_part_cap = 0;
+  void *bcg_st = nullptr, *bcg_hst = nullptr;
   // BiCGSTAB graph schedule: device scalars, loop graph (per block size)
   void *bgsc = nullptr;
   cudaGraphExec_t bg_exec = nullptr;
