@@ -208,8 +208,9 @@ def main():
                     help="callbacks: exchange steps through host callbacks over gloo (validation of the N>1 "
                          "path when ranks share a GPU; not a performance number)")
     ap.add_argument("--block", type=int, default=1, help="Block-Jacobi block size for the CUBE* BiCGSTAB configs")
-    ap.add_argument("--solver", default="pcg", choices=["pcg", "pipelined"],
-                    help="single-RHS solver: Jacobi-PCG (the benchmark) or the pipelined variant (SURVEY N3)")
+    ap.add_argument("--solver", default="pcg", choices=["pcg", "pipelined", "block"],
+                    help="Jacobi-PCG (the benchmark), the pipelined variant (single RHS) or block CG (k RHS), "
+                         "both SURVEY N3")
     args = ap.parse_args()
     if args.config.startswith("CUBE"):
         return run_bicgstab(args)
@@ -323,7 +324,8 @@ def main():
 
     def step(bb, out):
         if multi:
-            X, infos = A.solve_multi(bb, tol=tol, max_iter=max_iter, out=out)
+            solve_k = A.solve_block if args.solver == "block" else A.solve_multi
+            X, infos = solve_k(bb, tol=tol, max_iter=max_iter, out=out)
             return X, infos
         solve = A.solve_pipelined if args.solver == "pipelined" else A.solve
         x, inf = solve(bb, tol=tol, max_iter=max_iter, out=out)
@@ -469,6 +471,16 @@ def main():
                            "pd_fused_kernel + one allreduce + halo per iteration (per GPU, 160n schedule)"),
                 "pcg_kernels_for_comparison": roof}
 
+    if args.solver == "block" and multi:  # block CG, one shared Krylov space for the k columns
+        inf = infos[-1]
+        tot = sum(f["bytes_algorithmic"] for f in inf)
+        ach = tot / max(inf[0]["t_solve_s"], 1e-12) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "peak_source": peak_kind, "traffic": None,
+                "kernel": ("block CG iteration (bcg_spmm + 2 Gram passes + update + P update + 2 k x k solves: "
+                           "12 nnz + 4(n+1) + 112 k n + 8 n bytes per iteration)"),
+                "independent_solver_kernels_for_comparison": roof}
+
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -490,7 +502,8 @@ def main():
             "config": dict(workload_config(args.config, c, n, nnz, world), iterations=iters,
                            format={1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[stats["format"]], setup_s=round(t_setup, 3),
                            relres_true=max(i["relres_true"] for i in infos[-1]), k_rhs=kcols,
-                           solver="jacobi-pcg" if args.solver == "pcg" else "pipelined jacobi-pcg (N3)",
+                           solver={"pcg": "jacobi-pcg", "pipelined": "pipelined jacobi-pcg (N3)",
+                                   "block": "block cg, jacobi (N3)"}[args.solver],
                            **({"drop_zeros": True, "nnz_given": nnz_given} if args.drop_zeros else {}),
                            **({"relabel_seed": args.relabel} if args.relabel is not None else {}),
                            **({"reorder": args.reorder, "n_ghost": stats["n_ghost"]} if reorder else {})),

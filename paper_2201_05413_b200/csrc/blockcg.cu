@@ -16,7 +16,9 @@
 //                                                      56 m n + 8 n
 //   bcg_small     stop test; beta = Gam^-1 Gam'
 //   bcg_pupdate   P = Z + P beta                       24 m n
-// Tiles of 32 rows x m columns are staged in shared memory for the m x m products.
+// The Gram matrices run on the fp64 tensor cores (mma.sync m8n8k4 over 32-row tiles
+// staged per warp in shared memory); the k x k mixing (X, R, P updates) is one thread
+// per row with its m entries in registers and alpha/beta broadcast from shared memory.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -159,152 +161,214 @@ __global__ void __launch_bounds__(GT) bcg_reduce_kernel(const double *__restrict
   }
 }
 
-// ---------------------------------------------------------------- G = P^T Q
-__global__ void __launch_bounds__(GT) bcg_gram_kernel(int64_t n, int m, int64_t ld, const double *__restrict__ U,
-                                                      const double *__restrict__ V, double *partials, BcgState *st) {
-  if (st->done != BCG_RUNNING) return;
-  __shared__ double su[BK][TR + 1], sv[BK][TR + 1];
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  const int mm = m * m;
-  for (int64_t r0 = (int64_t)blockIdx.x * TR; r0 < n; r0 += (int64_t)gridDim.x * TR) {
-    for (int idx = threadIdx.x; idx < m * TR; idx += GT) {
-      const int c = idx / TR, r = idx % TR;
-      const int64_t row = r0 + r;
-      su[c][r] = row < n ? U[(size_t)c * ld + row] : 0.0;
-      sv[c][r] = row < n ? V[(size_t)c * ld + row] : 0.0;
-    }
-    __syncthreads();
+// ---------------------------------------------------------------- tall-skinny products on the fp64 tensor cores
+// The m x m Gram matrices are dense contractions over n: each warp stages a 32-row tile
+// (row-major [row][col], columns >= m zero) in shared memory and accumulates
+// U^T V with mma.sync m8n8k4 f64 (A = U^T: a(i,k) = U[k][i]; B = V: b(k,j) = V[k][j]).
+constexpr int TW = 4;  // warps per block of the tile kernels
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int MB>
+__device__ __forceinline__ void warp_gram(const double *tu, const double *tv, double (&acc)[MB / 8][MB / 8][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int e = threadIdx.x + GT * u;
-      if (e < mm) {
-        const int a = e / m, b = e % m;
-        double s = acc[u];
-#pragma unroll 8
-        for (int r = 0; r < TR; r++) s = __fma_rn(su[a][r], sv[b][r], s);
-        acc[u] = s;
-      }
+  for (int s = 0; s < 8; s++) {
+    const int kk = 4 * s + q;
+    double av[MB / 8], bv[MB / 8];
+#pragma unroll
+    for (int I = 0; I < MB / 8; I++) {
+      av[I] = tu[kk * (MB + 1) + 8 * I + g];
+      bv[I] = tv[kk * (MB + 1) + 8 * I + g];
+    }
+#pragma unroll
+    for (int I = 0; I < MB / 8; I++)
+#pragma unroll
+      for (int J = 0; J < MB / 8; J++) dmma(acc[I][J][0], acc[I][J][1], av[I], bv[J]);
+  }
+}
+
+// block-wide fixed-order sum of the warps' fragments -> partials[e * gridDim.x + block]
+// (e = a * m + b for a, b < m; then `extra` per-column values at e = m*m + a)
+template <int MB>
+__device__ __forceinline__ void block_store(const double (&acc)[MB / 8][MB / 8][2], const double *extra, int m,
+                                            double *red, double *partials) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+  for (int t = threadIdx.x; t < MB * MB + MB; t += blockDim.x) red[t] = 0.0;
+  __syncthreads();
+  for (int w = 0; w < TW; w++) {
+    if (wid == w) {
+#pragma unroll
+      for (int I = 0; I < MB / 8; I++)
+#pragma unroll
+        for (int J = 0; J < MB / 8; J++) {
+          red[(8 * I + g) * MB + 8 * J + 2 * q] += acc[I][J][0];
+          red[(8 * I + g) * MB + 8 * J + 2 * q + 1] += acc[I][J][1];
+        }
+      if (extra && lane < MB) red[MB * MB + lane] += extra[lane];
     }
     __syncthreads();
   }
-  bcg_store_partials<4>(acc, mm, partials);
+  const int mm = m * m;
+  for (int e = threadIdx.x; e < mm + (extra ? m : 0); e += blockDim.x) {
+    const double v = e < mm ? red[(e / m) * MB + e % m] : red[MB * MB + e - mm];
+    partials[(size_t)e * gridDim.x + blockIdx.x] = v;
+  }
+}
+
+// G = P^T Q
+template <int MB>
+__global__ void __launch_bounds__(TW * 32) bcg_gram_kernel(int64_t n, int m, int64_t ld, const double *__restrict__ U,
+                                                           const double *__restrict__ V, double *partials,
+                                                           const BcgState *st) {
+  if (st->done != BCG_RUNNING) return;
+  extern __shared__ double dsm[];
+  __shared__ double red[MB * MB + MB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *tu = dsm + (size_t)wid * 2 * 32 * (MB + 1), *tv = tu + 32 * (MB + 1);
+  for (int c = 0; c < MB; c++) tu[lane * (MB + 1) + c] = tv[lane * (MB + 1) + c] = 0.0;
+  double acc[MB / 8][MB / 8][2] = {};
+  const int64_t ntile = (n + 31) / 32, w0 = (int64_t)blockIdx.x * TW + wid, nw = (int64_t)gridDim.x * TW;
+  for (int64_t t = w0; t < ntile; t += nw) {
+    const int64_t row = t * 32 + lane;
+    const bool ok = row < n;
+    for (int c = 0; c < m; c++) {
+      tu[lane * (MB + 1) + c] = ok ? U[(size_t)c * ld + row] : 0.0;
+      tv[lane * (MB + 1) + c] = ok ? V[(size_t)c * ld + row] : 0.0;
+    }
+    __syncwarp();
+    warp_gram<MB>(tu, tv, acc);
+    __syncwarp();
+  }
+  block_store<MB>(acc, nullptr, m, red, partials);
 }
 
 // ---------------------------------------------------------------- X, R, Z (and P at a restart) + R^T Z, diag R^T R
+// one thread per row (its m entries in registers; alpha broadcast from shared memory)
 // MODE 0 (restart / exit check): R = B - Q (Q = A X), Z = dinv R, P = Z
 // MODE 1 (step):                  X += P alpha, R -= Q alpha, Z = dinv R
-template <int MODE>
-__global__ void __launch_bounds__(GT) bcg_update_kernel(int64_t n, int m, int64_t ld, double *__restrict__ X,
-                                                        double *__restrict__ R, double *__restrict__ Z,
-                                                        double *__restrict__ P, const double *__restrict__ Q,
-                                                        const double *__restrict__ Bm, const double *__restrict__ dinv,
-                                                        double *partials, BcgState *st) {
+template <int MB, int MODE>
+__global__ void __launch_bounds__(TW * 32) bcg_update_kernel(int64_t n, int m, int64_t ld, double *__restrict__ X,
+                                                             double *__restrict__ R, double *__restrict__ Z,
+                                                             double *__restrict__ P, const double *__restrict__ Q,
+                                                             const double *__restrict__ Bm,
+                                                             const double *__restrict__ dinv, double *partials,
+                                                             const BcgState *st) {
   if (MODE == 1 && st->done != BCG_RUNNING) return;
-  __shared__ double sal[BK * BK];
-  __shared__ double sp[MODE == 1 ? BK : 1][TR + 1], sq[MODE == 1 ? BK : 1][TR + 1];
-  __shared__ double sr[BK][TR + 1], sz[BK][TR + 1];
-  const int mm = m * m;
+  extern __shared__ double dsm[];
+  __shared__ double sal[MB * MB];
+  __shared__ double red[MB * MB + MB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (MODE == 1)
-    for (int e = threadIdx.x; e < mm; e += GT) sal[e] = st->al[e];
-  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  for (int64_t r0 = (int64_t)blockIdx.x * TR; r0 < n; r0 += (int64_t)gridDim.x * TR) {
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) sal[(e / m) * MB + e % m] = st->al[e];
+  double *tr = dsm + (size_t)wid * 2 * 32 * (MB + 1), *tz = tr + 32 * (MB + 1);
+  for (int c = 0; c < MB; c++) tr[lane * (MB + 1) + c] = tz[lane * (MB + 1) + c] = 0.0;
+  __syncthreads();
+  double acc[MB / 8][MB / 8][2] = {};
+  double rr[MB];
+#pragma unroll
+  for (int c = 0; c < MB; c++) rr[c] = 0.0;
+  const int64_t ntile = (n + 31) / 32, w0 = (int64_t)blockIdx.x * TW + wid, nw = (int64_t)gridDim.x * TW;
+  for (int64_t t = w0; t < ntile; t += nw) {
+    const int64_t row = t * 32 + lane;
+    const bool ok = row < n;
+    double pv[MB], qv[MB];
     if (MODE == 1) {
-      for (int idx = threadIdx.x; idx < m * TR; idx += GT) {
-        const int c = idx / TR, r = idx % TR;
-        const int64_t row = r0 + r;
-        sp[c][r] = row < n ? P[(size_t)c * ld + row] : 0.0;
-        sq[c][r] = row < n ? Q[(size_t)c * ld + row] : 0.0;
+#pragma unroll
+      for (int b = 0; b < MB; b++) {
+        pv[b] = ok && b < m ? P[(size_t)b * ld + row] : 0.0;
+        qv[b] = ok && b < m ? Q[(size_t)b * ld + row] : 0.0;
       }
     }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < m * TR; idx += GT) {
-      const int c = idx / TR, r = idx % TR;
-      const int64_t row = r0 + r;
+    const double di = ok ? dinv[row] : 0.0;
+#pragma unroll
+    for (int c = 0; c < MB; c++) {
+      if (c >= m) break;
       double rv = 0.0, zv = 0.0;
-      if (row < n) {
+      if (ok) {
         const size_t e = (size_t)c * ld + row;
         if (MODE == 0) {
           rv = Bm[e] - Q[e];
         } else {
           double x = X[e];
           rv = R[e];
-          for (int b = 0; b < m; b++) {
-            const double ab = sal[b * m + c];
-            x = __fma_rn(sp[b][r], ab, x);
-            rv = __fma_rn(-sq[b][r], ab, rv);
+#pragma unroll
+          for (int b = 0; b < MB; b++) {
+            const double ab = sal[b * MB + c];  // (0 for b >= m)
+            x = __fma_rn(pv[b], ab, x);
+            rv = __fma_rn(-qv[b], ab, rv);
           }
           X[e] = x;
         }
-        zv = dinv[row] * rv;
+        zv = di * rv;
         R[e] = rv;
         Z[e] = zv;
         if (MODE == 0) P[e] = zv;
       }
-      sr[c][r] = rv;
-      sz[c][r] = zv;
+      tr[lane * (MB + 1) + c] = rv;
+      tz[lane * (MB + 1) + c] = zv;
+      rr[c] = __fma_rn(rv, rv, rr[c]);
     }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 5; u++) {
-      const int e = threadIdx.x + GT * u;
-      if (e < mm) {
-        const int a = e / m, b = e % m;
-        double s = acc[u];
-#pragma unroll 8
-        for (int r = 0; r < TR; r++) s = __fma_rn(sr[a][r], sz[b][r], s);
-        acc[u] = s;
-      } else if (e < mm + m) {
-        const int a = e - mm;
-        double s = acc[u];
-#pragma unroll 8
-        for (int r = 0; r < TR; r++) s = __fma_rn(sr[a][r], sr[a][r], s);
-        acc[u] = s;
-      }
-    }
-    __syncthreads();
+    __syncwarp();
+    warp_gram<MB>(tr, tz, acc);
+    __syncwarp();
   }
-  bcg_store_partials<5>(acc, mm + m, partials);
+  // rr: per-thread column sums -> per-warp (fixed xor tree) -> lane c holds column c
+  double ex[MB];
+#pragma unroll
+  for (int c = 0; c < MB; c++) ex[c] = warp_sum(rr[c]);
+  __shared__ double wex[TW][MB];
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < MB; c++) wex[wid][c] = ex[c];
+  __syncthreads();
+  block_store<MB>(acc, wex[wid], m, red, partials);
 }
 
-// ---------------------------------------------------------------- P = Z + P beta
-__global__ void __launch_bounds__(GT) bcg_pupdate_kernel(int64_t n, int m, int64_t ld, double *__restrict__ P,
-                                                         const double *__restrict__ Z, const BcgState *st) {
+// ---------------------------------------------------------------- P = Z + P beta (one thread per row)
+template <int MB>
+__global__ void __launch_bounds__(TW * 32) bcg_pupdate_kernel(int64_t n, int m, int64_t ld, double *__restrict__ P,
+                                                              const double *__restrict__ Z, const BcgState *st) {
   if (st->done != BCG_RUNNING) return;
-  __shared__ double sbe[BK * BK];
-  __shared__ double sp[BK][TR + 1];
-  for (int e = threadIdx.x; e < m * m; e += GT) sbe[e] = st->be[e];
-  for (int64_t r0 = (int64_t)blockIdx.x * TR; r0 < n; r0 += (int64_t)gridDim.x * TR) {
-    for (int idx = threadIdx.x; idx < m * TR; idx += GT) {
-      const int c = idx / TR, r = idx % TR;
-      const int64_t row = r0 + r;
-      sp[c][r] = row < n ? P[(size_t)c * ld + row] : 0.0;
+  __shared__ double sbe[MB * MB];
+  for (int e = threadIdx.x; e < MB * MB; e += blockDim.x) sbe[e] = 0.0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) sbe[(e / m) * MB + e % m] = st->be[e];
+  __syncthreads();
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += (int64_t)gridDim.x * blockDim.x) {
+    double pv[MB];
+#pragma unroll
+    for (int b = 0; b < MB; b++) pv[b] = b < m ? P[(size_t)b * ld + row] : 0.0;
+#pragma unroll
+    for (int c = 0; c < MB; c++) {
+      if (c >= m) break;
+      double v = Z[(size_t)c * ld + row];
+#pragma unroll
+      for (int b = 0; b < MB; b++) v = __fma_rn(pv[b], sbe[b * MB + c], v);
+      P[(size_t)c * ld + row] = v;
     }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < m * TR; idx += GT) {
-      const int c = idx / TR, r = idx % TR;
-      const int64_t row = r0 + r;
-      if (row < n) {
-        const size_t e = (size_t)c * ld + row;
-        double v = Z[e];
-        for (int b = 0; b < m; b++) v = __fma_rn(sp[b][r], sbe[b * m + c], v);
-        P[e] = v;
-      }
-    }
-    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------- k x k solves (one warp)
 // Y = G^-1 C by Cholesky G = L L^T (as oracle.c chol_solve); false on a non-positive pivot
 __device__ bool bcg_chol_solve(int m, const double *G, const double *Cm, double *Y) {
-  __shared__ double L[BK * BK];
+  __shared__ double L[BK * BK], sC[BK * BK], sY[BK * BK];
   __shared__ int s_fail;
   const int t = threadIdx.x;
+  for (int e = t; e < m * m; e += 32) {
+    L[e] = G[e];  // lower triangle overwritten by the factor
+    sC[e] = Cm[e];
+  }
   if (t == 0) s_fail = 0;
   __syncwarp();
   for (int j = 0; j < m; j++) {
     if (t == 0) {
-      double d = G[j * m + j];
+      double d = L[j * m + j];
       for (int s = 0; s < j; s++) d -= L[j * m + s] * L[j * m + s];
       if (!(d > 0.0)) s_fail = 1;
       L[j * m + j] = sqrt(d);
@@ -312,7 +376,7 @@ __device__ bool bcg_chol_solve(int m, const double *G, const double *Cm, double 
     __syncwarp();
     if (s_fail) return false;
     if (t > j && t < m) {
-      double s = G[t * m + j];
+      double s = L[t * m + j];
       for (int q = 0; q < j; q++) s -= L[t * m + q] * L[j * m + q];
       L[t * m + j] = s / L[j * m + j];
     }
@@ -321,16 +385,18 @@ __device__ bool bcg_chol_solve(int m, const double *G, const double *Cm, double 
   if (t < m) {
     const int c = t;
     for (int i = 0; i < m; i++) {
-      double s = Cm[i * m + c];
-      for (int q = 0; q < i; q++) s -= L[i * m + q] * Y[q * m + c];
-      Y[i * m + c] = s / L[i * m + i];
+      double s = sC[i * m + c];
+      for (int q = 0; q < i; q++) s -= L[i * m + q] * sY[q * m + c];
+      sY[i * m + c] = s / L[i * m + i];
     }
     for (int i = m - 1; i >= 0; i--) {
-      double s = Y[i * m + c];
-      for (int q = i + 1; q < m; q++) s -= L[q * m + i] * Y[q * m + c];
-      Y[i * m + c] = s / L[i * m + i];
+      double s = sY[i * m + c];
+      for (int q = i + 1; q < m; q++) s -= L[q * m + i] * sY[q * m + c];
+      sY[i * m + c] = s / L[i * m + i];
     }
   }
+  __syncwarp();
+  for (int e = t; e < m * m; e += 32) Y[e] = sY[e];
   __syncwarp();
   return true;
 }
@@ -399,8 +465,8 @@ struct BcgBufs {
   double *X, *R, *Z, *P, *Q, *Bm;
 };
 
-int tile_grid(int64_t n, int sms) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>((n + TR - 1) / TR, (int64_t)sms * 4));
+int tile_grid(int64_t n, int sms) {  // blocks of TW warps, one 32-row tile per warp at a time
+  return (int)std::max<int64_t>(1, std::min<int64_t>(((n + 31) / 32 + TW - 1) / TW, (int64_t)sms * 8));
 }
 }  // namespace
 
@@ -421,10 +487,29 @@ static pcg_status bcg_spmm(pcg_matrix *A, const double *P, double *Q, int m, int
 }
 
 // restart / exit check: R = B - A X, Z = dinv R, P = Z, Gam = R^T Z, rr; done = OK iff all small
-static pcg_status bcg_restart(pcg_matrix *A, const BcgBufs &b, int m, int64_t ld, BcgState *st, double *part, int gt,
-                              cudaStream_t s) {
+template <int MB>
+static size_t bcg_dyn_smem() { return (size_t)TW * 2 * 32 * (MB + 1) * sizeof(double); }
+
+template <int MB>
+static pcg_status bcg_prepare() {
+  static bool done = false;
+  if (done) return PCG_OK;
+  const int sm = (int)bcg_dyn_smem<MB>();
+  PCG_CUDA(cudaFuncSetAttribute(bcg_gram_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  PCG_CUDA(cudaFuncSetAttribute(bcg_update_kernel<MB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  PCG_CUDA(cudaFuncSetAttribute(bcg_update_kernel<MB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  done = true;
+  return PCG_OK;
+}
+
+// restart / exit check: R = B - A X, Z = dinv R, P = Z, Gam = R^T Z, rr; done = OK iff all small
+template <int MB>
+static pcg_status bcg_restart_mb(pcg_matrix *A, const BcgBufs &b, int m, int64_t ld, BcgState *st, double *part,
+                                 int gt, cudaStream_t s) {
+  PCG_TRY(bcg_prepare<MB>());
   PCG_TRY(bcg_spmm(A, b.X, b.Q, m, ld, nullptr, s));
-  bcg_update_kernel<0><<<gt, GT, 0, s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm, A->d_dinv, part, st);
+  bcg_update_kernel<MB, 0><<<gt, TW * 32, bcg_dyn_smem<MB>(), s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm,
+                                                                   A->d_dinv, part, st);
   bcg_reduce_kernel<<<m * m + m, GT, 0, s>>>(part, gt, m * m, st->Gn, st->rr, nullptr);
   bcg_small_kernel<<<1, 32, 0, s>>>(st, BS_INIT);
   count_launch(3);
@@ -432,19 +517,35 @@ static pcg_status bcg_restart(pcg_matrix *A, const BcgBufs &b, int m, int64_t ld
   return PCG_OK;
 }
 
-static pcg_status bcg_step(pcg_matrix *A, const BcgBufs &b, int m, int64_t ld, BcgState *st, double *part, int gt,
-                           cudaStream_t s) {
+template <int MB>
+static pcg_status bcg_step_mb(pcg_matrix *A, const BcgBufs &b, int m, int64_t ld, BcgState *st, double *part, int gt,
+                              cudaStream_t s) {
   PCG_TRY(bcg_spmm(A, b.P, b.Q, m, ld, st, s));
-  bcg_gram_kernel<<<gt, GT, 0, s>>>(A->n, m, ld, b.P, b.Q, part, st);
+  bcg_gram_kernel<MB><<<gt, TW * 32, bcg_dyn_smem<MB>(), s>>>(A->n, m, ld, b.P, b.Q, part, st);
   bcg_reduce_kernel<<<m * m, GT, 0, s>>>(part, gt, m * m, st->G, nullptr, st);
   bcg_small_kernel<<<1, 32, 0, s>>>(st, BS_ALPHA);
-  bcg_update_kernel<1><<<gt, GT, 0, s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm, A->d_dinv, part, st);
+  bcg_update_kernel<MB, 1><<<gt, TW * 32, bcg_dyn_smem<MB>(), s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm,
+                                                                   A->d_dinv, part, st);
   bcg_reduce_kernel<<<m * m + m, GT, 0, s>>>(part, gt, m * m, st->Gn, st->rr, st);
   bcg_small_kernel<<<1, 32, 0, s>>>(st, BS_BETA);
-  bcg_pupdate_kernel<<<gt, GT, 0, s>>>(A->n, m, ld, b.P, b.Z, st);
+  const unsigned gp = (unsigned)std::max<int64_t>(1, std::min<int64_t>((A->n + 127) / 128, (int64_t)gt * 2));
+  bcg_pupdate_kernel<MB><<<gp, TW * 32, 0, s>>>(A->n, m, ld, b.P, b.Z, st);
   count_launch(7);
   PCG_CUDA(cudaGetLastError());
   return PCG_OK;
+}
+
+static pcg_status bcg_restart(pcg_matrix *A, const BcgBufs &b, int m, int64_t ld, BcgState *st, double *part, int gt,
+                              cudaStream_t s) {
+  if (m <= 8) return bcg_restart_mb<8>(A, b, m, ld, st, part, gt, s);
+  if (m <= 16) return bcg_restart_mb<16>(A, b, m, ld, st, part, gt, s);
+  return bcg_restart_mb<32>(A, b, m, ld, st, part, gt, s);
+}
+static pcg_status bcg_step(pcg_matrix *A, const BcgBufs &b, int m, int64_t ld, BcgState *st, double *part, int gt,
+                           cudaStream_t s) {
+  if (m <= 8) return bcg_step_mb<8>(A, b, m, ld, st, part, gt, s);
+  if (m <= 16) return bcg_step_mb<16>(A, b, m, ld, st, part, gt, s);
+  return bcg_step_mb<32>(A, b, m, ld, st, part, gt, s);
 }
 
 static pcg_status block_cg_impl(pcg_matrix *A, int k, const double *B, int64_t ldb, double *X, int64_t ldx, double tol,
