@@ -236,9 +236,16 @@ __global__ void __launch_bounds__(TW * 32) bcg_gram_kernel(int64_t n, int m, int
   for (int64_t t = w0; t < ntile; t += nw) {
     const int64_t row = t * 32 + lane;
     const bool ok = row < n;
-    for (int c = 0; c < m; c++) {
-      tu[lane * (MB + 1) + c] = ok ? U[(size_t)c * ld + row] : 0.0;
-      tv[lane * (MB + 1) + c] = ok ? V[(size_t)c * ld + row] : 0.0;
+    double uv[MB], vv[MB];  // all 2m loads of the row in flight at once
+#pragma unroll
+    for (int c = 0; c < MB; c++) {
+      uv[c] = ok && c < m ? U[(size_t)c * ld + row] : 0.0;
+      vv[c] = ok && c < m ? V[(size_t)c * ld + row] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < MB; c++) {
+      tu[lane * (MB + 1) + c] = uv[c];
+      tv[lane * (MB + 1) + c] = vv[c];
     }
     __syncwarp();
     warp_gram<MB>(tu, tv, acc);
@@ -248,9 +255,11 @@ __global__ void __launch_bounds__(TW * 32) bcg_gram_kernel(int64_t n, int m, int
 }
 
 // ---------------------------------------------------------------- X, R, Z (and P at a restart) + R^T Z, diag R^T R
-// one thread per row (its m entries in registers; alpha broadcast from shared memory)
 // MODE 0 (restart / exit check): R = B - Q (Q = A X), Z = dinv R, P = Z
-// MODE 1 (step):                  X += P alpha, R -= Q alpha, Z = dinv R
+// MODE 1 (step): X += P alpha, R -= Q alpha on the tensor cores: per warp a 32-row
+//   tile, the (32 x m) . (m x m) products as m8n8k4 mma with the accumulators
+//   initialised from X and R (fragment rows 8I + g, columns 8J + 2q + {0, 1}); then
+//   Z = dinv R in the fragments.  R and Z go to shared-memory tiles for R^T Z.
 template <int MB, int MODE>
 __global__ void __launch_bounds__(TW * 32) bcg_update_kernel(int64_t n, int m, int64_t ld, double *__restrict__ X,
                                                              double *__restrict__ R, double *__restrict__ Z,
@@ -262,95 +271,168 @@ __global__ void __launch_bounds__(TW * 32) bcg_update_kernel(int64_t n, int m, i
   extern __shared__ double dsm[];
   __shared__ double sal[MB * MB];
   __shared__ double red[MB * MB + MB];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ double wex[TW][MB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+  for (int e = threadIdx.x; e < MB * MB; e += blockDim.x) sal[e] = 0.0;
+  __syncthreads();
   if (MODE == 1)
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) sal[(e / m) * MB + e % m] = st->al[e];
-  double *tr = dsm + (size_t)wid * 2 * 32 * (MB + 1), *tz = tr + 32 * (MB + 1);
-  for (int c = 0; c < MB; c++) tr[lane * (MB + 1) + c] = tz[lane * (MB + 1) + c] = 0.0;
+  // per warp: tr, tz (R, Z for the Gram) and tp, tq (P, Q tiles of the step)
+  double *tr = dsm + (size_t)wid * 4 * 32 * (MB + 1), *tz = tr + 32 * (MB + 1);
+  double *tp = tz + 32 * (MB + 1), *tq = tp + 32 * (MB + 1);
+  for (int c = 0; c < MB; c++) {
+    tr[lane * (MB + 1) + c] = tz[lane * (MB + 1) + c] = 0.0;
+    tp[lane * (MB + 1) + c] = tq[lane * (MB + 1) + c] = 0.0;
+  }
   __syncthreads();
   double acc[MB / 8][MB / 8][2] = {};
-  double rr[MB];
-#pragma unroll
-  for (int c = 0; c < MB; c++) rr[c] = 0.0;
+  double rr[MB / 8][2] = {};  // this lane's columns 8J + 2q + e
   const int64_t ntile = (n + 31) / 32, w0 = (int64_t)blockIdx.x * TW + wid, nw = (int64_t)gridDim.x * TW;
   for (int64_t t = w0; t < ntile; t += nw) {
-    const int64_t row = t * 32 + lane;
-    const bool ok = row < n;
-    double pv[MB], qv[MB];
+    const int64_t r0 = t * 32;
     if (MODE == 1) {
+      const int64_t row = r0 + lane;
+      const bool ok = row < n;
+      double pv[MB], qv[MB];
 #pragma unroll
-      for (int b = 0; b < MB; b++) {
-        pv[b] = ok && b < m ? P[(size_t)b * ld + row] : 0.0;
-        qv[b] = ok && b < m ? Q[(size_t)b * ld + row] : 0.0;
+      for (int c = 0; c < MB; c++) {
+        pv[c] = ok && c < m ? P[(size_t)c * ld + row] : 0.0;
+        qv[c] = ok && c < m ? Q[(size_t)c * ld + row] : 0.0;
       }
+#pragma unroll
+      for (int c = 0; c < MB; c++) {
+        tp[lane * (MB + 1) + c] = pv[c];
+        tq[lane * (MB + 1) + c] = qv[c];
+      }
+      __syncwarp();
     }
-    const double di = ok ? dinv[row] : 0.0;
+    // all fragment loads of the tile first (X, R or B - Q; dinv), then the mma and stores
+    double xf[4][MB / 8][2], rf[4][MB / 8][2], dv[4];
 #pragma unroll
-    for (int c = 0; c < MB; c++) {
-      if (c >= m) break;
-      double rv = 0.0, zv = 0.0;
-      if (ok) {
-        const size_t e = (size_t)c * ld + row;
-        if (MODE == 0) {
-          rv = Bm[e] - Q[e];
-        } else {
-          double x = X[e];
-          rv = R[e];
+    for (int I = 0; I < 4; I++) {
+      const int64_t row = r0 + 8 * I + g;
+      const bool rok = row < n;
+      dv[I] = rok ? dinv[row] : 0.0;
 #pragma unroll
-          for (int b = 0; b < MB; b++) {
-            const double ab = sal[b * MB + c];  // (0 for b >= m)
-            x = __fma_rn(pv[b], ab, x);
-            rv = __fma_rn(-qv[b], ab, rv);
+      for (int J = 0; J < MB / 8; J++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int cc = 8 * J + 2 * q + e;
+          xf[I][J][e] = rf[I][J][e] = 0.0;
+          if (rok && cc < m) {
+            const size_t ix = (size_t)cc * ld + row;
+            if (MODE == 0) {
+              rf[I][J][e] = Bm[ix] - Q[ix];
+            } else {
+              xf[I][J][e] = X[ix];
+              rf[I][J][e] = R[ix];
+            }
           }
-          X[e] = x;
         }
-        zv = di * rv;
-        R[e] = rv;
-        Z[e] = zv;
-        if (MODE == 0) P[e] = zv;
+    }
+#pragma unroll
+    for (int I = 0; I < 4; I++) {
+      const int rl = 8 * I + g;
+      const int64_t row = r0 + rl;
+      const bool rok = row < n;
+#pragma unroll
+      for (int J = 0; J < MB / 8; J++) {
+        double *xv = xf[I][J], *rv = rf[I][J];
+        if (MODE == 1) {
+#pragma unroll
+          for (int s4 = 0; s4 < MB / 4; s4++) {
+            const double bal = sal[(4 * s4 + q) * MB + 8 * J + g];
+            dmma(xv[0], xv[1], tp[rl * (MB + 1) + 4 * s4 + q], bal);
+            dmma(rv[0], rv[1], -tq[rl * (MB + 1) + 4 * s4 + q], bal);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int cc = 8 * J + 2 * q + e;
+          const bool ok = rok && cc < m;
+          const double zv = dv[I] * rv[e];
+          if (ok) {
+            const size_t ix = (size_t)cc * ld + row;
+            if (MODE == 1) X[ix] = xv[e];
+            R[ix] = rv[e];
+            Z[ix] = zv;
+            if (MODE == 0) P[ix] = zv;
+          }
+          tr[rl * (MB + 1) + cc] = ok ? rv[e] : 0.0;
+          tz[rl * (MB + 1) + cc] = ok ? zv : 0.0;
+          rr[J][e] = __fma_rn(ok ? rv[e] : 0.0, ok ? rv[e] : 0.0, rr[J][e]);
+        }
       }
-      tr[lane * (MB + 1) + c] = rv;
-      tz[lane * (MB + 1) + c] = zv;
-      rr[c] = __fma_rn(rv, rv, rr[c]);
     }
     __syncwarp();
     warp_gram<MB>(tr, tz, acc);
     __syncwarp();
   }
-  // rr: per-thread column sums -> per-warp (fixed xor tree) -> lane c holds column c
-  double ex[MB];
+  // diag R^T R: lanes with the same q hold the same columns; fold over g (fixed xor tree)
 #pragma unroll
-  for (int c = 0; c < MB; c++) ex[c] = warp_sum(rr[c]);
-  __shared__ double wex[TW][MB];
-  if (lane == 0)
+  for (int J = 0; J < MB / 8; J++)
 #pragma unroll
-    for (int c = 0; c < MB; c++) wex[wid][c] = ex[c];
+    for (int e = 0; e < 2; e++) {
+      double v = rr[J][e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      if (g == 0) wex[wid][8 * J + 2 * q + e] = v;
+    }
   __syncthreads();
   block_store<MB>(acc, wex[wid], m, red, partials);
 }
 
-// ---------------------------------------------------------------- P = Z + P beta (one thread per row)
+// ---------------------------------------------------------------- P = Z + P beta (tensor cores, as the step update)
 template <int MB>
 __global__ void __launch_bounds__(TW * 32) bcg_pupdate_kernel(int64_t n, int m, int64_t ld, double *__restrict__ P,
                                                               const double *__restrict__ Z, const BcgState *st) {
   if (st->done != BCG_RUNNING) return;
+  extern __shared__ double dsm[];
   __shared__ double sbe[MB * MB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
   for (int e = threadIdx.x; e < MB * MB; e += blockDim.x) sbe[e] = 0.0;
   __syncthreads();
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) sbe[(e / m) * MB + e % m] = st->be[e];
+  double *tp = dsm + (size_t)wid * 32 * (MB + 1);
+  for (int c = 0; c < MB; c++) tp[lane * (MB + 1) + c] = 0.0;
   __syncthreads();
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += (int64_t)gridDim.x * blockDim.x) {
-    double pv[MB];
+  const int64_t ntile = (n + 31) / 32, w0 = (int64_t)blockIdx.x * TW + wid, nw = (int64_t)gridDim.x * TW;
+  for (int64_t t = w0; t < ntile; t += nw) {
+    const int64_t r0 = t * 32;
+    {
+      const int64_t row = r0 + lane;
+      const bool ok = row < n;
+      double pv[MB];
 #pragma unroll
-    for (int b = 0; b < MB; b++) pv[b] = b < m ? P[(size_t)b * ld + row] : 0.0;
+      for (int c = 0; c < MB; c++) pv[c] = ok && c < m ? P[(size_t)c * ld + row] : 0.0;
 #pragma unroll
-    for (int c = 0; c < MB; c++) {
-      if (c >= m) break;
-      double v = Z[(size_t)c * ld + row];
-#pragma unroll
-      for (int b = 0; b < MB; b++) v = __fma_rn(pv[b], sbe[b * MB + c], v);
-      P[(size_t)c * ld + row] = v;
+      for (int c = 0; c < MB; c++) tp[lane * (MB + 1) + c] = pv[c];
     }
+    __syncwarp();
+#pragma unroll
+    for (int I = 0; I < 4; I++) {
+      const int rl = 8 * I + g;
+      const int64_t row = r0 + rl;
+      const bool rok = row < n;
+#pragma unroll
+      for (int J = 0; J < MB / 8; J++) {
+        double v[2] = {0.0, 0.0};
+        int cc[2];
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          cc[e] = 8 * J + 2 * q + e;
+          if (rok && cc[e] < m) v[e] = Z[(size_t)cc[e] * ld + row];
+        }
+#pragma unroll
+        for (int s4 = 0; s4 < MB / 4; s4++)
+          dmma(v[0], v[1], tp[rl * (MB + 1) + 4 * s4 + q], sbe[(4 * s4 + q) * MB + 8 * J + g]);
+#pragma unroll
+        for (int e = 0; e < 2; e++)
+          if (rok && cc[e] < m) P[(size_t)cc[e] * ld + row] = v[e];
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -488,16 +570,17 @@ static pcg_status bcg_spmm(pcg_matrix *A, const double *P, double *Q, int m, int
 
 // restart / exit check: R = B - A X, Z = dinv R, P = Z, Gam = R^T Z, rr; done = OK iff all small
 template <int MB>
-static size_t bcg_dyn_smem() { return (size_t)TW * 2 * 32 * (MB + 1) * sizeof(double); }
+static size_t bcg_dyn_smem(int tiles = 2) { return (size_t)TW * tiles * 32 * (MB + 1) * sizeof(double); }
 
 template <int MB>
 static pcg_status bcg_prepare() {
   static bool done = false;
   if (done) return PCG_OK;
-  const int sm = (int)bcg_dyn_smem<MB>();
+  const int sm = (int)bcg_dyn_smem<MB>(), sm4 = (int)bcg_dyn_smem<MB>(4), sm1 = (int)bcg_dyn_smem<MB>(1);
   PCG_CUDA(cudaFuncSetAttribute(bcg_gram_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  PCG_CUDA(cudaFuncSetAttribute(bcg_update_kernel<MB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  PCG_CUDA(cudaFuncSetAttribute(bcg_update_kernel<MB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  PCG_CUDA(cudaFuncSetAttribute(bcg_update_kernel<MB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4));
+  PCG_CUDA(cudaFuncSetAttribute(bcg_update_kernel<MB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4));
+  PCG_CUDA(cudaFuncSetAttribute(bcg_pupdate_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1));
   done = true;
   return PCG_OK;
 }
@@ -508,7 +591,7 @@ static pcg_status bcg_restart_mb(pcg_matrix *A, const BcgBufs &b, int m, int64_t
                                  int gt, cudaStream_t s) {
   PCG_TRY(bcg_prepare<MB>());
   PCG_TRY(bcg_spmm(A, b.X, b.Q, m, ld, nullptr, s));
-  bcg_update_kernel<MB, 0><<<gt, TW * 32, bcg_dyn_smem<MB>(), s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm,
+  bcg_update_kernel<MB, 0><<<gt, TW * 32, bcg_dyn_smem<MB>(4), s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm,
                                                                    A->d_dinv, part, st);
   bcg_reduce_kernel<<<m * m + m, GT, 0, s>>>(part, gt, m * m, st->Gn, st->rr, nullptr);
   bcg_small_kernel<<<1, 32, 0, s>>>(st, BS_INIT);
@@ -520,16 +603,16 @@ static pcg_status bcg_restart_mb(pcg_matrix *A, const BcgBufs &b, int m, int64_t
 template <int MB>
 static pcg_status bcg_step_mb(pcg_matrix *A, const BcgBufs &b, int m, int64_t ld, BcgState *st, double *part, int gt,
                               cudaStream_t s) {
+  PCG_TRY(bcg_prepare<MB>());
   PCG_TRY(bcg_spmm(A, b.P, b.Q, m, ld, st, s));
   bcg_gram_kernel<MB><<<gt, TW * 32, bcg_dyn_smem<MB>(), s>>>(A->n, m, ld, b.P, b.Q, part, st);
   bcg_reduce_kernel<<<m * m, GT, 0, s>>>(part, gt, m * m, st->G, nullptr, st);
   bcg_small_kernel<<<1, 32, 0, s>>>(st, BS_ALPHA);
-  bcg_update_kernel<MB, 1><<<gt, TW * 32, bcg_dyn_smem<MB>(), s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm,
+  bcg_update_kernel<MB, 1><<<gt, TW * 32, bcg_dyn_smem<MB>(4), s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm,
                                                                    A->d_dinv, part, st);
   bcg_reduce_kernel<<<m * m + m, GT, 0, s>>>(part, gt, m * m, st->Gn, st->rr, st);
   bcg_small_kernel<<<1, 32, 0, s>>>(st, BS_BETA);
-  const unsigned gp = (unsigned)std::max<int64_t>(1, std::min<int64_t>((A->n + 127) / 128, (int64_t)gt * 2));
-  bcg_pupdate_kernel<MB><<<gp, TW * 32, 0, s>>>(A->n, m, ld, b.P, b.Z, st);
+  bcg_pupdate_kernel<MB><<<gt, TW * 32, bcg_dyn_smem<MB>(1), s>>>(A->n, m, ld, b.P, b.Z, st);
   count_launch(7);
   PCG_CUDA(cudaGetLastError());
   return PCG_OK;
