@@ -20,6 +20,7 @@
 // staged per warp in shared memory); the k x k mixing (X, R, P updates) is one thread
 // per row with its m entries in registers and alpha/beta broadcast from shared memory.
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -558,10 +559,12 @@ static pcg_status bcg_spmm(pcg_matrix *A, const double *P, double *Q, int m, int
   if (A->format == PCG_FORMAT_CSR) {
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((A->n + BLOCK - 1) / BLOCK, (int64_t)sms * 8));
     bcg_spmm_csr<<<g, BLOCK, 0, s>>>(A->csr(), P, Q, m, ld, st);
-  } else {
+  } else if (getenv("PCG_BCG_OWN_SPMM")) {  // A/B knob: this file's simpler SpMM
     const unsigned g =
         (unsigned)std::max<int64_t>(1, std::min<int64_t>((A->n_slices + WARPS - 1) / WARPS, (int64_t)sms * 4));
     bcg_spmm_sell<<<g, BLOCK, 0, s>>>(A->sell(), P, Q, m, ld, st);
+  } else {  // the multi-RHS SpMM (L2 first-touch prefetch), gated on the block state
+    return block_spmm(A, P, Q, m, ld, st ? &st->done : nullptr, s);
   }
   count_launch();
   PCG_CUDA(cudaGetLastError());

@@ -605,7 +605,7 @@ void free_work(pcg_matrix *A) {
   for (void *q : {(void *)w.bv, w.bstate, w.bbar, (void *)w.bminv, w.bgsc, (void *)w.pv, w.pstate, w.ppbar, w.pdsc})
     if (q) cudaFree(q);
   if (w.h_msc) cudaFreeHost(w.h_msc);
-  for (void *q : {(void *)w.bcg, (void *)w.bcg_part, w.bcg_st})
+  for (void *q : {(void *)w.bcg, (void *)w.bcg_part, w.bcg_st, w.bspmm_sc, (void *)w.bspmm_part})
     if (q) cudaFree(q);
   if (w.bcg_hst) cudaFreeHost(w.bcg_hst);
   w = SolveWork();

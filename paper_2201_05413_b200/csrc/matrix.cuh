@@ -65,6 +65,8 @@ struct SolveWork {
   double *bcg = nullptr, *bcg_part = nullptr;
   int64_t bcg_cap = 0, bcg_part_cap = 0;
   void *bcg_st = nullptr, *bcg_hst = nullptr;
+  void *bspmm_sc = nullptr;  // scratch MultiScalars of the block-CG SpMM (multi.cu block_spmm)
+  double *bspmm_part = nullptr;
   // BiCGSTAB graph schedule: device scalars, loop graph (per block size)
   void *bgsc = nullptr;
   cudaGraphExec_t bg_exec = nullptr;
@@ -151,6 +153,8 @@ void sigma_swap(pcg_matrix *A, SigmaSys *S);
 void sigma_free(SigmaSys *S);
 pcg_status apply_perm(pcg_matrix *A, int *perm, cudaStream_t st);
 pcg_status rcm_order(int64_t n, const int *rp, const int *col, int *perm, cudaStream_t st);
+pcg_status block_spmm(pcg_matrix *A, const double *P, double *Q, int k, int64_t ld, const int *d_done,
+                      cudaStream_t st);
 pcg_status perm_in(pcg_matrix *A, const double *src_dev, double *dst, cudaStream_t st);
 pcg_status perm_out(pcg_matrix *A, const double *src, double *dst_dev, cudaStream_t st);
 pcg_status perm_in_cols(pcg_matrix *A, int k, const double *src, int64_t lds, double *dst, int64_t ldd, cudaStream_t st);

@@ -617,6 +617,50 @@ static void launch_mspmm(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cu
     mspmm_kernel<MODE, false><<<g, BLOCK, smem, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
 }
 
+// ---------------------------------------------------------------- the SpMM alone, for block CG (blockcg.cu)
+// Q = A P over SELL-32 for k <= 32 column-major columns (ld), through mspmm_kernel on
+// a scratch MultiScalars re-armed before every launch (all k columns active; none if
+// *d_done != 0, so finished block solves skip it).  Its sigma side results stay in
+// the scratch state.
+__global__ void bspmm_arm_kernel(MultiScalars *sc, int k, const int *d_done) {
+  const int t = threadIdx.x;
+  if (t < KMAX) {
+    sc->active[t] = t < k;
+    sc->done[t] = 0;
+    sc->rho[t] = 1.0;
+  }
+  if (t == 0) {
+    sc->n_active = (d_done && *d_done != 0) ? 0 : k;
+    sc->kcols = k;
+    sc->cnt_a = 0;
+  }
+}
+
+pcg_status block_spmm(pcg_matrix *A, const double *P, double *Q, int k, int64_t ld, const int *d_done,
+                      cudaStream_t st) {
+  SolveWork &w = A->work;
+  if (!w.bspmm_sc) {
+    PCG_CUDA(cudaMalloc(&w.bspmm_sc, sizeof(MultiScalars)));
+    PCG_CUDA(cudaMemset(w.bspmm_sc, 0, sizeof(MultiScalars)));
+    PCG_CUDA(cudaMalloc(&w.bspmm_part, sizeof(double) * 3 * KMAX * (size_t)num_sms(A->device) * 8));
+  }
+  MultiScalars *sc = (MultiScalars *)w.bspmm_sc;
+  bspmm_arm_kernel<<<1, 32, 0, st>>>(sc, k, d_done);
+  const int g = mgrid_spmm(A, k);
+  MVecs v{};
+  v.P = const_cast<double *>(P);
+  v.Q = Q;
+  v.ld = ld;
+  const size_t smem = k <= 16 ? sizeof(double) * BLOCK * k : 0;
+  if (A->max_row_len > 8)
+    mspmm_kernel<MS_SPMM, true><<<g, BLOCK, smem, st>>>(A->sell(), v, sc, w.bspmm_part, k, spmm_prefetch(), 0, 0);
+  else
+    mspmm_kernel<MS_SPMM, false><<<g, BLOCK, smem, st>>>(A->sell(), v, sc, w.bspmm_part, k, spmm_prefetch(), 0, 0);
+  count_launch(2);
+  PCG_CUDA(cudaGetLastError());
+  return PCG_OK;
+}
+
 static double *mpart_rz(pcg_matrix *A) { return A->work.mpart + (size_t)3 * KMAX * num_sms(A->device) * 8; }
 
 static pcg_status mlaunch_iteration(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
