@@ -278,13 +278,11 @@ __global__ void __launch_bounds__(TW * 32) bcg_update_kernel(int64_t n, int m, i
   __syncthreads();
   if (MODE == 1)
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) sal[(e / m) * MB + e % m] = st->al[e];
-  // per warp: tr, tz (R, Z for the Gram) and tp, tq (P, Q tiles of the step)
-  double *tr = dsm + (size_t)wid * 4 * 32 * (MB + 1), *tz = tr + 32 * (MB + 1);
-  double *tp = tz + 32 * (MB + 1), *tq = tp + 32 * (MB + 1);
-  for (int c = 0; c < MB; c++) {
-    tr[lane * (MB + 1) + c] = tz[lane * (MB + 1) + c] = 0.0;
-    tp[lane * (MB + 1) + c] = tq[lane * (MB + 1) + c] = 0.0;
-  }
+  // per warp two tiles: P, Q of the step, then (once every mma of the tile is done) R, Z
+  // for the Gram in the same space
+  double *tp = dsm + (size_t)wid * 2 * 32 * (MB + 1), *tq = tp + 32 * (MB + 1);
+  double *tr = tp, *tz = tq;
+  for (int c = 0; c < MB; c++) tp[lane * (MB + 1) + c] = tq[lane * (MB + 1) + c] = 0.0;
   __syncthreads();
   double acc[MB / 8][MB / 8][2] = {};
   double rr[MB / 8][2] = {};  // this lane's columns 8J + 2q + e
@@ -331,6 +329,21 @@ __global__ void __launch_bounds__(TW * 32) bcg_update_kernel(int64_t n, int m, i
           }
         }
     }
+    if (MODE == 1) {
+#pragma unroll
+      for (int I = 0; I < 4; I++) {
+        const int rl = 8 * I + g;
+#pragma unroll
+        for (int J = 0; J < MB / 8; J++)
+#pragma unroll
+          for (int s4 = 0; s4 < MB / 4; s4++) {
+            const double bal = sal[(4 * s4 + q) * MB + 8 * J + g];
+            dmma(xf[I][J][0], xf[I][J][1], tp[rl * (MB + 1) + 4 * s4 + q], bal);
+            dmma(rf[I][J][0], rf[I][J][1], -tq[rl * (MB + 1) + 4 * s4 + q], bal);
+          }
+      }
+      __syncwarp();  // the P, Q tiles are dead: R, Z take their place
+    }
 #pragma unroll
     for (int I = 0; I < 4; I++) {
       const int rl = 8 * I + g;
@@ -339,14 +352,6 @@ __global__ void __launch_bounds__(TW * 32) bcg_update_kernel(int64_t n, int m, i
 #pragma unroll
       for (int J = 0; J < MB / 8; J++) {
         double *xv = xf[I][J], *rv = rf[I][J];
-        if (MODE == 1) {
-#pragma unroll
-          for (int s4 = 0; s4 < MB / 4; s4++) {
-            const double bal = sal[(4 * s4 + q) * MB + 8 * J + g];
-            dmma(xv[0], xv[1], tp[rl * (MB + 1) + 4 * s4 + q], bal);
-            dmma(rv[0], rv[1], -tq[rl * (MB + 1) + 4 * s4 + q], bal);
-          }
-        }
 #pragma unroll
         for (int e = 0; e < 2; e++) {
           const int cc = 8 * J + 2 * q + e;
@@ -579,7 +584,7 @@ template <int MB>
 static pcg_status bcg_prepare() {
   static bool done = false;
   if (done) return PCG_OK;
-  const int sm = (int)bcg_dyn_smem<MB>(), sm4 = (int)bcg_dyn_smem<MB>(4), sm1 = (int)bcg_dyn_smem<MB>(1);
+  const int sm = (int)bcg_dyn_smem<MB>(), sm4 = (int)bcg_dyn_smem<MB>(2), sm1 = (int)bcg_dyn_smem<MB>(1);
   PCG_CUDA(cudaFuncSetAttribute(bcg_gram_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   PCG_CUDA(cudaFuncSetAttribute(bcg_update_kernel<MB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4));
   PCG_CUDA(cudaFuncSetAttribute(bcg_update_kernel<MB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4));
@@ -594,7 +599,7 @@ static pcg_status bcg_restart_mb(pcg_matrix *A, const BcgBufs &b, int m, int64_t
                                  int gt, cudaStream_t s) {
   PCG_TRY(bcg_prepare<MB>());
   PCG_TRY(bcg_spmm(A, b.X, b.Q, m, ld, nullptr, s));
-  bcg_update_kernel<MB, 0><<<gt, TW * 32, bcg_dyn_smem<MB>(4), s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm,
+  bcg_update_kernel<MB, 0><<<gt, TW * 32, bcg_dyn_smem<MB>(2), s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm,
                                                                    A->d_dinv, part, st);
   bcg_reduce_kernel<<<m * m + m, GT, 0, s>>>(part, gt, m * m, st->Gn, st->rr, nullptr);
   bcg_small_kernel<<<1, 32, 0, s>>>(st, BS_INIT);
@@ -611,7 +616,7 @@ static pcg_status bcg_step_mb(pcg_matrix *A, const BcgBufs &b, int m, int64_t ld
   bcg_gram_kernel<MB><<<gt, TW * 32, bcg_dyn_smem<MB>(), s>>>(A->n, m, ld, b.P, b.Q, part, st);
   bcg_reduce_kernel<<<m * m, GT, 0, s>>>(part, gt, m * m, st->G, nullptr, st);
   bcg_small_kernel<<<1, 32, 0, s>>>(st, BS_ALPHA);
-  bcg_update_kernel<MB, 1><<<gt, TW * 32, bcg_dyn_smem<MB>(4), s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm,
+  bcg_update_kernel<MB, 1><<<gt, TW * 32, bcg_dyn_smem<MB>(2), s>>>(A->n, m, ld, b.X, b.R, b.Z, b.P, b.Q, b.Bm,
                                                                    A->d_dinv, part, st);
   bcg_reduce_kernel<<<m * m + m, GT, 0, s>>>(part, gt, m * m, st->Gn, st->rr, st);
   bcg_small_kernel<<<1, 32, 0, s>>>(st, BS_BETA);
