@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(TW * 32) bcg_gram_kernel(int64_t n, int m, int
 //   initialised from X and R (fragment rows 8I + g, columns 8J + 2q + {0, 1}); then
 //   Z = dinv R in the fragments.  R and Z go to shared-memory tiles for R^T Z.
 template <int MB, int MODE>
-__global__ void __launch_bounds__(TW * 32) bcg_update_kernel(int64_t n, int m, int64_t ld, double *__restrict__ X,
+__global__ void __launch_bounds__(TW * 32, 4) bcg_update_kernel(int64_t n, int m, int64_t ld, double *__restrict__ X,
                                                              double *__restrict__ R, double *__restrict__ Z,
                                                              double *__restrict__ P, const double *__restrict__ Q,
                                                              const double *__restrict__ Bm,
@@ -292,82 +292,87 @@ __global__ void __launch_bounds__(TW * 32) bcg_update_kernel(int64_t n, int m, i
     if (MODE == 1) {
       const int64_t row = r0 + lane;
       const bool ok = row < n;
-      double pv[MB], qv[MB];
 #pragma unroll
-      for (int c = 0; c < MB; c++) {
-        pv[c] = ok && c < m ? P[(size_t)c * ld + row] : 0.0;
-        qv[c] = ok && c < m ? Q[(size_t)c * ld + row] : 0.0;
-      }
+      for (int c0 = 0; c0 < MB; c0 += 8) {  // 16 loads in flight, few registers
+        double pv[8], qv[8];
 #pragma unroll
-      for (int c = 0; c < MB; c++) {
-        tp[lane * (MB + 1) + c] = pv[c];
-        tq[lane * (MB + 1) + c] = qv[c];
+        for (int u = 0; u < 8; u++) {
+          pv[u] = ok && c0 + u < m ? P[(size_t)(c0 + u) * ld + row] : 0.0;
+          qv[u] = ok && c0 + u < m ? Q[(size_t)(c0 + u) * ld + row] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          tp[lane * (MB + 1) + c0 + u] = pv[u];
+          tq[lane * (MB + 1) + c0 + u] = qv[u];
+        }
       }
       __syncwarp();
     }
-    // all fragment loads of the tile first (X, R or B - Q; dinv), then the mma and stores
-    double xf[4][MB / 8][2], rf[4][MB / 8][2], dv[4];
+    // per pair of 8-row blocks: all fragment loads (X, R or B - Q; dinv), the mma, then
+    // the stores and the R, Z tile (rows of other pairs are not touched meanwhile)
 #pragma unroll
-    for (int I = 0; I < 4; I++) {
-      const int64_t row = r0 + 8 * I + g;
-      const bool rok = row < n;
-      dv[I] = rok ? dinv[row] : 0.0;
+    for (int I0 = 0; I0 < 4; I0 += 2) {
+      double xf[2][MB / 8][2], rf[2][MB / 8][2], dv[2];
 #pragma unroll
-      for (int J = 0; J < MB / 8; J++)
-#pragma unroll
-        for (int e = 0; e < 2; e++) {
-          const int cc = 8 * J + 2 * q + e;
-          xf[I][J][e] = rf[I][J][e] = 0.0;
-          if (rok && cc < m) {
-            const size_t ix = (size_t)cc * ld + row;
-            if (MODE == 0) {
-              rf[I][J][e] = Bm[ix] - Q[ix];
-            } else {
-              xf[I][J][e] = X[ix];
-              rf[I][J][e] = R[ix];
-            }
-          }
-        }
-    }
-    if (MODE == 1) {
-#pragma unroll
-      for (int I = 0; I < 4; I++) {
-        const int rl = 8 * I + g;
+      for (int i = 0; i < 2; i++) {
+        const int64_t row = r0 + 8 * (I0 + i) + g;
+        const bool rok = row < n;
+        dv[i] = rok ? dinv[row] : 0.0;
 #pragma unroll
         for (int J = 0; J < MB / 8; J++)
 #pragma unroll
-          for (int s4 = 0; s4 < MB / 4; s4++) {
-            const double bal = sal[(4 * s4 + q) * MB + 8 * J + g];
-            dmma(xf[I][J][0], xf[I][J][1], tp[rl * (MB + 1) + 4 * s4 + q], bal);
-            dmma(rf[I][J][0], rf[I][J][1], -tq[rl * (MB + 1) + 4 * s4 + q], bal);
+          for (int e = 0; e < 2; e++) {
+            const int cc = 8 * J + 2 * q + e;
+            xf[i][J][e] = rf[i][J][e] = 0.0;
+            if (rok && cc < m) {
+              const size_t ix = (size_t)cc * ld + row;
+              if (MODE == 0) {
+                rf[i][J][e] = Bm[ix] - Q[ix];
+              } else {
+                xf[i][J][e] = X[ix];
+                rf[i][J][e] = R[ix];
+              }
+            }
           }
       }
-      __syncwarp();  // the P, Q tiles are dead: R, Z take their place
-    }
+      if (MODE == 1) {
 #pragma unroll
-    for (int I = 0; I < 4; I++) {
-      const int rl = 8 * I + g;
-      const int64_t row = r0 + rl;
-      const bool rok = row < n;
+        for (int i = 0; i < 2; i++) {
+          const int rl = 8 * (I0 + i) + g;
 #pragma unroll
-      for (int J = 0; J < MB / 8; J++) {
-        double *xv = xf[I][J], *rv = rf[I][J];
+          for (int J = 0; J < MB / 8; J++)
 #pragma unroll
-        for (int e = 0; e < 2; e++) {
-          const int cc = 8 * J + 2 * q + e;
-          const bool ok = rok && cc < m;
-          const double zv = dv[I] * rv[e];
-          if (ok) {
-            const size_t ix = (size_t)cc * ld + row;
-            if (MODE == 1) X[ix] = xv[e];
-            R[ix] = rv[e];
-            Z[ix] = zv;
-            if (MODE == 0) P[ix] = zv;
-          }
-          tr[rl * (MB + 1) + cc] = ok ? rv[e] : 0.0;
-          tz[rl * (MB + 1) + cc] = ok ? zv : 0.0;
-          rr[J][e] = __fma_rn(ok ? rv[e] : 0.0, ok ? rv[e] : 0.0, rr[J][e]);
+            for (int s4 = 0; s4 < MB / 4; s4++) {
+              const double bal = sal[(4 * s4 + q) * MB + 8 * J + g];
+              dmma(xf[i][J][0], xf[i][J][1], tp[rl * (MB + 1) + 4 * s4 + q], bal);
+              dmma(rf[i][J][0], rf[i][J][1], -tq[rl * (MB + 1) + 4 * s4 + q], bal);
+            }
         }
+        __syncwarp();  // these rows of the P, Q tiles are dead: R, Z take their place
+      }
+#pragma unroll
+      for (int i = 0; i < 2; i++) {
+        const int rl = 8 * (I0 + i) + g;
+        const int64_t row = r0 + rl;
+        const bool rok = row < n;
+#pragma unroll
+        for (int J = 0; J < MB / 8; J++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int cc = 8 * J + 2 * q + e;
+            const bool ok = rok && cc < m;
+            const double rv = rf[i][J][e], zv = dv[i] * rv;
+            if (ok) {
+              const size_t ix = (size_t)cc * ld + row;
+              if (MODE == 1) X[ix] = xf[i][J][e];
+              R[ix] = rv;
+              Z[ix] = zv;
+              if (MODE == 0) P[ix] = zv;
+            }
+            tr[rl * (MB + 1) + cc] = ok ? rv : 0.0;
+            tz[rl * (MB + 1) + cc] = ok ? zv : 0.0;
+            rr[J][e] = __fma_rn(ok ? rv : 0.0, ok ? rv : 0.0, rr[J][e]);
+          }
       }
     }
     __syncwarp();
