@@ -21,8 +21,9 @@
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is
  *     ordered after prior work on it; calls return when results are in place
  *     (synchronous).
- *   - Deterministic: same inputs and same GPU count give bitwise-identical x
- *     and iteration counts (fixed grid, fixed-order block reductions).
+ *   - Deterministic: same inputs, flags and GPU count give bitwise-identical x
+ *     and iteration counts (rule-based format choice, fixed grid per device
+ *     model, fixed-order block reductions).
  *   - Thread-safe for distinct matrix handles.
  */
 #ifndef PCG_B200_H
@@ -62,7 +63,11 @@ typedef enum {
                                * inside the calls, so the caller's numbering is unchanged.
                                * restores gather locality for a mesh
                                * numbered arbitrarily.  INVALID_ARG on a distributed handle. */
-#define PCG_FMT_AUTO 0x00  /* pick the faster device format, measured */
+#define PCG_FMT_AUTO 0x00  /* pick the format by a deterministic rule on slice padding:
+                              SELL-32 if its 32-row slices pad <= 2 %, else SELL-C-sigma
+                              if sorting cuts the padding by >= 1 % to <= 25 %, else SELL-32
+                              if <= 25 %, else CSR (environment PCG_FMT_TIMED=1: time 5
+                              SpMVs per candidate instead; not deterministic across runs) */
 #define PCG_FMT_CSR 0x10   /* force CSR (sub-warp per row)            */
 #define PCG_FMT_SELL 0x20  /* force SELL-32 (slices of 32 rows)       */
 #define PCG_FMT_SELL_TMA 0x30 /* force SELL-32 with TMA-staged tiles  */

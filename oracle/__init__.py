@@ -76,6 +76,10 @@ def lib():
         L.orc_pcg.argtypes = [P(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64,
                               P(C.c_int64), P(C.c_double), P(C.c_double),
                               C.c_void_p, C.c_void_p, C.c_int64]
+        L.orc_pcg_ex.argtypes = [P(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64,
+                                 P(C.c_int64), P(C.c_double), P(C.c_double),
+                                 C.c_void_p, C.c_void_p, C.c_int64, P(C.c_int64), C.c_void_p, P(C.c_int64)]
+        L.orc_assemble_free_lattice.argtypes = [P(_Mesh), C.c_int, C.c_void_p, P(_Csr), C.c_void_p]
         L.orc_partition.argtypes = [C.c_int64, C.c_void_p, C.c_int, C.c_void_p]
         L.orc_fd_cube.argtypes = [C.c_int64, C.c_int, P(_Csr), C.c_void_p]
         L.orc_bicgstab.argtypes = [P(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_int64,
@@ -116,6 +120,19 @@ class Csr:
                     self.val.ctypes.data_as(C.POINTER(C.c_double)))
 
     @staticmethod
+    def _adopt_c(s: _Csr) -> "Csr":
+        """Wrap the C arrays without copying (for the largest systems); the C memory
+        stays owned by the returned object and is freed with it."""
+        n, nnz = s.n, s.nnz
+        A = Csr.__new__(Csr)
+        A.n, A.nnz = int(n), int(nnz)
+        A.row_ptr = np.ctypeslib.as_array(s.row_ptr, shape=(n + 1,))
+        A.col = np.ctypeslib.as_array(s.col, shape=(max(nnz, 1),))[:nnz]
+        A.val = np.ctypeslib.as_array(s.val, shape=(max(nnz, 1),))[:nnz]
+        A._owner = _CsrOwner(s)
+        return A
+
+    @staticmethod
     def _from_c(s: _Csr) -> "Csr":
         n, nnz = s.n, s.nnz
         rp = np.ctypeslib.as_array(s.row_ptr, shape=(n + 1,)).copy()
@@ -134,6 +151,17 @@ class Csr:
     def to_scipy(self):
         import scipy.sparse as sp
         return sp.csr_matrix((self.val, self.col, self.row_ptr), shape=(self.n, self.n))
+
+
+class _CsrOwner:
+    def __init__(self, s):
+        self.s = s
+
+    def __del__(self):
+        try:
+            lib().orc_csr_free(C.byref(self.s))
+        except Exception:
+            pass
 
 
 class Mesh:
@@ -247,6 +275,34 @@ def pcg(A: Csr, b, x0=None, tol=1e-10, max_iter=50000, hist: int = 0) -> PcgResu
                        C.byref(rt), _ptr(ah), _ptr(bh), hist)
     return PcgResult(x=x, iterations=it.value, relres_rec=rr.value, relres_true=rt.value,
                      status=st, alpha=ah, beta=bh)
+
+
+def pcg_ex(A: Csr, b, x0=None, tol=1e-10, max_iter=50000) -> PcgResult:
+    """pcg() plus the residual-replacement record (oracle.h orc_pcg_ex): the number of
+    replacements, and the iterate / iteration count at the first one."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(A.n) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+    it, rr, rt = C.c_int64(0), C.c_double(0), C.c_double(0)
+    nrep, kf = C.c_int64(0), C.c_int64(-1)
+    xf = np.zeros(A.n)
+    Ac = A._c()
+    st = lib().orc_pcg_ex(C.byref(Ac), _ptr(b), _ptr(x), tol, max_iter, C.byref(it), C.byref(rr), C.byref(rt),
+                          None, None, 0, C.byref(nrep), _ptr(xf), C.byref(kf))
+    return PcgResult(x=x, iterations=it.value, relres_rec=rr.value, relres_true=rt.value, status=st,
+                     replacements=nrep.value, x_first=xf if kf.value >= 0 else None, k_first=kf.value)
+
+
+def assemble_free_lattice(mesh: Mesh, fkind: int, fparam=(0.0, 0.0, 0.0, 0.0), copy: bool = True):
+    """K_FF and b_F of a lattice P1 mesh with g = 0 and the AXIS policy, without the
+    Neumann K (oracle.h orc_assemble_free_lattice; bitwise assemble + dirichlet)."""
+    fp = np.ascontiguousarray(list(fparam) + [0.0] * (4 - len(fparam)), dtype=np.float64)
+    nf = int((~mesh.boundary).sum())
+    bF = np.zeros(nf)
+    s = _Csr()
+    st = lib().orc_assemble_free_lattice(C.byref(mesh._m), fkind, _ptr(fp), C.byref(s), _ptr(bF))
+    if st != OK:
+        raise RuntimeError(f"orc_assemble_free_lattice failed: {st}")
+    return (Csr._from_c(s) if copy else Csr._adopt_c(s)), bF
 
 
 FD_X2MY2, FD_EXPSIN = 1, 2

@@ -504,6 +504,100 @@ int orc_dirichlet(const orc_mesh *m, const orc_csr *K, const double *F, const do
   return ORC_OK;
 }
 
+/* §8(c).3-6 for the lattice P1 configs with g = 0 and the AXIS policy, without
+ * the Neumann K (oracle.h).  Same element loop and accumulation order as
+ * orc_assemble; row pattern = free axis neighbours + self, ascending. */
+int orc_assemble_free_lattice(const orc_mesh *m, int fkind, const double *fparam, orc_csr *Kff, double *bF) {
+  memset(Kff, 0, sizeof(*Kff));
+  if (m->family != ORC_P1_TRI && m->family != ORC_P1_TET) return ORC_ERR_INVALID_ARG;
+  const int64_t nn = m->n_nodes, np = (int64_t)m->c + 1;
+  const int npe = m->npe, dim = m->dim;
+  /* lattice check: every node at its lattice point (no jitter) */
+  const double h = 1.0 / m->c;
+  for (int64_t id = 0; id < nn; id++) {
+    int64_t q = id;
+    for (int d = 0; d < dim; d++) {
+      if (m->coord[dim * id + d] != (q % np) * h) return ORC_ERR_INVALID_ARG;
+      q /= np;
+    }
+  }
+  int64_t *free_of_node = malloc(sizeof(int64_t) * (nn > 0 ? nn : 1));
+  double *F = malloc(sizeof(double) * (nn > 0 ? nn : 1));
+  if (!free_of_node || !F) return ORC_ERR_OOM;
+  int64_t nf = 0;
+  for (int64_t i = 0; i < nn; i++) free_of_node[i] = m->boundary[i] ? -1 : nf++;
+  /* pattern: node i's free axis neighbours and i, ascending node id (= ascending free id) */
+  const int64_t stride[3] = {1, np, np * np};
+  Kff->n = nf;
+  Kff->row_ptr = calloc(nf + 1, sizeof(int64_t));
+  if (!Kff->row_ptr) return ORC_ERR_OOM;
+  for (int pass = 0; pass < 2; pass++) {
+    for (int64_t i = 0; i < nn; i++) {
+      const int64_t fi = free_of_node[i];
+      if (fi < 0) continue;
+      int64_t nb[7], cnt = 0;
+      for (int d = dim - 1; d >= 0; d--) nb[cnt++] = i - stride[d]; /* interior node: in range */
+      nb[cnt++] = i;
+      for (int d = 0; d < dim; d++) nb[cnt++] = i + stride[d];
+      int64_t u = 0;
+      for (int64_t t = 0; t < cnt; t++) {
+        if (free_of_node[nb[t]] < 0) continue;
+        if (pass == 1) {
+          Kff->col[Kff->row_ptr[fi] + u] = free_of_node[nb[t]];
+          Kff->val[Kff->row_ptr[fi] + u] = 0.0;
+        }
+        u++;
+      }
+      if (pass == 0) Kff->row_ptr[fi + 1] = u;
+    }
+    if (pass == 0) {
+      for (int64_t i = 0; i < nf; i++) Kff->row_ptr[i + 1] += Kff->row_ptr[i];
+      Kff->nnz = Kff->row_ptr[nf];
+      Kff->col = malloc(sizeof(int64_t) * (Kff->nnz > 0 ? Kff->nnz : 1));
+      Kff->val = malloc(sizeof(double) * (Kff->nnz > 0 ? Kff->nnz : 1));
+      if (!Kff->col || !Kff->val) return ORC_ERR_OOM;
+    }
+  }
+  /* values: element by element, local (a,b) order (as orc_assemble) */
+  for (int64_t i = 0; i < nn; i++) F[i] = 0.0;
+  double xe[4 * 3], Ke[16], fe[4];
+  for (int64_t e = 0; e < m->n_elem; e++) {
+    const int32_t *t = m->elem + npe * e;
+    for (int a = 0; a < npe; a++)
+      for (int d = 0; d < dim; d++) xe[dim * a + d] = m->coord[dim * t[a] + d];
+    orc_elem_stiffness(m->family, xe, Ke);
+    for (int a = 0; a < npe; a++) {
+      const int64_t fa = free_of_node[t[a]];
+      if (fa < 0) continue;
+      for (int b = 0; b < npe; b++) {
+        const int64_t fb = free_of_node[t[b]];
+        if (fb < 0) continue;
+        if (!axis_neighbour(m, t[a], t[b])) {
+          if (Ke[npe * a + b] != 0.0) return ORC_ERR_POLICY;
+          continue;
+        }
+        int64_t lo = Kff->row_ptr[fa], hi = Kff->row_ptr[fa + 1] - 1, k = -1;
+        while (lo <= hi) {
+          int64_t mid = lo + (hi - lo) / 2;
+          if (Kff->col[mid] == fb) { k = mid; break; }
+          if (Kff->col[mid] < fb) lo = mid + 1; else hi = mid - 1;
+        }
+        if (k < 0) return ORC_ERR_INVALID_ARG;
+        Kff->val[k] += Ke[npe * a + b];
+      }
+    }
+    for (int a = 0; a < npe; a++) fe[a] = 0.0;
+    orc_elem_load(m->family, xe, fkind, fparam, fe);
+    for (int a = 0; a < npe; a++) F[t[a]] += fe[a];
+  }
+  /* b_F = F_F - K_FB g_B with g = 0: the sum of K_ik * 0 is +0.0, so b_F = F_F */
+  for (int64_t i = 0; i < nn; i++)
+    if (free_of_node[i] >= 0) bF[free_of_node[i]] = F[i] - 0.0;
+  free(F);
+  free(free_of_node);
+  return ORC_OK;
+}
+
 /* ------------------------------------------------------------------ */
 /* kernels of the method, written as their definitions                 */
 /* ------------------------------------------------------------------ */
@@ -552,7 +646,22 @@ static double true_relres(const orc_csr *A, const double *b, const double *x, do
 int orc_pcg(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter,
             int64_t *iters, double *relres_rec, double *relres_true,
             double *alpha_hist, double *beta_hist, int64_t hist_len) {
+  return orc_pcg_ex(A, b, x, tol, max_iter, iters, relres_rec, relres_true, alpha_hist, beta_hist, hist_len,
+                    NULL, NULL, NULL);
+}
+
+/* orc_pcg with the residual-replacement record (§8(c).8 "Exit"): *replacements =
+ * how many times the exit check failed and the loop restarted from the current x;
+ * x_first / k_first (may be NULL) = the iterate and the iteration count at the
+ * first replacement. */
+int orc_pcg_ex(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter,
+               int64_t *iters, double *relres_rec, double *relres_true,
+               double *alpha_hist, double *beta_hist, int64_t hist_len,
+               int64_t *replacements, double *x_first, int64_t *k_first) {
   int64_t n = A->n;
+  int64_t nrep = 0;
+  if (replacements) *replacements = 0;
+  if (k_first) *k_first = -1;
   *iters = 0;
   *relres_rec = 0.0;
   *relres_true = 0.0;
@@ -608,6 +717,12 @@ int orc_pcg(const orc_csr *A, const double *b, double *x, double tol, int64_t ma
       /* exit check on the true residual; residual replacement otherwise */
       double t = true_relres(A, b, x, nb, q);
       if (t <= tol) break;
+      if (nrep == 0) {
+        if (x_first) memcpy(x_first, x, sizeof(double) * n);
+        if (k_first) *k_first = k;
+      }
+      nrep++;
+      if (replacements) *replacements = nrep;
       restart = 1;
       continue;
     }

@@ -93,6 +93,28 @@ int orc_pcg(const orc_csr *A, const double *b, double *x, double tol, int64_t ma
             int64_t *iters, double *relres_rec, double *relres_true,
             double *alpha_hist, double *beta_hist, int64_t hist_len);
 
+/* orc_pcg plus the residual-replacement record: *replacements = number of failed
+ * exit checks (each restarts the loop from the current x, §8(c).8); x_first (n
+ * values) and *k_first = the iterate and iteration count at the first one (k_first
+ * = -1 if none).  Any of the three may be NULL. */
+int orc_pcg_ex(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter,
+               int64_t *iters, double *relres_rec, double *relres_true,
+               double *alpha_hist, double *beta_hist, int64_t hist_len,
+               int64_t *replacements, double *x_first, int64_t *k_first);
+
+/* §8(c).3-6 for the lattice P1 configs only (C1, C4, C5: family P1_TRI / P1_TET
+ * without jitter, homogeneous Dirichlet data g = 0, AXIS pattern policy), without
+ * the Neumann K: K_FF and b_F = F_F are accumulated element by element in the
+ * order of orc_assemble (elements ascending, local (a,b) ascending), so every
+ * entry receives the same additions in the same order as orc_assemble followed by
+ * orc_dirichlet(ORC_PAT_AXIS) and is bitwise equal to it (pinned in tests).  Row i
+ * of K_FF holds the free axis neighbours of node i and i itself, ascending.  An
+ * element coupling between two free non-axis nodes must be exactly 0.0
+ * (ORC_ERR_POLICY otherwise: per element, which implies orc_dirichlet's check on
+ * the sum).  Memory: the mesh + K_FF + one n_nodes load vector (the C5 system at
+ * c = 512 in ~35 GB instead of the Neumann K's ~75 GB). */
+int orc_assemble_free_lattice(const orc_mesh *m, int fkind, const double *fparam, orc_csr *Kff, double *bF);
+
 /* row partition, §8(c).10: bounds[0..G] */
 void orc_partition(int64_t n, const int64_t *row_ptr, int G, int64_t *bounds);
 /* halo list of rows [r0,r1): sorted unique remote columns; returns count,

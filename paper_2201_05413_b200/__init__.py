@@ -46,6 +46,28 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else C.c_void_p(0 if t is None else t.data_ptr())
 
 
+def _pin_host(b, x, out):
+    """Host tensors are staged from pinned memory.  A non-pinned host `out` is replaced
+    by a pinned copy for the call and written back afterwards (_copy_back), so `out`
+    holds the solution on return as documented."""
+    user_out = None
+    if b.device.type == "cpu":
+        if not b.is_pinned():
+            b = b.pin_memory()
+        if not x.is_pinned():
+            if out is not None and x.data_ptr() == out.data_ptr():
+                user_out = out
+            x = x.pin_memory()
+    return b, x, user_out
+
+
+def _copy_back(x, user_out):
+    if user_out is None:
+        return x
+    user_out.copy_(x)
+    return user_out
+
+
 def kernel_launches() -> int:
     """Kernels launched by the library in this process (host launches + graph-executed)."""
     return int(lib().pcg_kernel_launches())
@@ -141,11 +163,7 @@ class Matrix:
             x = out
         else:
             x = torch.zeros_like(b) if x0 is None else _as_tensor(x0, torch.float64).clone()
-        if b.device.type == "cpu":
-            if not b.is_pinned():
-                b = b.pin_memory()
-            if not x.is_pinned():
-                x = x.pin_memory()
+        b, x, user_out = _pin_host(b, x, out)
         info = _lib.PcgInfo()
         st = lib().pcg_solve(self._h, _ptr(b), _ptr(x), float(tol), int(max_iter), _stream_ptr(stream),
                              C.byref(info))
@@ -153,7 +171,7 @@ class Matrix:
             raise PcgError(st, "pcg_solve")
         d = info.as_dict()
         d["status_name"] = _lib.STATUS[st]
-        return x, d
+        return _copy_back(x, user_out), d
 
     def solve_pipelined(self, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None,
                         raise_on=("error",), out=None):
@@ -165,11 +183,7 @@ class Matrix:
             x = out
         else:
             x = torch.zeros_like(b) if x0 is None else _as_tensor(x0, torch.float64).clone()
-        if b.device.type == "cpu":
-            if not b.is_pinned():
-                b = b.pin_memory()
-            if not x.is_pinned():
-                x = x.pin_memory()
+        b, x, user_out = _pin_host(b, x, out)
         info = _lib.PcgInfo()
         st = lib().pcg_solve_pipelined(self._h, _ptr(b), _ptr(x), float(tol), int(max_iter), _stream_ptr(stream),
                                        C.byref(info))
@@ -177,7 +191,7 @@ class Matrix:
             raise PcgError(st, "pcg_solve_pipelined")
         d = info.as_dict()
         d["status_name"] = _lib.STATUS[st]
-        return x, d
+        return _copy_back(x, user_out), d
 
     def bicgstab(self, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, block: int = 1, stream=None,
                  raise_on=("error",), out=None):
@@ -189,11 +203,7 @@ class Matrix:
             x = out
         else:
             x = torch.zeros_like(b) if x0 is None else _as_tensor(x0, torch.float64).clone()
-        if b.device.type == "cpu":
-            if not b.is_pinned():
-                b = b.pin_memory()
-            if not x.is_pinned():
-                x = x.pin_memory()
+        b, x, user_out = _pin_host(b, x, out)
         info = _lib.PcgInfo()
         st = lib().pcg_bicgstab(self._h, _ptr(b), _ptr(x), float(tol), int(max_iter), int(block), _stream_ptr(stream),
                                 C.byref(info))
@@ -201,7 +211,7 @@ class Matrix:
             raise PcgError(st, "pcg_bicgstab")
         d = info.as_dict()
         d["status_name"] = _lib.STATUS[st]
-        return x, d
+        return _copy_back(x, user_out), d
 
     def solve_multi(self, B, X0=None, tol: float = 1e-10, max_iter: int = 50000, stream=None, out=None):
         """k right-hand sides, B an (n, k) tensor (column-major storage is used at the ABI:
@@ -227,11 +237,7 @@ class Matrix:
             Xc = out.t()
         else:
             Xc = torch.zeros_like(Bc) if X0 is None else _as_tensor(X0, torch.float64).t().contiguous()
-        if Bc.device.type == "cpu":
-            if not Bc.is_pinned():
-                Bc = Bc.pin_memory()
-            if not Xc.is_pinned():
-                Xc = Xc.pin_memory()
+        Bc, Xc, user_out = _pin_host(Bc, Xc, out.t() if out is not None else None)
         infos = (_lib.PcgInfo * k)()
         st = getattr(lib(), fname)(self._h, k, _ptr(Bc), n, _ptr(Xc), n, float(tol), int(max_iter),
                                    _stream_ptr(stream), infos)
@@ -242,7 +248,7 @@ class Matrix:
             d = infos[i].as_dict()
             d["status_name"] = _lib.STATUS[infos[i].status]
             out.append(d)
-        return Xc.t(), out
+        return _copy_back(Xc, user_out).t(), out
 
 
 class Comm:

@@ -135,7 +135,7 @@ template <int FMT, int L, int MODE>
 __device__ __forceinline__ void spmv_body(const SellView &S, const CsrView &C, const BicgVecs &v, double &a0,
                                           double &a1, double &a2) {
   const double *__restrict__ G = MODE == SP_AV ? v.ph : (MODE == SP_AT ? v.sh : v.x);
-  auto gather = [&](int j) { return __ldg(G + j); };
+  auto gather = [&](int j) { return ld_weak(G + j); };  // also inside the cooperative kernel
   auto epi = [&](int64_t i, double sv) {
     if (MODE == SP_RESID || MODE == SP_FINAL) {
       const double bi = v.b[i];

@@ -19,6 +19,7 @@
 // The Gram matrices run on the fp64 tensor cores (mma.sync m8n8k4 over 32-row tiles
 // staged per warp in shared memory); the k x k mixing (X, R, P updates) is one thread
 // per row with its m entries in registers and alpha/beta broadcast from shared memory.
+#include <atomic>
 #include <algorithm>
 #include <cstdlib>
 #include <chrono>
@@ -505,7 +506,7 @@ __global__ void bcg_small_kernel(BcgState *st, int mode) {
     if (t == 0) {
       bool all = true;
       for (int a = 0; a < m; a++) all = all && sqrt(st->rr[a]) <= st->tol * st->nb[a];
-      st->done = all ? BCG_OK : BCG_RUNNING;
+      st->done = all ? BCG_OK : (st->it >= st->max_iter ? BCG_MAXIT : BCG_RUNNING);  // orc_block_cg's order
     }
     return;
   }
@@ -585,16 +586,21 @@ static pcg_status bcg_spmm(pcg_matrix *A, const double *P, double *Q, int m, int
 template <int MB>
 static size_t bcg_dyn_smem(int tiles = 2) { return (size_t)TW * tiles * 32 * (MB + 1) * sizeof(double); }
 
+// The dynamic shared-memory opt-in is a per-device function attribute: recorded per
+// device (a second GPU in the same process needs its own), set idempotently (two
+// threads racing here both set the same value).
 template <int MB>
 static pcg_status bcg_prepare() {
-  static bool done = false;
-  if (done) return PCG_OK;
+  static std::atomic<bool> done[64];
+  int dev = 0;
+  PCG_CUDA(cudaGetDevice(&dev));
+  if (dev >= 0 && dev < 64 && done[dev].load(std::memory_order_acquire)) return PCG_OK;
   const int sm = (int)bcg_dyn_smem<MB>(), sm4 = (int)bcg_dyn_smem<MB>(2), sm1 = (int)bcg_dyn_smem<MB>(1);
   PCG_CUDA(cudaFuncSetAttribute(bcg_gram_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   PCG_CUDA(cudaFuncSetAttribute(bcg_update_kernel<MB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4));
   PCG_CUDA(cudaFuncSetAttribute(bcg_update_kernel<MB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4));
   PCG_CUDA(cudaFuncSetAttribute(bcg_pupdate_kernel<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1));
-  done = true;
+  if (dev >= 0 && dev < 64) done[dev].store(true, std::memory_order_release);
   return PCG_OK;
 }
 

@@ -183,6 +183,19 @@ __device__ __forceinline__ int ld_stream(const int *p) {
   return v;
 }
 
+// Coherent (weak, L1-cacheable) load for vectors that the SAME kernel also writes —
+// the gathers of the persistent cooperative kernels, where a grid barrier separates
+// the pass that writes a vector from the pass that reads it.  The PTX memory model
+// orders such a plain load after the barrier's acquire (bar.sync carries thread 0's
+// ld.acquire.gpu to the CTA), whereas ld.global.nc (__ldg) is defined only for data
+// that is read-only for the whole kernel.  volatile for the reason given above; the
+// barrier's own asm carries the memory clobber.
+__device__ __forceinline__ double ld_weak(const double *p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 int num_sms(int device);
 
 }  // namespace pcgb

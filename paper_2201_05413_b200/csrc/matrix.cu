@@ -440,8 +440,16 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
     // built/used on request
     cands = {PCG_FORMAT_CSR, PCG_FORMAT_SELL};
   }
-  // ---- measured format choice (time 5 SpMVs of each candidate)
-  const bool timed = n > 0 && (cands.size() > 1 || (try_sigma && fmt_req == PCG_FMT_AUTO));
+  // ---- format choice.  Default: a deterministic rule on the padding of the slices
+  // (pcg.h promises bitwise-identical results for identical inputs, and the formats
+  // sum in different orders): natural SELL-32 if its slices pad <= 2 %; otherwise
+  // SELL-C-sigma if sorting the sigma-windows cuts the padding by >= 1 % and leaves
+  // <= 25 %, else natural SELL-32 if it pads <= 25 %, else CSR.  The measured choice
+  // (time 5 SpMVs per candidate, round 1's rule) is kept behind PCG_FMT_TIMED=1.
+  const bool fmt_timed = getenv("PCG_FMT_TIMED") != nullptr;
+  if (!fmt_timed && fmt_req == PCG_FMT_AUTO && cands.size() > 1)
+    cands = {want_sell ? PCG_FORMAT_SELL : PCG_FORMAT_CSR};
+  const bool timed = n > 0 && (cands.size() > 1 || (try_sigma && fmt_req == PCG_FMT_AUTO && fmt_timed));
   float best = 1e30f;
   int best_fmt = cands.empty() ? PCG_FORMAT_SELL : cands[0];
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -488,9 +496,16 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
       if (fmt_req == PCG_FMT_SELL_SIGMA) return bs;
     } else {
       float ms = 0;
-      PCG_TRY(time_fmt(PCG_FORMAT_SELL, &ms));
-      A->spmv_us_sigma = ms * 1e3 / 5;
-      if (fmt_req == PCG_FMT_SELL_SIGMA || ms < best) {  // keep the permuted system
+      const double pad_sig = nnz > 0 ? (double)A->sell_entries / (double)nnz : 1.0;
+      bool keep;
+      if (fmt_timed) {
+        PCG_TRY(time_fmt(PCG_FORMAT_SELL, &ms));
+        A->spmv_us_sigma = ms * 1e3 / 5;
+        keep = ms < best;
+      } else {
+        keep = pad_sig <= 1.25 && pad_sig <= pad_nat - 0.01;
+      }
+      if (fmt_req == PCG_FMT_SELL_SIGMA || keep) {  // keep the permuted system
         sigma_free(&S);
         if (A->d_lead) cudaFree(A->d_lead);
         A->d_lead = nullptr;

@@ -575,12 +575,10 @@ static dim3 mgrid_vec(pcg_matrix *A, int k) {
 
 // SpMM pass: persistent grid of SMs x resident blocks (<= 8 per SM: the partials capacity)
 static int mgrid_spmm(pcg_matrix *A, int k) {
-  static bool attr = false;  // up to 32 KB of per-thread sigma partials (k <= 16)
-  if (!attr) {
-    cudaFuncSetAttribute(mspmm_kernel<MS_SPMM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * BLOCK * 16);
-    cudaFuncSetAttribute(mspmm_kernel<MS_SPMM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * BLOCK * 16);
-    attr = true;
-  }
+  // up to 32 KB of per-thread sigma partials (k <= 16): a per-device function attribute,
+  // set on every call (cheap, idempotent) so a second GPU in the process gets it too
+  cudaFuncSetAttribute(mspmm_kernel<MS_SPMM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * BLOCK * 16);
+  cudaFuncSetAttribute(mspmm_kernel<MS_SPMM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * BLOCK * 16);
   int b = 0;
   const size_t smem = k <= 16 ? sizeof(double) * BLOCK * k : 0;
   cudaError_t e = A->max_row_len > 8

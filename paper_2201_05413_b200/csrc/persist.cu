@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(BLOCK, 3) pcg_persist_kernel(SellView S, CsrVi
       if (FMT == PCG_FORMAT_SELL) {
         k1_sell_rows<8>(S, beta, alpha, pold, pnew, v.z, v.x, q, acc);
       } else {
-        auto gather = [&](int j) { return __fma_rn(beta, __ldg(pold + j), __ldg(v.z + j)); };
+        auto gather = [&](int j) { return __fma_rn(beta, ld_weak(pold + j), ld_weak(v.z + j)); };
         auto epi = [&](int64_t i, double s) {
           const double po = pold[i];
           const double pi = __fma_rn(beta, po, v.z[i]);
@@ -93,10 +93,10 @@ __global__ void __launch_bounds__(BLOCK, 3) pcg_persist_kernel(SellView S, CsrVi
     // ---- K1b: q = A p ; sigma = p.q
     {
       double acc = 0.0;
-      auto gather = [&](int j) { return __ldg(p + j); };
+      auto gather = [&](int j) { return ld_weak(p + j); };
       auto epi = [&](int64_t i, double s) {
         __stcs(q + i, s);
-        acc = __fma_rn(__ldg(p + i), s, acc);
+        acc = __fma_rn(ld_weak(p + i), s, acc);
       };
       if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
       else csr_rows<L>(C, gather, epi);

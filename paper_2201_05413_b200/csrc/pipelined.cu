@@ -56,7 +56,7 @@ template <int FMT, int L, int MODE>
 __device__ __noinline__ void pipe_spmv(const SellView &S, const CsrView &C, const PipeVecs &v, double *m_out,
                                        double (&a)[3]) {  // (re)start / exit check only: kept out of the hot loop
   const double *__restrict__ G = MODE == PP_W ? v.u : v.x;
-  auto gather = [&](int j) { return __ldg(G + j); };
+  auto gather = [&](int j) { return ld_weak(G + j); };  // inside the cooperative kernel
   auto epi = [&](int64_t i, double sv) {
     if (MODE == PP_W) {
       v.w[i] = sv;
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) pipe_kernel(SellView S_, CsrView 
       double a[3] = {0.0, 0.0, 0.0};
       const double *__restrict__ m = mc;
       double *__restrict__ m2 = mn;
-      auto gather = [&](int j) { return __ldg(m + j); };
+      auto gather = [&](int j) { return ld_weak(m + j); };  // m is written by this kernel
       auto epi = [&](int64_t i, double nv) {
         const double zi = axpy_rn(nv, beta, v.z[i]);
         const double qi = axpy_rn(m[i], beta, v.q[i]);

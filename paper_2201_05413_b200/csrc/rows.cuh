@@ -134,8 +134,8 @@ __device__ __forceinline__ void k1_sell_rows(const SellView &A, double beta, dou
     // own-row vectors, issued with the matrix stream
     double po = 0.0, zi = 0.0, xi = 0.0;
     if (ok) {
-      po = __ldg(pold + row);
-      zi = __ldg(z + row);
+      po = ld_weak(pold + row);  // written by this kernel in the persistent schedule
+      zi = ld_weak(z + row);
       xi = __ldcs(x + row);
     }
     const double *vp = A.val + base + lane;
@@ -155,7 +155,7 @@ __device__ __forceinline__ void k1_sell_rows(const SellView &A, double beta, dou
       double g[CH];
 #pragma unroll
       for (int u = 0; u < CH; u++)
-        if (t + u < len) g[u] = __fma_rn(beta, __ldg(pold + j[u]), __ldg(z + j[u]));
+        if (t + u < len) g[u] = __fma_rn(beta, ld_weak(pold + j[u]), ld_weak(z + j[u]));
 #pragma unroll
       for (int u = 0; u < CH; u++)
         if (t + u < len) sum = __fma_rn(a[u], g[u], sum);

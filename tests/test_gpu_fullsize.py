@@ -39,13 +39,29 @@ def pcg():
     return p
 
 
+@pytest.fixture(params=["default", "graph"])
+def schedule(request, monkeypatch):
+    """default: the library's own choice (the persistent kernel below 32M rows);
+    graph: PCG_PERSIST=0, the conditional-WHILE graph schedule the C5 bench times."""
+    for k in ("PCG_PERSIST", "PCG_SCHEDULE", "PCG_NO_GRAPH"):
+        monkeypatch.delenv(k, raising=False)
+    if request.param == "graph":
+        monkeypatch.setenv("PCG_PERSIST", "0")
+    return request.param
+
+
 @pytest.mark.parametrize("name", ["C1", "C2", "C4", "C3", "C6"])
-def test_fullsize_vs_oracle_golden(pcg, name):
+def test_fullsize_vs_oracle_golden(pcg, name, schedule):
+    _golden_case(pcg, name)
+
+
+def _golden_case(pcg, name, key=None, c=None):
     g = _gold()
-    if name not in g:
-        pytest.skip(f"{name} golden not generated")
-    g = g[name]
-    spec = pcg.fem_spec(name)
+    key = key or name
+    if key not in g:
+        pytest.skip(f"{key} golden not generated")
+    g = g[key]
+    spec = pcg.fem_spec(name, c=c) if c else pcg.fem_spec(name)
     P = pcg.fem_build(spec)
     n = P["row_ptr"].numel() - 1
     assert n == g["n"] and P["col"].numel() == g["nnz"]
@@ -68,6 +84,23 @@ def test_fullsize_vs_oracle_golden(pcg, name):
         xs, xo = X[idx, j], np.array(ref["x_sample"])
         assert np.linalg.norm(xs - xo) <= 1e-9 * np.linalg.norm(xo), j
         assert abs(np.linalg.norm(X[:, j]) - ref["x_norm"]) <= 1e-9 * ref["x_norm"]
+
+
+def test_c5_c256_vs_oracle_golden(pcg, schedule):
+    """The C5 construction at c = 256 (16.6M unknowns, 116M nnz) against the oracle's
+    solve through the standard pipeline (tests/golden oracle_full.json "C5c256")."""
+    _golden_case(pcg, "C5", key="C5c256", c=256)
+
+
+def test_c5_fullsize_vs_oracle_golden(pcg, monkeypatch):
+    """C5 itself (c = 512, 133M unknowns, 932M nnz) in the launch configuration
+    bench.py times (device generator, PCG_FMT_AUTO, n > 32M -> the graph schedule)
+    against the oracle's full-size solve ("C5full": orc_assemble_free_lattice, bitwise
+    the standard pipeline, + orc_pcg): iterations within max(2 %, 1), x on 257
+    sampled entries and ||x|| within 1e-9, structure at the sampled rows exact."""
+    for k in ("PCG_PERSIST", "PCG_SCHEDULE", "PCG_NO_GRAPH"):
+        monkeypatch.delenv(k, raising=False)
+    _golden_case(pcg, "C5", key="C5full")
 
 
 def test_c5_fullsize_properties(pcg):

@@ -268,3 +268,36 @@ def test_sigma_pcg_parity(pcg, name, c):
         rj = O.pcg(A, B[:, j], tol=tol)
         assert np.linalg.norm(X[:, j] - rj.x) / np.linalg.norm(rj.x) <= 1e-9
         assert abs(infos[j]["iterations"] - rj.iterations) <= max(1, 0.02 * rj.iterations)
+
+
+def test_host_out_not_pinned_receives_the_solution(pcg):
+    """a non-pinned host `out` is staged through pinned memory and must hold
+    x on return (solve, solve_multi)."""
+    import torch
+    P = O.build_problem("C1", c=32)
+    A, b = P["A"], P["B"][:, 0]
+    M = _matrix(pcg, A)
+    out = torch.zeros(A.n, dtype=torch.float64)
+    x, info = M.solve(torch.as_tensor(b), out=out)
+    assert x is out and info["status"] == 0
+    xd, _ = M.solve(_dev(b))
+    assert np.array_equal(out.numpy(), xd.cpu().numpy())
+    B = np.column_stack([b, 2 * b])
+    outk = torch.zeros(2, A.n, dtype=torch.float64).t()  # (n, 2) column-major
+    X, infos = M.solve_multi(torch.as_tensor(B), out=outk)
+    assert X.data_ptr() == outk.data_ptr()
+    assert np.array_equal(outk[:, 0].numpy(), xd.cpu().numpy())
+
+
+@pytest.mark.parametrize("name,c", [("C3", 48), ("C2", 96), ("C6", 20)])
+def test_format_choice_is_deterministic(pcg, name, c):
+    """pcg.h: identical inputs give bitwise-identical results — the AUTO format rule
+    depends on the pattern only, so two handles of one matrix agree exactly."""
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    M1, M2 = _matrix(pcg, A), _matrix(pcg, A)
+    s1, s2 = M1.stats(), M2.stats()
+    assert (s1["format"], s1["sigma"]) == (s2["format"], s2["sigma"])
+    x1, i1 = M1.solve(_dev(b))
+    x2, i2 = M2.solve(_dev(b))
+    assert i1["iterations"] == i2["iterations"] and bool((x1 == x2).all())

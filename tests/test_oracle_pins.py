@@ -768,3 +768,109 @@ def test_pipelined_max_iter():
     P = O.build_problem("C1", c=16, k=1)
     r = O.pcg_pipelined(P["A"], P["B"][:, 0], tol=1e-12, max_iter=5)
     assert r.status == O.NOT_CONVERGED and r.iterations == 5
+
+
+# ---------------------------------------------------------------- round 2 pins
+def test_sin3d_load_discretisation_error_sequence():
+    """C5's load f = 3π² sin πx sin πy sin πz (BASELINE.json configs[4]): x_err (Eq.
+    ERROR-METRIC) against the sampled u = sin πx sin πy sin πz follows the
+    O(h²) sequence SURVEY §8(c) fixes from its independent probe: 1.64e-3 (c = 32),
+    4.11e-4 (c = 64).  A 3π² -> 2π² slip (u scaled by 2/3) gives x_err ≈ 0.33."""
+    want = {32: 1.64e-3, 64: 4.11e-4}
+    errs = {}
+    for c in want:
+        P = O.build_problem("C5", c=c)
+        r = O.pcg(P["A"], P["B"][:, 0], tol=1e-12)
+        X = P["mesh"].coord[P["free_nodes"]]
+        u = np.sin(np.pi * X[:, 0]) * np.sin(np.pi * X[:, 1]) * np.sin(np.pi * X[:, 2])
+        errs[c] = np.linalg.norm(u - r.x) / np.linalg.norm(u)
+        assert abs(errs[c] - want[c]) <= 0.01 * want[c], (c, errs[c])
+    assert 3.9 < errs[32] / errs[64] < 4.1
+
+
+@pytest.mark.parametrize("centre", [(0.5, 0.5, 0.5), (0.37, 0.52, 0.61)])
+def test_bump3d_load_integrates_the_gaussian(centre):
+    """C4's load f = exp(-|x - c|²/(2σ²)) (BASELINE.json configs[3], σ = 0.05, reading
+    Q10): for an interior bump the Neumann load vector sums to ∫f = (2πσ²)^{3/2} (the
+    Gaussian integral; the tail outside the cube is < 1e-20).  σ² in place of 2σ²
+    changes the sum by 2^{-3/2}; a dropped quadrature weight by 4/3 or more."""
+    sigma = 0.05
+    m = O.Mesh(O.P1_TET, 32)
+    F = O.assemble_load(m, O.F_BUMP3D, (centre[0], centre[1], centre[2], sigma))
+    want = (2 * math.pi * sigma ** 2) ** 1.5
+    assert abs(F.sum() - want) <= 1e-9 * want
+
+
+def _splitmix64_py(seed, idx):
+    """SplitMix64 (Steele, Lea, Flood 2014) in Python integers, itself pinned below by
+    the published sequence test (tests/golden/splitmix64_seed0.txt)."""
+    M = (1 << 64) - 1
+    z = (seed + (idx + 1) * 0x9E3779B97F4A7C15) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+def test_splitmix64_python_twin_matches_published_sequence():
+    rows = _golden_rows("splitmix64_seed0.txt")
+    for i, row in enumerate(rows):
+        assert _splitmix64_py(0, i) == int(row[0], 16)
+
+
+def test_bump_centres_index_mapping():
+    """§8(c).11: c_s = (u(seed, 3s), u(seed, 3s+1), u(seed, 3s+2)), u = top 53 bits of
+    SplitMix64 × 2^-53, computed here from the Python twin (not the oracle's C)."""
+    seed = O.configs()["C4"]["seed"]
+    cs = O.bump_centres(seed, 16)
+    for s in range(16):
+        for a in range(3):
+            u = (_splitmix64_py(seed, 3 * s + a) >> 11) * 2.0 ** -53
+            assert cs[s, a] == u, (s, a)
+
+
+@pytest.mark.parametrize("name,c", [("C1", 16), ("C1", 64), ("C4", 8), ("C5", 12)])
+def test_free_lattice_assembly_is_bitwise_the_pipeline(name, c):
+    """orc_assemble_free_lattice (the C5 full-size golden's builder) equals
+    orc_assemble + orc_dirichlet(AXIS) bitwise: same pattern, same values, same b."""
+    P = O.build_problem(name, c=c, k=1 if name == "C4" else None)
+    cfg = P["cfg"]
+    if cfg["f"] == "BUMP3D":
+        cs = O.bump_centres(cfg["seed"], 1)[0]
+        fk, fp = O.F_BUMP3D, (cs[0], cs[1], cs[2], cfg["sigma"])
+    else:
+        fk, fp = {"SIN2D": O.F_SIN2D, "SIN3D": O.F_SIN3D}[cfg["f"]], (1.0, 0.0, 0.0, 0.0)
+    A, b = O.assemble_free_lattice(P["mesh"], fk, fp)
+    assert np.array_equal(A.row_ptr, P["A"].row_ptr) and np.array_equal(A.col, P["A"].col)
+    assert A.val.tobytes() == P["A"].val.tobytes()
+    assert b.tobytes() == P["B"][:, 0].tobytes()
+
+
+def test_residual_replacement_fires_and_is_a_restart():
+    """§8(c).8 exit: when the recurrence residual passes tol but the true residual
+    (Eq. relativeError) does not, the loop restarts from the current x with
+    r = b - Ax, z = dinv r, p = z, counting on.  At tol = 1e-15 on C1 the recurrence
+    drops below the attainable accuracy (true relres floor ~1e-13), so replacements
+    fire; the continuation after the first one must be exactly a fresh solve from that
+    iterate with the remaining iteration budget (same x bits, same count)."""
+    P = O.build_problem("C1")
+    A, b = P["A"], P["B"][:, 0]
+    r = O.pcg_ex(A, b, tol=1e-15, max_iter=400)
+    assert r.status == O.NOT_CONVERGED and r.iterations == 400
+    assert r.replacements >= 2 and 100 <= r.k_first < 400
+    assert r.relres_true < 1e-12  # replacement keeps the iterate at attainable accuracy
+    r2 = O.pcg_ex(A, b, x0=r.x_first, tol=1e-15, max_iter=400 - r.k_first)
+    assert r2.iterations == 400 - r.k_first and r2.replacements == r.replacements - 1
+    assert r2.x.tobytes() == r.x.tobytes()
+    # without replacement firing, pcg_ex is pcg
+    r3 = O.pcg_ex(A, b, tol=1e-10)
+    r4 = O.pcg(A, b, tol=1e-10)
+    assert r3.replacements == 0 and r3.k_first == -1 and r3.x.tobytes() == r4.x.tobytes()
+
+
+def test_residual_replacement_then_convergence():
+    """A replacement followed by convergence (status OK): C4 construction at c = 16,
+    bump 0, tol = 1e-15 — the true residual fails the exit check once, the restart
+    converges in the next iteration."""
+    P = O.build_problem("C4", c=16, k=1)
+    r = O.pcg_ex(P["A"], P["B"][:, 0], tol=1e-15, max_iter=300)
+    assert r.status == O.OK and r.replacements >= 1 and r.relres_true <= 1e-15
