@@ -37,6 +37,40 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+_lib_omp = None
+
+
+def build_omp(force: bool = False) -> str:
+    """TIMING-ONLY all-cores build of the same oracle.c (-fopenmp -DORC_OMP: OpenMP
+    static loops, chunked Dot2).  Used by bench.py's CPU legs only, never for parity."""
+    if force or not os.path.exists(_LIB_OMP) or os.path.getmtime(_LIB_OMP) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+                               "-DORC_OMP", "-fPIC", "-shared", "-o", _LIB_OMP, _SRC, "-lm"])
+    return _LIB_OMP
+
+
+def pcg_all_cores(A, b, tol=1e-10, max_iter=50000):
+    """Jacobi-PCG of the all-cores timing build (OMP_NUM_THREADS / all host cores).
+    Returns (iterations, status, threads).  Timing only."""
+    global _lib_omp
+    if _lib_omp is None:
+        L = C.CDLL(build_omp())
+        L.orc_pcg.argtypes = [C.POINTER(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64,
+                              C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                              C.c_void_p, C.c_void_p, C.c_int64]
+        _lib_omp = L
+    import numpy as _np
+    b = _np.ascontiguousarray(b, dtype=_np.float64)
+    x = _np.zeros(A.n)
+    it, rr, rt = C.c_int64(0), C.c_double(0), C.c_double(0)
+    Ac = A._c()
+    st = _lib_omp.orc_pcg(C.byref(Ac), b.ctypes.data_as(C.c_void_p), x.ctypes.data_as(C.c_void_p), tol, max_iter,
+                          C.byref(it), C.byref(rr), C.byref(rt), None, None, 0)
+    threads = int(os.environ.get("OMP_NUM_THREADS", "0")) or len(os.sched_getaffinity(0))
+    return it.value, st, threads
+
+
 class _Mesh(C.Structure):
     _fields_ = [("dim", C.c_int), ("family", C.c_int), ("c", C.c_int),
                 ("n_nodes", C.c_int64), ("n_elem", C.c_int64), ("npe", C.c_int),

@@ -15,6 +15,18 @@
  */
 #include "oracle.h"
 
+/* ORC_OMP: the TIMING-ONLY all-cores build of this same file (bench.py's CPU legs,
+ * SURVEY §8(d) "at all host cores"): the SpMV and the PCG vector loops become
+ * OpenMP static loops and the Dot2 inner product sums fixed chunks, one per thread,
+ * whose (sum, error) pairs are combined in chunk order.  The default build (every
+ * test and golden) compiles none of this: ORC_PARFOR expands to nothing. */
+#ifdef ORC_OMP
+#include <omp.h>
+#define ORC_PARFOR _Pragma("omp parallel for schedule(static)")
+#else
+#define ORC_PARFOR
+#endif
+
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -602,6 +614,7 @@ int orc_assemble_free_lattice(const orc_mesh *m, int fkind, const double *fparam
 /* kernels of the method, written as their definitions                 */
 /* ------------------------------------------------------------------ */
 void orc_spmv(const orc_csr *A, const double *x, double *y) {
+  ORC_PARFOR
   for (int64_t i = 0; i < A->n; i++) {
     double s = 0.0;
     for (int64_t k = A->row_ptr[i]; k < A->row_ptr[i + 1]; k++) s += A->val[k] * x[A->col[k]];
@@ -618,9 +631,9 @@ void orc_spmv(const orc_csr *A, const double *x, double *y) {
  * n ~ 4e6 that accumulated error alone delays convergence by 10-17 % (C3 at
  * c = 512: 2673 vs 2422 iterations), so the plain loop would not be "the
  * recurrence of §8(c).8" the parity contract compares against (R1). */
-static double dot(int64_t n, const double *a, const double *b) {
+static void dot2_range(int64_t i0, int64_t i1, const double *a, const double *b, double *pp, double *ss) {
   double p = 0.0, s = 0.0;
-  for (int64_t i = 0; i < n; i++) {
+  for (int64_t i = i0; i < i1; i++) {
     const double h = a[i] * b[i];
     const double r = fma(a[i], b[i], -h); /* TwoProduct: h + r == a_i b_i exactly */
     const double x = p + h;               /* TwoSum: x + q == p + h exactly */
@@ -629,7 +642,30 @@ static double dot(int64_t n, const double *a, const double *b) {
     p = x;
     s += q + r;
   }
+  *pp = p;
+  *ss = s;
+}
+
+static double dot(int64_t n, const double *a, const double *b) {
+#ifdef ORC_OMP
+  enum { MAXCH = 256 };
+  double P[MAXCH], S[MAXCH];
+  int T = omp_get_max_threads();
+  if (T > MAXCH) T = MAXCH;
+#pragma omp parallel for schedule(static, 1)
+  for (int t = 0; t < T; t++) dot2_range(n * t / T, n * (t + 1) / T, a, b, &P[t], &S[t]);
+  double p = 0.0, s = 0.0;
+  for (int t = 0; t < T; t++) { /* TwoSum of the chunk sums, in chunk order */
+    const double x = p + P[t], z = x - p;
+    s += ((p - (x - z)) + (P[t] - z)) + S[t];
+    p = x;
+  }
   return p + s;
+#else
+  double p, s;
+  dot2_range(0, n, a, b, &p, &s);
+  return p + s;
+#endif
 }
 
 double orc_dot(int64_t n, const double *a, const double *b) { return dot(n, a, b); }
@@ -683,6 +719,7 @@ int orc_pcg_ex(const orc_csr *A, const double *b, double *x, double tol, int64_t
   }
   double nb = sqrt(dot(n, b, b));
   if (nb == 0.0) {
+    ORC_PARFOR
     for (int64_t i = 0; i < n; i++) x[i] = 0.0;
     goto out;
   }
@@ -693,11 +730,14 @@ int orc_pcg_ex(const orc_csr *A, const double *b, double *x, double tol, int64_t
     if (restart) {
       /* r = b - A x; z = dinv∘r; p = z; rho = r·z */
       orc_spmv(A, x, q);
+      ORC_PARFOR
       for (int64_t i = 0; i < n; i++) r[i] = b[i] - q[i];
       double rr = sqrt(dot(n, r, r));
       *relres_rec = rr / nb;
       if (rr <= tol * nb) break; /* -> exit check */
+      ORC_PARFOR
       for (int64_t i = 0; i < n; i++) z[i] = dinv[i] * r[i];
+      ORC_PARFOR
       for (int64_t i = 0; i < n; i++) p[i] = z[i];
       rho = dot(n, r, z);
       restart = 0;
@@ -709,7 +749,9 @@ int orc_pcg_ex(const orc_csr *A, const double *b, double *x, double tol, int64_t
     double alpha = rho / sigma;
     if (alpha_hist && k < hist_len) alpha_hist[k] = alpha;
     k++;
+    ORC_PARFOR
     for (int64_t i = 0; i < n; i++) x[i] = x[i] + alpha * p[i];
+    ORC_PARFOR
     for (int64_t i = 0; i < n; i++) r[i] = r[i] - alpha * q[i];
     double gamma = dot(n, r, r);
     *relres_rec = sqrt(gamma) / nb;
@@ -726,11 +768,13 @@ int orc_pcg_ex(const orc_csr *A, const double *b, double *x, double tol, int64_t
       restart = 1;
       continue;
     }
+    ORC_PARFOR
     for (int64_t i = 0; i < n; i++) z[i] = dinv[i] * r[i];
     double rho_new = dot(n, r, z);
     double beta = rho_new / rho;
     if (beta_hist && k - 1 < hist_len) beta_hist[k - 1] = beta;
     rho = rho_new;
+    ORC_PARFOR
     for (int64_t i = 0; i < n; i++) p[i] = z[i] + beta * p[i];
   }
   *iters = k;

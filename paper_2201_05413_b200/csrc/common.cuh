@@ -66,6 +66,7 @@ struct MultiScalars {
   double xpend[KMAX];        // alpha still owed to x (applied by the next K1 / tail)
   double part[3][KMAX];      // allreduce staging (sigma | rho',gamma | ww,wz,bb)
   long long k[KMAX];
+  long long nrep[KMAX];      // residual replacements per column (exit check failed, restarted)
   int done[KMAX];            // per column, same codes as Scalars::done
   int active[KMAX];          // 1 while the column iterates (frozen columns: 0)
   int replace[KMAX];         // residual replacement requested by the exit check

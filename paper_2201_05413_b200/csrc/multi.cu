@@ -446,6 +446,7 @@ __global__ void mresid_finish_kernel(MultiScalars *sc, int mode) {
     const double ww = sc->part[0][c], wz = sc->part[1][c], bb = sc->part[2][c];
     if (mode == 0) {  // init
       sc->k[c] = 0;
+      sc->nrep[c] = 0;
       sc->xpend[c] = 0.0;
       sc->alpha[c] = sc->beta[c] = 0.0;
       sc->relres_true[c] = 0.0;
@@ -480,6 +481,7 @@ __global__ void mresid_finish_kernel(MultiScalars *sc, int mode) {
           sc->done[c] = DONE_RUNNING;
           sc->active[c] = 1;
           sc->replace[c] = 1;
+          sc->nrep[c] += 1;
           sc->rho[c] = wz;
           sc->beta[c] = 0.0;
           sc->xpend[c] = 0.0;
@@ -803,6 +805,7 @@ static pcg_status solve_multi_chunk(pcg_matrix *A, int k, const double *B, int64
       pcg_info &I = infos[c];
       memset(&I, 0, sizeof(I));
       I.iterations = h->k[c];
+      I.replacements = h->nrep[c];
       I.relres_recurrence = h->relres_rec[c];
       I.relres_true = h->done[c] == DONE_ZERO_RHS ? 0.0 : h->relres_true[c];
       I.converged = s == PCG_OK;
