@@ -98,52 +98,111 @@ class ClockSampler:
         return False
 
 
-# ------------------------------------------------------------------------------ CPU oracle leg
-def oracle_sample(cfg_name: str, c_sample: int, reps: int = 1):
-    """Time the oracle (as it stands, 1 thread) on the same construction at c_sample."""
+# ------------------------------------------------------------------------------ CPU oracle legs
+# The oracle (oracle/oracle.c, plain C, one thread, "as it stands") is timed on this
+# host's cores; nothing here loads the product library (libpcg_b200.so).
+GOLD = os.path.join(ROOT, "tests", "golden", "oracle_full.json")
+
+
+def host_cpu():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu": model, "host_cores": len(os.sched_getaffinity(0)), "logical_cpus": os.cpu_count()}
+
+
+def closed_form_size(name, c):
+    """n, nnz of the configs from SURVEY §8(c).7's closed forms (no library, no oracle);
+    None for C6 (jittered element graph: no closed form)."""
+    m = c - 1
+    if name == "C1":
+        return m * m, 5 * m * m - 4 * m
+    if name == "C2":
+        return m * m, 7 * m * m - 8 * m + 2
+    if name == "C3":
+        return (2 * c - 1) ** 2, 46 * c * c - 96 * c + 53
+    if name in ("C4", "C5"):
+        return m ** 3, 7 * m ** 3 - 6 * m * m
+    return None
+
+
+def oracle_golden(key):
+    if os.path.exists(GOLD):
+        with open(GOLD) as fh:
+            return json.load(fh).get(key)
+    return None
+
+
+def oracle_sample(cfg_name: str, c_sample: int, reps: int = 1, all_cores: bool = True):
+    """Time the oracle on the same construction at c_sample: the plain 1-thread build
+    (as it stands) and, once, the all-cores timing build (oracle/__init__.py build_omp)."""
     import oracle as O
     P = O.build_problem(cfg_name, c=c_sample)
     A, b = P["A"], P["B"][:, 0]
+    tol = O.configs()[cfg_name]["tol"]
     times, its = [], None
     for _ in range(reps):
         t0 = time.perf_counter()
-        r = O.pcg(A, b, tol=O.configs()[cfg_name]["tol"])
+        r = O.pcg(A, b, tol=tol)
         times.append(time.perf_counter() - t0)
         its = r.iterations
-    return {"n": A.n, "nnz": A.nnz, "iterations": its, "t_solve": times}
+    out = {"n": A.n, "nnz": A.nnz, "iterations": its, "t_solve": times, "c": c_sample}
+    if all_cores:
+        t0 = time.perf_counter()
+        it2, st2, threads = O.pcg_all_cores(A, b, tol=tol)
+        out["all_cores"] = {"t_solve": time.perf_counter() - t0, "threads": threads, "iterations": it2}
+    return out
 
 
 def iter_bytes(n, nnz, k=1):
     return 12.0 * nnz + 4.0 * (n + 1) + 88.0 * k * n
 
 
-def scale_to_workload(sample, n, nnz, iters):
-    """time-to-solution of the workload implied by the sample's per-iteration cost
-    (per-iteration bytes ratio) and the workload's iteration count."""
-    per_iter = statistics.median(sample["t_solve"]) / sample["iterations"]
+def scale_to_workload(t_solve, sample, n, nnz, iters):
+    """time-to-solution of the workload implied by the sample's measured per-iteration
+    time (scaled by per-iteration bytes) and an iteration count for the workload."""
+    per_iter = t_solve / sample["iterations"]
     return per_iter * iter_bytes(n, nnz) / iter_bytes(sample["n"], sample["nnz"]) * iters
 
 
-def estimate_iterations(name, c_full, sample):
-    # Jacobi-PCG iterations on the lattice grow ~1.95x per doubling of c (SURVEY §8(c) probes)
-    import math
-    return sample["iterations"] * 1.95 ** math.log2(c_full / sample["c"])
+def oracle_full_iterations(name, c):
+    """The oracle's own iteration count on the workload, from its full-size golden run
+    (tests/golden/oracle_full.json, written by oracle/make_golden.py), if present."""
+    cfg_c = None
+    try:
+        import oracle as O
+        cfg_c = O.configs()[name]["c"]
+    except Exception:
+        pass
+    if c != cfg_c:
+        return None, None
+    g = oracle_golden("C5full" if name == "C5" else name)
+    if not g:
+        return None, None
+    return max(r["iterations"] for r in g["rhs"]), g.get("oracle_timing")
 
 
 def run_reference(args):
+    """The reference arm of this tier: the oracle itself, timed on this host.  A step =
+    one complete oracle time-to-solution (plain 1-thread build, as it stands) of the
+    workload's construction at c = --ref-c (a bounded sample: the full C5 solve takes
+    over an hour on one core); value = the measured median step.  The full-workload
+    figure derived from it is reported separately and labelled as an estimate."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_2201_05413_b200.problems import configs
-    cfg = configs()[args.config]
-    c_full = args.c or cfg["c"]
-    from paper_2201_05413_b200.problems import fem_spec, problem_size
-    n, nnz, _ = problem_size(fem_spec(args.config, c=c_full))
     import oracle as O
-    P = O.build_problem(args.config, c=args.sample_c)
+    cfg = O.configs()[args.config]
+    c_full = args.c or cfg["c"]
+    cs = args.ref_c
+    P = O.build_problem(args.config, c=cs)
     A, b = P["A"], P["B"][:, 0]
-    if nnz < 0:  # 3D element pattern: no closed form; the sample's nnz per row
-        nnz = int(round(A.nnz / A.n * n))
     times, its = [], 0
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -152,17 +211,34 @@ def run_reference(args):
         if s >= args.warmup:
             times.append(dt)
         its = r.iterations
-    sample = {"n": A.n, "nnz": A.nnz, "iterations": its, "t_solve": times, "c": args.sample_c}
-    iters = args.ref_iters or estimate_iterations(args.config, c_full, sample)
-    value = scale_to_workload(sample, n, nnz, iters)
-    desc = (f"oracle Jacobi-PCG (oracle/oracle.c, 1 thread, as it stands) on the {args.config} construction at "
-            f"c={args.sample_c} ({A.n} unknowns, {A.nnz} nnz, {its} iterations, median {statistics.median(times):.2f}"
-            f" s/solve); scaled to the workload by per-iteration bytes x {iters:.0f} iterations")
+    value = statistics.median(times)
+    sample = {"n": A.n, "nnz": A.nnz, "iterations": its, "c": cs}
+    t0 = time.perf_counter()
+    it2, _, threads = O.pcg_all_cores(A, b, tol=cfg["tol"])
+    t_all = time.perf_counter() - t0
+    size = closed_form_size(args.config, c_full)
+    est = None
+    if size:
+        n, nnz = size
+        iters_full, timing = oracle_full_iterations(args.config, c_full)
+        if iters_full:
+            est = {"value": scale_to_workload(value, sample, n, nnz, iters_full), "unit": "s",
+                   "basis": (f"this run's per-iteration time x per-iteration bytes ({n} / {A.n} unknowns) x the "
+                             f"oracle's own {iters_full} iterations on the full workload (tests/golden)"),
+                   "oracle_measured_full_size": timing}
+    hc = host_cpu()
+    desc = (f"{args.config} construction at c={cs} ({A.n} unknowns, {A.nnz} nnz, {its} iterations): one complete "
+            f"oracle Jacobi-PCG solve per step (oracle/oracle.c as it stands, 1 thread); measured, not scaled")
+    wl = workload_config(args.config, c_full, *(size or (None, None)), args.gpus)
+    wl["timed_sample"] = f"{args.config} construction at c={cs} (the reference arm's bounded sample)"
     line = {"impl": "reference", "metric": "pcg_time_to_solution", "value": value, "unit": "s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(args.config, c_full, n, nnz, args.gpus),
-            "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "oracle", "sample": desc},
+            "data": "synthetic", "config": wl,
+            "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "oracle", "sample": desc, **hc,
+                             "all_cores": {"value": t_all, "unit": "s", "cores": threads, "iterations": it2,
+                                           "build": "oracle.c -fopenmp -DORC_OMP (timing only)"}},
+            "full_workload_estimate": est,
             "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -176,6 +252,8 @@ def workload_config(name, c, n, nnz, gpus):
             "C1": f"C1: 2D P1 {c}^2 cells, sin RHS",
             "C6": f"C6: 3D P1 Kuhn tets on a {c}^3-cell cube, interior nodes jittered by +-0.15h (irregular "
                   f"stand-in for the paper's Sphere meshes), f = 0, linear Dirichlet data"}[name]
+    if n is None:
+        return {"workload": desc, "config": name, "global_batch": 1, "tol": 1e-10}
     return {"workload": desc, "config": name, "n": n, "nnz": nnz, "global_batch": 1, "tol": 1e-10,
             "parallelism": f"row-partition over {gpus} GPU(s): halo of z + 2 scalar allreduces per iteration"
             if gpus > 1 else "1 GPU",
@@ -194,8 +272,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
     ap.add_argument("--c", type=int, default=None, help="override cells per axis (testing)")
-    ap.add_argument("--sample-c", type=int, default=96, help="oracle sample size for the CPU legs")
-    ap.add_argument("--ref-iters", type=float, default=None)
+    ap.add_argument("--sample-c", type=int, default=96, help="oracle sample size of the GPU arm's cpu_baseline")
+    ap.add_argument("--ref-c", type=int, default=64, help="oracle sample size of the reference arm's steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fmt", default="auto", choices=["auto", "csr", "sell", "sigma"])
     ap.add_argument("--relabel", type=int, default=None, metavar="SEED",
@@ -481,16 +559,24 @@ def main():
                            "12 nnz + 4(n+1) + 112 k n + 8 n bytes per iteration)"),
                 "independent_solver_kernels_for_comparison": roof}
 
-    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    # ---- CPU oracle baseline (rank 0, N = 1 only): measured on a bounded sample, scaled
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = oracle_sample(args.config, args.sample_c)
-        smp["c"] = args.sample_c
-        v = scale_to_workload(smp, n, nnz_given, iters) * kcols  # the oracle solves the k columns one by one
-        cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
-               "sample": f"oracle/oracle.c Jacobi-PCG, 1 thread, {args.config} construction at c={args.sample_c} "
-                         f"({smp['n']} unknowns, {smp['nnz']} nnz, {smp['iterations']} iterations, "
-                         f"{smp['t_solve'][0]:.2f} s); scaled by per-iteration bytes x {iters} GPU iterations"}
+        iters_full, timing = oracle_full_iterations(args.config, c)
+        it_w = iters_full or iters
+        t1 = statistics.median(smp["t_solve"])
+        v = scale_to_workload(t1, smp, n, nnz_given, it_w) * kcols  # the oracle solves the k columns one by one
+        ac = smp.get("all_cores")
+        cpu = {"value": v, "unit": "s", "cores": 1, "kind": "oracle", **host_cpu(),
+               "sample": (f"oracle/oracle.c Jacobi-PCG as it stands, 1 thread, on the {args.config} construction at "
+                          f"c={args.sample_c} ({smp['n']} unknowns, {smp['nnz']} nnz, {smp['iterations']} "
+                          f"iterations, measured {t1:.2f} s); scaled to the workload by per-iteration bytes x "
+                          f"{it_w} iterations ({'the oracle own full-size count, tests/golden' if iters_full else 'the GPU count'})"),
+               "all_cores": ({"value": scale_to_workload(ac["t_solve"], smp, n, nnz_given, it_w) * kcols,
+                              "cores": ac["threads"], "measured_sample_s": ac["t_solve"],
+                              "build": "oracle.c -fopenmp -DORC_OMP (timing only)"} if ac else None),
+               "oracle_measured_full_size": timing}
 
     if rank == 0:
         h2d = 16 * (r1 - r0) * kcols  # b and x0 per column
@@ -551,18 +637,24 @@ def run_bicgstab(args):
             if s_ >= args.warmup:
                 times.append(time.perf_counter() - t0)
             its = r.iterations
+        value = statistics.median(times)
         iters = its * (N - 1) / (Ns - 1)  # BiCGSTAB+Jacobi steps grow ~linearly in N here (37/81/169 at 16/32/64)
         nnz = 7 * (N - 2) ** 3 + n - (N - 2) ** 3
         per_iter_bytes = lambda nn, zz: 2 * (12.0 * zz + 28.0 * nn) + 136.0 * nn  # noqa: E731
-        v = statistics.median(times) / its * per_iter_bytes(n, nnz) / per_iter_bytes(A.n, A.nnz) * iters
-        line = {"impl": "reference", "metric": "bicgstab_time_to_solution", "value": v, "unit": "s", "n_gpus": 1,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"{args.config}: Table 1 grid {N}^3 nodes, BiCGSTAB block={bs}", "n": n},
-                "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle",
-                                 "sample": f"oracle BiCGSTAB on the {Ns}^3 grid ({its} iterations), scaled by "
-                                           f"per-iteration bytes x {iters:.0f} estimated iterations"},
-                "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        est = value / its * per_iter_bytes(n, nnz) / per_iter_bytes(A.n, A.nnz) * iters
+        desc = (f"oracle BiCGSTAB (1 thread, as it stands) on the {Ns}^3 Table 1 grid ({its} iterations), one "
+                f"complete solve per step; measured, not scaled")
+        line = {"impl": "reference", "metric": "bicgstab_time_to_solution", "value": value, "unit": "s",
+                "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": f"{args.config}: Table 1 grid {N}^3 nodes, BiCGSTAB block={bs}", "n": n,
+                           "timed_sample": f"{Ns}^3 nodes"},
+                "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "oracle", "sample": desc,
+                                 **host_cpu()},
+                "full_workload_estimate": {"value": est, "unit": "s",
+                                           "basis": f"per-iteration bytes x {iters:.0f} estimated iterations"},
+                "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
     import ctypes as C

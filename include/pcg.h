@@ -225,6 +225,17 @@ pcg_status pcg_partition_rows(int64_t n, const int64_t *row_ptr, int32_t G, int6
 pcg_status pcg_comm_unique_id(void *id128);
 pcg_status pcg_comm_init(int32_t rank, int32_t size, const void *id128, pcg_comm_t *out);
 pcg_status pcg_comm_destroy(pcg_comm_t comm);
+/* Failure detection (every host wait of a distributed call): the library polls the
+ * queued work and ncclCommGetAsyncError; an asynchronous NCCL error, or no completion
+ * within the communicator's timeout (default 300 s, environment PCG_COMM_TIMEOUT_S at
+ * pcg_comm_init, or pcg_comm_set_timeout), aborts the communicator (ncclCommAbort)
+ * and the call returns PCG_ERR_NCCL instead of blocking.  Every rank applies the same
+ * rule, so a rank that dies or fails makes its peers fail within their timeout.  An
+ * aborted communicator stays unusable: later calls on handles built on it return
+ * PCG_ERR_NCCL; destroy the handles and the communicator and build new ones.
+ * pcg_comm_abort aborts on request (e.g. from a caller's own watchdog). */
+pcg_status pcg_comm_set_timeout(pcg_comm_t comm, double seconds);
+pcg_status pcg_comm_abort(pcg_comm_t comm);
 
 /* Host-callback communicator: the same distributed path (csr_create_dist, pcg_solve,
  * pcg_spmv) with every exchange step done by caller-supplied host functions instead of

@@ -348,6 +348,16 @@ class Comm:
         self.rank, self.size = rank, size
         return self
 
+    def set_timeout(self, seconds: float):
+        """Failure detection (pcg.h): a distributed call that sees no progress for
+        `seconds` (or an asynchronous NCCL error) aborts the communicator and raises
+        PcgError(PCG_ERR_NCCL) instead of blocking."""
+        check(lib().pcg_comm_set_timeout(self._h, float(seconds)), "pcg_comm_set_timeout")
+
+    def abort(self):
+        """ncclCommAbort: pending and later calls on this communicator fail with PCG_ERR_NCCL."""
+        check(lib().pcg_comm_abort(self._h), "pcg_comm_abort")
+
     def close(self):
         if self._h and self._h.value:
             lib().pcg_comm_destroy(self._h)

@@ -845,7 +845,7 @@ static pcg_status bg_solve(pcg_matrix *A, const BicgVecs &v, int bs, double tol,
   auto read = [&]() -> pcg_status {
     PCG_CUDA(cudaGetLastError());
     PCG_CUDA(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
-    PCG_CUDA(cudaStreamSynchronize(st));
+    PCG_TRY(comm_wait(A->comm, st));
     return PCG_OK;
   };
   ops.resid(A, v, sc, w.partials, BR_INIT, st);
@@ -925,7 +925,7 @@ static pcg_status bgd_solve(pcg_matrix *A, const BicgVecs &v, double tol, int64_
   auto read = [&]() -> pcg_status {
     PCG_CUDA(cudaGetLastError());
     PCG_CUDA(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
-    PCG_CUDA(cudaStreamSynchronize(st));
+    PCG_TRY(comm_wait(A->comm, st));
     return PCG_OK;
   };
   auto finish = [&](int which, int rmode, int count) -> pcg_status {
@@ -1008,7 +1008,7 @@ static pcg_status bicg_setup(pcg_matrix *A, int bs, cudaStream_t st) {
     count_launch();
     int h = 0;
     PCG_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    PCG_CUDA(cudaStreamSynchronize(st));
+    PCG_TRY(comm_wait(A->comm, st));
     cudaFree(err);
     if (h) return fail(PCG_ERR_ZERO_DIAGONAL, "pcg_bicgstab: a Block-Jacobi diagonal block is singular");
     w.bminv_bs = bs;
@@ -1104,7 +1104,7 @@ static pcg_status bicg_impl(pcg_matrix *A, const double *b, double *x, double to
   } else {
     PCG_CUDA(cudaMemcpyAsync(x, v.x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   }
-  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_TRY(comm_wait(A->comm, st));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
@@ -1144,6 +1144,7 @@ using namespace pcgb;
 
 extern "C" pcg_status pcg_bicgstab(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
                                    int32_t block_size, void *stream, pcg_info *info) {
+  pcgb::NvtxRange nvtx_("pcg:pcg_bicgstab");
   if (!A || ((!b || !x) && A->n > 0)) return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab: null argument");
   if (!(tol > 0.0) || max_iter < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab: tol > 0 and max_iter >= 1");
   if (block_size != 1 && block_size != 2 && block_size != 4 && block_size != 8)

@@ -806,6 +806,7 @@ using namespace pcgb;
 
 extern "C" pcg_status pcg_solve_block(pcg_matrix_t A, int32_t k, const double *B, int64_t ldb, double *X, int64_t ldx,
                                       double tol, int64_t max_iter, void *stream, pcg_info *infos) {
+  pcgb::NvtxRange nvtx_("pcg:pcg_solve_block");
   if (!A || !B || !X) return fail(PCG_ERR_INVALID_ARG, "pcg_solve_block: null argument");
   if (k < 1 || k > BK) return fail(PCG_ERR_INVALID_ARG, "pcg_solve_block: 1 <= k <= 32");
   if (ldb < A->n || ldx < A->n) return fail(PCG_ERR_INVALID_ARG, "pcg_solve_block: ld < n");

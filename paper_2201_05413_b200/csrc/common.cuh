@@ -8,9 +8,21 @@
 #include <mutex>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "pcg.h"
 
 namespace pcgb {
+
+// NVTX phase ranges (SURVEY §5 tracing): visible in Nsight Systems / ncu --nvtx; the
+// header-only NVTX3 calls are no-ops unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 
 // ------------------------------------------------------------------ errors
 void set_error(const std::string &msg);

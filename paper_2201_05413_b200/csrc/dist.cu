@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "matrix.cuh"
@@ -68,6 +70,49 @@ __global__ void to_local_rows_kernel(int64_t m, const int64_t *__restrict__ g, i
     out[s] = (int)(g[s] - r0);
 }
 
+// ---------------------------------------------------------------- failure detection
+// A collective whose peer died, hung or failed never completes, and a plain
+// cudaStreamSynchronize would block every surviving rank forever.  Every host wait of
+// the distributed paths therefore polls an event on the stream and, between polls,
+// ncclCommGetAsyncError; an asynchronous NCCL error or `timeout_s` without completion
+// aborts the communicator (ncclCommAbort unblocks the NCCL kernels queued on this
+// rank) and returns PCG_ERR_NCCL.  Every rank runs the same rule, so when one rank
+// fails the others fail too, within their timeout, instead of hanging.  The handle's
+// communicator is unusable afterwards (aborted: every later call returns PCG_ERR_NCCL).
+static pcg_status abort_comm(pcg_comm *C, const std::string &why) {
+  if (C->nccl) ncclCommAbort(C->nccl);
+  C->nccl = nullptr;
+  C->aborted = true;
+  return fail(PCG_ERR_NCCL, "NCCL communicator aborted: " + why);
+}
+
+pcg_status comm_wait(pcg_comm *C, cudaStream_t st) {
+  if (C && C->aborted) return fail(PCG_ERR_NCCL, "NCCL communicator was aborted");
+  if (!C || C->use_ops || !C->nccl) {
+    PCG_CUDA(cudaStreamSynchronize(st));
+    return PCG_OK;
+  }
+  NvtxRange r_("pcg:comm_wait");
+  if (!C->wait_ev) PCG_CUDA(cudaEventCreateWithFlags(&C->wait_ev, cudaEventDisableTiming));
+  PCG_CUDA(cudaEventRecord(C->wait_ev, st));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int poll = 0;; poll++) {
+    const cudaError_t q = cudaEventQuery(C->wait_ev);
+    if (q == cudaSuccess) return PCG_OK;
+    if (q != cudaErrorNotReady) {
+      cudaGetLastError();
+      return fail(PCG_ERR_CUDA, std::string("comm_wait: ") + cudaGetErrorString(q));
+    }
+    ncclResult_t ae = ncclSuccess;
+    if (ncclCommGetAsyncError(C->nccl, &ae) != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress))
+      return abort_comm(C, std::string("asynchronous error: ") + ncclGetErrorString(ae));
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (dt > C->timeout_s)
+      return abort_comm(C, "no progress for " + std::to_string(dt) + " s (PCG_COMM_TIMEOUT_S)");
+    if (poll > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
 // ---------------------------------------------------------------- communicator backends
 // NCCL (the product path, stream-ordered and graph-capturable) or caller-supplied
 // host callbacks (pcg_comm_init_ops: device data staged through host memory).
@@ -78,7 +123,12 @@ bool comm_uses_graphs(const pcg_comm *c) { return c && !c->use_ops; }
     if ((call) != 0) return ::pcgb::fail(PCG_ERR_NCCL, std::string(what) + ": host communicator callback failed"); \
   } while (0)
 
+static pcg_status comm_alive(pcg_comm *C) {
+  return C->aborted ? fail(PCG_ERR_NCCL, "NCCL communicator was aborted") : PCG_OK;
+}
+
 static pcg_status comm_allreduce_f64(pcg_comm *C, double *dbuf, int count, cudaStream_t st) {
+  PCG_TRY(comm_alive(C));
   // a 1-rank NCCL communicator still issues the (trivial) collective: it keeps the
   // captured-graph + NCCL path testable on one GPU
   if (count == 0 || (C->use_ops && C->size == 1)) return PCG_OK;
@@ -96,6 +146,7 @@ static pcg_status comm_allreduce_f64(pcg_comm *C, double *dbuf, int count, cudaS
 }
 
 static pcg_status comm_allreduce_max_i32(pcg_comm *C, int *dbuf, int count, cudaStream_t st) {
+  PCG_TRY(comm_alive(C));
   if (C->size == 1 || count == 0) return PCG_OK;
   if (!C->use_ops) {
     PCG_NCCL(ncclAllReduce(dbuf, dbuf, (size_t)count, ncclInt32, ncclMax, C->nccl, st));
@@ -112,6 +163,7 @@ static pcg_status comm_allreduce_max_i32(pcg_comm *C, int *dbuf, int count, cuda
 
 // all[r*count + i] = rank r's mine[i]; mine is C->rank's slot of all (device)
 static pcg_status comm_allgather_i64(pcg_comm *C, int64_t *dall, int count, cudaStream_t st) {
+  PCG_TRY(comm_alive(C));
   if (C->size == 1) return PCG_OK;
   if (!C->use_ops) {
     PCG_NCCL(ncclAllGather(dall + (size_t)count * C->rank, dall, (size_t)count, ncclInt64, C->nccl, st));
@@ -139,6 +191,7 @@ struct Xfer {
 static pcg_status comm_exchange(pcg_comm *C, const std::vector<Xfer> &xs, ncclDataType_t ty, size_t esize,
                                 cudaStream_t st) {
   if (xs.empty()) return PCG_OK;
+  PCG_TRY(comm_alive(C));
   if (!C->use_ops) {
     PCG_NCCL(ncclGroupStart());
     for (const Xfer &x : xs) {
@@ -175,6 +228,7 @@ static pcg_status comm_exchange(pcg_comm *C, const std::vector<Xfer> &xs, ncclDa
 
 pcg_status halo_exchange(pcg_matrix *A, double *vec, int width, cudaStream_t st) {
   (void)width;
+  NvtxRange r_("pcg:halo_exchange");
   if (!A->comm || A->halo.nbr.empty()) return PCG_OK;
   HaloPlan &hp = A->halo;
   if (hp.n_send > 0) {
@@ -286,7 +340,7 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
   int64_t ends[2];
   PCG_CUDA(cudaMemcpyAsync(&ends[0], drp, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   PCG_CUDA(cudaMemcpyAsync(&ends[1], drp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_TRY(comm_wait(C, st));
   if (ends[0] != 0 || ends[1] != nnz)
     return fail(PCG_ERR_DIMENSION_MISMATCH, "csr_create_dist: row_ptr_local[0] must be 0 and [n] = nnz_local");
   // ---- ghost list: sorted unique remote columns (device mark + compaction)
@@ -307,7 +361,7 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
     PCG_CUDA(cudaMalloc(&tbuf, tb));
     cub::DeviceSelect::Flagged(tbuf, tb, it, flag, ghost, d_cnt, n_global, st);
     PCG_CUDA(cudaMemcpyAsync(&A->n_ghost, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    PCG_CUDA(cudaStreamSynchronize(st));
+    PCG_TRY(comm_wait(C, st));
     cudaFree(tbuf);
   }
   cudaFree(flag);
@@ -334,7 +388,7 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
   PCG_TRY(comm_allgather_i64(C, d_bounds, 2, st));
   std::vector<int64_t> hb(2 * G);
   PCG_CUDA(cudaMemcpyAsync(hb.data(), d_bounds, sizeof(int64_t) * 2 * G, cudaMemcpyDeviceToHost, st));
-  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_TRY(comm_wait(C, st));
   cudaFree(d_bounds);
   for (int g = 0; g < G; g++)
     if (g > 0 && hb[2 * g] != hb[2 * g - 1])
@@ -351,7 +405,7 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
   PCG_TRY(comm_allgather_i64(C, d_M, G, st));
   std::vector<int64_t> M((size_t)G * G);
   PCG_CUDA(cudaMemcpyAsync(M.data(), d_M, sizeof(int64_t) * G * G, cudaMemcpyDeviceToHost, st));
-  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_TRY(comm_wait(C, st));
   cudaFree(d_M);
   HaloPlan &hp = A->halo;
   int64_t send_total = 0;
@@ -385,7 +439,7 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
         send_total, d_send_g, r0, hp.d_send_idx);
     count_launch();
   }
-  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_TRY(comm_wait(C, st));
   cudaFree(d_recv_idx);
   cudaFree(d_send_g);
   // ---- local matrix: n rows, n + n_ghost columns, diagonal at local i
@@ -405,8 +459,9 @@ static pcg_status create_dist_impl(pcg_comm *C, int64_t n_global, int64_t r0, in
       (void)comm_allreduce_max_i32(C, d_s, 1, st);
       int all = 0;
       cudaMemcpyAsync(&all, d_s, sizeof(int), cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
+      const pcg_status ws = comm_wait(C, st);
       cudaFree(d_s);
+      if (ws != PCG_OK) all = (int)ws;
       if (s == PCG_OK && all != PCG_OK) s = fail((pcg_status)all, "csr_create_dist: another rank failed validation");
     }
   }
@@ -479,6 +534,7 @@ extern "C" pcg_status pcg_comm_init(int32_t rank, int32_t size, const void *id12
   c->size = size;
   ncclUniqueId id;
   memcpy(&id, id128, sizeof(id));
+  if (const char *e = getenv("PCG_COMM_TIMEOUT_S")) c->timeout_s = atof(e) > 0 ? atof(e) : c->timeout_s;
   ncclResult_t r = ncclCommInitRank(&c->nccl, size, id, rank);
   if (r != ncclSuccess) {
     delete c;
@@ -504,7 +560,24 @@ extern "C" pcg_status pcg_comm_init_ops(int32_t rank, int32_t size, const pcg_co
 extern "C" pcg_status pcg_comm_destroy(pcg_comm_t c) {
   if (!c) return PCG_OK;
   if (c->nccl) ncclCommDestroy(c->nccl);
+  if (c->wait_ev) cudaEventDestroy(c->wait_ev);
   delete c;
+  return PCG_OK;
+}
+
+extern "C" pcg_status pcg_comm_abort(pcg_comm_t c) {
+  if (!c) return fail(PCG_ERR_INVALID_ARG, "pcg_comm_abort: null communicator");
+  if (c->use_ops) {
+    c->aborted = true;
+    return PCG_OK;
+  }
+  if (!c->aborted) (void)abort_comm(c, "pcg_comm_abort");
+  return PCG_OK;
+}
+
+extern "C" pcg_status pcg_comm_set_timeout(pcg_comm_t c, double seconds) {
+  if (!c || !(seconds > 0.0)) return fail(PCG_ERR_INVALID_ARG, "pcg_comm_set_timeout: bad argument");
+  c->timeout_s = seconds;
   return PCG_OK;
 }
 
@@ -512,6 +585,7 @@ extern "C" pcg_status csr_create_dist(pcg_comm_t comm, int64_t n_global, int64_t
                                       int64_t nnz_local, const int64_t *row_ptr_local,
                                       const int64_t *col_idx_global, const double *val, int flags, void *stream,
                                       pcg_matrix_t *out) {
+  pcgb::NvtxRange nvtx_("pcg:csr_create_dist");
   if (!comm || !out || !row_ptr_local || (nnz_local > 0 && (!col_idx_global || !val)))
     return fail(PCG_ERR_INVALID_ARG, "csr_create_dist: null argument");
   *out = nullptr;

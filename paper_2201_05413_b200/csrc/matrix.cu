@@ -632,6 +632,7 @@ using namespace pcgb;
 
 extern "C" pcg_status csr_create(int64_t n, int64_t nnz, const int64_t *row_ptr, const int64_t *col_idx,
                                  const double *val, int flags, void *stream, pcg_matrix_t *out) {
+  pcgb::NvtxRange nvtx_("pcg:csr_create");
   if (!out) return fail(PCG_ERR_INVALID_ARG, "csr_create: out is null");
   *out = nullptr;
   if (n < 0 || nnz < 0) return fail(PCG_ERR_INVALID_ARG, "csr_create: n and nnz must be >= 0");

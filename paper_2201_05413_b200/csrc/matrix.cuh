@@ -12,9 +12,18 @@ struct pcg_comm {
   cudaStream_t comm_stream = nullptr;
   bool use_ops = false;        // host-callback backend (pcg_comm_init_ops)
   pcg_comm_ops ops{};
+  // failure detection: waits poll ncclCommGetAsyncError and give up after
+  // timeout_s (PCG_COMM_TIMEOUT_S, default 300) with ncclCommAbort -> PCG_ERR_NCCL
+  double timeout_s = 300.0;
+  bool aborted = false;
+  cudaEvent_t wait_ev = nullptr;
 };
 
 namespace pcgb {
+
+// Wait for the work queued on `st` (distributed handles: with NCCL failure detection
+// and the communicator's timeout; see dist.cu comm_wait).
+pcg_status comm_wait(pcg_comm *C, cudaStream_t st);
 
 // Halo plan for a distributed handle: this rank's rows are
 // [row_begin,row_end); local column ids: owned j -> j-row_begin, ghosts -> n+g.

@@ -884,6 +884,7 @@ extern "C" pcg_status pcg_profile_multi(pcg_matrix_t A, int32_t k, const double 
 
 extern "C" pcg_status pcg_solve_multi(pcg_matrix_t A, int32_t k, const double *B, int64_t ldb, double *X,
                                       int64_t ldx, double tol, int64_t max_iter, void *stream, pcg_info *infos) {
+  pcgb::NvtxRange nvtx_("pcg:pcg_solve_multi");
   if (!A || !B || !X) return fail(PCG_ERR_INVALID_ARG, "pcg_solve_multi: null argument");
   if (k < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_solve_multi: k must be >= 1");
   if (ldb < A->n || ldx < A->n) return fail(PCG_ERR_INVALID_ARG, "pcg_solve_multi: ld < n");

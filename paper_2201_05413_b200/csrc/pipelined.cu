@@ -518,7 +518,7 @@ static pcg_status pd_solve(pcg_matrix *A, const PipeVecs &v, double tol, int64_t
   auto read = [&]() -> pcg_status {
     PCG_CUDA(cudaGetLastError());
     PCG_CUDA(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
-    PCG_CUDA(cudaStreamSynchronize(st));
+    PCG_TRY(comm_wait(A->comm, st));
     return PCG_OK;
   };
   auto residual = [&](int mode) -> pcg_status {  // r = b - A x (+ ||b||^2), allreduced, start / restart
@@ -665,7 +665,7 @@ static pcg_status pipe_impl(pcg_matrix *A, const double *b, double *x, double to
     PCG_TRY(pd_solve(A, v, tol, max_iter, st, &hs));
     PCG_CUDA(cudaEventRecord(f1, st));
     PCG_CUDA(cudaMemcpyAsync(x, v.x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-    PCG_CUDA(cudaStreamSynchronize(st));
+    PCG_TRY(comm_wait(A->comm, st));
     float fms = 0;
     cudaEventElapsedTime(&fms, f0, f1);
     cudaEventDestroy(f0);
@@ -703,7 +703,7 @@ static pcg_status pipe_impl(pcg_matrix *A, const double *b, double *x, double to
     PCG_CUDA(cudaMemcpyAsync(x, v.x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   }
   PCG_CUDA(cudaMemcpyAsync(&hs, dst, sizeof(hs), cudaMemcpyDeviceToHost, st));
-  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_TRY(comm_wait(A->comm, st));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
@@ -717,6 +717,7 @@ using namespace pcgb;
 
 extern "C" pcg_status pcg_solve_pipelined(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
                                           void *stream, pcg_info *info) {
+  pcgb::NvtxRange nvtx_("pcg:pcg_solve_pipelined");
   if (!A || ((!b || !x) && A->n > 0)) return fail(PCG_ERR_INVALID_ARG, "pcg_solve_pipelined: null argument");
   if (!(tol > 0.0) || max_iter < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_solve_pipelined: tol > 0 and max_iter >= 1");
   if (A->n == 0) {

@@ -726,8 +726,12 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
   PCG_CUDA(cudaEventCreate(&e0));
   PCG_CUDA(cudaEventCreate(&e1));
   PCG_CUDA(cudaEventRecord(e0, st));
-  PCG_TRY(launch_resid(A, db, MODE_INIT, st));
+  {
+    NvtxRange r_("pcg:init");
+    PCG_TRY(launch_resid(A, db, MODE_INIT, st));
+  }
   for (int round = 0;; round++) {
+    NvtxRange r_("pcg:iterate+exit_check");
     if (persist) {
       PCG_TRY(persist_launch(A, vecs_of(A), st));
     } else if (w.graph_kind == 1) {
@@ -735,7 +739,7 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
     } else {
       for (;;) {  // unrolled chunks, host-polled
         PCG_CUDA(cudaMemcpyAsync(h, w.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
-        PCG_CUDA(cudaStreamSynchronize(st));
+        PCG_TRY(comm_wait(A->comm, st));
         if (h->done != DONE_RUNNING) break;
         if (w.graph_kind == 2) {
           PCG_CUDA(cudaGraphLaunch(w.loop_exec, st));
@@ -752,7 +756,7 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
     count_launch(2);
     PCG_TRY(launch_resid(A, db, MODE_EXIT, st));
     PCG_CUDA(cudaMemcpyAsync(h, w.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
-    PCG_CUDA(cudaStreamSynchronize(st));
+    PCG_TRY(comm_wait(A->comm, st));
     if (h->done != DONE_RUNNING) break;  // else: residual replacement, run the loop again
   }
   PCG_CUDA(cudaEventRecord(e1, st));
@@ -767,7 +771,7 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
   } else {
     PCG_CUDA(cudaMemcpyAsync(x, w.x, sizeof(double) * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   }
-  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_TRY(comm_wait(A->comm, st));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
@@ -800,6 +804,7 @@ using namespace pcgb;
 
 extern "C" pcg_status pcg_solve(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
                                 void *stream, pcg_info *info) {
+  pcgb::NvtxRange nvtx_("pcg:pcg_solve");
   if (!A || ((!b || !x) && A->n > 0)) return fail(PCG_ERR_INVALID_ARG, "pcg_solve: null argument");
   if (!(tol > 0.0)) return fail(PCG_ERR_INVALID_ARG, "pcg_solve: tol must be > 0");
   if (max_iter < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_solve: max_iter must be >= 1");
@@ -849,7 +854,7 @@ extern "C" pcg_status pcg_spmv(pcg_matrix_t A, const double *x, double *y, void 
   double *dy = yd ? y : A->work.w;
   PCG_TRY(launch_spmv(A, dx, dy, st));
   if (!yd) PCG_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * A->n, cudaMemcpyDeviceToHost, st));
-  PCG_CUDA(cudaStreamSynchronize(st));
+  PCG_TRY(comm_wait(A->comm, st));
   return PCG_OK;
 }
 

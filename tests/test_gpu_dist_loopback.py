@@ -310,3 +310,43 @@ def test_distributed_bicgstab_on_one_gpu(world, N):
     i = np.arange(N)
     X, Y = np.tile(i, N * N) / (N - 1), np.tile(np.repeat(i, N), N) / (N - 1)
     assert np.max(np.abs(x - (X * X - Y * Y))) <= 1e-9
+
+
+def test_nccl_failure_detection_aborts_instead_of_blocking():
+    """SURVEY §5 failure detection: every host wait of a distributed call polls the
+    queued work and ncclCommGetAsyncError under the communicator's timeout.  With a
+    timeout no real wait can meet, the solve must return PCG_ERR_NCCL (communicator
+    aborted) instead of blocking, later calls must keep failing with PCG_ERR_NCCL, and
+    the handles must still be destroyable.  A fresh communicator then solves normally."""
+    import torch
+    import torch.distributed as dist
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_05413_b200 as pcg
+    from paper_2201_05413_b200._lib import STATUS
+    nccl_err = STATUS.index("PCG_ERR_NCCL")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        P = O.build_problem("C2", c=96, k=1)
+        A, b = P["A"], P["B"][:, 0]
+        dev = [torch.as_tensor(a).cuda() for a in (A.row_ptr, A.col, A.val)]
+        comm = pcg.Comm.from_process_group()
+        M = pcg.Matrix.from_csr_dist(comm, A.n, 0, A.n, *dev)
+        comm.set_timeout(1e-9)
+        for _ in range(2):
+            with pytest.raises(pcg.PcgError) as e:
+                M.solve(torch.as_tensor(b).cuda(), tol=1e-10)
+            assert e.value.status == nccl_err, e.value
+        M.close()
+        comm.close()
+        comm = pcg.Comm.from_process_group()
+        M = pcg.Matrix.from_csr_dist(comm, A.n, 0, A.n, *dev)
+        x, info = M.solve(torch.as_tensor(b).cuda(), tol=1e-10)
+        r = O.pcg(A, b, tol=1e-10)
+        assert info["status"] == 0
+        assert np.linalg.norm(x.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-9
+        M.close()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
