@@ -445,6 +445,12 @@ def main():
         ms, infos, launches, cs, x = timed(True)
         remeasured = True
     iters = max(i["iterations"] for i in infos[-1])  # block iterations (max over columns)
+    rank_iters = None
+    if world > 1:  # every rank must report the same count (the recurrence scalars are global)
+        t = torch.tensor([float(iters)], dtype=torch.float64, device="cpu" if cb else "cuda")
+        gathered = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(gathered, t)
+        rank_iters = [int(g.item()) for g in gathered]
     ms_e2e, infos_e2e, _, _, _ = timed(False)
 
     # ---- roofline of the dominant kernel (K1) + standalone SpMV bandwidth
@@ -592,7 +598,8 @@ def main():
                                    "block": "block cg, jacobi (N3)"}[args.solver],
                            **({"drop_zeros": True, "nnz_given": nnz_given} if args.drop_zeros else {}),
                            **({"relabel_seed": args.relabel} if args.relabel is not None else {}),
-                           **({"reorder": args.reorder, "n_ghost": stats["n_ghost"]} if reorder else {})),
+                           **({"reorder": args.reorder, "n_ghost": stats["n_ghost"]} if reorder else {}),
+                           **({"iterations_per_rank": rank_iters} if rank_iters else {})),
             "throughput": {"cg_iterations_per_s": iters / (ms / 1e3),
                            "effective_GBps": iter_bytes(n, nnz, kcols) * iters / (ms / 1e3) / 1e9,
                            "spmv_GBps": spmv_gbs, "spmv_frac_of_hbm": spmv_gbs / hbm if spmv_gbs else None},

@@ -114,6 +114,9 @@ typedef struct {
   int32_t sigma;             /* sorting window of SELL-C-sigma (0: natural row order) */
   int32_t reorder;           /* 1: the device system is RCM-reordered (PCG_REORDER_RCM) */
   int64_t overlap_rows;      /* distributed: rows whose SpMV overlaps the halo exchange (0: off) */
+  int64_t d16_slices;        /* SELL slices whose column ids are stored as 16-bit deltas from the row
+                                (10.125 instead of 12 bytes per entry; 0: not built, or environment
+                                PCG_NO_D16) — same ids, so results are bitwise those of the int32 form */
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */

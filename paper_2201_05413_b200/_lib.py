@@ -45,7 +45,7 @@ class MatrixStats(C.Structure):
                 ("row_end", C.c_int64), ("n_global", C.c_int64), ("spmv_us_tma", C.c_double),
                 ("stage_entries", C.c_int64), ("stages", C.c_int32), ("schedule", C.c_int32),
                 ("spmv_us_sigma", C.c_double), ("sigma", C.c_int32), ("reorder", C.c_int32),
-                ("overlap_rows", C.c_int64)]
+                ("overlap_rows", C.c_int64), ("d16_slices", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -109,7 +109,15 @@ struct SellView {
   int64_t stage_entries;   // ... and the largest tile (8 slices) in entries
   const int *lead;         // per tile: max column referenced by tiles 0..t (prefix max)
   int zero;                // always 0 at run time; opaque to the compiler (see cols_ready)
+  // 16-bit delta column ids (null: not built).  Entry e of slice s at position t:
+  // col = row + cbase[e >> 5] + dcol[e]; cbase has one value per (slice, t) row of 32
+  // entries; a slice whose columns do not fit holds CB_INT32 at cbase[slice_ptr[s] >> 5]
+  // and is read through `col`.  10.125 instead of 12 bytes per stored entry.
+  const int16_t *dcol;
+  const int *cbase;
+  int64_t row0;  // absolute row of the view's slice 0 (views over a row range; decoding)
 };
+constexpr int CB_INT32 = (int)0x80000000;
 
 // internal format code of the TMA-staged SELL kernels (reported as PCG_FORMAT_SELL_TMA)
 constexpr int FMT_SELL_TMA = 3;
@@ -193,6 +201,11 @@ __device__ __forceinline__ double ld_stream(const double *p) {
 __device__ __forceinline__ int ld_stream(const int *p) {
   int v;
   asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_stream(const int16_t *p) {  // sign-extended to 32 bits
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s16 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 

@@ -6,6 +6,7 @@
 // within a row) plus finiteness and the Jacobi preconditioner's need
 // for a positive diagonal.  All checks run on the device, one
 // thread per row; the first offending row is reported.
+#include <climits>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -227,7 +228,95 @@ pcg_status build_sell(pcg_matrix *A, cudaStream_t st) {
   return PCG_OK;
 }
 
+// 16-bit delta column ids (common.cuh SellView::dcol), one warp per slice.  Per
+// entry row t of the slice, the offsets col - row of the real entries (t < row
+// length) must span <= 65535: cbase = min offset + 32768, delta = offset - cbase.
+// Padding entries (a = 0) keep a valid column: delta = -cbase (col = row) when it
+// fits, else the nearest representable one if it lies in [0, n_cols).  A slice where
+// any of this fails is marked CB_INT32 and read through the int32 ids.
+__global__ void d16_build_kernel(int64_t n, int64_t n_cols, int64_t n_slices, const int *__restrict__ rp,
+                                 const int64_t *__restrict__ slice_ptr, const int *__restrict__ scol,
+                                 int16_t *__restrict__ dcol, int *__restrict__ cbase,
+                                 unsigned long long *__restrict__ n_ok) {
+  const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= n_slices) return;
+  const int64_t row = s * 32 + lane;
+  const int64_t base = slice_ptr[s];
+  const int len = (int)((slice_ptr[s + 1] - base) >> 5);
+  if (len == 0) return;
+  const int rl = row < n ? rp[row + 1] - rp[row] : 0;
+  bool ok = true;
+  for (int t = 0; t < len; t++) {
+    const int64_t e = base + (int64_t)t * 32 + lane;
+    const bool real = t < rl;
+    const long long off = (long long)scol[e] - row;
+    long long lo = real ? off : LLONG_MAX, hi = real ? off : LLONG_MIN;
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, (long long)__shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, (long long)__shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    long long b = 0;
+    if (lo != LLONG_MAX) {
+      if (hi - lo > 65535) ok = false;
+      b = lo + 32768;
+    }
+    long long d;
+    if (real) {
+      d = off - b;
+    } else {
+      d = -b;  // aim at col = row
+      if (d < -32768) d = -32768;
+      if (d > 32767) d = 32767;
+      const long long c = row + b + d;
+      if (c < 0 || c >= n_cols) ok = false;
+    }
+    if (d < -32768 || d > 32767) ok = false;
+    dcol[e] = (int16_t)(ok ? d : 0);
+    if (lane == 0) cbase[e >> 5] = (int)b;
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  if (lane == 0) {
+    if (ok) atomicAdd(n_ok, 1ull);
+    else cbase[base >> 5] = CB_INT32;
+  }
+}
+
+pcg_status build_d16(pcg_matrix *A, cudaStream_t st) {
+  if (A->d_sdcol || !A->d_slice_ptr || A->n_slices == 0 || getenv("PCG_NO_D16")) return PCG_OK;
+  PCG_CUDA(cudaMalloc(&A->d_sdcol, sizeof(int16_t) * std::max<int64_t>(A->sell_entries, 1)));
+  PCG_CUDA(cudaMalloc(&A->d_scbase, sizeof(int) * std::max<int64_t>(A->sell_entries / 32, 1)));
+  unsigned long long *d_ok;
+  PCG_CUDA(cudaMalloc(&d_ok, sizeof(unsigned long long)));
+  PCG_CUDA(cudaMemsetAsync(d_ok, 0, sizeof(unsigned long long), st));
+  d16_build_kernel<<<(unsigned)((A->n_slices * 32 + 255) / 256), 256, 0, st>>>(
+      A->n, A->n + A->n_ghost, A->n_slices, A->d_row_ptr, A->d_slice_ptr, A->d_scol, A->d_sdcol, A->d_scbase, d_ok);
+  count_launch();
+  unsigned long long ok = 0;
+  PCG_CUDA(cudaMemcpyAsync(&ok, d_ok, sizeof(ok), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_ok);
+  A->d16_slices = (int64_t)ok;
+  if (ok == 0) {  // nothing compresses: keep the int32 form only
+    cudaFree(A->d_sdcol);
+    cudaFree(A->d_scbase);
+    A->d_sdcol = nullptr;
+    A->d_scbase = nullptr;
+  } else {
+    A->device_bytes += (double)A->sell_entries * 2 + (double)(A->sell_entries / 32) * 4;
+  }
+  return PCG_OK;
+}
+
 void free_sell(pcg_matrix *A) {
+  if (A->d_sdcol) {
+    cudaFree(A->d_sdcol);
+    cudaFree(A->d_scbase);
+    A->device_bytes -= (double)A->sell_entries * 2 + (double)(A->sell_entries / 32) * 4;
+    A->d_sdcol = nullptr;
+    A->d_scbase = nullptr;
+    A->d16_slices = 0;
+  }
   for (void *p : {(void *)A->d_slice_ptr, (void *)A->d_scol, (void *)A->d_sval})
     if (p) cudaFree(p);
   if (A->d_slice_ptr) A->device_bytes -= (double)(A->n_slices + 1) * 8 + (double)A->sell_entries * 12;
@@ -521,6 +610,7 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
   configure(best_fmt);
+  if (A->format == PCG_FORMAT_SELL) PCG_TRY(build_d16(A, st));
   {
     const char *sch = getenv("PCG_SCHEDULE");
     A->schedule = (sch && atoi(sch) == 2) ? 2 : 3;
@@ -695,5 +785,6 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->sigma = A->sigma;
   o->reorder = A->reorder;
   o->overlap_rows = A->ov ? A->ov_ib - A->ov_ia : 0;
+  o->d16_slices = A->d16_slices;
   return PCG_OK;
 }

@@ -146,7 +146,13 @@ struct pcg_matrix {
   int64_t ov_ia = 0, ov_ib = 0;
   cudaStream_t ov_side = nullptr;
   cudaEvent_t ov_fork = nullptr, ov_join = nullptr;
-  pcgb::SellView sell() const { return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0}; }
+  // 16-bit delta column ids of the SELL entries (common.cuh SellView::dcol)
+  int16_t *d_sdcol = nullptr;
+  int *d_scbase = nullptr;
+  int64_t d16_slices = 0;
+  pcgb::SellView sell() const {
+    return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0, d_sdcol, d_scbase, 0};
+  }
 };
 
 namespace pcgb {

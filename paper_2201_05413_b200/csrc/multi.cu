@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
     const bool ok = row < S.n;
     const double *vp = S.val + base + lane;
     const int *cp = S.col + base + lane;
+    const int cb0 = sell_cb0(S, base, len);
     // epilogue of column c for this slice (row sum -> output + reduction values)
     auto finish_col = [&](int c, double sum) {
       double r[NV];
@@ -301,11 +302,9 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
 #pragma unroll
       for (int u = 0; u < 8; u++) {
         a[u] = 0.0;
-        if (u < len) {
-          a[u] = ld_stream(vp + (size_t)u * 32);
-          j[u] = ld_stream(cp + (size_t)u * 32);
-        }
+        if (u < len) a[u] = ld_stream(vp + (size_t)u * 32);
       }
+      sell_cols<8>(S, base, lane, (int)(S.row0 + row), cb0, 0, len, j);
       cols_ready(j, S.zero);
       if (pf) {  // first touch of a gathered line is (mostly) its largest column: start every
                  // column's fetch now so only the first gather round waits on HBM (padding

@@ -26,6 +26,29 @@ __device__ __forceinline__ void cols_ready(int (&j)[8], int zero) {
 // or 128-B (col) coalesced transaction.  Loads are issued 8 entries at a time
 // before any gather so each thread keeps 16 independent loads in flight.
 // gather(j) -> value multiplied by a_ij;  epi(row, sum) for rows < n.
+// Column ids of a slice's entries t0 .. t0+CH-1 (those < len): from the int32 array, or
+// (cb0 != CB_INT32) decoded from the 16-bit deltas, col = row + cbase + delta.  Both
+// forms give the same ids, so every sum is bitwise the same in either form.
+template <int CH>
+__device__ __forceinline__ void sell_cols(const SellView &A, int64_t base, int lane, int row, int cb0, int t0, int len,
+                                          int (&j)[8]) {
+  if (cb0 != CB_INT32) {
+    const int16_t *dp = A.dcol + base + lane;
+    const int *cb = A.cbase + (base >> 5);
+#pragma unroll
+    for (int u = 0; u < CH; u++)
+      if (t0 + u < len) j[u] = row + ld_stream(cb + t0 + u) + ld_stream(dp + (size_t)(t0 + u) * 32);
+  } else {
+    const int *cp = A.col + base + lane;
+#pragma unroll
+    for (int u = 0; u < CH; u++)
+      if (t0 + u < len) j[u] = ld_stream(cp + (size_t)(t0 + u) * 32);
+  }
+}
+__device__ __forceinline__ int sell_cb0(const SellView &A, int64_t base, int len) {
+  return (A.dcol && len > 0) ? ld_stream(A.cbase + (base >> 5)) : CB_INT32;
+}
+
 template <class Gather, class Epi>
 __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi epi) {
   const int lane = threadIdx.x & 31;
@@ -35,18 +58,15 @@ __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi 
     const int64_t base = A.slice_ptr[s];
     const int len = (int)((A.slice_ptr[s + 1] - base) >> 5);
     const double *vp = A.val + base + lane;
-    const int *cp = A.col + base + lane;
+    const int cb0 = sell_cb0(A, base, len);
     double sum = 0.0;
     for (int t = 0; t < len; t += 8) {
       double a[8];
       int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
-        if (t + u < len) {
-          a[u] = ld_stream(vp + (size_t)(t + u) * 32);
-          j[u] = ld_stream(cp + (size_t)(t + u) * 32);
-        }
-      }
+      for (int u = 0; u < 8; u++)
+        if (t + u < len) a[u] = ld_stream(vp + (size_t)(t + u) * 32);
+      sell_cols<8>(A, base, lane, (int)(A.row0 + s * 32 + lane), cb0, t, len, j);
       cols_ready(j, A.zero);
       double g[8];
 #pragma unroll
@@ -139,18 +159,15 @@ __device__ __forceinline__ void k1_sell_rows(const SellView &A, double beta, dou
       xi = __ldcs(x + row);
     }
     const double *vp = A.val + base + lane;
-    const int *cp = A.col + base + lane;
+    const int cb0 = sell_cb0(A, base, len);
     double sum = 0.0;
     for (int t = 0; t < len; t += CH) {
       double a[CH];
       int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-      for (int u = 0; u < CH; u++) {
-        if (t + u < len) {
-          a[u] = ld_stream(vp + (size_t)(t + u) * 32);
-          j[u] = ld_stream(cp + (size_t)(t + u) * 32);
-        }
-      }
+      for (int u = 0; u < CH; u++)
+        if (t + u < len) a[u] = ld_stream(vp + (size_t)(t + u) * 32);
+      sell_cols<CH>(A, base, lane, (int)(A.row0 + row), cb0, t, len, j);
       cols_ready(j, A.zero);
       double g[CH];
 #pragma unroll

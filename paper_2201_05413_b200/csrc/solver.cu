@@ -516,6 +516,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
       CsrView Cv = A->csr();
       const int64_t s0 = R.r0 / 32, s1 = R.r1 == A->n ? A->n_slices : R.r1 / 32;
       S.slice_ptr += s0;
+      S.row0 = s0 * 32;
       S.n_slices = s1 - s0;
       S.n = R.r1 - R.r0;
       Cv.row_ptr += R.r0;

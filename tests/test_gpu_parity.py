@@ -302,3 +302,33 @@ def test_format_choice_is_deterministic(pcg, name, c):
     x1, i1 = M1.solve(_dev(b))
     x2, i2 = M2.solve(_dev(b))
     assert i1["iterations"] == i2["iterations"] and bool((x1 == x2).all())
+
+
+@pytest.mark.parametrize("name,c,fmt", [("C5", 32, "auto"), ("C4", 24, "sell"), ("C3", 40, "sigma"), ("C2", 64, "sell"),
+                                        ("C6", 16, "sell")])
+def test_d16_column_form_is_bitwise_the_int32_form(pcg, monkeypatch, name, c, fmt):
+    """The 16-bit delta column ids (pcg.h d16_slices) decode to the same ids as the
+    int32 SELL array, so SpMV, single- and multi-RHS solves are bitwise identical with
+    and without them (PCG_NO_D16=1), and match the oracle."""
+    P = O.build_problem(name, c=c, k=2 if name == "C4" else 1)
+    A = P["A"]
+    monkeypatch.delenv("PCG_NO_D16", raising=False)
+    M1 = _matrix(pcg, A, fmt)
+    monkeypatch.setenv("PCG_NO_D16", "1")
+    M0 = _matrix(pcg, A, fmt)
+    monkeypatch.delenv("PCG_NO_D16")
+    s1, s0 = M1.stats(), M0.stats()
+    assert s0["d16_slices"] == 0
+    assert s1["d16_slices"] > 0.5 * ((A.n + 31) // 32), s1
+    x = np.random.default_rng(11).standard_normal(A.n)
+    y1, y0 = M1.spmv(_dev(x)).cpu().numpy(), M0.spmv(_dev(x)).cpu().numpy()
+    assert np.array_equal(y1, y0)
+    assert np.all(np.abs(y1 - O.spmv(A, x)) <= _spmv_bound(A, x))
+    b = P["B"][:, 0]
+    x1, i1 = M1.solve(_dev(b))
+    x0, i0 = M0.solve(_dev(b))
+    assert i1["iterations"] == i0["iterations"] and bool((x1 == x0).all())
+    if P["B"].shape[1] > 1:
+        X1, _ = M1.solve_multi(_dev(P["B"]))
+        X0, _ = M0.solve_multi(_dev(P["B"]))
+        assert bool((X1 == X0).all())
