@@ -118,6 +118,10 @@ def lib():
         L.orc_fd_cube.argtypes = [C.c_int64, C.c_int, P(_Csr), C.c_void_p]
         L.orc_bicgstab.argtypes = [P(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_int64,
                                    P(C.c_int64), P(C.c_double), P(C.c_double)]
+        L.orc_bicgstab_pc.argtypes = [P(_Csr), C.c_void_p, C.c_void_p, C.c_double, C.c_int64, C.c_int, C.c_int64,
+                                      P(C.c_int64), P(C.c_double), P(C.c_double)]
+        L.orc_ilu0_factor.argtypes = [P(_Csr), C.c_int64, C.c_void_p]
+        L.orc_ilu0_apply.argtypes = [P(_Csr), C.c_int64, C.c_void_p, C.c_void_p]
         L.orc_halo.restype = C.c_int64
         L.orc_coo_to_csr.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -362,6 +366,41 @@ def bicgstab(A: Csr, b, x0=None, tol=1e-10, max_iter=50000, block=1) -> PcgResul
     st = lib().orc_bicgstab(C.byref(Ac), _ptr(b), _ptr(x), tol, max_iter, block, C.byref(it), C.byref(rr),
                             C.byref(rt))
     return PcgResult(x=x, iterations=it.value, relres_rec=rr.value, relres_true=rt.value, status=st)
+
+
+PC_BJ_LU, PC_BJ_ILU0 = 0, 1
+
+
+def bicgstab_ilu(A: Csr, b, x0=None, tol=1e-10, max_iter=50000, block=None) -> PcgResult:
+    """BiCGSTAB with Block-Jacobi ILU(0) blocks of `block` rows (default: one block, n rows),
+    oracle.h orc_bicgstab_pc / DESIGN.md reading R6."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(A.n) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+    it, rr, rt = C.c_int64(0), C.c_double(0), C.c_double(0)
+    Ac = A._c()
+    st = lib().orc_bicgstab_pc(C.byref(Ac), _ptr(b), _ptr(x), tol, max_iter, PC_BJ_ILU0, int(block or max(A.n, 1)),
+                               C.byref(it), C.byref(rr), C.byref(rt))
+    return PcgResult(x=x, iterations=it.value, relres_rec=rr.value, relres_true=rt.value, status=st)
+
+
+def ilu0_factor(A: Csr, block: int) -> np.ndarray:
+    """ILU(0) factor values of the Block-Jacobi blocks in A's pattern (oracle.h orc_ilu0_factor)."""
+    f = np.zeros(max(A.nnz, 1))
+    Ac = A._c()
+    st = lib().orc_ilu0_factor(C.byref(Ac), int(block), _ptr(f))
+    if st != OK:
+        raise RuntimeError(f"orc_ilu0_factor: {st}")
+    return f[:A.nnz]
+
+
+def ilu0_apply(A: Csr, block: int, v) -> np.ndarray:
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    y = np.zeros(A.n)
+    Ac = A._c()
+    st = lib().orc_ilu0_apply(C.byref(Ac), int(block), _ptr(v), _ptr(y))
+    if st != OK:
+        raise RuntimeError(f"orc_ilu0_apply: {st}")
+    return y
 
 
 def coo_to_csr(n_rows: int, n_cols: int, row, col, val):

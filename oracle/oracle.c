@@ -893,13 +893,90 @@ typedef struct {
   double *lu;   /* nb blocks of bs*bs, row-major, L (unit) and U packed */
   int64_t *piv; /* nb*bs row permutations */
   double *dinv; /* bs == 1 */
+  /* ILU(0) sub-solver (ilu = 1): the factor values f in A's pattern (nnz), L strictly
+   * lower with unit diagonal, U upper; entries outside the row's block are unused */
+  int ilu;
+  const orc_csr *A;
+  double *f;
 } orc_bj;
 
 static void bj_free(orc_bj *M) {
   free(M->lu);
   free(M->piv);
   free(M->dinv);
+  free(M->f);
   memset(M, 0, sizeof(*M));
+}
+
+/* Block-Jacobi with ILU(0) blocks (PETSc's default Block-Jacobi sub-solver, P:194,
+ * P:295; reading R6): blocks of bs consecutive rows [r0, r1); each block's
+ * matrix A_BB (the entries of its rows with columns in [r0, r1)) is factorised by the
+ * incomplete LU with zero fill, Saad, "Iterative Methods for Sparse Linear Systems"
+ * (2nd ed.), Algorithm 10.4 (IKJ variant), written out:
+ *   for i = r0+1 .. r1-1, for k = r0 .. i-1 with (i,k) in the pattern, ascending:
+ *       a_ik := a_ik / a_kk
+ *       for j = k+1 .. r1-1 with (i,j) in the pattern, ascending:
+ *           if (k,j) is in the pattern: a_ij := a_ij - a_ik * a_kj
+ * M_B = L U with L the unit lower triangle, U the upper triangle of the result
+ * ((L U)_ij = a_ij on the pattern: the defining property, pinned in tests).  A zero
+ * pivot a_kk is ORC_ERR_ZERO_DIAGONAL. */
+static int ilu0_setup(const orc_csr *A, int64_t bs, orc_bj *M) {
+  memset(M, 0, sizeof(*M));
+  const int64_t n = A->n;
+  M->n = n;
+  M->bs = bs;
+  M->ilu = 1;
+  M->A = A;
+  M->nb = (n + bs - 1) / bs;
+  M->f = malloc(sizeof(double) * (A->nnz > 0 ? A->nnz : 1));
+  if (!M->f) return ORC_ERR_OOM;
+  for (int64_t e = 0; e < A->nnz; e++) M->f[e] = A->val[e];
+  for (int64_t i = 0; i < n; i++) {
+    const int64_t r0 = (i / bs) * bs, r1 = (r0 + bs < n) ? r0 + bs : n;
+    if (csr_find(A, i, i) < 0) return ORC_ERR_ZERO_DIAGONAL;
+    for (int64_t kk = A->row_ptr[i]; kk < A->row_ptr[i + 1]; kk++) {
+      const int64_t k = A->col[kk];
+      if (k < r0 || k >= i) continue;
+      const double fkk = M->f[csr_find(A, k, k)];
+      if (fkk == 0.0) return ORC_ERR_ZERO_DIAGONAL;
+      M->f[kk] = M->f[kk] / fkk;
+      for (int64_t jj = kk + 1; jj < A->row_ptr[i + 1]; jj++) {
+        const int64_t j = A->col[jj];
+        if (j >= r1) break;
+        const int64_t kj = csr_find(A, k, j);
+        if (kj >= 0) M->f[jj] = M->f[jj] - M->f[kk] * M->f[kj];
+      }
+    }
+    if (M->f[csr_find(A, i, i)] == 0.0) return ORC_ERR_ZERO_DIAGONAL;
+  }
+  return ORC_OK;
+}
+
+/* y = (L U)^{-1} v block by block: forward L y' = v (unit diagonal, k ascending), then
+ * backward U y = y' (i descending; j ascending, then the division by u_ii) */
+static void ilu0_apply(const orc_bj *M, const double *v, double *y) {
+  const orc_csr *A = M->A;
+  const int64_t n = M->n, bs = M->bs;
+  for (int64_t blk = 0; blk < M->nb; blk++) {
+    const int64_t r0 = blk * bs, r1 = (r0 + bs < n) ? r0 + bs : n;
+    for (int64_t i = r0; i < r1; i++) {
+      double s = v[i];
+      for (int64_t kk = A->row_ptr[i]; kk < A->row_ptr[i + 1]; kk++) {
+        const int64_t k = A->col[kk];
+        if (k >= r0 && k < i) s = s - M->f[kk] * y[k];
+      }
+      y[i] = s;
+    }
+    for (int64_t i = r1 - 1; i >= r0; i--) {
+      double s = y[i], d = 0.0;
+      for (int64_t jj = A->row_ptr[i]; jj < A->row_ptr[i + 1]; jj++) {
+        const int64_t j = A->col[jj];
+        if (j == i) d = M->f[jj];
+        else if (j > i && j < r1) s = s - M->f[jj] * y[j];
+      }
+      y[i] = s / d;
+    }
+  }
 }
 
 static int bj_setup(const orc_csr *A, int64_t bs, orc_bj *M) {
@@ -959,6 +1036,10 @@ static int bj_setup(const orc_csr *A, int64_t bs, orc_bj *M) {
 
 /* y = M^{-1} v */
 static void bj_apply(const orc_bj *M, const double *v, double *y) {
+  if (M->ilu) {
+    ilu0_apply(M, v, y);
+    return;
+  }
   if (M->bs == 1) {
     for (int64_t i = 0; i < M->n; i++) y[i] = M->dinv[i] * v[i];
     return;
@@ -994,13 +1075,19 @@ static void bj_apply(const orc_bj *M, const double *v, double *y) {
  * point Jacobi).  DESIGN.md reading R2. */
 int orc_bicgstab(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter, int64_t bs,
                  int64_t *iters, double *relres_rec, double *relres_true) {
+  return orc_bicgstab_pc(A, b, x, tol, max_iter, ORC_PC_BJ_LU, bs, iters, relres_rec, relres_true);
+}
+
+int orc_bicgstab_pc(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter, int pc, int64_t bs,
+                    int64_t *iters, double *relres_rec, double *relres_true) {
   const int64_t n = A->n;
   *iters = 0;
   *relres_rec = 0.0;
   *relres_true = 0.0;
-  if (n < 0 || !(tol > 0.0) || max_iter < 1 || bs < 1) return ORC_ERR_INVALID_ARG;
+  if (n < 0 || !(tol > 0.0) || max_iter < 1 || bs < 1 || (pc != ORC_PC_BJ_LU && pc != ORC_PC_BJ_ILU0))
+    return ORC_ERR_INVALID_ARG;
   orc_bj M;
-  int st = bj_setup(A, bs, &M);
+  int st = pc == ORC_PC_BJ_ILU0 ? ilu0_setup(A, bs, &M) : bj_setup(A, bs, &M);
   if (st != ORC_OK) {
     bj_free(&M);
     return st;
@@ -1486,5 +1573,28 @@ int orc_block_cg(const orc_csr *A, int k, const double *B, double *X, double tol
 out:
   free(col); free(nb); free(dinv); free(R); free(Z); free(P); free(Q); free(Xm); free(T);
   free(G); free(Gam); free(Gn); free(al);
+  return st;
+}
+
+/* ------------------------------------------------------------------ */
+/* the ILU(0) Block-Jacobi factor and its application, */
+/* exposed for the pins (oracle.h)                                      */
+/* ------------------------------------------------------------------ */
+int orc_ilu0_factor(const orc_csr *A, int64_t bs, double *f) {
+  if (bs < 1) return ORC_ERR_INVALID_ARG;
+  orc_bj M;
+  int st = ilu0_setup(A, bs, &M);
+  if (st == ORC_OK)
+    for (int64_t e = 0; e < A->nnz; e++) f[e] = M.f[e];
+  bj_free(&M);
+  return st;
+}
+
+int orc_ilu0_apply(const orc_csr *A, int64_t bs, const double *v, double *y) {
+  if (bs < 1) return ORC_ERR_INVALID_ARG;
+  orc_bj M;
+  int st = ilu0_setup(A, bs, &M);
+  if (st == ORC_OK) ilu0_apply(&M, v, y);
+  bj_free(&M);
   return st;
 }

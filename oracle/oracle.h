@@ -133,6 +133,19 @@ int64_t orc_fd_identity_rows_nnz(int64_t N);
 int orc_fd_cube(int64_t N, int fkind, orc_csr *A, double *b /* N^3 */);
 int orc_bicgstab(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter, int64_t bs,
                  int64_t *iters, double *relres_rec, double *relres_true);
+/* the same BiCGSTAB with the preconditioner chosen by pc: ORC_PC_BJ_LU (Block-Jacobi,
+ * dense LU blocks of bs rows; bs = 1 point Jacobi — orc_bicgstab) or ORC_PC_BJ_ILU0
+ * (Block-Jacobi with ILU(0) blocks of bs consecutive rows, PETSc's default sub-solver,
+ * DESIGN.md reading R6; bs = n: one block, the paper's one-process run) */
+#define ORC_PC_BJ_LU 0
+#define ORC_PC_BJ_ILU0 1
+int orc_bicgstab_pc(const orc_csr *A, const double *b, double *x, double tol, int64_t max_iter, int pc, int64_t bs,
+                    int64_t *iters, double *relres_rec, double *relres_true);
+/* ILU(0) of the Block-Jacobi blocks (bs rows each), Saad Alg. 10.4: the factor values in
+ * A's pattern (f: nnz; L strictly lower with unit diagonal, U upper; entries whose column
+ * lies outside the row's block are copied unchanged); and y = M^{-1} v. */
+int orc_ilu0_factor(const orc_csr *A, int64_t bs, double *f);
+int orc_ilu0_apply(const orc_csr *A, int64_t bs, const double *v, double *y);
 
 /* SURVEY §8(f) N3 (reading R4): preconditioned pipelined CG (Ghysels &
  * Vanroose 2014, "Hiding global synchronization latency in the preconditioned
