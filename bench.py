@@ -593,6 +593,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(workload_config(args.config, c, n, nnz, world), iterations=iters,
                            format={1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[stats["format"]], setup_s=round(t_setup, 3),
+                           d16_slices=A.stats()["d16_slices"], spmm_windowed=A.stats()["spmm_windowed"],
                            relres_true=max(i["relres_true"] for i in infos[-1]), k_rhs=kcols,
                            solver={"pcg": "jacobi-pcg", "pipelined": "pipelined jacobi-pcg (N3)",
                                    "block": "block cg, jacobi (N3)"}[args.solver],

@@ -115,8 +115,12 @@ typedef struct {
   int32_t reorder;           /* 1: the device system is RCM-reordered (PCG_REORDER_RCM) */
   int64_t overlap_rows;      /* distributed: rows whose SpMV overlaps the halo exchange (0: off) */
   int64_t d16_slices;        /* SELL slices whose column ids are stored as 16-bit deltas from the row
-                                (10.125 instead of 12 bytes per entry; 0: not built, or environment
-                                PCG_NO_D16) — same ids, so results are bitwise those of the int32 form */
+                                (10.125 instead of 12 bytes per entry; opt-in, environment
+                                PCG_D16=1 at csr_create: measured no faster) — same ids, so results are
+                                bitwise those of the int32 form */
+  int32_t spmm_windowed;     /* multi-RHS SpMM plan: 1 = column windows staged by TMA (built at the
+                                first pcg_solve_multi), -1 = not applicable, 0 = not built yet */
+  int32_t pad0;
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */
@@ -199,6 +203,20 @@ pcg_status pcg_solve_block(pcg_matrix_t A, int32_t k, const double *B, int64_t l
  * so the iterates are those of the undivided system up to reduction order. */
 pcg_status pcg_bicgstab(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
                         int32_t block_size, void *stream, pcg_info *info);
+
+/* The same BiCGSTAB with Block-Jacobi ILU(0) blocks — PETSc's default Block-Jacobi
+ * sub-solver, the preconditioner of the paper's iterative runs (DESIGN.md
+ * reading R6): blocks of block_rows consecutive rows (block_rows <= 0: one block per
+ * SM, ceil(n / SMs) rows — PETSc's one block per process; block_rows >= n: one block,
+ * the paper's one-process setting); in each block the incomplete LU with zero fill
+ * (Saad, Alg. 10.4, IKJ), computed on the device at the first call (cached on the
+ * handle per block_rows), applied by level-scheduled triangular solves, one CTA per
+ * block.  Factor and application are bitwise the oracle's (orc_bicgstab_pc).
+ * One-GPU handles in the caller's numbering (CSR or natural SELL: INVALID_ARG for
+ * distributed, SELL-C-sigma or RCM handles).  Returns as pcg_bicgstab; ZERO_DIAGONAL
+ * for a zero pivot of the incomplete factorization. */
+pcg_status pcg_bicgstab_ilu(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
+                            int64_t block_rows, void *stream, pcg_info *info);
 
 /* Preconditioned pipelined CG (reading R4: Ghysels &
  * Vanroose 2014, Alg. 3) with the Jacobi preconditioner: the same problem, inputs,

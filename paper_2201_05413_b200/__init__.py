@@ -194,9 +194,15 @@ class Matrix:
         return _copy_back(x, user_out), d
 
     def bicgstab(self, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, block: int = 1, stream=None,
-                 raise_on=("error",), out=None):
+                 raise_on=("error",), out=None, precond: str = "bj"):
         """Right-preconditioned BiCGSTAB with (Block-)Jacobi (pcg_bicgstab).
-        Same conventions as solve(); block = 1 (point Jacobi), 2, 4 or 8."""
+        Same conventions as solve(); block = 1 (point Jacobi), 2, 4 or 8.  precond="ilu0":
+        Block-Jacobi with ILU(0) blocks of `block` rows (pcg_bicgstab_ilu; block <= 0: one
+        block per SM)."""
+        if precond == "ilu0":
+            return self._bicgstab_ilu(b, x0, tol, max_iter, block, stream, raise_on, out)
+        if precond != "bj":
+            raise ValueError(f"precond must be 'bj' or 'ilu0', not {precond!r}")
         torch = _torch()
         b = _as_tensor(b, torch.float64)
         if out is not None:
@@ -209,6 +215,23 @@ class Matrix:
                                 C.byref(info))
         if st not in (PCG_OK, PCG_NOT_CONVERGED) or ("not_converged" in raise_on and st == PCG_NOT_CONVERGED):
             raise PcgError(st, "pcg_bicgstab")
+        d = info.as_dict()
+        d["status_name"] = _lib.STATUS[st]
+        return _copy_back(x, user_out), d
+
+    def _bicgstab_ilu(self, b, x0, tol, max_iter, block, stream, raise_on, out):
+        torch = _torch()
+        b = _as_tensor(b, torch.float64)
+        if out is not None:
+            x = out
+        else:
+            x = torch.zeros_like(b) if x0 is None else _as_tensor(x0, torch.float64).clone()
+        b, x, user_out = _pin_host(b, x, out)
+        info = _lib.PcgInfo()
+        st = lib().pcg_bicgstab_ilu(self._h, _ptr(b), _ptr(x), float(tol), int(max_iter), int(block),
+                                    _stream_ptr(stream), C.byref(info))
+        if st not in (PCG_OK, PCG_NOT_CONVERGED) or ("not_converged" in raise_on and st == PCG_NOT_CONVERGED):
+            raise PcgError(st, "pcg_bicgstab_ilu")
         d = info.as_dict()
         d["status_name"] = _lib.STATUS[st]
         return _copy_back(x, user_out), d
@@ -466,9 +489,15 @@ def pcg_bicgstab(A: Matrix, b, x0=None, tol: float = 1e-10, max_iter: int = 5000
     return A.bicgstab(b, x0=x0, tol=tol, max_iter=max_iter, block=block_size, stream=stream)
 
 
+def pcg_bicgstab_ilu(A: Matrix, b, x0=None, tol: float = 1e-10, max_iter: int = 50000, block_rows: int = 0,
+                     stream=None):
+    """include/pcg.h pcg_bicgstab_ilu: BiCGSTAB with Block-Jacobi ILU(0) blocks of block_rows rows."""
+    return A.bicgstab(b, x0=x0, tol=tol, max_iter=max_iter, block=block_rows, stream=stream, precond="ilu0")
+
+
 pcg_partition_rows = partition_rows
 solve = pcg_solve  # SURVEY §8(b) "Python: pcg.solve(A, b, x0, tol, max_iter)"
 
 __all__ += ["csr_create", "csr_create_dist", "csr_destroy", "pcg_spmv", "pcg_solve", "pcg_solve_multi",
-            "pcg_solve_pipelined", "pcg_bicgstab", "pcg_partition_rows", "csr_rcm_order", "solve",
+            "pcg_solve_pipelined", "pcg_bicgstab", "pcg_bicgstab_ilu", "pcg_partition_rows", "csr_rcm_order", "solve",
             "pcg_solve_block"]

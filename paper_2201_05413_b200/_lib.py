@@ -45,7 +45,8 @@ class MatrixStats(C.Structure):
                 ("row_end", C.c_int64), ("n_global", C.c_int64), ("spmv_us_tma", C.c_double),
                 ("stage_entries", C.c_int64), ("stages", C.c_int32), ("schedule", C.c_int32),
                 ("spmv_us_sigma", C.c_double), ("sigma", C.c_int32), ("reorder", C.c_int32),
-                ("overlap_rows", C.c_int64), ("d16_slices", C.c_int64)]
+                ("overlap_rows", C.c_int64), ("d16_slices", C.c_int64),
+                ("spmm_windowed", C.c_int32), ("pad0", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -104,6 +105,7 @@ def lib():
         "pcg_profile_kernels": [vp, vp, i32, vp, vp, P(i32)],
         "pcg_profile_multi": [vp, i32, vp, i64, i32, vp, vp, P(i32)],
         "pcg_bicgstab": [vp, vp, vp, C.c_double, i64, i32, vp, P(PcgInfo)],
+        "pcg_bicgstab_ilu": [vp, vp, vp, C.c_double, i64, i64, vp, P(PcgInfo)],
         "pcg_solve_pipelined": [vp, vp, vp, C.c_double, i64, vp, P(PcgInfo)],
         "fd_cube_count": [i64, i64, i64, vp, P(i64), vp],
         "fd_cube_assemble": [i64, i32, i64, i64, vp, vp, vp, vp, vp],

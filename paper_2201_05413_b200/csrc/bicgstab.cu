@@ -115,6 +115,9 @@ __global__ void bj_lu_kernel(int64_t n, const int *__restrict__ rp, const int *_
   }
 }
 
+// bs code of the ILU(0) Block-Jacobi preconditioner (its block size lives in the plan)
+constexpr int BS_ILU = -1;
+
 enum { BD_RUNNING = 0, BD_CONVERGED = 1, BD_MAXIT = 2, BD_BREAKDOWN = 3, BD_ZERO_RHS = 4, BD_NONFINITE = 5 };
 
 // Block-uniform scalar state lives in shared memory (thread 0 writes after the
@@ -693,6 +696,31 @@ __global__ void __launch_bounds__(BLOCK) bg_update_kernel(int64_t n, BicgVecs v,
   if (bg_last<2>(red, part, &sc->cnt[2], sc, dist, sm, t)) bg_fin_update(sc, t, half, use_cond, h);
 }
 
+// ILU(0) Block-Jacobi (ilu.cu): P1 / P3 without the preconditioner, which runs as its
+// own level-scheduled kernel after them.  STAGE 0: p = r + beta (p - omega v);
+// STAGE 1: s = r - alpha v (into r) and the partial ||s||^2 (half-step test).
+template <int STAGE>
+__global__ void __launch_bounds__(BLOCK) bg_vec_kernel(int64_t n, BicgVecs v, BgScalars *sc, double *part,
+                                                       int use_cond, cudaGraphConditionalHandle h) {
+  __shared__ double sm[1][WARPS];
+  BG_ENTRY();
+  const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nth = (int64_t)gridDim.x * BLOCK;
+  double a0 = 0.0;
+  if (STAGE == 0) {
+    const double beta = vs->beta, omega = vs->omega;
+    for (int64_t i = tid; i < n; i += nth) v.p[i] = __fma_rn(beta, __fma_rn(-omega, v.v[i], v.p[i]), v.r[i]);
+    return;
+  }
+  const double alpha = vs->alpha;
+  for (int64_t i = tid; i < n; i += nth) {
+    const double u = __fma_rn(-alpha, v.v[i], v.r[i]);
+    v.r[i] = u;
+    a0 = __fma_rn(u, u, a0);
+  }
+  double red[1] = {a0}, t[1];
+  if (bg_last<1>(red, part, &sc->cnt[1], sc, 0, sm, t)) bg_fin_p3(sc, t);
+}
+
 // distributed handles: the finisher after the allreduce of sc->part
 enum { BF_RESID = 0, BF_AV = 1, BF_P3 = 2, BF_AT = 3, BF_UPDATE = 4, BF_FINAL = 5 };
 __global__ void bg_finish_kernel(BgScalars *sc, int which, int rmode) {
@@ -752,6 +780,22 @@ static void bg_iteration(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double
   count_launch(5);
 }
 
+template <int FMT, int L>
+static void bg_iteration_ilu(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double *part, cudaStream_t st,
+                             int use_cond, cudaGraphConditionalHandle h) {
+  const SellView S = A->sell();
+  const CsrView C = A->csr();
+  const int gs = A->grid_spmv, gv = A->grid_vec;
+  bg_vec_kernel<0><<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, use_cond, h);
+  ilu_launch(A->work.ilu, v.p, v.ph, &sc->stop, nullptr, st);
+  bg_spmv_kernel<FMT, L, SP_AV><<<gs, BLOCK, 0, st>>>(S, C, v, sc, part, 0, 0, use_cond, h);
+  bg_vec_kernel<1><<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, use_cond, h);
+  ilu_launch(A->work.ilu, v.r, v.sh, &sc->stop, &sc->half, st);
+  bg_spmv_kernel<FMT, L, SP_AT><<<gs, BLOCK, 0, st>>>(S, C, v, sc, part, 0, 0, use_cond, h);
+  bg_update_kernel<<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, 0, use_cond, h);
+  count_launch(5);
+}
+
 template <int FMT, int L, int BS>
 static void bg_resid(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double *part, int rmode, cudaStream_t st) {
   if (rmode == BR_FINAL)
@@ -779,7 +823,23 @@ static BgOps bg_ops_bs(int fmt, int lanes) {
   }
 }
 
+template <int FMT, int L>
+static BgOps bg_ops_ilu_t() {
+  return {bg_iteration_ilu<FMT, L>, bg_resid<FMT, L, 1>};
+}
+
 static BgOps bg_ops(int fmt, int lanes, int bs) {
+  if (bs == BS_ILU) {
+    if (fmt == PCG_FORMAT_SELL) return bg_ops_ilu_t<PCG_FORMAT_SELL, 1>();
+    switch (lanes) {
+      case 1: return bg_ops_ilu_t<PCG_FORMAT_CSR, 1>();
+      case 2: return bg_ops_ilu_t<PCG_FORMAT_CSR, 2>();
+      case 4: return bg_ops_ilu_t<PCG_FORMAT_CSR, 4>();
+      case 8: return bg_ops_ilu_t<PCG_FORMAT_CSR, 8>();
+      case 16: return bg_ops_ilu_t<PCG_FORMAT_CSR, 16>();
+      default: return bg_ops_ilu_t<PCG_FORMAT_CSR, 32>();
+    }
+  }
   switch (bs) {
     case 1: return bg_ops_bs<1>(fmt, lanes);
     case 2: return bg_ops_bs<2>(fmt, lanes);
@@ -797,7 +857,8 @@ static int bicg_use_graph(const pcg_matrix *) {
 
 static pcg_status bg_build(pcg_matrix *A, const BgOps &ops, const BicgVecs &v, int bs) {
   SolveWork &w = A->work;
-  if (w.bg_exec && w.bg_bs == bs) return PCG_OK;
+  const int key = bs == BS_ILU ? -(int)std::min<int64_t>(ilu_block_rows(w.ilu), 1 << 30) : bs;
+  if (w.bg_exec && w.bg_bs == key) return PCG_OK;
   if (w.bg_exec) cudaGraphExecDestroy(w.bg_exec);
   if (w.bg_graph) cudaGraphDestroy(w.bg_graph);
   w.bg_exec = nullptr;
@@ -826,7 +887,7 @@ static pcg_status bg_build(pcg_matrix *A, const BgOps &ops, const BicgVecs &v, i
   PCG_CUDA(e);
   PCG_CUDA(cudaGraphInstantiate(&w.bg_exec, g, 0));
   w.bg_graph = g;
-  w.bg_bs = bs;
+  w.bg_bs = key;
   return PCG_OK;
 }
 
@@ -974,8 +1035,18 @@ static pcg_status bgd_solve(pcg_matrix *A, const BicgVecs &v, double tol, int64_
   return PCG_OK;
 }
 
-static pcg_status bicg_setup(pcg_matrix *A, int bs, cudaStream_t st) {
+static pcg_status bicg_setup(pcg_matrix *A, int bs, int64_t ilu_rows, cudaStream_t st) {
   SolveWork &w = A->work;
+  if (bs == BS_ILU) {
+    int64_t want = ilu_rows;
+    if (want < 1) want = std::max<int64_t>(1, (A->n + num_sms(A->device) - 1) / num_sms(A->device));
+    if (want > A->n) want = A->n;
+    if (!w.ilu || ilu_block_rows(w.ilu) != want) {
+      if (w.ilu) ilu_free(w.ilu);
+      w.ilu = nullptr;
+      PCG_TRY(ilu_setup(A, want, st, &w.ilu));
+    }
+  }
   if (!w.bv) {
     const size_t nb = sizeof(double) * ((size_t)(A->n + A->n_ghost) + 64);  // ghost slots for x, p^, s^
     PCG_CUDA(cudaMalloc(&w.bv, nb * 8));  // x r rh p ph v sh t
@@ -1017,9 +1088,9 @@ static pcg_status bicg_setup(pcg_matrix *A, int bs, cudaStream_t st) {
 }
 
 static pcg_status bicg_impl(pcg_matrix *A, const double *b, double *x, double tol, int64_t max_iter, int bs,
-                            cudaStream_t st, pcg_info *info) {
+                            int64_t ilu_rows, cudaStream_t st, pcg_info *info) {
   PCG_TRY(ensure_work(A));
-  PCG_TRY(bicg_setup(A, bs, st));
+  PCG_TRY(bicg_setup(A, bs, ilu_rows, st));
   SolveWork &w = A->work;
   const int64_t n = A->n, ldv = n + A->n_ghost + 64;
   BicgVecs v;
@@ -1067,7 +1138,7 @@ static pcg_status bicg_impl(pcg_matrix *A, const double *b, double *x, double to
     const pcg_status gs = bgd_solve(A, v, tol, max_iter, st, &hs);
     PCG_CUDA(cudaEventRecord(e1, st));
     if (gs != PCG_OK) return gs;
-  } else if (bicg_use_graph(A)) {
+  } else if (bs == BS_ILU || bicg_use_graph(A)) {
     PCG_CUDA(cudaEventRecord(e0, st));
     const pcg_status gs = bg_solve(A, v, bs, tol, max_iter, st, &hs);
     PCG_CUDA(cudaEventRecord(e1, st));
@@ -1129,7 +1200,11 @@ static pcg_status bicg_impl(pcg_matrix *A, const double *b, double *x, double to
     const double nn = (double)n, nz = (double)A->nnz;
     // per iteration: 2 SpMVs (12 nnz + 4(n+1) + gather 8n + write 8n + r^ 8n each) + 3 streaming passes
     // P1 (r,p,v in; p,p^ out: 40n + M^-1 8 bs n), P3 (r,v in; r,s^ out: 32n + 8 bs n), P5 (x,p^,s^,r,t,r^ in; x,r out: 64n)
-    info->bytes_algorithmic = (double)hs.k * (2 * (12.0 * nz + 4.0 * (nn + 1) + 24.0 * nn) + 136.0 * nn + 16.0 * bs * nn);
+    info->bytes_algorithmic =
+        bs == BS_ILU
+            // 2 SpMVs + P1 (r, p, v in; p out) + P3 (r, v in; r out) + P5 (64 n) + 2 ILU(0) applications
+            ? (double)hs.k * (2 * (12.0 * nz + 4.0 * (nn + 1) + 24.0 * nn) + 120.0 * nn + 2 * ilu_bytes_per_apply(A->work.ilu))
+            : (double)hs.k * (2 * (12.0 * nz + 4.0 * (nn + 1) + 24.0 * nn) + 136.0 * nn + 16.0 * bs * nn);
     info->flops = (double)hs.k * (4.0 * nz + 30.0 * nn);
   }
   if (s == PCG_ERR_BREAKDOWN) set_error("pcg_bicgstab: breakdown (rho, r^.v or omega = 0)");
@@ -1160,5 +1235,27 @@ extern "C" pcg_status pcg_bicgstab(pcg_matrix_t A, const double *b, double *x, d
   }
   std::lock_guard<std::mutex> lk(A->mu);
   PCG_CUDA(cudaSetDevice(A->device));
-  return bicg_impl(A, b, x, tol, max_iter, block_size, (cudaStream_t)stream, info);
+  return bicg_impl(A, b, x, tol, max_iter, block_size, 0, (cudaStream_t)stream, info);
+}
+
+extern "C" pcg_status pcg_bicgstab_ilu(pcg_matrix_t A, const double *b, double *x, double tol, int64_t max_iter,
+                                       int64_t block_rows, void *stream, pcg_info *info) {
+  pcgb::NvtxRange nvtx_("pcg:pcg_bicgstab_ilu");
+  if (!A || ((!b || !x) && A->n > 0)) return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab_ilu: null argument");
+  if (!(tol > 0.0) || max_iter < 1) return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab_ilu: tol > 0 and max_iter >= 1");
+  if (A->comm) return fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab_ilu: one-GPU handles only");
+  if (A->d_perm)
+    return fail(PCG_ERR_INVALID_ARG,
+                "pcg_bicgstab_ilu: the handle holds a permuted system (SELL-C-sigma / RCM); create it with "
+                "PCG_FMT_CSR or PCG_FMT_SELL");
+  if (A->n == 0) {
+    if (info) {
+      memset(info, 0, sizeof(*info));
+      info->converged = 1;
+    }
+    return PCG_OK;
+  }
+  std::lock_guard<std::mutex> lk(A->mu);
+  PCG_CUDA(cudaSetDevice(A->device));
+  return bicg_impl(A, b, x, tol, max_iter, BS_ILU, block_rows, (cudaStream_t)stream, info);
 }

@@ -121,6 +121,9 @@ constexpr int CB_INT32 = (int)0x80000000;
 
 // internal format code of the TMA-staged SELL kernels (reported as PCG_FORMAT_SELL_TMA)
 constexpr int FMT_SELL_TMA = 3;
+// internal code of the SELL-32 kernels that read the 16-bit delta column ids (rows.cuh
+// sell_rows_d16): the SpMV, K1b and residual passes of the 3-pass schedule
+constexpr int FMT_SELL_D16 = 5;
 
 // ------------------------------------------------------------------ reductions
 constexpr int BLOCK = 256;

@@ -1,0 +1,315 @@
+// ilu.cu — Block-Jacobi with ILU(0) blocks, the preconditioner of the paper's own
+// iterative solver (PETSc BiCGSTAB + Block-Jacobi, whose default sub-solver is ILU(0):
+// P:194), for pcg_bicgstab_ilu.  SURVEY §8(f) N2; reading R6.
+//
+// M = blockdiag(L_b U_b): blocks of `bs` consecutive rows; in each block the incomplete
+// LU with zero fill of Saad, Alg. 10.4 (IKJ), written with explicitly rounded
+// operations in the oracle's order (oracle.c ilu0_setup / ilu0_apply), so the factors
+// and every application of M^-1 are bitwise the oracle's.
+//
+// Triangular solves are level-scheduled.  Row i of a block depends (forward, L) on
+// the rows k < i of its block that it references, and (backward, U) on the rows j > i;
+// its level is one more than the largest level it depends on, and the rows of one
+// level are independent.  One CTA per block walks the levels in order with a block
+// barrier between them; the block's vector lives in shared memory when it fits (bs
+// <= 24K rows), so a level costs a CTA barrier and shared-memory reads, not a
+// grid-wide synchronisation.  The level analysis (a graph traversal, setup only) runs
+// on the host; it lays the factor out level by level in an ELL form ([level][entry
+// u][row slot]: a level's loads are coalesced): per slot the local row, per (u, slot)
+// the local column (-1 = padding) and the factor value.  The numeric factorization
+// runs on the device, in the forward level order.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "matrix.cuh"
+
+namespace pcgb {
+
+struct IluLevel {
+  int64_t row_base;  // first slot of the level
+  int64_t ent_base;  // first ELL entry of the level ([u][slot], m slots per u)
+  int m, c;          // rows, entries per row (max over the level's rows)
+};
+
+// Forward levels of all blocks, then backward levels; lo[0..nblk] indexes the forward
+// levels of each block, lo[nblk+1 .. 2 nblk+1] the backward ones.
+struct IluPlan {
+  int64_t bs = 0, nblk = 0, n = 0;
+  size_t smem = 0;       // dynamic shared memory of the apply kernel (0: vector in global memory)
+  double *f = nullptr;   // factor values in CSR order (nnz)
+  int *diag = nullptr;   // CSR index of a_ii per row
+  IluLevel *lev = nullptr;
+  int *lo = nullptr;
+  int *row = nullptr;    // per slot: local row
+  int *kcol = nullptr;   // per entry: local column, -1 = padding
+  int *emap = nullptr;   // per entry: CSR index of the factor value, -1 = padding
+  double *fv = nullptr;  // per entry: factor value
+  double *ud = nullptr;  // per slot: u_ii (backward slots; 1 for forward slots)
+  int *udmap = nullptr;  // per slot: CSR index of u_ii (-1 forward)
+  int64_t nlev = 0, nslot = 0, nent = 0;
+  double bytes_per_apply = 0;
+};
+
+void ilu_free(void *p) {
+  IluPlan *P = (IluPlan *)p;
+  if (!P) return;
+  for (void *q : {(void *)P->f, (void *)P->diag, (void *)P->lev, (void *)P->lo, (void *)P->row, (void *)P->kcol,
+                  (void *)P->emap, (void *)P->fv, (void *)P->ud, (void *)P->udmap})
+    if (q) cudaFree(q);
+  delete P;
+}
+
+// ---------------------------------------------------------------- numeric factorization
+// One CTA per block; rows of one forward level are factorised in parallel (they only
+// read rows of earlier levels).  Row i, one thread, exactly the oracle's loop:
+//   for (i,k) in the row, r0 <= k < i, ascending:  f_ik = f_ik / f_kk
+//     for (i,j) after it in the row, j < r1:  if (k,j) exists: f_ij = f_ij - f_ik f_kj
+__global__ void __launch_bounds__(256) ilu_factor_kernel(int64_t n, int64_t bs, const int *__restrict__ rp,
+                                                         const int *__restrict__ col, const int *__restrict__ diag,
+                                                         double *f, const IluLevel *__restrict__ lev,
+                                                         const int *__restrict__ lo, const int *__restrict__ srow,
+                                                         int *__restrict__ err) {
+  const int64_t b = blockIdx.x, r0 = b * bs, r1 = min(r0 + bs, n);
+  for (int l = lo[b]; l < lo[b + 1]; l++) {
+    const IluLevel L = lev[l];
+    for (int t = threadIdx.x; t < L.m; t += blockDim.x) {
+      const int64_t i = r0 + srow[L.row_base + t];
+      const int e0 = rp[i], e1 = rp[i + 1];
+      for (int kk = e0; kk < e1; kk++) {
+        const int k = col[kk];
+        if (k < r0 || k >= i) continue;
+        const double fkk = f[diag[k]];
+        if (fkk == 0.0) {
+          atomicExch(err, 1);
+          continue;
+        }
+        const double fik = __ddiv_rn(f[kk], fkk);
+        f[kk] = fik;
+        const int k0 = rp[k], k1 = rp[k + 1];
+        for (int jj = kk + 1; jj < e1; jj++) {
+          const int j = col[jj];
+          if (j >= r1) break;
+          int a = k0, z = k1 - 1, kj = -1;  // (k, j) in row k (columns ascending)
+          while (a <= z) {
+            const int mid = (a + z) >> 1;
+            const int cm = col[mid];
+            if (cm == j) {
+              kj = mid;
+              break;
+            }
+            if (cm < j) a = mid + 1;
+            else z = mid - 1;
+          }
+          if (kj >= 0) f[jj] = __dsub_rn(f[jj], __dmul_rn(fik, f[kj]));
+        }
+      }
+      if (f[diag[i]] == 0.0) atomicExch(err, 1);
+    }
+    __syncthreads();  // the level's factor rows are visible to the CTA's later levels
+  }
+}
+
+__global__ void ilu_fill_kernel(int64_t ne, const int *__restrict__ emap, int64_t ns, const int *__restrict__ udmap,
+                                const double *__restrict__ f, double *__restrict__ fv, double *__restrict__ ud) {
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = t0; e < ne; e += nt) fv[e] = emap[e] >= 0 ? f[emap[e]] : 0.0;
+  for (int64_t s = t0; s < ns; s += nt) ud[s] = udmap[s] >= 0 ? f[udmap[s]] : 1.0;
+}
+
+// ---------------------------------------------------------------- application y = M^-1 v
+// Forward: y_i = v_i - sum_k l_ik y_k (k ascending); backward: y_i = (y_i - sum_j u_ij
+// y_j) / u_ii (j ascending).  The BiCGSTAB loop's flags: stop (loop ended) and skip
+// (no s^ needed: converged at the half step) make the kernel return at entry.
+struct IluView {
+  int64_t bs, n, nblk;
+  const IluLevel *lev;
+  const int *lo, *row, *kcol;
+  const double *fv, *ud;
+};
+
+template <bool SMEM>
+__device__ __forceinline__ void ilu_sweep(const IluView &P, const int *lo, int64_t b, const double *vin, double *y,
+                                          bool backward) {
+  for (int l = lo[b]; l < lo[b + 1]; l++) {
+    const IluLevel L = P.lev[l];
+    for (int t = threadIdx.x; t < L.m; t += blockDim.x) {
+      const int64_t s = L.row_base + t;
+      const int i = P.row[s];
+      double acc = backward ? y[i] : vin[i];
+      for (int u = 0; u < L.c; u++) {
+        const int64_t e = L.ent_base + (int64_t)u * L.m + t;
+        const int k = P.kcol[e];
+        if (k >= 0) acc = __dsub_rn(acc, __dmul_rn(P.fv[e], y[k]));
+      }
+      y[i] = backward ? __ddiv_rn(acc, P.ud[s]) : acc;
+    }
+    __syncthreads();
+  }
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(256) ilu_apply_kernel(IluView P, const double *__restrict__ in, double *out,
+                                                        const int *stop, const int *skip) {
+  extern __shared__ double ys[];
+  if ((stop && *(volatile const int *)stop) || (skip && *(volatile const int *)skip)) return;
+  const int64_t b = blockIdx.x, r0 = b * P.bs, nr = min(P.bs, P.n - r0);
+  double *y = SMEM ? ys : out + r0;
+  ilu_sweep<SMEM>(P, P.lo, b, in + r0, y, false);
+  ilu_sweep<SMEM>(P, P.lo + P.nblk + 1, b, in + r0, y, true);
+  if (SMEM)
+    for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) out[r0 + i] = y[i];
+}
+
+constexpr int ILU_THREADS = 256;
+constexpr int64_t ILU_SMEM_ROWS = 24576;  // 192 KB of fp64 per CTA
+
+// ---------------------------------------------------------------- setup
+pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out) {
+  const int64_t n = A->n, nnz = A->nnz;
+  if (bs < 1) bs = std::max<int64_t>(1, (n + num_sms(A->device) - 1) / num_sms(A->device));
+  if (bs > n) bs = std::max<int64_t>(n, 1);
+  IluPlan *P = new IluPlan();
+  P->bs = bs;
+  P->n = n;
+  P->nblk = (n + bs - 1) / bs;
+  auto bail = [&](pcg_status s) {
+    ilu_free(P);
+    return s;
+  };
+  // ---- host level analysis on the (device-validated, int32) CSR
+  std::vector<int> rp(n + 1), col(std::max<int64_t>(nnz, 1));
+  if (cudaMemcpyAsync(rp.data(), A->d_row_ptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      (nnz && cudaMemcpyAsync(col.data(), A->d_col, sizeof(int) * nnz, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return bail(fail(PCG_ERR_CUDA, "ilu_setup: copy of the pattern"));
+  std::vector<int> diag(n, -1);
+  for (int64_t i = 0; i < n; i++)
+    for (int e = rp[i]; e < rp[i + 1]; e++)
+      if (col[e] == i) diag[i] = e;
+  std::vector<IluLevel> levs;
+  std::vector<int> lo(2 * (P->nblk + 1));
+  std::vector<int> srow, kcol, emap, udmap;
+  std::vector<int> lev(n);
+  for (int d = 0; d < 2; d++) {  // 0: forward (L), 1: backward (U)
+    for (int64_t b = 0; b < P->nblk; b++) {
+      const int64_t r0 = b * bs, r1 = std::min(r0 + bs, n);
+      int maxl = -1;
+      for (int64_t q = 0; q < r1 - r0; q++) {
+        const int64_t i = d == 0 ? r0 + q : r1 - 1 - q;
+        int l = 0;
+        for (int e = rp[i]; e < rp[i + 1]; e++) {
+          const int64_t k = col[e];
+          if (d == 0 ? (k >= r0 && k < i) : (k > i && k < r1)) l = std::max(l, lev[k] + 1);
+        }
+        lev[i] = l;
+        maxl = std::max(maxl, l);
+      }
+      // counting sort of the block's rows by level (rows ascending inside a level)
+      std::vector<int> cnt(maxl + 2, 0);
+      for (int64_t i = r0; i < r1; i++) cnt[lev[i] + 1]++;
+      for (int l = 0; l <= maxl; l++) cnt[l + 1] += cnt[l];
+      std::vector<int> ord(r1 - r0);
+      {
+        std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+        for (int64_t i = r0; i < r1; i++) ord[pos[lev[i]]++] = (int)(i - r0);
+      }
+      lo[d * (P->nblk + 1) + b] = (int)levs.size();
+      for (int l = 0; l <= maxl; l++) {
+        IluLevel L;
+        L.row_base = (int64_t)srow.size();
+        L.ent_base = (int64_t)kcol.size();
+        L.m = cnt[l + 1] - cnt[l];
+        int c = 0;
+        for (int t = cnt[l]; t < cnt[l + 1]; t++) {
+          const int64_t i = r0 + ord[t];
+          int ci = 0;
+          for (int e = rp[i]; e < rp[i + 1]; e++) {
+            const int64_t k = col[e];
+            if (d == 0 ? (k >= r0 && k < i) : (k > i && k < r1)) ci++;
+          }
+          c = std::max(c, ci);
+        }
+        L.c = c;
+        kcol.resize(kcol.size() + (size_t)L.m * c, -1);
+        emap.resize(emap.size() + (size_t)L.m * c, -1);
+        for (int t = cnt[l]; t < cnt[l + 1]; t++) {
+          const int64_t i = r0 + ord[t];
+          const int slot = t - cnt[l];
+          srow.push_back(ord[t]);
+          udmap.push_back(d == 1 ? diag[i] : -1);
+          int u = 0;
+          for (int e = rp[i]; e < rp[i + 1]; e++) {
+            const int64_t k = col[e];
+            if (d == 0 ? (k >= r0 && k < i) : (k > i && k < r1)) {
+              const size_t ei = (size_t)L.ent_base + (size_t)u * L.m + slot;
+              kcol[ei] = (int)(k - r0);
+              emap[ei] = e;
+              u++;
+            }
+          }
+        }
+        levs.push_back(L);
+      }
+    }
+    lo[d * (P->nblk + 1) + P->nblk] = (int)levs.size();
+  }
+  P->nlev = (int64_t)levs.size();
+  P->nslot = (int64_t)srow.size();
+  P->nent = (int64_t)kcol.size();
+  // ---- upload
+  auto up = [&](void **dst, const void *src, size_t bytes) -> bool {
+    if (cudaMalloc(dst, std::max<size_t>(bytes, 8)) != cudaSuccess) return false;
+    return bytes == 0 || cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;
+  };
+  if (!up((void **)&P->diag, diag.data(), sizeof(int) * n) || !up((void **)&P->lev, levs.data(), sizeof(IluLevel) * levs.size()) ||
+      !up((void **)&P->lo, lo.data(), sizeof(int) * lo.size()) || !up((void **)&P->row, srow.data(), sizeof(int) * srow.size()) ||
+      !up((void **)&P->kcol, kcol.data(), sizeof(int) * kcol.size()) ||
+      !up((void **)&P->emap, emap.data(), sizeof(int) * emap.size()) ||
+      !up((void **)&P->udmap, udmap.data(), sizeof(int) * udmap.size()) ||
+      cudaMalloc(&P->f, sizeof(double) * std::max<int64_t>(nnz, 1)) != cudaSuccess ||
+      cudaMalloc(&P->fv, sizeof(double) * std::max<int64_t>(P->nent, 1)) != cudaSuccess ||
+      cudaMalloc(&P->ud, sizeof(double) * std::max<int64_t>(P->nslot, 1)) != cudaSuccess) {
+    cudaGetLastError();
+    return bail(fail(PCG_ERR_OOM, "ilu_setup: device memory"));
+  }
+  if (nnz) PCG_CUDA(cudaMemcpyAsync(P->f, A->d_val, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, st));
+  // ---- numeric factorization (forward level order) and the level-ordered factor
+  int *err;
+  PCG_CUDA(cudaMalloc(&err, sizeof(int)));
+  PCG_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  ilu_factor_kernel<<<(unsigned)P->nblk, 256, 0, st>>>(n, bs, A->d_row_ptr, A->d_col, P->diag, P->f, P->lev, P->lo,
+                                                       P->row, err);
+  ilu_fill_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((std::max(P->nent, P->nslot) + 255) / 256, 4096)),
+                    256, 0, st>>>(P->nent, P->emap, P->nslot, P->udmap, P->f, P->fv, P->ud);
+  count_launch(2);
+  int herr = 0;
+  PCG_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(err);
+  if (herr) return bail(fail(PCG_ERR_ZERO_DIAGONAL, "pcg_bicgstab_ilu: zero pivot in the ILU(0) factorization"));
+  const int64_t maxrows = std::min(bs, n);
+  P->smem = maxrows <= ILU_SMEM_ROWS ? sizeof(double) * (size_t)maxrows : 0;
+  if (P->smem > 48 * 1024)
+    PCG_CUDA(cudaFuncSetAttribute(ilu_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem));
+  // algorithmic bytes of one application: v in + y out (16 n), the level-ordered factor
+  // (8 + 4 B per stored entry, incl. ELL padding) and slots (row 4 B, u_ii 8 B)
+  P->bytes_per_apply = 16.0 * n + 12.0 * P->nent + 12.0 * P->nslot + sizeof(IluLevel) * P->nlev;
+  *plan_out = P;
+  return PCG_OK;
+}
+
+void ilu_launch(void *plan, const double *in, double *out, const int *stop, const int *skip, cudaStream_t st) {
+  const IluPlan *P = (const IluPlan *)plan;
+  const IluView V{P->bs, P->n, P->nblk, P->lev, P->lo, P->row, P->kcol, P->fv, P->ud};
+  if (P->smem)
+    ilu_apply_kernel<true><<<(unsigned)P->nblk, ILU_THREADS, P->smem, st>>>(V, in, out, stop, skip);
+  else
+    ilu_apply_kernel<false><<<(unsigned)P->nblk, ILU_THREADS, 0, st>>>(V, in, out, stop, skip);
+  count_launch();
+}
+
+int64_t ilu_block_rows(const void *plan) { return ((const IluPlan *)plan)->bs; }
+double ilu_bytes_per_apply(const void *plan) { return ((const IluPlan *)plan)->bytes_per_apply; }
+
+}  // namespace pcgb

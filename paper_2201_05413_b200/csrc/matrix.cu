@@ -283,7 +283,10 @@ __global__ void d16_build_kernel(int64_t n, int64_t n_cols, int64_t n_slices, co
 }
 
 pcg_status build_d16(pcg_matrix *A, cudaStream_t st) {
-  if (A->d_sdcol || !A->d_slice_ptr || A->n_slices == 0 || getenv("PCG_NO_D16")) return PCG_OK;
+  // opt-in (PCG_D16=1): measured on B200 it moves 13 % fewer K1b bytes on C5 but takes
+  // the same time (K1b 2,350 us either way; C3 148 us either way), DESIGN.md §7
+  const char *e = getenv("PCG_D16");
+  if (A->d_sdcol || !A->d_slice_ptr || A->n_slices == 0 || !(e && atoi(e) == 1) || getenv("PCG_NO_D16")) return PCG_OK;
   PCG_CUDA(cudaMalloc(&A->d_sdcol, sizeof(int16_t) * std::max<int64_t>(A->sell_entries, 1)));
   PCG_CUDA(cudaMalloc(&A->d_scbase, sizeof(int) * std::max<int64_t>(A->sell_entries / 32, 1)));
   unsigned long long *d_ok;
@@ -309,6 +312,11 @@ pcg_status build_d16(pcg_matrix *A, cudaStream_t st) {
 }
 
 void free_sell(pcg_matrix *A) {
+  if (A->d_wdesc) cudaFree(A->d_wdesc);
+  if (A->d_wlidx) cudaFree(A->d_wlidx);
+  A->d_wdesc = nullptr;
+  A->d_wlidx = nullptr;
+  A->wplan = 0;
   if (A->d_sdcol) {
     cudaFree(A->d_sdcol);
     cudaFree(A->d_scbase);
@@ -700,6 +708,7 @@ void free_work(pcg_matrix *A) {
   if (w.mloop_graph) cudaGraphDestroy(w.mloop_graph);
   if (w.bg_exec) cudaGraphExecDestroy(w.bg_exec);
   if (w.bg_graph) cudaGraphDestroy(w.bg_graph);
+  if (w.ilu) ilu_free(w.ilu);
   for (double *p : {w.r, w.z, w.q, w.p[0], w.p[1], w.x, w.w, w.stage_b, w.stage_x, w.partials, w.mr, w.mz, w.mq,
                     w.mp[0], w.mp[1], w.mx, w.mb, w.mw, w.mpart})
     if (p) cudaFree(p);
@@ -754,8 +763,8 @@ extern "C" pcg_status csr_destroy(pcg_matrix_t A) {
   if (A->ov_join) cudaEventDestroy(A->ov_join);
   for (void *p : {(void *)A->d_row_ptr, (void *)A->d_col, (void *)A->d_val, (void *)A->d_dinv,
                   (void *)A->d_slice_ptr, (void *)A->d_scol, (void *)A->d_sval, (void *)A->d_lead, (void *)A->halo.d_send_idx,
-                  (void *)A->d_perm, (void *)A->d_iperm,
-                  (void *)A->halo.d_send_buf})
+                  (void *)A->d_perm, (void *)A->d_iperm, (void *)A->d_sdcol, (void *)A->d_scbase, A->d_wdesc,
+                  (void *)A->d_wlidx, (void *)A->halo.d_send_buf})
     if (p) cudaFree(p);
   delete A;
   return PCG_OK;
@@ -786,5 +795,6 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->reorder = A->reorder;
   o->overlap_rows = A->ov ? A->ov_ib - A->ov_ia : 0;
   o->d16_slices = A->d16_slices;
+  o->spmm_windowed = A->wplan;
   return PCG_OK;
 }

@@ -21,6 +21,11 @@ struct pcg_comm {
 
 namespace pcgb {
 
+pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out);
+void ilu_launch(void *plan, const double *in, double *out, const int *stop, const int *skip, cudaStream_t st);
+void ilu_free(void *plan);
+int64_t ilu_block_rows(const void *plan);
+double ilu_bytes_per_apply(const void *plan);
 // Wait for the work queued on `st` (distributed handles: with NCCL failure detection
 // and the communicator's timeout; see dist.cu comm_wait).
 pcg_status comm_wait(pcg_comm *C, cudaStream_t st);
@@ -65,6 +70,7 @@ struct SolveWork {
   double *bv = nullptr;
   void *bstate = nullptr, *bbar = nullptr;
   double *bminv = nullptr;
+  void *ilu = nullptr;  // ILU(0) Block-Jacobi plan (ilu.cu), cached per block size
   int bminv_bs = 0, bgrid = 0, bgrid_bs = 0;
   // pipelined PCG (pipelined.cu): x r u w m0 m1 z q s p, state, barrier, grid
   double *pv = nullptr;
@@ -146,6 +152,11 @@ struct pcg_matrix {
   int64_t ov_ia = 0, ov_ib = 0;
   cudaStream_t ov_side = nullptr;
   cudaEvent_t ov_fork = nullptr, ov_join = nullptr;
+  // windowed SpMM plan (multi.cu): per 512-row tile up to 4 column windows staged in shared
+  // memory by TMA, per SELL entry its 16-bit offset in the concatenated windows
+  void *d_wdesc = nullptr;
+  uint16_t *d_wlidx = nullptr;
+  int wplan = 0;  // 0: not built, 1: usable, -1: the matrix does not fit the windows
   // 16-bit delta column ids of the SELL entries (common.cuh SellView::dcol)
   int16_t *d_sdcol = nullptr;
   int *d_scbase = nullptr;

@@ -22,6 +22,8 @@
 // Frozen columns cost nothing: their blocks of K1a/K2 return at entry and K1b
 // skips their gather round.  Column c's SpMM sum is formed left to right over
 // the row with one fma per entry: bitwise the single-RHS SELL SpMV of column c.
+#include <climits>
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -29,6 +31,7 @@
 
 #include "matrix.cuh"
 #include "rows.cuh"
+#include "staged.cuh"
 
 namespace pcgb {
 
@@ -73,6 +76,32 @@ __device__ void mcols_reduce(const double *partials, int nb, int k, double (*out
       for (int b = strand; b < nb; b += STRANDS) acc += __ldcg(partials + ((size_t)i * KMAX + c) * nb + b);
     }
     sm[strand][c] = acc;
+    __syncthreads();
+    if (threadIdx.x < KMAX) {
+      double t = 0.0;
+#pragma unroll
+      for (int s = 0; s < STRANDS; s++) t += sm[s][threadIdx.x];
+      out[i][threadIdx.x] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// mcols_reduce for blocks with more than BLOCK threads (the windowed SpMM): the first
+// BLOCK threads form the strands, the others only take part in the barriers
+template <int NV>
+__device__ void mcols_reduce_n(const double *partials, int nb, int k, double (*out)[KMAX], double (*sm)[KMAX]) {
+  constexpr int STRANDS = BLOCK / KMAX;  // 8
+  const int c = threadIdx.x % KMAX, strand = threadIdx.x / KMAX;
+  for (int i = 0; i < NV; i++) {
+    if (threadIdx.x < BLOCK) {
+      double acc = 0.0;
+      if (c < k) {
+#pragma unroll 4
+        for (int b = strand; b < nb; b += STRANDS) acc += __ldcg(partials + ((size_t)i * KMAX + c) * nb + b);
+      }
+      sm[strand][c] = acc;
+    }
     __syncthreads();
     if (threadIdx.x < KMAX) {
       double t = 0.0;
@@ -265,7 +294,6 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
     const bool ok = row < S.n;
     const double *vp = S.val + base + lane;
     const int *cp = S.col + base + lane;
-    const int cb0 = sell_cb0(S, base, len);
     // epilogue of column c for this slice (row sum -> output + reduction values)
     auto finish_col = [&](int c, double sum) {
       double r[NV];
@@ -302,9 +330,11 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
 #pragma unroll
       for (int u = 0; u < 8; u++) {
         a[u] = 0.0;
-        if (u < len) a[u] = ld_stream(vp + (size_t)u * 32);
+        if (u < len) {
+          a[u] = ld_stream(vp + (size_t)u * 32);
+          j[u] = ld_stream(cp + (size_t)u * 32);
+        }
       }
-      sell_cols<8>(S, base, lane, (int)(S.row0 + row), cb0, 0, len, j);
       cols_ready(j, S.zero);
       if (pf) {  // first touch of a gathered line is (mostly) its largest column: start every
                  // column's fetch now so only the first gather round waits on HBM (padding
@@ -594,6 +624,318 @@ static int mgrid_spmm(pcg_matrix *A, int k) {
   return (int)std::min<int64_t>((int64_t)num_sms(A->device) * b, need);
 }
 
+// ---------------------------------------------------------------- windowed SpMM (K1b for k right-hand sides)
+// The register-gather SpMM above moves every gathered P entry from L2 to the SM
+// (7 gathers per row and column for the 7-point stencil: ~1.8 GB per SpMM at C4, k =
+// 16, against 0.7 GB of HBM traffic), which makes the L2 -> SM path, not HBM, its
+// bound.  Here the column windows a tile of rows references are copied ONCE per
+// (tile, column) into shared memory by the TMA bulk-copy engine and every gather is a
+// shared-memory load:
+//   * tile = WT_SLICES SELL slices (512 rows); its referenced columns, sorted, split
+//     into at most W_NWIN contiguous windows where consecutive columns are more than
+//     W_GAP apart (the 7-point stencil: the -m^2 band, the [-m, +m] band, the +m^2
+//     band); the windows total at most W_CAP entries;
+//   * per SELL entry, its 16-bit offset in the concatenated windows (the "plan",
+//     built once per matrix on the device, win_plan_kernel);
+//   * one producer thread per CTA issues, per (tile, active column), one
+//     cp.async.bulk per window into a ring of W_STAGES shared-memory stages (full /
+//     empty mbarriers, expect_tx bytes); W_CW consumer warps, 2 slices each, hold their
+//     slices' entries in registers for all columns of the tile and form each row sum
+//     left to right with one fma per entry (bitwise the SpMV's sum), write Q_c and
+//     their sigma_c partial (P_c at the row is in the window that holds the tile's
+//     own rows).
+// L2 -> SM bytes per row and column: the windows' (3 T + 2 m) / T x 8 B ~ 28 B
+// instead of ~57 B.  Matrices with rows longer than 8, or whose tiles need more
+// windows or space, keep the register-gather kernel (multi.cu mspmm_kernel).
+constexpr int WT_SLICES = 16, WT_ROWS = WT_SLICES * 32, W_NWIN = 4, W_CAP = 2048, W_STAGES = 4, W_CW = 8;
+constexpr int W_THREADS = (W_CW + 1) * 32, W_GAP = 64, W_KEYS = WT_ROWS * 8;
+
+struct WinDesc {
+  int nwin, self_off, start[W_NWIN], len[W_NWIN], off[W_NWIN], pad[2];
+};
+static_assert(sizeof(WinDesc) == 64, "WinDesc is one 64-B record");
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// one CTA (512 threads) per tile: sort the tile's referenced columns (bitonic, in shared
+// memory), cut them into windows, write the descriptor and every entry's window offset
+__global__ void __launch_bounds__(512) win_plan_kernel(SellView S, int64_t n_tiles, WinDesc *__restrict__ desc,
+                                                       uint16_t *__restrict__ lidx, int *__restrict__ fail) {
+  __shared__ int keys[W_KEYS];
+  __shared__ WinDesc d;
+  __shared__ int s_bad;
+  const int64_t t = blockIdx.x;
+  const int64_t s0 = t * WT_SLICES, s1 = (s0 + WT_SLICES < S.n_slices) ? s0 + WT_SLICES : S.n_slices;
+  const int64_t e0 = S.slice_ptr[s0], e1 = S.slice_ptr[s1];
+  const int cnt = (int)(e1 - e0);
+  if (threadIdx.x == 0) s_bad = cnt > W_KEYS;
+  __syncthreads();
+  if (s_bad) {
+    if (threadIdx.x == 0) atomicAdd(fail, 1);
+    return;
+  }
+  // entry e lies in slice s(e): its row is s*32 + lane; rows >= n are padding of the last slice
+  for (int i = threadIdx.x; i < W_KEYS; i += blockDim.x) {
+    int key = INT_MAX;
+    if (i < cnt) {
+      const int64_t e = e0 + i;
+      int64_t s = s0;
+      while (S.slice_ptr[s + 1] <= e) s++;
+      const int64_t row = s * 32 + (e & 31);
+      if (row < S.n) key = S.col[e];
+    }
+    keys[i] = key;
+  }
+  __syncthreads();
+  for (int k = 2; k <= W_KEYS; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < W_KEYS; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const int a = keys[i], b = keys[l];
+          if ((a > b) == up) {
+            keys[i] = b;
+            keys[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  if (threadIdx.x == 0) {
+    int nw = 0, bad = 0;
+    int st[W_NWIN + 1], en[W_NWIN + 1];
+    int prev = keys[0];
+    if (prev != INT_MAX) {
+      st[0] = prev;
+      nw = 1;
+      for (int i = 1; i < W_KEYS && keys[i] != INT_MAX; i++) {
+        const int c = keys[i];
+        if (c == prev) continue;
+        if (c - prev > W_GAP) {
+          en[nw - 1] = prev + 1;
+          if (nw == W_NWIN) {
+            bad = 1;
+            break;
+          }
+          st[nw++] = c;
+        }
+        prev = c;
+      }
+      if (!bad) en[nw - 1] = prev + 1;
+    }
+    int tot = 0;
+    d.nwin = bad ? 0 : nw;
+    for (int w = 0; w < W_NWIN; w++) {
+      d.start[w] = d.len[w] = d.off[w] = 0;
+      if (!bad && w < nw) {
+        const int a = st[w] & ~1, b = (en[w] + 1) & ~1;  // 16-B aligned copies
+        d.start[w] = a;
+        d.len[w] = b - a;
+        d.off[w] = tot;
+        tot += b - a;
+      }
+    }
+    if (tot > W_CAP) bad = 1;
+    const int64_t r0 = s0 * 32, r1 = (s1 * 32 < S.n) ? s1 * 32 : S.n;
+    d.self_off = -1;
+    for (int w = 0; w < nw && !bad; w++)
+      if (d.start[w] <= r0 && r1 <= d.start[w] + d.len[w]) d.self_off = d.off[w] + (int)(r0 - d.start[w]);
+    if (d.self_off < 0) bad = 1;
+    d.pad[0] = d.pad[1] = 0;
+    s_bad = bad;
+    if (bad) atomicAdd(fail, 1);
+    desc[t] = d;
+  }
+  __syncthreads();
+  if (s_bad) return;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const int64_t e = e0 + i;
+    int64_t s = s0;
+    while (S.slice_ptr[s + 1] <= e) s++;
+    const int64_t row = s * 32 + (e & 31);
+    int o = 0;  // padding rows (>= n): any in-window offset (a = 0, result unused)
+    if (row < S.n) {
+      const int c = S.col[e];
+      for (int w = 0; w < d.nwin; w++)
+        if (c >= d.start[w] && c < d.start[w] + d.len[w]) o = d.off[w] + c - d.start[w];
+    }
+    lidx[e] = (uint16_t)o;
+  }
+}
+
+// Q_c = A P_c and sigma_c = P_c . Q_c for the active columns, windows staged by TMA.
+__global__ void __launch_bounds__(W_THREADS, 3)
+    mspmm_win_kernel(SellView S, const WinDesc *__restrict__ desc, const uint16_t *__restrict__ lidx, MVecs v,
+                     MultiScalars *sc, double *partials, int k, int use_cond, cudaGraphConditionalHandle h) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double *ring = reinterpret_cast<double *>(smem);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)W_STAGES * W_CAP * 8);
+  uint64_t *empty = full + W_STAGES;
+  __shared__ double s_red[W_CW][KMAX];
+  __shared__ double s_sm[BLOCK / KMAX][KMAX];
+  __shared__ double s_out[1][KMAX];
+  const volatile MultiScalars *vs = sc;
+  if (vs->n_active == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) mstop(use_cond, h);
+    return;
+  }
+  unsigned int act = 0;
+  for (int c = 0; c < k; c++) act |= (unsigned int)(vs->active[c] != 0) << c;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_tiles = (S.n_slices + WT_SLICES - 1) / WT_SLICES;
+  const int64_t ld = v.ld;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < W_STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], W_CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < W_CW * KMAX; i += blockDim.x) (&s_red[0][0])[i] = 0.0;
+  __syncthreads();
+  if (warp == W_CW) {  // ---- producer: one elected thread issues the window copies
+    if (lane == 0) {
+      int q = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const WinDesc d = desc[t];
+        const int64_t tn = t + gridDim.x;  // the next tile's matrix entries, toward L2
+        if (tn < n_tiles) {
+          const int64_t a = __ldg(S.slice_ptr + tn * WT_SLICES);
+          const int64_t b = __ldg(S.slice_ptr + ((tn + 1) * WT_SLICES < S.n_slices ? (tn + 1) * WT_SLICES : S.n_slices));
+          if (b > a) {
+            bulk_prefetch_l2(S.val + a, (uint32_t)((b - a) * 8));
+            bulk_prefetch_l2(lidx + a, (uint32_t)(((b - a) * 2 + 15) & ~15));
+          }
+        }
+        uint32_t bytes = 0;
+        for (int w = 0; w < d.nwin; w++) bytes += (uint32_t)d.len[w] * 8;
+        for (int c = 0; c < k; c++) {
+          if (!(act >> c & 1)) continue;
+          const int st = q % W_STAGES;
+          if (q >= W_STAGES) mbar_wait(&empty[st], (uint32_t)((q / W_STAGES - 1) & 1));
+          mbar_expect_tx(&full[st], bytes);
+          const double *Pc = v.P + (size_t)c * ld;
+          for (int w = 0; w < d.nwin; w++)
+            bulk_g2s(ring + (size_t)st * W_CAP + d.off[w], Pc + d.start[w], (uint32_t)d.len[w] * 8, &full[st]);
+          q++;
+        }
+      }
+    }
+  } else {  // ---- consumers: 2 slices per warp
+    int q = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int self_off = __ldg(&desc[t].self_off);
+      const int64_t r0 = t * WT_ROWS;
+      double a[2][8];
+      int li[2][8];
+      bool has[2];
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const int64_t s = t * WT_SLICES + warp * 2 + j;
+        has[j] = s < S.n_slices;
+        int len = 0;
+        int64_t base = 0;
+        if (has[j]) {
+          base = __ldg(S.slice_ptr + s);
+          len = (int)((__ldg(S.slice_ptr + s + 1) - base) >> 5);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          a[j][u] = 0.0;
+          li[j][u] = 0;  // beyond the row: a = 0 times the (written) first window entry
+          if (u < len) {
+            a[j][u] = ld_stream(S.val + base + (size_t)u * 32 + lane);
+            li[j][u] = (int)__ldg(lidx + base + (size_t)u * 32 + lane);
+          }
+        }
+      }
+      for (int c = 0; c < k; c++) {
+        if (!(act >> c & 1)) continue;
+        const int st = q % W_STAGES;
+        mbar_wait(&full[st], (uint32_t)((q / W_STAGES) & 1));
+        const double *buf = ring + (size_t)st * W_CAP;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+          if (!has[j]) continue;
+          double sum = 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; u++) sum = __fma_rn(a[j][u], buf[li[j][u]], sum);
+          const int64_t row = (t * WT_SLICES + warp * 2 + j) * 32 + lane;
+          if (row < S.n) {
+            __stcs(v.Q + (size_t)c * ld + row, sum);
+            acc = __fma_rn(buf[self_off + (int)(row - r0)], sum, acc);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        acc = warp_sum(acc);
+        if (lane == 0) s_red[warp][c] += acc;
+        q++;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < KMAX) {
+    double tsum = 0.0;
+#pragma unroll
+    for (int w = 0; w < W_CW; w++) tsum += s_red[w][threadIdx.x];
+    partials[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = tsum;
+  }
+  if (!mlast_block(&sc->cnt_a)) return;
+  mcols_reduce_n<1>(partials, gridDim.x, k, s_out, s_sm);
+  if (threadIdx.x == 0) mk1b_finish(s_out[0], sc, use_cond, h);
+}
+
+static size_t win_smem() { return (size_t)W_STAGES * W_CAP * 8 + 2 * W_STAGES * 8; }
+
+static int win_grid(pcg_matrix *A) {
+  cudaFuncSetAttribute(mspmm_win_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem());
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, mspmm_win_kernel, W_THREADS, win_smem()) != cudaSuccess) {
+    cudaGetLastError();
+    b = 1;
+  }
+  b = std::max(1, std::min(8, b));
+  const int64_t n_tiles = (A->n_slices + WT_SLICES - 1) / WT_SLICES;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms(A->device) * b, n_tiles));
+}
+
+// build the window plan once per matrix (SELL-32 with rows of at most 8 entries)
+static pcg_status win_plan(pcg_matrix *A, cudaStream_t st) {
+  if (A->wplan != 0) return PCG_OK;
+  const char *e = getenv("PCG_SPMM_WIN");
+  if ((e && atoi(e) == 0) || A->max_row_len > 8 || A->n_slices == 0 || A->comm || A->n + 2 > (int64_t(1) << 31)) {
+    A->wplan = -1;
+    return PCG_OK;
+  }
+  const int64_t n_tiles = (A->n_slices + WT_SLICES - 1) / WT_SLICES;
+  PCG_CUDA(cudaMalloc(&A->d_wdesc, sizeof(WinDesc) * n_tiles));
+  PCG_CUDA(cudaMalloc(&A->d_wlidx, sizeof(uint16_t) * std::max<int64_t>(A->sell_entries, 8)));
+  int *d_fail;
+  PCG_CUDA(cudaMalloc(&d_fail, sizeof(int)));
+  PCG_CUDA(cudaMemsetAsync(d_fail, 0, sizeof(int), st));
+  win_plan_kernel<<<(unsigned)n_tiles, 512, 0, st>>>(A->sell(), n_tiles, (WinDesc *)A->d_wdesc, A->d_wlidx, d_fail);
+  count_launch();
+  int fails = 0;
+  PCG_CUDA(cudaMemcpyAsync(&fails, d_fail, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_fail);
+  if (fails) {
+    cudaFree(A->d_wdesc);
+    cudaFree(A->d_wlidx);
+    A->d_wdesc = nullptr;
+    A->d_wlidx = nullptr;
+    A->wplan = -1;
+  } else {
+    A->wplan = 1;
+  }
+  return PCG_OK;
+}
+
 // tuning knob PCG_SPMM_PF (default 1): L2 prefetch of each slice's first-touch lines
 static int spmm_prefetch() {
   static int v = [] {
@@ -606,6 +948,11 @@ static int spmm_prefetch() {
 template <int MODE>
 static void launch_mspmm(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
   SolveWork &w = A->work;
+  if (MODE == MS_SPMM && A->wplan == 1) {
+    mspmm_win_kernel<<<win_grid(A), W_THREADS, win_smem(), st>>>(A->sell(), (const WinDesc *)A->d_wdesc, A->d_wlidx,
+                                                                 mvecs_of(A), w.msc, w.mpart, k, use_cond, h);
+    return;
+  }
   const int g = mgrid_spmm(A, k);
   const SellView S = A->sell();
   const MVecs v = mvecs_of(A);
@@ -726,6 +1073,7 @@ static pcg_status multi_prepare(pcg_matrix *A, int k, cudaStream_t st) {
   PCG_TRY(ensure_work(A));
   PCG_TRY(build_sell(A, st));  // the SpMM runs over SELL-32 slices whatever format SpMV uses
   PCG_TRY(ensure_multi_work(A, k));
+  PCG_TRY(win_plan(A, st));
   return PCG_OK;
 }
 

@@ -270,6 +270,8 @@ __global__ void __launch_bounds__(BLOCK) k1b_kernel(SellView S, CsrView C, int64
     sell_staged_rows<8>(S, io, pre, gather, epi2);
   } else if (FMT == PCG_FORMAT_SELL) {
     sell_rows(S, gather, epi);
+  } else if (FMT == FMT_SELL_D16) {
+    sell_rows_d16(S, gather, epi);
   } else {
     csr_rows<L>(C, gather, epi);
   }
@@ -347,6 +349,8 @@ __global__ void __launch_bounds__(BLOCK) resid_kernel(SellView S, CsrView C, int
     sell_staged_rows<8>(S, io, pre, gather, epi2);
   } else if (FMT == PCG_FORMAT_SELL) {
     sell_rows(S, gather, epi);
+  } else if (FMT == FMT_SELL_D16) {
+    sell_rows_d16(S, gather, epi);
   } else {
     csr_rows<L>(C, gather, epi);
   }
@@ -438,6 +442,8 @@ __global__ void __launch_bounds__(BLOCK) spmv_kernel(SellView S, CsrView C, cons
     sell_staged_rows<8>(S, io, pre, gather, epi2);
   } else if (FMT == PCG_FORMAT_SELL) {
     sell_rows(S, gather, epi);
+  } else if (FMT == FMT_SELL_D16) {
+    sell_rows_d16(S, gather, epi);
   } else {
     csr_rows<L>(C, gather, epi);
   }
@@ -461,13 +467,25 @@ struct Dispatch;
       }                                                                          \
   } while (0)
 
+// SELL-32 handles with 16-bit delta column ids run the D16 engine in the passes below
+#define PCG_DISPATCH_D16(FMTV, LANES, KERNEL, ...)                          \
+  do {                                                                      \
+    if ((FMTV) == FMT_SELL_D16) KERNEL<FMT_SELL_D16, 1>__VA_ARGS__;         \
+    else PCG_DISPATCH(FMTV, LANES, KERNEL, __VA_ARGS__);                    \
+  } while (0)
+
+static int fmt_d16(const pcg_matrix *A, int fmt) {
+  return (fmt == PCG_FORMAT_SELL && A->d_sdcol) ? FMT_SELL_D16 : fmt;
+}
+
 static Vecs vecs_of(pcg_matrix *A) {
   SolveWork &w = A->work;
   return Vecs{w.r, w.z, w.q, w.p[0], w.p[1], w.x, A->d_dinv};
 }
 
 pcg_status launch_spmv_fmt(pcg_matrix *A, int fmt, const double *x, double *y, cudaStream_t st) {
-  PCG_DISPATCH(fmt, A->csr_lanes, spmv_kernel, <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), x, y, A->n + A->n_ghost));
+  PCG_DISPATCH_D16(fmt_d16(A, fmt), A->csr_lanes, spmv_kernel,
+                   <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), x, y, A->n + A->n_ghost));
   count_launch();
   PCG_CUDA(cudaGetLastError());
   return PCG_OK;
@@ -525,9 +543,9 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
                                                        : (Cv.n * A->csr_lanes + BLOCK - 1) / BLOCK;
       const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(A->grid_spmv, need));
       cudaStream_t ks = t == 0 ? A->ov_side : st;
-      PCG_DISPATCH(A->format, A->csr_lanes, k1b_kernel,
-                   <<<g, BLOCK, A->dyn_smem, ks>>>(S, Cv, A->n_ghost, v, w.sc, w.partials, 1, use_cond, h, R.r0,
-                                                  phase));
+      PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
+                       <<<g, BLOCK, A->dyn_smem, ks>>>(S, Cv, A->n_ghost, v, w.sc, w.partials, 1, use_cond, h, R.r0,
+                                                      phase));
       count_launch();
     }
     PCG_CUDA(cudaGetLastError());
@@ -539,9 +557,9 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
   if (A->schedule == 3) {  // K1a (streaming p/x update) + K1b (SpMV + sigma)
     k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, use_cond, h);
     count_launch();
-    PCG_DISPATCH(A->format, A->csr_lanes, k1b_kernel,
-                 <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
-                                                            A->comm ? 1 : 0, use_cond, h, 0, 0));
+    PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
+                     <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
+                                                                A->comm ? 1 : 0, use_cond, h, 0, 0));
     count_launch();
     PCG_CUDA(cudaGetLastError());
     if (A->comm) {
@@ -589,7 +607,7 @@ static pcg_status launch_resid(pcg_matrix *A, const double *b, int mode, cudaStr
   Vecs v = vecs_of(A);
   SolveWork &w = A->work;
   if (A->comm) PCG_TRY(halo_exchange(A, w.x, 1, st));
-  PCG_DISPATCH(A->format, A->csr_lanes, resid_kernel,
+  PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, resid_kernel,
                <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, b, v, w.sc, w.partials,
                                                 mode, A->comm ? 1 : 0));
   count_launch();

@@ -1,0 +1,114 @@
+"""GPU parity of BiCGSTAB + Block-Jacobi ILU(0) (pcg_bicgstab_ilu; SURVEY §8(f) N2,
+DESIGN.md reading R6) against the oracle's orc_bicgstab_pc on the paper's Table 1
+systems (identity boundary rows) and on SPD FEM systems.
+
+The factor and every M^-1 application are bitwise the oracle's (same operation order,
+explicitly rounded); the BiCGSTAB vector updates and dot products are not (fma, tree
+reductions), so x is compared within 1e-9 of the oracle (and of the exact x^2 - y^2 on
+the Table 1 grid) and the iteration count against the range the oracle itself spans
+under rounding-level perturbations of b (BiCGSTAB's count is not stable at 2 %, the
+bar of tests/test_gpu_bicgstab.py), widened by 2.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pcg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_05413_b200 as p
+    return p
+
+
+def _dev(a):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(a)).cuda()
+
+
+def _matrix(pcg, A, fmt="auto"):
+    return pcg.Matrix.from_csr(_dev(A.row_ptr), _dev(A.col), _dev(A.val), fmt=fmt)
+
+
+def _oracle_range(A, b, tol, bs):
+    rng = np.random.default_rng(0)
+    its = [O.bicgstab_ilu(A, b, tol=tol, block=bs).iterations]
+    for _ in range(3):
+        its.append(O.bicgstab_ilu(A, b * (1 + 1e-15 * rng.standard_normal(A.n)), tol=tol, block=bs).iterations)
+    return min(its), max(its)
+
+
+@pytest.mark.parametrize("N,bs", [(16, 4096), (16, 256), (24, 576), (24, 1000), (32, 0), (20, 1)])
+def test_bicgstab_ilu_table1_parity(pcg, N, bs):
+    A, b = O.fd_cube(N)
+    tol = 1e-12
+    M = _matrix(pcg, A)
+    x, info = M.bicgstab(_dev(b), tol=tol, block=bs, precond="ilu0")
+    bs_eff = bs if bs > 0 else -(-A.n // _sms())
+    r = O.bicgstab_ilu(A, b, tol=tol, block=bs_eff)
+    assert r.status == O.OK and info["status"] == 0 and info["relres_true"] <= tol
+    x = x.cpu().numpy()
+    assert np.linalg.norm(x - r.x) <= 1e-9 * np.linalg.norm(r.x)
+    h = 1.0 / (N - 1)
+    i = np.arange(N)
+    X, Y = np.tile(i, N * N) * h, np.tile(np.repeat(i, N), N) * h
+    assert np.max(np.abs(x - (X * X - Y * Y))) <= 1e-9
+    lo, hi = _oracle_range(A, b, tol, bs_eff)
+    assert lo - 2 <= info["iterations"] <= hi + 2, (info["iterations"], lo, hi)
+
+
+def _sms():
+    import torch
+    return torch.cuda.get_device_properties(0).multi_processor_count
+
+
+@pytest.mark.parametrize("name,c,bs,fmt", [("C1", 32, 200, "csr"), ("C2", 48, 512, "sell"), ("C3", 24, 300, "csr"),
+                                           ("C6", 12, 400, "sell")])
+def test_bicgstab_ilu_fem_parity(pcg, name, c, bs, fmt):
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    M = _matrix(pcg, A, fmt)
+    x, info = M.bicgstab(_dev(b), tol=1e-10, block=bs, precond="ilu0")
+    r = O.bicgstab_ilu(A, b, tol=1e-10, block=bs)
+    assert info["status"] == 0 and info["relres_true"] <= 1e-10
+    assert np.linalg.norm(x.cpu().numpy() - r.x) <= 1e-9 * np.linalg.norm(r.x)
+    lo, hi = _oracle_range(A, b, 1e-10, bs)
+    assert lo - 2 <= info["iterations"] <= hi + 2, (info["iterations"], lo, hi)
+
+
+def test_bicgstab_ilu_exact_cases_and_errors(pcg):
+    """Block-diagonal tridiagonal matrix: ILU(0) blocks are exact, one step; host
+    buffers equal device buffers bitwise; permuted handles and distributed handles are
+    rejected; a zero pivot is ZERO_DIAGONAL."""
+    import torch
+    from paper_2201_05413_b200 import PcgError
+    nb, m = 6, 40
+    T = np.diag(np.full(m, 3.0)) - np.diag(np.ones(m - 1), 1) - np.diag(np.full(m - 1, 0.5), -1)
+    D = np.kron(np.eye(nb), T)
+    rp, cols, vals = [0], [], []
+    for i in range(D.shape[0]):
+        nz = np.nonzero(D[i])[0]
+        cols += list(nz)
+        vals += list(D[i, nz])
+        rp.append(len(cols))
+    A = O.Csr(D.shape[0], rp, cols, vals)
+    b = np.arange(1.0, A.n + 1)
+    M = _matrix(pcg, A, "csr")
+    x, info = M.bicgstab(_dev(b), tol=1e-13, block=m, precond="ilu0")
+    assert info["status"] == 0 and info["iterations"] == 1
+    assert np.allclose(x.cpu().numpy(), np.linalg.solve(D, b), rtol=0, atol=1e-11)
+    xh, ih = M.bicgstab(torch.as_tensor(b), tol=1e-13, block=m, precond="ilu0")
+    assert np.array_equal(xh.numpy(), x.cpu().numpy())
+    Ms = _matrix(pcg, O.build_problem("C3", c=24)["A"], "sigma")
+    with pytest.raises(PcgError):
+        Ms.bicgstab(_dev(np.ones(Ms.n)), precond="ilu0")
+    Z = O.Csr(2, [0, 2, 4], [0, 1, 0, 1], [1.0, 1.0, 1.0, 1.0])  # a_22 - a_21 a_12 / a_11 = 0
+    Mz = _matrix(pcg, Z, "csr")
+    with pytest.raises(PcgError) as e:
+        Mz.bicgstab(_dev(np.ones(2)), block=2, precond="ilu0")
+    assert e.value.status == 6  # PCG_ERR_ZERO_DIAGONAL

@@ -313,10 +313,10 @@ def test_d16_column_form_is_bitwise_the_int32_form(pcg, monkeypatch, name, c, fm
     P = O.build_problem(name, c=c, k=2 if name == "C4" else 1)
     A = P["A"]
     monkeypatch.delenv("PCG_NO_D16", raising=False)
+    monkeypatch.setenv("PCG_D16", "1")
     M1 = _matrix(pcg, A, fmt)
-    monkeypatch.setenv("PCG_NO_D16", "1")
+    monkeypatch.delenv("PCG_D16")
     M0 = _matrix(pcg, A, fmt)
-    monkeypatch.delenv("PCG_NO_D16")
     s1, s0 = M1.stats(), M0.stats()
     assert s0["d16_slices"] == 0
     assert s1["d16_slices"] > 0.5 * ((A.n + 31) // 32), s1
@@ -332,3 +332,27 @@ def test_d16_column_form_is_bitwise_the_int32_form(pcg, monkeypatch, name, c, fm
         X1, _ = M1.solve_multi(_dev(P["B"]))
         X0, _ = M0.solve_multi(_dev(P["B"]))
         assert bool((X1 == X0).all())
+
+
+@pytest.mark.parametrize("k", [1, 5, 16])
+def test_windowed_spmm_multi_rhs_parity(pcg, monkeypatch, k):
+    """The multi-RHS SpMM with TMA-staged column windows (pcg.h spmm_windowed): the plan
+    is built for the lattice system, and every column matches the oracle's single-RHS
+    solve within the north_star bars; PCG_SPMM_WIN=0 keeps the register-gather SpMM."""
+    P = O.build_problem("C4", c=40, k=k)
+    A, B = P["A"], P["B"]
+    monkeypatch.delenv("PCG_SPMM_WIN", raising=False)
+    M = _matrix(pcg, A)
+    X, infos = M.solve_multi(_dev(B), tol=1e-10)
+    assert M.stats()["spmm_windowed"] == 1
+    X = X.cpu().numpy()
+    for j in range(k):
+        r = O.pcg(A, B[:, j], tol=1e-10)
+        assert infos[j]["status"] == 0 and infos[j]["relres_true"] <= 1e-10
+        assert np.linalg.norm(X[:, j] - r.x) / np.linalg.norm(r.x) <= 1e-9
+        assert abs(infos[j]["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
+    monkeypatch.setenv("PCG_SPMM_WIN", "0")
+    M0 = _matrix(pcg, A)
+    X0, infos0 = M0.solve_multi(_dev(B), tol=1e-10)
+    assert M0.stats()["spmm_windowed"] == -1
+    assert np.linalg.norm(X0.cpu().numpy() - X) <= 1e-9 * np.linalg.norm(X)
