@@ -285,7 +285,11 @@ def main():
     ap.add_argument("--comm", default="nccl", choices=["nccl", "callbacks"],
                     help="callbacks: exchange steps through host callbacks over gloo (validation of the N>1 "
                          "path when ranks share a GPU; not a performance number)")
-    ap.add_argument("--block", type=int, default=1, help="Block-Jacobi block size for the CUBE* BiCGSTAB configs")
+    ap.add_argument("--block", type=int, default=1, help="Block-Jacobi block size for the CUBE* BiCGSTAB configs "
+                    "(--precond ilu0: rows per ILU(0) block, 0 = one block per SM)")
+    ap.add_argument("--precond", default="bj", choices=["bj", "ilu0"],
+                    help="CUBE* BiCGSTAB: Block-Jacobi with dense LU blocks (bj) or ILU(0) blocks (ilu0, the "
+                         "paper's PETSc default sub-solver)")
     ap.add_argument("--solver", default="pcg", choices=["pcg", "pipelined", "block"],
                     help="Jacobi-PCG (the benchmark), the pipelined variant (single RHS) or block CG (k RHS), "
                          "both SURVEY N3")
@@ -692,7 +696,8 @@ def run_bicgstab(args):
     if world == 1:
         r0, r1 = 0, n
         G = fd_cube_build(N)
-        A = pcg.Matrix.from_csr(G["row_ptr"], G["col"], G["val"], fmt=args.fmt)
+        fmt = "sell" if (args.precond == "ilu0" and args.fmt == "auto") else args.fmt  # ILU(0): caller's order
+        A = pcg.Matrix.from_csr(G["row_ptr"], G["col"], G["val"], fmt=fmt)
         nnz = G["col"].numel()
     else:  # the partition rule on the full row pointer, then this rank's rows on its GPU
         rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
@@ -711,7 +716,7 @@ def run_bicgstab(args):
     torch.cuda.synchronize()
     setup = time.perf_counter() - t0
     for _ in range(args.warmup):
-        A.bicgstab(b, tol=tol, block=bs)
+        A.bicgstab(b, tol=tol, block=bs, precond=args.precond)
 
     def barrier():
         if world > 1:
@@ -737,7 +742,7 @@ def run_bicgstab(args):
             e0.record(st)
             for _ in range(args.steps):
                 xx.zero_()
-                x, inf = A.bicgstab(bb, tol=tol, block=bs, out=xx)
+                x, inf = A.bicgstab(bb, tol=tol, block=bs, out=xx, precond=args.precond)
                 infos.append(inf)
             e1.record(st)
             barrier()
@@ -772,12 +777,16 @@ def run_bicgstab(args):
         dist.destroy_process_group()
     if rank != 0:
         return 0
+    if args.precond == "ilu0":
+        pc_desc = f"Block-Jacobi ILU(0), {(bs if bs > 0 else -(-n // torch.cuda.get_device_properties(local).multi_processor_count))} rows per block"
+    else:
+        pc_desc = "Jacobi" if bs == 1 else f"Block-Jacobi({bs})"
     line = {"metric": "bicgstab_time_to_solution", "value": ms / 1e3, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: paper Table 1 grid, {N}^3 nodes, identity boundary rows, "
                                    f"b = x^2 - y^2 on the boundary; BiCGSTAB + "
-                                   f"{'Jacobi' if bs == 1 else f'Block-Jacobi({bs})'}, eps = 1e-12, x0 = 0",
+                                   f"{pc_desc}, eps = 1e-12, x0 = 0",
                        "n": n, "nnz": nnz, "tol": tol, "block": bs, "iterations": iters, "relres_true": inf["relres_true"],
                        "x_err": x_err, "format": {1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[A_fmt],
                        "setup_s": round(setup, 3),

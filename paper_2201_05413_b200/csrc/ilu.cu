@@ -12,7 +12,7 @@
 // its level is one more than the largest level it depends on, and the rows of one
 // level are independent.  One CTA per block walks the levels in order with a block
 // barrier between them; the block's vector lives in shared memory when it fits (bs
-// <= 24K rows), so a level costs a CTA barrier and shared-memory reads, not a
+// <= 22K rows), so a level costs a CTA barrier and shared-memory reads, not a
 // grid-wide synchronisation.  The level analysis (a graph traversal, setup only) runs
 // on the host; it lays the factor out level by level in an ELL form ([level][entry
 // u][row slot]: a level's loads are coalesced): per slot the local row, per (u, slot)
@@ -36,7 +36,9 @@ struct IluLevel {
 // levels of each block, lo[nblk+1 .. 2 nblk+1] the backward ones.
 struct IluPlan {
   int64_t bs = 0, nblk = 0, n = 0;
-  size_t smem = 0;       // dynamic shared memory of the apply kernel (0: vector in global memory)
+  size_t smem = 0;       // dynamic shared memory of the apply kernel (level records + the vector)
+  bool vec_smem = false; // the block's vector in shared memory (bs <= ILU_SMEM_ROWS)
+  int cmax = 4;          // entries per row and direction the apply kernel is compiled for
   double *f = nullptr;   // factor values in CSR order (nnz)
   int *diag = nullptr;   // CSR index of a_ii per row
   IluLevel *lev = nullptr;
@@ -128,41 +130,104 @@ struct IluView {
   const double *fv, *ud;
 };
 
-template <bool SMEM>
-__device__ __forceinline__ void ilu_sweep(const IluView &P, const int *lo, int64_t b, const double *vin, double *y,
-                                          bool backward) {
-  for (int l = lo[b]; l < lo[b + 1]; l++) {
-    const IluLevel L = P.lev[l];
-    for (int t = threadIdx.x; t < L.m; t += blockDim.x) {
-      const int64_t s = L.row_base + t;
-      const int i = P.row[s];
-      double acc = backward ? y[i] : vin[i];
-      for (int u = 0; u < L.c; u++) {
+// One direction's levels of block b.  Level records come from shared memory (copied
+// at kernel entry) when the block has at most ILU_LEVS of them.  Every thread owns slot
+// t of each level (levels wider than the CTA loop over the extra slots); the loads of
+// level l + 1 that do not depend on y (its row, u_ii, input value, columns and factor
+// values) are issued before level l computes and synchronises, so a level costs a CTA
+// barrier plus shared-memory reads, not a chain of global-memory round trips.
+constexpr int ILU_LEVS = 2048;
+struct IluSlot {
+  int i;
+  double v, d;
+};
+
+template <int CMAX>
+__device__ __forceinline__ void ilu_load(const IluView &P, const IluLevel &L, int t, const double *vin, bool backward,
+                                         IluSlot &sl, int (&k)[CMAX], double (&f)[CMAX]) {
+  sl.i = -1;
+  if (t < L.m) {
+    const int64_t s = L.row_base + t;
+    sl.i = __ldg(P.row + s);
+    sl.d = backward ? __ldg(P.ud + s) : 1.0;
+    sl.v = backward ? 0.0 : __ldg(vin + sl.i);
+#pragma unroll
+    for (int u = 0; u < CMAX; u++) {
+      k[u] = -1;
+      if (u < L.c) {
         const int64_t e = L.ent_base + (int64_t)u * L.m + t;
-        const int k = P.kcol[e];
-        if (k >= 0) acc = __dsub_rn(acc, __dmul_rn(P.fv[e], y[k]));
+        k[u] = __ldg(P.kcol + e);
+        f[u] = __ldg(P.fv + e);
       }
-      y[i] = backward ? __ddiv_rn(acc, P.ud[s]) : acc;
     }
-    __syncthreads();
   }
 }
 
-template <bool SMEM>
+template <int CMAX>
+__device__ __forceinline__ void ilu_row(const IluSlot &sl, const int (&k)[CMAX], const double (&f)[CMAX], double *y,
+                                        bool backward) {
+  if (sl.i < 0) return;
+  double acc = backward ? y[sl.i] : sl.v;
+#pragma unroll
+  for (int u = 0; u < CMAX; u++)
+    if (k[u] >= 0) acc = __dsub_rn(acc, __dmul_rn(f[u], y[k[u]]));
+  y[sl.i] = backward ? __ddiv_rn(acc, sl.d) : acc;
+}
+
+template <int CMAX>
+__device__ __forceinline__ void ilu_sweep(const IluView &P, const IluLevel *lv, int nl, const double *vin, double *y,
+                                          bool backward) {
+  const int t = threadIdx.x;
+  IluSlot cur, nxt;
+  int kc[CMAX], kn[CMAX];
+  double fc[CMAX], fn[CMAX];
+  if (nl > 0) ilu_load<CMAX>(P, lv[0], t, vin, backward, cur, kc, fc);
+  for (int l = 0; l < nl; l++) {
+    const IluLevel L = lv[l];
+    if (l + 1 < nl) ilu_load<CMAX>(P, lv[l + 1], t, vin, backward, nxt, kn, fn);
+    ilu_row<CMAX>(cur, kc, fc, y, backward);
+    for (int t2 = t + blockDim.x; t2 < L.m; t2 += blockDim.x) {  // levels wider than the CTA
+      IluSlot sx;
+      int kx[CMAX];
+      double fx[CMAX];
+      ilu_load<CMAX>(P, L, t2, vin, backward, sx, kx, fx);
+      ilu_row<CMAX>(sx, kx, fx, y, backward);
+    }
+    __syncthreads();
+    cur = nxt;
+#pragma unroll
+    for (int u = 0; u < CMAX; u++) {
+      kc[u] = kn[u];
+      fc[u] = fn[u];
+    }
+  }
+}
+
+template <bool SMEM, int CMAX>
 __global__ void __launch_bounds__(256) ilu_apply_kernel(IluView P, const double *__restrict__ in, double *out,
                                                         const int *stop, const int *skip) {
-  extern __shared__ double ys[];
+  extern __shared__ __align__(16) unsigned char ilu_smem[];
   if ((stop && *(volatile const int *)stop) || (skip && *(volatile const int *)skip)) return;
   const int64_t b = blockIdx.x, r0 = b * P.bs, nr = min(P.bs, P.n - r0);
-  double *y = SMEM ? ys : out + r0;
-  ilu_sweep<SMEM>(P, P.lo, b, in + r0, y, false);
-  ilu_sweep<SMEM>(P, P.lo + P.nblk + 1, b, in + r0, y, true);
+  IluLevel *slev = reinterpret_cast<IluLevel *>(ilu_smem);
+  double *y = SMEM ? reinterpret_cast<double *>(ilu_smem + sizeof(IluLevel) * ILU_LEVS) : out + r0;
+  const int f0 = P.lo[b], f1 = P.lo[b + 1], b0 = P.lo[P.nblk + 1 + b], b1 = P.lo[P.nblk + 1 + b + 1];
+  const bool lev_smem = (f1 - f0) + (b1 - b0) <= ILU_LEVS;
+  if (lev_smem) {
+    for (int q = threadIdx.x; q < f1 - f0; q += blockDim.x) slev[q] = P.lev[f0 + q];
+    for (int q = threadIdx.x; q < b1 - b0; q += blockDim.x) slev[(f1 - f0) + q] = P.lev[b0 + q];
+    __syncthreads();
+  }
+  const IluLevel *lf = lev_smem ? slev : P.lev + f0;
+  const IluLevel *lb = lev_smem ? slev + (f1 - f0) : P.lev + b0;
+  ilu_sweep<CMAX>(P, lf, f1 - f0, in + r0, y, false);
+  ilu_sweep<CMAX>(P, lb, b1 - b0, in + r0, y, true);
   if (SMEM)
     for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) out[r0 + i] = y[i];
 }
 
 constexpr int ILU_THREADS = 256;
-constexpr int64_t ILU_SMEM_ROWS = 24576;  // 192 KB of fp64 per CTA
+constexpr int64_t ILU_SMEM_ROWS = 22528;  // 176 KB of fp64 per CTA (+ 48 KB of level records)
 
 // ---------------------------------------------------------------- setup
 pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out) {
@@ -289,9 +354,16 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
   cudaFree(err);
   if (herr) return bail(fail(PCG_ERR_ZERO_DIAGONAL, "pcg_bicgstab_ilu: zero pivot in the ILU(0) factorization"));
   const int64_t maxrows = std::min(bs, n);
-  P->smem = maxrows <= ILU_SMEM_ROWS ? sizeof(double) * (size_t)maxrows : 0;
-  if (P->smem > 48 * 1024)
-    PCG_CUDA(cudaFuncSetAttribute(ilu_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem));
+  P->vec_smem = maxrows <= ILU_SMEM_ROWS;
+  P->smem = sizeof(IluLevel) * ILU_LEVS + (P->vec_smem ? sizeof(double) * (size_t)maxrows : 0);
+  int cmax = 0;
+  for (const IluLevel &L : levs) cmax = std::max(cmax, L.c);
+  P->cmax = cmax <= 4 ? 4 : cmax <= 8 ? 8 : 16;
+  if (cmax > 16) return bail(fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab_ilu: rows with more than 16 entries per triangle"));
+  for (auto fn : {(const void *)ilu_apply_kernel<true, 4>, (const void *)ilu_apply_kernel<true, 8>,
+                  (const void *)ilu_apply_kernel<true, 16>, (const void *)ilu_apply_kernel<false, 4>,
+                  (const void *)ilu_apply_kernel<false, 8>, (const void *)ilu_apply_kernel<false, 16>})
+    PCG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem));
   // algorithmic bytes of one application: v in + y out (16 n), the level-ordered factor
   // (8 + 4 B per stored entry, incl. ELL padding) and slots (row 4 B, u_ii 8 B)
   P->bytes_per_apply = 16.0 * n + 12.0 * P->nent + 12.0 * P->nslot + sizeof(IluLevel) * P->nlev;
@@ -302,10 +374,18 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
 void ilu_launch(void *plan, const double *in, double *out, const int *stop, const int *skip, cudaStream_t st) {
   const IluPlan *P = (const IluPlan *)plan;
   const IluView V{P->bs, P->n, P->nblk, P->lev, P->lo, P->row, P->kcol, P->fv, P->ud};
-  if (P->smem)
-    ilu_apply_kernel<true><<<(unsigned)P->nblk, ILU_THREADS, P->smem, st>>>(V, in, out, stop, skip);
-  else
-    ilu_apply_kernel<false><<<(unsigned)P->nblk, ILU_THREADS, 0, st>>>(V, in, out, stop, skip);
+  const unsigned g = (unsigned)P->nblk;
+#define ILU_GO(SM, CM) ilu_apply_kernel<SM, CM><<<g, ILU_THREADS, P->smem, st>>>(V, in, out, stop, skip)
+  if (P->vec_smem) {
+    if (P->cmax == 4) ILU_GO(true, 4);
+    else if (P->cmax == 8) ILU_GO(true, 8);
+    else ILU_GO(true, 16);
+  } else {
+    if (P->cmax == 4) ILU_GO(false, 4);
+    else if (P->cmax == 8) ILU_GO(false, 8);
+    else ILU_GO(false, 16);
+  }
+#undef ILU_GO
   count_launch();
 }
 

@@ -43,11 +43,12 @@ def _oracle_range(A, b, tol, bs):
     return min(its), max(its)
 
 
-@pytest.mark.parametrize("N,bs", [(16, 4096), (16, 256), (24, 576), (24, 1000), (32, 0), (20, 1)])
-def test_bicgstab_ilu_table1_parity(pcg, N, bs):
+@pytest.mark.parametrize("N,bs,fmt", [(16, 4096, "sell"), (16, 256, "csr"), (24, 576, "sell"), (24, 1000, "csr"),
+                                      (32, 0, "sell"), (20, 1, "sell")])
+def test_bicgstab_ilu_table1_parity(pcg, N, bs, fmt):
     A, b = O.fd_cube(N)
     tol = 1e-12
-    M = _matrix(pcg, A)
+    M = _matrix(pcg, A, fmt)
     x, info = M.bicgstab(_dev(b), tol=tol, block=bs, precond="ilu0")
     bs_eff = bs if bs > 0 else -(-A.n // _sms())
     r = O.bicgstab_ilu(A, b, tol=tol, block=bs_eff)
