@@ -136,7 +136,16 @@ struct IluView {
 // level l + 1 that do not depend on y (its row, u_ii, input value, columns and factor
 // values) are issued before level l computes and synchronises, so a level costs a CTA
 // barrier plus shared-memory reads, not a chain of global-memory round trips.
-constexpr int ILU_LEVS = 2048;
+constexpr int ILU_LEVS = 1024;
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+constexpr int ILU_PF = 6;  // levels of L2 prefetch ahead (register-prefetch sweep)
+
+__device__ __forceinline__ void prefetch_range(const void *p, size_t bytes) {
+  if (bytes == 0) return;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t b = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(b - a)) : "memory");
+}
 struct IluSlot {
   int i;
   double v, d;
@@ -150,7 +159,7 @@ __device__ __forceinline__ void ilu_load(const IluView &P, const IluLevel &L, in
     const int64_t s = L.row_base + t;
     sl.i = __ldg(P.row + s);
     sl.d = backward ? __ldg(P.ud + s) : 1.0;
-    sl.v = backward ? 0.0 : __ldg(vin + sl.i);
+    sl.v = 0.0;  // the input vector is in y already (copied at kernel entry)
 #pragma unroll
     for (int u = 0; u < CMAX; u++) {
       k[u] = -1;
@@ -167,7 +176,7 @@ template <int CMAX>
 __device__ __forceinline__ void ilu_row(const IluSlot &sl, const int (&k)[CMAX], const double (&f)[CMAX], double *y,
                                         bool backward) {
   if (sl.i < 0) return;
-  double acc = backward ? y[sl.i] : sl.v;
+  double acc = y[sl.i];  // forward: v_i (y was initialised with v); backward: the forward result
 #pragma unroll
   for (int u = 0; u < CMAX; u++)
     if (k[u] >= 0) acc = __dsub_rn(acc, __dmul_rn(f[u], y[k[u]]));
@@ -184,6 +193,13 @@ __device__ __forceinline__ void ilu_sweep(const IluView &P, const IluLevel *lv, 
   if (nl > 0) ilu_load<CMAX>(P, lv[0], t, vin, backward, cur, kc, fc);
   for (int l = 0; l < nl; l++) {
     const IluLevel L = lv[l];
+    if (t == 0 && l + ILU_PF < nl) {  // level l + ILU_PF toward L2: the register prefetch then hits L2
+      const IluLevel F = lv[l + ILU_PF];
+      prefetch_range(P.row + F.row_base, (size_t)F.m * 4);
+      if (backward) prefetch_range(P.ud + F.row_base, (size_t)F.m * 8);
+      prefetch_range(P.kcol + F.ent_base, (size_t)F.m * F.c * 4);
+      prefetch_range(P.fv + F.ent_base, (size_t)F.m * F.c * 8);
+    }
     if (l + 1 < nl) ilu_load<CMAX>(P, lv[l + 1], t, vin, backward, nxt, kn, fn);
     ilu_row<CMAX>(cur, kc, fc, y, backward);
     for (int t2 = t + blockDim.x; t2 < L.m; t2 += blockDim.x) {  // levels wider than the CTA
@@ -203,6 +219,87 @@ __device__ __forceinline__ void ilu_sweep(const IluView &P, const IluLevel *lv, 
   }
 }
 
+// The same sweep with the y-independent slot data of the next ILU_RING - 1 levels in
+// flight through shared memory (cp.async, one commit group per level, a ring of
+// ILU_RING level slots): each thread copies and later reads only its own slot's data,
+// so the ring needs no barrier of its own, and the level barrier orders the y traffic.
+constexpr int ILU_RING = 4;
+template <int CMAX>
+struct IluRing {
+  int row[ILU_RING][256];
+  double ud[ILU_RING][256];
+  int k[ILU_RING][CMAX][256];
+  double f[ILU_RING][CMAX][256];
+};
+
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int CMAX>
+__device__ __forceinline__ void ilu_sweep_ring(const IluView &P, const IluLevel *lv, int nl, double *y, bool backward,
+                                               IluRing<CMAX> &R) {
+  const int t = threadIdx.x;
+  auto issue = [&](int l) {
+    if (l < nl) {
+      const IluLevel L = lv[l];
+      const int q = l % ILU_RING;
+      if (t < L.m) {
+        const int64_t s = L.row_base + t;
+        cp_async4(&R.row[q][t], P.row + s);
+        if (backward) cp_async8(&R.ud[q][t], P.ud + s);
+        for (int u = 0; u < L.c; u++) {
+          const int64_t e = L.ent_base + (int64_t)u * L.m + t;
+          cp_async4(&R.k[q][u][t], P.kcol + e);
+          cp_async8(&R.f[q][u][t], P.fv + e);
+        }
+      }
+    }
+    cp_async_commit();  // one group per level (empty past the end): the wait counts stay uniform
+  };
+  for (int l = 0; l < ILU_RING - 1; l++) issue(l);
+  for (int l = 0; l < nl; l++) {
+    // (an L2 bulk prefetch of level l + 12 by thread 0 here measured slower: 0.165 vs 0.131 s on
+    // Cube 1 — thread 0 sits on every level's critical path)
+    issue(l + ILU_RING - 1);
+    cp_async_wait<ILU_RING - 1>();  // this thread's copies for level l have landed
+    const IluLevel L = lv[l];
+    const int q = l % ILU_RING;
+    if (t < L.m) {
+      const int i = R.row[q][t];
+      double acc = y[i];
+      for (int u = 0; u < L.c; u++) {
+        const int k = R.k[q][u][t];
+        if (k >= 0) acc = __dsub_rn(acc, __dmul_rn(R.f[q][u][t], y[k]));
+      }
+      y[i] = backward ? __ddiv_rn(acc, R.ud[q][t]) : acc;
+    }
+    for (int t2 = t + blockDim.x; t2 < L.m; t2 += blockDim.x) {  // levels wider than the CTA
+      IluSlot sx;
+      int kx[CMAX];
+      double fx[CMAX];
+      ilu_load<CMAX>(P, L, t2, nullptr, backward, sx, kx, fx);
+      ilu_row<CMAX>(sx, kx, fx, y, backward);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+// shared memory: [level records][the cp.async ring (CMAX <= 8)][the block's vector]
+__host__ __device__ constexpr size_t ilu_vec_offset(int cmax) {
+  return sizeof(IluLevel) * ILU_LEVS +
+         (cmax <= 4 ? sizeof(IluRing<4>) : cmax <= 8 ? sizeof(IluRing<8>) : 0);
+}
+
 template <bool SMEM, int CMAX>
 __global__ void __launch_bounds__(256) ilu_apply_kernel(IluView P, const double *__restrict__ in, double *out,
                                                         const int *stop, const int *skip) {
@@ -210,7 +307,7 @@ __global__ void __launch_bounds__(256) ilu_apply_kernel(IluView P, const double 
   if ((stop && *(volatile const int *)stop) || (skip && *(volatile const int *)skip)) return;
   const int64_t b = blockIdx.x, r0 = b * P.bs, nr = min(P.bs, P.n - r0);
   IluLevel *slev = reinterpret_cast<IluLevel *>(ilu_smem);
-  double *y = SMEM ? reinterpret_cast<double *>(ilu_smem + sizeof(IluLevel) * ILU_LEVS) : out + r0;
+  double *y = SMEM ? reinterpret_cast<double *>(ilu_smem + ilu_vec_offset(CMAX)) : out + r0;
   const int f0 = P.lo[b], f1 = P.lo[b + 1], b0 = P.lo[P.nblk + 1 + b], b1 = P.lo[P.nblk + 1 + b + 1];
   const bool lev_smem = (f1 - f0) + (b1 - b0) <= ILU_LEVS;
   if (lev_smem) {
@@ -218,16 +315,24 @@ __global__ void __launch_bounds__(256) ilu_apply_kernel(IluView P, const double 
     for (int q = threadIdx.x; q < b1 - b0; q += blockDim.x) slev[(f1 - f0) + q] = P.lev[b0 + q];
     __syncthreads();
   }
+  for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) y[i] = in[r0 + i];  // coalesced; the sweeps work in place
+  __syncthreads();
   const IluLevel *lf = lev_smem ? slev : P.lev + f0;
   const IluLevel *lb = lev_smem ? slev + (f1 - f0) : P.lev + b0;
-  ilu_sweep<CMAX>(P, lf, f1 - f0, in + r0, y, false);
-  ilu_sweep<CMAX>(P, lb, b1 - b0, in + r0, y, true);
+  if (CMAX <= 8) {
+    IluRing<CMAX> &R = *reinterpret_cast<IluRing<CMAX> *>(ilu_smem + sizeof(IluLevel) * ILU_LEVS);
+    ilu_sweep_ring<CMAX>(P, lf, f1 - f0, y, false, R);
+    ilu_sweep_ring<CMAX>(P, lb, b1 - b0, y, true, R);
+  } else {
+    ilu_sweep<CMAX>(P, lf, f1 - f0, in + r0, y, false);
+    ilu_sweep<CMAX>(P, lb, b1 - b0, in + r0, y, true);
+  }
   if (SMEM)
     for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) out[r0 + i] = y[i];
 }
 
 constexpr int ILU_THREADS = 256;
-constexpr int64_t ILU_SMEM_ROWS = 22528;  // 176 KB of fp64 per CTA (+ 48 KB of level records)
+constexpr size_t ILU_SMEM_MAX = 227 * 1024;  // opt-in shared memory per CTA
 
 // ---------------------------------------------------------------- setup
 pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out) {
@@ -354,12 +459,13 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
   cudaFree(err);
   if (herr) return bail(fail(PCG_ERR_ZERO_DIAGONAL, "pcg_bicgstab_ilu: zero pivot in the ILU(0) factorization"));
   const int64_t maxrows = std::min(bs, n);
-  P->vec_smem = maxrows <= ILU_SMEM_ROWS;
-  P->smem = sizeof(IluLevel) * ILU_LEVS + (P->vec_smem ? sizeof(double) * (size_t)maxrows : 0);
   int cmax = 0;
   for (const IluLevel &L : levs) cmax = std::max(cmax, L.c);
   P->cmax = cmax <= 4 ? 4 : cmax <= 8 ? 8 : 16;
   if (cmax > 16) return bail(fail(PCG_ERR_INVALID_ARG, "pcg_bicgstab_ilu: rows with more than 16 entries per triangle"));
+  const size_t vo = ilu_vec_offset(P->cmax);
+  P->vec_smem = vo + sizeof(double) * (size_t)maxrows <= ILU_SMEM_MAX;
+  P->smem = vo + (P->vec_smem ? sizeof(double) * (size_t)maxrows : 0);
   for (auto fn : {(const void *)ilu_apply_kernel<true, 4>, (const void *)ilu_apply_kernel<true, 8>,
                   (const void *)ilu_apply_kernel<true, 16>, (const void *)ilu_apply_kernel<false, 4>,
                   (const void *)ilu_apply_kernel<false, 8>, (const void *)ilu_apply_kernel<false, 16>})

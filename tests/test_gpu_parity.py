@@ -356,3 +356,41 @@ def test_windowed_spmm_multi_rhs_parity(pcg, monkeypatch, k):
     X0, infos0 = M0.solve_multi(_dev(B), tol=1e-10)
     assert M0.stats()["spmm_windowed"] == -1
     assert np.linalg.norm(X0.cpu().numpy() - X) <= 1e-9 * np.linalg.norm(X)
+
+
+def test_multi_rhs_chunking_and_leading_dimensions(pcg):
+    """pcg.h pcg_solve_multi promises k > 32 (chunked internally by 32 columns) and
+    leading dimensions ldb, ldx > n (column-major, SPEC DenseBlock S:39-42): called
+    through the raw C ABI with k = 37 columns in padded host and device buffers, every
+    column matches its own oracle solve, and the padding rows are left untouched."""
+    import ctypes as C
+    import torch
+    from paper_2201_05413_b200 import _lib
+    P = O.build_problem("C1", c=24)
+    A = P["A"]
+    n, k, ldb, ldx = A.n, 37, A.n + 5, A.n + 11
+    rng = np.random.default_rng(4)
+    B = rng.standard_normal((n, k))
+    Bp = np.full((k, ldb), 7.0)
+    Bp[:, :n] = B.T
+    M = _matrix(pcg, A)
+    for dev in (False, True):
+        Xp = np.full((k, ldx), -3.0)
+        tb = torch.as_tensor(Bp).contiguous()
+        tx = torch.as_tensor(Xp).contiguous()
+        if dev:
+            tb, tx = tb.cuda(), tx.cuda()
+        else:
+            tb, tx = tb.pin_memory(), tx.pin_memory()
+        tx[:, :n] = 0.0
+        infos = (_lib.PcgInfo * k)()
+        st = _lib.lib().pcg_solve_multi(M._h, k, C.c_void_p(tb.data_ptr()), ldb, C.c_void_p(tx.data_ptr()), ldx,
+                                        1e-10, 50000, C.c_void_p(torch.cuda.current_stream().cuda_stream), infos)
+        assert st == 0
+        X = tx.cpu().numpy()
+        assert np.all(X[:, n:] == -3.0)  # padding untouched
+        for j in (0, 1, 31, 32, 36):
+            r = O.pcg(A, B[:, j], tol=1e-10)
+            assert infos[j].status == 0
+            assert np.linalg.norm(X[j, :n] - r.x) / np.linalg.norm(r.x) <= 1e-9
+            assert abs(infos[j].iterations - r.iterations) <= max(1, 0.02 * r.iterations)
