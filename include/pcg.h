@@ -118,8 +118,9 @@ typedef struct {
                                 (10.125 instead of 12 bytes per entry; opt-in, environment
                                 PCG_D16=1 at csr_create: measured no faster) — same ids, so results are
                                 bitwise those of the int32 form */
-  int32_t spmm_windowed;     /* multi-RHS SpMM plan: 1 = column windows staged by TMA (built at the
-                                first pcg_solve_multi), -1 = not applicable, 0 = not built yet */
+  int32_t spmm_windowed;     /* multi-RHS SpMM plan: 1 = column windows staged by TMA (opt-in,
+                                environment PCG_SPMM_WIN=1; built at the first pcg_solve_multi),
+                                -1 = not used, 0 = not decided yet */
   int32_t pad0;
 } pcg_matrix_stats;
 

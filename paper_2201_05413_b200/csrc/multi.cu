@@ -907,8 +907,10 @@ static int win_grid(pcg_matrix *A) {
 // build the window plan once per matrix (SELL-32 with rows of at most 8 entries)
 static pcg_status win_plan(pcg_matrix *A, cudaStream_t st) {
   if (A->wplan != 0) return PCG_OK;
+  // opt-in (PCG_SPMM_WIN=1): measured as fast as the register-gather SpMM, not faster
+  // (the SM's load pipe, not L2, bounds both)
   const char *e = getenv("PCG_SPMM_WIN");
-  if ((e && atoi(e) == 0) || A->max_row_len > 8 || A->n_slices == 0 || A->comm || A->n + 2 > (int64_t(1) << 31)) {
+  if (!(e && atoi(e) == 1) || A->max_row_len > 8 || A->n_slices == 0 || A->comm || A->n + 2 > (int64_t(1) << 31)) {
     A->wplan = -1;
     return PCG_OK;
   }

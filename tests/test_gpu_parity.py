@@ -337,11 +337,12 @@ def test_d16_column_form_is_bitwise_the_int32_form(pcg, monkeypatch, name, c, fm
 @pytest.mark.parametrize("k", [1, 5, 16])
 def test_windowed_spmm_multi_rhs_parity(pcg, monkeypatch, k):
     """The multi-RHS SpMM with TMA-staged column windows (pcg.h spmm_windowed): the plan
-    is built for the lattice system, and every column matches the oracle's single-RHS
-    solve within the north_star bars; PCG_SPMM_WIN=0 keeps the register-gather SpMM."""
+    is built for the lattice system (opt-in, PCG_SPMM_WIN=1), and every column matches the
+    oracle's single-RHS solve within the north_star bars; PCG_SPMM_WIN=0 keeps the
+    register-gather SpMM."""
     P = O.build_problem("C4", c=40, k=k)
     A, B = P["A"], P["B"]
-    monkeypatch.delenv("PCG_SPMM_WIN", raising=False)
+    monkeypatch.setenv("PCG_SPMM_WIN", "1")
     M = _matrix(pcg, A)
     X, infos = M.solve_multi(_dev(B), tol=1e-10)
     assert M.stats()["spmm_windowed"] == 1
