@@ -31,11 +31,20 @@ __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi 
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * WARPS;
-  for (int64_t s = w0; s < A.n_slices; s += nw) {
-    const int64_t base = A.slice_ptr[s];
-    const int len = (int)((A.slice_ptr[s + 1] - base) >> 5);
+  // the next slice's offsets are fetched while this slice's entries are in flight (issued
+  // after them: an SM's loads complete in issue order), so a slice costs two dependent
+  // round trips (entries, gathers) instead of three
+  int64_t s = w0, base = 0, next = 0;
+  if (s < A.n_slices) {
+    base = A.slice_ptr[s];
+    next = A.slice_ptr[s + 1];
+  }
+  for (; s < A.n_slices; s += nw) {
+    const int len = (int)((next - base) >> 5);
     const double *vp = A.val + base + lane;
     const int *cp = A.col + base + lane;
+    const int64_t s2 = s + nw;
+    int64_t base2 = 0, next2 = 0;
     double sum = 0.0;
     for (int t = 0; t < len; t += 8) {
       double a[8];
@@ -47,6 +56,10 @@ __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi 
           j[u] = ld_stream(cp + (size_t)(t + u) * 32);
         }
       }
+      if (t == 0 && s2 < A.n_slices) {
+        base2 = A.slice_ptr[s2];
+        next2 = A.slice_ptr[s2 + 1];
+      }
       cols_ready(j, A.zero);
       double g[8];
 #pragma unroll
@@ -56,8 +69,14 @@ __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi 
       for (int u = 0; u < 8; u++)
         if (t + u < len) sum = __fma_rn(a[u], g[u], sum);
     }
+    if (len == 0 && s2 < A.n_slices) {
+      base2 = A.slice_ptr[s2];
+      next2 = A.slice_ptr[s2 + 1];
+    }
     const int64_t row = s * 32 + lane;
     if (row < A.n) epi(row, sum);
+    base = base2;
+    next = next2;
   }
 }
 
