@@ -258,6 +258,21 @@ pcg_status pcg_comm_destroy(pcg_comm_t comm);
  * pcg_comm_abort aborts on request (e.g. from a caller's own watchdog). */
 pcg_status pcg_comm_set_timeout(pcg_comm_t comm, double seconds);
 pcg_status pcg_comm_abort(pcg_comm_t comm);
+/* Device-initiated allreduce (opt-in, environment PCG_DEVICE_ALLREDUCE=1
+ * at pcg_comm_init on EVERY rank, NCCL communicators of <= 8 ranks on one node): the
+ * scalar reductions of the distributed solvers (sigma; rho', gamma; the BiCGSTAB and
+ * pipelined sums) run as one single-thread kernel each that writes the rank's values
+ * into every peer's mailbox over NVLink (CUDA IPC mappings made at pcg_comm_init) and
+ * sums all ranks' values in rank order — the same bits on every rank — instead of an
+ * ncclAllReduce.  If any rank cannot map its peers, every rank keeps NCCL.  A peer that
+ * stops making progress for ~8 s makes the kernel flag an error that the next host
+ * wait turns into PCG_ERR_NCCL (communicator aborted).  device_allreduce reports
+ * whether it is active.  pcg_dar_emulate: the protocol's self-test on ONE GPU — G <= 8
+ * "ranks" as G co-resident blocks of one cooperative kernel, each with its own mailbox,
+ * `rounds` successive reductions of nv <= 4 values; in/out host arrays of
+ * rounds x G x nv doubles (rank g's input / result of round r at [(r G + g) nv]). */
+pcg_status pcg_comm_get_info(pcg_comm_t comm, int32_t *rank, int32_t *size, int32_t *device_allreduce);
+pcg_status pcg_dar_emulate(int32_t G, int32_t rounds, int32_t nv, const double *in, double *out);
 
 /* Host-callback communicator: the same distributed path (csr_create_dist, pcg_solve,
  * pcg_spmv) with every exchange step done by caller-supplied host functions instead of

@@ -377,6 +377,11 @@ class Comm:
         PcgError(PCG_ERR_NCCL) instead of blocking."""
         check(lib().pcg_comm_set_timeout(self._h, float(seconds)), "pcg_comm_set_timeout")
 
+    def info(self) -> dict:
+        r, n, d = C.c_int32(), C.c_int32(), C.c_int32()
+        check(lib().pcg_comm_get_info(self._h, C.byref(r), C.byref(n), C.byref(d)), "pcg_comm_get_info")
+        return {"rank": r.value, "size": n.value, "device_allreduce": bool(d.value)}
+
     def abort(self):
         """ncclCommAbort: pending and later calls on this communicator fail with PCG_ERR_NCCL."""
         check(lib().pcg_comm_abort(self._h), "pcg_comm_abort")

@@ -101,6 +101,8 @@ def lib():
         "pcg_comm_destroy": [vp],
         "pcg_comm_abort": [vp],
         "pcg_comm_set_timeout": [vp, dbl],
+        "pcg_comm_get_info": [vp, P(i32), P(i32), P(i32)],
+        "pcg_dar_emulate": [i32, i32, i32, vp, vp],
         "csr_create_dist": [vp, i64, i64, i64, i64, vp, vp, vp, C.c_int, vp, P(vp)],
         "pcg_profile_kernels": [vp, vp, i32, vp, vp, P(i32)],
         "pcg_profile_multi": [vp, i32, vp, i64, i32, vp, vp, P(i32)],

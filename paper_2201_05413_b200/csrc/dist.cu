@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -98,6 +99,8 @@ pcg_status comm_wait(pcg_comm *C, cudaStream_t st) {
   const auto t0 = std::chrono::steady_clock::now();
   for (int poll = 0;; poll++) {
     const cudaError_t q = cudaEventQuery(C->wait_ev);
+    if (C->dar && dar_failed(C->dar))  // a device allreduce saw no peer progress for ~8 s
+      return abort_comm(C, "device allreduce: a peer stopped making progress");
     if (q == cudaSuccess) return PCG_OK;
     if (q != cudaErrorNotReady) {
       cudaGetLastError();
@@ -132,6 +135,7 @@ static pcg_status comm_allreduce_f64(pcg_comm *C, double *dbuf, int count, cudaS
   // a 1-rank NCCL communicator still issues the (trivial) collective: it keeps the
   // captured-graph + NCCL path testable on one GPU
   if (count == 0 || (C->use_ops && C->size == 1)) return PCG_OK;
+  if (!C->use_ops && C->dar) return dar_allreduce(C->dar, dbuf, count, st);  // opt-in, dar.cu
   if (!C->use_ops) {
     PCG_NCCL(ncclAllReduce(dbuf, dbuf, (size_t)count, ncclDouble, ncclSum, C->nccl, st));
     return PCG_OK;
@@ -540,6 +544,16 @@ extern "C" pcg_status pcg_comm_init(int32_t rank, int32_t size, const void *id12
     delete c;
     return fail(PCG_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   }
+  if (const char *e = getenv("PCG_DEVICE_ALLREDUCE")) {  // collective: every rank must set it alike
+    if (atoi(e) == 1) {
+      pcg_status s = dar_setup(c->nccl, rank, size, &c->dar);
+      if (s != PCG_OK) {
+        ncclCommDestroy(c->nccl);
+        delete c;
+        return s;
+      }
+    }
+  }
   *out = c;
   return PCG_OK;
 }
@@ -561,6 +575,7 @@ extern "C" pcg_status pcg_comm_destroy(pcg_comm_t c) {
   if (!c) return PCG_OK;
   if (c->nccl) ncclCommDestroy(c->nccl);
   if (c->wait_ev) cudaEventDestroy(c->wait_ev);
+  if (c->dar) dar_free(c->dar);
   delete c;
   return PCG_OK;
 }
@@ -572,6 +587,14 @@ extern "C" pcg_status pcg_comm_abort(pcg_comm_t c) {
     return PCG_OK;
   }
   if (!c->aborted) (void)abort_comm(c, "pcg_comm_abort");
+  return PCG_OK;
+}
+
+extern "C" pcg_status pcg_comm_get_info(pcg_comm_t c, int32_t *rank, int32_t *size, int32_t *device_allreduce) {
+  if (!c) return fail(PCG_ERR_INVALID_ARG, "pcg_comm_get_info: null communicator");
+  if (rank) *rank = c->rank;
+  if (size) *size = c->size;
+  if (device_allreduce) *device_allreduce = c->dar != nullptr;
   return PCG_OK;
 }
 

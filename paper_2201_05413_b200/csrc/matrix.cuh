@@ -17,10 +17,15 @@ struct pcg_comm {
   double timeout_s = 300.0;
   bool aborted = false;
   cudaEvent_t wait_ev = nullptr;
+  void *dar = nullptr;  // device-initiated allreduce over NVLink peer memory (dar.cu), opt-in
 };
 
 namespace pcgb {
 
+pcg_status dar_setup(ncclComm_t nccl, int rank, int size, void **out);
+pcg_status dar_allreduce(void *dar, double *buf, int count, cudaStream_t st);
+bool dar_failed(const void *dar);
+void dar_free(void *dar);
 pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out);
 void ilu_launch(void *plan, const double *in, double *out, const int *stop, const int *skip, cudaStream_t st);
 void ilu_free(void *plan);

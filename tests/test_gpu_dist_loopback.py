@@ -350,3 +350,69 @@ def test_nccl_failure_detection_aborts_instead_of_blocking():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("G,nv", [(1, 1), (2, 3), (3, 2), (8, 3)])
+def test_device_allreduce_protocol_emulated(G, nv):
+    """The device-initiated allreduce's protocol (csrc/dar.cu) with G
+    ranks played by G co-resident blocks of one cooperative kernel, each with its own
+    mailbox, over 64 successive rounds: every rank's result equals the rank-order sum
+    of all ranks' inputs, bitwise, and all ranks agree (the parity-alternating mailbox
+    slots and monotonic flags survive back-to-back rounds)."""
+    import ctypes as C
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2201_05413_b200 import _lib
+    rounds = 64
+    rng = np.random.default_rng(G * 10 + nv)
+    x = rng.standard_normal((rounds, G, nv)) * 10.0 ** rng.integers(-8, 8, (rounds, G, nv))
+    out = np.zeros_like(x)
+    st = _lib.lib().pcg_dar_emulate(G, rounds, nv, x.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p))
+    assert st == 0
+    for r in range(rounds):
+        for v in range(nv):
+            s = 0.0
+            for g in range(G):
+                s += x[r, g, v]
+            for g in range(G):
+                assert out[r, g, v] == s, (r, g, v)
+
+
+def test_device_allreduce_single_rank_nccl_solves(monkeypatch):
+    """PCG_DEVICE_ALLREDUCE=1 on a 1-rank NCCL communicator: the mailbox is set up, the
+    distributed PCG, pipelined PCG and BiCGSTAB loops run their scalar reductions
+    through the device kernel (captured in the iteration graphs) and match the oracle."""
+    import torch
+    import torch.distributed as dist
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_05413_b200 as pcg
+    monkeypatch.setenv("PCG_DEVICE_ALLREDUCE", "1")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        P = O.build_problem("C2", c=48, k=1)
+        A, b = P["A"], P["B"][:, 0]
+        comm = pcg.Comm.from_process_group()
+        assert comm.info()["device_allreduce"]
+        M = pcg.Matrix.from_csr_dist(comm, A.n, 0, A.n, torch.as_tensor(A.row_ptr).cuda(),
+                                     torch.as_tensor(A.col).cuda(), torch.as_tensor(A.val).cuda())
+        x, info = M.solve(torch.as_tensor(b).cuda(), tol=1e-10)
+        r = O.pcg(A, b, tol=1e-10)
+        assert info["status"] == 0 and info["relres_true"] <= 1e-10
+        assert np.linalg.norm(x.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-9
+        assert abs(info["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
+        xp, ip = M.solve_pipelined(torch.as_tensor(b).cuda(), tol=1e-10)
+        assert ip["status"] == 0 and np.linalg.norm(xp.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-8
+        M.close()
+        Af, bf = O.fd_cube(16)
+        Mf = pcg.Matrix.from_csr_dist(comm, Af.n, 0, Af.n, torch.as_tensor(Af.row_ptr).cuda(),
+                                      torch.as_tensor(Af.col).cuda(), torch.as_tensor(Af.val).cuda())
+        xb, ib = Mf.bicgstab(torch.as_tensor(bf).cuda(), tol=1e-12)
+        rb = O.bicgstab(Af, bf, tol=1e-12)
+        assert ib["status"] == 0 and np.linalg.norm(xb.cpu().numpy() - rb.x) <= 1e-9 * np.linalg.norm(rb.x)
+        Mf.close()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
