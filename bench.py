@@ -514,7 +514,7 @@ def main():
         dom = max(kern, key=lambda d: d["us_per_launch"])
         it_us = sum(us)
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "r01", "traffic_c5.json")
+        tp = os.path.join(ROOT, "profiles", "r02", "traffic_c5.json")
         if args.config == "C5" and c == 512 and stats["schedule"] == 3 and stats["format"] == 2 and os.path.exists(tp):
             with open(tp) as fh:
                 tk = json.load(fh)["kernels"]
@@ -522,7 +522,7 @@ def main():
             traffic = tk.get(key, {}).get("traffic_bytes")
         roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved_GBps"], "peak": hbm,
                 "unit": "GB/s", "frac": dom["achieved_GBps"] / hbm, "peak_source": peak_kind, "traffic": traffic,
-                "traffic_source": "profiles/r01/traffic_c5.json (ncu --set full, dram read+write per launch)"
+                "traffic_source": "profiles/r02/traffic_c5.json (ncu --set full, dram read+write per launch)"
                 if traffic else None,
                 "bytes_per_launch": dom["bytes_per_launch"], "us_per_launch": dom["us_per_launch"],
                 "kernels": kern, "schedule": stats["schedule"],
