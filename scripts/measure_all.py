@@ -62,7 +62,7 @@ for name in names:
     row = {"config": name, "n": n, "nnz": nnz, "k": k, "time_s": t, "iterations": its,
            "relres_true_max": max(i["relres_true"] for i in infos), "spmv_GBps": spmv_gbs,
            "spmv_frac": spmv_gbs / peak, "iteration_frac_96kn": frac, "format": A.stats()["format"]}
-    g = gold.get(name)
+    g = gold.get("C5full" if name == "C5" else name)
     if g:
         idx = np.array(g["sample_idx"])
         Xc = X.cpu().numpy()
