@@ -480,13 +480,13 @@ def main():
         dom = max(kern, key=lambda d: d["us_per_launch"])
         it_us = sum(us)
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "r01", "traffic_c4.json")
+        tp = os.path.join(ROOT, "profiles", "r02", "traffic_c4.json")
         if args.config == "C4" and c == 128 and kcols == 16 and os.path.exists(tp):
             with open(tp) as fh:  # the dominant kernel's DRAM bytes per launch (ncu, steady-state launch)
                 traffic = json.load(fh)["kernels"].get(dom["kernel"].split(" ")[0], {}).get("traffic_bytes")
         roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved_GBps"], "peak": hbm,
                 "unit": "GB/s", "frac": dom["achieved_GBps"] / hbm, "peak_source": peak_kind, "traffic": traffic,
-                "traffic_source": "profiles/r01/traffic_c4.json (ncu --set full, dram read+write per launch)"
+                "traffic_source": "profiles/r02/traffic_c4.json (ncu --set full, dram read+write per launch)"
                 if traffic else None,
                 "bytes_per_launch": dom["bytes_per_launch"], "us_per_launch": dom["us_per_launch"],
                 "kernels": kern, "schedule": 3,
