@@ -44,7 +44,8 @@ def _oracle_range(A, b, tol, bs):
 
 
 @pytest.mark.parametrize("N,bs,fmt", [(16, 4096, "sell"), (16, 256, "csr"), (24, 576, "sell"), (24, 1000, "csr"),
-                                      (32, 0, "sell"), (20, 1, "sell")])
+                                      (32, 0, "sell"), (20, 1, "sell"),
+                                      (32, 32768, "sell")])  # one block, vector beyond shared memory
 def test_bicgstab_ilu_table1_parity(pcg, N, bs, fmt):
     A, b = O.fd_cube(N)
     tol = 1e-12
