@@ -118,6 +118,15 @@ struct SellView {
   int64_t row0;  // absolute row of the view's slice 0 (views over a row range; decoding)
 };
 constexpr int CB_INT32 = (int)0x80000000;
+// the 16-bit id engine needs ~98 registers unconstrained (2 blocks of 256 per SM); its
+// kernels are compiled for 3 resident blocks (<= 80 registers), as the int32 engine runs
+#ifndef PCG_D16_MINB
+#define PCG_D16_MINB 3
+#endif
+#ifndef PCG_SELL_MINB  // A/B knob: 0 = unconstrained (80 registers, 3 blocks/SM)
+#define PCG_SELL_MINB 0
+#endif
+#define D16_MINB(FMT) ((FMT) == FMT_SELL_D16 ? PCG_D16_MINB : (FMT) == PCG_FORMAT_SELL ? PCG_SELL_MINB : 0)
 
 // internal format code of the TMA-staged SELL kernels (reported as PCG_FORMAT_SELL_TMA)
 constexpr int FMT_SELL_TMA = 3;

@@ -92,22 +92,37 @@ __device__ __forceinline__ void sell_rows_d16(const SellView &A, Gather gather, 
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * WARPS;
-  for (int64_t s = w0; s < A.n_slices; s += nw) {
-    const int64_t base = A.slice_ptr[s];
-    const int len = (int)((A.slice_ptr[s + 1] - base) >> 5);
+  // next-slice offsets fetched one slice ahead, as in sell_rows
+  int64_t s = w0, base = 0, next = 0;
+  if (s < A.n_slices) {
+    base = A.slice_ptr[s];
+    next = A.slice_ptr[s + 1];
+  }
+  for (; s < A.n_slices; s += nw) {
+    const int len = (int)((next - base) >> 5);
     const int row = (int)(A.row0 + s * 32 + lane);
     const double *vp = A.val + base + lane;
     const int16_t *dp = A.dcol + base + lane;
     const int *cbp = A.cbase + (base >> 5);
+    const int64_t s2 = s + nw;
+    int64_t base2 = 0, next2 = 0;
     bool fb = false;
     double sum = 0.0;
     for (int t = 0; t < len; t += 8) {
       double a[8];
       int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      // issue order: bases, deltas, values, next offsets (the ids return first)
       const int cbl = (lane < 8 && t + lane < len) ? ld_stream(cbp + t + lane) : 0;
 #pragma unroll
       for (int u = 0; u < 8; u++)
         if (t + u < len) j[u] = ld_stream(dp + (size_t)(t + u) * 32);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (t + u < len) a[u] = ld_stream(vp + (size_t)(t + u) * 32);
+      if (t == 0 && s2 < A.n_slices) {
+        base2 = A.slice_ptr[s2];
+        next2 = A.slice_ptr[s2 + 1];
+      }
       if (t == 0) fb = __shfl_sync(0xffffffffu, cbl, 0) == CB_INT32;
       if (fb) {
         const int *cp = A.col + base + lane;
@@ -118,9 +133,6 @@ __device__ __forceinline__ void sell_rows_d16(const SellView &A, Gather gather, 
 #pragma unroll
         for (int u = 0; u < 8; u++) j[u] += row + __shfl_sync(0xffffffffu, cbl, u);
       }
-#pragma unroll
-      for (int u = 0; u < 8; u++)
-        if (t + u < len) a[u] = ld_stream(vp + (size_t)(t + u) * 32);
       cols_ready(j, A.zero);
       double g[8];
 #pragma unroll
@@ -130,7 +142,13 @@ __device__ __forceinline__ void sell_rows_d16(const SellView &A, Gather gather, 
       for (int u = 0; u < 8; u++)
         if (t + u < len) sum = __fma_rn(a[u], g[u], sum);
     }
+    if (len == 0 && s2 < A.n_slices) {
+      base2 = A.slice_ptr[s2];
+      next2 = A.slice_ptr[s2 + 1];
+    }
     if (row - A.row0 < A.n) epi(row - A.row0, sum);
+    base = base2;
+    next = next2;
   }
 }
 

@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, 
 template <int FMT, int L>
 // row0/phase: the distributed overlap runs K1b over row ranges (views offset by row0);
 // phase 1 starts p.q (sigma_acc = local), 3 adds to it, 2 completes it (sigma = acc + local)
-__global__ void __launch_bounds__(BLOCK) k1b_kernel(SellView S, CsrView C, int64_t n_ghost, Vecs v, Scalars *sc,
+__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) k1b_kernel(SellView S, CsrView C, int64_t n_ghost, Vecs v, Scalars *sc,
                                                     double *partials, int dist, int use_cond,
                                                     cudaGraphConditionalHandle h, int64_t row0, int phase) {
   __shared__ double sm[1][WARPS];
@@ -320,7 +320,7 @@ __global__ void finish_beta_kernel(Scalars *sc, int use_cond, cudaGraphCondition
 // ---------------------------------------------------------------- residual (init / exit check / replacement)
 // w = b - A x; r = w; z = dinv w; p[parity] = 0; partial sums (w.w, w.z, b.b).
 template <int FMT, int L>
-__global__ void __launch_bounds__(BLOCK) resid_kernel(SellView S, CsrView C, int64_t n_ghost,
+__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) resid_kernel(SellView S, CsrView C, int64_t n_ghost,
                                                       const double *__restrict__ b, Vecs v, Scalars *sc,
                                                       double *partials, int mode, int dist) {
   __shared__ double sm[3][WARPS];
@@ -429,7 +429,7 @@ __global__ void clear_alpha_kernel(Scalars *sc) { sc->alpha = 0.0; }
 
 // ---------------------------------------------------------------- standalone SpMV  y = A x
 template <int FMT, int L>
-__global__ void __launch_bounds__(BLOCK) spmv_kernel(SellView S, CsrView C, const double *__restrict__ x,
+__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) spmv_kernel(SellView S, CsrView C, const double *__restrict__ x,
                                                      double *__restrict__ y, int64_t x_len) {
   auto gather = [&](int j) { return __ldg(x + j); };
   auto epi = [&](int64_t i, double s) { __stcs(y + i, s); };
@@ -945,9 +945,9 @@ extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32
     if (A->schedule == 3) {
       k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, 0, 0);
       PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
-      PCG_DISPATCH(A->format, A->csr_lanes, k1b_kernel,
-                   <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
-                                                              0, 0, 0, 0, 0));
+      PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
+                       <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc,
+                                                                  w.partials, 0, 0, 0, 0, 0));
       count_launch(2);
     } else {
       PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
