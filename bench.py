@@ -502,10 +502,14 @@ def main():
                                                  C.byref(done)), "pcg_profile_kernels")
         mat = 12.0 * nnz + 4.0 * (n + 1)
         if stats["schedule"] == 3:
-            names = ["k1a_kernel (p = z + beta p, x += alpha p_old; streaming)",
+            # x deferred (solver.cu k1a_deferred; PCG_XDEFER=0 turns it off): K1a alternates
+            # hold (24n B) and apply (48n B) launches, timed as pairs: 36n per launch on average
+            xdefer = os.environ.get("PCG_XDEFER", "1") != "0"
+            names = ["k1a_kernel (p = z + beta p, x += alpha p_old; streaming" +
+                     ("; x every 2nd iteration: hold/apply pair mean)" if xdefer else ")"),
                      "k1b_kernel (SpMV q = A p + sigma = p.q, grid finish -> alpha)",
                      "k2_kernel (r -= alpha q, z = dinv r, rho', gamma, grid finish -> beta)"]
-            byts = [40.0 * n, mat + 16.0 * n, 40.0 * n]
+            byts = [(36.0 if xdefer else 40.0) * n, mat + 16.0 * n, 40.0 * n]
         else:
             names = ["-", "k1_kernel (fused SpMV + p/x updates + sigma)", "k2_kernel (r/z updates + dots)"]
             byts = [0.0, mat + 48.0 * n, 40.0 * n]

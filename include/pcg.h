@@ -323,7 +323,8 @@ const char *pcg_status_string(pcg_status s);
 /* Per-kernel timing for the roofline (bench/profiling only): runs the init pass on b
  * (device pointer, x0 = 0), then `reps` PCG iterations launched one kernel at a time
  * with CUDA events between the passes on `stream`.  us[0..2] = mean device time in
- * microseconds of: K1a (streaming p/x update; 0 under the fused schedule), K1b (SpMV
+ * microseconds of: K1a (streaming p/x update, averaged over the loop's hold / apply pairs
+ * when x is updated every second iteration; 0 under the fused schedule), K1b (SpMV
  * + sigma; the fused K1 under schedule 2), K2 (r/z updates + dots).
  * Single-GPU handles only; stops early (fewer reps) if the solve converges. */
 pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32_t reps, void *stream, double *us,

@@ -59,6 +59,7 @@ struct SolveWork {
   bool graph_ready = false;
   int graph_kind = 0;  // 1 = conditional while node, 2 = unrolled chunk
   int unroll = 0;
+  bool xdefer = false;  // single-GPU 3-pass graph: x updated every second iteration (solver.cu)
   // multi-RHS workspace (row-major n x kcap)
   int kcap = 0;
   double *mr = nullptr, *mz = nullptr, *mq = nullptr, *mp[2] = {nullptr, nullptr}, *mx = nullptr,

@@ -39,12 +39,29 @@ __device__ __forceinline__ void stop_loop(int use_cond, cudaGraphConditionalHand
 }
 
 // ---------------------------------------------------------------- finishers
-__device__ void finish_alpha(Scalars *sc, double sigma, int use_cond, cudaGraphConditionalHandle h, int flip = 1) {
+// xdefer (deferred x update, k1a_kernel): 1 = a "hold" iteration (its K1a left
+// alpha_{k-1} p_{k-1} owed to x and wrote p_k to p[1]), 2 = an "apply" iteration (x is
+// current up to alpha_{k-1}, p_k in p[0]); 0 = off.
+__device__ void finish_alpha(Scalars *sc, double sigma, int use_cond, cudaGraphConditionalHandle h, int flip = 1,
+                             int xdefer = 0) {
   sc->sigma = sigma;
   if (!(sigma > 0.0)) {  // p^T A p <= 0 (or NaN): CG breakdown, A not SPD
     sc->done = DONE_BREAKDOWN;
     stop_loop(use_cond, h);
+    if (xdefer == 1) {  // alpha_{k-1} p_{k-1} (in p[0]) is still owed: the tail applies it
+      sc->alpha_old = sc->alpha;
+      sc->alpha = 0.0;
+      sc->xhold = 1;
+      sc->parity = 1;
+    } else if (xdefer == 2) {  // this iteration's K1a applied everything owed
+      sc->xhold = 0;
+    }
   } else {
+    if (xdefer) {
+      sc->alpha_old = sc->alpha;
+      sc->xhold = xdefer == 1;
+      sc->parity = xdefer == 1;
+    }
     sc->alpha = sc->rho / sigma;
     sc->k += 1;
     sc->parity ^= flip;
@@ -210,14 +227,61 @@ __global__ void __launch_bounds__(BLOCK) k2_kernel(int64_t n, Vecs v, Scalars *s
 // K1b (SpMV):      q = A p ; sigma = p.q -> alpha           (matrix + 16n B)
 // K2  (as above):  r, z updates + rho', gamma -> beta       (40n B)
 // 96n + matrix bytes per iteration, every pass a plain streaming or SpMV pass.
+//
+// Deferred x update (xdefer, single-GPU graph loop; SURVEY §8(d) bytes): x changes only
+// every second iteration, so K1a alternates
+//   hold  (xdefer 1): p[1] = z + beta p[0]; x untouched          (reads z, p: 24n B)
+//   apply (xdefer 2): x = fma(alpha_k, p[1], fma(alpha_{k-1}, p[0], x)); p[0] = z + beta p[1]
+//                                                                 (reads z, p, p, x: 48n B)
+// 36n instead of 40n per iteration, and the SAME fused multiply-adds in the same order
+// as the every-iteration update, so x is bitwise the same.  The tail applies what a
+// stop leaves owed (Scalars::xhold, alpha_old).
+__device__ __forceinline__ void k1a_deferred(int64_t n, const Vecs &v, double beta, double alpha, double alpha_old,
+                                             int xdefer) {
+  const int64_t npair = n >> 1;
+  const double2 *__restrict__ z2 = reinterpret_cast<const double2 *>(v.z);
+  const int64_t t = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nt = (int64_t)gridDim.x * BLOCK;
+  if (xdefer == 1) {
+    const double2 *__restrict__ a2 = reinterpret_cast<const double2 *>(v.p0);
+    double2 *__restrict__ b2 = reinterpret_cast<double2 *>(v.p1);
+    for (int64_t i = t; i < npair; i += nt) {
+      const double2 zz = __ldcs(z2 + i), po = __ldcs(a2 + i);
+      b2[i] = make_double2(__fma_rn(beta, po.x, zz.x), __fma_rn(beta, po.y, zz.y));
+    }
+    if ((n & 1) && t == 0) v.p1[n - 1] = __fma_rn(beta, v.p0[n - 1], v.z[n - 1]);
+  } else {
+    double2 *__restrict__ a2 = reinterpret_cast<double2 *>(v.p0);
+    const double2 *__restrict__ b2 = reinterpret_cast<const double2 *>(v.p1);
+    double2 *__restrict__ x2 = reinterpret_cast<double2 *>(v.x);
+    for (int64_t i = t; i < npair; i += nt) {
+      const double2 zz = __ldcs(z2 + i), pk = b2[i], pm = __ldcs(a2 + i);
+      double2 xx = __ldcs(x2 + i);
+      xx.x = __fma_rn(alpha, pk.x, __fma_rn(alpha_old, pm.x, xx.x));
+      xx.y = __fma_rn(alpha, pk.y, __fma_rn(alpha_old, pm.y, xx.y));
+      a2[i] = make_double2(__fma_rn(beta, pk.x, zz.x), __fma_rn(beta, pk.y, zz.y));
+      __stcs(x2 + i, xx);
+    }
+    if ((n & 1) && t == 0) {
+      const int64_t i = n - 1;
+      const double pk = v.p1[i];
+      v.x[i] = __fma_rn(alpha, pk, __fma_rn(alpha_old, v.p0[i], v.x[i]));
+      v.p0[i] = __fma_rn(beta, pk, v.z[i]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, Vecs v, Scalars *sc, int use_cond,
-                                                    cudaGraphConditionalHandle h) {
+                                                    cudaGraphConditionalHandle h, int xdefer) {
   const volatile Scalars *vs = sc;
   if (vs->done != DONE_RUNNING) {
     if (blockIdx.x == 0 && threadIdx.x == 0) stop_loop(use_cond, h);
     return;
   }
   const double beta = vs->beta, alpha_prev = vs->alpha;
+  if (xdefer) {
+    k1a_deferred(n, v, beta, alpha_prev, vs->alpha_old, xdefer);
+    return;
+  }
   double *__restrict__ p = v.p0;
   const int64_t npair = n >> 1;
   const double2 *__restrict__ z2 = reinterpret_cast<const double2 *>(v.z);
@@ -245,7 +309,8 @@ template <int FMT, int L>
 // phase 1 starts p.q (sigma_acc = local), 3 adds to it, 2 completes it (sigma = acc + local)
 __global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) k1b_kernel(SellView S, CsrView C, int64_t n_ghost, Vecs v, Scalars *sc,
                                                     double *partials, int dist, int use_cond,
-                                                    cudaGraphConditionalHandle h, int64_t row0, int phase) {
+                                                    cudaGraphConditionalHandle h, int64_t row0, int phase,
+                                                    int xdefer) {
   __shared__ double sm[1][WARPS];
   const volatile Scalars *vs = sc;
   if (vs->done != DONE_RUNNING) {
@@ -292,7 +357,7 @@ __global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) k1b_kernel(SellView S, C
         sc->sigma = tot[0];
         sc->graph_launches += use_cond;
       } else {
-        finish_alpha(sc, tot[0], use_cond, h, 0);
+        finish_alpha(sc, tot[0], use_cond, h, 0, xdefer);
       }
     }
   }
@@ -416,16 +481,30 @@ __global__ void resid_finish_kernel(Scalars *sc, int mode) {
 }
 
 // deferred x += alpha_k p_k after the loop stops on the recurrence or max_iter
+// x += alpha_k p_k still owed at a stop (converged / max_iter), after the held
+// alpha_{k-1} p_{k-1} of the deferred update (xhold) in the order the loop would apply them
 __global__ void tail_kernel(int64_t n, Vecs v, const Scalars *sc) {
   const int done = sc->done;
-  if (done != DONE_CONVERGED && done != DONE_MAXIT) return;
-  const double alpha = sc->alpha;
-  if (alpha == 0.0) return;
+  const double alpha = sc->alpha, alpha_old = sc->alpha_old;
+  const bool last = (done == DONE_CONVERGED || done == DONE_MAXIT) && alpha != 0.0;
+  const bool hold = sc->xhold != 0;
+  if (!last && !hold) return;
   const double *p = sc->parity ? v.p1 : v.p0;
-  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK)
-    v.x[i] = __fma_rn(alpha, p[i], v.x[i]);
+  const double *ph = sc->parity ? v.p0 : v.p1;
+  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
+    double xi = v.x[i];
+    if (hold) xi = __fma_rn(alpha_old, ph[i], xi);
+    if (last) xi = __fma_rn(alpha, p[i], xi);
+    v.x[i] = xi;
+  }
 }
-__global__ void clear_alpha_kernel(Scalars *sc) { sc->alpha = 0.0; }
+// after the tail: nothing owed; the deferred loop restarts (replacement) with p in p[0]
+__global__ void clear_alpha_kernel(Scalars *sc, int xdefer) {
+  sc->alpha = 0.0;
+  sc->alpha_old = 0.0;
+  sc->xhold = 0;
+  if (xdefer) sc->parity = 0;
+}
 
 // ---------------------------------------------------------------- standalone SpMV  y = A x
 template <int FMT, int L>
@@ -503,7 +582,8 @@ static int k1_chunk() {  // tuning knob (PCG_K1_CHUNK=4|8), default 8
   return c;
 }
 
-static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
+static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h,
+                            int xdefer = 0) {
   Vecs v = vecs_of(A);
   SolveWork &w = A->work;
   if (A->schedule == 3 && A->comm && A->ov) {
@@ -512,7 +592,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     // after the join the ghost p update and K1b over the boundary rows (head, tail)
     PCG_CUDA(cudaEventRecord(A->ov_fork, st));
     PCG_CUDA(cudaStreamWaitEvent(A->ov_side, A->ov_fork, 0));
-    k1a_kernel<<<A->grid_vec, BLOCK, 0, A->ov_side>>>(A->n, 0, v, w.sc, use_cond, h);
+    k1a_kernel<<<A->grid_vec, BLOCK, 0, A->ov_side>>>(A->n, 0, v, w.sc, use_cond, h, 0);
     count_launch();
     struct Range {
       int64_t r0, r1;
@@ -545,7 +625,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
       cudaStream_t ks = t == 0 ? A->ov_side : st;
       PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
                        <<<g, BLOCK, A->dyn_smem, ks>>>(S, Cv, A->n_ghost, v, w.sc, w.partials, 1, use_cond, h, R.r0,
-                                                      phase));
+                                                      phase, 0));
       count_launch();
     }
     PCG_CUDA(cudaGetLastError());
@@ -555,11 +635,13 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     return PCG_OK;
   }
   if (A->schedule == 3) {  // K1a (streaming p/x update) + K1b (SpMV + sigma)
-    k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, use_cond, h);
+    k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, use_cond, h, xdefer);
     count_launch();
+    Vecs vb = v;
+    if (xdefer == 1) vb.p0 = v.p1;  // a hold iteration wrote p_k to p[1]
     PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
-                     <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc, w.partials,
-                                                                A->comm ? 1 : 0, use_cond, h, 0, 0));
+                     <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, vb, w.sc, w.partials,
+                                                                A->comm ? 1 : 0, use_cond, h, 0, 0, xdefer));
     count_launch();
     PCG_CUDA(cudaGetLastError());
     if (A->comm) {
@@ -620,6 +702,12 @@ static pcg_status launch_resid(pcg_matrix *A, const double *b, int mode, cudaStr
   return PCG_OK;
 }
 
+// deferred x update (k1a_deferred): single GPU, 3-pass schedule; PCG_XDEFER=0 turns it off
+static bool xdefer_wanted(const pcg_matrix *A) {
+  const char *xd = getenv("PCG_XDEFER");
+  return !A->comm && A->schedule == 3 && !(xd && atoi(xd) == 0);
+}
+
 // Build the loop graph once per handle: WHILE(cond) { K1; K2 } (1 GPU), or an
 // unrolled chunk of U iterations polled from the host (distributed: NCCL calls
 // are kept out of conditional bodies).
@@ -628,9 +716,10 @@ static pcg_status build_loop_graph(pcg_matrix *A) {
   if (w.graph_ready) return PCG_OK;
   // host-callback communicator, or PCG_NO_GRAPH=1 (profilers that do not descend into
   // conditional graph bodies): the same iterations as direct launches, host-polled
+  w.xdefer = xdefer_wanted(A);
   if ((A->comm && !comm_uses_graphs(A->comm)) || getenv("PCG_NO_GRAPH")) {
     w.graph_kind = 3;
-    w.unroll = 8;
+    w.unroll = 8;  // even: hold / apply pairs
     w.graph_ready = true;
     return PCG_OK;
   }
@@ -653,7 +742,7 @@ static pcg_status build_loop_graph(pcg_matrix *A) {
     cudaGraph_t body = np.conditional.phGraph_out[0];
     PCG_CUDA(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     for (int u = 0; u < 2 && st == PCG_OK; u++) {
-      st = launch_k1(A, cap, 1, h);
+      st = launch_k1(A, cap, 1, h, w.xdefer ? 1 + u : 0);
       if (st == PCG_OK) st = launch_k2(A, cap, 1, h);
     }
     cudaGraph_t out;
@@ -764,14 +853,14 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
           PCG_CUDA(cudaGraphLaunch(w.loop_exec, st));
         } else {  // 3: the same iterations launched directly (collectives through host callbacks)
           for (int u = 0; u < w.unroll; u++) {
-            PCG_TRY(launch_k1(A, st, 0, 0));
+            PCG_TRY(launch_k1(A, st, 0, 0, w.xdefer ? 1 + (u & 1) : 0));
             PCG_TRY(launch_k2(A, st, 0, 0));
           }
         }
       }
     }
     tail_kernel<<<A->grid_vec, BLOCK, 0, st>>>(n, vecs_of(A), w.sc);
-    clear_alpha_kernel<<<1, 1, 0, st>>>(w.sc);
+    clear_alpha_kernel<<<1, 1, 0, st>>>(w.sc, !persist && w.xdefer);
     count_launch(2);
     PCG_TRY(launch_resid(A, db, MODE_EXIT, st));
     PCG_CUDA(cudaMemcpyAsync(h, w.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
@@ -808,7 +897,8 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
     info->t_solve_s = ms * 1e-3;
     const double nn = (double)A->n, nz = (double)A->nnz;
     const int sched = persist ? persist_schedule(A) : A->schedule;
-    info->bytes_algorithmic = (double)h->k * (12.0 * nz + 4.0 * (nn + 1) + (sched == 3 ? 96.0 : 88.0) * nn);
+    const double vb = sched == 3 ? (!persist && w.xdefer ? 92.0 : 96.0) : 88.0;  // K1a 36n deferred
+    info->bytes_algorithmic = (double)h->k * (12.0 * nz + 4.0 * (nn + 1) + vb * nn);
     info->flops = (double)h->k * (2.0 * nz + 13.0 * nn);
   }
   if (s == PCG_ERR_NOT_SPD) set_error("pcg_solve: p^T A p <= 0 (matrix not SPD)");
@@ -942,12 +1032,15 @@ extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32
   for (auto &e : ev) PCG_CUDA(cudaEventCreate(&e));
   PCG_CUDA(cudaEventRecord(ev[0], st));
   for (int r = 0; r < reps; r++) {
-    if (A->schedule == 3) {
-      k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, 0, 0);
+    if (A->schedule == 3) {  // the loop's kernels: hold / apply K1a pairs when x is deferred
+      const int xd = xdefer_wanted(A) ? 1 + (r & 1) : 0;
+      Vecs vb = v;
+      if (xd == 1) vb.p0 = v.p1;
+      k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, 0, 0, xd);
       PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
       PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
-                       <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, v, w.sc,
-                                                                  w.partials, 0, 0, 0, 0, 0));
+                       <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, vb, w.sc,
+                                                                  w.partials, 0, 0, 0, 0, 0, xd));
       count_launch(2);
     } else {
       PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));

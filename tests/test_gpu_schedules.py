@@ -6,7 +6,9 @@ conditional-WHILE CUDA graph of k1a/k1b/k2 with in-kernel finishers (the path th
 C5 benchmark times).  Every schedule is compared against the oracle here, through
 the C ABI, by forcing it with the documented knobs:
   persist  PCG_PERSIST=1                 (cooperative kernel)
-  graph    PCG_PERSIST=0                 (graph, 3 passes: the C5 bench path)
+  graph    PCG_PERSIST=0                 (graph, 3 passes: the C5 bench path, x updated
+                                          every second iteration)
+  graph_xevery PCG_PERSIST=0 PCG_XDEFER=0 (the same graph, x updated every iteration)
   graph2   PCG_PERSIST=0 PCG_SCHEDULE=2  (graph, fused K1 + K2)
   direct   PCG_PERSIST=0 PCG_NO_GRAPH=1  (same kernels, host-launched, host-polled)
 Bars as tests/test_gpu_parity.py (north_star): rel-L2 <= 1e-9, true relres <= tol,
@@ -24,10 +26,11 @@ pytestmark = pytest.mark.gpu
 SCHEDULES = {
     "persist": {"PCG_PERSIST": "1"},
     "graph": {"PCG_PERSIST": "0"},
+    "graph_xevery": {"PCG_PERSIST": "0", "PCG_XDEFER": "0"},
     "graph2": {"PCG_PERSIST": "0", "PCG_SCHEDULE": "2"},
     "direct": {"PCG_PERSIST": "0", "PCG_NO_GRAPH": "1"},
 }
-KNOBS = ("PCG_PERSIST", "PCG_SCHEDULE", "PCG_NO_GRAPH")
+KNOBS = ("PCG_PERSIST", "PCG_SCHEDULE", "PCG_NO_GRAPH", "PCG_XDEFER")
 
 
 @pytest.fixture(scope="module")
@@ -61,7 +64,7 @@ def _check_schedule(M, schedule):
     st = M.stats()
     if schedule == "graph2":
         assert st["schedule"] == 2
-    elif schedule in ("graph", "direct"):
+    elif schedule in ("graph", "graph_xevery", "direct"):
         assert st["schedule"] == 3
 
 

@@ -1,0 +1,133 @@
+"""The deferred x update of the single-GPU graph loop (solver.cu k1a_deferred): x is
+updated every second iteration with the same fused multiply-adds in the same order, so
+x must be BITWISE the every-iteration update's (PCG_XDEFER=0) at every kind of stop:
+converged after a hold or an apply iteration, max_iter odd and even, residual
+replacement (§8(c).8), breakdown (p^T A p <= 0) after either kind, warm start.  The
+oracle bars of the graph schedule are in tests/test_gpu_schedules.py.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pcg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_05413_b200 as p
+    return p
+
+
+def _dev(a):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(a)).cuda()
+
+
+def _pair(pcg, monkeypatch, A, graph=True):
+    """(deferred handle, every-iteration handle) of the same matrix on the graph path"""
+    monkeypatch.setenv("PCG_PERSIST", "0")
+    if not graph:
+        monkeypatch.setenv("PCG_NO_GRAPH", "1")
+    out = []
+    for xd in ("1", "0"):
+        monkeypatch.setenv("PCG_XDEFER", xd)
+        M = pcg.Matrix.from_csr(_dev(A.row_ptr), _dev(A.col), _dev(A.val), fmt="sell")
+        _solve(M, np.ones(A.n), max_iter=3)  # builds the loop graph under this env
+        out.append(M)
+    monkeypatch.delenv("PCG_XDEFER")
+    return out
+
+
+def _solve(M, b, **kw):
+    import torch
+    from paper_2201_05413_b200 import PcgError
+    x = torch.zeros(len(b), dtype=torch.float64, device="cuda")
+    if "x0" in kw:
+        x.copy_(_dev(kw.pop("x0")))
+    try:
+        _, info = M.solve(_dev(b), out=x, **kw)
+        st = info["status"]
+    except PcgError as e:
+        info, st = None, e.status
+    return x.cpu().numpy(), st, info
+
+
+@pytest.mark.parametrize("graph", [True, False])
+@pytest.mark.parametrize("name,c", [("C1", None), ("C2", 48), ("C4", 16)])
+def test_deferred_x_bitwise_converged(pcg, monkeypatch, graph, name, c):
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    Md, Me = _pair(pcg, monkeypatch, A, graph)
+    tol = O.configs()[name]["tol"]
+    xd, sd, infd = _solve(Md, b, tol=tol)
+    xe, se, infe = _solve(Me, b, tol=tol)
+    assert sd == se == 0 and infd["iterations"] == infe["iterations"]
+    assert np.array_equal(xd, xe)
+    # the oracle, for the record of what the bitwise pair computes
+    r = O.pcg(A, b, tol=tol)
+    assert np.linalg.norm(xd - r.x) / np.linalg.norm(r.x) <= 1e-9
+
+
+def test_deferred_x_bitwise_stop_parities(pcg, monkeypatch):
+    """max_iter 1..9 stops after hold (odd k) and apply (even k) iterations; tolerances
+    that converge at both parities; a warm start."""
+    P = O.build_problem("C1", c=32)
+    A, b = P["A"], P["B"][:, 0]
+    Md, Me = _pair(pcg, monkeypatch, A)
+    for mi in range(1, 10):
+        xd, sd, _ = _solve(Md, b, tol=1e-12, max_iter=mi)
+        xe, se, _ = _solve(Me, b, tol=1e-12, max_iter=mi)
+        assert sd == se == 1 and np.array_equal(xd, xe), mi
+    its = set()
+    for tol in (1e-2, 3e-3, 1e-3, 3e-4, 1e-4, 3e-5, 1e-6):
+        xd, sd, infd = _solve(Md, b, tol=tol)
+        xe, se, infe = _solve(Me, b, tol=tol)
+        assert sd == se and infd["iterations"] == infe["iterations"] and np.array_equal(xd, xe), tol
+        its.add(infd["iterations"] % 2)
+    assert its == {0, 1}  # both parities exercised
+    x0 = np.random.default_rng(3).standard_normal(A.n)
+    xd, _, infd = _solve(Md, b, tol=1e-10, x0=x0)
+    xe, _, infe = _solve(Me, b, tol=1e-10, x0=x0)
+    assert infd["iterations"] == infe["iterations"] and np.array_equal(xd, xe)
+
+
+def test_deferred_x_bitwise_replacement(pcg, monkeypatch):
+    """below attainable accuracy: replacements restart the deferred loop (p in p[0])"""
+    P = O.build_problem("C1")
+    A, b = P["A"], P["B"][:, 0]
+    Md, Me = _pair(pcg, monkeypatch, A)
+    for mi in (399, 400):
+        xd, sd, infd = _solve(Md, b, tol=1e-15, max_iter=mi)
+        xe, se, infe = _solve(Me, b, tol=1e-15, max_iter=mi)
+        assert sd == se == 1 and infd["replacements"] == infe["replacements"] >= 2
+        assert np.array_equal(xd, xe)
+
+
+def test_deferred_x_bitwise_breakdown(pcg, monkeypatch):
+    """symmetric indefinite systems (C1 Laplacian - s I, random b): CG breaks down
+    (NOT_SPD) at iterations of both parities (the oracle's count); x holds every applied
+    update, bitwise the same on both paths"""
+    import scipy.sparse as sp
+    P = O.build_problem("C1", c=24)
+    A0 = P["A"].to_scipy().tocsr()
+    b = np.random.default_rng(1).standard_normal(A0.shape[0])
+    lam = np.linalg.eigvalsh(A0.toarray())
+    parities = set()
+    for f in (0.0005, 0.001, 0.002, 0.005, 0.01, 0.02, 0.05, 0.1, 0.2, 0.3):
+        s = lam[0] + f * (lam[-1] - lam[0])
+        B = (A0 - s * sp.identity(A0.shape[0])).tocsr()
+        B.sort_indices()
+        C = O.Csr(B.shape[0], B.indptr, B.indices, B.data)
+        r = O.pcg(C, b, tol=1e-12, max_iter=2000)
+        assert r.status == O.ERR_NOT_SPD
+        Md, Me = _pair(pcg, monkeypatch, C)
+        xd, sd, _ = _solve(Md, b, tol=1e-12, max_iter=2000)
+        xe, se, _ = _solve(Me, b, tol=1e-12, max_iter=2000)
+        assert sd == se == 7, (f, sd, se)  # PCG_ERR_NOT_SPD
+        assert np.array_equal(xd, xe), f
+        parities.add(r.iterations % 2)
+    assert parities == {0, 1}
