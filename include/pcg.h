@@ -121,7 +121,9 @@ typedef struct {
   int32_t spmm_windowed;     /* multi-RHS SpMM plan: 1 = column windows staged by TMA (opt-in,
                                 environment PCG_SPMM_WIN=1; built at the first pcg_solve_multi),
                                 -1 = not used, 0 = not decided yet */
-  int32_t pad0;
+  int32_t short_rows;        /* 1: SELL-32 with every row <= 8 entries runs the one-chunk row
+                                engine (64 registers, 4 resident blocks/SM instead of 3; same
+                                entries, same sums); environment PCG_SHORT=0 at csr_create: off */
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */

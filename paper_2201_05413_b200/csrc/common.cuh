@@ -127,13 +127,19 @@ constexpr int CB_INT32 = (int)0x80000000;
 #ifndef PCG_SELL_MINB  // A/B knob: 0 = unconstrained (80 registers, 3 blocks/SM)
 #define PCG_SELL_MINB 0
 #endif
-#define D16_MINB(FMT) ((FMT) == FMT_SELL_D16 ? PCG_D16_MINB : (FMT) == PCG_FORMAT_SELL ? PCG_SELL_MINB : 0)
+#ifndef PCG_SHORT_MINB  // the short-row engine (rows.cuh sell_rows_short): resident blocks per SM
+#define PCG_SHORT_MINB 4
+#endif
+#define D16_MINB(FMT)                                                     \
+  ((FMT) == FMT_SELL_D16 ? PCG_D16_MINB : (FMT) == FMT_SELL_SHORT ? PCG_SHORT_MINB \
+   : (FMT) == PCG_FORMAT_SELL ? PCG_SELL_MINB : 0)
 
 // internal format code of the TMA-staged SELL kernels (reported as PCG_FORMAT_SELL_TMA)
 constexpr int FMT_SELL_TMA = 3;
 // internal code of the SELL-32 kernels that read the 16-bit delta column ids (rows.cuh
 // sell_rows_d16): the SpMV, K1b and residual passes of the 3-pass schedule
 constexpr int FMT_SELL_D16 = 5;
+constexpr int FMT_SELL_SHORT = 6;  // SELL-32, every row <= 8 entries: one-chunk engine
 
 // ------------------------------------------------------------------ reductions
 constexpr int BLOCK = 256;

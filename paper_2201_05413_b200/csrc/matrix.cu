@@ -619,6 +619,15 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
   if (e1) cudaEventDestroy(e1);
   configure(best_fmt);
   if (A->format == PCG_FORMAT_SELL) PCG_TRY(build_d16(A, st));
+  {  // rows of at most 8 entries: the one-chunk SELL engine and its grid (PCG_SHORT=0: off)
+    const char *se = getenv("PCG_SHORT");
+    A->short_rows = A->format == PCG_FORMAT_SELL && !A->d_sdcol && A->max_row_len <= 8 && !(se && atoi(se) == 0);
+    if (A->short_rows) {
+      const int64_t need = (A->n_slices + WARPS - 1) / WARPS;
+      const int64_t g = (int64_t)sms * k1_blocks_per_sm(FMT_SELL_SHORT, 1, 0);
+      A->grid_spmv = (int)std::max<int64_t>(1, std::min(g, need));
+    }
+  }
   {
     const char *sch = getenv("PCG_SCHEDULE");
     A->schedule = (sch && atoi(sch) == 2) ? 2 : 3;
@@ -796,5 +805,6 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->overlap_rows = A->ov ? A->ov_ib - A->ov_ia : 0;
   o->d16_slices = A->d16_slices;
   o->spmm_windowed = A->wplan;
+  o->short_rows = A->short_rows ? 1 : 0;
   return PCG_OK;
 }

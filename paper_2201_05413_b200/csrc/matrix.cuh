@@ -119,6 +119,7 @@ struct pcg_matrix {
   int device = 0;
   int64_t n = 0, nnz = 0;  // local rows / nnz
   int32_t max_row_len = 0;
+  bool short_rows = false;  // SELL with rows <= 8 entries: the one-chunk engine (rows.cuh)
   int format = PCG_FORMAT_CSR;
   // CSR (int32)
   int *d_row_ptr = nullptr, *d_col = nullptr;

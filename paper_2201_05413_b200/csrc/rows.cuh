@@ -80,6 +80,55 @@ __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi 
   }
 }
 
+// SELL-32 for systems whose rows hold at most 8 entries (the lattice P1 systems: 7):
+// every slice is one chunk, so the chunk loop, its predicates' live ranges and the
+// per-chunk state disappear and the kernel fits in fewer registers (more resident warps,
+// more slices in flight); the ids are issued before the values (an SM completes loads
+// in issue order).  Same entries, same left-to-right sums as sell_rows (bitwise).
+template <class Gather, class Epi>
+__device__ __forceinline__ void sell_rows_short(const SellView &A, Gather gather, Epi epi) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  int64_t s = w0, base = 0, next = 0;
+  if (s < A.n_slices) {
+    base = A.slice_ptr[s];
+    next = A.slice_ptr[s + 1];
+  }
+  for (; s < A.n_slices; s += nw) {
+    const int len = (int)((next - base) >> 5);  // <= 8 (host-checked)
+    const double *vp = A.val + base + lane;
+    const int *cp = A.col + base + lane;
+    double a[8];
+    int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (u < len) j[u] = ld_stream(cp + (size_t)u * 32);
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (u < len) a[u] = ld_stream(vp + (size_t)u * 32);
+    const int64_t s2 = s + nw;
+    int64_t base2 = 0, next2 = 0;
+    if (s2 < A.n_slices) {
+      base2 = A.slice_ptr[s2];
+      next2 = A.slice_ptr[s2 + 1];
+    }
+    cols_ready(j, A.zero);
+    double g[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (u < len) g[u] = gather(j[u]);
+    double sum = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (u < len) sum = __fma_rn(a[u], g[u], sum);
+    const int64_t row = s * 32 + lane;
+    if (row < A.n) epi(row, sum);
+    base = base2;
+    next = next2;
+  }
+}
+
 // SELL-32 with the 16-bit delta column ids (common.cuh SellView::dcol): the same row
 // engine, the same ids (so the same sums, bitwise), 10.125 instead of 12 bytes per entry.
 // Per slice the deltas and the per-(slice, t) bases are loaded (indices first: an SM's

@@ -334,6 +334,33 @@ def test_d16_column_form_is_bitwise_the_int32_form(pcg, monkeypatch, name, c, fm
         assert bool((X1 == X0).all())
 
 
+@pytest.mark.parametrize("name,c", [("C1", None), ("C2", 40), ("C4", 12), ("C5", 24)])
+def test_short_row_engine_is_bitwise_the_chunked_engine(pcg, monkeypatch, name, c):
+    """Rows of at most 8 entries (the lattice P1 systems) run the one-chunk SELL engine
+    (pcg.h short_rows): the same entries summed in the same order, so the SpMV is
+    bitwise the chunked engine's (PCG_SHORT=0); the graph-loop solve (the C5 bench
+    path) meets the oracle bars with it; C3 (P2, up to 19 entries) keeps the chunked one."""
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    monkeypatch.setenv("PCG_PERSIST", "0")
+    monkeypatch.setenv("PCG_SHORT", "0")
+    M0 = _matrix(pcg, A, "sell")
+    monkeypatch.delenv("PCG_SHORT")
+    M1 = _matrix(pcg, A, "sell")
+    assert M0.stats()["short_rows"] == 0 and M1.stats()["short_rows"] == 1
+    x = np.random.default_rng(12).standard_normal(A.n)
+    y1, y0 = M1.spmv(_dev(x)).cpu().numpy(), M0.spmv(_dev(x)).cpu().numpy()
+    assert np.array_equal(y1, y0)
+    tol = O.configs()[name]["tol"]
+    r = O.pcg(A, b, tol=tol)
+    xs, info = M1.solve(_dev(b), tol=tol)
+    assert info["status"] == 0 and info["relres_true"] <= tol
+    assert np.linalg.norm(xs.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-9
+    assert abs(info["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
+    P3 = O.build_problem("C3", c=16, k=1)
+    assert _matrix(pcg, P3["A"], "sell").stats()["short_rows"] == 0
+
+
 @pytest.mark.parametrize("k", [1, 5, 16])
 def test_windowed_spmm_multi_rhs_parity(pcg, monkeypatch, k):
     """The multi-RHS SpMM with TMA-staged column windows (pcg.h spmm_windowed): the plan
