@@ -25,8 +25,12 @@ namespace pcgb {
 // SCHED 3: K1a | K1b | K2, three barriers per iteration (96 n bytes); SCHED 2: K1 (SpMV
 // with p = z + beta p recomputed at gather time, x += alpha_prev p_old) | K2, two
 // barriers (88 n bytes, twice the gathers).
+#ifndef PCG_PERSIST_MINB  // resident blocks per SM the persistent kernel is compiled for
+#define PCG_PERSIST_MINB 3
+#endif
+
 template <int FMT, int L, int SCHED>
-__global__ void __launch_bounds__(BLOCK, 3) pcg_persist_kernel(SellView S, CsrView C, Vecs v, Scalars *sc, double *part,
+__global__ void __launch_bounds__(BLOCK, PCG_PERSIST_MINB) pcg_persist_kernel(SellView S, CsrView C, Vecs v, Scalars *sc, double *part,
                                                             GridBar *bar) {
   __shared__ double sm[2][WARPS];
   __shared__ double s_tot[2];

@@ -15,18 +15,26 @@ namespace pcgb {
 // entry.  Making every gather index depend on ALL column ids of the chunk
 // (j |= xor(j) & zero, with `zero` a run-time 0 the compiler cannot fold) forces
 // all column loads to be issued before the first gather address exists.
-__device__ __forceinline__ void cols_ready(int (&j)[8], int zero) {
-  const int x = (j[0] ^ j[1] ^ j[2] ^ j[3] ^ j[4] ^ j[5] ^ j[6] ^ j[7]) & zero;
+template <int N>
+__device__ __forceinline__ void cols_ready(int (&j)[N], int zero) {
+  int x = j[0];
 #pragma unroll
-  for (int u = 0; u < 8; u++) j[u] |= x;
+  for (int u = 1; u < N; u++) x ^= j[u];
+  x &= zero;
+#pragma unroll
+  for (int u = 0; u < N; u++) j[u] |= x;
 }
+
+#ifndef PCG_SELL_CH  // entries per chunk of the general SELL engine (A/B knob)
+#define PCG_SELL_CH 8
+#endif
 
 // SELL-32: one warp per slice of 32 consecutive rows, lane = row.  Entries of a
 // slice are stored [t][lane] so every load of the t-th entry is one 256-B (val)
 // or 128-B (col) coalesced transaction.  Loads are issued 8 entries at a time
 // before any gather so each thread keeps 16 independent loads in flight.
 // gather(j) -> value multiplied by a_ij;  epi(row, sum) for rows < n.
-template <class Gather, class Epi>
+template <int CH = PCG_SELL_CH, class Gather, class Epi>
 __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi epi) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
@@ -46,11 +54,13 @@ __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi 
     const int64_t s2 = s + nw;
     int64_t base2 = 0, next2 = 0;
     double sum = 0.0;
-    for (int t = 0; t < len; t += 8) {
-      double a[8];
-      int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int t = 0; t < len; t += CH) {
+      double a[CH];
+      int j[CH];
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
+      for (int u = 0; u < CH; u++) j[u] = 0;
+#pragma unroll
+      for (int u = 0; u < CH; u++) {
         if (t + u < len) {
           a[u] = ld_stream(vp + (size_t)(t + u) * 32);
           j[u] = ld_stream(cp + (size_t)(t + u) * 32);
@@ -61,12 +71,12 @@ __device__ __forceinline__ void sell_rows(const SellView &A, Gather gather, Epi 
         next2 = A.slice_ptr[s2 + 1];
       }
       cols_ready(j, A.zero);
-      double g[8];
+      double g[CH];
 #pragma unroll
-      for (int u = 0; u < 8; u++)
+      for (int u = 0; u < CH; u++)
         if (t + u < len) g[u] = gather(j[u]);
 #pragma unroll
-      for (int u = 0; u < 8; u++)
+      for (int u = 0; u < CH; u++)
         if (t + u < len) sum = __fma_rn(a[u], g[u], sum);
     }
     if (len == 0 && s2 < A.n_slices) {
