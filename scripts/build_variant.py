@@ -13,7 +13,7 @@ from paper_2201_05413_b200 import build as B  # noqa: E402
 
 name, defs = sys.argv[1], sys.argv[2:]
 out = os.path.join(B.HERE, "_variants")
-obj = os.path.join(out, name)
+obj = os.path.join("/tmp", "pcg_variant_objs", name)  # objects stay out of the gpurun snapshot
 os.makedirs(obj, exist_ok=True)
 srcs = sorted(f for f in os.listdir(B.CSRC) if f.endswith(".cu"))
 
