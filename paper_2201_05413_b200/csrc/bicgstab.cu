@@ -161,6 +161,7 @@ __device__ __forceinline__ void spmv_body(const SellView &S, const CsrView &C, c
     }
   };
   if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
+  else if (FMT == FMT_SELL_SHORT) sell_rows_short(S, gather, epi);  // rows of <= 8 entries (graph schedule)
   else csr_rows<L>(C, gather, epi);
 }
 
@@ -645,7 +646,7 @@ __device__ __forceinline__ bool bg_last(double (&red)[NV], double *part, unsigne
 
 // SpMV kernels: RESID (rmode BR_INIT / BR_CHECK), AV, AT, FINAL (rmode BR_FINAL)
 template <int FMT, int L, int MODE>
-__global__ void __launch_bounds__(BLOCK) bg_spmv_kernel(SellView S, CsrView C, BicgVecs v, BgScalars *sc,
+__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) bg_spmv_kernel(SellView S, CsrView C, BicgVecs v, BgScalars *sc,
                                                         double *part, int rmode, int dist, int use_cond,
                                                         cudaGraphConditionalHandle h) {
   __shared__ double sm[3][WARPS];
@@ -812,6 +813,7 @@ static BgOps bg_ops_t() {
 
 template <int BS>
 static BgOps bg_ops_bs(int fmt, int lanes) {
+  if (fmt == FMT_SELL_SHORT) return bg_ops_t<FMT_SELL_SHORT, 1, BS>();
   if (fmt == PCG_FORMAT_SELL) return bg_ops_t<PCG_FORMAT_SELL, 1, BS>();
   switch (lanes) {
     case 1: return bg_ops_t<PCG_FORMAT_CSR, 1, BS>();
@@ -828,8 +830,16 @@ static BgOps bg_ops_ilu_t() {
   return {bg_iteration_ilu<FMT, L>, bg_resid<FMT, L, 1>};
 }
 
+// the SpMV engine of the graph / distributed schedules: SELL (TMA handles too), the
+// one-chunk engine where every row has <= 8 entries (pcg_matrix::short_rows), or CSR
+static int bg_fmt(const pcg_matrix *A) {
+  const int f = A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format;
+  return f == PCG_FORMAT_SELL && A->short_rows ? FMT_SELL_SHORT : f;
+}
+
 static BgOps bg_ops(int fmt, int lanes, int bs) {
   if (bs == BS_ILU) {
+    if (fmt == FMT_SELL_SHORT) return bg_ops_ilu_t<FMT_SELL_SHORT, 1>();
     if (fmt == PCG_FORMAT_SELL) return bg_ops_ilu_t<PCG_FORMAT_SELL, 1>();
     switch (lanes) {
       case 1: return bg_ops_ilu_t<PCG_FORMAT_CSR, 1>();
@@ -896,7 +906,7 @@ static pcg_status bg_solve(pcg_matrix *A, const BicgVecs &v, int bs, double tol,
                            BicgState *hs) {
   SolveWork &w = A->work;
   if (!w.bgsc) PCG_CUDA(cudaMalloc(&w.bgsc, sizeof(BgScalars)));
-  const BgOps ops = bg_ops(A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format, A->csr_lanes, bs);
+  const BgOps ops = bg_ops(bg_fmt(A), A->csr_lanes, bs);
   PCG_TRY(bg_build(A, ops, v, bs));
   BgScalars *sc = (BgScalars *)w.bgsc, h;
   memset(&h, 0, sizeof(h));
@@ -961,6 +971,7 @@ struct BgdOps {
 };
 using BgdSpmv = void (*)(pcg_matrix *, const BicgVecs &, BgScalars *, int, int, cudaStream_t);
 static BgdSpmv bgd_spmv_fn(int fmt, int lanes) {
+  if (fmt == FMT_SELL_SHORT) return BgdOps<FMT_SELL_SHORT, 1>::spmv;
   if (fmt == PCG_FORMAT_SELL) return BgdOps<PCG_FORMAT_SELL, 1>::spmv;
   switch (lanes) {
     case 1: return BgdOps<PCG_FORMAT_CSR, 1>::spmv;
@@ -981,7 +992,7 @@ static pcg_status bgd_solve(pcg_matrix *A, const BicgVecs &v, double tol, int64_
   h.tol = tol;
   h.max_iter = max_iter;
   PCG_CUDA(cudaMemcpyAsync(sc, &h, sizeof(h), cudaMemcpyHostToDevice, st));
-  const BgdSpmv spmv = bgd_spmv_fn(A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format, A->csr_lanes);
+  const BgdSpmv spmv = bgd_spmv_fn(bg_fmt(A), A->csr_lanes);
   double *part = w.partials;
   auto read = [&]() -> pcg_status {
     PCG_CUDA(cudaGetLastError());
