@@ -23,14 +23,23 @@
 #include <vector>
 
 #include "matrix.cuh"
+#include "staged.cuh"
 
 namespace pcgb {
 
 struct IluLevel {
   int64_t row_base;  // first slot of the level
   int64_t ent_base;  // first ELL entry of the level ([u][slot], m slots per u)
+  int64_t pbase;     // byte offset of the level's packed record (pk_bytes), -1: not packed
   int m, c;          // rows, entries per row (max over the level's rows)
 };
+
+// Packed level record (one bulk copy per level): [kcol c x m int32][row m int32] (8-B
+// aligned) [fv c x m f64][u_ii m f64, backward levels], padded to 16 B.
+__host__ __device__ constexpr int pk_fv_off(int m, int c) { return ((4 * c * m + 4 * m) + 7) & ~7; }
+__host__ __device__ constexpr int pk_bytes(int m, int c, bool backward) {
+  return (pk_fv_off(m, c) + 8 * c * m + (backward ? 8 * m : 0) + 15) & ~15;
+}
 
 // Forward levels of all blocks, then backward levels; lo[0..nblk] indexes the forward
 // levels of each block, lo[nblk+1 .. 2 nblk+1] the backward ones.
@@ -51,13 +60,16 @@ struct IluPlan {
   int *udmap = nullptr;  // per slot: CSR index of u_ii (-1 forward)
   int64_t nlev = 0, nslot = 0, nent = 0;
   double bytes_per_apply = 0;
+  unsigned char *pk = nullptr;  // packed level records (apply_packed), null: not used
+  int pk_threads = 0;           // CTA size of the packed kernel (>= every level's rows)
+  int maxlev = 0;               // most levels (forward + backward) of any block
 };
 
 void ilu_free(void *p) {
   IluPlan *P = (IluPlan *)p;
   if (!P) return;
   for (void *q : {(void *)P->f, (void *)P->diag, (void *)P->lev, (void *)P->lo, (void *)P->row, (void *)P->kcol,
-                  (void *)P->emap, (void *)P->fv, (void *)P->ud, (void *)P->udmap})
+                  (void *)P->emap, (void *)P->fv, (void *)P->ud, (void *)P->udmap, (void *)P->pk})
     if (q) cudaFree(q);
   delete P;
 }
@@ -128,7 +140,32 @@ struct IluView {
   const IluLevel *lev;
   const int *lo, *row, *kcol;
   const double *fv, *ud;
+  const unsigned char *pk;
 };
+
+// the packed level records, written once after the factorization (one CTA per level)
+__global__ void ilu_pack_kernel(const IluLevel *__restrict__ lev, int64_t nfwd_end, const int *__restrict__ lo,
+                                int64_t nblk, const int *__restrict__ row, const int *__restrict__ kcol,
+                                const double *__restrict__ fv, const double *__restrict__ ud, unsigned char *pk) {
+  const int64_t l = blockIdx.x;
+  const IluLevel L = lev[l];
+  if (L.pbase < 0) return;
+  const bool backward = l >= nfwd_end;
+  unsigned char *rec = pk + L.pbase;
+  int *k = reinterpret_cast<int *>(rec);
+  int *rw = k + L.c * L.m;
+  double *f = reinterpret_cast<double *>(rec + pk_fv_off(L.m, L.c));
+  double *d = f + (size_t)L.c * L.m;
+  for (int t = threadIdx.x; t < L.m; t += blockDim.x) {
+    rw[t] = row[L.row_base + t];
+    if (backward) d[t] = ud[L.row_base + t];
+    for (int u = 0; u < L.c; u++) {
+      const int64_t e = L.ent_base + (int64_t)u * L.m + t;
+      k[u * L.m + t] = kcol[e];
+      f[u * L.m + t] = fv[e];
+    }
+  }
+}
 
 // One direction's levels of block b.  Level records come from shared memory (copied
 // at kernel entry) when the block has at most ILU_LEVS of them.  Every thread owns slot
@@ -223,13 +260,25 @@ __device__ __forceinline__ void ilu_sweep(const IluView &P, const IluLevel *lv, 
 // flight through shared memory (cp.async, one commit group per level, a ring of
 // ILU_RING level slots): each thread copies and later reads only its own slot's data,
 // so the ring needs no barrier of its own, and the level barrier orders the y traffic.
-constexpr int ILU_RING = 4;
+#ifndef PCG_ILU_RING  // A/B knobs: ring depth (levels) and threads per CTA of the apply kernel
+#define PCG_ILU_RING 4
+#endif
+#ifndef PCG_ILU_THREADS
+#define PCG_ILU_THREADS 256
+#endif
+#ifndef PCG_ILU_SPT  // level slots per thread held in the ring
+#define PCG_ILU_SPT 1
+#endif
+constexpr int ILU_RING = PCG_ILU_RING;
+constexpr int ILU_THREADS = PCG_ILU_THREADS;
+constexpr int ILU_SPT = PCG_ILU_SPT;
+constexpr int ILU_RSLOTS = ILU_THREADS * ILU_SPT;
 template <int CMAX>
 struct IluRing {
-  int row[ILU_RING][256];
-  double ud[ILU_RING][256];
-  int k[ILU_RING][CMAX][256];
-  double f[ILU_RING][CMAX][256];
+  int row[ILU_RING][ILU_RSLOTS];
+  double ud[ILU_RING][ILU_RSLOTS];
+  int k[ILU_RING][CMAX][ILU_RSLOTS];
+  double f[ILU_RING][CMAX][ILU_RSLOTS];
 };
 
 __device__ __forceinline__ void cp_async4(void *dst, const void *src) {
@@ -252,14 +301,18 @@ __device__ __forceinline__ void ilu_sweep_ring(const IluView &P, const IluLevel 
     if (l < nl) {
       const IluLevel L = lv[l];
       const int q = l % ILU_RING;
-      if (t < L.m) {
-        const int64_t s = L.row_base + t;
-        cp_async4(&R.row[q][t], P.row + s);
-        if (backward) cp_async8(&R.ud[q][t], P.ud + s);
-        for (int u = 0; u < L.c; u++) {
-          const int64_t e = L.ent_base + (int64_t)u * L.m + t;
-          cp_async4(&R.k[q][u][t], P.kcol + e);
-          cp_async8(&R.f[q][u][t], P.fv + e);
+#pragma unroll
+      for (int j = 0; j < ILU_SPT; j++) {
+        const int ts = t + j * ILU_THREADS;
+        if (ts < L.m) {
+          const int64_t s = L.row_base + ts;
+          cp_async4(&R.row[q][ts], P.row + s);
+          if (backward) cp_async8(&R.ud[q][ts], P.ud + s);
+          for (int u = 0; u < L.c; u++) {
+            const int64_t e = L.ent_base + (int64_t)u * L.m + ts;
+            cp_async4(&R.k[q][u][ts], P.kcol + e);
+            cp_async8(&R.f[q][u][ts], P.fv + e);
+          }
         }
       }
     }
@@ -273,16 +326,20 @@ __device__ __forceinline__ void ilu_sweep_ring(const IluView &P, const IluLevel 
     cp_async_wait<ILU_RING - 1>();  // this thread's copies for level l have landed
     const IluLevel L = lv[l];
     const int q = l % ILU_RING;
-    if (t < L.m) {
-      const int i = R.row[q][t];
-      double acc = y[i];
-      for (int u = 0; u < L.c; u++) {
-        const int k = R.k[q][u][t];
-        if (k >= 0) acc = __dsub_rn(acc, __dmul_rn(R.f[q][u][t], y[k]));
+#pragma unroll
+    for (int j = 0; j < ILU_SPT; j++) {
+      const int ts = t + j * ILU_THREADS;
+      if (ts < L.m) {
+        const int i = R.row[q][ts];
+        double acc = y[i];
+        for (int u = 0; u < L.c; u++) {
+          const int k = R.k[q][u][ts];
+          if (k >= 0) acc = __dsub_rn(acc, __dmul_rn(R.f[q][u][ts], y[k]));
+        }
+        y[i] = backward ? __ddiv_rn(acc, R.ud[q][ts]) : acc;
       }
-      y[i] = backward ? __ddiv_rn(acc, R.ud[q][t]) : acc;
     }
-    for (int t2 = t + blockDim.x; t2 < L.m; t2 += blockDim.x) {  // levels wider than the CTA
+    for (int t2 = t + ILU_RSLOTS; t2 < L.m; t2 += blockDim.x) {  // levels wider than the ring's slots
       IluSlot sx;
       int kx[CMAX];
       double fx[CMAX];
@@ -301,7 +358,7 @@ __host__ __device__ constexpr size_t ilu_vec_offset(int cmax) {
 }
 
 template <bool SMEM, int CMAX>
-__global__ void __launch_bounds__(256) ilu_apply_kernel(IluView P, const double *__restrict__ in, double *out,
+__global__ void __launch_bounds__(ILU_THREADS) ilu_apply_kernel(IluView P, const double *__restrict__ in, double *out,
                                                         const int *stop, const int *skip) {
   extern __shared__ __align__(16) unsigned char ilu_smem[];
   if ((stop && *(volatile const int *)stop) || (skip && *(volatile const int *)skip)) return;
@@ -331,8 +388,80 @@ __global__ void __launch_bounds__(256) ilu_apply_kernel(IluView P, const double 
     for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) out[r0 + i] = y[i];
 }
 
-constexpr int ILU_THREADS = 256;
+// The application with every level's y-independent data in ONE packed record per level,
+// brought into a shared-memory ring by one bulk copy (TMA engine) per level, issued
+// ILU_PK_RING - 1 levels ahead by thread 0, completion on an mbarrier per ring slot:
+// no per-thread copy instructions on the level's critical path (the cp.async ring
+// above issues 2 + 2c copies per thread per level).  Forward and backward levels form
+// one sequence (slot = g % RING, phase = (g / RING) & 1).  One thread per slot: the
+// CTA has at least as many threads as the widest level (pk_threads).
+constexpr int ILU_PK_RING = 6;
+template <int T>
+__global__ void __launch_bounds__(T) ilu_apply_packed_kernel(IluView P, const double *__restrict__ in, double *out,
+                                                             const int *stop, const int *skip, int rec_cap) {
+  extern __shared__ __align__(128) unsigned char ilu_smem[];
+  if ((stop && *(volatile const int *)stop) || (skip && *(volatile const int *)skip)) return;
+  constexpr int SLOT = pk_bytes(T, 4, true);
+  const int64_t b = blockIdx.x, r0 = b * P.bs, nr = min(P.bs, P.n - r0);
+  const int f0 = P.lo[b], f1 = P.lo[b + 1], b0 = P.lo[P.nblk + 1 + b], b1 = P.lo[P.nblk + 1 + b + 1];
+  const int nf = f1 - f0, ntot = nf + (b1 - b0);
+  unsigned char *ring = ilu_smem;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(ilu_smem + (size_t)ILU_PK_RING * SLOT);
+  IluLevel *slev = reinterpret_cast<IluLevel *>(ilu_smem + (size_t)ILU_PK_RING * SLOT + 8 * ILU_PK_RING);
+  double *y = reinterpret_cast<double *>(ilu_smem + (size_t)ILU_PK_RING * SLOT + 8 * ILU_PK_RING +
+                                         sizeof(IluLevel) * (size_t)rec_cap);
+  const int t = threadIdx.x;
+  for (int q = t; q < nf; q += T) slev[q] = P.lev[f0 + q];
+  for (int q = t; q < ntot - nf; q += T) slev[nf + q] = P.lev[b0 + q];
+  if (t == 0) {
+    for (int q = 0; q < ILU_PK_RING; q++) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int64_t i = t; i < nr; i += T) y[i] = in[r0 + i];
+  __syncthreads();
+  auto issue = [&](int g) {  // thread 0
+    if (g >= ntot) return;
+    const IluLevel L = slev[g];
+    const int q = g % ILU_PK_RING;
+    const uint32_t bytes = (uint32_t)pk_bytes(L.m, L.c, g >= nf);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's earlier generic reads
+    mbar_expect_tx(&bars[q], bytes);
+    bulk_g2s(ring + (size_t)q * SLOT, P.pk + L.pbase, bytes, &bars[q]);
+  };
+  if (t == 0)
+    for (int g = 0; g < ILU_PK_RING - 1; g++) issue(g);
+  for (int g = 0; g < ntot; g++) {
+    if (t == 0) issue(g + ILU_PK_RING - 1);  // slot of level g - 1: every thread passed its barrier
+    const IluLevel L = slev[g];
+    const bool backward = g >= nf;
+    const int q = g % ILU_PK_RING;
+    mbar_wait(&bars[q], (uint32_t)((g / ILU_PK_RING) & 1));
+    if (t < L.m) {
+      const unsigned char *rec = ring + (size_t)q * SLOT;
+      const int *k = reinterpret_cast<const int *>(rec);
+      const double *f = reinterpret_cast<const double *>(rec + pk_fv_off(L.m, L.c));
+      const int i = k[L.c * L.m + t];
+      double acc = y[i];
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (u < L.c) {
+          const int kk = k[u * L.m + t];
+          if (kk >= 0) acc = __dsub_rn(acc, __dmul_rn(f[u * L.m + t], y[kk]));
+        }
+      y[i] = backward ? __ddiv_rn(acc, f[L.c * L.m + t]) : acc;
+    }
+    __syncthreads();
+  }
+  for (int64_t i = t; i < nr; i += T) out[r0 + i] = y[i];
+}
+
 constexpr size_t ILU_SMEM_MAX = 227 * 1024;  // opt-in shared memory per CTA
+
+template <int T>
+static size_t ilu_packed_smem(int rec_cap, int64_t rows) {
+  return (size_t)ILU_PK_RING * pk_bytes(T, 4, true) + 8 * ILU_PK_RING + sizeof(IluLevel) * (size_t)rec_cap +
+         sizeof(double) * (size_t)rows;
+}
 
 // ---------------------------------------------------------------- setup
 pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out) {
@@ -361,6 +490,15 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
   std::vector<int> lo(2 * (P->nblk + 1));
   std::vector<int> srow, kcol, emap, udmap;
   std::vector<int> lev(n);
+  // emit(chunk): the level-ordered layout; chunk > 0 splits levels wider than `chunk` rows
+  // into records of at most `chunk` rows (rows of one level are independent, so its
+  // records may run one after the other)
+  auto emit = [&](int chunk) {
+  levs.clear();
+  srow.clear();
+  kcol.clear();
+  emap.clear();
+  udmap.clear();
   for (int d = 0; d < 2; d++) {  // 0: forward (L), 1: backward (U)
     for (int64_t b = 0; b < P->nblk; b++) {
       const int64_t r0 = b * bs, r1 = std::min(r0 + bs, n);
@@ -385,13 +523,16 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
         for (int64_t i = r0; i < r1; i++) ord[pos[lev[i]]++] = (int)(i - r0);
       }
       lo[d * (P->nblk + 1) + b] = (int)levs.size();
-      for (int l = 0; l <= maxl; l++) {
+      for (int l = 0; l <= maxl; l++)
+      for (int c0 = cnt[l]; c0 < cnt[l + 1]; c0 += chunk > 0 ? chunk : (cnt[l + 1] - cnt[l])) {
+        const int c1 = chunk > 0 ? std::min(cnt[l + 1], c0 + chunk) : cnt[l + 1];
         IluLevel L;
+        L.pbase = -1;
         L.row_base = (int64_t)srow.size();
         L.ent_base = (int64_t)kcol.size();
-        L.m = cnt[l + 1] - cnt[l];
+        L.m = c1 - c0;
         int c = 0;
-        for (int t = cnt[l]; t < cnt[l + 1]; t++) {
+        for (int t = c0; t < c1; t++) {
           const int64_t i = r0 + ord[t];
           int ci = 0;
           for (int e = rp[i]; e < rp[i + 1]; e++) {
@@ -403,9 +544,9 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
         L.c = c;
         kcol.resize(kcol.size() + (size_t)L.m * c, -1);
         emap.resize(emap.size() + (size_t)L.m * c, -1);
-        for (int t = cnt[l]; t < cnt[l + 1]; t++) {
+        for (int t = c0; t < c1; t++) {
           const int64_t i = r0 + ord[t];
-          const int slot = t - cnt[l];
+          const int slot = t - c0;
           srow.push_back(ord[t]);
           udmap.push_back(d == 1 ? diag[i] : -1);
           int u = 0;
@@ -423,6 +564,44 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
       }
     }
     lo[d * (P->nblk + 1) + P->nblk] = (int)levs.size();
+  }
+  };
+  emit(0);
+  // ---- packed level records (ilu_apply_packed_kernel): at most 4 entries per row and
+  // direction, levels split into records of <= 128 rows, and the block's vector + level
+  // records + ring in shared memory; otherwise the cp.async-ring kernel on the unsplit
+  // levels (PCG_ILU_PACKED=0 forces it)
+  int64_t pk_total = 0;
+  {
+    constexpr int T = 128;
+    auto maxc_of = [&]() {
+      int c = 0;
+      for (const IluLevel &L : levs) c = std::max(c, L.c);
+      return c;
+    };
+    auto maxlev_of = [&]() {
+      int m = 0;
+      for (int64_t b = 0; b < P->nblk; b++)
+        m = std::max(m, (lo[b + 1] - lo[b]) + (lo[P->nblk + 1 + b + 1] - lo[P->nblk + 1 + b]));
+      return m;
+    };
+    const char *pe = getenv("PCG_ILU_PACKED");
+    const int64_t rows = std::min(bs, n);
+    if (!(pe && atoi(pe) == 0) && maxc_of() <= 4 && ilu_packed_smem<T>(0, rows) < ILU_SMEM_MAX) {
+      emit(T);
+      const int ml = maxlev_of();
+      if (ilu_packed_smem<T>(ml, rows) <= ILU_SMEM_MAX) {
+        P->pk_threads = T;
+        P->maxlev = ml;
+        const int64_t nfwd_end = lo[P->nblk];
+        for (int64_t l = 0; l < (int64_t)levs.size(); l++) {
+          levs[l].pbase = pk_total;
+          pk_total += pk_bytes(levs[l].m, levs[l].c, l >= nfwd_end);
+        }
+      } else {
+        emit(0);
+      }
+    }
   }
   P->nlev = (int64_t)levs.size();
   P->nslot = (int64_t)srow.size();
@@ -453,6 +632,17 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
   ilu_fill_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((std::max(P->nent, P->nslot) + 255) / 256, 4096)),
                     256, 0, st>>>(P->nent, P->emap, P->nslot, P->udmap, P->f, P->fv, P->ud);
   count_launch(2);
+  if (P->pk_threads) {
+    if (cudaMalloc(&P->pk, (size_t)std::max<int64_t>(pk_total, 16)) != cudaSuccess) {
+      cudaGetLastError();
+      P->pk = nullptr;
+      P->pk_threads = 0;
+    } else {
+      ilu_pack_kernel<<<(unsigned)P->nlev, 128, 0, st>>>(P->lev, lo[P->nblk], P->lo, P->nblk, P->row, P->kcol, P->fv,
+                                                         P->ud, P->pk);
+      count_launch();
+    }
+  }
   int herr = 0;
   PCG_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   PCG_CUDA(cudaStreamSynchronize(st));
@@ -466,6 +656,12 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
   const size_t vo = ilu_vec_offset(P->cmax);
   P->vec_smem = vo + sizeof(double) * (size_t)maxrows <= ILU_SMEM_MAX;
   P->smem = vo + (P->vec_smem ? sizeof(double) * (size_t)maxrows : 0);
+  if (P->pk_threads) {
+    P->smem = P->pk_threads == 128 ? ilu_packed_smem<128>(P->maxlev, maxrows) : ilu_packed_smem<256>(P->maxlev, maxrows);
+    PCG_CUDA(cudaFuncSetAttribute(P->pk_threads == 128 ? (const void *)ilu_apply_packed_kernel<128>
+                                                       : (const void *)ilu_apply_packed_kernel<256>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem));
+  } else
   for (auto fn : {(const void *)ilu_apply_kernel<true, 4>, (const void *)ilu_apply_kernel<true, 8>,
                   (const void *)ilu_apply_kernel<true, 16>, (const void *)ilu_apply_kernel<false, 4>,
                   (const void *)ilu_apply_kernel<false, 8>, (const void *)ilu_apply_kernel<false, 16>})
@@ -479,8 +675,16 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
 
 void ilu_launch(void *plan, const double *in, double *out, const int *stop, const int *skip, cudaStream_t st) {
   const IluPlan *P = (const IluPlan *)plan;
-  const IluView V{P->bs, P->n, P->nblk, P->lev, P->lo, P->row, P->kcol, P->fv, P->ud};
+  const IluView V{P->bs, P->n, P->nblk, P->lev, P->lo, P->row, P->kcol, P->fv, P->ud, P->pk};
   const unsigned g = (unsigned)P->nblk;
+  if (P->pk_threads) {
+    if (P->pk_threads == 128)
+      ilu_apply_packed_kernel<128><<<g, 128, P->smem, st>>>(V, in, out, stop, skip, P->maxlev);
+    else
+      ilu_apply_packed_kernel<256><<<g, 256, P->smem, st>>>(V, in, out, stop, skip, P->maxlev);
+    count_launch();
+    return;
+  }
 #define ILU_GO(SM, CM) ilu_apply_kernel<SM, CM><<<g, ILU_THREADS, P->smem, st>>>(V, in, out, stop, skip)
   if (P->vec_smem) {
     if (P->cmax == 4) ILU_GO(true, 4);
