@@ -21,12 +21,14 @@ ap.add_argument("--c", type=int, default=None)
 ap.add_argument("--fmt", default="auto")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--solve", action="store_true")
+ap.add_argument("--drop-zeros", action="store_true")
 a = ap.parse_args()
 spec = fem_spec(a.config, c=a.c)
 n, nnz, _ = problem_size(spec)
 P = fem_build(spec)
 nnz = P["col"].numel()  # the 3D element pattern has no closed form (problem_size: -1)
-A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"], fmt=a.fmt)
+A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"], fmt=a.fmt, drop_zeros=a.drop_zeros)
+nnz = A.stats()["nnz"]  # stored entries (fewer with --drop-zeros)
 b = P["B"][:, 0].contiguous()
 del P
 torch.cuda.synchronize()
