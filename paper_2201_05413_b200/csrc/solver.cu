@@ -236,8 +236,8 @@ __global__ void __launch_bounds__(BLOCK) k2_kernel(int64_t n, Vecs v, Scalars *s
 // 36n instead of 40n per iteration, and the SAME fused multiply-adds in the same order
 // as the every-iteration update, so x is bitwise the same.  The tail applies what a
 // stop leaves owed (Scalars::xhold, alpha_old).
-__device__ __forceinline__ void k1a_deferred(int64_t n, const Vecs &v, double beta, double alpha, double alpha_old,
-                                             int xdefer) {
+__device__ __forceinline__ void k1a_deferred(int64_t n, int64_t n_ghost, const Vecs &v, double beta, double alpha,
+                                             double alpha_old, int xdefer) {
   const int64_t npair = n >> 1;
   const double2 *__restrict__ z2 = reinterpret_cast<const double2 *>(v.z);
   const int64_t t = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nt = (int64_t)gridDim.x * BLOCK;
@@ -249,6 +249,7 @@ __device__ __forceinline__ void k1a_deferred(int64_t n, const Vecs &v, double be
       b2[i] = make_double2(__fma_rn(beta, po.x, zz.x), __fma_rn(beta, po.y, zz.y));
     }
     if ((n & 1) && t == 0) v.p1[n - 1] = __fma_rn(beta, v.p0[n - 1], v.z[n - 1]);
+    for (int64_t g = t; g < n_ghost; g += nt) v.p1[n + g] = __fma_rn(beta, v.p0[n + g], v.z[n + g]);
   } else {
     double2 *__restrict__ a2 = reinterpret_cast<double2 *>(v.p0);
     const double2 *__restrict__ b2 = reinterpret_cast<const double2 *>(v.p1);
@@ -267,6 +268,7 @@ __device__ __forceinline__ void k1a_deferred(int64_t n, const Vecs &v, double be
       v.x[i] = __fma_rn(alpha, pk, __fma_rn(alpha_old, v.p0[i], v.x[i]));
       v.p0[i] = __fma_rn(beta, pk, v.z[i]);
     }
+    for (int64_t g = t; g < n_ghost; g += nt) v.p0[n + g] = __fma_rn(beta, v.p1[n + g], v.z[n + g]);
   }
 }
 
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, 
   }
   const double beta = vs->beta, alpha_prev = vs->alpha;
   if (xdefer) {
-    k1a_deferred(n, v, beta, alpha_prev, vs->alpha_old, xdefer);
+    k1a_deferred(n, n_ghost, v, beta, alpha_prev, vs->alpha_old, xdefer);
     return;
   }
   double *__restrict__ p = v.p0;
@@ -366,18 +368,22 @@ __global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) k1b_kernel(SellView S, C
 }
 
 // distributed overlap: ghost copies of p advance once the z halo has arrived
-__global__ void __launch_bounds__(BLOCK) ghost_p_kernel(int64_t n, int64_t n_ghost, Vecs v, const Scalars *sc) {
+// (deferred x update: a hold iteration advances p[0] -> p[1], an apply iteration p[1] -> p[0])
+__global__ void __launch_bounds__(BLOCK) ghost_p_kernel(int64_t n, int64_t n_ghost, Vecs v, const Scalars *sc,
+                                                        int xdefer) {
   const volatile Scalars *vs = sc;
   if (vs->done != DONE_RUNNING) return;
   const double beta = vs->beta;
+  const double *src = xdefer == 2 ? v.p1 : v.p0;
+  double *dst = xdefer == 1 ? v.p1 : v.p0;
   for (int64_t g = (int64_t)blockIdx.x * BLOCK + threadIdx.x; g < n_ghost; g += (int64_t)gridDim.x * BLOCK)
-    v.p0[n + g] = __fma_rn(beta, v.p0[n + g], v.z[n + g]);
+    dst[n + g] = __fma_rn(beta, src[n + g], v.z[n + g]);
 }
 
 // distributed finishers (after the NCCL allreduce of the partials)
-__global__ void finish_alpha_kernel(Scalars *sc, int use_cond, cudaGraphConditionalHandle h, int flip) {
+__global__ void finish_alpha_kernel(Scalars *sc, int use_cond, cudaGraphConditionalHandle h, int flip, int xdefer) {
   if (sc->done != DONE_RUNNING) return;
-  finish_alpha(sc, sc->sigma, use_cond, h, flip);
+  finish_alpha(sc, sc->sigma, use_cond, h, flip, xdefer);
 }
 __global__ void finish_beta_kernel(Scalars *sc, int use_cond, cudaGraphConditionalHandle h) {
   if (sc->done != DONE_RUNNING) return;
@@ -603,8 +609,10 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     // after the join the ghost p update and K1b over the boundary rows (head, tail)
     PCG_CUDA(cudaEventRecord(A->ov_fork, st));
     PCG_CUDA(cudaStreamWaitEvent(A->ov_side, A->ov_fork, 0));
-    k1a_kernel<<<A->grid_vec, BLOCK, 0, A->ov_side>>>(A->n, 0, v, w.sc, use_cond, h, 0);
+    k1a_kernel<<<A->grid_vec, BLOCK, 0, A->ov_side>>>(A->n, 0, v, w.sc, use_cond, h, xdefer);
     count_launch();
+    Vecs vb = v;
+    if (xdefer == 1) vb.p0 = v.p1;  // a hold iteration writes p_k to p[1]
     struct Range {
       int64_t r0, r1;
     } rs[3] = {{A->ov_ia, A->ov_ib}, {0, A->ov_ia}, {A->ov_ib, A->n}};
@@ -616,7 +624,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
         PCG_TRY(halo_exchange(A, w.z, 1, st));
         PCG_CUDA(cudaStreamWaitEvent(st, A->ov_join, 0));
         ghost_p_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((A->n_ghost + BLOCK - 1) / BLOCK, 1184)),
-                         BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc);
+                         BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, xdefer);
         count_launch();
       }
       if (R.r1 <= R.r0) continue;
@@ -635,13 +643,13 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
       const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(A->grid_spmv, need));
       cudaStream_t ks = t == 0 ? A->ov_side : st;
       PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
-                       <<<g, BLOCK, A->dyn_smem, ks>>>(S, Cv, A->n_ghost, v, w.sc, w.partials, 1, use_cond, h, R.r0,
+                       <<<g, BLOCK, A->dyn_smem, ks>>>(S, Cv, A->n_ghost, vb, w.sc, w.partials, 1, use_cond, h, R.r0,
                                                       phase, 0));
       count_launch();
     }
     PCG_CUDA(cudaGetLastError());
     PCG_TRY(allreduce_sum(A, &w.sc->sigma, 1, st));
-    finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h, 0);
+    finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h, 0, xdefer);
     count_launch();
     return PCG_OK;
   }
@@ -657,7 +665,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     PCG_CUDA(cudaGetLastError());
     if (A->comm) {
       PCG_TRY(allreduce_sum(A, &w.sc->sigma, 1, st));
-      finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h, 0);
+      finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h, 0, xdefer);
       count_launch();
     }
     return PCG_OK;
@@ -673,7 +681,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
   PCG_CUDA(cudaGetLastError());
   if (A->comm) {
     PCG_TRY(allreduce_sum(A, &w.sc->sigma, 1, st));
-    finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h, 1);
+    finish_alpha_kernel<<<1, 1, 0, st>>>(w.sc, use_cond, h, 1, 0);
     count_launch();
   }
   return PCG_OK;
@@ -713,10 +721,10 @@ static pcg_status launch_resid(pcg_matrix *A, const double *b, int mode, cudaStr
   return PCG_OK;
 }
 
-// deferred x update (k1a_deferred): single GPU, 3-pass schedule; PCG_XDEFER=0 turns it off
+// deferred x update (k1a_deferred): 3-pass schedule (one GPU or distributed); PCG_XDEFER=0 turns it off
 static bool xdefer_wanted(const pcg_matrix *A) {
   const char *xd = getenv("PCG_XDEFER");
-  return !A->comm && A->schedule == 3 && !(xd && atoi(xd) == 0);
+  return A->schedule == 3 && !(xd && atoi(xd) == 0);
 }
 
 // Build the loop graph once per handle: WHILE(cond) { K1; K2 } (1 GPU), or an
@@ -765,8 +773,8 @@ static pcg_status build_loop_graph(pcg_matrix *A) {
   } else {
     const int U = 8;
     PCG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    for (int u = 0; u < U && st == PCG_OK; u++) {
-      st = launch_k1(A, cap, 0, 0);
+    for (int u = 0; u < U && st == PCG_OK; u++) {  // U even: hold / apply pairs
+      st = launch_k1(A, cap, 0, 0, w.xdefer ? 1 + (u & 1) : 0);
       if (st == PCG_OK) st = launch_k2(A, cap, 0, 0);
     }
     cudaGraph_t out;

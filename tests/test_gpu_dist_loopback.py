@@ -53,10 +53,17 @@ def _worker(rank, world, port, name, c, use_generator, out_q, drop=False):
         M = pcg.Matrix.from_csr_dist(comm, A.n, r0, r1, rp, col, val, drop_zeros=drop)
         st = M.stats()
         x, info = M.solve(bl, tol=1e-10)
+        # the every-iteration x update (PCG_XDEFER=0) on a second handle: bitwise the same
+        os.environ["PCG_XDEFER"] = "0"
+        M0 = pcg.Matrix.from_csr_dist(comm, A.n, r0, r1, rp, col, val, drop_zeros=drop)
+        x0e, info0e = M0.solve(bl, tol=1e-10)
+        del os.environ["PCG_XDEFER"]
+        M0.close()
         xp, infop = M.solve_pipelined(bl, tol=1e-10)  # N3: one allreduce per iteration
         xr = np.random.default_rng(100 + rank).standard_normal(r1 - r0)
         y = M.spmv(torch.as_tensor(xr).cuda()).cpu().numpy()
         out_q.put((rank, dict(r0=r0, r1=r1, n_ghost=st["n_ghost"], overlap_rows=st["overlap_rows"], x=x.cpu().numpy(), info=info, xr=xr, y=y,
+                              x_every=x0e.cpu().numpy(), it_every=info0e["iterations"],
                               b=bl.cpu().numpy(), xp=xp.cpu().numpy(), infop=infop)))
         M.close()
         comm.close()
@@ -122,6 +129,8 @@ def test_distributed_path_on_one_gpu(world, name, c, gen, drop):
     assert all(d["info"]["status"] == 0 and d["info"]["relres_true"] <= tol for d in parts)
     assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) <= 1e-9
     assert abs(it - r.iterations) <= max(1, 0.02 * r.iterations), (it, r.iterations)
+    # x updated every second iteration (default) == every iteration, bitwise, on every rank
+    assert all(d["it_every"] == it and np.array_equal(d["x"], d["x_every"]) for d in parts)
 
 
 @pytest.mark.parametrize("world,name,c", [(2, "C1", None), (3, "C4", 24), (2, "C2", 48)])
@@ -230,6 +239,24 @@ def test_nccl_single_rank_distributed_handle(force_overlap, monkeypatch):
         assert info["status"] == 0 and info["relres_true"] <= 1e-10
         assert np.linalg.norm(x.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-9
         assert abs(info["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
+        # the loop graph with x updated every iteration: bitwise the same x
+        monkeypatch.setenv("PCG_XDEFER", "0")
+        M0 = pcg.Matrix.from_csr_dist(comm, A.n, 0, A.n, torch.as_tensor(A.row_ptr).cuda(),
+                                      torch.as_tensor(A.col).cuda(), torch.as_tensor(A.val).cuda())
+        x0, i0 = M0.solve(torch.as_tensor(b).cuda(), tol=1e-10)
+        monkeypatch.delenv("PCG_XDEFER")
+        assert i0["iterations"] == info["iterations"] and bool((x0 == x).all())
+        M0.close()
+        # max_iter stops after hold and apply passes: bitwise too
+        for mi in (5, 6):
+            xa, _ = M.solve(torch.as_tensor(b).cuda(), tol=1e-10, max_iter=mi)
+            monkeypatch.setenv("PCG_XDEFER", "0")
+            M1 = pcg.Matrix.from_csr_dist(comm, A.n, 0, A.n, torch.as_tensor(A.row_ptr).cuda(),
+                                          torch.as_tensor(A.col).cuda(), torch.as_tensor(A.val).cuda())
+            xb, _ = M1.solve(torch.as_tensor(b).cuda(), tol=1e-10, max_iter=mi)
+            monkeypatch.delenv("PCG_XDEFER")
+            M1.close()
+            assert bool((xa == xb).all()), mi
         # the pipelined solver's distributed schedule through NCCL (one allreduce per step)
         xp, ip = M.solve_pipelined(torch.as_tensor(b).cuda(), tol=1e-10)
         rp = O.pcg_pipelined(A, b, tol=1e-10)
@@ -403,6 +430,24 @@ def test_device_allreduce_single_rank_nccl_solves(monkeypatch):
         assert info["status"] == 0 and info["relres_true"] <= 1e-10
         assert np.linalg.norm(x.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-9
         assert abs(info["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
+        # the loop graph with x updated every iteration: bitwise the same x
+        monkeypatch.setenv("PCG_XDEFER", "0")
+        M0 = pcg.Matrix.from_csr_dist(comm, A.n, 0, A.n, torch.as_tensor(A.row_ptr).cuda(),
+                                      torch.as_tensor(A.col).cuda(), torch.as_tensor(A.val).cuda())
+        x0, i0 = M0.solve(torch.as_tensor(b).cuda(), tol=1e-10)
+        monkeypatch.delenv("PCG_XDEFER")
+        assert i0["iterations"] == info["iterations"] and bool((x0 == x).all())
+        M0.close()
+        # max_iter stops after hold and apply passes: bitwise too
+        for mi in (5, 6):
+            xa, _ = M.solve(torch.as_tensor(b).cuda(), tol=1e-10, max_iter=mi)
+            monkeypatch.setenv("PCG_XDEFER", "0")
+            M1 = pcg.Matrix.from_csr_dist(comm, A.n, 0, A.n, torch.as_tensor(A.row_ptr).cuda(),
+                                          torch.as_tensor(A.col).cuda(), torch.as_tensor(A.val).cuda())
+            xb, _ = M1.solve(torch.as_tensor(b).cuda(), tol=1e-10, max_iter=mi)
+            monkeypatch.delenv("PCG_XDEFER")
+            M1.close()
+            assert bool((xa == xb).all()), mi
         xp, ip = M.solve_pipelined(torch.as_tensor(b).cuda(), tol=1e-10)
         assert ip["status"] == 0 and np.linalg.norm(xp.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-8
         M.close()
