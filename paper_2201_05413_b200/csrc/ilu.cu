@@ -17,7 +17,12 @@
 // on the host; it lays the factor out level by level in an ELL form ([level][entry
 // u][row slot]: a level's loads are coalesced): per slot the local row, per (u, slot)
 // the local column (-1 = padding) and the factor value.  The numeric factorization
-// runs on the device, in the forward level order.
+// runs on the device, in the forward level order.  Where every row has at most 4
+// entries per triangle and a block fits shared memory (the Table 1 grids), the levels
+// are split into records of at most 128 rows and each record's data is also packed
+// contiguously, so the application brings a level in with one bulk copy
+// (ilu_apply_packed_kernel); otherwise each thread streams its slot through a cp.async
+// ring (ilu_apply_kernel).
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -144,9 +149,9 @@ struct IluView {
 };
 
 // the packed level records, written once after the factorization (one CTA per level)
-__global__ void ilu_pack_kernel(const IluLevel *__restrict__ lev, int64_t nfwd_end, const int *__restrict__ lo,
-                                int64_t nblk, const int *__restrict__ row, const int *__restrict__ kcol,
-                                const double *__restrict__ fv, const double *__restrict__ ud, unsigned char *pk) {
+__global__ void ilu_pack_kernel(const IluLevel *__restrict__ lev, int64_t nfwd_end, const int *__restrict__ row,
+                                const int *__restrict__ kcol, const double *__restrict__ fv,
+                                const double *__restrict__ ud, unsigned char *pk) {
   const int64_t l = blockIdx.x;
   const IluLevel L = lev[l];
   if (L.pbase < 0) return;
@@ -638,8 +643,7 @@ pcg_status ilu_setup(pcg_matrix *A, int64_t bs, cudaStream_t st, void **plan_out
       P->pk = nullptr;
       P->pk_threads = 0;
     } else {
-      ilu_pack_kernel<<<(unsigned)P->nlev, 128, 0, st>>>(P->lev, lo[P->nblk], P->lo, P->nblk, P->row, P->kcol, P->fv,
-                                                         P->ud, P->pk);
+      ilu_pack_kernel<<<(unsigned)P->nlev, 128, 0, st>>>(P->lev, lo[P->nblk], P->row, P->kcol, P->fv, P->ud, P->pk);
       count_launch();
     }
   }
