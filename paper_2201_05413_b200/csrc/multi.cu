@@ -37,6 +37,7 @@ namespace pcgb {
 
 struct MVecs {
   double *R, *Z, *Q, *P, *X, *W;
+  double *P1;        // deferred x update: the second direction block (hold passes write it)
   const double *Bm;  // right-hand sides (column-major, ld)
   const double *dinv;
   int64_t ld;        // leading dimension (n rounded up to 32)
@@ -114,23 +115,42 @@ __device__ void mcols_reduce_n(const double *partials, int nb, int k, double (*o
 }
 
 // ---------------------------------------------------------------- finishers (thread 0 of the last block)
-__device__ void mk1b_finish(const double *sig, MultiScalars *sc, int use_cond, cudaGraphConditionalHandle h) {
+// pass: 0 = x updated every iteration; deferred x update (mk1a_kernel): 1 = hold (the
+// owed alpha of the direction in P stays owed, the new direction is in P1), 2 = apply
+__device__ void mk1b_finish(const double *sig, MultiScalars *sc, int use_cond, cudaGraphConditionalHandle h,
+                            int pass) {
   sc->cnt_a = 0;
   int na = 0;
   for (int c = 0; c < sc->kcols; c++) {
     if (!sc->active[c]) {
       sc->xpend[c] = 0.0;  // an owed x update was applied by this iteration's K1a
+      sc->xhold[c] = 0.0;
       continue;
     }
     const double sigma = sig[c];
     sc->sigma[c] = sigma;
+    const double owed = sc->xpend[c];  // alpha of the direction this iteration's K1a read
     if (!(sigma > 0.0)) {  // p^T A p <= 0: breakdown, A not SPD
       sc->done[c] = DONE_BREAKDOWN;
       sc->active[c] = 0;
       sc->xpend[c] = 0.0;
+      if (pass == 1) {  // a hold pass left alpha_{k-1} p_{k-1} (in P) owed
+        sc->xhold[c] = owed;
+        sc->lbuf[c] = 1;
+      } else {
+        sc->xhold[c] = 0.0;
+        sc->lbuf[c] = 0;
+      }
     } else {
       sc->alpha[c] = sc->rho[c] / sigma;
       sc->xpend[c] = sc->alpha[c];  // x += alpha p is deferred to the next K1a / the tail
+      if (pass == 1) {
+        sc->xhold[c] = owed;
+        sc->lbuf[c] = 1;
+      } else if (pass == 2) {
+        sc->xhold[c] = 0.0;
+        sc->lbuf[c] = 0;
+      }
       sc->k[c] += 1;
       na++;
     }
@@ -173,14 +193,75 @@ __device__ void mk2_finish(const double (*t)[KMAX], MultiScalars *sc, int use_co
 // ---------------------------------------------------------------- K1a: X_c += xpend_c P_c ; P_c = Z_c + beta_c P_c
 // grid (gx, k): blockIdx.y = column.  Just-frozen columns only receive their owed
 // x update; settled frozen columns return at entry.
-__global__ void __launch_bounds__(BLOCK) mk1a_kernel(int64_t n, MVecs v, MultiScalars *sc, int use_cond,
-                                                     cudaGraphConditionalHandle h) {
+// Deferred x update (pass 1 / 2, as the single-RHS k1a_kernel): a hold pass writes
+// P1_c = Z_c + beta_c P_c and leaves X_c alone; an apply pass applies both owed updates,
+// X_c = fma(xpend_c, P1_c, fma(xhold_c, P_c, X_c)), and writes P_c = Z_c + beta_c P1_c —
+// the fused multiply-adds of the every-iteration update in the same order (bitwise the
+// same X).  A just-frozen column applies what it owes (held, then latest: P[lbuf_c]).
+__device__ __forceinline__ void mk1a_deferred(int64_t n, const MVecs &v, const volatile MultiScalars *vs, int c,
+                                              int pass) {
+  const double xp = vs->xpend[c], xh = vs->xhold[c], beta = vs->beta[c];
+  const int act = vs->active[c];
+  if (!act && xp == 0.0 && xh == 0.0) return;
+  double *__restrict__ P0 = v.P + (size_t)c * v.ld;
+  double *__restrict__ P1 = v.P1 + (size_t)c * v.ld;
+  double *__restrict__ X = v.X + (size_t)c * v.ld;
+  const double *__restrict__ Z = v.Z + (size_t)c * v.ld;
+  const int64_t t0 = (int64_t)blockIdx.x * BLOCK + threadIdx.x, ts = (int64_t)gridDim.x * BLOCK;
+  if (!act) {  // just frozen: the owed updates, held direction first
+    const int lb = vs->lbuf[c];
+    const double *Pl = lb ? P1 : P0, *Ph = lb ? P0 : P1;
+    for (int64_t i = t0; i < n; i += ts) {
+      double x = X[i];
+      if (xh != 0.0) x = __fma_rn(xh, Ph[i], x);
+      if (xp != 0.0) x = __fma_rn(xp, Pl[i], x);
+      X[i] = x;
+    }
+    return;
+  }
+  const int64_t npair = n >> 1;
+  const double2 *__restrict__ Z2 = reinterpret_cast<const double2 *>(Z);
+  if (pass == 1) {
+    const double2 *__restrict__ A2 = reinterpret_cast<const double2 *>(P0);
+    double2 *__restrict__ B2 = reinterpret_cast<double2 *>(P1);
+    for (int64_t t = t0; t < npair; t += ts) {
+      const double2 po = __ldcs(A2 + t), zz = __ldcs(Z2 + t);
+      B2[t] = make_double2(__fma_rn(beta, po.x, zz.x), __fma_rn(beta, po.y, zz.y));
+    }
+    if ((n & 1) && t0 == 0) P1[n - 1] = __fma_rn(beta, P0[n - 1], Z[n - 1]);
+  } else {
+    double2 *__restrict__ A2 = reinterpret_cast<double2 *>(P0);
+    const double2 *__restrict__ B2 = reinterpret_cast<const double2 *>(P1);
+    double2 *__restrict__ X2 = reinterpret_cast<double2 *>(X);
+    for (int64_t t = t0; t < npair; t += ts) {
+      const double2 pk = B2[t], pm = __ldcs(A2 + t), zz = __ldcs(Z2 + t);
+      double2 xx = __ldcs(X2 + t);
+      xx.x = __fma_rn(xp, pk.x, __fma_rn(xh, pm.x, xx.x));
+      xx.y = __fma_rn(xp, pk.y, __fma_rn(xh, pm.y, xx.y));
+      __stcs(X2 + t, xx);
+      A2[t] = make_double2(__fma_rn(beta, pk.x, zz.x), __fma_rn(beta, pk.y, zz.y));
+    }
+    if ((n & 1) && t0 == 0) {
+      const int64_t i = n - 1;
+      const double pk = P1[i];
+      X[i] = __fma_rn(xp, pk, __fma_rn(xh, P0[i], X[i]));
+      P0[i] = __fma_rn(beta, pk, Z[i]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(BLOCK, 4) mk1a_kernel(int64_t n, MVecs v, MultiScalars *sc, int use_cond,
+                                                     cudaGraphConditionalHandle h, int pass) {
   const volatile MultiScalars *vs = sc;
   if (vs->n_active == 0) {
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) mstop(use_cond, h);
     return;
   }
   const int c = blockIdx.y;
+  if (pass) {
+    mk1a_deferred(n, v, vs, c, pass);
+    return;
+  }
   const double xp = vs->xpend[c], beta = vs->beta[c];
   const int act = vs->active[c];
   if (!act && xp == 0.0) return;
@@ -258,7 +339,8 @@ __device__ __forceinline__ double long_row_sum(const double *vp, const int *cp, 
 // them to the warp's accumulator in slice order; warps are combined in order.
 template <int MODE, bool LONG>
 __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, MVecs v, MultiScalars *sc, double *partials, int k,
-                                                      int pf, int use_cond, cudaGraphConditionalHandle h) {
+                                                      int pf, int use_cond, cudaGraphConditionalHandle h,
+                                                      int pass) {
   constexpr int NV = MODE == MS_SPMM ? 1 : 3;
   __shared__ int s_act[KMAX];
   __shared__ double s_red[NV][WARPS][KMAX];
@@ -393,7 +475,7 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
   mcols_reduce<NV>(partials, gridDim.x, k, s_out, s_sm);
   if (threadIdx.x == 0) {
     if (MODE == MS_SPMM) {
-      mk1b_finish(s_out[0], sc, use_cond, h);
+      mk1b_finish(s_out[0], sc, use_cond, h, pass);
     } else {
       sc->cnt_c = 0;
       for (int c = 0; c < KMAX; c++)
@@ -536,16 +618,26 @@ __global__ void mreplace_kernel(int64_t n, MVecs v, const MultiScalars *sc) {
 }
 
 // deferred X_c += xpend_c P_c after the loop stops; grid (gx, k)
+// (deferred x update: the held direction first, then the latest one in P[lbuf])
 __global__ void mtail_kernel(int64_t n, MVecs v, const MultiScalars *sc) {
   const int c = blockIdx.y;
-  const double xp = sc->xpend[c];
-  if (xp == 0.0) return;
+  const double xp = sc->xpend[c], xh = sc->xhold[c];
+  if (xp == 0.0 && xh == 0.0) return;
   const size_t o = (size_t)c * v.ld;
-  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK)
-    v.X[o + i] = __fma_rn(xp, v.P[o + i], v.X[o + i]);
+  const double *Pl = (sc->lbuf[c] ? v.P1 : v.P) + o, *Ph = (sc->lbuf[c] ? v.P : v.P1) + o;
+  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
+    double x = v.X[o + i];
+    if (xh != 0.0) x = __fma_rn(xh, Ph[i], x);
+    if (xp != 0.0) x = __fma_rn(xp, Pl[i], x);
+    v.X[o + i] = x;
+  }
 }
 __global__ void mclear_xpend_kernel(MultiScalars *sc) {
-  for (int c = 0; c < KMAX; c++) sc->xpend[c] = 0.0;
+  for (int c = 0; c < KMAX; c++) {
+    sc->xpend[c] = 0.0;
+    sc->xhold[c] = 0.0;
+    sc->lbuf[c] = 0;
+  }
 }
 // x = 0 for b = 0 columns; grid (gx, k)
 __global__ void mzero_rhs_kernel(int64_t n, MVecs v, const MultiScalars *sc) {
@@ -561,9 +653,9 @@ static int64_t mld(int64_t n) { return ((n > 0 ? n : 1) + 31) / 32 * 32; }
 pcg_status ensure_multi_work(pcg_matrix *A, int k) {
   SolveWork &w = A->work;
   if (w.kcap >= k && w.msc) return PCG_OK;
-  for (double *p : {w.mr, w.mz, w.mq, w.mp[0], w.mx, w.mb, w.mw})
+  for (double *p : {w.mr, w.mz, w.mq, w.mp[0], w.mp[1], w.mx, w.mb, w.mw})
     if (p) cudaFree(p);
-  w.mr = w.mz = w.mq = w.mp[0] = w.mx = w.mb = w.mw = nullptr;
+  w.mr = w.mz = w.mq = w.mp[0] = w.mp[1] = w.mx = w.mb = w.mw = nullptr;
   if (w.mloop_exec) cudaGraphExecDestroy(w.mloop_exec);
   if (w.mloop_graph) cudaGraphDestroy(w.mloop_graph);
   w.mloop_exec = nullptr;
@@ -575,6 +667,8 @@ pcg_status ensure_multi_work(pcg_matrix *A, int k) {
   PCG_CUDA(cudaMalloc(&w.mz, nk));
   PCG_CUDA(cudaMalloc(&w.mq, nk));
   PCG_CUDA(cudaMalloc(&w.mp[0], nk));
+  PCG_CUDA(cudaMalloc(&w.mp[1], nk));
+  PCG_CUDA(cudaMemset(w.mp[1], 0, nk));
   PCG_CUDA(cudaMalloc(&w.mx, nk));
   PCG_CUDA(cudaMalloc(&w.mb, nk));
   PCG_CUDA(cudaMalloc(&w.mw, nk));
@@ -594,7 +688,7 @@ pcg_status ensure_multi_work(pcg_matrix *A, int k) {
 
 static MVecs mvecs_of(pcg_matrix *A) {
   SolveWork &w = A->work;
-  return MVecs{w.mr, w.mz, w.mq, w.mp[0], w.mx, w.mw, w.mb, A->d_dinv, mld(A->n)};
+  return MVecs{w.mr, w.mz, w.mq, w.mp[0], w.mx, w.mw, w.mp[1], w.mb, A->d_dinv, mld(A->n)};
 }
 
 // streaming passes: grid (gx, k) with gx * k ~ 8 blocks per SM
@@ -887,7 +981,7 @@ __global__ void __launch_bounds__(W_THREADS, 3)
   }
   if (!mlast_block(&sc->cnt_a)) return;
   mcols_reduce_n<1>(partials, gridDim.x, k, s_out, s_sm);
-  if (threadIdx.x == 0) mk1b_finish(s_out[0], sc, use_cond, h);
+  if (threadIdx.x == 0) mk1b_finish(s_out[0], sc, use_cond, h, 0);  // (the deferred x update is off here)
 }
 
 static size_t win_smem() { return (size_t)W_STAGES * W_CAP * 8 + 2 * W_STAGES * 8; }
@@ -948,7 +1042,8 @@ static int spmm_prefetch() {
 }
 
 template <int MODE>
-static void launch_mspmm(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
+static void launch_mspmm(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h,
+                         int pass = 0) {
   SolveWork &w = A->work;
   if (MODE == MS_SPMM && A->wplan == 1) {
     mspmm_win_kernel<<<win_grid(A), W_THREADS, win_smem(), st>>>(A->sell(), (const WinDesc *)A->d_wdesc, A->d_wlidx,
@@ -957,12 +1052,13 @@ static void launch_mspmm(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cu
   }
   const int g = mgrid_spmm(A, k);
   const SellView S = A->sell();
-  const MVecs v = mvecs_of(A);
+  MVecs v = mvecs_of(A);
+  if (pass == 1) v.P = v.P1;  // a hold pass wrote the directions to P1
   const size_t smem = MODE == MS_SPMM && k <= 16 ? sizeof(double) * BLOCK * k : 0;
   if (A->max_row_len > 8)
-    mspmm_kernel<MODE, true><<<g, BLOCK, smem, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
+    mspmm_kernel<MODE, true><<<g, BLOCK, smem, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h, pass);
   else
-    mspmm_kernel<MODE, false><<<g, BLOCK, smem, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h);
+    mspmm_kernel<MODE, false><<<g, BLOCK, smem, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h, pass);
 }
 
 // ---------------------------------------------------------------- the SpMM alone, for block CG (blockcg.cu)
@@ -1001,9 +1097,9 @@ pcg_status block_spmm(pcg_matrix *A, const double *P, double *Q, int k, int64_t 
   v.ld = ld;
   const size_t smem = k <= 16 ? sizeof(double) * BLOCK * k : 0;
   if (A->max_row_len > 8)
-    mspmm_kernel<MS_SPMM, true><<<g, BLOCK, smem, st>>>(A->sell(), v, sc, w.bspmm_part, k, spmm_prefetch(), 0, 0);
+    mspmm_kernel<MS_SPMM, true><<<g, BLOCK, smem, st>>>(A->sell(), v, sc, w.bspmm_part, k, spmm_prefetch(), 0, 0, 0);
   else
-    mspmm_kernel<MS_SPMM, false><<<g, BLOCK, smem, st>>>(A->sell(), v, sc, w.bspmm_part, k, spmm_prefetch(), 0, 0);
+    mspmm_kernel<MS_SPMM, false><<<g, BLOCK, smem, st>>>(A->sell(), v, sc, w.bspmm_part, k, spmm_prefetch(), 0, 0, 0);
   count_launch(2);
   PCG_CUDA(cudaGetLastError());
   return PCG_OK;
@@ -1011,12 +1107,20 @@ pcg_status block_spmm(pcg_matrix *A, const double *P, double *Q, int k, int64_t 
 
 static double *mpart_rz(pcg_matrix *A) { return A->work.mpart + (size_t)3 * KMAX * num_sms(A->device) * 8; }
 
-static pcg_status mlaunch_iteration(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h) {
+// deferred x update for the k-column loop (mk1a_deferred): not with the windowed SpMM
+// (opt-in); PCG_XDEFER=0 turns it off
+static bool mxdefer(const pcg_matrix *A) {
+  const char *e = getenv("PCG_XDEFER");
+  return A->wplan != 1 && !(e && atoi(e) == 0);
+}
+
+static pcg_status mlaunch_iteration(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h,
+                                    int pass) {
   SolveWork &w = A->work;
   MVecs v = mvecs_of(A);
   const dim3 gv = mgrid_vec(A, k);
-  mk1a_kernel<<<gv, BLOCK, 0, st>>>(A->n, v, w.msc, use_cond, h);
-  launch_mspmm<MS_SPMM>(A, k, st, use_cond, h);
+  mk1a_kernel<<<gv, BLOCK, 0, st>>>(A->n, v, w.msc, use_cond, h, pass);
+  launch_mspmm<MS_SPMM>(A, k, st, use_cond, h, pass);
   mk2_kernel<<<gv, BLOCK, 0, st>>>(A->n, v, w.msc, mpart_rz(A), use_cond, h);
   count_launch(3);
   PCG_CUDA(cudaGetLastError());
@@ -1047,7 +1151,9 @@ static pcg_status mbuild_graph(pcg_matrix *A, int k) {
   cudaGraph_t body = np.conditional.phGraph_out[0];
   PCG_CUDA(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   pcg_status s = PCG_OK;
-  for (int u = 0; u < 2 && s == PCG_OK; u++) s = mlaunch_iteration(A, k, cap, 1, h);  // body = two iterations
+  const bool xd = mxdefer(A);
+  for (int u = 0; u < 2 && s == PCG_OK; u++)  // body = two iterations (hold, apply)
+    s = mlaunch_iteration(A, k, cap, 1, h, xd ? 1 + u : 0);
   cudaGraph_t out;
   cudaError_t e = cudaStreamEndCapture(cap, &out);
   if (s != PCG_OK) return s;
@@ -1163,7 +1269,7 @@ static pcg_status solve_multi_chunk(pcg_matrix *A, int k, const double *B, int64
       const double nn = (double)n, nz = (double)A->nnz;
       // the matrix pass is shared: per block iteration 12 nnz + 4(n+1), attributed 1/k per
       // column, plus 96 n per column iteration (SURVEY §8(d), 3-pass schedule)
-      I.bytes_algorithmic = (double)kmax * (12.0 * nz + 4.0 * (nn + 1)) / k + (double)h->k[c] * 96.0 * nn;
+      I.bytes_algorithmic = (double)kmax * (12.0 * nz + 4.0 * (nn + 1)) / k + (double)h->k[c] * (mxdefer(A) ? 92.0 : 96.0) * nn;
       I.flops = (double)h->k[c] * (2.0 * nz + 13.0 * nn);
     }
   }
@@ -1204,9 +1310,10 @@ extern "C" pcg_status pcg_profile_multi(pcg_matrix_t A, int32_t k, const double 
   for (auto &e : ev) PCG_CUDA(cudaEventCreate(&e));
   PCG_CUDA(cudaEventRecord(ev[0], st));
   for (int r = 0; r < reps; r++) {
-    mk1a_kernel<<<gv, BLOCK, 0, st>>>(n, v, w.msc, 0, 0);
+    const int pass = mxdefer(A) ? 1 + (r & 1) : 0;
+    mk1a_kernel<<<gv, BLOCK, 0, st>>>(n, v, w.msc, 0, 0, pass);
     PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
-    launch_mspmm<MS_SPMM>(A, k, st, 0, 0);
+    launch_mspmm<MS_SPMM>(A, k, st, 0, 0, pass);
     PCG_CUDA(cudaEventRecord(ev[3 * r + 2], st));
     mk2_kernel<<<gv, BLOCK, 0, st>>>(n, v, w.msc, mpart_rz(A), 0, 0);
     PCG_CUDA(cudaEventRecord(ev[3 * r + 3], st));

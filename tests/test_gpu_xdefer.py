@@ -131,3 +131,71 @@ def test_deferred_x_bitwise_breakdown(pcg, monkeypatch):
         assert np.array_equal(xd, xe), f
         parities.add(r.iterations % 2)
     assert parities == {0, 1}
+
+
+# ---------------------------------------------------------------- k right-hand sides (mk1a_deferred)
+def _mpair(pcg, monkeypatch, A, k):
+    out = []
+    for xd in ("1", "0"):
+        monkeypatch.setenv("PCG_XDEFER", xd)
+        M = pcg.Matrix.from_csr(_dev(A.row_ptr), _dev(A.col), _dev(A.val), fmt="sell")
+        _msolve(M, np.ones((A.n, k)), max_iter=3)  # builds the k-column loop graph under this env
+        out.append(M)
+    monkeypatch.delenv("PCG_XDEFER")
+    return out
+
+
+def _msolve(M, B, **kw):
+    import torch
+    from paper_2201_05413_b200 import PcgError
+    X = torch.zeros((B.shape[1], B.shape[0]), dtype=torch.float64, device="cuda").t()  # column-major
+    try:
+        _, infos = M.solve_multi(_dev(B), out=X, **kw)
+        st = [i["status"] for i in infos]
+        its = [i["iterations"] for i in infos]
+        reps = [i["replacements"] for i in infos]
+    except PcgError as e:
+        infos, st, its, reps = None, e.status, None, None
+    return X.cpu().numpy(), st, its, reps
+
+
+def test_deferred_x_multi_bitwise(pcg, monkeypatch):
+    """C4's k = 16 Gaussian-bump columns converge at different iterations (549-578), so
+    columns freeze after hold and after apply passes; max_iter odd and even; below
+    attainable accuracy (per-column replacements).  X bitwise the every-iteration X."""
+    P = O.build_problem("C4", c=16, k=16)
+    A, B = P["A"], P["B"]
+    Md, Me = _mpair(pcg, monkeypatch, A, 16)
+    xd, sd, itd, _ = _msolve(Md, B, tol=1e-10)
+    xe, se, ite, _ = _msolve(Me, B, tol=1e-10)
+    assert sd == se and itd == ite and np.array_equal(xd, xe)
+    assert len({i % 2 for i in itd}) == 2, itd  # frozen after both kinds of pass
+    for j in range(16):
+        r = O.pcg(A, B[:, j], tol=1e-10)
+        assert np.linalg.norm(xd[:, j] - r.x) / np.linalg.norm(r.x) <= 1e-9
+    for mi in (7, 8):
+        xd, _, _, _ = _msolve(Md, B, tol=1e-10, max_iter=mi)
+        xe, _, _, _ = _msolve(Me, B, tol=1e-10, max_iter=mi)
+        assert np.array_equal(xd, xe), mi
+    xd, sd, itd, rd = _msolve(Md, B[:, :5], tol=1e-16, max_iter=251)
+    xe, se, ite, re = _msolve(Me, B[:, :5], tol=1e-16, max_iter=251)
+    assert rd == re and min(rd) >= 1 and np.array_equal(xd, xe)
+
+
+def test_deferred_x_multi_bitwise_breakdown(pcg, monkeypatch):
+    """indefinite C1 Laplacian - s I, k = 4 random columns: per-column breakdown at
+    iterations of both parities; X bitwise the every-iteration X"""
+    import scipy.sparse as sp
+    P = O.build_problem("C1", c=24)
+    A0 = P["A"].to_scipy().tocsr()
+    lam = np.linalg.eigvalsh(A0.toarray())
+    B = np.random.default_rng(2).standard_normal((A0.shape[0], 4))
+    for f in (0.001, 0.01, 0.05):
+        s = lam[0] + f * (lam[-1] - lam[0])
+        Bm = (A0 - s * sp.identity(A0.shape[0])).tocsr()
+        Bm.sort_indices()
+        C = O.Csr(Bm.shape[0], Bm.indptr, Bm.indices, Bm.data)
+        Md, Me = _mpair(pcg, monkeypatch, C, 4)
+        xd, sd, _, _ = _msolve(Md, B, tol=1e-12, max_iter=2000)
+        xe, se, _, _ = _msolve(Me, B, tol=1e-12, max_iter=2000)
+        assert sd == se and np.array_equal(xd, xe), f
