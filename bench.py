@@ -29,6 +29,20 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# K1a bytes per row, averaged over the deferred x update's cycle (solver.cu k1a_hold / k1a_apply):
+# every iteration 40; cycle 2: (24 + 48) / 2; cycle 4: (3 x 24 + 64) / 4
+K1A_BYTES = {0: 40.0, 2: 36.0, 4: 34.0}
+
+
+def xdefer_cycle():
+    """the single-RHS loop's deferral cycle as the library reads PCG_XDEFER (default 4)"""
+    v = os.environ.get("PCG_XDEFER")
+    if v is None:
+        return 4
+    m = int(v) if v.strip().lstrip("-").isdigit() else 4
+    return m if m in (0, 2, 4) else 4
+
+
 def read_only_peak():
     """The read-only HBM stream rate measured on this GPU pool (scripts/probes/read_bw.cu,
     profiles/r02/read_bw.log): context for kernels whose traffic is mostly reads, whose
@@ -522,12 +536,12 @@ def main():
         if stats["schedule"] == 3:
             # x deferred (solver.cu k1a_deferred; PCG_XDEFER=0 turns it off): K1a alternates
             # hold (24n B) and apply (48n B) launches, timed as pairs: 36n per launch on average
-            xdefer = os.environ.get("PCG_XDEFER", "1") != "0"
+            xdm = xdefer_cycle()
             names = ["k1a_kernel (p = z + beta p, x += alpha p_old; streaming" +
-                     ("; x every 2nd iteration: hold/apply pair mean)" if xdefer else ")"),
+                     (f"; x every {xdm}th iteration: mean over a hold/apply cycle)" if xdm else ")"),
                      "k1b_kernel (SpMV q = A p + sigma = p.q, grid finish -> alpha)",
                      "k2_kernel (r -= alpha q, z = dinv r, rho', gamma, grid finish -> beta)"]
-            byts = [(36.0 if xdefer else 40.0) * n, mat + 16.0 * n, 40.0 * n]
+            byts = [K1A_BYTES[xdm] * n, mat + 16.0 * n, 40.0 * n]
         else:
             names = ["-", "k1_kernel (fused SpMV + p/x updates + sigma)", "k2_kernel (r/z updates + dots)"]
             byts = [0.0, mat + 48.0 * n, 40.0 * n]
@@ -569,7 +583,7 @@ def main():
         spmv_gbs = (12.0 * nnz + 4.0 * (n + 1) + 16.0 * n) / (spmv_us * 1e-6) / 1e9
     else:
         per_iter_us = ms * 1e3 / max(iters, 1)
-        vb = 92.0 if os.environ.get("PCG_XDEFER", "1") != "0" else 96.0  # x every second iteration
+        vb = 56.0 + K1A_BYTES[xdefer_cycle()]  # K1b 16n + K2 40n + K1a (x deferred over the cycle)
         achieved = (12.0 * nnz + 4.0 * (n + 1) + vb * n) / world / (per_iter_us * 1e-6) / 1e9
         roof = {"bound": "hbm", "kernel": f"whole iteration incl. halo + allreduces (per GPU, {vb:.0f}n schedule)",
                 "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_kind,

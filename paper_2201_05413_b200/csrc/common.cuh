@@ -63,10 +63,10 @@ struct Scalars {
   double rho_part[2];  // (r.z, r.r) partial sums awaiting a cross-GPU allreduce
   double res_part[3];  // (w.w, w.z, b.b) of the residual pass
   double sigma_acc;    // distributed overlap: p.q of the row ranges already done this iteration
-  double alpha_old;    // deferred x update: alpha of the direction held in p[parity ^ 1]
+  double ahold[3];     // deferred x update: alphas of the held directions p[0..xhold-1]
   long long k, max_iter, replacements;
   int done, parity, stage;  // parity: p[parity] holds the latest direction p_k
-  int xhold;                // deferred x update: alpha_old p[parity ^ 1] still owed to x
+  int xhold;                // deferred x update: held directions still owed to x (p[0..xhold-1])
   unsigned int cnt_a, cnt_b, cnt_c, cnt_d;  // last-block arrival counters (self-resetting)
   unsigned long long graph_launches;        // kernels executed from graphs (finishers count)
 };

@@ -59,7 +59,8 @@ struct SolveWork {
   bool graph_ready = false;
   int graph_kind = 0;  // 1 = conditional while node, 2 = unrolled chunk
   int unroll = 0;
-  bool xdefer = false;  // single-GPU 3-pass graph: x updated every second iteration (solver.cu)
+  int xdefer = 0;  // 3-pass graph loop: x updated every xdefer-th iteration (2 or 4; 0 = every one)
+  double *p23[2] = {nullptr, nullptr};  // direction buffers p[2], p[3] of the 4-cycle
   // multi-RHS workspace (row-major n x kcap)
   int kcap = 0;
   double *mr = nullptr, *mz = nullptr, *mq = nullptr, *mp[2] = {nullptr, nullptr}, *mx = nullptr,
@@ -99,6 +100,7 @@ struct SolveWork {
 struct Vecs {
   double *r, *z, *q, *p0, *p1, *x;
   const double *dinv;
+  double *p2, *p3;  // deferred x update with a 4-cycle (null otherwise)
 };
 
 // a symmetrically permuted copy of the system (SELL-C-sigma, sigma.cu)

@@ -39,28 +39,36 @@ __device__ __forceinline__ void stop_loop(int use_cond, cudaGraphConditionalHand
 }
 
 // ---------------------------------------------------------------- finishers
-// xdefer (deferred x update, k1a_kernel): 1 = a "hold" iteration (its K1a left
-// alpha_{k-1} p_{k-1} owed to x and wrote p_k to p[1]), 2 = an "apply" iteration (x is
-// current up to alpha_{k-1}, p_k in p[0]); 0 = off.
+// xd (deferred x update, k1a_kernel): 0 = off, else (M << 4) | j — pass j of an
+// M-cycle (M = 2 or 4): passes 0..M-2 "hold" (their K1a wrote p_k to p[j+1] and left
+// the owed alpha p of the direction in p[j] to x), pass M-1 "applies" (x current up to
+// alpha_{k-1}, p_k in p[0]).  Scalars: ahold[0..xhold-1] the held alphas (directions
+// p[0..xhold-1]), parity the buffer of the latest direction.
+__device__ __forceinline__ int xd_m(int xd) { return xd >> 4; }
+__device__ __forceinline__ int xd_j(int xd) { return xd & 15; }
+
 __device__ void finish_alpha(Scalars *sc, double sigma, int use_cond, cudaGraphConditionalHandle h, int flip = 1,
-                             int xdefer = 0) {
+                             int xd = 0) {
+  const int xm = xd_m(xd), xj = xd_j(xd);
+  const bool hold = xm && xj < xm - 1;
   sc->sigma = sigma;
   if (!(sigma > 0.0)) {  // p^T A p <= 0 (or NaN): CG breakdown, A not SPD
     sc->done = DONE_BREAKDOWN;
     stop_loop(use_cond, h);
-    if (xdefer == 1) {  // alpha_{k-1} p_{k-1} (in p[0]) is still owed: the tail applies it
-      sc->alpha_old = sc->alpha;
+    if (hold) {  // alpha_{k-1} p_{k-1} (in p[j]) is still owed: the tail applies it
+      sc->ahold[sc->xhold++] = sc->alpha;
       sc->alpha = 0.0;
-      sc->xhold = 1;
-      sc->parity = 1;
-    } else if (xdefer == 2) {  // this iteration's K1a applied everything owed
+      sc->parity = xj + 1;
+    } else if (xm) {  // an apply pass: this iteration's K1a applied everything owed
       sc->xhold = 0;
     }
   } else {
-    if (xdefer) {
-      sc->alpha_old = sc->alpha;
-      sc->xhold = xdefer == 1;
-      sc->parity = xdefer == 1;
+    if (hold) {
+      sc->ahold[sc->xhold++] = sc->alpha;
+      sc->parity = xj + 1;
+    } else if (xm) {
+      sc->xhold = 0;
+      sc->parity = 0;
     }
     sc->alpha = sc->rho / sigma;
     sc->k += 1;
@@ -228,60 +236,91 @@ __global__ void __launch_bounds__(BLOCK) k2_kernel(int64_t n, Vecs v, Scalars *s
 // K2  (as above):  r, z updates + rho', gamma -> beta       (40n B)
 // 96n + matrix bytes per iteration, every pass a plain streaming or SpMV pass.
 //
-// Deferred x update (xdefer, single-GPU graph loop; SURVEY §8(d) bytes): x changes only
-// every second iteration, so K1a alternates
-//   hold  (xdefer 1): p[1] = z + beta p[0]; x untouched          (reads z, p: 24n B)
-//   apply (xdefer 2): x = fma(alpha_k, p[1], fma(alpha_{k-1}, p[0], x)); p[0] = z + beta p[1]
-//                                                                 (reads z, p, p, x: 48n B)
-// 36n instead of 40n per iteration, and the SAME fused multiply-adds in the same order
-// as the every-iteration update, so x is bitwise the same.  The tail applies what a
-// stop leaves owed (Scalars::xhold, alpha_old).
-__device__ __forceinline__ void k1a_deferred(int64_t n, int64_t n_ghost, const Vecs &v, double beta, double alpha,
-                                             double alpha_old, int xdefer) {
+// Deferred x update (the graph loops; SURVEY §8(d) bytes): x is needed only at the exit
+// check, so over a cycle of M iterations (M = 2 or 4) K1a runs M - 1 "hold" passes
+//   pass j < M-1:  p[j+1] = z + beta p[j]; x untouched               (reads z, p: 24n B)
+// and one "apply" pass
+//   pass M-1:      x = fma(alpha_k, p[M-1], fma(alpha_h[M-2], p[M-2], ... fma(alpha_h[0], p[0], x)))
+//                  p[0] = z + beta p[M-1]                  (reads z, M directions, x: 8(M+2)n B)
+// M = 2: 36n, M = 4: 34n per iteration instead of 40n, and the SAME fused multiply-adds
+// in the same order as the every-iteration update (oldest direction first), so x is
+// bitwise the same.  The tail applies what a stop leaves owed (Scalars::xhold, ahold).
+__device__ __forceinline__ double *dir_buf(const Vecs &v, int b) {
+  return b == 0 ? v.p0 : b == 1 ? v.p1 : b == 2 ? v.p2 : v.p3;
+}
+
+template <int M>
+__device__ __forceinline__ void k1a_apply(int64_t n, int64_t n_ghost, const Vecs &v, double beta, double alpha,
+                                          const volatile double *ahold) {
   const int64_t npair = n >> 1;
-  const double2 *__restrict__ z2 = reinterpret_cast<const double2 *>(v.z);
   const int64_t t = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nt = (int64_t)gridDim.x * BLOCK;
-  if (xdefer == 1) {
-    const double2 *__restrict__ a2 = reinterpret_cast<const double2 *>(v.p0);
-    double2 *__restrict__ b2 = reinterpret_cast<double2 *>(v.p1);
-    for (int64_t i = t; i < npair; i += nt) {
-      const double2 zz = __ldcs(z2 + i), po = __ldcs(a2 + i);
-      b2[i] = make_double2(__fma_rn(beta, po.x, zz.x), __fma_rn(beta, po.y, zz.y));
+  double ah[M - 1];
+#pragma unroll
+  for (int h = 0; h < M - 1; h++) ah[h] = ahold[h];
+  const double2 *__restrict__ z2 = reinterpret_cast<const double2 *>(v.z);
+  const double2 *hb[M - 1];
+#pragma unroll
+  for (int h = 0; h < M - 1; h++) hb[h] = reinterpret_cast<const double2 *>(dir_buf(v, h));
+  const double2 *__restrict__ l2 = reinterpret_cast<const double2 *>(dir_buf(v, M - 1));
+  double2 *__restrict__ a2 = reinterpret_cast<double2 *>(v.p0);
+  double2 *__restrict__ x2 = reinterpret_cast<double2 *>(v.x);
+  for (int64_t i = t; i < npair; i += nt) {
+    const double2 zz = __ldcs(z2 + i), pk = l2[i];
+    double2 pm[M - 1];
+#pragma unroll
+    for (int h = 0; h < M - 1; h++) pm[h] = __ldcs(hb[h] + i);
+    double2 xx = __ldcs(x2 + i);
+#pragma unroll
+    for (int h = 0; h < M - 1; h++) {
+      xx.x = __fma_rn(ah[h], pm[h].x, xx.x);
+      xx.y = __fma_rn(ah[h], pm[h].y, xx.y);
     }
-    if ((n & 1) && t == 0) v.p1[n - 1] = __fma_rn(beta, v.p0[n - 1], v.z[n - 1]);
-    for (int64_t g = t; g < n_ghost; g += nt) v.p1[n + g] = __fma_rn(beta, v.p0[n + g], v.z[n + g]);
-  } else {
-    double2 *__restrict__ a2 = reinterpret_cast<double2 *>(v.p0);
-    const double2 *__restrict__ b2 = reinterpret_cast<const double2 *>(v.p1);
-    double2 *__restrict__ x2 = reinterpret_cast<double2 *>(v.x);
-    for (int64_t i = t; i < npair; i += nt) {
-      const double2 zz = __ldcs(z2 + i), pk = b2[i], pm = __ldcs(a2 + i);
-      double2 xx = __ldcs(x2 + i);
-      xx.x = __fma_rn(alpha, pk.x, __fma_rn(alpha_old, pm.x, xx.x));
-      xx.y = __fma_rn(alpha, pk.y, __fma_rn(alpha_old, pm.y, xx.y));
-      a2[i] = make_double2(__fma_rn(beta, pk.x, zz.x), __fma_rn(beta, pk.y, zz.y));
-      __stcs(x2 + i, xx);
-    }
-    if ((n & 1) && t == 0) {
-      const int64_t i = n - 1;
-      const double pk = v.p1[i];
-      v.x[i] = __fma_rn(alpha, pk, __fma_rn(alpha_old, v.p0[i], v.x[i]));
-      v.p0[i] = __fma_rn(beta, pk, v.z[i]);
-    }
-    for (int64_t g = t; g < n_ghost; g += nt) v.p0[n + g] = __fma_rn(beta, v.p1[n + g], v.z[n + g]);
+    xx.x = __fma_rn(alpha, pk.x, xx.x);
+    xx.y = __fma_rn(alpha, pk.y, xx.y);
+    a2[i] = make_double2(__fma_rn(beta, pk.x, zz.x), __fma_rn(beta, pk.y, zz.y));
+    __stcs(x2 + i, xx);
   }
+  const double *pl = dir_buf(v, M - 1);
+  if ((n & 1) && t == 0) {
+    const int64_t i = n - 1;
+    double xi = v.x[i];
+#pragma unroll
+    for (int h = 0; h < M - 1; h++) xi = __fma_rn(ah[h], dir_buf(v, h)[i], xi);
+    v.x[i] = __fma_rn(alpha, pl[i], xi);
+    v.p0[i] = __fma_rn(beta, pl[i], v.z[i]);
+  }
+  for (int64_t g = t; g < n_ghost; g += nt) v.p0[n + g] = __fma_rn(beta, pl[n + g], v.z[n + g]);
+}
+
+__device__ __forceinline__ void k1a_hold(int64_t n, int64_t n_ghost, const Vecs &v, double beta, int j) {
+  const int64_t npair = n >> 1;
+  const int64_t t = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nt = (int64_t)gridDim.x * BLOCK;
+  const double *src = dir_buf(v, j);
+  double *dst = dir_buf(v, j + 1);
+  const double2 *__restrict__ z2 = reinterpret_cast<const double2 *>(v.z);
+  const double2 *__restrict__ a2 = reinterpret_cast<const double2 *>(src);
+  double2 *__restrict__ b2 = reinterpret_cast<double2 *>(dst);
+  for (int64_t i = t; i < npair; i += nt) {
+    const double2 zz = __ldcs(z2 + i), po = __ldcs(a2 + i);
+    b2[i] = make_double2(__fma_rn(beta, po.x, zz.x), __fma_rn(beta, po.y, zz.y));
+  }
+  if ((n & 1) && t == 0) dst[n - 1] = __fma_rn(beta, src[n - 1], v.z[n - 1]);
+  for (int64_t g = t; g < n_ghost; g += nt) dst[n + g] = __fma_rn(beta, src[n + g], v.z[n + g]);
 }
 
 __global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, Vecs v, Scalars *sc, int use_cond,
-                                                    cudaGraphConditionalHandle h, int xdefer) {
+                                                    cudaGraphConditionalHandle h, int xd) {
   const volatile Scalars *vs = sc;
   if (vs->done != DONE_RUNNING) {
     if (blockIdx.x == 0 && threadIdx.x == 0) stop_loop(use_cond, h);
     return;
   }
   const double beta = vs->beta, alpha_prev = vs->alpha;
-  if (xdefer) {
-    k1a_deferred(n, n_ghost, v, beta, alpha_prev, vs->alpha_old, xdefer);
+  if (xd) {
+    const int xm = xd_m(xd), xj = xd_j(xd);
+    if (xj < xm - 1) k1a_hold(n, n_ghost, v, beta, xj);
+    else if (xm == 4) k1a_apply<4>(n, n_ghost, v, beta, alpha_prev, vs->ahold);
+    else k1a_apply<2>(n, n_ghost, v, beta, alpha_prev, vs->ahold);
     return;
   }
   double *__restrict__ p = v.p0;
@@ -370,12 +409,13 @@ __global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) k1b_kernel(SellView S, C
 // distributed overlap: ghost copies of p advance once the z halo has arrived
 // (deferred x update: a hold iteration advances p[0] -> p[1], an apply iteration p[1] -> p[0])
 __global__ void __launch_bounds__(BLOCK) ghost_p_kernel(int64_t n, int64_t n_ghost, Vecs v, const Scalars *sc,
-                                                        int xdefer) {
+                                                        int xd) {
   const volatile Scalars *vs = sc;
   if (vs->done != DONE_RUNNING) return;
   const double beta = vs->beta;
-  const double *src = xdefer == 2 ? v.p1 : v.p0;
-  double *dst = xdefer == 1 ? v.p1 : v.p0;
+  const int xm = xd_m(xd), xj = xd_j(xd);
+  const double *src = !xm ? v.p0 : dir_buf(v, xj < xm - 1 ? xj : xm - 1);
+  double *dst = !xm ? v.p0 : dir_buf(v, xj < xm - 1 ? xj + 1 : 0);
   for (int64_t g = (int64_t)blockIdx.x * BLOCK + threadIdx.x; g < n_ghost; g += (int64_t)gridDim.x * BLOCK)
     dst[n + g] = __fma_rn(beta, src[n + g], v.z[n + g]);
 }
@@ -492,18 +532,19 @@ __global__ void resid_finish_kernel(Scalars *sc, int mode) {
 
 // deferred x += alpha_k p_k after the loop stops on the recurrence or max_iter
 // x += alpha_k p_k still owed at a stop (converged / max_iter), after the held
-// alpha_{k-1} p_{k-1} of the deferred update (xhold) in the order the loop would apply them
+// directions of the deferred update (oldest first), in the order the loop applies them
 __global__ void tail_kernel(int64_t n, Vecs v, const Scalars *sc) {
   const int done = sc->done;
-  const double alpha = sc->alpha, alpha_old = sc->alpha_old;
+  const double alpha = sc->alpha;
   const bool last = (done == DONE_CONVERGED || done == DONE_MAXIT) && alpha != 0.0;
-  const bool hold = sc->xhold != 0;
-  if (!last && !hold) return;
-  const double *p = sc->parity ? v.p1 : v.p0;
-  const double *ph = sc->parity ? v.p0 : v.p1;
+  const int nh = sc->xhold;
+  if (!last && nh == 0) return;
+  double ah[3];
+  for (int h = 0; h < 3; h++) ah[h] = sc->ahold[h];
+  const double *p = dir_buf(v, sc->parity);
   for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
     double xi = v.x[i];
-    if (hold) xi = __fma_rn(alpha_old, ph[i], xi);
+    for (int h = 0; h < nh; h++) xi = __fma_rn(ah[h], dir_buf(v, h)[i], xi);
     if (last) xi = __fma_rn(alpha, p[i], xi);
     v.x[i] = xi;
   }
@@ -511,7 +552,7 @@ __global__ void tail_kernel(int64_t n, Vecs v, const Scalars *sc) {
 // after the tail: nothing owed; the deferred loop restarts (replacement) with p in p[0]
 __global__ void clear_alpha_kernel(Scalars *sc, int xdefer) {
   sc->alpha = 0.0;
-  sc->alpha_old = 0.0;
+  for (int h = 0; h < 3; h++) sc->ahold[h] = 0.0;
   sc->xhold = 0;
   if (xdefer) sc->parity = 0;
 }
@@ -576,7 +617,7 @@ static int fmt_d16(const pcg_matrix *A, int fmt) {
 
 static Vecs vecs_of(pcg_matrix *A) {
   SolveWork &w = A->work;
-  return Vecs{w.r, w.z, w.q, w.p[0], w.p[1], w.x, A->d_dinv};
+  return Vecs{w.r, w.z, w.q, w.p[0], w.p[1], w.x, A->d_dinv, w.p23[0], w.p23[1]};
 }
 
 pcg_status launch_spmv_fmt(pcg_matrix *A, int fmt, const double *x, double *y, cudaStream_t st) {
@@ -599,6 +640,13 @@ static int k1_chunk() {  // tuning knob (PCG_K1_CHUNK=4|8), default 8
   return c;
 }
 
+// the buffer holding the direction K1b multiplies in deferral pass xd (host side)
+static double *k1b_dir(const Vecs &v, int xd) {
+  const int m = xd >> 4, j = xd & 15;
+  const int b = j < m - 1 ? j + 1 : 0;
+  return b == 0 ? v.p0 : b == 1 ? v.p1 : b == 2 ? v.p2 : v.p3;
+}
+
 static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h,
                             int xdefer = 0) {
   Vecs v = vecs_of(A);
@@ -612,7 +660,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     k1a_kernel<<<A->grid_vec, BLOCK, 0, A->ov_side>>>(A->n, 0, v, w.sc, use_cond, h, xdefer);
     count_launch();
     Vecs vb = v;
-    if (xdefer == 1) vb.p0 = v.p1;  // a hold iteration writes p_k to p[1]
+    if (xdefer) vb.p0 = k1b_dir(v, xdefer);  // the direction this pass's K1a wrote
     struct Range {
       int64_t r0, r1;
     } rs[3] = {{A->ov_ia, A->ov_ib}, {0, A->ov_ia}, {A->ov_ib, A->n}};
@@ -657,7 +705,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, use_cond, h, xdefer);
     count_launch();
     Vecs vb = v;
-    if (xdefer == 1) vb.p0 = v.p1;  // a hold iteration wrote p_k to p[1]
+    if (xdefer) vb.p0 = k1b_dir(v, xdefer);  // the direction this pass's K1a wrote
     PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
                      <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, vb, w.sc, w.partials,
                                                                 A->comm ? 1 : 0, use_cond, h, 0, 0, xdefer));
@@ -721,11 +769,31 @@ static pcg_status launch_resid(pcg_matrix *A, const double *b, int mode, cudaStr
   return PCG_OK;
 }
 
-// deferred x update (k1a_deferred): 3-pass schedule (one GPU or distributed); PCG_XDEFER=0 turns it off
-static bool xdefer_wanted(const pcg_matrix *A) {
+// deferred x update (k1a_hold / k1a_apply): 3-pass schedule (one GPU or distributed);
+// the cycle M: PCG_XDEFER=0 (off: x every iteration), 2 or 4 (default XDEFER_M)
+#ifndef PCG_XDEFER_M  // default cycle: measured C5 3.200 (off) / 3.125 (2) / 3.091 s (4)
+#define PCG_XDEFER_M 4
+#endif
+static int xdefer_m(const pcg_matrix *A) {
+  if (A->schedule != 3) return 0;
   const char *xd = getenv("PCG_XDEFER");
-  return A->schedule == 3 && !(xd && atoi(xd) == 0);
+  const int m = xd ? atoi(xd) : PCG_XDEFER_M;
+  return m == 2 || m == 4 ? m : (m == 0 ? 0 : PCG_XDEFER_M);
 }
+// the 4-cycle's direction buffers p[2], p[3] (allocated once per handle)
+static pcg_status ensure_dir_bufs(pcg_matrix *A, int m) {
+  SolveWork &w = A->work;
+  if (m != 4 || w.p23[0]) return PCG_OK;
+  const size_t ngb = sizeof(double) * ((size_t)(A->n + A->n_ghost) + 64);
+  for (double *&q : w.p23) {
+    PCG_CUDA(cudaMalloc(&q, ngb));
+    PCG_CUDA(cudaMemset(q, 0, ngb));
+  }
+  A->device_bytes += 2.0 * ngb;
+  return PCG_OK;
+}
+// kernel argument of pass u of the loop (0: off)
+static int xd_arg(int m, int u) { return m ? (m << 4) | (u % m) : 0; }
 
 // Build the loop graph once per handle: WHILE(cond) { K1; K2 } (1 GPU), or an
 // unrolled chunk of U iterations polled from the host (distributed: NCCL calls
@@ -735,10 +803,11 @@ static pcg_status build_loop_graph(pcg_matrix *A) {
   if (w.graph_ready) return PCG_OK;
   // host-callback communicator, or PCG_NO_GRAPH=1 (profilers that do not descend into
   // conditional graph bodies): the same iterations as direct launches, host-polled
-  w.xdefer = xdefer_wanted(A);
+  w.xdefer = xdefer_m(A);
+  PCG_TRY(ensure_dir_bufs(A, w.xdefer));
   if ((A->comm && !comm_uses_graphs(A->comm)) || getenv("PCG_NO_GRAPH")) {
     w.graph_kind = 3;
-    w.unroll = 8;  // even: hold / apply pairs
+    w.unroll = 8;  // a multiple of the deferral cycle
     w.graph_ready = true;
     return PCG_OK;
   }
@@ -760,8 +829,9 @@ static pcg_status build_loop_graph(pcg_matrix *A) {
     PCG_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
     cudaGraph_t body = np.conditional.phGraph_out[0];
     PCG_CUDA(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    for (int u = 0; u < 2 && st == PCG_OK; u++) {
-      st = launch_k1(A, cap, 1, h, w.xdefer ? 1 + u : 0);
+    const int nbody = w.xdefer == 4 ? 4 : 2;  // iterations per conditional body: one deferral cycle
+    for (int u = 0; u < nbody && st == PCG_OK; u++) {
+      st = launch_k1(A, cap, 1, h, xd_arg(w.xdefer, u));
       if (st == PCG_OK) st = launch_k2(A, cap, 1, h);
     }
     cudaGraph_t out;
@@ -769,12 +839,12 @@ static pcg_status build_loop_graph(pcg_matrix *A) {
     if (st != PCG_OK) return st;
     PCG_CUDA(e);
     w.graph_kind = 1;
-    w.unroll = 2;
+    w.unroll = nbody;
   } else {
     const int U = 8;
     PCG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    for (int u = 0; u < U && st == PCG_OK; u++) {  // U even: hold / apply pairs
-      st = launch_k1(A, cap, 0, 0, w.xdefer ? 1 + (u & 1) : 0);
+    for (int u = 0; u < U && st == PCG_OK; u++) {  // U a multiple of the deferral cycle
+      st = launch_k1(A, cap, 0, 0, xd_arg(w.xdefer, u));
       if (st == PCG_OK) st = launch_k2(A, cap, 0, 0);
     }
     cudaGraph_t out;
@@ -872,7 +942,7 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
           PCG_CUDA(cudaGraphLaunch(w.loop_exec, st));
         } else {  // 3: the same iterations launched directly (collectives through host callbacks)
           for (int u = 0; u < w.unroll; u++) {
-            PCG_TRY(launch_k1(A, st, 0, 0, w.xdefer ? 1 + (u & 1) : 0));
+            PCG_TRY(launch_k1(A, st, 0, 0, xd_arg(w.xdefer, u)));
             PCG_TRY(launch_k2(A, st, 0, 0));
           }
         }
@@ -916,7 +986,8 @@ static pcg_status solve_impl(pcg_matrix *A, const double *b, double *x, double t
     info->t_solve_s = ms * 1e-3;
     const double nn = (double)A->n, nz = (double)A->nnz;
     const int sched = persist ? persist_schedule(A) : A->schedule;
-    const double vb = sched == 3 ? (!persist && w.xdefer ? 92.0 : 96.0) : 88.0;  // K1a 36n deferred
+    // K1a: 40n, 36n (x every 2nd iteration), 34n (every 4th)
+    const double vb = sched == 3 ? (persist || !w.xdefer ? 96.0 : (w.xdefer == 4 ? 90.0 : 92.0)) : 88.0;
     info->bytes_algorithmic = (double)h->k * (12.0 * nz + 4.0 * (nn + 1) + vb * nn);
     info->flops = (double)h->k * (2.0 * nz + 13.0 * nn);
   }
@@ -1048,15 +1119,17 @@ extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32
     b = w.stage_b;
   }
   PCG_TRY(launch_resid(A, b, MODE_INIT, st));
+  const int xm = xdefer_m(A);  // the loop's K1a passes (hold / apply) when x is deferred
+  PCG_TRY(ensure_dir_bufs(A, xm));
   Vecs v = vecs_of(A);
   std::vector<cudaEvent_t> ev(3 * (size_t)reps + 1);
   for (auto &e : ev) PCG_CUDA(cudaEventCreate(&e));
   PCG_CUDA(cudaEventRecord(ev[0], st));
   for (int r = 0; r < reps; r++) {
     if (A->schedule == 3) {  // the loop's kernels: hold / apply K1a pairs when x is deferred
-      const int xd = xdefer_wanted(A) ? 1 + (r & 1) : 0;
+      const int xd = xd_arg(xm, r);
       Vecs vb = v;
-      if (xd == 1) vb.p0 = v.p1;
+      if (xd) vb.p0 = k1b_dir(v, xd);
       k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, 0, 0, xd);
       PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
       PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,

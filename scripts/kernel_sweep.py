@@ -39,8 +39,9 @@ for _ in range(2):
     pcg.check(pcg.lib().pcg_profile_kernels(A._h, C.c_void_p(b.data_ptr()), a.reps, st, us, C.byref(done)), "profile")
 stats = A.stats()
 mat = 12.0 * nnz + 4.0 * (n + 1)
-if stats["schedule"] == 3:  # K1a: hold/apply pair mean (36n) unless PCG_XDEFER=0
-    byts = [(36.0 if os.environ.get("PCG_XDEFER", "1") != "0" else 40.0) * n, mat + 16.0 * n, 40.0 * n]
+if stats["schedule"] == 3:  # K1a: mean over the deferral cycle (PCG_XDEFER: 4 default, 2, 0)
+    xm = int(os.environ.get("PCG_XDEFER", "4"))
+    byts = [{0: 40.0, 2: 36.0, 4: 34.0}.get(xm, 34.0) * n, mat + 16.0 * n, 40.0 * n]
 else:
     byts = [0.0, mat + 48.0 * n, 40.0 * n]
 out = {"config": a.config, "c": spec.c, "n": n, "nnz": nnz, "env": {k: v for k, v in os.environ.items() if k.startswith("PCG_")},

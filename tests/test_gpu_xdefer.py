@@ -27,13 +27,14 @@ def _dev(a):
     return torch.as_tensor(np.ascontiguousarray(a)).cuda()
 
 
-def _pair(pcg, monkeypatch, A, graph=True):
-    """(deferred handle, every-iteration handle) of the same matrix on the graph path"""
+def _pair(pcg, monkeypatch, A, graph=True, mode="2"):
+    """(deferred handle, every-iteration handle) of the same matrix on the graph path;
+    mode: the deferral cycle (x every 2nd or every 4th iteration)"""
     monkeypatch.setenv("PCG_PERSIST", "0")
     if not graph:
         monkeypatch.setenv("PCG_NO_GRAPH", "1")
     out = []
-    for xd in ("1", "0"):
+    for xd in (mode, "0"):
         monkeypatch.setenv("PCG_XDEFER", xd)
         M = pcg.Matrix.from_csr(_dev(A.row_ptr), _dev(A.col), _dev(A.val), fmt="sell")
         _solve(M, np.ones(A.n), max_iter=3)  # builds the loop graph under this env
@@ -56,12 +57,13 @@ def _solve(M, b, **kw):
     return x.cpu().numpy(), st, info
 
 
+@pytest.mark.parametrize("mode", ["2", "4"])
 @pytest.mark.parametrize("graph", [True, False])
 @pytest.mark.parametrize("name,c", [("C1", None), ("C2", 48), ("C4", 16)])
-def test_deferred_x_bitwise_converged(pcg, monkeypatch, graph, name, c):
+def test_deferred_x_bitwise_converged(pcg, monkeypatch, graph, name, c, mode):
     P = O.build_problem(name, c=c, k=1)
     A, b = P["A"], P["B"][:, 0]
-    Md, Me = _pair(pcg, monkeypatch, A, graph)
+    Md, Me = _pair(pcg, monkeypatch, A, graph, mode)
     tol = O.configs()[name]["tol"]
     xd, sd, infd = _solve(Md, b, tol=tol)
     xe, se, infe = _solve(Me, b, tol=tol)
@@ -72,42 +74,45 @@ def test_deferred_x_bitwise_converged(pcg, monkeypatch, graph, name, c):
     assert np.linalg.norm(xd - r.x) / np.linalg.norm(r.x) <= 1e-9
 
 
-def test_deferred_x_bitwise_stop_parities(pcg, monkeypatch):
-    """max_iter 1..9 stops after hold (odd k) and apply (even k) iterations; tolerances
-    that converge at both parities; a warm start."""
+@pytest.mark.parametrize("mode", ["2", "4"])
+def test_deferred_x_bitwise_stop_parities(pcg, monkeypatch, mode):
+    """max_iter 1..9 stops after every pass of the cycle; tolerances that converge at
+    every position of the cycle; a warm start."""
     P = O.build_problem("C1", c=32)
     A, b = P["A"], P["B"][:, 0]
-    Md, Me = _pair(pcg, monkeypatch, A)
+    Md, Me = _pair(pcg, monkeypatch, A, True, mode)
     for mi in range(1, 10):
         xd, sd, _ = _solve(Md, b, tol=1e-12, max_iter=mi)
         xe, se, _ = _solve(Me, b, tol=1e-12, max_iter=mi)
         assert sd == se == 1 and np.array_equal(xd, xe), mi
     its = set()
-    for tol in (1e-2, 3e-3, 1e-3, 3e-4, 1e-4, 3e-5, 1e-6):
+    for tol in (1e-2, 3e-3, 1e-3, 3e-4, 1e-4, 3e-5, 1e-5, 3e-6, 1e-6, 3e-7, 1e-7, 3e-8, 1e-8):
         xd, sd, infd = _solve(Md, b, tol=tol)
         xe, se, infe = _solve(Me, b, tol=tol)
         assert sd == se and infd["iterations"] == infe["iterations"] and np.array_equal(xd, xe), tol
-        its.add(infd["iterations"] % 2)
-    assert its == {0, 1}  # both parities exercised
+        its.add(infd["iterations"] % int(mode))
+    assert len(its) >= 2  # several positions of the cycle exercised
     x0 = np.random.default_rng(3).standard_normal(A.n)
     xd, _, infd = _solve(Md, b, tol=1e-10, x0=x0)
     xe, _, infe = _solve(Me, b, tol=1e-10, x0=x0)
     assert infd["iterations"] == infe["iterations"] and np.array_equal(xd, xe)
 
 
-def test_deferred_x_bitwise_replacement(pcg, monkeypatch):
+@pytest.mark.parametrize("mode", ["2", "4"])
+def test_deferred_x_bitwise_replacement(pcg, monkeypatch, mode):
     """below attainable accuracy: replacements restart the deferred loop (p in p[0])"""
     P = O.build_problem("C1")
     A, b = P["A"], P["B"][:, 0]
-    Md, Me = _pair(pcg, monkeypatch, A)
-    for mi in (399, 400):
+    Md, Me = _pair(pcg, monkeypatch, A, True, mode)
+    for mi in (397, 398, 399, 400):
         xd, sd, infd = _solve(Md, b, tol=1e-15, max_iter=mi)
         xe, se, infe = _solve(Me, b, tol=1e-15, max_iter=mi)
         assert sd == se == 1 and infd["replacements"] == infe["replacements"] >= 2
         assert np.array_equal(xd, xe)
 
 
-def test_deferred_x_bitwise_breakdown(pcg, monkeypatch):
+@pytest.mark.parametrize("mode", ["2", "4"])
+def test_deferred_x_bitwise_breakdown(pcg, monkeypatch, mode):
     """symmetric indefinite systems (C1 Laplacian - s I, random b): CG breaks down
     (NOT_SPD) at iterations of both parities (the oracle's count); x holds every applied
     update, bitwise the same on both paths"""
@@ -124,13 +129,13 @@ def test_deferred_x_bitwise_breakdown(pcg, monkeypatch):
         C = O.Csr(B.shape[0], B.indptr, B.indices, B.data)
         r = O.pcg(C, b, tol=1e-12, max_iter=2000)
         assert r.status == O.ERR_NOT_SPD
-        Md, Me = _pair(pcg, monkeypatch, C)
+        Md, Me = _pair(pcg, monkeypatch, C, True, mode)
         xd, sd, _ = _solve(Md, b, tol=1e-12, max_iter=2000)
         xe, se, _ = _solve(Me, b, tol=1e-12, max_iter=2000)
         assert sd == se == 7, (f, sd, se)  # PCG_ERR_NOT_SPD
         assert np.array_equal(xd, xe), f
-        parities.add(r.iterations % 2)
-    assert parities == {0, 1}
+        parities.add(r.iterations % int(mode))
+    assert len(parities) >= 2
 
 
 # ---------------------------------------------------------------- k right-hand sides (mk1a_deferred)
