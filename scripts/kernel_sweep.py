@@ -49,7 +49,8 @@ out = {"config": a.config, "c": spec.c, "n": n, "nnz": nnz, "env": {k: v for k, 
        "us": list(us), "GBps": [b_ / u / 1e3 if u else 0 for b_, u in zip(byts, us)],
        "iter_us": sum(us), "iter_frac": sum(byts) / sum(us) / 1e3 / 6556.2,
        "iter_frac_vs_88n": (mat + 88.0 * n) / sum(us) / 1e3 / 6556.2,
-       "spmv_us": {"csr": stats["spmv_us_csr"], "sell": stats["spmv_us_sell"], "tma": stats["spmv_us_tma"]}}
+       "spmv_us": {"csr": stats["spmv_us_csr"], "sell": stats["spmv_us_sell"], "tma": stats["spmv_us_tma"]},
+       "sell_pad": stats["sell_entries"] / max(nnz, 1), "short_rows": stats["short_rows"], "max_row_len": stats["max_row_len"]}
 if a.solve:
     x, info = A.solve(b)
     x, info = A.solve(b)
