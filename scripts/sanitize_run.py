@@ -45,6 +45,25 @@ A = pcg.Matrix.from_csr(G["row_ptr"], G["col"], G["val"])
 for bs in (1, 2, 4, 8):
     x, info = A.bicgstab(G["b"], tol=1e-12, block=bs)
     out.append(("CUBE10", bs, "bicg", info["iterations"], info["status"]))
+# round 2 paths: ILU(0) blocks (packed records and the cp.async ring), the deferred x
+# update's cycles (graph loop), max_iter stops inside a cycle
+for pk in ("1", "0"):
+    os.environ["PCG_ILU_PACKED"] = pk
+    for bs in (100, 0):
+        A = pcg.Matrix.from_csr(G["row_ptr"], G["col"], G["val"], fmt="sell")
+        x, info = A.bicgstab(G["b"], tol=1e-12, block=bs, precond="ilu0")
+        out.append(("CUBE10-ilu0", pk, bs, info["iterations"], info["status"]))
+        A.close()
+os.environ["PCG_PERSIST"] = "0"
+P = fem_build(fem_spec("C1", c=16))
+for xd in ("4", "2", "0"):
+    os.environ["PCG_XDEFER"] = xd
+    A = pcg.Matrix.from_csr(P["row_ptr"], P["col"], P["val"])
+    b = P["B"][:, 0].contiguous()
+    for mi in (5, 6, 7, 1000):
+        x, info = A.solve(b, tol=1e-10, max_iter=mi)
+        out.append(("C1-xdefer", xd, mi, info["iterations"], info["status"]))
+    A.close()
 torch.cuda.synchronize()
 for o in out:
     print(o)
