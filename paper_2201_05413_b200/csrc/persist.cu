@@ -220,7 +220,12 @@ bool persist_wanted(const pcg_matrix *A) {
   if (getenv("PCG_NO_GRAPH")) return false;  // profiling: one launch per pass
   const char *e = getenv("PCG_PERSIST");
   if (e) return atoi(e) != 0;
-  return A->n <= (int64_t(32) << 20);
+  // measured crossover (µs per iteration, persistent -> graph): rows of <= 8 entries run the
+  // graph loop's one-chunk SpMV at 4 blocks/SM and its x deferral, and win from ~4M rows
+  // (C1 4.2M 121.6 -> 113.3, C2 4.2M 132.0 -> 131.3, C5 construction 16.6M 498 -> 461;
+  // 2M rows: C4 62 -> 73); longer rows keep the persistent kernel up to 32M (C3 4.2M
+  // 177 -> 192, C6 16.6M 754 -> 763)
+  return A->n <= (A->short_rows ? int64_t(3) << 20 : int64_t(32) << 20);
 }
 
 pcg_status persist_launch(pcg_matrix *A, Vecs v, cudaStream_t st) {
