@@ -30,6 +30,10 @@
 #include "matrix.cuh"
 #include "staged.cuh"
 
+#ifndef PCG_ILU_RCP
+#define PCG_ILU_RCP 0
+#endif
+
 namespace pcgb {
 
 struct IluLevel {
@@ -163,7 +167,11 @@ __global__ void ilu_pack_kernel(const IluLevel *__restrict__ lev, int64_t nfwd_e
   double *d = f + (size_t)L.c * L.m;
   for (int t = threadIdx.x; t < L.m; t += blockDim.x) {
     rw[t] = row[L.row_base + t];
+#if PCG_ILU_RCP  // A/B knob: reciprocal pivots (not the oracle's rounding)
+    if (backward) d[t] = 1.0 / ud[L.row_base + t];
+#else
     if (backward) d[t] = ud[L.row_base + t];
+#endif
     for (int u = 0; u < L.c; u++) {
       const int64_t e = L.ent_base + (int64_t)u * L.m + t;
       k[u * L.m + t] = kcol[e];
@@ -453,7 +461,11 @@ __global__ void __launch_bounds__(T) ilu_apply_packed_kernel(IluView P, const do
           const int kk = k[u * L.m + t];
           if (kk >= 0) acc = __dsub_rn(acc, __dmul_rn(f[u * L.m + t], y[kk]));
         }
+#if PCG_ILU_RCP
+      y[i] = backward ? acc * f[L.c * L.m + t] : acc;
+#else
       y[i] = backward ? __ddiv_rn(acc, f[L.c * L.m + t]) : acc;
+#endif
     }
     __syncthreads();
   }
