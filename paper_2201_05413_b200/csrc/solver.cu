@@ -56,7 +56,8 @@ __device__ void finish_alpha(Scalars *sc, double sigma, int use_cond, cudaGraphC
     sc->done = DONE_BREAKDOWN;
     stop_loop(use_cond, h);
     if (hold) {  // alpha_{k-1} p_{k-1} (in p[j]) is still owed: the tail applies it
-      sc->ahold[sc->xhold++] = sc->alpha;
+      sc->ahold[xj] = sc->alpha;  // pass j holds direction j (xhold == j before)
+      sc->xhold = xj + 1;
       sc->alpha = 0.0;
       sc->parity = xj + 1;
     } else if (xm) {  // an apply pass: this iteration's K1a applied everything owed
@@ -64,7 +65,8 @@ __device__ void finish_alpha(Scalars *sc, double sigma, int use_cond, cudaGraphC
     }
   } else {
     if (hold) {
-      sc->ahold[sc->xhold++] = sc->alpha;
+      sc->ahold[xj] = sc->alpha;
+      sc->xhold = xj + 1;
       sc->parity = xj + 1;
     } else if (xm) {
       sc->xhold = 0;
