@@ -501,12 +501,12 @@ def main():
                                                C.c_void_p(torch.cuda.current_stream().cuda_stream), us,
                                                C.byref(done)), "pcg_profile_multi")
         mat = 12.0 * nnz + 4.0 * (n + 1)
-        xdm = os.environ.get("PCG_XDEFER", "1") != "0"  # X every second iteration: hold/apply pair mean 36 k n
+        xdm = xdefer_cycle()  # X deferred over the cycle (multi.cu mk1a_deferred): mean over a hold/apply cycle
         names = ["mk1a_kernel (X += alpha P, P = Z + beta P; streaming, per column" +
-                 ("; X every 2nd iteration: hold/apply pair mean)" if xdm else ")"),
+                 (f"; X every {xdm}th iteration: mean over a hold/apply cycle)" if xdm else ")"),
                  "mspmm_kernel (SpMM Q = A P over SELL-32, per-column sigma, grid finish -> alpha)",
                  "mk2_kernel (R -= alpha Q, Z = dinv R, rho', gamma per column, finish -> beta)"]
-        byts = [(36.0 if xdm else 40.0) * kcols * n, mat + 16.0 * kcols * n, 40.0 * kcols * n]
+        byts = [K1A_BYTES[xdm] * kcols * n, mat + 16.0 * kcols * n, 40.0 * kcols * n]
         kern = [{"kernel": nm, "bytes_per_launch": bt, "us_per_launch": u, "achieved_GBps": bt / u / 1e3 if u else None}
                 for nm, bt, u in zip(names, byts, us)]
         dom = max(kern, key=lambda d: d["us_per_launch"])

@@ -77,8 +77,9 @@ struct MultiScalars {
   double rho[KMAX], alpha[KMAX], beta[KMAX], sigma[KMAX], gamma[KMAX];
   double nb[KMAX], relres_rec[KMAX], relres_true[KMAX];
   double xpend[KMAX];        // alpha still owed to x (applied by the next K1 / tail)
-  double xhold[KMAX];        // deferred x update: alpha of the held older direction (0: none)
-  int lbuf[KMAX];            // deferred x update: the latest direction is in P[lbuf] (P or P1)
+  double ahold[3][KMAX];     // deferred x update: alphas of the held directions P[0..nheld-1]
+  int nheld[KMAX];           // deferred x update: held directions still owed to X
+  int lbuf[KMAX];            // deferred x update: the latest direction is in block P[lbuf] (0..3)
   double part[3][KMAX];      // allreduce staging (sigma | rho',gamma | ww,wz,bb)
   long long k[KMAX];
   long long nrep[KMAX];      // residual replacements per column (exit check failed, restarted)

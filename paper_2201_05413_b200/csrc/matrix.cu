@@ -719,7 +719,7 @@ void free_work(pcg_matrix *A) {
   if (w.bg_graph) cudaGraphDestroy(w.bg_graph);
   if (w.ilu) ilu_free(w.ilu);
   for (double *p : {w.r, w.z, w.q, w.p[0], w.p[1], w.p23[0], w.p23[1], w.x, w.w, w.stage_b, w.stage_x, w.partials,
-                    w.mr, w.mz, w.mq, w.mp[0], w.mp[1], w.mx, w.mb, w.mw, w.mpart})
+                    w.mr, w.mz, w.mq, w.mp[0], w.mp[1], w.mp23[0], w.mp23[1], w.mx, w.mb, w.mw, w.mpart})
     if (p) cudaFree(p);
   if (w.sc) cudaFree(w.sc);
   if (w.h_sc) cudaFreeHost(w.h_sc);

@@ -63,7 +63,7 @@ struct SolveWork {
   double *p23[2] = {nullptr, nullptr};  // direction buffers p[2], p[3] of the 4-cycle
   // multi-RHS workspace (row-major n x kcap)
   int kcap = 0;
-  double *mr = nullptr, *mz = nullptr, *mq = nullptr, *mp[2] = {nullptr, nullptr}, *mx = nullptr,
+  double *mr = nullptr, *mz = nullptr, *mq = nullptr, *mp[2] = {nullptr, nullptr}, *mp23[2] = {nullptr, nullptr}, *mx = nullptr,
          *mb = nullptr, *mw = nullptr;
   MultiScalars *msc = nullptr, *h_msc = nullptr;
   double *mpart = nullptr;

@@ -35,9 +35,13 @@
 
 namespace pcgb {
 
+#ifndef PCG_MXDEFER_M  // default cycle of the k-column loop's deferred X update
+#define PCG_MXDEFER_M 4
+#endif
+
 struct MVecs {
   double *R, *Z, *Q, *P, *X, *W;
-  double *P1;        // deferred x update: the second direction block (hold passes write it)
+  double *P1, *P2, *P3;  // deferred x update: the direction blocks hold passes write (P2, P3: 4-cycle)
   const double *Bm;  // right-hand sides (column-major, ld)
   const double *dinv;
   int64_t ld;        // leading dimension (n rounded up to 32)
@@ -115,16 +119,19 @@ __device__ void mcols_reduce_n(const double *partials, int nb, int k, double (*o
 }
 
 // ---------------------------------------------------------------- finishers (thread 0 of the last block)
-// pass: 0 = x updated every iteration; deferred x update (mk1a_kernel): 1 = hold (the
-// owed alpha of the direction in P stays owed, the new direction is in P1), 2 = apply
+// pass: 0 = X updated every iteration; else the deferred X update's (M << 4) | j, pass
+// j of an M-cycle (M = 2 or 4, mk1a_kernel): j < M-1 holds (the owed alpha of the direction
+// in P[j] stays owed, the new direction is in P[j+1]), j = M-1 applies
 __device__ void mk1b_finish(const double *sig, MultiScalars *sc, int use_cond, cudaGraphConditionalHandle h,
                             int pass) {
+  const int xm = pass >> 4, xj = pass & 15;
+  const bool hold = xm && xj < xm - 1;
   sc->cnt_a = 0;
   int na = 0;
   for (int c = 0; c < sc->kcols; c++) {
     if (!sc->active[c]) {
       sc->xpend[c] = 0.0;  // an owed x update was applied by this iteration's K1a
-      sc->xhold[c] = 0.0;
+      sc->nheld[c] = 0;
       continue;
     }
     const double sigma = sig[c];
@@ -134,21 +141,23 @@ __device__ void mk1b_finish(const double *sig, MultiScalars *sc, int use_cond, c
       sc->done[c] = DONE_BREAKDOWN;
       sc->active[c] = 0;
       sc->xpend[c] = 0.0;
-      if (pass == 1) {  // a hold pass left alpha_{k-1} p_{k-1} (in P) owed
-        sc->xhold[c] = owed;
-        sc->lbuf[c] = 1;
+      if (hold) {  // a hold pass left alpha_{k-1} p_{k-1} (in P[j]) owed
+        sc->ahold[xj][c] = owed;
+        sc->nheld[c] = xj + 1;
+        sc->lbuf[c] = xj + 1;
       } else {
-        sc->xhold[c] = 0.0;
+        sc->nheld[c] = 0;
         sc->lbuf[c] = 0;
       }
     } else {
       sc->alpha[c] = sc->rho[c] / sigma;
       sc->xpend[c] = sc->alpha[c];  // x += alpha p is deferred to the next K1a / the tail
-      if (pass == 1) {
-        sc->xhold[c] = owed;
-        sc->lbuf[c] = 1;
-      } else if (pass == 2) {
-        sc->xhold[c] = 0.0;
+      if (hold) {
+        sc->ahold[xj][c] = owed;
+        sc->nheld[c] = xj + 1;
+        sc->lbuf[c] = xj + 1;
+      } else if (xm) {
+        sc->nheld[c] = 0;
         sc->lbuf[c] = 0;
       }
       sc->k[c] += 1;
@@ -193,60 +202,98 @@ __device__ void mk2_finish(const double (*t)[KMAX], MultiScalars *sc, int use_co
 // ---------------------------------------------------------------- K1a: X_c += xpend_c P_c ; P_c = Z_c + beta_c P_c
 // grid (gx, k): blockIdx.y = column.  Just-frozen columns only receive their owed
 // x update; settled frozen columns return at entry.
-// Deferred x update (pass 1 / 2, as the single-RHS k1a_kernel): a hold pass writes
-// P1_c = Z_c + beta_c P_c and leaves X_c alone; an apply pass applies both owed updates,
-// X_c = fma(xpend_c, P1_c, fma(xhold_c, P_c, X_c)), and writes P_c = Z_c + beta_c P1_c —
-// the fused multiply-adds of the every-iteration update in the same order (bitwise the
-// same X).  A just-frozen column applies what it owes (held, then latest: P[lbuf_c]).
+// Deferred X update (as the single-RHS k1a_hold / k1a_apply, per column): hold pass j
+// writes P[j+1]_c = Z_c + beta_c P[j]_c and leaves X_c alone; the apply pass applies the
+// held directions oldest first and then the latest, X_c = fma(xpend_c, P[M-1]_c,
+// fma(ahold[M-2]_c, P[M-2]_c, ... X_c)), and writes P[0]_c = Z_c + beta_c P[M-1]_c — the
+// fused multiply-adds of the every-iteration update in the same order (bitwise the same
+// X).  A just-frozen column applies what it owes (held, then latest: P[lbuf_c]).
+__host__ __device__ __forceinline__ double *mbuf(const MVecs &v, int b) {
+  return b == 0 ? v.P : b == 1 ? v.P1 : b == 2 ? v.P2 : v.P3;
+}
+
+template <int M>
+__device__ __forceinline__ void mk1a_apply(int64_t n, const MVecs &v, const volatile MultiScalars *vs, int c,
+                                           double xp, double beta) {
+  const size_t o = (size_t)c * v.ld;
+  double ah[M - 1];
+#pragma unroll
+  for (int h = 0; h < M - 1; h++) ah[h] = vs->ahold[h][c];
+  const double2 *hb[M - 1];
+#pragma unroll
+  for (int h = 0; h < M - 1; h++) hb[h] = reinterpret_cast<const double2 *>(mbuf(v, h) + o);
+  const double *Pl = mbuf(v, M - 1) + o;
+  const double2 *__restrict__ L2 = reinterpret_cast<const double2 *>(Pl);
+  double2 *__restrict__ A2 = reinterpret_cast<double2 *>(v.P + o);
+  double2 *__restrict__ X2 = reinterpret_cast<double2 *>(v.X + o);
+  const double2 *__restrict__ Z2 = reinterpret_cast<const double2 *>(v.Z + o);
+  const int64_t npair = n >> 1;
+  const int64_t t0 = (int64_t)blockIdx.x * BLOCK + threadIdx.x, ts = (int64_t)gridDim.x * BLOCK;
+  for (int64_t t = t0; t < npair; t += ts) {
+    const double2 pk = L2[t], zz = __ldcs(Z2 + t);
+    double2 pm[M - 1];
+#pragma unroll
+    for (int h = 0; h < M - 1; h++) pm[h] = __ldcs(hb[h] + t);
+    double2 xx = __ldcs(X2 + t);
+#pragma unroll
+    for (int h = 0; h < M - 1; h++) {
+      xx.x = __fma_rn(ah[h], pm[h].x, xx.x);
+      xx.y = __fma_rn(ah[h], pm[h].y, xx.y);
+    }
+    xx.x = __fma_rn(xp, pk.x, xx.x);
+    xx.y = __fma_rn(xp, pk.y, xx.y);
+    __stcs(X2 + t, xx);
+    A2[t] = make_double2(__fma_rn(beta, pk.x, zz.x), __fma_rn(beta, pk.y, zz.y));
+  }
+  if ((n & 1) && t0 == 0) {
+    const int64_t i = n - 1;
+    double xi = v.X[o + i];
+#pragma unroll
+    for (int h = 0; h < M - 1; h++) xi = __fma_rn(ah[h], mbuf(v, h)[o + i], xi);
+    v.X[o + i] = __fma_rn(xp, Pl[i], xi);
+    v.P[o + i] = __fma_rn(beta, Pl[i], v.Z[o + i]);
+  }
+}
+
 __device__ __forceinline__ void mk1a_deferred(int64_t n, const MVecs &v, const volatile MultiScalars *vs, int c,
                                               int pass) {
-  const double xp = vs->xpend[c], xh = vs->xhold[c], beta = vs->beta[c];
-  const int act = vs->active[c];
-  if (!act && xp == 0.0 && xh == 0.0) return;
-  double *__restrict__ P0 = v.P + (size_t)c * v.ld;
-  double *__restrict__ P1 = v.P1 + (size_t)c * v.ld;
-  double *__restrict__ X = v.X + (size_t)c * v.ld;
-  const double *__restrict__ Z = v.Z + (size_t)c * v.ld;
+  const int xm = pass >> 4, xj = pass & 15;
+  const double xp = vs->xpend[c], beta = vs->beta[c];
+  const int act = vs->active[c], nh = vs->nheld[c];
+  if (!act && xp == 0.0 && nh == 0) return;
+  const size_t o = (size_t)c * v.ld;
   const int64_t t0 = (int64_t)blockIdx.x * BLOCK + threadIdx.x, ts = (int64_t)gridDim.x * BLOCK;
-  if (!act) {  // just frozen: the owed updates, held direction first
-    const int lb = vs->lbuf[c];
-    const double *Pl = lb ? P1 : P0, *Ph = lb ? P0 : P1;
+  if (!act) {  // just frozen: the owed updates, held directions first
+    const double *Pl = mbuf(v, vs->lbuf[c]) + o;
+    double ah[3];
+    for (int h = 0; h < 3; h++) ah[h] = vs->ahold[h][c];
+    double *X = v.X + o;
     for (int64_t i = t0; i < n; i += ts) {
       double x = X[i];
-      if (xh != 0.0) x = __fma_rn(xh, Ph[i], x);
+      for (int h = 0; h < nh; h++)
+        if (ah[h] != 0.0) x = __fma_rn(ah[h], mbuf(v, h)[o + i], x);
       if (xp != 0.0) x = __fma_rn(xp, Pl[i], x);
       X[i] = x;
     }
     return;
   }
-  const int64_t npair = n >> 1;
-  const double2 *__restrict__ Z2 = reinterpret_cast<const double2 *>(Z);
-  if (pass == 1) {
-    const double2 *__restrict__ A2 = reinterpret_cast<const double2 *>(P0);
-    double2 *__restrict__ B2 = reinterpret_cast<double2 *>(P1);
+  if (xj < xm - 1) {  // hold: P[j+1] = Z + beta P[j]
+    const double *src = mbuf(v, xj) + o;
+    double *dst = mbuf(v, xj + 1) + o;
+    const double *Z = v.Z + o;
+    const int64_t npair = n >> 1;
+    const double2 *__restrict__ A2 = reinterpret_cast<const double2 *>(src);
+    double2 *__restrict__ B2 = reinterpret_cast<double2 *>(dst);
+    const double2 *__restrict__ Z2 = reinterpret_cast<const double2 *>(Z);
     for (int64_t t = t0; t < npair; t += ts) {
       const double2 po = __ldcs(A2 + t), zz = __ldcs(Z2 + t);
       B2[t] = make_double2(__fma_rn(beta, po.x, zz.x), __fma_rn(beta, po.y, zz.y));
     }
-    if ((n & 1) && t0 == 0) P1[n - 1] = __fma_rn(beta, P0[n - 1], Z[n - 1]);
+    if ((n & 1) && t0 == 0) dst[n - 1] = __fma_rn(beta, src[n - 1], Z[n - 1]);
+  } else if (xm == 4) {
+    mk1a_apply<4>(n, v, vs, c, xp, beta);
   } else {
-    double2 *__restrict__ A2 = reinterpret_cast<double2 *>(P0);
-    const double2 *__restrict__ B2 = reinterpret_cast<const double2 *>(P1);
-    double2 *__restrict__ X2 = reinterpret_cast<double2 *>(X);
-    for (int64_t t = t0; t < npair; t += ts) {
-      const double2 pk = B2[t], pm = __ldcs(A2 + t), zz = __ldcs(Z2 + t);
-      double2 xx = __ldcs(X2 + t);
-      xx.x = __fma_rn(xp, pk.x, __fma_rn(xh, pm.x, xx.x));
-      xx.y = __fma_rn(xp, pk.y, __fma_rn(xh, pm.y, xx.y));
-      __stcs(X2 + t, xx);
-      A2[t] = make_double2(__fma_rn(beta, pk.x, zz.x), __fma_rn(beta, pk.y, zz.y));
-    }
-    if ((n & 1) && t0 == 0) {
-      const int64_t i = n - 1;
-      const double pk = P1[i];
-      X[i] = __fma_rn(xp, pk, __fma_rn(xh, P0[i], X[i]));
-      P0[i] = __fma_rn(beta, pk, Z[i]);
-    }
+    mk1a_apply<2>(n, v, vs, c, xp, beta);
   }
 }
 
@@ -618,16 +665,20 @@ __global__ void mreplace_kernel(int64_t n, MVecs v, const MultiScalars *sc) {
 }
 
 // deferred X_c += xpend_c P_c after the loop stops; grid (gx, k)
-// (deferred x update: the held direction first, then the latest one in P[lbuf])
+// (deferred x update: the held directions first, then the latest one in P[lbuf])
 __global__ void mtail_kernel(int64_t n, MVecs v, const MultiScalars *sc) {
   const int c = blockIdx.y;
-  const double xp = sc->xpend[c], xh = sc->xhold[c];
-  if (xp == 0.0 && xh == 0.0) return;
+  const double xp = sc->xpend[c];
+  const int nh = sc->nheld[c];
+  if (xp == 0.0 && nh == 0) return;
   const size_t o = (size_t)c * v.ld;
-  const double *Pl = (sc->lbuf[c] ? v.P1 : v.P) + o, *Ph = (sc->lbuf[c] ? v.P : v.P1) + o;
+  const double *Pl = mbuf(v, sc->lbuf[c]) + o;
+  double ah[3];
+  for (int h = 0; h < 3; h++) ah[h] = sc->ahold[h][c];
   for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
     double x = v.X[o + i];
-    if (xh != 0.0) x = __fma_rn(xh, Ph[i], x);
+    for (int h = 0; h < nh; h++)
+      if (ah[h] != 0.0) x = __fma_rn(ah[h], mbuf(v, h)[o + i], x);
     if (xp != 0.0) x = __fma_rn(xp, Pl[i], x);
     v.X[o + i] = x;
   }
@@ -635,7 +686,8 @@ __global__ void mtail_kernel(int64_t n, MVecs v, const MultiScalars *sc) {
 __global__ void mclear_xpend_kernel(MultiScalars *sc) {
   for (int c = 0; c < KMAX; c++) {
     sc->xpend[c] = 0.0;
-    sc->xhold[c] = 0.0;
+    for (int h = 0; h < 3; h++) sc->ahold[h][c] = 0.0;
+    sc->nheld[c] = 0;
     sc->lbuf[c] = 0;
   }
 }
@@ -653,9 +705,9 @@ static int64_t mld(int64_t n) { return ((n > 0 ? n : 1) + 31) / 32 * 32; }
 pcg_status ensure_multi_work(pcg_matrix *A, int k) {
   SolveWork &w = A->work;
   if (w.kcap >= k && w.msc) return PCG_OK;
-  for (double *p : {w.mr, w.mz, w.mq, w.mp[0], w.mp[1], w.mx, w.mb, w.mw})
+  for (double *p : {w.mr, w.mz, w.mq, w.mp[0], w.mp[1], w.mp23[0], w.mp23[1], w.mx, w.mb, w.mw})
     if (p) cudaFree(p);
-  w.mr = w.mz = w.mq = w.mp[0] = w.mp[1] = w.mx = w.mb = w.mw = nullptr;
+  w.mr = w.mz = w.mq = w.mp[0] = w.mp[1] = w.mp23[0] = w.mp23[1] = w.mx = w.mb = w.mw = nullptr;
   if (w.mloop_exec) cudaGraphExecDestroy(w.mloop_exec);
   if (w.mloop_graph) cudaGraphDestroy(w.mloop_graph);
   w.mloop_exec = nullptr;
@@ -688,7 +740,7 @@ pcg_status ensure_multi_work(pcg_matrix *A, int k) {
 
 static MVecs mvecs_of(pcg_matrix *A) {
   SolveWork &w = A->work;
-  return MVecs{w.mr, w.mz, w.mq, w.mp[0], w.mx, w.mw, w.mp[1], w.mb, A->d_dinv, mld(A->n)};
+  return MVecs{w.mr, w.mz, w.mq, w.mp[0], w.mx, w.mw, w.mp[1], w.mp23[0], w.mp23[1], w.mb, A->d_dinv, mld(A->n)};
 }
 
 // streaming passes: grid (gx, k) with gx * k ~ 8 blocks per SM
@@ -1053,7 +1105,10 @@ static void launch_mspmm(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cu
   const int g = mgrid_spmm(A, k);
   const SellView S = A->sell();
   MVecs v = mvecs_of(A);
-  if (pass == 1) v.P = v.P1;  // a hold pass wrote the directions to P1
+  if (pass) {  // the block this pass's K1a wrote: P[j+1] after a hold, P[0] after the apply
+    const int xm = pass >> 4, xj = pass & 15;
+    v.P = mbuf(v, xj < xm - 1 ? xj + 1 : 0);
+  }
   const size_t smem = MODE == MS_SPMM && k <= 16 ? sizeof(double) * BLOCK * k : 0;
   if (A->max_row_len > 8)
     mspmm_kernel<MODE, true><<<g, BLOCK, smem, st>>>(S, v, w.msc, w.mpart, k, spmm_prefetch(), use_cond, h, pass);
@@ -1109,9 +1164,25 @@ static double *mpart_rz(pcg_matrix *A) { return A->work.mpart + (size_t)3 * KMAX
 
 // deferred x update for the k-column loop (mk1a_deferred): not with the windowed SpMM
 // (opt-in); PCG_XDEFER=0 turns it off
-static bool mxdefer(const pcg_matrix *A) {
+static int mxdefer(const pcg_matrix *A) {  // the cycle M (0: off); PCG_XDEFER as solver.cu
+  if (A->wplan == 1) return 0;
   const char *e = getenv("PCG_XDEFER");
-  return A->wplan != 1 && !(e && atoi(e) == 0);
+  const int m = e ? atoi(e) : PCG_MXDEFER_M;
+  return m == 2 || m == 4 ? m : (m == 0 ? 0 : PCG_MXDEFER_M);
+}
+static int mxd_arg(int m, int u) { return m ? (m << 4) | (u % m) : 0; }
+
+// the 4-cycle's direction blocks P[2], P[3] (once per workspace)
+static pcg_status ensure_mdir(pcg_matrix *A, int k, int m) {
+  SolveWork &w = A->work;
+  if (m != 4 || w.mp23[0]) return PCG_OK;
+  const size_t nk = sizeof(double) * (size_t)mld(A->n) * (size_t)w.kcap;
+  for (double *&q : w.mp23) {
+    PCG_CUDA(cudaMalloc(&q, nk));
+    PCG_CUDA(cudaMemset(q, 0, nk));
+  }
+  (void)k;
+  return PCG_OK;
 }
 
 static pcg_status mlaunch_iteration(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h,
@@ -1129,6 +1200,7 @@ static pcg_status mlaunch_iteration(pcg_matrix *A, int k, cudaStream_t st, int u
 
 static pcg_status mbuild_graph(pcg_matrix *A, int k) {
   SolveWork &w = A->work;
+  PCG_TRY(ensure_mdir(A, k, mxdefer(A)));
   if (w.mgraph_k == k && w.mloop_exec) return PCG_OK;
   if (w.mloop_exec) cudaGraphExecDestroy(w.mloop_exec);
   if (w.mloop_graph) cudaGraphDestroy(w.mloop_graph);
@@ -1151,9 +1223,9 @@ static pcg_status mbuild_graph(pcg_matrix *A, int k) {
   cudaGraph_t body = np.conditional.phGraph_out[0];
   PCG_CUDA(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   pcg_status s = PCG_OK;
-  const bool xd = mxdefer(A);
-  for (int u = 0; u < 2 && s == PCG_OK; u++)  // body = two iterations (hold, apply)
-    s = mlaunch_iteration(A, k, cap, 1, h, xd ? 1 + u : 0);
+  const int xm = mxdefer(A);
+  const int nbody = xm == 4 ? 4 : 2;  // body = one deferral cycle
+  for (int u = 0; u < nbody && s == PCG_OK; u++) s = mlaunch_iteration(A, k, cap, 1, h, mxd_arg(xm, u));
   cudaGraph_t out;
   cudaError_t e = cudaStreamEndCapture(cap, &out);
   if (s != PCG_OK) return s;
@@ -1269,7 +1341,7 @@ static pcg_status solve_multi_chunk(pcg_matrix *A, int k, const double *B, int64
       const double nn = (double)n, nz = (double)A->nnz;
       // the matrix pass is shared: per block iteration 12 nnz + 4(n+1), attributed 1/k per
       // column, plus 96 n per column iteration (SURVEY §8(d), 3-pass schedule)
-      I.bytes_algorithmic = (double)kmax * (12.0 * nz + 4.0 * (nn + 1)) / k + (double)h->k[c] * (mxdefer(A) ? 92.0 : 96.0) * nn;
+      I.bytes_algorithmic = (double)kmax * (12.0 * nz + 4.0 * (nn + 1)) / k + (double)h->k[c] * (96.0 - (mxdefer(A) == 4 ? 6.0 : mxdefer(A) == 2 ? 4.0 : 0.0)) * nn;
       I.flops = (double)h->k[c] * (2.0 * nz + 13.0 * nn);
     }
   }
@@ -1291,6 +1363,7 @@ extern "C" pcg_status pcg_profile_multi(pcg_matrix_t A, int32_t k, const double 
   PCG_CUDA(cudaSetDevice(A->device));
   cudaStream_t st = (cudaStream_t)stream;
   PCG_TRY(multi_prepare(A, k, st));
+  PCG_TRY(ensure_mdir(A, k, mxdefer(A)));
   SolveWork &w = A->work;
   const int64_t n = A->n, ld = mld(n);
   PCG_CUDA(cudaMemcpy2DAsync(A->d_perm ? w.mw : w.mb, sizeof(double) * ld, B, sizeof(double) * ldb,
@@ -1310,7 +1383,7 @@ extern "C" pcg_status pcg_profile_multi(pcg_matrix_t A, int32_t k, const double 
   for (auto &e : ev) PCG_CUDA(cudaEventCreate(&e));
   PCG_CUDA(cudaEventRecord(ev[0], st));
   for (int r = 0; r < reps; r++) {
-    const int pass = mxdefer(A) ? 1 + (r & 1) : 0;
+    const int pass = mxd_arg(mxdefer(A), r);
     mk1a_kernel<<<gv, BLOCK, 0, st>>>(n, v, w.msc, 0, 0, pass);
     PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
     launch_mspmm<MS_SPMM>(A, k, st, 0, 0, pass);

@@ -43,7 +43,8 @@ Kp = 1
 while Kp < k:
     Kp *= 2
 mat = 12.0 * nnz + 4.0 * (n + 1)
-byts = [(36.0 if os.environ.get("PCG_XDEFER", "1") != "0" else 40.0) * k * n, mat + 16.0 * k * n, 40.0 * k * n]
+byts = [{0: 40.0, 2: 36.0, 4: 34.0}.get(int(os.environ.get("PCG_XDEFER", "4")), 34.0) * k * n, mat + 16.0 * k * n,
+        40.0 * k * n]
 out = {"config": a.config, "c": spec.c, "n": n, "nnz": nnz, "k": k, "K": Kp,
        "env": {kk: v for kk, v in os.environ.items() if kk.startswith("PCG_")},
        "us": list(us), "GBps": [b_ / u / 1e3 if u else 0 for b_, u in zip(byts, us)],
