@@ -206,3 +206,34 @@ def test_deferred_x_multi_bitwise_breakdown(pcg, monkeypatch, mode):
         xd, sd, _, _ = _msolve(Md, B, tol=1e-12, max_iter=2000)
         xe, se, _, _ = _msolve(Me, B, tol=1e-12, max_iter=2000)
         assert sd == se and np.array_equal(xd, xe), f
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 33, 65, 97])
+def test_deferred_x_tiny_and_ragged_graph_loop(pcg, monkeypatch, n):
+    """the graph loop (one-chunk SpMV, x every 4th iteration) on tiny / ragged systems:
+    n below one slice, odd n (the streaming passes' pair tail), a ragged last slice;
+    bitwise the every-iteration x, and the oracle's solution"""
+    rng = np.random.default_rng(n)
+    T = np.diag(np.full(n, 2.5)) - np.diag(np.ones(n - 1), 1) - np.diag(np.ones(n - 1), -1) if n > 1 else np.eye(1) * 2.0
+    A = O.Csr(n, *[np.asarray(v) for v in _csr_arrays(T)])
+    b = rng.standard_normal(n)
+    Md, Me = _pair(pcg, monkeypatch, A, True, "4")
+    xd, sd, infd = _solve(Md, b, tol=1e-12)
+    xe, se, infe = _solve(Me, b, tol=1e-12)
+    assert sd == se == 0 and infd["iterations"] == infe["iterations"] and np.array_equal(xd, xe)
+    r = O.pcg(A, b, tol=1e-12)
+    assert np.linalg.norm(xd - r.x) <= 1e-9 * np.linalg.norm(r.x)
+    for mi in (1, 2, 3, 5):
+        xd, _, _ = _solve(Md, b, tol=1e-14, max_iter=mi)
+        xe, _, _ = _solve(Me, b, tol=1e-14, max_iter=mi)
+        assert np.array_equal(xd, xe), mi
+
+
+def _csr_arrays(D):
+    rp, cols, vals = [0], [], []
+    for i in range(D.shape[0]):
+        nz = np.nonzero(D[i])[0]
+        cols += list(nz)
+        vals += list(D[i, nz])
+        rp.append(len(cols))
+    return np.array(rp, dtype=np.int64), np.array(cols, dtype=np.int64), np.array(vals, dtype=np.float64)
