@@ -35,11 +35,14 @@ K1A_BYTES = {0: 40.0, 2: 36.0, 4: 34.0}
 
 
 def xdefer_cycle():
-    """the single-RHS loop's deferral cycle as the library reads PCG_XDEFER (default 4)"""
+    """the deferral cycle as the library reads PCG_XDEFER (solver.cu xdefer_m: atoi; 0 off,
+    2 or 4, anything else the default 4)"""
     v = os.environ.get("PCG_XDEFER")
     if v is None:
         return 4
-    m = int(v) if v.strip().lstrip("-").isdigit() else 4
+    import re
+    mt = re.match(r"\s*([+-]?\d+)", v)
+    m = int(mt.group(1)) if mt else 0  # atoi: no leading number -> 0
     return m if m in (0, 2, 4) else 4
 
 

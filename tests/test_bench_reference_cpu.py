@@ -36,3 +36,22 @@ def test_reference_arm_measures_the_oracle_without_the_product():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert 0 < d["value"] < 60
     assert "LOADED_PRODUCT=false" in out.stdout
+
+
+def test_bench_k1a_byte_accounting(monkeypatch):
+    """bench.py's K1a bytes per row over the deferred x update's cycle M follow the
+    passes' loads and stores: M - 1 holds read z and p and write p (24),
+    the apply reads z, the M directions and x and writes p and x (8 (M + 2) + 16);
+    PCG_XDEFER is parsed as the library parses it (atoi: 0 / 2 / 4, other numbers 4,
+    no number 0)."""
+    import runpy
+    g = runpy.run_path(os.path.join(ROOT, "bench.py"), run_name="bench_module")
+    for m, v in g["K1A_BYTES"].items():
+        want = 40.0 if m == 0 else ((m - 1) * 24 + 8 * (m + 2) + 16) / m
+        assert v == want, (m, v, want)
+    for env, m in ((None, 4), ("0", 0), ("2", 2), ("4", 4), ("1", 4), ("7", 4), ("x", 0), (" 2", 2)):
+        if env is None:
+            monkeypatch.delenv("PCG_XDEFER", raising=False)
+        else:
+            monkeypatch.setenv("PCG_XDEFER", env)
+        assert g["xdefer_cycle"]() == m, env
