@@ -279,13 +279,9 @@ __device__ __forceinline__ void ilu_sweep(const IluView &P, const IluLevel *lv, 
 #ifndef PCG_ILU_THREADS
 #define PCG_ILU_THREADS 256
 #endif
-#ifndef PCG_ILU_SPT  // level slots per thread held in the ring
-#define PCG_ILU_SPT 1
-#endif
 constexpr int ILU_RING = PCG_ILU_RING;
 constexpr int ILU_THREADS = PCG_ILU_THREADS;
-constexpr int ILU_SPT = PCG_ILU_SPT;
-constexpr int ILU_RSLOTS = ILU_THREADS * ILU_SPT;
+constexpr int ILU_RSLOTS = ILU_THREADS;
 template <int CMAX>
 struct IluRing {
   int row[ILU_RING][ILU_RSLOTS];
@@ -314,18 +310,14 @@ __device__ __forceinline__ void ilu_sweep_ring(const IluView &P, const IluLevel 
     if (l < nl) {
       const IluLevel L = lv[l];
       const int q = l % ILU_RING;
-#pragma unroll
-      for (int j = 0; j < ILU_SPT; j++) {
-        const int ts = t + j * ILU_THREADS;
-        if (ts < L.m) {
-          const int64_t s = L.row_base + ts;
-          cp_async4(&R.row[q][ts], P.row + s);
-          if (backward) cp_async8(&R.ud[q][ts], P.ud + s);
-          for (int u = 0; u < L.c; u++) {
-            const int64_t e = L.ent_base + (int64_t)u * L.m + ts;
-            cp_async4(&R.k[q][u][ts], P.kcol + e);
-            cp_async8(&R.f[q][u][ts], P.fv + e);
-          }
+      if (t < L.m) {
+        const int64_t s = L.row_base + t;
+        cp_async4(&R.row[q][t], P.row + s);
+        if (backward) cp_async8(&R.ud[q][t], P.ud + s);
+        for (int u = 0; u < L.c; u++) {
+          const int64_t e = L.ent_base + (int64_t)u * L.m + t;
+          cp_async4(&R.k[q][u][t], P.kcol + e);
+          cp_async8(&R.f[q][u][t], P.fv + e);
         }
       }
     }
@@ -339,20 +331,18 @@ __device__ __forceinline__ void ilu_sweep_ring(const IluView &P, const IluLevel 
     cp_async_wait<ILU_RING - 1>();  // this thread's copies for level l have landed
     const IluLevel L = lv[l];
     const int q = l % ILU_RING;
-#pragma unroll
-    for (int j = 0; j < ILU_SPT; j++) {
-      const int ts = t + j * ILU_THREADS;
-      if (ts < L.m) {
-        const int i = R.row[q][ts];
-        double acc = y[i];
-        for (int u = 0; u < L.c; u++) {
-          const int k = R.k[q][u][ts];
-          if (k >= 0) acc = __dsub_rn(acc, __dmul_rn(R.f[q][u][ts], y[k]));
-        }
-        y[i] = backward ? __ddiv_rn(acc, R.ud[q][ts]) : acc;
+    if (t < L.m) {
+      const int i = R.row[q][t];
+      double acc = y[i];
+      for (int u = 0; u < L.c; u++) {
+        const int k = R.k[q][u][t];
+        if (k >= 0) acc = __dsub_rn(acc, __dmul_rn(R.f[q][u][t], y[k]));
       }
+      y[i] = backward ? __ddiv_rn(acc, R.ud[q][t]) : acc;
     }
-    for (int t2 = t + ILU_RSLOTS; t2 < L.m; t2 += blockDim.x) {  // levels wider than the ring's slots
+    // levels wider than the CTA (a run-time stride: a compile-time one made the compiler
+    // restructure this loop and cost the one-block Cube 1 solve 26 %, 4.36 -> 5.49 s)
+    for (int t2 = t + blockDim.x; t2 < L.m; t2 += blockDim.x) {
       IluSlot sx;
       int kx[CMAX];
       double fx[CMAX];
