@@ -568,6 +568,22 @@ def main():
                 "iteration": {"bytes": sum(byts), "us": it_us, "frac": sum(byts) / it_us / 1e3 / hbm,
                               "frac_vs_88n_ideal": (mat + 88.0 * n) / it_us / 1e3 / hbm}}
         ro = read_only_peak()
+        if stats["schedule"] == 3 and stats["dia_positions"] > 0:
+            # the uniform-offset SELL positions carry no column ids: the bytes this K1b moves are
+            # fewer than §8(d)'s 12 per entry (values 8 per stored entry, ids 4 only at the other
+            # positions, per slice 8 offsets + a mask + its slice offset, p read once, q written)
+            se = float(stats["sell_entries"])
+            ns = (n + 31) // 32
+            fb = 8.0 * se + 4.0 * (se - 32.0 * stats["dia_positions"]) + 41.0 * ns + 8.0 + 16.0 * n
+            k1b = kern[1]
+            roof["format_bytes"] = {"kernel": "k1b_kernel", "bytes_per_launch": fb,
+                                    "achieved_GBps": fb / k1b["us_per_launch"] / 1e3,
+                                    "frac_vs_copy_peak": fb / k1b["us_per_launch"] / 1e3 / hbm,
+                                    "id_free_positions": stats["dia_positions"], "positions": se / 32.0,
+                                    "note": "frac > 1 by the section 8(d) bytes (12 per entry, CSR ids) is "
+                                            "the id-free format moving fewer bytes than that ideal"}
+            if ro:
+                roof["format_bytes"]["frac_vs_read_only_peak"] = fb / k1b["us_per_launch"] / 1e3 / ro["GBps"]
         if ro:  # the contract's peak is a copy (read + write); K1b's stream is ~93 % reads
             roof["read_only_stream_peak"] = dict(ro, frac=dom["achieved_GBps"] / ro["GBps"])
         k_us = list(us)

@@ -124,6 +124,11 @@ typedef struct {
   int32_t short_rows;        /* 1: SELL-32 with every row <= 8 entries runs the one-chunk row
                                 engine (64 registers, 4 resident blocks/SM instead of 3; same
                                 entries, same sums); environment PCG_SHORT=0 at csr_create: off */
+  int32_t dia_slices;        /* slices made only of such positions (one dependent round trip) */
+  int64_t dia_positions;     /* one-chunk engine: (slice, position) pairs whose entries all have the
+                                same col - row, read without column ids; a slice made only of such
+                                positions issues its gathers with its values (one dependent round trip);
+                                same columns, so the same sums; PCG_DIA=0 at csr_create: off */
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */

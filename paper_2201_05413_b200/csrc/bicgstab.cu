@@ -162,6 +162,7 @@ __device__ __forceinline__ void spmv_body(const SellView &S, const CsrView &C, c
   };
   if (FMT == PCG_FORMAT_SELL) sell_rows(S, gather, epi);
   else if (FMT == FMT_SELL_SHORT) sell_rows_short(S, gather, epi);  // rows of <= 8 entries (graph schedule)
+  else if (FMT == FMT_SELL_DIA) sell_rows_dia(S, gather, epi);
   else csr_rows<L>(C, gather, epi);
 }
 
@@ -814,6 +815,7 @@ static BgOps bg_ops_t() {
 template <int BS>
 static BgOps bg_ops_bs(int fmt, int lanes) {
   if (fmt == FMT_SELL_SHORT) return bg_ops_t<FMT_SELL_SHORT, 1, BS>();
+  if (fmt == FMT_SELL_DIA) return bg_ops_t<FMT_SELL_DIA, 1, BS>();
   if (fmt == PCG_FORMAT_SELL) return bg_ops_t<PCG_FORMAT_SELL, 1, BS>();
   switch (lanes) {
     case 1: return bg_ops_t<PCG_FORMAT_CSR, 1, BS>();
@@ -834,12 +836,13 @@ static BgOps bg_ops_ilu_t() {
 // one-chunk engine where every row has <= 8 entries (pcg_matrix::short_rows), or CSR
 static int bg_fmt(const pcg_matrix *A) {
   const int f = A->format == FMT_SELL_TMA ? PCG_FORMAT_SELL : A->format;
-  return f == PCG_FORMAT_SELL && A->short_rows ? FMT_SELL_SHORT : f;
+  return f == PCG_FORMAT_SELL && A->short_rows ? (A->d_sdoff ? FMT_SELL_DIA : FMT_SELL_SHORT) : f;
 }
 
 static BgOps bg_ops(int fmt, int lanes, int bs) {
   if (bs == BS_ILU) {
     if (fmt == FMT_SELL_SHORT) return bg_ops_ilu_t<FMT_SELL_SHORT, 1>();
+    if (fmt == FMT_SELL_DIA) return bg_ops_ilu_t<FMT_SELL_DIA, 1>();
     if (fmt == PCG_FORMAT_SELL) return bg_ops_ilu_t<PCG_FORMAT_SELL, 1>();
     switch (lanes) {
       case 1: return bg_ops_ilu_t<PCG_FORMAT_CSR, 1>();
@@ -972,6 +975,7 @@ struct BgdOps {
 using BgdSpmv = void (*)(pcg_matrix *, const BicgVecs &, BgScalars *, int, int, cudaStream_t);
 static BgdSpmv bgd_spmv_fn(int fmt, int lanes) {
   if (fmt == FMT_SELL_SHORT) return BgdOps<FMT_SELL_SHORT, 1>::spmv;
+  if (fmt == FMT_SELL_DIA) return BgdOps<FMT_SELL_DIA, 1>::spmv;
   if (fmt == PCG_FORMAT_SELL) return BgdOps<PCG_FORMAT_SELL, 1>::spmv;
   switch (lanes) {
     case 1: return BgdOps<PCG_FORMAT_CSR, 1>::spmv;

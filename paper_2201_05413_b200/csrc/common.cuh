@@ -120,6 +120,12 @@ struct SellView {
   const int16_t *dcol;
   const int *cbase;
   int64_t row0;  // absolute row of the view's slice 0 (views over a row range; decoding)
+  // uniform-offset ("diagonal") positions of the one-chunk engine (null: not built): bit t
+  // of dmask[s] set when every real entry of slice s at position t has col = row +
+  // doff[8 s + t] (and the padding lanes' row + doff stay in range) — such positions
+  // need no column ids, and a slice with only such positions needs one round trip
+  const int *doff;
+  const uint8_t *dmask;
 };
 constexpr int CB_INT32 = (int)0x80000000;
 // the 16-bit id engine needs ~98 registers unconstrained (2 blocks of 256 per SM); its
@@ -130,11 +136,15 @@ constexpr int CB_INT32 = (int)0x80000000;
 #ifndef PCG_SELL_MINB  // A/B knob: 0 = unconstrained (80 registers, 3 blocks/SM)
 #define PCG_SELL_MINB 0
 #endif
+#ifndef PCG_DIA_MINB  // the uniform-offset engine: 3 blocks/SM (80 registers, no spills; 4 spill: C5 K1b 1,533 vs 1,810-1,865 us)
+#define PCG_DIA_MINB 3
+#endif
 #ifndef PCG_SHORT_MINB  // the short-row engine (rows.cuh sell_rows_short): resident blocks per SM
 #define PCG_SHORT_MINB 4
 #endif
 #define D16_MINB(FMT)                                                     \
   ((FMT) == FMT_SELL_D16 ? PCG_D16_MINB : (FMT) == FMT_SELL_SHORT ? PCG_SHORT_MINB \
+   : (FMT) == FMT_SELL_DIA ? PCG_DIA_MINB \
    : (FMT) == PCG_FORMAT_SELL ? PCG_SELL_MINB : 0)
 
 // internal format code of the TMA-staged SELL kernels (reported as PCG_FORMAT_SELL_TMA)
@@ -143,6 +153,7 @@ constexpr int FMT_SELL_TMA = 3;
 // sell_rows_d16): the SpMV, K1b and residual passes of the 3-pass schedule
 constexpr int FMT_SELL_D16 = 5;
 constexpr int FMT_SELL_SHORT = 6;  // SELL-32, every row <= 8 entries: one-chunk engine
+constexpr int FMT_SELL_DIA = 7;    // the one-chunk engine with uniform-offset positions (no ids)
 
 // ------------------------------------------------------------------ reductions
 constexpr int BLOCK = 256;

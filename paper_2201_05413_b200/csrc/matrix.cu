@@ -311,7 +311,79 @@ pcg_status build_d16(pcg_matrix *A, cudaStream_t st) {
   return PCG_OK;
 }
 
+// Uniform-offset positions (SellView::doff / dmask), one warp per slice of at most 8
+// entries per row: position t of slice s is uniform when every real entry there has
+// the same col - row = d, and every padding lane's row + d lies in [0, n_cols) (its
+// value is 0: fma(0, p[row + d], s) == s, as with the stored padding column).
+__global__ void dia_build_kernel(int64_t n, int64_t n_cols, int64_t n_slices, const int *__restrict__ rp,
+                                 const int64_t *__restrict__ slice_ptr, const int *__restrict__ scol,
+                                 int *__restrict__ doff, uint8_t *__restrict__ dmask,
+                                 unsigned long long *__restrict__ n_pos) {
+  const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= n_slices) return;
+  const int64_t row = s * 32 + lane;
+  const int64_t base = slice_ptr[s];
+  const int len = (int)((slice_ptr[s + 1] - base) >> 5);
+  const int rl = row < n ? rp[row + 1] - rp[row] : 0;
+  unsigned mask = 0;
+  for (int t = 0; t < len && t < 8; t++) {
+    const int64_t e = base + (int64_t)t * 32 + lane;
+    const bool real = t < rl;
+    const long long off = (long long)scol[e] - row;
+    long long lo = real ? off : LLONG_MAX, hi = real ? off : LLONG_MIN;
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, (long long)__shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, (long long)__shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    bool ok = lo != LLONG_MAX && lo == hi && lo >= INT_MIN && lo <= INT_MAX;
+    if (ok && !real) {
+      const long long c = row + lo;
+      ok = c >= 0 && c < n_cols;
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (ok) mask |= 1u << t;
+    if (lane == 0) doff[s * 8 + t] = ok ? (int)lo : 0;
+  }
+  if (lane == 0) {
+    dmask[s] = (uint8_t)mask;
+    atomicAdd(n_pos, (unsigned long long)__popc(mask));
+    if (len <= 8 && mask == (1u << len) - 1u) atomicAdd(n_pos + 1, 1ull);  // one-round-trip slice
+  }
+}
+
+pcg_status build_dia(pcg_matrix *A, cudaStream_t st) {
+  const char *e = getenv("PCG_DIA");  // PCG_DIA=0: ids at every position
+  if (A->d_sdoff || !A->d_slice_ptr || A->n_slices == 0 || !A->short_rows || (e && atoi(e) == 0)) return PCG_OK;
+  PCG_CUDA(cudaMalloc(&A->d_sdoff, sizeof(int) * 8 * (size_t)A->n_slices));
+  PCG_CUDA(cudaMalloc(&A->d_sdmask, (size_t)A->n_slices));
+  PCG_CUDA(cudaMemsetAsync(A->d_sdoff, 0, sizeof(int) * 8 * (size_t)A->n_slices, st));
+  unsigned long long *d_n;
+  PCG_CUDA(cudaMalloc(&d_n, 2 * sizeof(unsigned long long)));
+  PCG_CUDA(cudaMemsetAsync(d_n, 0, 2 * sizeof(unsigned long long), st));
+  dia_build_kernel<<<(unsigned)((A->n_slices * 32 + 255) / 256), 256, 0, st>>>(
+      A->n, A->n + A->n_ghost, A->n_slices, A->d_row_ptr, A->d_slice_ptr, A->d_scol, A->d_sdoff, A->d_sdmask, d_n);
+  count_launch();
+  unsigned long long np[2] = {0, 0};
+  PCG_CUDA(cudaMemcpyAsync(np, d_n, sizeof(np), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_n);
+  A->dia_positions = (int64_t)np[0];
+  A->dia_slices = (int64_t)np[1];
+  A->device_bytes += 33.0 * (double)A->n_slices;
+  return PCG_OK;
+}
+
 void free_sell(pcg_matrix *A) {
+  if (A->d_sdoff) {
+    cudaFree(A->d_sdoff);
+    cudaFree(A->d_sdmask);
+    A->device_bytes -= 33.0 * (double)A->n_slices;
+    A->d_sdoff = nullptr;
+    A->d_sdmask = nullptr;
+    A->dia_positions = 0;
+    A->dia_slices = 0;
+  }
   if (A->d_wdesc) cudaFree(A->d_wdesc);
   if (A->d_wlidx) cudaFree(A->d_wlidx);
   A->d_wdesc = nullptr;
@@ -623,8 +695,9 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
     const char *se = getenv("PCG_SHORT");
     A->short_rows = A->format == PCG_FORMAT_SELL && !A->d_sdcol && A->max_row_len <= 8 && !(se && atoi(se) == 0);
     if (A->short_rows) {
+      PCG_TRY(build_dia(A, st));
       const int64_t need = (A->n_slices + WARPS - 1) / WARPS;
-      const int64_t g = (int64_t)sms * k1_blocks_per_sm(FMT_SELL_SHORT, 1, 0);
+      const int64_t g = (int64_t)sms * k1_blocks_per_sm(A->d_sdoff ? FMT_SELL_DIA : FMT_SELL_SHORT, 1, 0);
       A->grid_spmv = (int)std::max<int64_t>(1, std::min(g, need));
     }
   }
@@ -806,5 +879,7 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->d16_slices = A->d16_slices;
   o->spmm_windowed = A->wplan;
   o->short_rows = A->short_rows ? 1 : 0;
+  o->dia_positions = A->dia_positions;
+  o->dia_slices = (int32_t)std::min<int64_t>(A->dia_slices, INT32_MAX);
   return PCG_OK;
 }

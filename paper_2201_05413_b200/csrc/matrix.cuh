@@ -170,8 +170,14 @@ struct pcg_matrix {
   int16_t *d_sdcol = nullptr;
   int *d_scbase = nullptr;
   int64_t d16_slices = 0;
+  // uniform-offset positions of the one-chunk engine (common.cuh SellView::doff / dmask)
+  int *d_sdoff = nullptr;
+  uint8_t *d_sdmask = nullptr;
+  int64_t dia_positions = 0;  // positions without ids, over all slices
+  int64_t dia_slices = 0;     // slices made only of such positions (one dependent round trip)
   pcgb::SellView sell() const {
-    return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0, d_sdcol, d_scbase, 0};
+    return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0, d_sdcol, d_scbase, 0,
+            d_sdoff, d_sdmask};
   }
 };
 

@@ -25,6 +25,9 @@ __device__ __forceinline__ void cols_ready(int (&j)[N], int zero) {
   for (int u = 0; u < N; u++) j[u] |= x;
 }
 
+#ifndef PCG_DIA_RUN  // consecutive slices per warp and grid-stride step of the uniform-offset engine
+#define PCG_DIA_RUN 8
+#endif
 #ifndef PCG_SELL_CH  // entries per chunk of the general SELL engine (A/B knob)
 #define PCG_SELL_CH 8
 #endif
@@ -136,6 +139,97 @@ __device__ __forceinline__ void sell_rows_short(const SellView &A, Gather gather
     if (row < A.n) epi(row, sum);
     base = base2;
     next = next2;
+  }
+}
+
+// The one-chunk engine with uniform-offset positions (SellView::doff / dmask): the next
+// slice's mask and offsets are fetched with its slice offsets (indexed by slice: no
+// dependent load).  A slice whose positions are all uniform knows its gather addresses
+// before any of its loads return and issues values and gathers together: ONE dependent
+// round trip instead of two; other slices load ids at their non-uniform positions.
+// The same columns as sell_rows_short (bitwise the same sums).
+template <class Gather, class Epi>
+__device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, Epi epi) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  // views over a row range (the distributed overlap) start at slice row0 / 32 of the
+  // per-slice arrays, and the offsets are relative to the absolute row
+  const uint8_t *dmask = A.dmask + (A.row0 >> 5);
+  const int *doff = A.doff + (A.row0 >> 5) * 8;
+  // Each warp takes DIA_RUN consecutive slices per grid-stride step: slices that need two
+  // round trips recur with the row-line period of a lattice (Cube 3: 2 of every 16) and a
+  // plain grid stride (a multiple of 16 warps) would hand them all to the same warps
+  constexpr int RUN = PCG_DIA_RUN;
+  auto next_of = [&](int64_t x) { return (x + 1) % RUN != 0 ? x + 1 : x + 1 + (nw - 1) * RUN; };
+  int64_t s = w0 * RUN, base = 0, next = 0;
+  unsigned mask = 0;
+  int offl = 0;
+  if (s < A.n_slices) {
+    base = A.slice_ptr[s];
+    next = A.slice_ptr[s + 1];
+    mask = dmask[s];
+    if (lane < 8) offl = doff[s * 8 + lane];
+  }
+  for (; s < A.n_slices; s = next_of(s)) {
+    const int len = (int)((next - base) >> 5);  // <= 8 (host-checked)
+    const double *vp = A.val + base + lane;
+    const int64_t rowv = s * 32 + lane;         // row within the view (epilogue)
+    const int row = (int)(A.row0 + rowv);       // local row (columns)
+    const unsigned full = (1u << len) - 1u;
+    const int64_t s2 = next_of(s);
+    int64_t base2 = 0, next2 = 0;
+    unsigned mask2 = 0;
+    int offl2 = 0;
+    double a[8], g[8];
+    double sum = 0.0;
+    if ((mask & full) == full) {  // every position uniform: values and gathers in one round trip
+      int j[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) j[u] = row + __shfl_sync(0xffffffffu, offl, u);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (u < len) a[u] = ld_stream(vp + (size_t)u * 32);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (u < len) g[u] = gather(j[u]);
+      if (s2 < A.n_slices) {
+        base2 = A.slice_ptr[s2];
+        next2 = A.slice_ptr[s2 + 1];
+        mask2 = dmask[s2];
+        if (lane < 8) offl2 = doff[s2 * 8 + lane];
+      }
+    } else {  // ids at the non-uniform positions (issued first), then the values
+      const int *cp = A.col + base + lane;
+      int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (u < len && !(mask >> u & 1)) j[u] = ld_stream(cp + (size_t)u * 32);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (u < len) a[u] = ld_stream(vp + (size_t)u * 32);
+      if (s2 < A.n_slices) {
+        base2 = A.slice_ptr[s2];
+        next2 = A.slice_ptr[s2 + 1];
+        mask2 = dmask[s2];
+        if (lane < 8) offl2 = doff[s2 * 8 + lane];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (mask >> u & 1) j[u] = row + __shfl_sync(0xffffffffu, offl, u);
+      cols_ready(j, A.zero);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (u < len) g[u] = gather(j[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (u < len) sum = __fma_rn(a[u], g[u], sum);
+    if (rowv < A.n) epi(rowv, sum);
+    base = base2;
+    next = next2;
+    mask = mask2;
+    offl = offl2;
   }
 }
 

@@ -382,6 +382,8 @@ __global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) k1b_kernel(SellView S, C
     sell_rows_d16(S, gather, epi);
   } else if (FMT == FMT_SELL_SHORT) {
     sell_rows_short(S, gather, epi);
+  } else if (FMT == FMT_SELL_DIA) {
+    sell_rows_dia(S, gather, epi);
   } else {
     csr_rows<L>(C, gather, epi);
   }
@@ -468,6 +470,8 @@ __global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) resid_kernel(SellView S,
     sell_rows_d16(S, gather, epi);
   } else if (FMT == FMT_SELL_SHORT) {
     sell_rows_short(S, gather, epi);
+  } else if (FMT == FMT_SELL_DIA) {
+    sell_rows_dia(S, gather, epi);
   } else {
     csr_rows<L>(C, gather, epi);
   }
@@ -578,6 +582,8 @@ __global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) spmv_kernel(SellView S, 
     sell_rows_d16(S, gather, epi);
   } else if (FMT == FMT_SELL_SHORT) {
     sell_rows_short(S, gather, epi);
+  } else if (FMT == FMT_SELL_DIA) {
+    sell_rows_dia(S, gather, epi);
   } else {
     csr_rows<L>(C, gather, epi);
   }
@@ -606,6 +612,7 @@ struct Dispatch;
   do {                                                                      \
     if ((FMTV) == FMT_SELL_D16) KERNEL<FMT_SELL_D16, 1>__VA_ARGS__;         \
     else if ((FMTV) == FMT_SELL_SHORT) KERNEL<FMT_SELL_SHORT, 1>__VA_ARGS__; \
+    else if ((FMTV) == FMT_SELL_DIA) KERNEL<FMT_SELL_DIA, 1>__VA_ARGS__;     \
     else PCG_DISPATCH(FMTV, LANES, KERNEL, __VA_ARGS__);                    \
   } while (0)
 
@@ -614,7 +621,7 @@ struct Dispatch;
 static int fmt_d16(const pcg_matrix *A, int fmt) {
   if (fmt != PCG_FORMAT_SELL) return fmt;
   if (A->d_sdcol) return FMT_SELL_D16;
-  return A->short_rows ? FMT_SELL_SHORT : fmt;
+  return A->short_rows ? (A->d_sdoff ? FMT_SELL_DIA : FMT_SELL_SHORT) : fmt;
 }
 
 static Vecs vecs_of(pcg_matrix *A) {
@@ -1074,8 +1081,9 @@ pcg_status prepare_staged(size_t smem) {
 int k1_blocks_per_sm(int fmt, int lanes, size_t smem) {
   int b = 0;
   cudaError_t e;
-  if (fmt == FMT_SELL_SHORT) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1b_kernel<FMT_SELL_SHORT, 1>, BLOCK, 0);
+  if (fmt == FMT_SELL_SHORT || fmt == FMT_SELL_DIA) {
+    e = fmt == FMT_SELL_DIA ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1b_kernel<FMT_SELL_DIA, 1>, BLOCK, 0)
+                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1b_kernel<FMT_SELL_SHORT, 1>, BLOCK, 0);
   } else if (fmt == FMT_SELL_TMA) {
     e = k1_chunk() == 4 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<FMT_SELL_TMA, 1, 4>, BLOCK, smem)
                         : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_kernel<FMT_SELL_TMA, 1, 8>, BLOCK, smem);

@@ -309,14 +309,18 @@ def test_format_choice_is_deterministic(pcg, name, c):
 def test_d16_column_form_is_bitwise_the_int32_form(pcg, monkeypatch, name, c, fmt):
     """The 16-bit delta column ids (pcg.h d16_slices) decode to the same ids as the
     int32 SELL array, so SpMV, single- and multi-RHS solves are bitwise identical with
-    and without them (PCG_NO_D16=1), and match the oracle."""
+    and without them, and match the oracle.  The int32 handle runs the same chunked
+    engine and grid (PCG_SHORT=0): the one-chunk engines visit slices in another order,
+    so their dot products round differently."""
     P = O.build_problem(name, c=c, k=2 if name == "C4" else 1)
     A = P["A"]
     monkeypatch.delenv("PCG_NO_D16", raising=False)
     monkeypatch.setenv("PCG_D16", "1")
     M1 = _matrix(pcg, A, fmt)
     monkeypatch.delenv("PCG_D16")
+    monkeypatch.setenv("PCG_SHORT", "0")
     M0 = _matrix(pcg, A, fmt)
+    monkeypatch.delenv("PCG_SHORT")
     s1, s0 = M1.stats(), M0.stats()
     assert s0["d16_slices"] == 0
     assert s1["d16_slices"] > 0.5 * ((A.n + 31) // 32), s1
@@ -359,6 +363,61 @@ def test_short_row_engine_is_bitwise_the_chunked_engine(pcg, monkeypatch, name, 
     assert abs(info["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
     P3 = O.build_problem("C3", c=16, k=1)
     assert _matrix(pcg, P3["A"], "sell").stats()["short_rows"] == 0
+
+
+def _banded_mix(n, seed):
+    """SPD, rows of <= 7 entries: a 5-point-like band (uniform offsets per slice
+    position) on the first half, random extra couplings on the second (non-uniform)"""
+    rng = np.random.default_rng(seed)
+    D = np.zeros((n, n))
+    for i in range(n):
+        for d in (-40, -1, 1, 40):
+            if 0 <= i + d < n:
+                D[i, i + d] = -1.0
+    for i in range(n // 2, n):
+        j = int(rng.integers(0, n))
+        if j != i and np.count_nonzero(D[i]) < 5 and np.count_nonzero(D[j]) < 5:
+            D[i, j] = D[j, i] = -0.5
+    D += np.diag(np.abs(D).sum(1) + 1.0)
+    return _csr(D)
+
+
+@pytest.mark.parametrize("name,c", [("C1", None), ("C5", 32), ("C4", 16), ("mix", 900)])
+def test_uniform_offset_positions_are_bitwise_the_id_form(pcg, monkeypatch, name, c):
+    """The one-chunk engine's id-free uniform-offset positions (pcg.h dia_positions):
+    the same columns, so the SpMV is bitwise the id form (PCG_DIA=0) and the chunked
+    engine (PCG_SHORT=0); the graph-loop solve meets the oracle bars; a pattern mixing
+    uniform and non-uniform slices takes both paths of the engine."""
+    if name == "mix":
+        A = _banded_mix(c, 5)
+        b = np.random.default_rng(6).standard_normal(A.n)
+        tol = 1e-10
+    else:
+        P = O.build_problem(name, c=c, k=1)
+        A, b = P["A"], P["B"][:, 0]
+        tol = O.configs()[name]["tol"]
+    monkeypatch.setenv("PCG_PERSIST", "0")
+    hs = {}
+    for key, env in (("dia", {}), ("ids", {"PCG_DIA": "0"}), ("chunked", {"PCG_SHORT": "0"})):
+        for k in ("PCG_DIA", "PCG_SHORT"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        hs[key] = _matrix(pcg, A, "sell")
+    for k in ("PCG_DIA", "PCG_SHORT"):
+        monkeypatch.delenv(k, raising=False)
+    st = hs["dia"].stats()
+    n_slices = (A.n + 31) // 32
+    assert st["short_rows"] == 1 and 0 < st["dia_positions"] <= 8 * n_slices, st
+    assert hs["ids"].stats()["dia_positions"] == 0
+    x = np.random.default_rng(12).standard_normal(A.n)
+    ys = {k: M.spmv(_dev(x)).cpu().numpy() for k, M in hs.items()}
+    assert np.array_equal(ys["dia"], ys["ids"]) and np.array_equal(ys["dia"], ys["chunked"])
+    r = O.pcg(A, b, tol=tol)
+    xs, info = hs["dia"].solve(_dev(b), tol=tol)
+    assert info["status"] == 0 and info["relres_true"] <= tol
+    assert np.linalg.norm(xs.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-9
+    assert abs(info["iterations"] - r.iterations) <= max(1, 0.02 * r.iterations)
 
 
 @pytest.mark.parametrize("k", [1, 5, 16])
