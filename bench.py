@@ -569,17 +569,19 @@ def main():
                               "frac_vs_88n_ideal": (mat + 88.0 * n) / it_us / 1e3 / hbm}}
         ro = read_only_peak()
         if stats["schedule"] == 3 and stats["dia_positions"] > 0:
-            # the uniform-offset SELL positions carry no column ids: the bytes this K1b moves are
-            # fewer than §8(d)'s 12 per entry (values 8 per stored entry, ids 4 only at the other
-            # positions, per slice 8 offsets + a mask + its slice offset, p read once, q written)
+            # one-trip (uniform-offset) slices carry no column ids: the bytes this K1b moves are
+            # fewer than §8(d)'s 12 per entry (values 8 per stored entry, ids 4 in the other
+            # slices, per slice 8 offsets + a mask + its slice offset, p read once, q written)
             se = float(stats["sell_entries"])
             ns = (n + 31) // 32
-            fb = 8.0 * se + 4.0 * (se - 32.0 * stats["dia_positions"]) + 41.0 * ns + 8.0 + 16.0 * n
+            # ids are read by the slices that are not one-trip (an average slice's entries each)
+            ids = 4.0 * se * (1.0 - stats["dia_slices"] / max(ns, 1))
+            fb = 8.0 * se + ids + 41.0 * ns + 8.0 + 16.0 * n
             k1b = kern[1]
             roof["format_bytes"] = {"kernel": "k1b_kernel", "bytes_per_launch": fb,
                                     "achieved_GBps": fb / k1b["us_per_launch"] / 1e3,
                                     "frac_vs_copy_peak": fb / k1b["us_per_launch"] / 1e3 / hbm,
-                                    "id_free_positions": stats["dia_positions"], "positions": se / 32.0,
+                                    "one_trip_slices": stats["dia_slices"], "slices": ns,
                                     "note": "frac > 1 by the section 8(d) bytes (12 per entry, CSR ids) is "
                                             "the id-free format moving fewer bytes than that ideal"}
             if ro:

@@ -146,8 +146,9 @@ __device__ __forceinline__ void sell_rows_short(const SellView &A, Gather gather
 // slice's mask and offsets are fetched with its slice offsets (indexed by slice: no
 // dependent load).  A slice whose positions are all uniform knows its gather addresses
 // before any of its loads return and issues values and gathers together: ONE dependent
-// round trip instead of two; other slices load ids at their non-uniform positions.
-// The same columns as sell_rows_short (bitwise the same sums).
+// round trip instead of two; other slices read their stored ids as sell_rows_short (a
+// per-position choice there cost 10 registers for a few bytes).  The same columns as
+// sell_rows_short (bitwise the same sums).
 template <class Gather, class Epi>
 __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, Epi epi) {
   const int lane = threadIdx.x & 31;
@@ -199,12 +200,12 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
         mask2 = dmask[s2];
         if (lane < 8) offl2 = doff[s2 * 8 + lane];
       }
-    } else {  // ids at the non-uniform positions (issued first), then the values
+    } else {  // the stored ids (issued first), then the values
       const int *cp = A.col + base + lane;
       int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
       for (int u = 0; u < 8; u++)
-        if (u < len && !(mask >> u & 1)) j[u] = ld_stream(cp + (size_t)u * 32);
+        if (u < len) j[u] = ld_stream(cp + (size_t)u * 32);
 #pragma unroll
       for (int u = 0; u < 8; u++)
         if (u < len) a[u] = ld_stream(vp + (size_t)u * 32);
@@ -214,9 +215,6 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
         mask2 = dmask[s2];
         if (lane < 8) offl2 = doff[s2 * 8 + lane];
       }
-#pragma unroll
-      for (int u = 0; u < 8; u++)
-        if (mask >> u & 1) j[u] = row + __shfl_sync(0xffffffffu, offl, u);
       cols_ready(j, A.zero);
 #pragma unroll
       for (int u = 0; u < 8; u++)
