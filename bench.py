@@ -576,14 +576,22 @@ def main():
             ns = (n + 31) // 32
             # ids are read by the slices that are not one-trip (an average slice's entries each)
             ids = 4.0 * se * (1.0 - stats["dia_slices"] / max(ns, 1))
-            fb = 8.0 * se + ids + 41.0 * ns + 8.0 + 16.0 * n
+            # values are read by the slices that are not value-uniform too (the others take
+            # their 8 per-position values, 64 B + a mask, with their offsets)
+            dv = stats.get("dval_slices", 0)
+            vals = 8.0 * se * (1.0 - dv / max(ns, 1))
+            meta = 107.0  # per slice: its offset 8, offset mask 1, 8 offsets 32, length + value mask 2, 8 values 64
+            fb = vals + ids + meta * ns + 8.0 + 16.0 * n
             k1b = kern[1]
             roof["format_bytes"] = {"kernel": "k1b_kernel", "bytes_per_launch": fb,
                                     "achieved_GBps": fb / k1b["us_per_launch"] / 1e3,
                                     "frac_vs_copy_peak": fb / k1b["us_per_launch"] / 1e3 / hbm,
-                                    "one_trip_slices": stats["dia_slices"], "slices": ns,
+                                    "one_trip_slices": stats["dia_slices"], "value_free_slices": dv,
+                                    "slices": ns,
                                     "note": "frac > 1 by the section 8(d) bytes (12 per entry, CSR ids) is "
-                                            "the id-free format moving fewer bytes than that ideal"}
+                                            "the format moving fewer bytes than that ideal: no column ids in "
+                                            "uniform-offset slices, one value per position in value-uniform "
+                                            "ones (the same values and sums)"}
             if ro:
                 roof["format_bytes"]["frac_vs_read_only_peak"] = fb / k1b["us_per_launch"] / 1e3 / ro["GBps"]
         if ro:  # the contract's peak is a copy (read + write); K1b's stream is ~93 % reads
@@ -658,7 +666,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(workload_config(args.config, c, n, nnz, world), iterations=iters,
                            format={1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[stats["format"]], setup_s=round(t_setup, 3),
-                           d16_slices=A.stats()["d16_slices"], spmm_windowed=A.stats()["spmm_windowed"],
+                           d16_slices=A.stats()["d16_slices"], dval_slices=A.stats()["dval_slices"], spmm_windowed=A.stats()["spmm_windowed"],
                            relres_true=max(i["relres_true"] for i in infos[-1]), k_rhs=kcols,
                            solver={"pcg": "jacobi-pcg", "pipelined": "pipelined jacobi-pcg (N3)",
                                    "block": "block cg, jacobi (N3)"}[args.solver],

@@ -129,6 +129,11 @@ typedef struct {
                                 same col - row, read without column ids; a slice made only of such
                                 positions issues its gathers with its values (one dependent round trip);
                                 same columns, so the same sums; PCG_DIA=0 at csr_create: off */
+  int64_t dval_slices;       /* one-round-trip slices whose 32 stored values at every position are
+                                bitwise equal (a lattice stencil's interior): one value per (slice,
+                                position) is read with the offsets and the value stream is skipped
+                                (value sharing, as CSR-VI); same values, so the same sums;
+                                PCG_DIA_VAL=0 at csr_create: off */
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */

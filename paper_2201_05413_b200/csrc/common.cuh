@@ -126,6 +126,15 @@ struct SellView {
   // need no column ids, and a slice with only such positions needs one round trip
   const int *doff;
   const uint8_t *dmask;
+  // value-uniform positions of those slices (CSR-VI-style value sharing; built with doff):
+  // bit t of dvmeta[s] set when the 32 stored values of slice s at position t (padding
+  // zeros included) are bitwise equal (none with PCG_DIA_VAL=0); that value is
+  // dval[8 s + t]; bits 8-11 hold the slice's length.  A slice whose positions are all
+  // uniform in offset and value reads neither ids nor values — its 8 offsets and 8 values
+  // come with its metadata, and its gathers are its only loads.  The same values in the
+  // same order: bitwise the same sums.
+  const double *dval;
+  const uint16_t *dvmeta;
 };
 constexpr int CB_INT32 = (int)0x80000000;
 // the 16-bit id engine needs ~98 registers unconstrained (2 blocks of 256 per SM); its

@@ -315,10 +315,13 @@ pcg_status build_d16(pcg_matrix *A, cudaStream_t st) {
 // entries per row: position t of slice s is uniform when every real entry there has
 // the same col - row = d, and every padding lane's row + d lies in [0, n_cols) (its
 // value is 0: fma(0, p[row + d], s) == s, as with the stored padding column).
+// Also the value-uniform positions and the slice length (SellView::dval / dvmeta): the 32
+// stored values at position t (padding zeros included) bitwise equal (vals = 0: none).
 __global__ void dia_build_kernel(int64_t n, int64_t n_cols, int64_t n_slices, const int *__restrict__ rp,
                                  const int64_t *__restrict__ slice_ptr, const int *__restrict__ scol,
-                                 int *__restrict__ doff, uint8_t *__restrict__ dmask,
-                                 unsigned long long *__restrict__ n_pos) {
+                                 const double *__restrict__ sval, int vals, int *__restrict__ doff,
+                                 uint8_t *__restrict__ dmask, double *__restrict__ dval,
+                                 uint16_t *__restrict__ dvmeta, unsigned long long *__restrict__ n_pos) {
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= n_slices) return;
@@ -326,9 +329,15 @@ __global__ void dia_build_kernel(int64_t n, int64_t n_cols, int64_t n_slices, co
   const int64_t base = slice_ptr[s];
   const int len = (int)((slice_ptr[s + 1] - base) >> 5);
   const int rl = row < n ? rp[row + 1] - rp[row] : 0;
-  unsigned mask = 0;
+  unsigned mask = 0, vmask = 0;
   for (int t = 0; t < len && t < 8; t++) {
     const int64_t e = base + (int64_t)t * 32 + lane;
+    if (vals) {
+      const unsigned long long vb = (unsigned long long)__double_as_longlong(sval[e]);
+      const unsigned long long v0 = __shfl_sync(0xffffffffu, vb, 0);
+      if (__all_sync(0xffffffffu, vb == v0)) vmask |= 1u << t;
+      if (lane == 0) dval[s * 8 + t] = __longlong_as_double((long long)v0);
+    }
     const bool real = t < rl;
     const long long off = (long long)scol[e] - row;
     long long lo = real ? off : LLONG_MAX, hi = real ? off : LLONG_MIN;
@@ -348,7 +357,10 @@ __global__ void dia_build_kernel(int64_t n, int64_t n_cols, int64_t n_slices, co
   if (lane == 0) {
     dmask[s] = (uint8_t)mask;
     atomicAdd(n_pos, (unsigned long long)__popc(mask));
-    if (len <= 8 && mask == (1u << len) - 1u) atomicAdd(n_pos + 1, 1ull);  // one-round-trip slice
+    const unsigned full = (1u << len) - 1u;
+    if (len <= 8 && mask == full) atomicAdd(n_pos + 1, 1ull);  // one-round-trip slice
+    dvmeta[s] = (uint16_t)(vmask | (unsigned)min(len, 15) << 8);
+    if (len <= 8 && (mask & vmask) == full) atomicAdd(n_pos + 2, 1ull);  // ... without a value stream
   }
 }
 
@@ -358,19 +370,27 @@ pcg_status build_dia(pcg_matrix *A, cudaStream_t st) {
   PCG_CUDA(cudaMalloc(&A->d_sdoff, sizeof(int) * 8 * (size_t)A->n_slices));
   PCG_CUDA(cudaMalloc(&A->d_sdmask, (size_t)A->n_slices));
   PCG_CUDA(cudaMemsetAsync(A->d_sdoff, 0, sizeof(int) * 8 * (size_t)A->n_slices, st));
+  const char *ev = getenv("PCG_DIA_VAL");  // PCG_DIA_VAL=0: values read from the stream at every position
+  const int vals = !(ev && atoi(ev) == 0);
+  PCG_CUDA(cudaMalloc(&A->d_sdval, sizeof(double) * 8 * (size_t)A->n_slices));
+  PCG_CUDA(cudaMalloc(&A->d_sdvmeta, sizeof(uint16_t) * (size_t)A->n_slices));
+  PCG_CUDA(cudaMemsetAsync(A->d_sdval, 0, sizeof(double) * 8 * (size_t)A->n_slices, st));
   unsigned long long *d_n;
-  PCG_CUDA(cudaMalloc(&d_n, 2 * sizeof(unsigned long long)));
-  PCG_CUDA(cudaMemsetAsync(d_n, 0, 2 * sizeof(unsigned long long), st));
+  PCG_CUDA(cudaMalloc(&d_n, 3 * sizeof(unsigned long long)));
+  PCG_CUDA(cudaMemsetAsync(d_n, 0, 3 * sizeof(unsigned long long), st));
   dia_build_kernel<<<(unsigned)((A->n_slices * 32 + 255) / 256), 256, 0, st>>>(
-      A->n, A->n + A->n_ghost, A->n_slices, A->d_row_ptr, A->d_slice_ptr, A->d_scol, A->d_sdoff, A->d_sdmask, d_n);
+      A->n, A->n + A->n_ghost, A->n_slices, A->d_row_ptr, A->d_slice_ptr, A->d_scol, A->d_sval, vals,
+      A->d_sdoff, A->d_sdmask, A->d_sdval, A->d_sdvmeta, d_n);
   count_launch();
-  unsigned long long np[2] = {0, 0};
+  unsigned long long np[3] = {0, 0, 0};
   PCG_CUDA(cudaMemcpyAsync(np, d_n, sizeof(np), cudaMemcpyDeviceToHost, st));
   PCG_CUDA(cudaStreamSynchronize(st));
   cudaFree(d_n);
   A->dia_positions = (int64_t)np[0];
   A->dia_slices = (int64_t)np[1];
+  A->dval_slices = (int64_t)np[2];
   A->device_bytes += 33.0 * (double)A->n_slices;
+  A->device_bytes += 66.0 * (double)A->n_slices;
   return PCG_OK;
 }
 
@@ -383,6 +403,14 @@ void free_sell(pcg_matrix *A) {
     A->d_sdmask = nullptr;
     A->dia_positions = 0;
     A->dia_slices = 0;
+  }
+  if (A->d_sdval) {
+    cudaFree(A->d_sdval);
+    cudaFree(A->d_sdvmeta);
+    A->device_bytes -= 66.0 * (double)A->n_slices;
+    A->d_sdval = nullptr;
+    A->d_sdvmeta = nullptr;
+    A->dval_slices = 0;
   }
   if (A->d_wdesc) cudaFree(A->d_wdesc);
   if (A->d_wlidx) cudaFree(A->d_wlidx);
@@ -881,5 +909,6 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->short_rows = A->short_rows ? 1 : 0;
   o->dia_positions = A->dia_positions;
   o->dia_slices = (int32_t)std::min<int64_t>(A->dia_slices, INT32_MAX);
+  o->dval_slices = A->dval_slices;
   return PCG_OK;
 }

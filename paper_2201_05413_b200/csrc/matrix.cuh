@@ -175,9 +175,13 @@ struct pcg_matrix {
   uint8_t *d_sdmask = nullptr;
   int64_t dia_positions = 0;  // positions without ids, over all slices
   int64_t dia_slices = 0;     // slices made only of such positions (one dependent round trip)
+  // value-uniform positions of those slices (common.cuh SellView::dval / dvmeta)
+  double *d_sdval = nullptr;
+  uint16_t *d_sdvmeta = nullptr;
+  int64_t dval_slices = 0;    // one-trip slices whose values are all per-position uniform (no value stream)
   pcgb::SellView sell() const {
     return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0, d_sdcol, d_scbase, 0,
-            d_sdoff, d_sdmask};
+            d_sdoff, d_sdmask, d_sdval, d_sdvmeta};
   }
 };
 

@@ -148,7 +148,8 @@ __device__ __forceinline__ void sell_rows_short(const SellView &A, Gather gather
 // before any of its loads return and issues values and gathers together: ONE dependent
 // round trip instead of two; other slices read their stored ids as sell_rows_short (a
 // per-position choice there cost 10 registers for a few bytes).  The same columns as
-// sell_rows_short (bitwise the same sums).
+// sell_rows_short (bitwise the same sums).  A one-trip slice whose values are uniform per
+// position as well (SellView::dval) takes them from lanes 0-7 and reads no value stream.
 template <class Gather, class Epi>
 __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, Epi epi) {
   const int lane = threadIdx.x & 31;
@@ -158,50 +159,66 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
   // per-slice arrays, and the offsets are relative to the absolute row
   const uint8_t *dmask = A.dmask + (A.row0 >> 5);
   const int *doff = A.doff + (A.row0 >> 5) * 8;
+  const uint16_t *dvmeta = A.dvmeta + (A.row0 >> 5);
+  const double *dval = A.dval + (A.row0 >> 5) * 8;
   // Each warp takes DIA_RUN consecutive slices per grid-stride step: slices that need two
   // round trips recur with the row-line period of a lattice (Cube 3: 2 of every 16) and a
   // plain grid stride (a multiple of 16 warps) would hand them all to the same warps
   constexpr int RUN = PCG_DIA_RUN;
   auto next_of = [&](int64_t x) { return (x + 1) % RUN != 0 ? x + 1 : x + 1 + (nw - 1) * RUN; };
-  int64_t s = w0 * RUN, base = 0, next = 0;
-  unsigned mask = 0;
-  int offl = 0;
-  if (s < A.n_slices) {
-    base = A.slice_ptr[s];
-    next = A.slice_ptr[s + 1];
-    mask = dmask[s];
-    if (lane < 8) offl = doff[s * 8 + lane];
-  }
-  for (; s < A.n_slices; s = next_of(s)) {
-    const int len = (int)((next - base) >> 5);  // <= 8 (host-checked)
-    const double *vp = A.val + base + lane;
+  // per slice: its first entry; offset mask in bits 0-7, value mask in bits 8-15, length
+  // in bits 16-19; lanes 0-7 hold the position offsets and the uniform values
+  struct Meta {
+    int64_t base;
+    unsigned mask;
+    int off;
+    double val;
+  };
+  auto meta = [&](int64_t x) {
+    Meta m{0, 0u, 0, 0.0};
+    if (x < A.n_slices) {
+      m.base = A.slice_ptr[x];
+      m.mask = (unsigned)dmask[x] | (unsigned)dvmeta[x] << 8;
+      if (lane < 8) {
+        m.off = doff[x * 8 + lane];
+        m.val = dval[x * 8 + lane];
+      }
+    }
+    return m;
+  };
+  auto len_of = [](const Meta &m) { return (int)(m.mask >> 16 & 15u); };
+  int64_t s = w0 * RUN;
+  // the next slice's metadata is fetched while the current slice is in flight (indexed
+  // by slice: no dependent load)
+  Meta m0 = meta(s);
+  while (s < A.n_slices) {
+    const int64_t s2 = next_of(s);
+    const int len = len_of(m0);  // <= 8 (host-checked)
+    const double *vp = A.val + m0.base + lane;
     const int64_t rowv = s * 32 + lane;         // row within the view (epilogue)
     const int row = (int)(A.row0 + rowv);       // local row (columns)
     const unsigned full = (1u << len) - 1u;
-    const int64_t s2 = next_of(s);
-    int64_t base2 = 0, next2 = 0;
-    unsigned mask2 = 0;
-    int offl2 = 0;
+    Meta n1;
     double a[8], g[8];
     double sum = 0.0;
-    if ((mask & full) == full) {  // every position uniform: values and gathers in one round trip
+    if ((m0.mask & full) == full) {  // every position uniform: values and gathers in one round trip
       int j[8];
 #pragma unroll
-      for (int u = 0; u < 8; u++) j[u] = row + __shfl_sync(0xffffffffu, offl, u);
+      for (int u = 0; u < 8; u++) j[u] = row + __shfl_sync(0xffffffffu, m0.off, u);
+      if ((m0.mask >> 8 & full) == full) {  // ... and every value too: no value stream at all
 #pragma unroll
-      for (int u = 0; u < 8; u++)
-        if (u < len) a[u] = ld_stream(vp + (size_t)u * 32);
+        for (int u = 0; u < 8; u++) a[u] = __shfl_sync(0xffffffffu, m0.val, u);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (u < len) a[u] = ld_stream(vp + (size_t)u * 32);
+      }
 #pragma unroll
       for (int u = 0; u < 8; u++)
         if (u < len) g[u] = gather(j[u]);
-      if (s2 < A.n_slices) {
-        base2 = A.slice_ptr[s2];
-        next2 = A.slice_ptr[s2 + 1];
-        mask2 = dmask[s2];
-        if (lane < 8) offl2 = doff[s2 * 8 + lane];
-      }
+      n1 = meta(s2);
     } else {  // the stored ids (issued first), then the values
-      const int *cp = A.col + base + lane;
+      const int *cp = A.col + m0.base + lane;
       int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
       for (int u = 0; u < 8; u++)
@@ -209,12 +226,7 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
 #pragma unroll
       for (int u = 0; u < 8; u++)
         if (u < len) a[u] = ld_stream(vp + (size_t)u * 32);
-      if (s2 < A.n_slices) {
-        base2 = A.slice_ptr[s2];
-        next2 = A.slice_ptr[s2 + 1];
-        mask2 = dmask[s2];
-        if (lane < 8) offl2 = doff[s2 * 8 + lane];
-      }
+      n1 = meta(s2);
       cols_ready(j, A.zero);
 #pragma unroll
       for (int u = 0; u < 8; u++)
@@ -224,10 +236,8 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
     for (int u = 0; u < 8; u++)
       if (u < len) sum = __fma_rn(a[u], g[u], sum);
     if (rowv < A.n) epi(rowv, sum);
-    base = base2;
-    next = next2;
-    mask = mask2;
-    offl = offl2;
+    m0 = n1;
+    s = s2;
   }
 }
 

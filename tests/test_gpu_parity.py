@@ -382,14 +382,34 @@ def _banded_mix(n, seed):
     return _csr(D)
 
 
-@pytest.mark.parametrize("name,c", [("C1", None), ("C5", 32), ("C4", 16), ("mix", 900)])
+def _grid_values(m, seed):
+    """5-point Laplacian on an m x m grid (m > 32: slices inside a grid line are one-trip
+    and value-uniform) with every 37th x-coupling scaled by 0.75 (symmetric, diagonally
+    dominant): one-trip slices whose values are not uniform, and boundary slices that
+    are not one-trip"""
+    n = m * m
+    M = np.zeros((n, n))
+    for i in range(n):
+        x, y = i % m, i // m
+        for dx, dy in ((-1, 0), (1, 0), (0, -1), (0, 1)):
+            if 0 <= x + dx < m and 0 <= y + dy < m:
+                M[i, i + dx + m * dy] = -1.0
+        M[i, i] = 4.0
+    for i in range(0, n - 1, 37):
+        if (i + 1) % m:
+            M[i, i + 1] = M[i + 1, i] = -0.75
+    return _csr(M)
+
+
+@pytest.mark.parametrize("name,c", [("C1", None), ("C5", 32), ("C5", 64), ("C4", 16), ("mix", 900), ("mixv", 70)])
 def test_uniform_offset_positions_are_bitwise_the_id_form(pcg, monkeypatch, name, c):
-    """The one-chunk engine's id-free uniform-offset positions (pcg.h dia_positions):
-    the same columns, so the SpMV is bitwise the id form (PCG_DIA=0) and the chunked
-    engine (PCG_SHORT=0); the graph-loop solve meets the oracle bars; a pattern mixing
-    uniform and non-uniform slices takes both paths of the engine."""
-    if name == "mix":
-        A = _banded_mix(c, 5)
+    """The one-chunk engine's id-free uniform-offset positions (pcg.h dia_positions)
+    and value-uniform slices (pcg.h dval_slices): the same columns and values, so the
+    SpMV is bitwise the id form (PCG_DIA=0), the value-stream form (PCG_DIA_VAL=0) and
+    the chunked engine (PCG_SHORT=0); the graph-loop solve meets the oracle bars; a
+    pattern mixing uniform and non-uniform slices takes every path of the engine."""
+    if name in ("mix", "mixv"):
+        A = _banded_mix(c, 5) if name == "mix" else _grid_values(c, 5)
         b = np.random.default_rng(6).standard_normal(A.n)
         tol = 1e-10
     else:
@@ -398,21 +418,34 @@ def test_uniform_offset_positions_are_bitwise_the_id_form(pcg, monkeypatch, name
         tol = O.configs()[name]["tol"]
     monkeypatch.setenv("PCG_PERSIST", "0")
     hs = {}
-    for key, env in (("dia", {}), ("ids", {"PCG_DIA": "0"}), ("chunked", {"PCG_SHORT": "0"})):
-        for k in ("PCG_DIA", "PCG_SHORT"):
+    knobs = ("PCG_DIA", "PCG_SHORT", "PCG_DIA_VAL")
+    for key, env in (("dia", {}), ("ids", {"PCG_DIA": "0"}), ("chunked", {"PCG_SHORT": "0"}),
+                     ("novals", {"PCG_DIA_VAL": "0"})):
+        for k in knobs:
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         hs[key] = _matrix(pcg, A, "sell")
-    for k in ("PCG_DIA", "PCG_SHORT"):
+    for k in knobs:
         monkeypatch.delenv(k, raising=False)
     st = hs["dia"].stats()
     n_slices = (A.n + 31) // 32
     assert st["short_rows"] == 1 and 0 < st["dia_positions"] <= 8 * n_slices, st
     assert hs["ids"].stats()["dia_positions"] == 0
+    # lattice stencils and the constant band: value-uniform one-trip slices exist; the
+    # scaled couplings of mixv leave some one-trip slices reading their values
+    # (below c = 64 every 32-row slice of a lattice meets a boundary row: no one-trip slice)
+    assert st["dval_slices"] <= st["dia_slices"], st
+    if name == "mixv" or (name == "C5" and c >= 64):
+        assert st["dval_slices"] > 0, st
+    if name == "mixv":
+        assert st["dval_slices"] < st["dia_slices"], st
+    assert hs["novals"].stats()["dval_slices"] == 0
+    assert hs["novals"].stats()["dia_slices"] == st["dia_slices"]
     x = np.random.default_rng(12).standard_normal(A.n)
     ys = {k: M.spmv(_dev(x)).cpu().numpy() for k, M in hs.items()}
-    assert np.array_equal(ys["dia"], ys["ids"]) and np.array_equal(ys["dia"], ys["chunked"])
+    for k in ("ids", "chunked", "novals"):
+        assert np.array_equal(ys["dia"], ys[k]), k
     r = O.pcg(A, b, tol=tol)
     xs, info = hs["dia"].solve(_dev(b), tol=tol)
     assert info["status"] == 0 and info["relres_true"] <= tol
