@@ -580,13 +580,17 @@ def main():
             # their 8 per-position values, 64 B + a mask, with their offsets)
             dv = stats.get("dval_slices", 0)
             vals = 8.0 * se * (1.0 - dv / max(ns, 1))
-            meta = 107.0  # per slice: its offset 8, offset mask 1, 8 offsets 32, length + value mask 2, 8 values 64
-            fb = vals + ids + meta * ns + 8.0 + 16.0 * n
+            # per slice its pattern index (1 B); a slice without a shared pattern also its
+            # offset 8, offset mask 1, length + value mask 2, 8 offsets 32 and 8 values 64
+            pat = stats.get("pat_slices", 0)
+            meta = 1.0 * ns + 107.0 * (ns - pat)
+            fb = vals + ids + meta + 8.0 + 16.0 * n
             k1b = kern[1]
             roof["format_bytes"] = {"kernel": "k1b_kernel", "bytes_per_launch": fb,
                                     "achieved_GBps": fb / k1b["us_per_launch"] / 1e3,
                                     "frac_vs_copy_peak": fb / k1b["us_per_launch"] / 1e3 / hbm,
                                     "one_trip_slices": stats["dia_slices"], "value_free_slices": dv,
+                                    "pattern_slices": pat, "patterns": stats.get("npat", 0),
                                     "slices": ns,
                                     "note": "frac > 1 by the section 8(d) bytes (12 per entry, CSR ids) is "
                                             "the format moving fewer bytes than that ideal: no column ids in "
@@ -666,7 +670,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(workload_config(args.config, c, n, nnz, world), iterations=iters,
                            format={1: "csr", 2: "sell", 3: "sell_tma", 4: "sell_sigma"}[stats["format"]], setup_s=round(t_setup, 3),
-                           d16_slices=A.stats()["d16_slices"], dval_slices=A.stats()["dval_slices"], spmm_windowed=A.stats()["spmm_windowed"],
+                           d16_slices=A.stats()["d16_slices"], dval_slices=A.stats()["dval_slices"],
+                           pat_slices=A.stats()["pat_slices"], spmm_windowed=A.stats()["spmm_windowed"],
                            relres_true=max(i["relres_true"] for i in infos[-1]), k_rhs=kcols,
                            solver={"pcg": "jacobi-pcg", "pipelined": "pipelined jacobi-pcg (N3)",
                                    "block": "block cg, jacobi (N3)"}[args.solver],

@@ -134,6 +134,11 @@ typedef struct {
                                 position) is read with the offsets and the value stream is skipped
                                 (value sharing, as CSR-VI); same values, so the same sums;
                                 PCG_DIA_VAL=0 at csr_create: off */
+  int64_t pat_slices;        /* value-free slices that read their offsets and values from a table of
+                                the matrix's distinct such patterns, staged in shared memory per
+                                block (no per-slice metadata beyond a pattern index); PCG_DIA_PAT=0
+                                at csr_create: off */
+  int32_t npat;              /* distinct patterns in that table (<= 32) */
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */

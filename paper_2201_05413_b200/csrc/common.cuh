@@ -103,6 +103,7 @@ struct CsrView {
   int zero;             // run-time 0, opaque to the compiler (rows.cuh cols_ready)
 };
 
+struct DiaPat;  // value-free slice pattern (below)
 struct SellView {
   int64_t n;
   int64_t n_slices;        // ceil(n/32)
@@ -135,6 +136,20 @@ struct SellView {
   // same order: bitwise the same sums.
   const double *dval;
   const uint16_t *dvmeta;
+  // value-free slices grouped by pattern (null dpat: none): dpat[s] indexes ptab, the
+  // distinct (offsets, values) of such slices (a lattice stencil has a handful: interior,
+  // faces), staged in shared memory once per block; DIA_NOPAT: the slice reads its own.
+  // The pattern's offsets and values are the slice's own (checked when built).
+  const uint8_t *dpat;
+  const DiaPat *ptab;
+  const int *plen;  // per pattern: the slice length
+  int npat;
+};
+constexpr int DIA_MAXPAT = 32;
+constexpr uint8_t DIA_NOPAT = 0xFF;
+struct __align__(16) DiaPat {
+  int off[8];
+  double val[8];
 };
 constexpr int CB_INT32 = (int)0x80000000;
 // the 16-bit id engine needs ~98 registers unconstrained (2 blocks of 256 per SM); its

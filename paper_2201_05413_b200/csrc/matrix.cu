@@ -364,6 +364,132 @@ __global__ void dia_build_kernel(int64_t n, int64_t n_cols, int64_t n_slices, co
   }
 }
 
+// Value-free slice patterns: a 64-bit key per value-free one-trip slice (its length, 8
+// offsets and 8 value bit patterns; ~0 for the other slices), the host picks the first
+// DIA_MAXPAT distinct keys, dia_pat_fill_kernel copies each one's representative and
+// dia_pat_assign_kernel gives every slice whose metadata EQUALS a table entry its index
+// (a key collision only costs the pattern, never a wrong sum).
+__device__ __forceinline__ unsigned long long pat_mix(unsigned long long h, unsigned long long v) {
+  h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+  h ^= h >> 31;
+  h *= 0xBF58476D1CE4E5B9ull;
+  return h ^ (h >> 29);
+}
+__device__ __forceinline__ bool value_free(uint8_t dm, uint16_t vm) {
+  const int len = vm >> 8 & 15;
+  const unsigned full = (1u << len) - 1u;
+  return len <= 8 && (dm & full) == full && ((unsigned)vm & full) == full;
+}
+__global__ void dia_key_kernel(int64_t n_slices, const int *__restrict__ doff, const double *__restrict__ dval,
+                               const uint8_t *__restrict__ dmask, const uint16_t *__restrict__ dvmeta,
+                               unsigned long long *__restrict__ key) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_slices; s += (int64_t)gridDim.x * blockDim.x) {
+    if (!value_free(dmask[s], dvmeta[s])) {
+      key[s] = ~0ull;
+      continue;
+    }
+    unsigned long long h = pat_mix(0, dvmeta[s] >> 8);
+    for (int t = 0; t < 8; t++) {
+      h = pat_mix(h, (unsigned long long)(unsigned)doff[s * 8 + t]);
+      h = pat_mix(h, (unsigned long long)__double_as_longlong(dval[s * 8 + t]));
+    }
+    key[s] = h == ~0ull ? 0 : h;
+  }
+}
+__global__ void dia_pat_fill_kernel(int npat, const int64_t *__restrict__ rep, const int *__restrict__ doff,
+                                    const double *__restrict__ dval, const uint16_t *__restrict__ dvmeta,
+                                    DiaPat *__restrict__ tab, int *__restrict__ plen) {
+  const int p = blockIdx.x, t = threadIdx.x;
+  if (p >= npat || t >= 8) return;
+  if (t == 0) plen[p] = dvmeta[rep[p]] >> 8 & 15;
+  tab[p].off[t] = doff[rep[p] * 8 + t];
+  tab[p].val[t] = dval[rep[p] * 8 + t];
+}
+__global__ void dia_pat_assign_kernel(int64_t n_slices, int npat, const unsigned long long *__restrict__ key,
+                                      const unsigned long long *__restrict__ pkey, const int64_t *__restrict__ rep,
+                                      const int *__restrict__ doff, const double *__restrict__ dval,
+                                      const uint16_t *__restrict__ dvmeta, uint8_t *__restrict__ dpat,
+                                      unsigned long long *__restrict__ n_assigned) {
+  unsigned long long cnt = 0;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_slices; s += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t id = DIA_NOPAT;
+    const unsigned long long k = key[s];
+    if (k != ~0ull)
+      for (int p = 0; p < npat; p++)
+        if (pkey[p] == k) {
+          const int64_t r = rep[p];
+          bool eq = (dvmeta[s] >> 8) == (dvmeta[r] >> 8);
+          for (int t = 0; t < 8 && eq; t++)
+            eq = doff[s * 8 + t] == doff[r * 8 + t] &&
+                 __double_as_longlong(dval[s * 8 + t]) == __double_as_longlong(dval[r * 8 + t]);
+          if (eq) id = (uint8_t)p;
+          break;
+        }
+    dpat[s] = id;
+    cnt += id != DIA_NOPAT;
+  }
+  if (cnt) atomicAdd(n_assigned, cnt);
+}
+
+static pcg_status build_dia_patterns(pcg_matrix *A, cudaStream_t st) {
+  const char *e = getenv("PCG_DIA_PAT");  // PCG_DIA_PAT=0: every value-free slice reads its own metadata
+  if ((e && atoi(e) == 0) || A->dval_slices == 0) return PCG_OK;
+  const int64_t ns = A->n_slices;
+  unsigned long long *d_key = nullptr;
+  PCG_CUDA(cudaMalloc(&d_key, sizeof(unsigned long long) * (size_t)ns));
+  const unsigned g = (unsigned)std::min<int64_t>((ns + 255) / 256, 148 * 16);
+  dia_key_kernel<<<g, 256, 0, st>>>(ns, A->d_sdoff, A->d_sdval, A->d_sdmask, A->d_sdvmeta, d_key);
+  count_launch();
+  std::vector<unsigned long long> key((size_t)ns);
+  PCG_CUDA(cudaMemcpyAsync(key.data(), d_key, sizeof(unsigned long long) * (size_t)ns, cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  std::vector<unsigned long long> pkey;
+  std::vector<int64_t> rep;
+  unsigned long long last = ~0ull;
+  for (int64_t s = 0; s < ns; s++) {  // first DIA_MAXPAT distinct keys, in slice order
+    const unsigned long long k = key[(size_t)s];
+    if (k == ~0ull || k == last) continue;
+    last = k;
+    if (std::find(pkey.begin(), pkey.end(), k) != pkey.end()) continue;
+    if ((int)pkey.size() == DIA_MAXPAT) continue;
+    pkey.push_back(k);
+    rep.push_back(s);
+  }
+  const int np = (int)pkey.size();
+  if (np == 0) {
+    cudaFree(d_key);
+    return PCG_OK;
+  }
+  unsigned long long *d_pkey = nullptr, *d_cnt = nullptr;
+  int64_t *d_rep = nullptr;
+  PCG_CUDA(cudaMalloc(&d_pkey, sizeof(unsigned long long) * np));
+  PCG_CUDA(cudaMalloc(&d_rep, sizeof(int64_t) * np));
+  PCG_CUDA(cudaMalloc(&d_cnt, sizeof(unsigned long long)));
+  PCG_CUDA(cudaMalloc(&A->d_ptab, sizeof(DiaPat) * np));
+  PCG_CUDA(cudaMalloc(&A->d_plen, sizeof(int) * np));
+  PCG_CUDA(cudaMalloc(&A->d_sdpat, (size_t)ns));
+  PCG_CUDA(cudaMemcpyAsync(d_pkey, pkey.data(), sizeof(unsigned long long) * np, cudaMemcpyHostToDevice, st));
+  PCG_CUDA(cudaMemcpyAsync(d_rep, rep.data(), sizeof(int64_t) * np, cudaMemcpyHostToDevice, st));
+  PCG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), st));
+  dia_pat_fill_kernel<<<np, 32, 0, st>>>(np, d_rep, A->d_sdoff, A->d_sdval, A->d_sdvmeta,
+                                      A->d_ptab, A->d_plen);
+  count_launch();
+  dia_pat_assign_kernel<<<g, 256, 0, st>>>(ns, np, d_key, d_pkey, d_rep, A->d_sdoff, A->d_sdval, A->d_sdvmeta,
+                                           A->d_sdpat, d_cnt);
+  count_launch();
+  unsigned long long cnt = 0;
+  PCG_CUDA(cudaMemcpyAsync(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+  PCG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_key);
+  cudaFree(d_pkey);
+  cudaFree(d_rep);
+  cudaFree(d_cnt);
+  A->npat = np;
+  A->pat_slices = (int64_t)cnt;
+  A->device_bytes += (double)ns + sizeof(DiaPat) * (double)np;
+  return PCG_OK;
+}
+
 pcg_status build_dia(pcg_matrix *A, cudaStream_t st) {
   const char *e = getenv("PCG_DIA");  // PCG_DIA=0: ids at every position
   if (A->d_sdoff || !A->d_slice_ptr || A->n_slices == 0 || !A->short_rows || (e && atoi(e) == 0)) return PCG_OK;
@@ -391,6 +517,7 @@ pcg_status build_dia(pcg_matrix *A, cudaStream_t st) {
   A->dval_slices = (int64_t)np[2];
   A->device_bytes += 33.0 * (double)A->n_slices;
   A->device_bytes += 66.0 * (double)A->n_slices;
+  PCG_TRY(build_dia_patterns(A, st));
   return PCG_OK;
 }
 
@@ -410,6 +537,17 @@ void free_sell(pcg_matrix *A) {
     A->device_bytes -= 66.0 * (double)A->n_slices;
     A->d_sdval = nullptr;
     A->d_sdvmeta = nullptr;
+  }
+  if (A->d_sdpat) {
+    cudaFree(A->d_sdpat);
+    cudaFree(A->d_ptab);
+    cudaFree(A->d_plen);
+    A->d_plen = nullptr;
+    A->device_bytes -= (double)A->n_slices + sizeof(DiaPat) * (double)A->npat;
+    A->d_sdpat = nullptr;
+    A->d_ptab = nullptr;
+    A->npat = 0;
+    A->pat_slices = 0;
     A->dval_slices = 0;
   }
   if (A->d_wdesc) cudaFree(A->d_wdesc);
@@ -910,5 +1048,7 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->dia_positions = A->dia_positions;
   o->dia_slices = (int32_t)std::min<int64_t>(A->dia_slices, INT32_MAX);
   o->dval_slices = A->dval_slices;
+  o->npat = A->npat;
+  o->pat_slices = A->pat_slices;
   return PCG_OK;
 }

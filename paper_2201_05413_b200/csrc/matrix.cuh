@@ -179,9 +179,15 @@ struct pcg_matrix {
   double *d_sdval = nullptr;
   uint16_t *d_sdvmeta = nullptr;
   int64_t dval_slices = 0;    // one-trip slices whose values are all per-position uniform (no value stream)
+  // their patterns (common.cuh SellView::dpat / ptab)
+  uint8_t *d_sdpat = nullptr;
+  pcgb::DiaPat *d_ptab = nullptr;
+  int *d_plen = nullptr;
+  int npat = 0;
+  int64_t pat_slices = 0;     // value-free slices that read a shared pattern
   pcgb::SellView sell() const {
     return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0, d_sdcol, d_scbase, 0,
-            d_sdoff, d_sdmask, d_sdval, d_sdvmeta};
+            d_sdoff, d_sdmask, d_sdval, d_sdvmeta, d_sdpat, d_ptab, d_plen, npat};
   }
 };
 

@@ -25,6 +25,9 @@ __device__ __forceinline__ void cols_ready(int (&j)[N], int zero) {
   for (int u = 0; u < N; u++) j[u] |= x;
 }
 
+#ifndef PCG_DIA_SKIPMETA  // pattern slices skip their per-lane offsets/values (waits on the index)
+#define PCG_DIA_SKIPMETA 1
+#endif
 #ifndef PCG_DIA_RUN  // consecutive slices per warp and grid-stride step of the uniform-offset engine
 #define PCG_DIA_RUN 8
 #endif
@@ -149,7 +152,9 @@ __device__ __forceinline__ void sell_rows_short(const SellView &A, Gather gather
 // round trip instead of two; other slices read their stored ids as sell_rows_short (a
 // per-position choice there cost 10 registers for a few bytes).  The same columns as
 // sell_rows_short (bitwise the same sums).  A one-trip slice whose values are uniform per
-// position as well (SellView::dval) takes them from lanes 0-7 and reads no value stream.
+// position as well (SellView::dval) takes them from lanes 0-7 and reads no value stream;
+// if its offsets and values are one of the matrix's shared patterns (SellView::dpat) it
+// reads them from shared memory instead (six vector loads instead of 24 shuffles).
 template <class Gather, class Epi>
 __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, Epi epi) {
   const int lane = threadIdx.x & 31;
@@ -161,13 +166,25 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
   const int *doff = A.doff + (A.row0 >> 5) * 8;
   const uint16_t *dvmeta = A.dvmeta + (A.row0 >> 5);
   const double *dval = A.dval + (A.row0 >> 5) * 8;
+  const uint8_t *dpat = A.dpat ? A.dpat + (A.row0 >> 5) : nullptr;
+  // the matrix's value-free patterns, staged once per block (every thread of the block
+  // runs this engine: the barrier is block-uniform)
+  __shared__ DiaPat s_pat[DIA_MAXPAT];
+  __shared__ int s_plen[DIA_MAXPAT];
+  if (A.npat > 0) {
+    for (int t = threadIdx.x; t < A.npat * 12; t += blockDim.x)
+      reinterpret_cast<double *>(s_pat)[t] = reinterpret_cast<const double *>(A.ptab)[t];
+    for (int t = threadIdx.x; t < A.npat; t += blockDim.x) s_plen[t] = A.plen[t];
+    __syncthreads();
+  }
   // Each warp takes DIA_RUN consecutive slices per grid-stride step: slices that need two
   // round trips recur with the row-line period of a lattice (Cube 3: 2 of every 16) and a
   // plain grid stride (a multiple of 16 warps) would hand them all to the same warps
   constexpr int RUN = PCG_DIA_RUN;
   auto next_of = [&](int64_t x) { return (x + 1) % RUN != 0 ? x + 1 : x + 1 + (nw - 1) * RUN; };
   // per slice: its first entry; offset mask in bits 0-7, value mask in bits 8-15, length
-  // in bits 16-19; lanes 0-7 hold the position offsets and the uniform values
+  // in bits 16-19, pattern index in bits 24-31; lanes 0-7 hold the position offsets and
+  // the uniform values
   struct Meta {
     int64_t base;
     unsigned mask;
@@ -177,11 +194,16 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
   auto meta = [&](int64_t x) {
     Meta m{0, 0u, 0, 0.0};
     if (x < A.n_slices) {
-      m.base = A.slice_ptr[x];
-      m.mask = (unsigned)dmask[x] | (unsigned)dvmeta[x] << 8;
-      if (lane < 8) {
-        m.off = doff[x * 8 + lane];
-        m.val = dval[x * 8 + lane];
+      const unsigned pid = dpat ? dpat[x] : DIA_NOPAT;
+      if (PCG_DIA_SKIPMETA && pid != DIA_NOPAT) {  // a pattern slice: its index is all it needs
+        m.mask = pid << 24 | (unsigned)s_plen[pid] << 16;
+      } else {
+        m.base = A.slice_ptr[x];
+        m.mask = (unsigned)dmask[x] | (unsigned)dvmeta[x] << 8 | pid << 24;
+        if (lane < 8) {
+          m.off = doff[x * 8 + lane];
+          m.val = dval[x * 8 + lane];
+        }
       }
     }
     return m;
@@ -201,7 +223,21 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
     Meta n1;
     double a[8], g[8];
     double sum = 0.0;
-    if ((m0.mask & full) == full) {  // every position uniform: values and gathers in one round trip
+    if ((m0.mask >> 24) != DIA_NOPAT) {  // value-free slice with a shared pattern: no shuffles
+      const DiaPat &P = s_pat[m0.mask >> 24];
+      const int4 o0 = *reinterpret_cast<const int4 *>(P.off), o1 = *reinterpret_cast<const int4 *>(P.off + 4);
+      const int j[8] = {row + o0.x, row + o0.y, row + o0.z, row + o0.w, row + o1.x, row + o1.y, row + o1.z, row + o1.w};
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (u < len) g[u] = gather(j[u]);
+      n1 = meta(s2);
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        const double2 v = *reinterpret_cast<const double2 *>(P.val + u);
+        a[u] = v.x;
+        a[u + 1] = v.y;
+      }
+    } else if ((m0.mask & full) == full) {  // every position uniform: values and gathers in one round trip
       int j[8];
 #pragma unroll
       for (int u = 0; u < 8; u++) j[u] = row + __shfl_sync(0xffffffffu, m0.off, u);

@@ -418,9 +418,9 @@ def test_uniform_offset_positions_are_bitwise_the_id_form(pcg, monkeypatch, name
         tol = O.configs()[name]["tol"]
     monkeypatch.setenv("PCG_PERSIST", "0")
     hs = {}
-    knobs = ("PCG_DIA", "PCG_SHORT", "PCG_DIA_VAL")
+    knobs = ("PCG_DIA", "PCG_SHORT", "PCG_DIA_VAL", "PCG_DIA_PAT")
     for key, env in (("dia", {}), ("ids", {"PCG_DIA": "0"}), ("chunked", {"PCG_SHORT": "0"}),
-                     ("novals", {"PCG_DIA_VAL": "0"})):
+                     ("novals", {"PCG_DIA_VAL": "0"}), ("nopat", {"PCG_DIA_PAT": "0"})):
         for k in knobs:
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
@@ -440,11 +440,16 @@ def test_uniform_offset_positions_are_bitwise_the_id_form(pcg, monkeypatch, name
         assert st["dval_slices"] > 0, st
     if name == "mixv":
         assert st["dval_slices"] < st["dia_slices"], st
-    assert hs["novals"].stats()["dval_slices"] == 0
+    # the value-free slices read a shared pattern (a lattice has a handful: interior, faces)
+    assert st["pat_slices"] <= st["dval_slices"] and st["npat"] <= 32, st
+    if st["dval_slices"] > 0:
+        assert st["pat_slices"] > 0 and st["npat"] > 0, st
+    assert hs["nopat"].stats()["pat_slices"] == 0 and hs["nopat"].stats()["dval_slices"] == st["dval_slices"]
+    assert hs["novals"].stats()["dval_slices"] == 0 and hs["novals"].stats()["pat_slices"] == 0
     assert hs["novals"].stats()["dia_slices"] == st["dia_slices"]
     x = np.random.default_rng(12).standard_normal(A.n)
     ys = {k: M.spmv(_dev(x)).cpu().numpy() for k, M in hs.items()}
-    for k in ("ids", "chunked", "novals"):
+    for k in ("ids", "chunked", "novals", "nopat"):
         assert np.array_equal(ys["dia"], ys[k]), k
     r = O.pcg(A, b, tol=tol)
     xs, info = hs["dia"].solve(_dev(b), tol=tol)
