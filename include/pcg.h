@@ -139,6 +139,10 @@ typedef struct {
                                 block (no per-slice metadata beyond a pattern index); PCG_DIA_PAT=0
                                 at csr_create: off */
   int32_t npat;              /* distinct patterns in that table (<= 32) */
+  int64_t aligned_slices;    /* value-free slices stored in the aligned form: positions = the union of
+                                the rows' column offsets, a row without an entry at a position adds
+                                0 * p[row + d] there (exact), so a lattice's grid-line ends need no ids
+                                or values either; PCG_DIA_ALIGN=0 at csr_create: off */
 } pcg_matrix_stats;
 
 /* ---------------------------------------------------------------- setup (§8(a) a1) */

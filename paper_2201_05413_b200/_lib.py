@@ -47,7 +47,8 @@ class MatrixStats(C.Structure):
                 ("spmv_us_sigma", C.c_double), ("sigma", C.c_int32), ("reorder", C.c_int32),
                 ("overlap_rows", C.c_int64), ("d16_slices", C.c_int64),
                 ("spmm_windowed", C.c_int32), ("short_rows", C.c_int32), ("dia_slices", C.c_int32),
-                ("dia_positions", C.c_int64), ("dval_slices", C.c_int64), ("pat_slices", C.c_int64), ("npat", C.c_int32)]
+                ("dia_positions", C.c_int64), ("dval_slices", C.c_int64), ("pat_slices", C.c_int64), ("npat", C.c_int32),
+                ("aligned_slices", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -136,6 +136,10 @@ struct SellView {
   // same order: bitwise the same sums.
   const double *dval;
   const uint16_t *dvmeta;
+  // aligned slices (dvmeta bit 12): the positions are the union of the rows' column
+  // offsets; bit l of dzmask[8 s + t] set when row l has no entry at position t (it adds
+  // 0 * p[row + d]: exact).  Null: not built.
+  const unsigned *dzmask;
   // value-free slices grouped by pattern (null dpat: none): dpat[s] indexes ptab, the
   // distinct (offsets, values) of such slices (a lattice stencil has a handful: interior,
   // faces), staged in shared memory once per block; DIA_NOPAT: the slice reads its own.

@@ -321,7 +321,8 @@ __global__ void dia_build_kernel(int64_t n, int64_t n_cols, int64_t n_slices, co
                                  const int64_t *__restrict__ slice_ptr, const int *__restrict__ scol,
                                  const double *__restrict__ sval, int vals, int *__restrict__ doff,
                                  uint8_t *__restrict__ dmask, double *__restrict__ dval,
-                                 uint16_t *__restrict__ dvmeta, unsigned long long *__restrict__ n_pos) {
+                                 uint16_t *__restrict__ dvmeta, unsigned *__restrict__ dzmask,
+                                 unsigned long long *__restrict__ n_pos) {
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= n_slices) return;
@@ -354,6 +355,54 @@ __global__ void dia_build_kernel(int64_t n, int64_t n_cols, int64_t n_slices, co
     if (ok) mask |= 1u << t;
     if (lane == 0) doff[s * 8 + t] = ok ? (int)lo : 0;
   }
+  const unsigned fl = (1u << len) - 1u;
+  if (vals && dzmask && len <= 8 && (mask & vmask) != fl) {
+    // Aligned form: the union of the rows' column offsets as the positions (ascending, so
+    // each row keeps its column order), a row without an entry at a position adds
+    // 0 * p[row + d] there (exact: the sum never is -0 and p[row + d] is in range).  Kept
+    // when every position's present values are bitwise equal (a value-free slice with
+    // a zero mask: a lattice's rows at the ends of grid lines).
+    int cur = 0, np = 0;
+    bool ok = true;
+    int aoff[8];
+    double aval[8];
+    unsigned azm[8];
+    for (int t = 0; t < 8 && ok; t++) {
+      const long long my = cur < rl ? (long long)scol[base + (int64_t)cur * 32 + lane] - row : LLONG_MAX;
+      long long d = my;
+      for (int o = 16; o > 0; o >>= 1) d = min(d, (long long)__shfl_xor_sync(0xffffffffu, d, o));
+      if (d == LLONG_MAX) break;  // every row consumed
+      const bool present = my == d;
+      const unsigned pres = __ballot_sync(0xffffffffu, present);
+      const unsigned long long vb =
+          present ? (unsigned long long)__double_as_longlong(sval[base + (int64_t)cur * 32 + lane]) : 0ull;
+      const unsigned long long v0 = __shfl_sync(0xffffffffu, vb, __ffs(pres) - 1);
+      const long long c = row + d;
+      ok = __all_sync(0xffffffffu, (present ? vb == v0 : (c >= 0 && c < n_cols))) && d >= INT_MIN && d <= INT_MAX;
+      aoff[t] = (int)d;
+      aval[t] = __longlong_as_double((long long)v0);
+      azm[t] = ~pres;
+      cur += present;
+      np = t + 1;
+    }
+    ok = ok && __all_sync(0xffffffffu, cur == rl) && np > 0;
+    if (ok) {
+      if (lane < 8) {
+        doff[s * 8 + lane] = lane < np ? aoff[lane] : 0;
+        dval[s * 8 + lane] = lane < np ? aval[lane] : 0.0;
+        dzmask[s * 8 + lane] = lane < np ? azm[lane] : 0u;
+      }
+      if (lane == 0) {
+        const unsigned f = (1u << np) - 1u;
+        dmask[s] = (uint8_t)f;
+        dvmeta[s] = (uint16_t)(f | (unsigned)np << 8 | 1u << 12);
+        atomicAdd(n_pos, (unsigned long long)np);
+        atomicAdd(n_pos + 1, 1ull);
+        atomicAdd(n_pos + 3, 1ull);
+      }
+      return;
+    }
+  }
   if (lane == 0) {
     dmask[s] = (uint8_t)mask;
     atomicAdd(n_pos, (unsigned long long)__popc(mask));
@@ -376,6 +425,7 @@ __device__ __forceinline__ unsigned long long pat_mix(unsigned long long h, unsi
   return h ^ (h >> 29);
 }
 __device__ __forceinline__ bool value_free(uint8_t dm, uint16_t vm) {
+  if (vm >> 12 & 1) return false;  // aligned slices keep their zero masks: no shared pattern
   const int len = vm >> 8 & 15;
   const unsigned full = (1u << len) - 1u;
   return len <= 8 && (dm & full) == full && ((unsigned)vm & full) == full;
@@ -501,20 +551,27 @@ pcg_status build_dia(pcg_matrix *A, cudaStream_t st) {
   PCG_CUDA(cudaMalloc(&A->d_sdval, sizeof(double) * 8 * (size_t)A->n_slices));
   PCG_CUDA(cudaMalloc(&A->d_sdvmeta, sizeof(uint16_t) * (size_t)A->n_slices));
   PCG_CUDA(cudaMemsetAsync(A->d_sdval, 0, sizeof(double) * 8 * (size_t)A->n_slices, st));
+  const char *ea = getenv("PCG_DIA_ALIGN");  // PCG_DIA_ALIGN=0: no aligned (zero-mask) slices
+  if (vals && !(ea && atoi(ea) == 0)) {
+    PCG_CUDA(cudaMalloc(&A->d_sdzmask, sizeof(unsigned) * 8 * (size_t)A->n_slices));
+    PCG_CUDA(cudaMemsetAsync(A->d_sdzmask, 0, sizeof(unsigned) * 8 * (size_t)A->n_slices, st));
+  }
   unsigned long long *d_n;
-  PCG_CUDA(cudaMalloc(&d_n, 3 * sizeof(unsigned long long)));
-  PCG_CUDA(cudaMemsetAsync(d_n, 0, 3 * sizeof(unsigned long long), st));
+  PCG_CUDA(cudaMalloc(&d_n, 4 * sizeof(unsigned long long)));
+  PCG_CUDA(cudaMemsetAsync(d_n, 0, 4 * sizeof(unsigned long long), st));
   dia_build_kernel<<<(unsigned)((A->n_slices * 32 + 255) / 256), 256, 0, st>>>(
       A->n, A->n + A->n_ghost, A->n_slices, A->d_row_ptr, A->d_slice_ptr, A->d_scol, A->d_sval, vals,
-      A->d_sdoff, A->d_sdmask, A->d_sdval, A->d_sdvmeta, d_n);
+      A->d_sdoff, A->d_sdmask, A->d_sdval, A->d_sdvmeta, A->d_sdzmask, d_n);
   count_launch();
-  unsigned long long np[3] = {0, 0, 0};
+  unsigned long long np[4] = {0, 0, 0, 0};
   PCG_CUDA(cudaMemcpyAsync(np, d_n, sizeof(np), cudaMemcpyDeviceToHost, st));
   PCG_CUDA(cudaStreamSynchronize(st));
   cudaFree(d_n);
   A->dia_positions = (int64_t)np[0];
   A->dia_slices = (int64_t)np[1];
-  A->dval_slices = (int64_t)np[2];
+  A->dval_slices = (int64_t)np[2] + (int64_t)np[3];
+  A->aligned_slices = (int64_t)np[3];
+  if (A->d_sdzmask) A->device_bytes += 32.0 * (double)A->n_slices;
   A->device_bytes += 33.0 * (double)A->n_slices;
   A->device_bytes += 66.0 * (double)A->n_slices;
   PCG_TRY(build_dia_patterns(A, st));
@@ -537,6 +594,12 @@ void free_sell(pcg_matrix *A) {
     A->device_bytes -= 66.0 * (double)A->n_slices;
     A->d_sdval = nullptr;
     A->d_sdvmeta = nullptr;
+  }
+  if (A->d_sdzmask) {
+    cudaFree(A->d_sdzmask);
+    A->device_bytes -= 32.0 * (double)A->n_slices;
+    A->d_sdzmask = nullptr;
+    A->aligned_slices = 0;
   }
   if (A->d_sdpat) {
     cudaFree(A->d_sdpat);
@@ -1049,6 +1112,7 @@ extern "C" pcg_status pcg_matrix_get_stats(pcg_matrix_t A, pcg_matrix_stats *o) 
   o->dia_slices = (int32_t)std::min<int64_t>(A->dia_slices, INT32_MAX);
   o->dval_slices = A->dval_slices;
   o->npat = A->npat;
+  o->aligned_slices = A->aligned_slices;
   o->pat_slices = A->pat_slices;
   return PCG_OK;
 }

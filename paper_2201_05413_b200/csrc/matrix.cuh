@@ -178,6 +178,8 @@ struct pcg_matrix {
   // value-uniform positions of those slices (common.cuh SellView::dval / dvmeta)
   double *d_sdval = nullptr;
   uint16_t *d_sdvmeta = nullptr;
+  unsigned *d_sdzmask = nullptr;
+  int64_t aligned_slices = 0;  // value-free slices in the aligned (zero-mask) form
   int64_t dval_slices = 0;    // one-trip slices whose values are all per-position uniform (no value stream)
   // their patterns (common.cuh SellView::dpat / ptab)
   uint8_t *d_sdpat = nullptr;
@@ -187,7 +189,7 @@ struct pcg_matrix {
   int64_t pat_slices = 0;     // value-free slices that read a shared pattern
   pcgb::SellView sell() const {
     return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0, d_sdcol, d_scbase, 0,
-            d_sdoff, d_sdmask, d_sdval, d_sdvmeta, d_sdpat, d_ptab, d_plen, npat};
+            d_sdoff, d_sdmask, d_sdval, d_sdvmeta, d_sdzmask, d_sdpat, d_ptab, d_plen, npat};
   }
 };
 

@@ -190,9 +190,10 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
     unsigned mask;
     int off;
     double val;
+    unsigned zm;  // aligned slices: lanes without an entry at position `lane` (lanes 0-7)
   };
   auto meta = [&](int64_t x) {
-    Meta m{0, 0u, 0, 0.0};
+    Meta m{0, 0u, 0, 0.0, 0u};
     if (x < A.n_slices) {
       const unsigned pid = dpat ? dpat[x] : DIA_NOPAT;
       if (PCG_DIA_SKIPMETA && pid != DIA_NOPAT) {  // a pattern slice: its index is all it needs
@@ -203,6 +204,7 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
         if (lane < 8) {
           m.off = doff[x * 8 + lane];
           m.val = dval[x * 8 + lane];
+          if (A.dzmask) m.zm = A.dzmask[(x + (A.row0 >> 5)) * 8 + lane];
         }
       }
     }
@@ -244,6 +246,11 @@ __device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, 
       if ((m0.mask >> 8 & full) == full) {  // ... and every value too: no value stream at all
 #pragma unroll
         for (int u = 0; u < 8; u++) a[u] = __shfl_sync(0xffffffffu, m0.val, u);
+        if (m0.mask >> 20 & 1u) {  // aligned form: rows without an entry there add 0 * p
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+            if (__shfl_sync(0xffffffffu, m0.zm, u) >> lane & 1u) a[u] = 0.0;
+        }
       } else {
 #pragma unroll
         for (int u = 0; u < 8; u++)

@@ -418,9 +418,10 @@ def test_uniform_offset_positions_are_bitwise_the_id_form(pcg, monkeypatch, name
         tol = O.configs()[name]["tol"]
     monkeypatch.setenv("PCG_PERSIST", "0")
     hs = {}
-    knobs = ("PCG_DIA", "PCG_SHORT", "PCG_DIA_VAL", "PCG_DIA_PAT")
+    knobs = ("PCG_DIA", "PCG_SHORT", "PCG_DIA_VAL", "PCG_DIA_PAT", "PCG_DIA_ALIGN")
     for key, env in (("dia", {}), ("ids", {"PCG_DIA": "0"}), ("chunked", {"PCG_SHORT": "0"}),
-                     ("novals", {"PCG_DIA_VAL": "0"}), ("nopat", {"PCG_DIA_PAT": "0"})):
+                     ("novals", {"PCG_DIA_VAL": "0"}), ("nopat", {"PCG_DIA_PAT": "0"}),
+                     ("noalign", {"PCG_DIA_ALIGN": "0"})):
         for k in knobs:
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
@@ -434,22 +435,26 @@ def test_uniform_offset_positions_are_bitwise_the_id_form(pcg, monkeypatch, name
     assert hs["ids"].stats()["dia_positions"] == 0
     # lattice stencils and the constant band: value-uniform one-trip slices exist; the
     # scaled couplings of mixv leave some one-trip slices reading their values
-    # (below c = 64 every 32-row slice of a lattice meets a boundary row: no one-trip slice)
-    assert st["dval_slices"] <= st["dia_slices"], st
+    # (below c = 64 every 32-row slice of a lattice meets a boundary row: only the aligned
+    # form, positions = the union of the rows' offsets, makes such slices one-trip)
+    assert st["aligned_slices"] <= st["dval_slices"] <= st["dia_slices"], st
+    if name in ("mixv", "C5", "C1"):
+        assert st["aligned_slices"] > 0, st
     if name == "mixv" or (name == "C5" and c >= 64):
-        assert st["dval_slices"] > 0, st
+        assert st["dval_slices"] > st["aligned_slices"], st
+    assert hs["noalign"].stats()["aligned_slices"] == 0
     if name == "mixv":
         assert st["dval_slices"] < st["dia_slices"], st
     # the value-free slices read a shared pattern (a lattice has a handful: interior, faces)
     assert st["pat_slices"] <= st["dval_slices"] and st["npat"] <= 32, st
-    if st["dval_slices"] > 0:
+    if st["dval_slices"] > st["aligned_slices"]:  # (aligned slices keep their own zero masks)
         assert st["pat_slices"] > 0 and st["npat"] > 0, st
     assert hs["nopat"].stats()["pat_slices"] == 0 and hs["nopat"].stats()["dval_slices"] == st["dval_slices"]
     assert hs["novals"].stats()["dval_slices"] == 0 and hs["novals"].stats()["pat_slices"] == 0
-    assert hs["novals"].stats()["dia_slices"] == st["dia_slices"]
+    assert hs["novals"].stats()["dia_slices"] == st["dia_slices"] - st["aligned_slices"]
     x = np.random.default_rng(12).standard_normal(A.n)
     ys = {k: M.spmv(_dev(x)).cpu().numpy() for k, M in hs.items()}
-    for k in ("ids", "chunked", "novals", "nopat"):
+    for k in ("ids", "chunked", "novals", "nopat", "noalign"):
         assert np.array_equal(ys["dia"], ys[k]), k
     r = O.pcg(A, b, tol=tol)
     xs, info = hs["dia"].solve(_dev(b), tol=tol)
