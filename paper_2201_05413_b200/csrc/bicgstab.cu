@@ -135,7 +135,7 @@ enum { SP_RESID = 0, SP_AV = 1, SP_AT = 2, SP_FINAL = 3 };
 // the SpMV passes: RESID w = b - A x (r = w, p = v = 0; sums w.w, r^.w, b.b),
 // AV v = A p^ (r^.v), AT t = A s^ (t.s, t.t), FINAL w = b - A x (w.w)
 template <int FMT, int L, int MODE>
-__device__ __forceinline__ void spmv_body(const SellView &S, const CsrView &C, const BicgVecs &v, double &a0,
+__device__ __forceinline__ void spmv_body(const SellViewDia &S, const CsrView &C, const BicgVecs &v, double &a0,
                                           double &a1, double &a2) {
   const double *__restrict__ G = MODE == SP_AV ? v.ph : (MODE == SP_AT ? v.sh : v.x);
   auto gather = [&](int j) { return ld_weak(G + j); };  // also inside the cooperative kernel
@@ -167,7 +167,7 @@ __device__ __forceinline__ void spmv_body(const SellView &S, const CsrView &C, c
 }
 
 template <int FMT, int L, int MODE>
-__device__ __noinline__ void bicg_spmv_pass(const SellView &S, const CsrView &C, const BicgVecs &v, double *out,
+__device__ __noinline__ void bicg_spmv_pass(const SellViewDia &S, const CsrView &C, const BicgVecs &v, double *out,
                                             double (*sm)[WARPS]) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   spmv_body<FMT, L, MODE>(S, C, v, a0, a1, a2);
@@ -351,12 +351,12 @@ __device__ __noinline__ void bicg_update_pass(const BicgVecs &v, int64_t n, doub
 }
 
 template <int FMT, int L, int BS>
-__global__ void __launch_bounds__(BLOCK, 3) bicg_kernel(SellView S_, CsrView C_, BicgVecs v_, BicgState *st,
+__global__ void __launch_bounds__(BLOCK, 3) bicg_kernel(SellViewDia S_, CsrView C_, BicgVecs v_, BicgState *st,
                                                         double *part, GridBar *bar) {
   __shared__ double sm[2][WARPS];
   __shared__ double s_tot[2];
   __shared__ BicgShared q;
-  __shared__ SellView S;
+  __shared__ SellViewDia S;
   __shared__ CsrView C;
   __shared__ BicgVecs v;
   if (threadIdx.x == 0) {
@@ -647,7 +647,7 @@ __device__ __forceinline__ bool bg_last(double (&red)[NV], double *part, unsigne
 
 // SpMV kernels: RESID (rmode BR_INIT / BR_CHECK), AV, AT, FINAL (rmode BR_FINAL)
 template <int FMT, int L, int MODE>
-__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) bg_spmv_kernel(SellView S, CsrView C, BicgVecs v, BgScalars *sc,
+__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) bg_spmv_kernel(SellViewDia S, CsrView C, BicgVecs v, BgScalars *sc,
                                                         double *part, int rmode, int dist, int use_cond,
                                                         cudaGraphConditionalHandle h) {
   __shared__ double sm[3][WARPS];
@@ -771,7 +771,7 @@ struct BgOps {
 template <int FMT, int L, int BS>
 static void bg_iteration(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double *part, cudaStream_t st, int use_cond,
                          cudaGraphConditionalHandle h) {
-  const SellView S = A->sell();
+  const SellViewDia S = A->sell_dia();
   const CsrView C = A->csr();
   const int gs = A->grid_spmv, gv = A->grid_vec;
   bg_precond_kernel<BS, 0><<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, 0, use_cond, h);
@@ -785,7 +785,7 @@ static void bg_iteration(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double
 template <int FMT, int L>
 static void bg_iteration_ilu(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double *part, cudaStream_t st,
                              int use_cond, cudaGraphConditionalHandle h) {
-  const SellView S = A->sell();
+  const SellViewDia S = A->sell_dia();
   const CsrView C = A->csr();
   const int gs = A->grid_spmv, gv = A->grid_vec;
   bg_vec_kernel<0><<<gv, BLOCK, 0, st>>>(A->n, v, sc, part, use_cond, h);
@@ -801,9 +801,9 @@ static void bg_iteration_ilu(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, do
 template <int FMT, int L, int BS>
 static void bg_resid(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, double *part, int rmode, cudaStream_t st) {
   if (rmode == BR_FINAL)
-    bg_spmv_kernel<FMT, L, SP_FINAL><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), v, sc, part, rmode, 0, 0, 0);
+    bg_spmv_kernel<FMT, L, SP_FINAL><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell_dia(), A->csr(), v, sc, part, rmode, 0, 0, 0);
   else
-    bg_spmv_kernel<FMT, L, SP_RESID><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell(), A->csr(), v, sc, part, rmode, 0, 0, 0);
+    bg_spmv_kernel<FMT, L, SP_RESID><<<A->grid_spmv, BLOCK, 0, st>>>(A->sell_dia(), A->csr(), v, sc, part, rmode, 0, 0, 0);
   count_launch();
 }
 
@@ -961,7 +961,7 @@ template <int FMT, int L>
 struct BgdOps {
   static void spmv(pcg_matrix *A, const BicgVecs &v, BgScalars *sc, int mode, int rmode, cudaStream_t st) {
     double *part = A->work.partials;
-    const SellView S = A->sell();
+    const SellViewDia S = A->sell_dia();
     const CsrView C = A->csr();
     switch (mode) {
       case SP_RESID: bg_spmv_kernel<FMT, L, SP_RESID><<<A->grid_spmv, BLOCK, 0, st>>>(S, C, v, sc, part, rmode, 1, 0, 0); break;
@@ -1169,7 +1169,7 @@ static pcg_status bicg_impl(pcg_matrix *A, const double *b, double *x, double to
                                                            std::max<int64_t>(1, (n + BLOCK - 1) / BLOCK)));
       w.bgrid_bs = bs;
     }
-    SellView S = A->sell();
+    SellViewDia S = A->sell_dia();
     CsrView Cv = A->csr();
     double *part = w.partials;  // 4 x grid (<= 8 x SMs; partials hold 6 x 32 x SMs)
     GridBar *bar = (GridBar *)w.bbar;

@@ -127,6 +127,11 @@ struct SellView {
   // need no column ids, and a slice with only such positions needs one round trip
   const int *doff;
   const uint8_t *dmask;
+};
+// The uniform-offset engine's further metadata, a separate view so the kernels that do
+// not run that engine (the persistent and pipelined kernels, the SpMM) keep the smaller
+// parameter block (a larger one measured 7-9 % slower persistent solves: C2, C3, C6).
+struct SellViewDia : SellView {
   // value-uniform positions of those slices (CSR-VI-style value sharing; built with doff):
   // bit t of dvmeta[s] set when the 32 stored values of slice s at position t (padding
   // zeros included) are bitwise equal (none with PCG_DIA_VAL=0); that value is

@@ -189,7 +189,19 @@ struct pcg_matrix {
   int64_t pat_slices = 0;     // value-free slices that read a shared pattern
   pcgb::SellView sell() const {
     return {n, n_slices, d_slice_ptr, d_scol, d_sval, stages, stage_entries, d_lead, 0, d_sdcol, d_scbase, 0,
-            d_sdoff, d_sdmask, d_sdval, d_sdvmeta, d_sdzmask, d_sdpat, d_ptab, d_plen, npat};
+            d_sdoff, d_sdmask};
+  }
+  pcgb::SellViewDia sell_dia() const {
+    pcgb::SellViewDia v;
+    static_cast<pcgb::SellView &>(v) = sell();
+    v.dval = d_sdval;
+    v.dvmeta = d_sdvmeta;
+    v.dzmask = d_sdzmask;
+    v.dpat = d_sdpat;
+    v.ptab = d_ptab;
+    v.plen = d_plen;
+    v.npat = npat;
+    return v;
   }
 };
 

@@ -156,7 +156,7 @@ __device__ __forceinline__ void sell_rows_short(const SellView &A, Gather gather
 // if its offsets and values are one of the matrix's shared patterns (SellView::dpat) it
 // reads them from shared memory instead (six vector loads instead of 24 shuffles).
 template <class Gather, class Epi>
-__device__ __forceinline__ void sell_rows_dia(const SellView &A, Gather gather, Epi epi) {
+__device__ __forceinline__ void sell_rows_dia(const SellViewDia &A, Gather gather, Epi epi) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * WARPS;

@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, 
 template <int FMT, int L>
 // row0/phase: the distributed overlap runs K1b over row ranges (views offset by row0);
 // phase 1 starts p.q (sigma_acc = local), 3 adds to it, 2 completes it (sigma = acc + local)
-__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) k1b_kernel(SellView S, CsrView C, int64_t n_ghost, Vecs v, Scalars *sc,
+__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) k1b_kernel(SellViewDia S, CsrView C, int64_t n_ghost, Vecs v, Scalars *sc,
                                                     double *partials, int dist, int use_cond,
                                                     cudaGraphConditionalHandle h, int64_t row0, int phase,
                                                     int xdefer) {
@@ -437,7 +437,7 @@ __global__ void finish_beta_kernel(Scalars *sc, int use_cond, cudaGraphCondition
 // ---------------------------------------------------------------- residual (init / exit check / replacement)
 // w = b - A x; r = w; z = dinv w; p[parity] = 0; partial sums (w.w, w.z, b.b).
 template <int FMT, int L>
-__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) resid_kernel(SellView S, CsrView C, int64_t n_ghost,
+__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) resid_kernel(SellViewDia S, CsrView C, int64_t n_ghost,
                                                       const double *__restrict__ b, Vecs v, Scalars *sc,
                                                       double *partials, int mode, int dist) {
   __shared__ double sm[3][WARPS];
@@ -565,7 +565,7 @@ __global__ void clear_alpha_kernel(Scalars *sc, int xdefer) {
 
 // ---------------------------------------------------------------- standalone SpMV  y = A x
 template <int FMT, int L>
-__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) spmv_kernel(SellView S, CsrView C, const double *__restrict__ x,
+__global__ void __launch_bounds__(BLOCK, D16_MINB(FMT)) spmv_kernel(SellViewDia S, CsrView C, const double *__restrict__ x,
                                                      double *__restrict__ y, int64_t x_len) {
   auto gather = [&](int j) { return __ldg(x + j); };
   auto epi = [&](int64_t i, double s) { __stcs(y + i, s); };
@@ -631,7 +631,7 @@ static Vecs vecs_of(pcg_matrix *A) {
 
 pcg_status launch_spmv_fmt(pcg_matrix *A, int fmt, const double *x, double *y, cudaStream_t st) {
   PCG_DISPATCH_D16(fmt_d16(A, fmt), A->csr_lanes, spmv_kernel,
-                   <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), x, y, A->n + A->n_ghost));
+                   <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell_dia(), A->csr(), x, y, A->n + A->n_ghost));
   count_launch();
   PCG_CUDA(cudaGetLastError());
   return PCG_OK;
@@ -686,7 +686,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
       }
       if (R.r1 <= R.r0) continue;
       const int phase = t == 0 ? 1 : (t == last ? 2 : 3);
-      SellView S = A->sell();
+      SellViewDia S = A->sell_dia();
       CsrView Cv = A->csr();
       const int64_t s0 = R.r0 / 32, s1 = R.r1 == A->n ? A->n_slices : R.r1 / 32;
       S.slice_ptr += s0;
@@ -716,7 +716,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     Vecs vb = v;
     if (xdefer) vb.p0 = k1b_dir(v, xdefer);  // the direction this pass's K1a wrote
     PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
-                     <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, vb, w.sc, w.partials,
+                     <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell_dia(), A->csr(), A->n_ghost, vb, w.sc, w.partials,
                                                                 A->comm ? 1 : 0, use_cond, h, 0, 0, xdefer));
     count_launch();
     PCG_CUDA(cudaGetLastError());
@@ -766,7 +766,7 @@ static pcg_status launch_resid(pcg_matrix *A, const double *b, int mode, cudaStr
   SolveWork &w = A->work;
   if (A->comm) PCG_TRY(halo_exchange(A, w.x, 1, st));
   PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, resid_kernel,
-               <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, b, v, w.sc, w.partials,
+               <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell_dia(), A->csr(), A->n_ghost, b, v, w.sc, w.partials,
                                                 mode, A->comm ? 1 : 0));
   count_launch();
   PCG_CUDA(cudaGetLastError());
@@ -1143,7 +1143,7 @@ extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32
       k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, 0, 0, xd);
       PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
       PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
-                       <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell(), A->csr(), A->n_ghost, vb, w.sc,
+                       <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell_dia(), A->csr(), A->n_ghost, vb, w.sc,
                                                                   w.partials, 0, 0, 0, 0, 0, xd));
       count_launch(2);
     } else {
