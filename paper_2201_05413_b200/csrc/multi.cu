@@ -384,8 +384,11 @@ __device__ __forceinline__ double long_row_sum(const double *vp, const int *cp, 
 //   MS_RESID: W_c = B_c - A X_c, block partials (W.W, W.(dinv W), B.B)   (all k columns)
 // Per (slice, column) the row values meet in a fixed xor tree and lane 0 adds
 // them to the warp's accumulator in slice order; warps are combined in order.
+#ifndef PCG_SPMM_PAT  // A/B knob: the SpMM reads shared value-free slice patterns
+#define PCG_SPMM_PAT 1
+#endif
 template <int MODE, bool LONG>
-__global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, MVecs v, MultiScalars *sc, double *partials, int k,
+__global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellViewDia S, MVecs v, MultiScalars *sc, double *partials, int k,
                                                       int pf, int use_cond, cudaGraphConditionalHandle h,
                                                       int pass) {
   constexpr int NV = MODE == MS_SPMM ? 1 : 3;
@@ -407,6 +410,16 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
   const bool acc_smem = MODE == MS_SPMM && k <= 16;
   if (acc_smem)
     for (int t = threadIdx.x; t < k * BLOCK; t += BLOCK) s_acc[t] = 0.0;
+  // the matrix's value-free slice patterns (common.cuh SellViewDia::dpat): such a slice's
+  // entries come from shared memory instead of the value/id streams
+  __shared__ DiaPat s_pat[DIA_MAXPAT];
+  __shared__ int s_plen[DIA_MAXPAT];
+  const bool pats = PCG_SPMM_PAT && S.dpat != nullptr && S.npat > 0;
+  if (pats) {
+    for (int t = threadIdx.x; t < S.npat * 12; t += BLOCK)
+      reinterpret_cast<double *>(s_pat)[t] = reinterpret_cast<const double *>(S.ptab)[t];
+    for (int t = threadIdx.x; t < S.npat; t += BLOCK) s_plen[t] = S.plen[t];
+  }
   __syncthreads();
   unsigned int act = 0;  // active columns as a register mask (s_act costs a shared load per use)
   for (int c = 0; c < k; c++) act |= (unsigned int)s_act[c] << c;
@@ -416,9 +429,19 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
   // contiguous chunk per block, for L1 reuse, measured 316 vs 229 us on C4.)
   const int64_t w0 = (int64_t)blockIdx.x * WARPS + wid, nw = (int64_t)gridDim.x * WARPS;
   const double *__restrict__ G = MODE == MS_SPMM ? v.P : v.X;  // gathered block vector
+  // the next slice's pattern index is fetched one slice ahead (indexed by slice)
+  unsigned pid_n = pats && w0 < S.n_slices ? (unsigned)S.dpat[w0] : (unsigned)DIA_NOPAT;
   for (int64_t s = w0; s < S.n_slices; s += nw) {
-    const int64_t base = __ldg(S.slice_ptr + s);
-    const int len = (int)((__ldg(S.slice_ptr + s + 1) - base) >> 5);
+    const unsigned pid = pid_n;
+    pid_n = pats && s + nw < S.n_slices ? (unsigned)S.dpat[s + nw] : (unsigned)DIA_NOPAT;
+    int64_t base = 0;
+    int len;
+    if (pid != DIA_NOPAT) {
+      len = s_plen[pid];
+    } else {
+      base = __ldg(S.slice_ptr + s);
+      len = (int)((__ldg(S.slice_ptr + s + 1) - base) >> 5);
+    }
     const int64_t row = s * 32 + lane;
     const bool ok = row < S.n;
     const double *vp = S.val + base + lane;
@@ -456,15 +479,24 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellView S, 
     if (!LONG || len <= 8) {  // fast path: the slice's entries stay in registers for all columns
       double a[8];
       int j[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (pid != DIA_NOPAT) {  // the pattern's offsets and values (the slice's own, bitwise)
+        const DiaPat &P = s_pat[pid];
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
-        a[u] = 0.0;
-        if (u < len) {
-          a[u] = ld_stream(vp + (size_t)u * 32);
-          j[u] = ld_stream(cp + (size_t)u * 32);
+        for (int u = 0; u < 8; u++) {
+          a[u] = u < len ? P.val[u] : 0.0;
+          j[u] = u < len ? (int)row + P.off[u] : 0;
         }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          a[u] = 0.0;
+          if (u < len) {
+            a[u] = ld_stream(vp + (size_t)u * 32);
+            j[u] = ld_stream(cp + (size_t)u * 32);
+          }
+        }
+        cols_ready(j, S.zero);
       }
-      cols_ready(j, S.zero);
       if (pf) {  // first touch of a gathered line is (mostly) its largest column: start every
                  // column's fetch now so only the first gather round waits on HBM (padding
                  // entries are column 0; a select of j[len - 1] went to local memory)
@@ -1103,7 +1135,7 @@ static void launch_mspmm(pcg_matrix *A, int k, cudaStream_t st, int use_cond, cu
     return;
   }
   const int g = mgrid_spmm(A, k);
-  const SellView S = A->sell();
+  const SellViewDia S = A->sell_dia();
   MVecs v = mvecs_of(A);
   if (pass) {  // the block this pass's K1a wrote: P[j+1] after a hold, P[0] after the apply
     const int xm = pass >> 4, xj = pass & 15;
@@ -1152,9 +1184,9 @@ pcg_status block_spmm(pcg_matrix *A, const double *P, double *Q, int k, int64_t 
   v.ld = ld;
   const size_t smem = k <= 16 ? sizeof(double) * BLOCK * k : 0;
   if (A->max_row_len > 8)
-    mspmm_kernel<MS_SPMM, true><<<g, BLOCK, smem, st>>>(A->sell(), v, sc, w.bspmm_part, k, spmm_prefetch(), 0, 0, 0);
+    mspmm_kernel<MS_SPMM, true><<<g, BLOCK, smem, st>>>(A->sell_dia(), v, sc, w.bspmm_part, k, spmm_prefetch(), 0, 0, 0);
   else
-    mspmm_kernel<MS_SPMM, false><<<g, BLOCK, smem, st>>>(A->sell(), v, sc, w.bspmm_part, k, spmm_prefetch(), 0, 0, 0);
+    mspmm_kernel<MS_SPMM, false><<<g, BLOCK, smem, st>>>(A->sell_dia(), v, sc, w.bspmm_part, k, spmm_prefetch(), 0, 0, 0);
   count_launch(2);
   PCG_CUDA(cudaGetLastError());
   return PCG_OK;

@@ -401,7 +401,8 @@ def _grid_values(m, seed):
     return _csr(M)
 
 
-@pytest.mark.parametrize("name,c", [("C1", None), ("C5", 32), ("C5", 64), ("C4", 16), ("mix", 900), ("mixv", 70)])
+@pytest.mark.parametrize("name,c", [("C1", None), ("C1", 512), ("C5", 32), ("C5", 64), ("C4", 16), ("mix", 900),
+                                    ("mixv", 70)])
 def test_uniform_offset_positions_are_bitwise_the_id_form(pcg, monkeypatch, name, c):
     """The one-chunk engine's id-free uniform-offset positions (pcg.h dia_positions)
     and value-uniform slices (pcg.h dval_slices): the same columns and values, so the
@@ -456,6 +457,10 @@ def test_uniform_offset_positions_are_bitwise_the_id_form(pcg, monkeypatch, name
     ys = {k: M.spmv(_dev(x)).cpu().numpy() for k, M in hs.items()}
     for k in ("ids", "chunked", "novals", "nopat", "noalign"):
         assert np.array_equal(ys["dia"], ys[k]), k
+    # the multi-RHS SpMM reads the shared patterns too: bitwise the stream form
+    B3 = np.random.default_rng(13).standard_normal((A.n, 3))
+    X3 = {k: hs[k].solve_multi(_dev(B3), tol=1e-8)[0].cpu().numpy() for k in ("dia", "nopat", "ids")}
+    assert np.array_equal(X3["dia"], X3["nopat"]) and np.array_equal(X3["dia"], X3["ids"])
     r = O.pcg(A, b, tol=tol)
     xs, info = hs["dia"].solve(_dev(b), tol=tol)
     assert info["status"] == 0 and info["relres_true"] <= tol
