@@ -935,6 +935,10 @@ pcg_status create_local(pcg_matrix *A, int64_t n, int64_t nnz, const int64_t *d_
     A->schedule = (sch && atoi(sch) == 2) ? 2 : 3;
   }
   if (A->work.graph_ready) free_work(A);  // geometry changed after a provisional workspace
+  if (A->work.dslice) {  // dinv may have been permuted since (SELL-C-sigma, RCM)
+    cudaFree(A->work.dslice);
+    A->work.dslice = nullptr;
+  }
   A->device_bytes += (double)(n + 1) * 4 + (double)nnz * 12 + (double)n * 8;
   return PCG_OK;
 }
@@ -980,8 +984,34 @@ pcg_status csr_create_impl(int64_t n, int64_t nnz, const int64_t *row_ptr, const
 }
 
 // ---------------------------------------------------------------- workspace
+// SolveWork::dslice: per 32-row slice the common dinv, NaN when the slice's entries differ
+// (a full slice only: the last, partial one always reads per row)
+__global__ void dinv_slice_kernel(int64_t n, const double *__restrict__ dinv, double *__restrict__ dslice) {
+  const int64_t ns = (n + 31) / 32;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ns * 32; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = t >> 5;
+    const int lane = (int)(t & 31);
+    const unsigned long long b = t < n ? (unsigned long long)__double_as_longlong(dinv[t]) : ~0ull;
+    const unsigned long long b0 = __shfl_sync(0xffffffffu, b, 0);
+    const bool same = __all_sync(0xffffffffu, b == b0 && t < n);
+    if (lane == 0) dslice[s] = same ? __longlong_as_double((long long)b0) : __longlong_as_double(0x7ff8000000000000ll);
+  }
+}
+
 pcg_status ensure_work(pcg_matrix *A) {
   SolveWork &w = A->work;
+  if (!w.dslice) {  // (dropped when the format choice swaps dinv: rebuilt from the final one)
+    const char *ed = getenv("PCG_DINV_SLICE");  // PCG_DINV_SLICE=0: K2 reads dinv per row
+    if (A->n > 0 && !(ed && atoi(ed) == 0)) {
+      const int64_t ns = (A->n + 31) / 32;
+      PCG_CUDA(cudaMalloc(&w.dslice, sizeof(double) * (size_t)ns));
+      dinv_slice_kernel<<<(unsigned)std::min<int64_t>((ns * 32 + 255) / 256, 148 * 64), 256>>>(A->n, A->d_dinv,
+                                                                                          w.dslice);
+      count_launch();
+      PCG_CUDA(cudaGetLastError());
+      PCG_CUDA(cudaStreamSynchronize(0));  // (before any solve stream reads it)
+    }
+  }
   if (w.sc) return PCG_OK;
   // +64 entries of padding: TMA tile copies round row counts up to 16-B multiples
   const size_t n = (size_t)A->n, ng = (size_t)(A->n + A->n_ghost);
@@ -1021,7 +1051,7 @@ void free_work(pcg_matrix *A) {
   if (w.bg_graph) cudaGraphDestroy(w.bg_graph);
   if (w.ilu) ilu_free(w.ilu);
   for (double *p : {w.r, w.z, w.q, w.p[0], w.p[1], w.p23[0], w.p23[1], w.x, w.w, w.stage_b, w.stage_x, w.partials,
-                    w.mr, w.mz, w.mq, w.mp[0], w.mp[1], w.mp23[0], w.mp23[1], w.mx, w.mb, w.mw, w.mpart})
+                    w.dslice, w.mr, w.mz, w.mq, w.mp[0], w.mp[1], w.mp23[0], w.mp23[1], w.mx, w.mb, w.mw, w.mpart})
     if (p) cudaFree(p);
   if (w.sc) cudaFree(w.sc);
   if (w.h_sc) cudaFreeHost(w.h_sc);

@@ -52,6 +52,9 @@ struct SolveWork {
   double *w = nullptr;  // spmv scratch (exit check / standalone spmv)
   double *stage_b = nullptr, *stage_x = nullptr;  // device staging for host pointers
   double *partials = nullptr;  // 4 * max_grid
+  // per 32-row slice the slice's dinv when its 32 entries are bitwise equal, NaN otherwise
+  // (K2 then reads 8 bytes per 32 rows instead of 8 per row: a lattice's Jacobi diagonal)
+  double *dslice = nullptr;
   Scalars *sc = nullptr;       // device scalars
   Scalars *h_sc = nullptr;     // pinned host mirror
   cudaGraphExec_t loop_exec = nullptr;

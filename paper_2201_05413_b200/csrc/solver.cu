@@ -177,8 +177,12 @@ __global__ void __launch_bounds__(BLOCK) k1_kernel(SellView S, CsrView C, int64_
 }
 
 // ---------------------------------------------------------------- K2: r, z updates + rho', gamma
+#ifndef PCG_K2_UNROLL  // element pairs per thread and trip in K2 (A/B knob: 1 or 2)
+#define PCG_K2_UNROLL 1
+#endif
 __global__ void __launch_bounds__(BLOCK) k2_kernel(int64_t n, Vecs v, Scalars *sc, double *partials,
-                                                   int dist, int use_cond, cudaGraphConditionalHandle h) {
+                                                   int dist, int use_cond, cudaGraphConditionalHandle h,
+                                                   const double *__restrict__ dsl) {
   __shared__ double sm[2][WARPS];
   const volatile Scalars *vs = sc;
   if (vs->done != DONE_RUNNING) {
@@ -192,9 +196,9 @@ __global__ void __launch_bounds__(BLOCK) k2_kernel(int64_t n, Vecs v, Scalars *s
   const double2 *__restrict__ d2 = reinterpret_cast<const double2 *>(v.dinv);
   double2 *__restrict__ r2 = reinterpret_cast<double2 *>(v.r);
   double2 *__restrict__ z2 = reinterpret_cast<double2 *>(v.z);
-  for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < npair; i += (int64_t)gridDim.x * BLOCK) {
-    const double2 qq = __ldcs(q2 + i), dd = __ldg(d2 + i);
-    double2 rr = r2[i];
+  // a slice with one common dinv (SolveWork::dslice): 8 bytes per 32 rows, the same values
+  auto dinv2 = [&](int64_t i, double du) { return du == du ? make_double2(du, du) : __ldg(d2 + i); };
+  auto step = [&](double2 qq, double2 rr, double2 dd, int64_t i) {
     rr.x = __fma_rn(-alpha, qq.x, rr.x);
     rr.y = __fma_rn(-alpha, qq.y, rr.y);
     const double2 zz = make_double2(dd.x * rr.x, dd.y * rr.y);
@@ -204,6 +208,24 @@ __global__ void __launch_bounds__(BLOCK) k2_kernel(int64_t n, Vecs v, Scalars *s
     a0 = __fma_rn(rr.y, zz.y, a0);
     a1 = __fma_rn(rr.x, rr.x, a1);
     a1 = __fma_rn(rr.y, rr.y, a1);
+  };
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  const int64_t st = (int64_t)gridDim.x * BLOCK;
+  int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+  // PCG_K2_UNROLL pairs per trip, every load issued first (the same element order per
+  // thread, so the same sums)
+  for (; PCG_K2_UNROLL == 2 && i + st < npair; i += 2 * st) {
+    const double2 qa = __ldcs(q2 + i), qb = __ldcs(q2 + i + st);
+    const double2 ra = r2[i], rb = r2[i + st];
+    const double ua = dsl ? __ldg(dsl + (i >> 4)) : nan, ub = dsl ? __ldg(dsl + ((i + st) >> 4)) : nan;
+    const double2 da = dinv2(i, ua), db = dinv2(i + st, ub);
+    step(qa, ra, da, i);
+    step(qb, rb, db, i + st);
+  }
+  for (; i < npair; i += st) {
+    const double2 qq = __ldcs(q2 + i), rr = r2[i];
+    const double du = dsl ? __ldg(dsl + (i >> 4)) : nan;
+    step(qq, rr, dinv2(i, du), i);
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t i = n - 1;
@@ -748,7 +770,7 @@ static pcg_status launch_k2(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
   Vecs v = vecs_of(A);
   SolveWork &w = A->work;
   k2_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, v, w.sc, w.partials + 2 * (size_t)A->grid_spmv, A->comm ? 1 : 0,
-                                           use_cond, h);
+                                           use_cond, h, w.dslice);
   count_launch();
   PCG_CUDA(cudaGetLastError());
   if (A->comm) {

@@ -529,3 +529,30 @@ def test_multi_rhs_chunking_and_leading_dimensions(pcg):
             assert infos[j].status == 0
             assert np.linalg.norm(X[j, :n] - r.x) / np.linalg.norm(r.x) <= 1e-9
             assert abs(infos[j].iterations - r.iterations) <= max(1, 0.02 * r.iterations)
+
+
+@pytest.mark.parametrize("name,c", [("C5", 64), ("C1", 512), ("C3", 48), ("C2", 96)])
+def test_dinv_slices_are_bitwise_the_per_row_dinv(pcg, monkeypatch, name, c):
+    """K2 reads one dinv per 32-row slice where the slice's 32 entries are equal (a
+    lattice's Jacobi diagonal; SolveWork::dslice): the same values, so the graph-loop
+    solve is bitwise the per-row form (PCG_DINV_SLICE=0) — also on systems without such
+    slices (C2 jittered, C3 P2 and SELL-C-sigma permuted) and after the format choice
+    permuted dinv."""
+    P = O.build_problem(name, c=c, k=1)
+    A, b = P["A"], P["B"][:, 0]
+    tol = O.configs()[name]["tol"]
+    monkeypatch.setenv("PCG_PERSIST", "0")
+    out = {}
+    for key, env in (("slice", None), ("row", "0")):
+        if env is None:
+            monkeypatch.delenv("PCG_DINV_SLICE", raising=False)
+        else:
+            monkeypatch.setenv("PCG_DINV_SLICE", env)
+        M = _matrix(pcg, A)
+        out[key] = M.solve(_dev(b), tol=tol)
+    monkeypatch.delenv("PCG_DINV_SLICE", raising=False)
+    (xs, infs), (xr, infr) = out["slice"], out["row"]
+    assert infs["status"] == 0 and infs["iterations"] == infr["iterations"]
+    assert np.array_equal(xs.cpu().numpy(), xr.cpu().numpy())
+    r = O.pcg(A, b, tol=tol)
+    assert np.linalg.norm(xs.cpu().numpy() - r.x) / np.linalg.norm(r.x) <= 1e-9
