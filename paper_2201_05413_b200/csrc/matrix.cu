@@ -986,7 +986,8 @@ pcg_status csr_create_impl(int64_t n, int64_t nnz, const int64_t *row_ptr, const
 // ---------------------------------------------------------------- workspace
 // SolveWork::dslice: per 32-row slice the common dinv, NaN when the slice's entries differ
 // (a full slice only: the last, partial one always reads per row)
-__global__ void dinv_slice_kernel(int64_t n, const double *__restrict__ dinv, double *__restrict__ dslice) {
+__global__ void dinv_slice_kernel(int64_t n, const double *__restrict__ dinv, double *__restrict__ dslice,
+                                  unsigned long long *__restrict__ n_shared) {
   const int64_t ns = (n + 31) / 32;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ns * 32; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = t >> 5;
@@ -994,7 +995,10 @@ __global__ void dinv_slice_kernel(int64_t n, const double *__restrict__ dinv, do
     const unsigned long long b = t < n ? (unsigned long long)__double_as_longlong(dinv[t]) : ~0ull;
     const unsigned long long b0 = __shfl_sync(0xffffffffu, b, 0);
     const bool same = __all_sync(0xffffffffu, b == b0 && t < n);
-    if (lane == 0) dslice[s] = same ? __longlong_as_double((long long)b0) : __longlong_as_double(0x7ff8000000000000ll);
+    if (lane == 0) {
+      dslice[s] = same ? __longlong_as_double((long long)b0) : __longlong_as_double(0x7ff8000000000000ll);
+      if (same) atomicAdd(n_shared, 1ull);
+    }
   }
 }
 
@@ -1004,12 +1008,20 @@ pcg_status ensure_work(pcg_matrix *A) {
     const char *ed = getenv("PCG_DINV_SLICE");  // PCG_DINV_SLICE=0: K2 reads dinv per row
     if (A->n > 0 && !(ed && atoi(ed) == 0)) {
       const int64_t ns = (A->n + 31) / 32;
+      unsigned long long *d_cnt = nullptr, cnt = 0;
       PCG_CUDA(cudaMalloc(&w.dslice, sizeof(double) * (size_t)ns));
+      PCG_CUDA(cudaMalloc(&d_cnt, sizeof(unsigned long long)));
+      PCG_CUDA(cudaMemset(d_cnt, 0, sizeof(unsigned long long)));
       dinv_slice_kernel<<<(unsigned)std::min<int64_t>((ns * 32 + 255) / 256, 148 * 64), 256>>>(A->n, A->d_dinv,
-                                                                                          w.dslice);
+                                                                                          w.dslice, d_cnt);
       count_launch();
       PCG_CUDA(cudaGetLastError());
-      PCG_CUDA(cudaStreamSynchronize(0));  // (before any solve stream reads it)
+      PCG_CUDA(cudaMemcpy(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost));  // (synchronises)
+      cudaFree(d_cnt);
+      if (2 * (int64_t)cnt < ns) {  // mostly per-row diagonals (a jittered mesh): not worth a branch
+        cudaFree(w.dslice);
+        w.dslice = nullptr;
+      }
     }
   }
   if (w.sc) return PCG_OK;
