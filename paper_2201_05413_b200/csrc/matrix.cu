@@ -985,7 +985,7 @@ pcg_status csr_create_impl(int64_t n, int64_t nnz, const int64_t *row_ptr, const
 
 // ---------------------------------------------------------------- workspace
 // SolveWork::dslice: per 32-row slice the common dinv, NaN when the slice's entries differ
-// (a full slice only: the last, partial one always reads per row)
+// (the last slice: its existing rows)
 __global__ void dinv_slice_kernel(int64_t n, const double *__restrict__ dinv, double *__restrict__ dslice,
                                   unsigned long long *__restrict__ n_shared) {
   const int64_t ns = (n + 31) / 32;
@@ -994,7 +994,7 @@ __global__ void dinv_slice_kernel(int64_t n, const double *__restrict__ dinv, do
     const int lane = (int)(t & 31);
     const unsigned long long b = t < n ? (unsigned long long)__double_as_longlong(dinv[t]) : ~0ull;
     const unsigned long long b0 = __shfl_sync(0xffffffffu, b, 0);
-    const bool same = __all_sync(0xffffffffu, b == b0 && t < n);
+    const bool same = __all_sync(0xffffffffu, b == b0 || t >= n);  // (the last slice's missing rows)
     if (lane == 0) {
       dslice[s] = same ? __longlong_as_double((long long)b0) : __longlong_as_double(0x7ff8000000000000ll);
       if (same) atomicAdd(n_shared, 1ull);
@@ -1018,6 +1018,7 @@ pcg_status ensure_work(pcg_matrix *A) {
       PCG_CUDA(cudaGetLastError());
       PCG_CUDA(cudaMemcpy(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost));  // (synchronises)
       cudaFree(d_cnt);
+      w.dslice_all = (int64_t)cnt == ns;
       if (2 * (int64_t)cnt < ns) {  // mostly per-row diagonals (a jittered mesh): not worth a branch
         cudaFree(w.dslice);
         w.dslice = nullptr;

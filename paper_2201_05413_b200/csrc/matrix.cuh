@@ -55,6 +55,7 @@ struct SolveWork {
   // per 32-row slice the slice's dinv when its 32 entries are bitwise equal, NaN otherwise
   // (K2 then reads 8 bytes per 32 rows instead of 8 per row: a lattice's Jacobi diagonal)
   double *dslice = nullptr;
+  bool dslice_all = false;  // every slice shares one: K2 stores no z, K1a forms it from r
   Scalars *sc = nullptr;       // device scalars
   Scalars *h_sc = nullptr;     // pinned host mirror
   cudaGraphExec_t loop_exec = nullptr;

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(BLOCK) k1_kernel(SellView S, CsrView C, int64_
 #endif
 __global__ void __launch_bounds__(BLOCK) k2_kernel(int64_t n, Vecs v, Scalars *sc, double *partials,
                                                    int dist, int use_cond, cudaGraphConditionalHandle h,
-                                                   const double *__restrict__ dsl) {
+                                                   const double *__restrict__ dsl, int zlazy) {
   __shared__ double sm[2][WARPS];
   const volatile Scalars *vs = sc;
   if (vs->done != DONE_RUNNING) {
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(BLOCK) k2_kernel(int64_t n, Vecs v, Scalars *s
     rr.y = __fma_rn(-alpha, qq.y, rr.y);
     const double2 zz = make_double2(dd.x * rr.x, dd.y * rr.y);
     r2[i] = rr;
-    z2[i] = zz;
+    if (!zlazy) z2[i] = zz;  // (lazy: K1a forms z from r; the odd tail row below stores it)
     a0 = __fma_rn(rr.x, zz.x, a0);
     a0 = __fma_rn(rr.y, zz.y, a0);
     a1 = __fma_rn(rr.x, rr.x, a1);
@@ -273,9 +273,22 @@ __device__ __forceinline__ double *dir_buf(const Vecs &v, int b) {
   return b == 0 ? v.p0 : b == 1 ? v.p1 : b == 2 ? v.p2 : v.p3;
 }
 
-template <int M>
+// z = dinv r of the pair i.  Where every slice shares one dinv (SolveWork::dslice_all,
+// one GPU, 3-pass schedule: `zl` non-null) K2 stores no z and K1a forms it from r and the
+// slice's dinv — the same product, so bitwise the stored z.
+template <bool LAZY>
+__device__ __forceinline__ double2 z_pair(const Vecs &v, const double *__restrict__ zl, int64_t i) {
+  if (LAZY) {
+    const double du = __ldg(zl + (i >> 4));
+    const double2 rr = __ldcs(reinterpret_cast<const double2 *>(v.r) + i);
+    return make_double2(du * rr.x, du * rr.y);
+  }
+  return __ldcs(reinterpret_cast<const double2 *>(v.z) + i);
+}
+
+template <int M, bool LAZY>
 __device__ __forceinline__ void k1a_apply(int64_t n, int64_t n_ghost, const Vecs &v, double beta, double alpha,
-                                          const volatile double *ahold) {
+                                          const volatile double *ahold, const double *__restrict__ zl) {
   const int64_t npair = n >> 1;
   const int64_t t = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nt = (int64_t)gridDim.x * BLOCK;
   double ah[M - 1];
@@ -289,7 +302,7 @@ __device__ __forceinline__ void k1a_apply(int64_t n, int64_t n_ghost, const Vecs
   double2 *__restrict__ a2 = reinterpret_cast<double2 *>(v.p0);
   double2 *__restrict__ x2 = reinterpret_cast<double2 *>(v.x);
   for (int64_t i = t; i < npair; i += nt) {
-    const double2 zz = __ldcs(z2 + i), pk = l2[i];
+    const double2 zz = z_pair<LAZY>(v, zl, i), pk = l2[i];
     double2 pm[M - 1];
 #pragma unroll
     for (int h = 0; h < M - 1; h++) pm[h] = __ldcs(hb[h] + i);
@@ -316,7 +329,9 @@ __device__ __forceinline__ void k1a_apply(int64_t n, int64_t n_ghost, const Vecs
   for (int64_t g = t; g < n_ghost; g += nt) v.p0[n + g] = __fma_rn(beta, pl[n + g], v.z[n + g]);
 }
 
-__device__ __forceinline__ void k1a_hold(int64_t n, int64_t n_ghost, const Vecs &v, double beta, int j) {
+template <bool LAZY>
+__device__ __forceinline__ void k1a_hold(int64_t n, int64_t n_ghost, const Vecs &v, double beta, int j,
+                                         const double *__restrict__ zl) {
   const int64_t npair = n >> 1;
   const int64_t t = (int64_t)blockIdx.x * BLOCK + threadIdx.x, nt = (int64_t)gridDim.x * BLOCK;
   const double *src = dir_buf(v, j);
@@ -325,15 +340,17 @@ __device__ __forceinline__ void k1a_hold(int64_t n, int64_t n_ghost, const Vecs 
   const double2 *__restrict__ a2 = reinterpret_cast<const double2 *>(src);
   double2 *__restrict__ b2 = reinterpret_cast<double2 *>(dst);
   for (int64_t i = t; i < npair; i += nt) {
-    const double2 zz = __ldcs(z2 + i), po = __ldcs(a2 + i);
+    const double2 zz = z_pair<LAZY>(v, zl, i), po = __ldcs(a2 + i);
     b2[i] = make_double2(__fma_rn(beta, po.x, zz.x), __fma_rn(beta, po.y, zz.y));
   }
   if ((n & 1) && t == 0) dst[n - 1] = __fma_rn(beta, src[n - 1], v.z[n - 1]);
   for (int64_t g = t; g < n_ghost; g += nt) dst[n + g] = __fma_rn(beta, src[n + g], v.z[n + g]);
 }
 
+template <bool LAZY>
 __global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, Vecs v, Scalars *sc, int use_cond,
-                                                    cudaGraphConditionalHandle h, int xd) {
+                                                    cudaGraphConditionalHandle h, int xd,
+                                                    const double *__restrict__ zl = nullptr) {
   const volatile Scalars *vs = sc;
   if (vs->done != DONE_RUNNING) {
     if (blockIdx.x == 0 && threadIdx.x == 0) stop_loop(use_cond, h);
@@ -342,9 +359,9 @@ __global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, 
   const double beta = vs->beta, alpha_prev = vs->alpha;
   if (xd) {
     const int xm = xd_m(xd), xj = xd_j(xd);
-    if (xj < xm - 1) k1a_hold(n, n_ghost, v, beta, xj);
-    else if (xm == 4) k1a_apply<4>(n, n_ghost, v, beta, alpha_prev, vs->ahold);
-    else k1a_apply<2>(n, n_ghost, v, beta, alpha_prev, vs->ahold);
+    if (xj < xm - 1) k1a_hold<LAZY>(n, n_ghost, v, beta, xj, zl);
+    else if (xm == 4) k1a_apply<4, LAZY>(n, n_ghost, v, beta, alpha_prev, vs->ahold, zl);
+    else k1a_apply<2, LAZY>(n, n_ghost, v, beta, alpha_prev, vs->ahold, zl);
     return;
   }
   double *__restrict__ p = v.p0;
@@ -353,7 +370,7 @@ __global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, 
   double2 *__restrict__ p2 = reinterpret_cast<double2 *>(p);
   double2 *__restrict__ x2 = reinterpret_cast<double2 *>(v.x);
   for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < npair; i += (int64_t)gridDim.x * BLOCK) {
-    const double2 zz = __ldcs(z2 + i), po = p2[i];
+    const double2 zz = z_pair<LAZY>(v, zl, i), po = p2[i];
     double2 xx = __ldcs(x2 + i);
     xx.x = __fma_rn(alpha_prev, po.x, xx.x);
     xx.y = __fma_rn(alpha_prev, po.y, xx.y);
@@ -678,6 +695,16 @@ static double *k1b_dir(const Vecs &v, int xd) {
   return b == 0 ? v.p0 : b == 1 ? v.p1 : b == 2 ? v.p2 : v.p3;
 }
 
+// K2 stores no z and K1a forms it from r where every slice shares one dinv (one GPU, the
+// 3-pass schedule: no z halo, no gather of z; PCG_ZLAZY=0: off)
+static int zlazy(const pcg_matrix *A) {
+  static const int off = [] {
+    const char *e = getenv("PCG_ZLAZY");
+    return e && atoi(e) == 0;
+  }();
+  return !off && !A->comm && A->schedule == 3 && A->work.dslice && A->work.dslice_all ? 1 : 0;
+}
+
 static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGraphConditionalHandle h,
                             int xdefer = 0) {
   Vecs v = vecs_of(A);
@@ -688,7 +715,7 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     // after the join the ghost p update and K1b over the boundary rows (head, tail)
     PCG_CUDA(cudaEventRecord(A->ov_fork, st));
     PCG_CUDA(cudaStreamWaitEvent(A->ov_side, A->ov_fork, 0));
-    k1a_kernel<<<A->grid_vec, BLOCK, 0, A->ov_side>>>(A->n, 0, v, w.sc, use_cond, h, xdefer);
+    k1a_kernel<false><<<A->grid_vec, BLOCK, 0, A->ov_side>>>(A->n, 0, v, w.sc, use_cond, h, xdefer);
     count_launch();
     Vecs vb = v;
     if (xdefer) vb.p0 = k1b_dir(v, xdefer);  // the direction this pass's K1a wrote
@@ -733,7 +760,10 @@ static pcg_status launch_k1(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
     return PCG_OK;
   }
   if (A->schedule == 3) {  // K1a (streaming p/x update) + K1b (SpMV + sigma)
-    k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, use_cond, h, xdefer);
+    if (zlazy(A))
+      k1a_kernel<true><<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, use_cond, h, xdefer, w.dslice);
+    else
+      k1a_kernel<false><<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, use_cond, h, xdefer);
     count_launch();
     Vecs vb = v;
     if (xdefer) vb.p0 = k1b_dir(v, xdefer);  // the direction this pass's K1a wrote
@@ -770,7 +800,7 @@ static pcg_status launch_k2(pcg_matrix *A, cudaStream_t st, int use_cond, cudaGr
   Vecs v = vecs_of(A);
   SolveWork &w = A->work;
   k2_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, v, w.sc, w.partials + 2 * (size_t)A->grid_spmv, A->comm ? 1 : 0,
-                                           use_cond, h, w.dslice);
+                                           use_cond, h, w.dslice, zlazy(A));
   count_launch();
   PCG_CUDA(cudaGetLastError());
   if (A->comm) {
@@ -1162,7 +1192,10 @@ extern "C" pcg_status pcg_profile_kernels(pcg_matrix_t A, const double *b, int32
       const int xd = xd_arg(xm, r);
       Vecs vb = v;
       if (xd) vb.p0 = k1b_dir(v, xd);
-      k1a_kernel<<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, 0, 0, xd);
+      if (zlazy(A))
+        k1a_kernel<true><<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, 0, 0, xd, w.dslice);
+      else
+        k1a_kernel<false><<<A->grid_vec, BLOCK, 0, st>>>(A->n, A->n_ghost, v, w.sc, 0, 0, xd);
       PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
       PCG_DISPATCH_D16(fmt_d16(A, A->format), A->csr_lanes, k1b_kernel,
                        <<<A->grid_spmv, BLOCK, A->dyn_smem, st>>>(A->sell_dia(), A->csr(), A->n_ghost, vb, w.sc,
