@@ -543,7 +543,7 @@ def main():
             names = ["k1a_kernel (p = z + beta p, x += alpha p_old; streaming" +
                      (f"; x every {xdm}th iteration: mean over a hold/apply cycle)" if xdm else ")"),
                      "k1b_kernel (SpMV q = A p + sigma = p.q, grid finish -> alpha)",
-                     "k2_kernel (r -= alpha q, z = dinv r, rho', gamma, grid finish -> beta; bytes by the 40 n formula: it reads dinv once per 32-row slice where the slice shares one, 32.25 n on a lattice)"]
+                     "k2_kernel (r -= alpha q, z = dinv r, rho', gamma, grid finish -> beta; bytes by the 40 n formula: it reads dinv once per 32-row slice where the slice shares one, and where every slice does it stores no z (K1a forms it from r): 24.25 n on a lattice)"]
             byts = [K1A_BYTES[xdm] * n, mat + 16.0 * n, 40.0 * n]
         else:
             names = ["-", "k1_kernel (fused SpMV + p/x updates + sigma)", "k2_kernel (r/z updates + dots)"]

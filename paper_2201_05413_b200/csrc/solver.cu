@@ -348,7 +348,7 @@ __device__ __forceinline__ void k1a_hold(int64_t n, int64_t n_ghost, const Vecs 
 }
 
 template <bool LAZY>
-__global__ void __launch_bounds__(BLOCK) k1a_kernel(int64_t n, int64_t n_ghost, Vecs v, Scalars *sc, int use_cond,
+__global__ void __launch_bounds__(BLOCK, 4) k1a_kernel(int64_t n, int64_t n_ghost, Vecs v, Scalars *sc, int use_cond,
                                                     cudaGraphConditionalHandle h, int xd,
                                                     const double *__restrict__ zl = nullptr) {
   const volatile Scalars *vs = sc;
