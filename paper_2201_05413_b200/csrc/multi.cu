@@ -566,7 +566,8 @@ __global__ void __launch_bounds__(BLOCK, LONG ? 1 : 4) mspmm_kernel(SellViewDia 
 // ---------------------------------------------------------------- K2: R_c -= alpha_c Q_c ; Z_c = dinv R_c ; rho'_c, gamma_c
 // grid (gx, k): blockIdx.y = column; frozen columns publish zero partials.
 __global__ void __launch_bounds__(BLOCK) mk2_kernel(int64_t n, MVecs v, MultiScalars *sc, double *partials,
-                                                    int use_cond, cudaGraphConditionalHandle h) {
+                                                    int use_cond, cudaGraphConditionalHandle h,
+                                                    const double *__restrict__ dsl) {
   __shared__ double sm2[2][WARPS];
   __shared__ double s_sm[BLOCK / KMAX][KMAX];
   __shared__ double s_out[2][KMAX];
@@ -590,8 +591,11 @@ __global__ void __launch_bounds__(BLOCK) mk2_kernel(int64_t n, MVecs v, MultiSca
     double2 *__restrict__ z2 = reinterpret_cast<double2 *>(Z);
     const int64_t t0 = (int64_t)blockIdx.x * BLOCK + threadIdx.x, ts = (int64_t)gridDim.x * BLOCK;
     for (int64_t t = t0; t < npair; t += ts) {
-      const double2 qq = __ldcs(q2 + t), dd = __ldg(d2 + t);
+      const double2 qq = __ldcs(q2 + t);
       double2 rr = r2[t];
+      // one dinv per 32-row slice where the slice shares one (SolveWork::dslice; same values)
+      const double du = dsl ? __ldg(dsl + (t >> 4)) : __longlong_as_double(0x7ff8000000000000ll);
+      const double2 dd = du == du ? make_double2(du, du) : __ldg(d2 + t);
       rr.x = __fma_rn(-alpha, qq.x, rr.x);
       rr.y = __fma_rn(-alpha, qq.y, rr.y);
       const double2 zz = make_double2(dd.x * rr.x, dd.y * rr.y);
@@ -1224,7 +1228,7 @@ static pcg_status mlaunch_iteration(pcg_matrix *A, int k, cudaStream_t st, int u
   const dim3 gv = mgrid_vec(A, k);
   mk1a_kernel<<<gv, BLOCK, 0, st>>>(A->n, v, w.msc, use_cond, h, pass);
   launch_mspmm<MS_SPMM>(A, k, st, use_cond, h, pass);
-  mk2_kernel<<<gv, BLOCK, 0, st>>>(A->n, v, w.msc, mpart_rz(A), use_cond, h);
+  mk2_kernel<<<gv, BLOCK, 0, st>>>(A->n, v, w.msc, mpart_rz(A), use_cond, h, w.dslice);
   count_launch(3);
   PCG_CUDA(cudaGetLastError());
   return PCG_OK;
@@ -1420,7 +1424,7 @@ extern "C" pcg_status pcg_profile_multi(pcg_matrix_t A, int32_t k, const double 
     PCG_CUDA(cudaEventRecord(ev[3 * r + 1], st));
     launch_mspmm<MS_SPMM>(A, k, st, 0, 0, pass);
     PCG_CUDA(cudaEventRecord(ev[3 * r + 2], st));
-    mk2_kernel<<<gv, BLOCK, 0, st>>>(n, v, w.msc, mpart_rz(A), 0, 0);
+    mk2_kernel<<<gv, BLOCK, 0, st>>>(n, v, w.msc, mpart_rz(A), 0, 0, w.dslice);
     PCG_CUDA(cudaEventRecord(ev[3 * r + 3], st));
     count_launch(3);
   }

@@ -550,7 +550,10 @@ def test_dinv_slices_are_bitwise_the_per_row_dinv(pcg, monkeypatch, name, c):
             monkeypatch.setenv("PCG_DINV_SLICE", env)
         M = _matrix(pcg, A)
         out[key] = M.solve(_dev(b), tol=tol)
+        B2 = np.stack([b, np.random.default_rng(7).standard_normal(A.n)], axis=1)
+        out[key + "_k"] = M.solve_multi(_dev(B2), tol=1e-8)[0].cpu().numpy()  # the multi-RHS K2 too
     monkeypatch.delenv("PCG_DINV_SLICE", raising=False)
+    assert np.array_equal(out["slice_k"], out["row_k"])
     (xs, infs), (xr, infr) = out["slice"], out["row"]
     assert infs["status"] == 0 and infs["iterations"] == infr["iterations"]
     assert np.array_equal(xs.cpu().numpy(), xr.cpu().numpy())
